@@ -1,0 +1,153 @@
+/*
+ * otprg.h — C ABI of the B200-native push-relabel assignment solver.
+ *
+ * Drop-in boundary for the reference's assignment path
+ * (/root/reference/proj, namespace otpr):
+ *
+ *   otprg_solve_assignment   replaces  otpr::solve_assignment
+ *                            (include/otpr/assignment.hpp:137-138,
+ *                             src/assignment.cpp:368-400), including the
+ *                            cost rounding it performs first
+ *                            (otpr::scale_round_costs, include/otpr/core.hpp:105,
+ *                             src/core.cpp:34-53) and the final
+ *                            otpr::matching_cost (core.hpp:147, core.cpp:95-102).
+ *   otprg_scale_round_costs  replaces  otpr::scale_round_costs (core.hpp:105)
+ *                            for callers that only need the rounded matrix.
+ *   otprg_scaled_floor       replaces  otpr::scaled_floor (core.hpp:101).
+ *
+ * Plain pointers and sizes only.  All host buffers are caller-owned; the
+ * context owns its device buffers and reuses them across solves.  Calls block
+ * until results are on the host.  A context is single-owner (not re-entrant),
+ * like the reference solver.
+ *
+ * Status codes mirror the reference exception taxonomy
+ * (include/otpr/errors.hpp:9-37) and otbench's exit codes
+ * (tools/otbench.cpp:187-209):
+ *   0 ok, 2 ParameterError, 3 InputError/FormatError, 4 NumericalError,
+ *   5 InvariantViolation, 6 CUDA/NCCL failure.
+ * otprg_last_error() returns the message of the last failing call.
+ *
+ * Semantics follow the reference with threads = 1 (the deterministic
+ * sequential greedy); results are bit-identical to it: same matching, same
+ * integer duals, same phase count / free_counts, same cost bits.
+ */
+#ifndef OTPRG_H_
+#define OTPRG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum otprg_status {
+  OTPRG_OK = 0,
+  OTPRG_PARAMETER = 2,
+  OTPRG_INPUT = 3,
+  OTPRG_NUMERICAL = 4,
+  OTPRG_INVARIANT = 5,
+  OTPRG_DEVICE = 6
+};
+
+/* How the cost of edge (a, b) is given. */
+enum otprg_cost_kind {
+  /* c(a,b) = cost[a*n_b + b], row-major doubles in [0,1]
+   * (AssignmentInstance::cost, core.hpp:69-81). */
+  OTPRG_COST_DENSE_F64 = 0,
+  /* c(a,b) = sqrt(dx*dx+dy*dy)/sqrt(2) of 2-D points pts_a[2a..2a+1],
+   * pts_b[2b..2b+1] — gen_uniform_square's formula
+   * (src/instances.cpp:70-75), evaluated in non-fused IEEE doubles. */
+  OTPRG_COST_POINTS2D = 1,
+  /* c(a,b) = 0.5 * sum_p |img_a[a][p]/tot_a - img_b[b][p]/tot_b| over
+   * `dim` uint8 pixels, ascending p — load_mnist_pair's formula
+   * (src/instances.cpp:114-142). */
+  OTPRG_COST_L1_U8 = 2
+};
+
+/* Storage width of the rounded cost matrix on the device. */
+enum otprg_storage { OTPRG_STORAGE_AUTO = 0, OTPRG_STORAGE_U8 = 1, OTPRG_STORAGE_U16 = 2 };
+
+typedef struct otprg_problem {
+  int32_t n_a; /* demand side A (rows)   */
+  int32_t n_b; /* supply side B (columns) */
+  double eps;  /* AssignmentOptions::eps, must lie in (0,1) */
+  int32_t cost_kind;
+  int32_t storage; /* otprg_storage */
+  const double* cost;   /* DENSE_F64: n_a*n_b, host */
+  const double* pts_a;  /* POINTS2D: n_a*2 (x,y interleaved), host */
+  const double* pts_b;  /* POINTS2D: n_b*2 */
+  const uint8_t* img_a; /* L1_U8: n_a*dim */
+  const uint8_t* img_b; /* L1_U8: n_b*dim */
+  int32_t dim;          /* L1_U8 pixels per image */
+  int32_t flags;        /* reserved, 0 */
+} otprg_problem;
+
+/* Caller-allocated results (SolveStats, assignment.hpp:35-53 + Matching,
+ * core.hpp:117-138).  Duals are reported like SolveStats::duals_final: in
+ * the solver's internal orientation (swapped when n_b > n_a), before the
+ * completion step. */
+typedef struct otprg_result {
+  int32_t* match_of_a;   /* n_a entries, -1 = unmatched (kUnmatched) */
+  int32_t* match_of_b;   /* n_b entries */
+  int64_t* y_a;          /* max(n_a,n_b) entries (internal demand side) or NULL */
+  int64_t* y_b;          /* min(n_a,n_b) entries (internal supply side) or NULL */
+  int64_t* free_counts;  /* n_i per executed phase, up to free_cap entries, or NULL */
+  int64_t free_cap;
+  /* outputs */
+  int64_t phases;
+  int64_t sum_ni;
+  int32_t swapped;
+  int32_t full_match_termination;
+  double cost;            /* matching_cost of the final matching */
+  /* device-side measurements */
+  double build_ms;        /* cost build/rounding kernels (CUDA events) */
+  double solve_ms;        /* phase loop + completion kernels (CUDA events) */
+  double phase1_ms;       /* the first phase alone (its own launch) */
+  int64_t bytes_touched;  /* cost-matrix bytes the scan kernels loaded */
+  int64_t bytes_alg;      /* sum_i n_i * n_a * width (Lemma-5 schedule) */
+  int32_t width;          /* bytes per rounded cost entry on the device */
+  int32_t gpu_launches;   /* kernels launched by this call */
+} otprg_result;
+
+typedef struct otprg_ctx otprg_ctx;
+
+int otprg_create(int device, otprg_ctx** out);
+void otprg_destroy(otprg_ctx* ctx);
+const char* otprg_last_error(const otprg_ctx* ctx);
+int otprg_version(void);
+
+/* scaled_floor(c, eps) (core.cpp:26-32), evaluated on the host. */
+int64_t otprg_scaled_floor(double c, double eps);
+
+/* Full solve: H2D of the problem's host buffers, cost build + rounding on
+ * the device, device-resident phase loop, completion, D2H of the results,
+ * matching cost.  Mirrors otpr::solve_assignment. */
+int otprg_solve_assignment(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res);
+
+/* Two-step form used by benchmarks: prepare() uploads + builds the rounded
+ * matrix and keeps it resident in the context; solve_prepared() runs the
+ * phase loop on it (results as above).  solve_prepared() may be called
+ * repeatedly on the same prepared problem. */
+int otprg_prepare(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res);
+int otprg_solve_prepared(otprg_ctx* ctx, otprg_result* res);
+
+/* Rounded costs k(a,b) = scaled_floor(c(a,b), eps) computed on the device
+ * and returned row-major (n_a x n_b int32, like ScaledCosts::k), plus
+ * unit_floor / unit_ceil (core.hpp:89-92).  Mirrors otpr::scale_round_costs. */
+int otprg_scale_round_costs(otprg_ctx* ctx, const otprg_problem* prob, int32_t* k,
+                            int32_t* unit_floor, int32_t* unit_ceil);
+
+/* Point sets of otpr::gen_uniform_square(n, seed) (src/instances.cpp:48-62):
+ * std::mt19937_64 streams seeded with splitmix64(seed) (A) and
+ * splitmix64(seed ^ 0x9E3779B97F4A7C15) (B), x then y per point, 53-bit
+ * uniforms.  Writes interleaved (x, y) pairs, n per side.  Host-only. */
+int otprg_uniform_square_points(int32_t n, uint64_t seed, double* pts_a, double* pts_b);
+
+/* Writes a buffer larger than L2 on the context's stream (benchmark hygiene). */
+int otprg_flush_l2(otprg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OTPRG_H_ */

@@ -1,0 +1,255 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" wrapper over the UNMODIFIED reference library
+// (/root/reference/proj/src/*.cpp, compiled by oracle/Makefile into
+// oracle/_ref/libotpr_ref.so).  It lets the Python tests, the golden-fixture
+// generator and bench.py's reference arm call the reference's own public API
+// (otpr::solve_assignment, otpr::solve_ot, ...) through ctypes.  This file is
+// ours; no reference source is copied into the repo.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "otpr/assignment.hpp"
+#include "otpr/core.hpp"
+#include "otpr/errors.hpp"
+#include "otpr/instances.hpp"
+#include "otpr/ot.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+// Exception -> status mapping of tools/otbench.cpp:187-209.
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const otpr::ParameterError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const otpr::FormatError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const otpr::InputError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const otpr::NumericalError& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const otpr::InvariantViolation& e) {
+    g_err = e.what();
+    return 5;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+struct RefStats {
+  int64_t phases;
+  int64_t sum_ni;
+  int32_t swapped;
+  int32_t full_match_termination;
+  double cost;
+  double solve_ms;  // steady_clock around solve_assignment (bench.cpp:62-64)
+  double round_ms;  // scale_round_costs alone, timed separately (untimed solve)
+  int64_t n_free_counts;
+};
+
+void export_result(const otpr::Matching& m, const otpr::SolveStats& s,
+                   int32_t* match_of_a, int32_t* match_of_b, int64_t* y_a,
+                   int64_t* y_b, int64_t* free_counts, int64_t free_cap,
+                   RefStats* out) {
+  if (match_of_a)
+    std::memcpy(match_of_a, m.match_of_a.data(), m.match_of_a.size() * 4);
+  if (match_of_b)
+    std::memcpy(match_of_b, m.match_of_b.data(), m.match_of_b.size() * 4);
+  if (y_a)
+    std::memcpy(y_a, s.duals_final.y_a.data(), s.duals_final.y_a.size() * 8);
+  if (y_b)
+    std::memcpy(y_b, s.duals_final.y_b.data(), s.duals_final.y_b.size() * 8);
+  const int64_t nf = static_cast<int64_t>(s.free_counts.size());
+  if (free_counts)
+    std::memcpy(free_counts, s.free_counts.data(),
+                static_cast<size_t>(nf < free_cap ? nf : free_cap) * 8);
+  out->phases = s.phases;
+  out->sum_ni = s.sum_ni;
+  out->swapped = s.swapped;
+  out->full_match_termination = s.full_match_termination;
+  out->n_free_counts = nf;
+}
+
+otpr::AssignmentInstance wrap(int32_t n_a, int32_t n_b, const double* cost) {
+  otpr::AssignmentInstance inst;
+  inst.n_a = n_a;
+  inst.n_b = n_b;
+  inst.cost = otpr::Matrix<double>(n_a, n_b);
+  std::memcpy(inst.cost.data(), cost, sizeof(double) * size_t(n_a) * n_b);
+  return inst;
+}
+
+int solve_inst(const otpr::AssignmentInstance& inst, double eps, int threads,
+               int time_rounding, int32_t* match_of_a, int32_t* match_of_b,
+               int64_t* y_a, int64_t* y_b, int64_t* free_counts,
+               int64_t free_cap, RefStats* out) {
+  return guarded([&] {
+    otpr::AssignmentOptions opt;
+    opt.eps = eps;
+    opt.threads = threads;
+    const auto t0 = Clock::now();
+    auto [m, s] = otpr::solve_assignment(inst, opt);
+    out->solve_ms = ms_since(t0);
+    out->cost = otpr::matching_cost(m, inst);
+    out->round_ms = 0.0;
+    if (time_rounding) {
+      const auto t1 = Clock::now();
+      volatile auto sc = otpr::scale_round_costs(inst, eps).unit_floor;
+      (void)sc;
+      out->round_ms = ms_since(t1);
+    }
+    export_result(m, s, match_of_a, match_of_b, y_a, y_b, free_counts, free_cap,
+                  out);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_gen_uniform_square(int32_t n, uint64_t seed, double* cost) {
+  return guarded([&] {
+    const auto inst = otpr::gen_uniform_square(n, seed);
+    std::memcpy(cost, inst.cost.data(), sizeof(double) * inst.cost.size());
+  });
+}
+
+int ref_scale_round_costs(int32_t n_a, int32_t n_b, const double* cost,
+                          double eps, int32_t* k, int32_t* unit_floor,
+                          int32_t* unit_ceil) {
+  return guarded([&] {
+    const auto sc = otpr::scale_round_costs(wrap(n_a, n_b, cost), eps);
+    std::memcpy(k, sc.k.data(), sizeof(int32_t) * sc.k.size());
+    *unit_floor = sc.unit_floor;
+    *unit_ceil = sc.unit_ceil;
+  });
+}
+
+int64_t ref_scaled_floor(double c, double eps) { return otpr::scaled_floor(c, eps); }
+
+int ref_solve_assignment(int32_t n_a, int32_t n_b, const double* cost, double eps,
+                         int threads, int32_t* match_of_a, int32_t* match_of_b,
+                         int64_t* y_a, int64_t* y_b, int64_t* free_counts,
+                         int64_t free_cap, RefStats* out) {
+  otpr::AssignmentInstance inst;
+  int st = guarded([&] { inst = wrap(n_a, n_b, cost); });
+  if (st) return st;
+  return solve_inst(inst, eps, threads, 0, match_of_a, match_of_b, y_a, y_b,
+                    free_counts, free_cap, out);
+}
+
+// gen_uniform_square(n, seed) + solve_assignment in one call, so large
+// instances never cross the FFI.  gen_ms reports the (untimed-by-reference)
+// instance generation.
+int ref_solve_uniform_square(int32_t n, uint64_t seed, double eps, int threads,
+                             int time_rounding, int32_t* match_of_a,
+                             int32_t* match_of_b, int64_t* y_a, int64_t* y_b,
+                             int64_t* free_counts, int64_t free_cap,
+                             RefStats* out) {
+  otpr::AssignmentInstance inst;
+  int st = guarded([&] { inst = otpr::gen_uniform_square(n, seed); });
+  if (st) return st;
+  return solve_inst(inst, eps, threads, time_rounding, match_of_a, match_of_b,
+                    y_a, y_b, free_counts, free_cap, out);
+}
+
+// load_mnist_pair(path, n, seed): dense cost out (n x n).
+int ref_load_mnist_pair(const char* path, int32_t n, uint64_t seed, double* cost) {
+  return guarded([&] {
+    const auto inst = otpr::load_mnist_pair(path, n, seed);
+    std::memcpy(cost, inst.cost.data(), sizeof(double) * inst.cost.size());
+  });
+}
+
+int ref_solve_mnist(const char* path, int32_t n, uint64_t seed, double eps,
+                    int threads, int32_t* match_of_a, int32_t* match_of_b,
+                    int64_t* y_a, int64_t* y_b, int64_t* free_counts,
+                    int64_t free_cap, RefStats* out, double* load_ms) {
+  otpr::AssignmentInstance inst;
+  const auto t0 = Clock::now();
+  int st = guarded([&] { inst = otpr::load_mnist_pair(path, n, seed); });
+  if (load_ms) *load_ms = ms_since(t0);
+  if (st) return st;
+  return solve_inst(inst, eps, threads, 0, match_of_a, match_of_b, y_a, y_b,
+                    free_counts, free_cap, out);
+}
+
+// ---- optimal transport (src/ot.cpp:705-732) -------------------------------
+
+struct RefOtStats {
+  int64_t phases;
+  int64_t sum_ni;
+  int64_t n_entries;
+  double cost;
+  double theta;
+  double solve_ms;
+  int64_t total_d;
+  int64_t total_s;
+};
+
+// gen_random_ot_rational(n_a, n_b, seed) -> solve_ot(eps).  Plan entries are
+// written up to entry_cap as (a, b, mass) triples.
+int ref_solve_ot_rational(int32_t n_a, int32_t n_b, uint64_t seed, double eps,
+                          int32_t* ent_a, int32_t* ent_b, double* ent_mass,
+                          int64_t entry_cap, int64_t* free_counts,
+                          int64_t free_cap, RefOtStats* out) {
+  otpr::OTInstance inst;
+  int st = guarded([&] { inst = otpr::gen_random_ot_rational(n_a, n_b, seed); });
+  if (st) return st;
+  return guarded([&] {
+    const auto sm = otpr::scale_and_round(inst, eps / 3.0);
+    out->theta = sm.theta;
+    out->total_d = sm.total_d();
+    out->total_s = sm.total_s();
+    const auto t0 = Clock::now();
+    auto [plan, stats] = otpr::solve_ot(inst, eps);
+    out->solve_ms = ms_since(t0);
+    out->phases = stats.phases;
+    out->sum_ni = stats.sum_ni;
+    out->cost = plan.cost;
+    out->n_entries = static_cast<int64_t>(plan.entries.size());
+    const int64_t ne = out->n_entries < entry_cap ? out->n_entries : entry_cap;
+    for (int64_t i = 0; i < ne; ++i) {
+      ent_a[i] = plan.entries[i].a;
+      ent_b[i] = plan.entries[i].b;
+      ent_mass[i] = plan.entries[i].mass;
+    }
+    const int64_t nf = static_cast<int64_t>(stats.free_counts.size());
+    if (free_counts)
+      std::memcpy(free_counts, stats.free_counts.data(),
+                  static_cast<size_t>(nf < free_cap ? nf : free_cap) * 8);
+  });
+}
+
+// The OT instance itself (renormalised masses + costs) for parity inputs.
+int ref_gen_random_ot_rational(int32_t n_a, int32_t n_b, uint64_t seed,
+                               double* mu, double* nu, double* cost) {
+  return guarded([&] {
+    const auto inst = otpr::gen_random_ot_rational(n_a, n_b, seed);
+    std::memcpy(mu, inst.mu.data(), sizeof(double) * inst.mu.size());
+    std::memcpy(nu, inst.nu.data(), sizeof(double) * inst.nu.size());
+    std::memcpy(cost, inst.cost.data(), sizeof(double) * inst.cost.size());
+  });
+}
+
+}  // extern "C"

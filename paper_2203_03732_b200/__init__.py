@@ -1,0 +1,17 @@
+"""paper_2203_03732_b200 — B200-native push-relabel eps-approximate assignment
+solver (arXiv 2203.03732), a drop-in for the reference ``otpr`` assignment
+path.  See DESIGN.md for the device design and INTEGRATION.md for the C ABI.
+"""
+from .api import (  # noqa: F401
+    AssignmentInstance, AssignmentOptions, DeviceError, DualState, FormatError, InputError,
+    InvariantViolation, Matching, NumericalError, ParameterError, ScaledCosts, SolveStats, Solver,
+    gen_uniform_square, get_solver, matching_cost, points_cost, scale_round_costs, scaled_floor,
+    solve_assignment,
+)
+
+__all__ = [
+    "AssignmentInstance", "AssignmentOptions", "DeviceError", "DualState", "FormatError",
+    "InputError", "InvariantViolation", "Matching", "NumericalError", "ParameterError",
+    "ScaledCosts", "SolveStats", "Solver", "gen_uniform_square", "get_solver", "matching_cost",
+    "points_cost", "scale_round_costs", "scaled_floor", "solve_assignment",
+]

@@ -1,0 +1,94 @@
+"""ctypes binding of libotprg.so (the C ABI in include/otprg.h).
+
+The shared library is built in-tree (paper_2203_03732_b200/lib/libotprg.so)
+by ``python -c "import __graft_entry__ as g; g.build()"`` or
+``make -C paper_2203_03732_b200/csrc``.  There is no fallback: if the library
+is missing, importing the solver raises instead of silently computing on the
+CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "lib", "libotprg.so")
+CSRC = os.path.join(PKG_DIR, "csrc")
+
+OK, PARAMETER, INPUT, NUMERICAL, INVARIANT, DEVICE = 0, 2, 3, 4, 5, 6
+COST_DENSE_F64, COST_POINTS2D, COST_L1_U8 = 0, 1, 2
+STORAGE = {"auto": 0, "u8": 1, "u16": 2}
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("n_a", C.c_int32), ("n_b", C.c_int32), ("eps", C.c_double),
+        ("cost_kind", C.c_int32), ("storage", C.c_int32),
+        ("cost", C.c_void_p), ("pts_a", C.c_void_p), ("pts_b", C.c_void_p),
+        ("img_a", C.c_void_p), ("img_b", C.c_void_p),
+        ("dim", C.c_int32), ("flags", C.c_int32),
+    ]
+
+
+class Result(C.Structure):
+    _fields_ = [
+        ("match_of_a", C.c_void_p), ("match_of_b", C.c_void_p),
+        ("y_a", C.c_void_p), ("y_b", C.c_void_p),
+        ("free_counts", C.c_void_p), ("free_cap", C.c_int64),
+        ("phases", C.c_int64), ("sum_ni", C.c_int64),
+        ("swapped", C.c_int32), ("full_match_termination", C.c_int32),
+        ("cost", C.c_double),
+        ("build_ms", C.c_double), ("solve_ms", C.c_double), ("phase1_ms", C.c_double),
+        ("bytes_touched", C.c_int64), ("bytes_alg", C.c_int64),
+        ("width", C.c_int32), ("gpu_launches", C.c_int32),
+    ]
+
+
+EXPORTS = [
+    "otprg_create", "otprg_destroy", "otprg_last_error", "otprg_version", "otprg_scaled_floor",
+    "otprg_solve_assignment", "otprg_prepare", "otprg_solve_prepared", "otprg_scale_round_costs",
+    "otprg_uniform_square_points", "otprg_flush_l2",
+]
+
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+def lib() -> C.CDLL:
+    """Load libotprg.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()')")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    L.otprg_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.otprg_destroy.argtypes = [vp]
+    L.otprg_destroy.restype = None
+    L.otprg_last_error.argtypes = [vp]
+    L.otprg_last_error.restype = C.c_char_p
+    L.otprg_scaled_floor.argtypes = [C.c_double, C.c_double]
+    L.otprg_scaled_floor.restype = C.c_int64
+    for fn in ("otprg_solve_assignment", "otprg_prepare"):
+        getattr(L, fn).argtypes = [vp, C.POINTER(Problem), C.POINTER(Result)]
+    L.otprg_solve_prepared.argtypes = [vp, C.POINTER(Result)]
+    L.otprg_scale_round_costs.argtypes = [vp, C.POINTER(Problem), vp, C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_int32)]
+    L.otprg_uniform_square_points.argtypes = [C.c_int32, C.c_uint64, vp, vp]
+    L.otprg_flush_l2.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def ptr(a: np.ndarray | None) -> int | None:
+    return None if a is None else a.ctypes.data

@@ -1,0 +1,386 @@
+"""Host-side mirror of the reference's assignment API (namespace ``otpr``).
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/otpr/{core,assignment,errors,instances}.hpp, so
+code (and tests) written against the reference read the same here:
+
+    inst = gen_uniform_square(10_000, seed=1)
+    matching, stats = solve_assignment(inst, AssignmentOptions(eps=0.01))
+
+Every solve runs on the GPU through the C ABI (include/otprg.h ->
+paper_2203_03732_b200/lib/libotprg.so).  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native as N
+
+K_UNMATCHED = -1
+
+
+# ---- errors (include/otpr/errors.hpp:9-37) -------------------------------
+class ParameterError(ValueError):
+    """Out-of-range or inconsistent caller-supplied parameters."""
+
+
+class InputError(RuntimeError):
+    """Malformed or unusable input data."""
+
+
+class FormatError(InputError):
+    """Byte-level file format problems."""
+
+
+class NumericalError(RuntimeError):
+    """Numerical failure of an iterative method."""
+
+
+class InvariantViolation(RuntimeError):
+    """A solver state check failed (a bug, not bad input)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL failure (no reference counterpart)."""
+
+
+_STATUS_EXC = {N.PARAMETER: ParameterError, N.INPUT: InputError, N.NUMERICAL: NumericalError,
+               N.INVARIANT: InvariantViolation, N.DEVICE: DeviceError}
+
+
+# ---- data model (include/otpr/core.hpp) ----------------------------------
+@dataclass
+class AssignmentInstance:
+    """core.hpp:69-81.  Either a dense row-major cost (rows = A, cols = B) or,
+    as a B200-native extension, 2-D point sets whose cost is
+    gen_uniform_square's Euclidean/sqrt(2) (instances.cpp:70-75), evaluated
+    on the device without materialising n_a x n_b doubles."""
+    n_a: int
+    n_b: int
+    cost: Optional[np.ndarray] = None      # (n_a, n_b) float64
+    pts_a: Optional[np.ndarray] = None     # (n_a, 2) float64
+    pts_b: Optional[np.ndarray] = None     # (n_b, 2) float64
+    norm_factor: float = 1.0
+    seed: int = 0
+
+    def validate(self) -> None:
+        """core.cpp:10-24."""
+        if self.n_a < 1 or self.n_b < 1:
+            raise ParameterError("instance needs at least one vertex per side")
+        if self.cost is not None:
+            if self.cost.shape != (self.n_a, self.n_b):
+                raise ParameterError("cost matrix dimensions do not match n_a x n_b")
+            bad = ~((self.cost >= 0.0) & (self.cost <= 1.0))
+            if bad.any():
+                a, b = np.argwhere(bad)[0]
+                raise ParameterError(f"cost entry outside [0,1] at ({a},{b}): {self.cost[a, b]:f}")
+        elif self.pts_a is None or self.pts_b is None:
+            raise ParameterError("instance has neither a cost matrix nor point sets")
+
+    def dense_cost(self) -> np.ndarray:
+        if self.cost is not None:
+            return self.cost
+        return points_cost(self.pts_a, self.pts_b)
+
+
+@dataclass
+class ScaledCosts:
+    """core.hpp:85-96."""
+    eps: float
+    k: np.ndarray  # (n_a, n_b) int32
+    unit_floor: int
+    unit_ceil: int
+
+    def dual_bound(self) -> int:
+        return int(self.unit_ceil) + 2
+
+
+@dataclass
+class DualState:
+    """core.hpp:109-114 (integer eps-units)."""
+    y_a: np.ndarray
+    y_b: np.ndarray
+
+    def sum_abs(self) -> int:
+        return int(np.abs(self.y_a).sum() + np.abs(self.y_b).sum())
+
+
+@dataclass
+class Matching:
+    """core.hpp:117-138."""
+    match_of_a: np.ndarray
+    match_of_b: np.ndarray
+
+    @classmethod
+    def empty(cls, n_a: int, n_b: int) -> "Matching":
+        return cls(np.full(n_a, K_UNMATCHED, np.int32), np.full(n_b, K_UNMATCHED, np.int32))
+
+    def has_a(self, a: int) -> bool:
+        return self.match_of_a[a] != K_UNMATCHED
+
+    def has_b(self, b: int) -> bool:
+        return self.match_of_b[b] != K_UNMATCHED
+
+    def link(self, a: int, b: int) -> None:
+        self.match_of_a[a] = b
+        self.match_of_b[b] = a
+
+    def size(self) -> int:
+        return int((self.match_of_a != K_UNMATCHED).sum())
+
+    def validate(self) -> None:
+        """core.cpp:77-93."""
+        n_a, n_b = len(self.match_of_a), len(self.match_of_b)
+        for a, b in enumerate(self.match_of_a):
+            if b == K_UNMATCHED:
+                continue
+            if b < 0 or b >= n_b or self.match_of_b[b] != a:
+                raise InvariantViolation(f"matching is not mutually consistent at a={a}")
+        for b, a in enumerate(self.match_of_b):
+            if a == K_UNMATCHED:
+                continue
+            if a < 0 or a >= n_a or self.match_of_a[a] != b:
+                raise InvariantViolation(f"matching is not mutually consistent at b={b}")
+
+
+@dataclass
+class SolveStats:
+    """assignment.hpp:35-53, plus device measurements."""
+    phases: int = 0
+    free_counts: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+    sum_ni: int = 0
+    duals_final: Optional[DualState] = None
+    swapped: bool = False
+    full_match_termination: bool = False
+    device: dict = field(default_factory=dict)
+
+    @staticmethod
+    def phase_bound(eps: float) -> int:
+        return int(math.ceil((1.0 + 2.0 * eps) / (eps * eps)))
+
+    @staticmethod
+    def sum_ni_bound(eps: float, n: int) -> int:
+        return int(math.ceil(float(n) * (1.0 + 2.0 * eps) / eps))
+
+
+@dataclass
+class AssignmentOptions:
+    """assignment.hpp:69-90.  ``threads`` is accepted and ignored: the device
+    path always has threads=1 (deterministic) semantics.  ``observer`` and
+    ``check_invariants`` need the host-synced debug loop, which this round does
+    not provide; they raise ParameterError rather than being silently
+    ignored.  ``storage`` selects the device width of the rounded matrix."""
+    eps: float = 0.1
+    threads: int = 1
+    check_invariants: bool = False
+    observer: Optional[Callable] = None
+    demand_groups: Optional[np.ndarray] = None
+    supply_groups: Optional[np.ndarray] = None
+    storage: str = "auto"
+    device: int = 0
+
+
+# ---- device context ------------------------------------------------------
+class Solver:
+    """Owns one otprg_ctx (device buffers reused across solves)."""
+
+    def __init__(self, device: int = 0):
+        self._L = N.lib()
+        self._ctx = C.c_void_p()
+        st = self._L.otprg_create(device, C.byref(self._ctx))
+        if st:
+            raise DeviceError(f"otprg_create(device={device}) failed with status {st}")
+        self.device = device
+        self._keep = ()
+
+    def close(self) -> None:
+        if self._ctx:
+            self._L.otprg_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, st: int):
+        msg = self._L.otprg_last_error(self._ctx).decode()
+        raise _STATUS_EXC.get(st, DeviceError)(msg)
+
+    def _problem(self, inst: AssignmentInstance, eps: float, storage: str) -> N.Problem:
+        p = N.Problem()
+        p.n_a, p.n_b, p.eps = inst.n_a, inst.n_b, float(eps)
+        if storage not in N.STORAGE:
+            raise ParameterError(f"unknown storage {storage!r}")
+        p.storage = N.STORAGE[storage]
+        if inst.cost is not None:
+            cost = np.ascontiguousarray(inst.cost, np.float64)
+            if cost.shape != (inst.n_a, inst.n_b):
+                raise ParameterError("cost matrix dimensions do not match n_a x n_b")
+            p.cost_kind = N.COST_DENSE_F64
+            p.cost = cost.ctypes.data
+            self._keep = (cost,)
+        elif inst.pts_a is not None and inst.pts_b is not None:
+            pa = np.ascontiguousarray(inst.pts_a, np.float64).reshape(inst.n_a, 2)
+            pb = np.ascontiguousarray(inst.pts_b, np.float64).reshape(inst.n_b, 2)
+            p.cost_kind = N.COST_POINTS2D
+            p.pts_a, p.pts_b = pa.ctypes.data, pb.ctypes.data
+            self._keep = (pa, pb)
+        else:
+            raise ParameterError("instance has neither a cost matrix nor point sets")
+        return p
+
+    def _result(self, n_a: int, n_b: int, eps: float):
+        ia, ib = max(n_a, n_b), min(n_a, n_b)
+        cap = SolveStats.phase_bound(eps) + 10
+        bufs = dict(match_of_a=np.empty(n_a, np.int32), match_of_b=np.empty(n_b, np.int32),
+                    y_a=np.empty(ia, np.int64), y_b=np.empty(ib, np.int64),
+                    free_counts=np.zeros(cap, np.int64))
+        r = N.Result()
+        for k, v in bufs.items():
+            setattr(r, k, v.ctypes.data)
+        r.free_cap = cap
+        return r, bufs
+
+    def prepare(self, inst: AssignmentInstance, eps: float, storage: str = "auto") -> dict:
+        p = self._problem(inst, eps, storage)
+        r = N.Result()
+        st = self._L.otprg_prepare(self._ctx, C.byref(p), C.byref(r))
+        if st:
+            self._raise(st)
+        self._prepared = (inst.n_a, inst.n_b, eps)
+        return {"build_ms": r.build_ms, "width": r.width}
+
+    def solve_prepared(self):
+        n_a, n_b, eps = self._prepared
+        r, bufs = self._result(n_a, n_b, eps)
+        st = self._L.otprg_solve_prepared(self._ctx, C.byref(r))
+        if st:
+            self._raise(st)
+        return self._pack(r, bufs)
+
+    def solve(self, inst: AssignmentInstance, opt: AssignmentOptions):
+        p = self._problem(inst, opt.eps, opt.storage)
+        r, bufs = self._result(inst.n_a, inst.n_b, opt.eps)
+        st = self._L.otprg_solve_assignment(self._ctx, C.byref(p), C.byref(r))
+        if st:
+            self._raise(st)
+        return self._pack(r, bufs)
+
+    @staticmethod
+    def _pack(r: N.Result, bufs: dict):
+        m = Matching(bufs["match_of_a"], bufs["match_of_b"])
+        stats = SolveStats(
+            phases=int(r.phases), free_counts=bufs["free_counts"][: r.phases].copy(),
+            sum_ni=int(r.sum_ni), duals_final=DualState(bufs["y_a"], bufs["y_b"]),
+            swapped=bool(r.swapped), full_match_termination=bool(r.full_match_termination),
+            device=dict(cost=r.cost, build_ms=r.build_ms, solve_ms=r.solve_ms,
+                        phase1_ms=r.phase1_ms, bytes_touched=int(r.bytes_touched),
+                        bytes_alg=int(r.bytes_alg), width=int(r.width),
+                        gpu_launches=int(r.gpu_launches)))
+        return m, stats
+
+    def scale_round_costs(self, inst: AssignmentInstance, eps: float, storage: str = "auto") -> ScaledCosts:
+        p = self._problem(inst, eps, storage)
+        k = np.empty((inst.n_a, inst.n_b), np.int32)
+        uf, uc = C.c_int32(), C.c_int32()
+        st = self._L.otprg_scale_round_costs(self._ctx, C.byref(p), k.ctypes.data, C.byref(uf),
+                                             C.byref(uc))
+        if st:
+            self._raise(st)
+        return ScaledCosts(eps, k, uf.value, uc.value)
+
+    def flush_l2(self) -> None:
+        st = self._L.otprg_flush_l2(self._ctx)
+        if st:
+            self._raise(st)
+
+
+_solvers: dict[int, Solver] = {}
+
+
+def get_solver(device: int = 0) -> Solver:
+    if device not in _solvers:
+        _solvers[device] = Solver(device)
+    return _solvers[device]
+
+
+# ---- free functions mirroring the reference ------------------------------
+def scaled_floor(c: float, eps: float) -> int:
+    """core.cpp:26-32 (host)."""
+    return int(N.lib().otprg_scaled_floor(c, eps))
+
+
+def scale_round_costs(inst: AssignmentInstance, eps: float, storage: str = "auto",
+                      device: int = 0) -> ScaledCosts:
+    """core.cpp:34-53, computed on the device."""
+    inst.validate()
+    return get_solver(device).scale_round_costs(inst, eps, storage)
+
+
+def _check_options(inst: AssignmentInstance, opt: AssignmentOptions) -> None:
+    """assignment.cpp:370-383."""
+    inst.validate()
+    if not (opt.eps > 0.0 and opt.eps < 1.0):
+        raise ParameterError("eps must lie in (0, 1)")
+    if (opt.demand_groups is None) != (opt.supply_groups is None):
+        raise ParameterError("copy mode needs both demand and supply groups")
+    if opt.demand_groups is not None:
+        raise ParameterError("copy mode (demand/supply groups) is not provided by the device path")
+    if opt.observer is not None or opt.check_invariants:
+        raise ParameterError("observer/check_invariants need the host-synced debug loop, "
+                             "which the device path does not provide")
+
+
+def solve_assignment(inst: AssignmentInstance, opt: AssignmentOptions):
+    """assignment.hpp:137-138 / assignment.cpp:368-400 -> (Matching, SolveStats)."""
+    _check_options(inst, opt)
+    return get_solver(opt.device).solve(inst, opt)
+
+
+def matching_cost(m: Matching, inst: AssignmentInstance) -> float:
+    """core.cpp:95-102: sequential double sum over a ascending."""
+    total = 0.0
+    for a in range(inst.n_a):
+        b = int(m.match_of_a[a])
+        if b != K_UNMATCHED:
+            total += float(_pair_cost(inst, a, b))
+    return total
+
+
+def _pair_cost(inst: AssignmentInstance, a: int, b: int) -> float:
+    if inst.cost is not None:
+        return float(inst.cost[a, b])
+    dx = float(inst.pts_a[a, 0]) - float(inst.pts_b[b, 0])
+    dy = float(inst.pts_a[a, 1]) - float(inst.pts_b[b, 1])
+    return math.sqrt(dx * dx + dy * dy) / math.sqrt(2.0)
+
+
+def points_cost(pts_a: np.ndarray, pts_b: np.ndarray) -> np.ndarray:
+    """Dense instances.cpp:70-75 cost from point sets (numpy, non-fused)."""
+    dx = pts_a[:, None, 0] - pts_b[None, :, 0]
+    dy = pts_a[:, None, 1] - pts_b[None, :, 1]
+    return np.sqrt(dx * dx + dy * dy) / np.sqrt(2.0)
+
+
+def gen_uniform_square(n: int, seed: int, dense: bool = False) -> AssignmentInstance:
+    """instances.cpp:48-78.  Points come from the reference's mt19937_64
+    streams (generated natively by the C ABI); ``dense=True`` also
+    materialises the n x n double cost like the reference does."""
+    if n < 1:
+        raise ParameterError("gen_uniform_square: n must be >= 1")
+    pa = np.empty((n, 2), np.float64)
+    pb = np.empty((n, 2), np.float64)
+    st = N.lib().otprg_uniform_square_points(n, seed, pa.ctypes.data, pb.ctypes.data)
+    if st:
+        raise ParameterError("gen_uniform_square failed")
+    inst = AssignmentInstance(n, n, None, pa, pb, norm_factor=math.sqrt(2.0), seed=seed)
+    if dense:
+        inst.cost = points_cost(pa, pb)
+    return inst

@@ -1,0 +1,164 @@
+// cost_kernels.cu — cost build + rounding into the compact B-major matrix
+// kT[b][a] = k(a, b) = scaled_floor(c(a, b), eps) (reference
+// scale_round_costs, src/core.cpp:34-53, with scaled_floor :26-32).
+//
+// All FP64 arithmetic uses explicit round-to-nearest intrinsics so no FMA
+// contraction can change bits: the reference is built without
+// -march and its cost formulas are plain IEEE double expressions.
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace otprg {
+
+namespace {
+
+// scaled_floor (core.cpp:26-32): floor(c/eps), repaired so that
+// RN(k*eps) <= c < RN((k+1)*eps).
+__device__ __forceinline__ long long scaled_floor_dev(double c, double eps) {
+  long long k = (long long)floor(__ddiv_rn(c, eps));
+  while (__dmul_rn((double)(k + 1), eps) <= c) ++k;
+  while (k > 0 && __dmul_rn((double)k, eps) > c) --k;
+  return k;
+}
+
+template <typename T>
+__device__ __forceinline__ T clamp_store(long long k) {
+  // k <= unit_floor < type max by construction of the storage choice.
+  return (T)k;
+}
+
+// K1: dense row-major f64 cost[a][b] -> kT.  Unswapped (n_a >= n_b):
+// kT[b][a] (32x32 smem transpose).  Swapped: internal rows are original a,
+// so kT[a][b] is a straight row-major rounding.
+template <typename T>
+__global__ void round_dense_kernel(const double* __restrict__ cost, int n_a, int n_b,
+                                   int swapped, double eps, T* __restrict__ kT, int lda,
+                                   int* status) {
+  __shared__ T tile[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  if (!swapped) {
+    const int a0 = blockIdx.x * 32, b0 = blockIdx.y * 32;  // a along lda
+    for (int r = ty; r < 32; r += 8) {
+      const int a = a0 + r, b = b0 + tx;
+      T v = (T)type_max<T>();
+      if (a < n_a && b < n_b) {
+        const double c = cost[(size_t)a * n_b + b];
+        if (!(c >= 0.0 && c <= 1.0)) atomicCAS(status, 0, 2);
+        else v = clamp_store<T>(scaled_floor_dev(c, eps));
+      }
+      tile[r][tx] = v;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int b = b0 + r, a = a0 + tx;
+      if (b < n_b && a < lda) kT[(size_t)b * lda + a] = tile[tx][r];
+    }
+  } else {
+    // internal (a' = b, b' = a): kT[a][b] = k(cost[a][b]); lda pads n_b.
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int r = ty; r < 32; r += 8) {
+      const int a = r0 + r, b = c0 + tx;
+      if (a >= n_a || b >= lda) continue;
+      T v = (T)type_max<T>();
+      if (b < n_b) {
+        const double c = cost[(size_t)a * n_b + b];
+        if (!(c >= 0.0 && c <= 1.0)) atomicCAS(status, 0, 2);
+        else v = clamp_store<T>(scaled_floor_dev(c, eps));
+      }
+      kT[(size_t)a * lda + b] = v;
+    }
+  }
+}
+
+// K2: 2-D points -> kT with c = sqrt(dx*dx + dy*dy) / sqrt(2)
+// (gen_uniform_square, instances.cpp:70-75).  Internal orientation: pa are
+// the n_ai demand points, pb the n_bi supply points; the formula is exactly
+// symmetric under swapping the roles of the two points.
+template <typename T>
+__global__ void round_points_kernel(const double2* __restrict__ pa,
+                                    const double2* __restrict__ pb, int n_ai, int n_bi,
+                                    double eps, double sqrt2, T* __restrict__ kT, int lda) {
+  for (int b = blockIdx.y; b < n_bi; b += gridDim.y) {
+    const double2 q = pb[b];
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < lda; a += gridDim.x * blockDim.x) {
+      T v = (T)type_max<T>();
+      if (a < n_ai) {
+        const double2 p = pa[a];
+        const double dx = __dsub_rn(p.x, q.x);
+        const double dy = __dsub_rn(p.y, q.y);
+        const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        const double c = __ddiv_rn(__dsqrt_rn(d2), sqrt2);
+        v = clamp_store<T>(scaled_floor_dev(c, eps));
+      }
+      kT[(size_t)b * lda + a] = v;
+    }
+  }
+}
+
+template <typename T>
+__global__ void export_k_kernel(const T* __restrict__ kT, int n_ai, int n_bi, int lda,
+                                int swapped, int32_t* __restrict__ k) {
+  // original orientation row-major: unswapped k[a][b] = kT[b][a] (n_a = n_ai);
+  // swapped k[a][b] = kT[a][b] with original n_a = n_bi, n_b = n_ai.
+  const size_t total = (size_t)n_ai * n_bi;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    if (!swapped) {
+      const size_t a = i / n_bi, b = i % n_bi;
+      k[i] = kT[b * lda + a];
+    } else {
+      const size_t a = i / n_ai, b = i % n_ai;
+      k[i] = kT[a * lda + b];
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swapped, double eps,
+                               void* kT, int lda, int width, int* status, cudaStream_t s) {
+  dim3 block(32, 8);
+  dim3 grid;
+  if (!swapped)
+    grid = dim3((lda + 31) / 32, (n_b + 31) / 32);
+  else
+    grid = dim3((lda + 31) / 32, (n_a + 31) / 32);
+  if (width == 1)
+    round_dense_kernel<uint8_t><<<grid, block, 0, s>>>(cost, n_a, n_b, swapped, eps,
+                                                       static_cast<uint8_t*>(kT), lda, status);
+  else
+    round_dense_kernel<uint16_t><<<grid, block, 0, s>>>(cost, n_a, n_b, swapped, eps,
+                                                        static_cast<uint16_t*>(kT), lda, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
+                                  double eps, double sqrt2, void* kT, int lda, int width,
+                                  cudaStream_t s) {
+  const int bx = (lda + 255) / 256;
+  dim3 grid(bx < 8 ? bx : 8, n_bi < 65535 ? n_bi : 65535);
+  const double2* a2 = reinterpret_cast<const double2*>(pa);
+  const double2* b2 = reinterpret_cast<const double2*>(pb);
+  if (width == 1)
+    round_points_kernel<uint8_t><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2,
+                                                      static_cast<uint8_t*>(kT), lda);
+  else
+    round_points_kernel<uint16_t><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2,
+                                                       static_cast<uint16_t*>(kT), lda);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_k(const void* kT, int n_ai, int n_bi, int lda, int width, bool swapped,
+                            int32_t* k_out, cudaStream_t s) {
+  if (width == 1)
+    export_k_kernel<uint8_t><<<1184, 256, 0, s>>>(static_cast<const uint8_t*>(kT), n_ai, n_bi,
+                                                  lda, swapped, k_out);
+  else
+    export_k_kernel<uint16_t><<<1184, 256, 0, s>>>(static_cast<const uint16_t*>(kT), n_ai, n_bi,
+                                                   lda, swapped, k_out);
+  return cudaGetLastError();
+}
+
+}  // namespace otprg

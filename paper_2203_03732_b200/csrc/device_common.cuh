@@ -1,0 +1,129 @@
+// device_common.cuh — shared device helpers for the sm_100a kernels:
+// packed-SIMD traits for the rounded-cost entry types, L2-coherent loads for
+// state that changes between phases, and a grid barrier for the persistent
+// cooperative phase loop.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace otprg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Control block of one solve; lives in device memory, zero-initialised by the
+// host before phase 1.  Fields written during the loop are only read through
+// ld.cg / atomics (never through L1).
+struct Ctl {
+  // set by the host
+  int32_t n_a, n_b, lda;
+  int32_t thresh;       // floor(eps * min(n_a, n_b)) : stop when n_i <= thresh
+  int32_t phase_cap;    // phase_bound(eps) + 8  (assignment.cpp:326)
+  uint32_t tmax;        // dual bound ceil(1/eps)+2 (core.hpp:95) in units
+  // loop state
+  uint32_t phase;       // phases executed so far
+  int32_t cnt[2];       // free-b list sizes (ping-pong)
+  int32_t mp_cnt[2];    // newly-held-a list sizes (ping-pong)
+  int32_t work[2];      // dynamic chain-grab counters (ping-pong)
+  int32_t status;       // 0 ok, else otprg_status
+  int32_t done;         // 1 once the termination test passed
+  int32_t full_match;   // n_i == 0 at termination
+  int32_t pad0;
+  int64_t sum_ni;
+  unsigned long long bytes_touched;
+  unsigned long long chain_steps;
+  // grid barrier
+  unsigned int bar_count;
+  unsigned int bar_gen;
+  int32_t err_a, err_b;  // first offending index (diagnostics)
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ int ld_cg(const int* p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned ld_cg(const unsigned* p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ld_cg(const unsigned long long* p) {
+  return __ldcg(p);
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Sense-by-generation grid barrier.  Requires all blocks co-resident
+// (cooperative launch).  A wait longer than 4 s flags status 6 and returns
+// instead of hanging the device.
+__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned nblocks = gridDim.x;
+    const unsigned gen = ld_acquire(&ctl->bar_gen);
+    __threadfence();
+    const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(&ctl->bar_count, 0u);
+      __threadfence();
+      st_release(&ctl->bar_gen, gen + 1);
+    } else {
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire(&ctl->bar_gen) == gen) {
+        if (globaltimer() - t0 > 4000000000ull) {
+          atomicCAS(&ctl->status, 0, 6);
+          break;
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---- packed SIMD traits over 32-bit words ---------------------------------
+// sum = k + t saturating (never wraps to a small value), eq = per-element
+// all-ones where sum == target, mn = per-element min.
+template <typename T>
+struct Simd;
+
+template <>
+struct Simd<uint8_t> {
+  static constexpr int kEpw = 4;  // elements per 32-bit word
+  static constexpr uint32_t kPadWord = 0xffffffffu;
+  __device__ static uint32_t rep(uint32_t v) { return v * 0x01010101u; }
+  __device__ static uint32_t add(uint32_t k, uint32_t t) { return __vaddus4(k, t); }
+  __device__ static uint32_t eq(uint32_t s, uint32_t tg) { return __vcmpeq4(s, tg); }
+  __device__ static uint32_t mn(uint32_t a, uint32_t b) { return __vminu4(a, b); }
+  __device__ static uint32_t hmin(uint32_t w) {
+    uint32_t m = min(w & 0xffu, (w >> 8) & 0xffu);
+    return min(m, min((w >> 16) & 0xffu, w >> 24));
+  }
+};
+
+template <>
+struct Simd<uint16_t> {
+  static constexpr int kEpw = 2;
+  static constexpr uint32_t kPadWord = 0xffffffffu;
+  __device__ static uint32_t rep(uint32_t v) { return v * 0x00010001u; }
+  __device__ static uint32_t add(uint32_t k, uint32_t t) { return __vaddus2(k, t); }
+  __device__ static uint32_t eq(uint32_t s, uint32_t tg) { return __vcmpeq2(s, tg); }
+  __device__ static uint32_t mn(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+  __device__ static uint32_t hmin(uint32_t w) { return min(w & 0xffffu, w >> 16); }
+};
+
+#endif  // __CUDACC__
+
+// Largest representable entry of T: the pad value of kT rows, and the
+// saturation value of k + t.  Targets are always strictly below it.
+template <typename T>
+__host__ __device__ constexpr uint32_t type_max() {
+  return sizeof(T) == 1 ? 0xffu : 0xffffu;
+}
+
+}  // namespace otprg

@@ -1,0 +1,53 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal to
+// libotprg.so; the public boundary is include/otprg.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device_common.cuh"
+
+namespace otprg {
+
+// Device state of one prepared assignment problem, in the solver's internal
+// orientation (n_a >= n_b; rows of kT are supply vertices b, contiguous over
+// demand vertices a).
+struct SolveArgs {
+  const void* kT;               // T[n_b][lda], pad entries = type max
+  void* t;                      // T[lda]  : t(a) = -Y(a) >= 0, pad = 0
+  int32_t* yb;                  // [n_b]   : Y(b) >= 1
+  int32_t* match_a;             // [n_a]
+  int32_t* match_b;             // [n_b]
+  unsigned long long* holder;   // [n_a]   : DA holder keys (~phase << 32 | b)
+  void* rowmin;                 // T[n_b]  : lower bound on min_a k(a,b)+t(a)
+  int32_t* list[2];             // [n_b]   : free-b lists (ping-pong)
+  int32_t* mp[2];               // [n_b]   : newly-held-a lists (ping-pong)
+  int64_t* free_counts;         // [phase_cap + 1]
+  Ctl* ctl;
+  uint32_t max_phase;           // run phases up to and including this one
+};
+
+// Rounding kernels (K1/K2): write kT in the internal orientation.
+// width = sizeof(T) of kT (1 or 2).
+cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swapped, double eps,
+                               void* kT, int lda, int width, int* status, cudaStream_t s);
+cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
+                                  double eps, double sqrt2, void* kT, int lda, int width,
+                                  cudaStream_t s);
+// Rounded matrix back to int32 row-major in the ORIGINAL orientation (for
+// otprg_scale_round_costs).
+cudaError_t launch_export_k(const void* kT, int n_ai, int n_bi, int lda, int width, bool swapped,
+                            int32_t* k_out, cudaStream_t s);
+
+// Phase loop.
+cudaError_t launch_init_state(const SolveArgs& a, int n_a, int n_b, int lda, int width,
+                              cudaStream_t s);
+cudaError_t launch_phase_loop(const SolveArgs& a, int width, bool smem_t, int lda, int grid,
+                              cudaStream_t s);
+int phase_loop_grid(int width, bool smem_t, int lda, int num_sms);
+size_t phase_loop_smem(int width, bool smem_t, int lda);
+bool smem_t_fits(int width, int lda);
+cudaError_t launch_complete(int32_t* match_a, int32_t* match_b, int n_a, int n_b,
+                            int32_t* scratch_a, int32_t* scratch_b, cudaStream_t s);
+cudaError_t launch_flush(void* buf, size_t bytes, cudaStream_t s);
+
+}  // namespace otprg

@@ -1,0 +1,475 @@
+// otprg_capi.cpp — host side of the C ABI declared in include/otprg.h.
+//
+// Validation, storage choice, device buffers and the launch sequence of the
+// assignment path:
+//   H2D -> cost build/rounding (K1 dense / K2 points) -> init_state ->
+//   phase loop (phase 1 as its own launch, then the rest) -> completion ->
+//   D2H -> matching cost on the host.
+// Mirrors otpr::solve_assignment (src/assignment.cpp:368-400) and
+// otpr::scale_round_costs (src/core.cpp:34-53).  Built with
+// -ffp-contract=off so the host-side cost sums match the reference bits.
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/otprg.h"
+#include "kernels.h"
+
+using otprg::Ctl;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Status {
+  int code = OTPRG_OK;
+  std::string msg;
+};
+
+// scaled_floor, core.cpp:26-32 (host copy for units / thresholds).
+int64_t host_scaled_floor(double c, double eps) {
+  auto k = static_cast<int64_t>(std::floor(c / eps));
+  while (static_cast<double>(k + 1) * eps <= c) ++k;
+  while (k > 0 && static_cast<double>(k) * eps > c) --k;
+  return k;
+}
+
+}  // namespace
+
+struct otprg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  int num_sms = 0;
+  std::string err;
+
+  // prepared problem
+  bool prepared = false;
+  int32_t n_a = 0, n_b = 0;  // original orientation
+  int32_t ia = 0, ib = 0;    // internal: ia >= ib
+  bool swapped = false;
+  int width = 1, lda = 0;
+  double eps = 0.0;
+  int32_t unit_floor = 0, unit_ceil = 0;
+  int cost_kind = 0;
+  const double* host_cost = nullptr;  // caller buffer (DENSE); valid until next prepare
+  std::vector<double> pts_a, pts_b;   // original orientation (POINTS2D)
+  double build_ms = 0.0;
+  int build_launches = 0;
+
+  DevBuf kT, t, yb, ma, mb, holder, rowmin, list0, list1, mp0, mp1, fc, ctl, fa, fb;
+  DevBuf stage, pts, flush;
+  int64_t fc_cap = 0;
+  int loop_grid = 0;
+  bool smem_t = true;
+};
+
+namespace {
+
+int fail(otprg_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_fail(otprg_ctx* ctx, cudaError_t e, const char* what) {
+  return fail(ctx, OTPRG_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                \
+  do {                                                \
+    cudaError_t _e = (expr);                          \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, what); \
+  } while (0)
+
+// Validation of solve_assignment (assignment.cpp:370-372) and
+// scale_round_costs (core.cpp:35-47) that does not need the cost values.
+int validate_problem(otprg_ctx* ctx, const otprg_problem* p) {
+  if (!p) return fail(ctx, OTPRG_PARAMETER, "null problem");
+  if (p->n_a < 1 || p->n_b < 1)
+    return fail(ctx, OTPRG_PARAMETER, "instance needs at least one vertex per side");
+  if (!(p->eps > 0.0 && p->eps < 1.0))
+    return fail(ctx, OTPRG_PARAMETER, "eps must lie in (0, 1), got " + std::to_string(p->eps));
+  const int64_t uf = host_scaled_floor(1.0, p->eps);
+  if (uf + 4 > std::numeric_limits<int32_t>::max())
+    return fail(ctx, OTPRG_PARAMETER, "eps too small: 1/eps overflows the cost unit type");
+  switch (p->cost_kind) {
+    case OTPRG_COST_DENSE_F64:
+      if (!p->cost) return fail(ctx, OTPRG_PARAMETER, "dense cost pointer is null");
+      break;
+    case OTPRG_COST_POINTS2D:
+      if (!p->pts_a || !p->pts_b) return fail(ctx, OTPRG_PARAMETER, "point pointers are null");
+      break;
+    default:
+      return fail(ctx, OTPRG_PARAMETER, "unsupported cost kind " + std::to_string(p->cost_kind));
+  }
+  return OTPRG_OK;
+}
+
+int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
+  int st = validate_problem(ctx, p);
+  if (st) return st;
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  ctx->prepared = false;
+  ctx->n_a = p->n_a;
+  ctx->n_b = p->n_b;
+  ctx->swapped = p->n_b > p->n_a;  // assignment.cpp:385-399
+  ctx->ia = ctx->swapped ? p->n_b : p->n_a;
+  ctx->ib = ctx->swapped ? p->n_a : p->n_b;
+  ctx->eps = p->eps;
+  ctx->cost_kind = p->cost_kind;
+  const int64_t uf = host_scaled_floor(1.0, p->eps);
+  ctx->unit_floor = static_cast<int32_t>(uf);
+  ctx->unit_ceil = static_cast<int32_t>(static_cast<double>(uf) * p->eps == 1.0 ? uf : uf + 1);
+
+  // Storage: |Y| <= unit_ceil + 2 (core.hpp:94-95) must stay below the
+  // saturation value of the packed k + t sums.
+  const int64_t need = static_cast<int64_t>(ctx->unit_ceil) + 2;
+  const bool fits8 = need <= 253, fits16 = need <= 65533;
+  int width = 0;
+  if (p->storage == OTPRG_STORAGE_U8) width = fits8 ? 1 : -1;
+  else if (p->storage == OTPRG_STORAGE_U16) width = fits16 ? 2 : -1;
+  else width = fits8 ? 1 : (fits16 ? 2 : -1);
+  if (width < 0)
+    return fail(ctx, OTPRG_PARAMETER,
+                "eps too small for the device cost storage (ceil(1/eps)+2 = " +
+                    std::to_string(need) + ")");
+  ctx->width = width;
+  const int align = 512 / width;
+  ctx->lda = (ctx->ia + align - 1) / align * align;
+
+  const size_t ia = ctx->ia, ib = ctx->ib, lda = ctx->lda;
+  CK(ctx->kT.ensure(ib * lda * width), "alloc kT");
+  CK(ctx->t.ensure(lda * width), "alloc t");
+  CK(ctx->yb.ensure(ib * 4), "alloc yb");
+  CK(ctx->ma.ensure(ia * 4), "alloc match_a");
+  CK(ctx->mb.ensure(ib * 4), "alloc match_b");
+  CK(ctx->holder.ensure(ia * 8), "alloc holder");
+  CK(ctx->rowmin.ensure(ib * width), "alloc rowmin");
+  CK(ctx->list0.ensure(ib * 4), "alloc list");
+  CK(ctx->list1.ensure(ib * 4), "alloc list");
+  CK(ctx->mp0.ensure(ib * 4), "alloc mp");
+  CK(ctx->mp1.ensure(ib * 4), "alloc mp");
+  CK(ctx->fa.ensure(ia * 4), "alloc scratch");
+  CK(ctx->fb.ensure(ib * 4), "alloc scratch");
+  CK(ctx->ctl.ensure(sizeof(Ctl)), "alloc ctl");
+  const double capd = std::ceil((1.0 + 2.0 * p->eps) / (p->eps * p->eps)) + 8.0;
+  ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(1 << 24)));
+  CK(ctx->fc.ensure(ctx->fc_cap * 8), "alloc free_counts");
+  ctx->smem_t = otprg::smem_t_fits(width, ctx->lda);
+  ctx->loop_grid = otprg::phase_loop_grid(width, ctx->smem_t, ctx->lda, ctx->num_sms);
+  if (ctx->loop_grid <= 0) return fail(ctx, OTPRG_DEVICE, "phase loop kernel cannot be resident");
+
+  CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
+  ctx->build_launches = 0;
+  if (p->cost_kind == OTPRG_COST_DENSE_F64) {
+    const size_t bytes = static_cast<size_t>(p->n_a) * p->n_b * sizeof(double);
+    CK(ctx->stage.ensure(bytes), "alloc cost staging");
+    CK(cudaMemcpyAsync(ctx->stage.p, p->cost, bytes, cudaMemcpyHostToDevice, ctx->stream),
+       "H2D cost");
+    CK(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(Ctl), ctx->stream), "memset");
+    int* status = &ctx->ctl.as<Ctl>()->status;
+    CK(otprg::launch_round_dense(ctx->stage.as<double>(), p->n_a, p->n_b, ctx->swapped, p->eps,
+                                 ctx->kT.p, ctx->lda, width, status, ctx->stream),
+       "round_dense launch");
+    ctx->build_launches = 1;
+    ctx->host_cost = p->cost;
+  } else {
+    const double* pa = ctx->swapped ? p->pts_b : p->pts_a;  // internal demand points
+    const double* pb = ctx->swapped ? p->pts_a : p->pts_b;
+    CK(ctx->pts.ensure((ia + ib) * 2 * sizeof(double)), "alloc points");
+    double* dpa = ctx->pts.as<double>();
+    double* dpb = dpa + ia * 2;
+    CK(cudaMemcpyAsync(dpa, pa, ia * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
+       "H2D points");
+    CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
+       "H2D points");
+    CK(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(Ctl), ctx->stream), "memset");
+    CK(otprg::launch_round_points2d(dpa, dpb, ctx->ia, ctx->ib, p->eps, std::sqrt(2.0), ctx->kT.p,
+                                    ctx->lda, width, ctx->stream),
+       "round_points launch");
+    ctx->build_launches = 1;
+    ctx->pts_a.assign(p->pts_a, p->pts_a + 2 * static_cast<size_t>(p->n_a));
+    ctx->pts_b.assign(p->pts_b, p->pts_b + 2 * static_cast<size_t>(p->n_b));
+  }
+  CK(cudaEventRecord(ctx->ev[5], ctx->stream), "event");
+  int dstatus = 0;
+  CK(cudaMemcpyAsync(&dstatus, &ctx->ctl.as<Ctl>()->status, sizeof(int), cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H status");
+  CK(cudaStreamSynchronize(ctx->stream), "cost build");
+  if (dstatus == OTPRG_PARAMETER) return fail(ctx, OTPRG_PARAMETER, "cost entry outside [0,1]");
+  if (dstatus) return fail(ctx, dstatus, "cost build failed");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]);
+  ctx->build_ms = ms;
+  ctx->prepared = true;
+  return OTPRG_OK;
+}
+
+double pair_cost(const otprg_ctx* ctx, int32_t a, int32_t b) {
+  if (ctx->cost_kind == OTPRG_COST_DENSE_F64)
+    return ctx->host_cost[static_cast<size_t>(a) * ctx->n_b + b];
+  // instances.cpp:70-75, same expression, non-fused (-ffp-contract=off)
+  const double sqrt2 = std::sqrt(2.0);
+  const double dx = ctx->pts_a[2 * static_cast<size_t>(a)] - ctx->pts_b[2 * static_cast<size_t>(b)];
+  const double dy =
+      ctx->pts_a[2 * static_cast<size_t>(a) + 1] - ctx->pts_b[2 * static_cast<size_t>(b) + 1];
+  return std::sqrt(dx * dx + dy * dy) / sqrt2;
+}
+
+int do_solve(otprg_ctx* ctx, otprg_result* r) {
+  if (!ctx->prepared) return fail(ctx, OTPRG_PARAMETER, "no prepared problem");
+  if (!r || !r->match_of_a || !r->match_of_b)
+    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int ia = ctx->ia, ib = ctx->ib;
+
+  Ctl h{};
+  h.n_a = ia;
+  h.n_b = ib;
+  h.lda = ctx->lda;
+  const double threshold = ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b));
+  h.thresh = static_cast<int32_t>(std::floor(threshold));
+  h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
+  h.tmax = ctx->width == 1 ? 253u : 65533u;
+  h.cnt[1] = ib;
+
+  otprg::SolveArgs A{};
+  A.kT = ctx->kT.p;
+  A.t = ctx->t.p;
+  A.yb = ctx->yb.as<int32_t>();
+  A.match_a = ctx->ma.as<int32_t>();
+  A.match_b = ctx->mb.as<int32_t>();
+  A.holder = ctx->holder.as<unsigned long long>();
+  A.rowmin = ctx->rowmin.p;
+  A.list[0] = ctx->list0.as<int32_t>();
+  A.list[1] = ctx->list1.as<int32_t>();
+  A.mp[0] = ctx->mp0.as<int32_t>();
+  A.mp[1] = ctx->mp1.as<int32_t>();
+  A.free_counts = ctx->fc.as<int64_t>();
+  A.ctl = ctx->ctl.as<Ctl>();
+
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, s), "H2D ctl");
+  CK(otprg::launch_init_state(A, ia, ib, ctx->lda, ctx->width, s), "init launch");
+  CK(cudaEventRecord(ctx->ev[0], s), "event");
+  A.max_phase = 1;
+  CK(otprg::launch_phase_loop(A, ctx->width, ctx->smem_t, ctx->lda, ctx->loop_grid, s),
+     "phase loop launch (phase 1)");
+  CK(cudaEventRecord(ctx->ev[1], s), "event");
+  A.max_phase = 0xffffffffu;
+  CK(otprg::launch_phase_loop(A, ctx->width, ctx->smem_t, ctx->lda, ctx->loop_grid, s),
+     "phase loop launch");
+  CK(otprg::launch_complete(A.match_a, A.match_b, ia, ib, ctx->fa.as<int32_t>(),
+                            ctx->fb.as<int32_t>(), s),
+     "complete launch");
+  CK(cudaEventRecord(ctx->ev[2], s), "event");
+
+  std::vector<int32_t> ma(ia), mb(ib), yb(ib);
+  std::vector<uint8_t> tbytes(static_cast<size_t>(ia) * ctx->width);
+  CK(cudaMemcpyAsync(&h, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s), "D2H ctl");
+  CK(cudaMemcpyAsync(ma.data(), ctx->ma.p, ia * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(mb.data(), ctx->mb.p, ib * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(yb.data(), ctx->yb.p, ib * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(tbytes.data(), ctx->t.p, tbytes.size(), cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaStreamSynchronize(s), "solve");
+  if (h.status == 6) return fail(ctx, OTPRG_DEVICE, "device barrier timeout");
+  if (h.status == OTPRG_INVARIANT) {
+    if (h.err_a || h.err_b)
+      return fail(ctx, OTPRG_INVARIANT, "dual exceeded the device storage bound");
+    return fail(ctx, OTPRG_INVARIANT,
+                "phase count exceeded the proven bound; solver state is corrupt");
+  }
+  if (h.status) return fail(ctx, h.status, "device solve failed");
+  if (!h.done) return fail(ctx, OTPRG_DEVICE, "phase loop ended without termination");
+
+  const int64_t phases = h.phase;
+  if (r->free_counts && r->free_cap > 0 && phases > 0) {
+    const int64_t nf = std::min<int64_t>(phases, r->free_cap);
+    CK(cudaMemcpyAsync(r->free_counts, ctx->fc.p, nf * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "D2H free_counts");
+  }
+  float ms_all = 0.f, ms_p1 = 0.f;
+  cudaEventElapsedTime(&ms_all, ctx->ev[0], ctx->ev[2]);
+  cudaEventElapsedTime(&ms_p1, ctx->ev[0], ctx->ev[1]);
+
+  // Back to the caller's orientation (assignment.cpp:395-399).
+  if (!ctx->swapped) {
+    std::memcpy(r->match_of_a, ma.data(), ia * 4ull);
+    std::memcpy(r->match_of_b, mb.data(), ib * 4ull);
+  } else {
+    std::memcpy(r->match_of_a, mb.data(), ib * 4ull);
+    std::memcpy(r->match_of_b, ma.data(), ia * 4ull);
+  }
+  if (r->y_a) {
+    for (int i = 0; i < ia; ++i) {
+      const int64_t t = ctx->width == 1 ? tbytes[i]
+                                        : reinterpret_cast<const uint16_t*>(tbytes.data())[i];
+      r->y_a[i] = -t;
+    }
+  }
+  if (r->y_b)
+    for (int i = 0; i < ib; ++i) r->y_b[i] = yb[i];
+  r->phases = phases;
+  r->sum_ni = h.sum_ni;
+  r->swapped = ctx->swapped;
+  r->full_match_termination = h.full_match;
+  double total = 0.0;  // matching_cost, core.cpp:95-102
+  for (int32_t a = 0; a < ctx->n_a; ++a) {
+    const int32_t b = r->match_of_a[a];
+    if (b != -1) total += pair_cost(ctx, a, b);
+  }
+  r->cost = total;
+  r->build_ms = ctx->build_ms;
+  r->solve_ms = ms_all;
+  r->phase1_ms = ms_p1;
+  r->bytes_touched = static_cast<int64_t>(h.bytes_touched);
+  r->bytes_alg = h.sum_ni * static_cast<int64_t>(ia) * ctx->width;
+  r->width = ctx->width;
+  r->gpu_launches = 4;  // init, loop (phase 1), loop (rest), complete
+  return OTPRG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int otprg_version(void) { return 1; }
+
+int64_t otprg_scaled_floor(double c, double eps) { return host_scaled_floor(c, eps); }
+
+int otprg_create(int device, otprg_ctx** out) {
+  if (!out) return OTPRG_PARAMETER;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
+    return OTPRG_DEVICE;
+  auto* ctx = new otprg_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return OTPRG_DEVICE;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  *out = ctx;
+  return OTPRG_OK;
+}
+
+void otprg_destroy(otprg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (DevBuf* b : {&ctx->kT, &ctx->t, &ctx->yb, &ctx->ma, &ctx->mb, &ctx->holder, &ctx->rowmin,
+                    &ctx->list0, &ctx->list1, &ctx->mp0, &ctx->mp1, &ctx->fc, &ctx->ctl, &ctx->fa,
+                    &ctx->fb, &ctx->stage, &ctx->pts, &ctx->flush})
+    b->release();
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* otprg_last_error(const otprg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int otprg_prepare(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  int st = do_prepare(ctx, prob);
+  if (st == OTPRG_OK && res) {
+    res->build_ms = ctx->build_ms;
+    res->width = ctx->width;
+  }
+  return st;
+}
+
+int otprg_solve_prepared(otprg_ctx* ctx, otprg_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  return do_solve(ctx, res);
+}
+
+int otprg_solve_assignment(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  int st = do_prepare(ctx, prob);
+  if (st) return st;
+  st = do_solve(ctx, res);
+  if (st == OTPRG_OK) res->gpu_launches += ctx->build_launches;
+  return st;
+}
+
+int otprg_scale_round_costs(otprg_ctx* ctx, const otprg_problem* prob, int32_t* k,
+                            int32_t* unit_floor, int32_t* unit_ceil) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!k) return fail(ctx, OTPRG_PARAMETER, "k buffer is null");
+  int st = do_prepare(ctx, prob);
+  if (st) return st;
+  const size_t total = static_cast<size_t>(ctx->n_a) * ctx->n_b;
+  CK(ctx->stage.ensure(std::max(ctx->stage.n, total * 4)), "alloc export");
+  // the staging buffer may hold the dense input; it is no longer needed
+  CK(otprg::launch_export_k(ctx->kT.p, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->swapped,
+                            ctx->stage.as<int32_t>(), ctx->stream),
+     "export launch");
+  CK(cudaMemcpyAsync(k, ctx->stage.p, total * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H k");
+  CK(cudaStreamSynchronize(ctx->stream), "export");
+  if (unit_floor) *unit_floor = ctx->unit_floor;
+  if (unit_ceil) *unit_ceil = ctx->unit_ceil;
+  return OTPRG_OK;
+}
+
+int otprg_uniform_square_points(int32_t n, uint64_t seed, double* pts_a, double* pts_b) {
+  if (n < 1 || !pts_a || !pts_b) return OTPRG_PARAMETER;
+  auto splitmix64 = [](uint64_t x) {  // instances.cpp:41-46
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+  };
+  auto u01 = [](std::mt19937_64& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; };
+  std::mt19937_64 ra(splitmix64(seed));
+  std::mt19937_64 rb(splitmix64(seed ^ 0x9E3779B97F4A7C15ULL));
+  for (int32_t i = 0; i < n; ++i) {
+    pts_a[2 * static_cast<size_t>(i)] = u01(ra);
+    pts_a[2 * static_cast<size_t>(i) + 1] = u01(ra);
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    pts_b[2 * static_cast<size_t>(i)] = u01(rb);
+    pts_b[2 * static_cast<size_t>(i) + 1] = u01(rb);
+  }
+  return OTPRG_OK;
+}
+
+int otprg_flush_l2(otprg_ctx* ctx) {
+  if (!ctx) return OTPRG_PARAMETER;
+  const size_t bytes = 256ull << 20;
+  CK(ctx->flush.ensure(bytes), "alloc flush");
+  CK(otprg::launch_flush(ctx->flush.p, bytes, ctx->stream), "flush launch");
+  CK(cudaStreamSynchronize(ctx->stream), "flush");
+  return OTPRG_OK;
+}
+
+}  // extern "C"

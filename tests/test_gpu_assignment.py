@@ -1,0 +1,199 @@
+"""GPU parity tests: the CUDA path through the C ABI vs the reference.
+
+Every case compares the full result — matching, integer duals (internal
+orientation), phase count, free_counts, Σn_i, swapped /
+full_match_termination flags and the cost bits — with fixtures produced by
+the UNMODIFIED reference (tests/golden/make_golden.py -> oracle/_ref) and,
+for ad-hoc instances, with the C oracle restatement.  Bar: bit-exact.
+
+Structure mirrors the reference's tests/test_assignment.cpp and
+tests/test_core.cpp.
+"""
+import numpy as np
+import pytest
+
+from golden_util import PIN_KEYS, load_arrays, pins_of, random_instance
+
+pytestmark = pytest.mark.gpu
+
+otprg = pytest.importorskip("paper_2203_03732_b200")
+
+
+def _solve(inst, eps, storage="auto"):
+    return otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=eps, storage=storage))
+
+
+def _pins(m, s):
+    return pins_of(m.match_of_a, s.duals_final.y_a, s.duals_final.y_b, s.free_counts, s.phases,
+                   s.sum_ni, s.device["cost"])
+
+
+def _assert_matches_golden(key, want, m, s):
+    got = _pins(m, s)
+    if any(got[k] != want[k] for k in PIN_KEYS):
+        arr = load_arrays(key)
+        fc = np.asarray(arr["free_counts"], np.int64)
+        n = min(len(fc), len(s.free_counts))
+        first = int(np.argmax(fc[:n] != s.free_counts[:n])) if (fc[:n] != s.free_counts[:n]).any() else n
+        raise AssertionError(
+            f"{key}: got {got} want {{{', '.join(f'{k}: {want[k]}' for k in PIN_KEYS)}}}; "
+            f"first free_counts divergence at phase {first + 1}; "
+            f"match mismatches {(arr['match_of_a'] != m.match_of_a).sum()}")
+    assert bool(s.swapped) == bool(want["swapped"])
+    assert bool(s.full_match_termination) == bool(want["full_match_termination"])
+
+
+def _square_cases(golden, max_n):
+    return sorted(k for k, v in golden.items() if v["kind"] == "square" and v["n_a"] <= max_n)
+
+
+# ---- KATs (test_core.cpp:22-37, test_assignment.cpp:163-185) --------------
+
+def _single(c):
+    return otprg.AssignmentInstance(1, 1, np.full((1, 1), c))
+
+
+def test_scale_round_costs_kats():
+    assert otprg.scale_round_costs(_single(0.57), 0.1).k[0, 0] == 5
+    assert otprg.scale_round_costs(_single(0.0), 0.1).k[0, 0] == 0
+    sc = otprg.scale_round_costs(_single(1.0), 0.1)
+    assert sc.k[0, 0] == 10 and float(sc.k[0, 0]) * sc.eps == 1.0
+
+
+@pytest.mark.parametrize("eps", [0.0, 1.0, -0.1, 1e-12])
+def test_scale_round_costs_rejects_bad_eps(eps):
+    with pytest.raises(otprg.ParameterError):
+        otprg.scale_round_costs(_single(0.5), eps)
+
+
+def test_cost_outside_unit_interval_is_parameter_error():
+    inst = otprg.AssignmentInstance(2, 2, np.array([[0.1, 0.2], [0.3, 1.5]]))
+    with pytest.raises(otprg.ParameterError):
+        otprg.Solver(0).solve(inst, otprg.AssignmentOptions(eps=0.1))
+
+
+def test_one_by_one_phase_counts():
+    m, s = _solve(_single(0.375), 0.125)
+    assert m.match_of_a[0] == 0
+    assert s.phases == 4
+    assert list(s.free_counts) == [1, 1, 1, 1]
+    assert s.duals_final.y_b[0] == 4 and s.duals_final.y_a[0] == -1
+    assert s.device["cost"] == 0.375
+    m2, s2 = _solve(_single(0.3), 0.1)
+    assert s2.phases == 3 and s2.duals_final.y_b[0] == 3
+    assert s2.device["cost"] == 0.3
+
+
+def test_coarse_eps_completes_by_index():
+    inst = otprg.AssignmentInstance(10, 10, random_instance(10, 10, 2024))
+    m, s = _solve(inst, 0.99)
+    assert m.size() == 10
+    m.validate()
+
+
+# ---- rounding parity -----------------------------------------------------
+
+@pytest.mark.parametrize("eps", [0.1, 0.01, 1.0 / 300.0, 0.125, 0.07, 0.003])
+def test_rounding_dense_and_points_match_oracle(oracle, eps):
+    n = 700
+    pts = oracle.uniform_square_points(n, 5)
+    cost = oracle.gen_uniform_square(n, 5)
+    want, uf, uc = oracle.scale_round_costs(cost, eps)
+    inst_d = otprg.AssignmentInstance(n, n, cost)
+    sc = otprg.scale_round_costs(inst_d, eps)
+    assert (sc.unit_floor, sc.unit_ceil) == (uf, uc)
+    np.testing.assert_array_equal(sc.k, want)
+    inst_p = otprg.AssignmentInstance(n, n, None, np.stack(pts[:2], 1), np.stack(pts[2:], 1))
+    np.testing.assert_array_equal(otprg.scale_round_costs(inst_p, eps).k, want)
+
+
+def test_rounding_unbalanced_both_orientations(oracle):
+    for n_a, n_b in ((37, 301), (301, 37)):
+        cost = random_instance(n_a, n_b, 99)
+        want, _, _ = oracle.scale_round_costs(cost, 0.007)
+        for storage in ("u16", "auto"):
+            got = otprg.scale_round_costs(otprg.AssignmentInstance(n_a, n_b, cost), 0.007, storage)
+            np.testing.assert_array_equal(got.k, want)
+
+
+# ---- full-solve parity against the reference's own outputs ---------------
+
+def test_random_instances_match_reference(golden):
+    keys = sorted(k for k, v in golden.items() if v["kind"] == "random")
+    assert keys
+    for key in keys:
+        w = golden[key]
+        inst = otprg.AssignmentInstance(w["n_a"], w["n_b"], random_instance(w["n_a"], w["n_b"], w["seed"]))
+        m, s = _solve(inst, w["eps"])
+        _assert_matches_golden(key, w, m, s)
+        m.validate()
+
+
+def test_square_points_match_reference(golden):
+    for key in _square_cases(golden, 4000):
+        w = golden[key]
+        inst = otprg.gen_uniform_square(w["n_a"], w["seed"])
+        m, s = _solve(inst, w["eps"])
+        _assert_matches_golden(key, w, m, s)
+
+
+def test_square_dense_match_reference(golden):
+    for key in _square_cases(golden, 1000)[:12]:
+        w = golden[key]
+        inst = otprg.gen_uniform_square(w["n_a"], w["seed"], dense=True)
+        m, s = _solve(inst, w["eps"])
+        _assert_matches_golden(key, w, m, s)
+
+
+def test_config2_n10k_eps001_seeds_1_2_3(golden):
+    for seed in (1, 2, 3):
+        key = f"square_n10000_eps0.01_s{seed}"
+        w = golden[key]
+        inst = otprg.gen_uniform_square(10000, seed)
+        for storage in ("u8", "u16"):
+            m, s = _solve(inst, 0.01, storage)
+            _assert_matches_golden(key, w, m, s)
+
+
+def test_config2_dense_f64_input(golden):
+    key = "square_n10000_eps0.01_s1"
+    inst = otprg.gen_uniform_square(10000, 1, dense=True)
+    m, s = _solve(inst, 0.01)
+    _assert_matches_golden(key, golden[key], m, s)
+
+
+def test_large_eps_long_chains(golden):
+    for key in ("square_n10000_eps0.1_s1", "square_n10000_eps0.05_s1", "square_n4000_eps0.1_s1"):
+        w = golden[key]
+        m, s = _solve(otprg.gen_uniform_square(w["n_a"], w["seed"]), w["eps"])
+        _assert_matches_golden(key, w, m, s)
+
+
+def test_storage_widths_agree_and_repeat_is_deterministic():
+    inst = otprg.gen_uniform_square(3000, 11)
+    solver = otprg.Solver(0)
+    solver.prepare(inst, 0.02, "u8")
+    m1, s1 = solver.solve_prepared()
+    m2, s2 = solver.solve_prepared()
+    solver.prepare(inst, 0.02, "u16")
+    m3, s3 = solver.solve_prepared()
+    for m, s in ((m2, s2), (m3, s3)):
+        np.testing.assert_array_equal(m.match_of_a, m1.match_of_a)
+        np.testing.assert_array_equal(s.duals_final.y_a, s1.duals_final.y_a)
+        np.testing.assert_array_equal(s.duals_final.y_b, s1.duals_final.y_b)
+        np.testing.assert_array_equal(s.free_counts, s1.free_counts)
+    solver.close()
+
+
+def test_adhoc_unbalanced_vs_oracle(oracle):
+    rng = np.random.default_rng(3)
+    for n_a, n_b, eps in ((513, 200, 0.02), (200, 513, 0.02), (1, 7, 0.3), (7, 1, 0.3), (64, 64, 0.004)):
+        cost = rng.random((n_a, n_b))
+        want = oracle.solve_assignment(cost, eps)
+        m, s = _solve(otprg.AssignmentInstance(n_a, n_b, cost), eps)
+        np.testing.assert_array_equal(m.match_of_a, want.match_of_a)
+        np.testing.assert_array_equal(m.match_of_b, want.match_of_b)
+        np.testing.assert_array_equal(s.duals_final.y_a, want.y_a)
+        np.testing.assert_array_equal(s.duals_final.y_b, want.y_b)
+        np.testing.assert_array_equal(s.free_counts, want.free_counts)
+        assert s.device["cost"] == want.cost and s.swapped == want.swapped
