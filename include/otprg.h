@@ -131,6 +131,21 @@ int otprg_solve_assignment(otprg_ctx* ctx, const otprg_problem* prob, otprg_resu
 int otprg_prepare(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res);
 int otprg_solve_prepared(otprg_ctx* ctx, otprg_result* res);
 
+/* Stepping form (host-synced; used for per-phase observation like the
+ * reference's PhaseObserver, assignment.hpp:55-67, and for debugging):
+ *   otprg_begin     init_state on the prepared problem (assignment.cpp:54-60)
+ *   otprg_step      run phases until `max_phases` phases have executed in
+ *                   total (<= 0: until termination); reports the phase count
+ *                   and whether the termination test (:330-334) has passed
+ *   otprg_snapshot  copy the current state (matching, duals, free_counts,
+ *                   phases) without completing the matching
+ *   otprg_finish    run the remaining phases, complete the matching
+ *                   (:253-262) and return the final results. */
+int otprg_begin(otprg_ctx* ctx);
+int otprg_step(otprg_ctx* ctx, int64_t max_phases, int64_t* phases_done, int32_t* finished);
+int otprg_snapshot(otprg_ctx* ctx, otprg_result* res);
+int otprg_finish(otprg_ctx* ctx, otprg_result* res);
+
 /* Rounded costs k(a,b) = scaled_floor(c(a,b), eps) computed on the device
  * and returned row-major (n_a x n_b int32, like ScaledCosts::k), plus
  * unit_floor / unit_ceil (core.hpp:89-92).  Mirrors otpr::scale_round_costs. */

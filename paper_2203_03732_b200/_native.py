@@ -15,7 +15,7 @@ import subprocess
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libotprg.so")
+LIB_PATH = os.path.join(PKG_DIR, "lib", os.environ.get("OTPRG_LIB", "libotprg.so"))
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 OK, PARAMETER, INPUT, NUMERICAL, INVARIANT, DEVICE = 0, 2, 3, 4, 5, 6
@@ -50,7 +50,8 @@ class Result(C.Structure):
 EXPORTS = [
     "otprg_create", "otprg_destroy", "otprg_last_error", "otprg_version", "otprg_scaled_floor",
     "otprg_solve_assignment", "otprg_prepare", "otprg_solve_prepared", "otprg_scale_round_costs",
-    "otprg_uniform_square_points", "otprg_flush_l2",
+    "otprg_uniform_square_points", "otprg_flush_l2", "otprg_begin", "otprg_step",
+    "otprg_snapshot", "otprg_finish",
 ]
 
 _lib = None
@@ -86,6 +87,10 @@ def lib() -> C.CDLL:
                                           C.POINTER(C.c_int32)]
     L.otprg_uniform_square_points.argtypes = [C.c_int32, C.c_uint64, vp, vp]
     L.otprg_flush_l2.argtypes = [vp]
+    L.otprg_begin.argtypes = [vp]
+    L.otprg_step.argtypes = [vp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+    L.otprg_snapshot.argtypes = [vp, C.POINTER(Result)]
+    L.otprg_finish.argtypes = [vp, C.POINTER(Result)]
     _lib = L
     return L
 

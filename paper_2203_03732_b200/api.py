@@ -265,6 +265,36 @@ class Solver:
             self._raise(st)
         return self._pack(r, bufs)
 
+    # -- stepping (host-synced) form --
+    def begin(self) -> None:
+        st = self._L.otprg_begin(self._ctx)
+        if st:
+            self._raise(st)
+
+    def step(self, max_phases: int) -> tuple[int, bool]:
+        """Run until ``max_phases`` phases executed in total (<=0: to the end)."""
+        done, fin = C.c_int64(), C.c_int32()
+        st = self._L.otprg_step(self._ctx, max_phases, C.byref(done), C.byref(fin))
+        if st:
+            self._raise(st)
+        return int(done.value), bool(fin.value)
+
+    def snapshot(self):
+        n_a, n_b, eps = self._prepared
+        r, bufs = self._result(n_a, n_b, eps)
+        st = self._L.otprg_snapshot(self._ctx, C.byref(r))
+        if st:
+            self._raise(st)
+        return self._pack(r, bufs)
+
+    def finish(self):
+        n_a, n_b, eps = self._prepared
+        r, bufs = self._result(n_a, n_b, eps)
+        st = self._L.otprg_finish(self._ctx, C.byref(r))
+        if st:
+            self._raise(st)
+        return self._pack(r, bufs)
+
     def solve(self, inst: AssignmentInstance, opt: AssignmentOptions):
         p = self._problem(inst, opt.eps, opt.storage)
         r, bufs = self._result(inst.n_a, inst.n_b, opt.eps)

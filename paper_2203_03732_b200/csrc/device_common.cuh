@@ -34,7 +34,8 @@ struct Ctl {
   // grid barrier
   unsigned int bar_count;
   unsigned int bar_gen;
-  int32_t err_a, err_b;  // first offending index (diagnostics)
+  int32_t exh[2];        // b's that ended their chain unmatched (conservation check)
+  int32_t err[8];        // details of the first failure (written by its reporter only)
 };
 
 #ifdef __CUDACC__
@@ -58,6 +59,16 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Records the first failure: only the thread that moves status from 0 writes
+// the details, so they are never mixed between reporters.
+__device__ __forceinline__ void report(Ctl* ctl, int code, int e0, int e1 = 0, int e2 = 0,
+                                       int e3 = 0, int e4 = 0, int e5 = 0) {
+  if (atomicCAS(&ctl->status, 0, code) == 0) {
+    ctl->err[0] = e0; ctl->err[1] = e1; ctl->err[2] = e2;
+    ctl->err[3] = e3; ctl->err[4] = e4; ctl->err[5] = e5;
+  }
+}
+
 // Sense-by-generation grid barrier.  Requires all blocks co-resident
 // (cooperative launch).  A wait longer than 4 s flags status 6 and returns
 // instead of hanging the device.
@@ -76,7 +87,7 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl) {
       const unsigned long long t0 = globaltimer();
       while (ld_acquire(&ctl->bar_gen) == gen) {
         if (globaltimer() - t0 > 4000000000ull) {
-          atomicCAS(&ctl->status, 0, 6);
+          report(ctl, 6, (int)blockIdx.x);
           break;
         }
       }

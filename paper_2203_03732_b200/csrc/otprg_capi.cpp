@@ -90,6 +90,7 @@ struct otprg_ctx {
   int64_t fc_cap = 0;
   int loop_grid = 0;
   bool smem_t = true;
+  bool begun = false, completed = false;
 };
 
 namespace {
@@ -245,23 +246,7 @@ double pair_cost(const otprg_ctx* ctx, int32_t a, int32_t b) {
   return std::sqrt(dx * dx + dy * dy) / sqrt2;
 }
 
-int do_solve(otprg_ctx* ctx, otprg_result* r) {
-  if (!ctx->prepared) return fail(ctx, OTPRG_PARAMETER, "no prepared problem");
-  if (!r || !r->match_of_a || !r->match_of_b)
-    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
-  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-  const int ia = ctx->ia, ib = ctx->ib;
-
-  Ctl h{};
-  h.n_a = ia;
-  h.n_b = ib;
-  h.lda = ctx->lda;
-  const double threshold = ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b));
-  h.thresh = static_cast<int32_t>(std::floor(threshold));
-  h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
-  h.tmax = ctx->width == 1 ? 253u : 65533u;
-  h.cnt[1] = ib;
-
+otprg::SolveArgs make_args(otprg_ctx* ctx) {
   otprg::SolveArgs A{};
   A.kT = ctx->kT.p;
   A.t = ctx->t.p;
@@ -276,23 +261,78 @@ int do_solve(otprg_ctx* ctx, otprg_result* r) {
   A.mp[1] = ctx->mp1.as<int32_t>();
   A.free_counts = ctx->fc.as<int64_t>();
   A.ctl = ctx->ctl.as<Ctl>();
+  return A;
+}
 
-  cudaStream_t s = ctx->stream;
-  CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, s), "H2D ctl");
-  CK(otprg::launch_init_state(A, ia, ib, ctx->lda, ctx->width, s), "init launch");
-  CK(cudaEventRecord(ctx->ev[0], s), "event");
-  A.max_phase = 1;
-  CK(otprg::launch_phase_loop(A, ctx->width, ctx->smem_t, ctx->lda, ctx->loop_grid, s),
-     "phase loop launch (phase 1)");
-  CK(cudaEventRecord(ctx->ev[1], s), "event");
-  A.max_phase = 0xffffffffu;
-  CK(otprg::launch_phase_loop(A, ctx->width, ctx->smem_t, ctx->lda, ctx->loop_grid, s),
+// init_state (assignment.cpp:54-60) + loop control block.
+int do_begin(otprg_ctx* ctx) {
+  if (!ctx->prepared) return fail(ctx, OTPRG_PARAMETER, "no prepared problem");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  Ctl h{};
+  h.n_a = ctx->ia;
+  h.n_b = ctx->ib;
+  h.lda = ctx->lda;
+  // (double)n_i <= eps * m  <=>  n_i <= floor(eps * m)   (assignment.cpp:324-331)
+  const double threshold = ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b));
+  h.thresh = static_cast<int32_t>(std::floor(threshold));
+  h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
+  h.tmax = ctx->width == 1 ? 253u : 65533u;
+  h.cnt[1] = ctx->ib;
+  const otprg::SolveArgs A = make_args(ctx);
+  CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream), "H2D ctl");
+  CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->stream),
+     "init launch");
+  ctx->begun = true;
+  ctx->completed = false;
+  return OTPRG_OK;
+}
+
+int launch_loop(otprg_ctx* ctx, uint32_t max_phase) {
+  otprg::SolveArgs A = make_args(ctx);
+  A.max_phase = max_phase;
+  CK(otprg::launch_phase_loop(A, ctx->width, ctx->smem_t, ctx->lda, ctx->loop_grid, ctx->stream),
      "phase loop launch");
-  CK(otprg::launch_complete(A.match_a, A.match_b, ia, ib, ctx->fa.as<int32_t>(),
-                            ctx->fb.as<int32_t>(), s),
-     "complete launch");
-  CK(cudaEventRecord(ctx->ev[2], s), "event");
+  return OTPRG_OK;
+}
 
+int launch_finish(otprg_ctx* ctx) {
+  CK(otprg::launch_complete(ctx->ma.as<int32_t>(), ctx->mb.as<int32_t>(), ctx->ia, ctx->ib,
+                            ctx->fa.as<int32_t>(), ctx->fb.as<int32_t>(), ctx->stream),
+     "complete launch");
+  ctx->completed = true;
+  return OTPRG_OK;
+}
+
+// Device status words (Ctl::status; details in Ctl::err[], see report()).
+int check_status(otprg_ctx* ctx, const Ctl& h, bool need_done) {
+  if (h.status == 0) {
+    if (need_done && !h.done) return fail(ctx, OTPRG_DEVICE, "phase loop ended without termination");
+    return OTPRG_OK;
+  }
+  std::string d;
+  for (int i = 0; i < 6; ++i) d += (i ? "," : "") + std::to_string(h.err[i]);
+  switch (h.status) {
+    case 5:
+      return fail(ctx, OTPRG_INVARIANT,
+                  "phase count exceeded the proven bound; solver state is corrupt");
+    case 6: return fail(ctx, OTPRG_DEVICE, "device grid barrier timeout (block " + d + ")");
+    case 7: return fail(ctx, OTPRG_INVARIANT, "proposal conservation violated [phase,n,held,unmatched]=" + d);
+    case 8: return fail(ctx, OTPRG_INVARIANT, "scan missed an admissible edge [phase,b,start,a,x,target]=" + d);
+    case 9: return fail(ctx, OTPRG_INVARIANT, "scan returned an inadmissible edge [phase,b,start,a,k*1000+t,target]=" + d);
+    case 10: return fail(ctx, OTPRG_INVARIANT, "state inconsistent after phase [phase,list,free,bad_b]=" + d);
+    case 11: return fail(ctx, OTPRG_INVARIANT, "supply dual exceeded the device storage bound [phase,b,y]=" + d);
+    case 12: return fail(ctx, OTPRG_INVARIANT, "demand dual exceeded the device storage bound [phase,a,t]=" + d);
+    case 13: return fail(ctx, OTPRG_INVARIANT, "holder key from a later phase [phase,b,a,key_phase,key_b]=" + d);
+    default: return fail(ctx, h.status, "device solve failed [" + d + "]");
+  }
+}
+
+// Copies the current device state into the caller's result (caller
+// orientation for the matching; internal orientation for the duals).
+int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
+  const int ia = ctx->ia, ib = ctx->ib;
+  cudaStream_t s = ctx->stream;
+  Ctl h{};
   std::vector<int32_t> ma(ia), mb(ib), yb(ib);
   std::vector<uint8_t> tbytes(static_cast<size_t>(ia) * ctx->width);
   CK(cudaMemcpyAsync(&h, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s), "D2H ctl");
@@ -301,26 +341,13 @@ int do_solve(otprg_ctx* ctx, otprg_result* r) {
   CK(cudaMemcpyAsync(yb.data(), ctx->yb.p, ib * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
   CK(cudaMemcpyAsync(tbytes.data(), ctx->t.p, tbytes.size(), cudaMemcpyDeviceToHost, s), "D2H");
   CK(cudaStreamSynchronize(s), "solve");
-  if (h.status == 6) return fail(ctx, OTPRG_DEVICE, "device barrier timeout");
-  if (h.status == OTPRG_INVARIANT) {
-    if (h.err_a || h.err_b)
-      return fail(ctx, OTPRG_INVARIANT, "dual exceeded the device storage bound");
-    return fail(ctx, OTPRG_INVARIANT,
-                "phase count exceeded the proven bound; solver state is corrupt");
-  }
-  if (h.status) return fail(ctx, h.status, "device solve failed");
-  if (!h.done) return fail(ctx, OTPRG_DEVICE, "phase loop ended without termination");
-
+  if (hout) *hout = h;
   const int64_t phases = h.phase;
   if (r->free_counts && r->free_cap > 0 && phases > 0) {
     const int64_t nf = std::min<int64_t>(phases, r->free_cap);
     CK(cudaMemcpyAsync(r->free_counts, ctx->fc.p, nf * 8, cudaMemcpyDeviceToHost, s), "D2H");
     CK(cudaStreamSynchronize(s), "D2H free_counts");
   }
-  float ms_all = 0.f, ms_p1 = 0.f;
-  cudaEventElapsedTime(&ms_all, ctx->ev[0], ctx->ev[2]);
-  cudaEventElapsedTime(&ms_p1, ctx->ev[0], ctx->ev[1]);
-
   // Back to the caller's orientation (assignment.cpp:395-399).
   if (!ctx->swapped) {
     std::memcpy(r->match_of_a, ma.data(), ia * 4ull);
@@ -349,15 +376,35 @@ int do_solve(otprg_ctx* ctx, otprg_result* r) {
   }
   r->cost = total;
   r->build_ms = ctx->build_ms;
-  r->solve_ms = ms_all;
-  r->phase1_ms = ms_p1;
   r->bytes_touched = static_cast<int64_t>(h.bytes_touched);
   r->bytes_alg = h.sum_ni * static_cast<int64_t>(ia) * ctx->width;
   r->width = ctx->width;
-  r->gpu_launches = 4;  // init, loop (phase 1), loop (rest), complete
   return OTPRG_OK;
 }
 
+int do_solve(otprg_ctx* ctx, otprg_result* r) {
+  if (!r || !r->match_of_a || !r->match_of_b)
+    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
+  int st = do_begin(ctx);
+  if (st) return st;
+  cudaStream_t s = ctx->stream;
+  CK(cudaEventRecord(ctx->ev[0], s), "event");
+  if ((st = launch_loop(ctx, 1))) return st;  // phase 1 alone (full-width scan)
+  CK(cudaEventRecord(ctx->ev[1], s), "event");
+  if ((st = launch_loop(ctx, 0xffffffffu))) return st;
+  if ((st = launch_finish(ctx))) return st;
+  CK(cudaEventRecord(ctx->ev[2], s), "event");
+  Ctl h{};
+  if ((st = export_state(ctx, r, &h))) return st;
+  if ((st = check_status(ctx, h, true))) return st;
+  float ms_all = 0.f, ms_p1 = 0.f;
+  cudaEventElapsedTime(&ms_all, ctx->ev[0], ctx->ev[2]);
+  cudaEventElapsedTime(&ms_p1, ctx->ev[0], ctx->ev[1]);
+  r->solve_ms = ms_all;
+  r->phase1_ms = ms_p1;
+  r->gpu_launches = 4;  // init, loop (phase 1), loop (rest), complete
+  return OTPRG_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -461,6 +508,51 @@ int otprg_uniform_square_points(int32_t n, uint64_t seed, double* pts_a, double*
     pts_b[2 * static_cast<size_t>(i) + 1] = u01(rb);
   }
   return OTPRG_OK;
+}
+
+int otprg_begin(otprg_ctx* ctx) {
+  if (!ctx) return OTPRG_PARAMETER;
+  return do_begin(ctx);
+}
+
+int otprg_step(otprg_ctx* ctx, int64_t max_phases, int64_t* phases_done, int32_t* finished) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!ctx->begun || ctx->completed) return fail(ctx, OTPRG_PARAMETER, "otprg_begin() first");
+  const uint32_t cap = max_phases <= 0 || max_phases > 0xfffffffe ? 0xffffffffu
+                                                                  : static_cast<uint32_t>(max_phases);
+  int st = launch_loop(ctx, cap);
+  if (st) return st;
+  Ctl h{};
+  CK(cudaMemcpyAsync(&h, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream), "D2H ctl");
+  CK(cudaStreamSynchronize(ctx->stream), "step");
+  if ((st = check_status(ctx, h, false))) return st;
+  if (phases_done) *phases_done = h.phase;
+  if (finished) *finished = h.done;
+  return OTPRG_OK;
+}
+
+int otprg_snapshot(otprg_ctx* ctx, otprg_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!ctx->begun) return fail(ctx, OTPRG_PARAMETER, "otprg_begin() first");
+  if (!res || !res->match_of_a || !res->match_of_b)
+    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
+  Ctl h{};
+  int st = export_state(ctx, res, &h);
+  if (st) return st;
+  return check_status(ctx, h, false);
+}
+
+int otprg_finish(otprg_ctx* ctx, otprg_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!ctx->begun) return fail(ctx, OTPRG_PARAMETER, "otprg_begin() first");
+  if (!res || !res->match_of_a || !res->match_of_b)
+    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
+  int st = launch_loop(ctx, 0xffffffffu);  // run any remaining phases
+  if (st) return st;
+  if (!ctx->completed && (st = launch_finish(ctx))) return st;
+  Ctl h{};
+  if ((st = export_state(ctx, res, &h))) return st;
+  return check_status(ctx, h, true);
 }
 
 int otprg_flush_l2(otprg_ctx* ctx) {

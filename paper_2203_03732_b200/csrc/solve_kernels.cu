@@ -108,6 +108,7 @@ struct PhasePtrs {
   int32_t* mp_cur;    // a's first held this phase
   int* cnt_nxt;
   int* mp_cnt_cur;
+  int* exh_cur;
 };
 
 template <typename T, bool kSmem>
@@ -134,6 +135,17 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       a = warp_find_first<T, kSmem>(kT + (size_t)b * lda, tp, lda, start, target, fresh, mnw,
                                     lane, bytes);
       if (lane == 0) ++steps;
+#ifdef OTPRG_DEBUG_SCAN
+      if (lane == 0) {  // serial re-check of the warp scan
+        const T* row = kT + (size_t)b * lda;
+        const int hi = a < 0 ? lda : a;
+        for (int x = start; x < hi; ++x)
+          if ((uint32_t)row[x] + (uint32_t)tp[x] == target)
+            report(ctl, 8, (int)phase, b, start, a, x, (int)target);
+        if (a >= 0 && (uint32_t)row[a] + (uint32_t)tp[a] != target)
+          report(ctl, 9, (int)phase, b, start, a, (int)row[a] * 1000 + (int)tp[a], (int)target);
+      }
+#endif
     }
     if (a < 0) {
       // b stays free this phase: Y(b) += 1 (apply_phase :233-235).
@@ -141,13 +153,11 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       if (fresh && !skip) m = __reduce_min_sync(kFull, S::hmin(mnw));
       if (lane == 0) {
         if (fresh && !skip) rowmin[b] = (T)m;
-        if (yb + 1 > tmax) {
-          atomicCAS(&ctl->status, 0, 5);
-          ctl->err_b = b;
-        }
+        if (yb + 1 > tmax) report(ctl, 11, (int)phase, b, (int)yb);
         A.yb[b] = (int32_t)(yb + 1);
         const int pos = atomicAdd(P.cnt_nxt, 1);
         P.list_nxt[pos] = b;
+        atomicAdd(P.exh_cur, 1);
       }
       return;
     }
@@ -155,6 +165,10 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     unsigned long long old = 0;
     if (lane == 0) old = atomicMin(A.holder + a, key);
     old = __shfl_sync(kFull, old, 0);
+#ifdef OTPRG_DEBUG_SCAN
+    if (lane == 0 && (uint32_t)(old >> 32) < cur_tag)  // key from a later phase
+      report(ctl, 13, (int)phase, b, a, (int)~(uint32_t)(old >> 32), (int)(uint32_t)old);
+#endif
     if (old < key) {  // a is held by a lower b of this phase: next candidate
       start = a + 1;
       continue;
@@ -212,14 +226,13 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     }
     if (phase >= A.max_phase) break;
     if (phase + 1 > cap) {
-      if (leader) atomicCAS(&ctl->status, 0, 5);
+      if (leader) report(ctl, 5, (int)phase);
       break;
     }
     phase += 1;
     if (leader) {
       A.free_counts[phase - 1] = n;
       ctl->sum_ni += n;
-      ctl->phase = phase;
     }
     if constexpr (kSmem) {
       const uint4* src = reinterpret_cast<const uint4*>(tg);
@@ -237,6 +250,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     P.mp_cur = cur ? A.mp[1] : A.mp[0];
     P.cnt_nxt = &ctl->cnt[nxt];
     P.mp_cnt_cur = &ctl->mp_cnt[cur];
+    P.exh_cur = &ctl->exh[cur];
     while (true) {
       int i = 0;
       if (lane == 0) i = atomicAdd(&ctl->work[cur], 1);
@@ -248,12 +262,21 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     grid_barrier(ctl);
 
     // ---- A step: apply M' ----
+    const int m = ld_cg(&ctl->mp_cnt[cur]);
     if (leader) {
+      // Conservation: every proposer of B' either holds an a (M') or ended
+      // unmatched.  A violation means the chains lost or duplicated a b.
+      const int x = ld_cg(&ctl->exh[cur]);
+      if (x + m != n) report(ctl, 7, (int)phase, n, m, x);
+      // Published only after a grid barrier: every block reads ctl->phase
+      // once at launch, and a block may start late (cooperative launch only
+      // guarantees co-residency, not a common start).
+      ctl->phase = phase;
       ctl->work[nxt] = 0;
       ctl->cnt[cur] = 0;
       ctl->mp_cnt[nxt] = 0;
+      ctl->exh[nxt] = 0;
     }
-    const int m = ld_cg(&ctl->mp_cnt[cur]);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
       const int a = __ldcg(P.mp_cur + i);
       const unsigned long long key = __ldcg(A.holder + a);
@@ -267,13 +290,28 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       A.match_a[a] = b;
       A.match_b[b] = a;
       const uint32_t nt = (uint32_t)__ldcg(tg + a) + 1u;
-      if (nt > tmax) {
-        atomicCAS(&ctl->status, 0, 5);
-        ctl->err_a = a;
-      }
+      if (nt > tmax) report(ctl, 12, (int)phase, a, (int)nt);
       tg[a] = (T)nt;
     }
     grid_barrier(ctl);
+#ifdef OTPRG_DEBUG_SCAN
+    if (blockIdx.x == 0) {  // full state consistency after the phase
+      __shared__ int s_free, s_bad;
+      if (threadIdx.x == 0) s_free = 0, s_bad = -1;
+      __syncthreads();
+      for (int b = threadIdx.x; b < ctl->n_b; b += blockDim.x) {
+        const int a = __ldcg(A.match_b + b);
+        if (a == -1) atomicAdd(&s_free, 1);
+        else if (__ldcg(A.match_a + a) != b) atomicMax(&s_bad, b);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int nn = ld_cg(&ctl->cnt[nxt]);
+        if (s_free != nn || s_bad >= 0) report(ctl, 10, (int)phase, nn, s_free, s_bad);
+      }
+    }
+    grid_barrier(ctl);
+#endif
   }
   if (lane == 0 && (bytes | steps)) {
     atomicAdd(&ctl->bytes_touched, bytes);

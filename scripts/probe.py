@@ -4,10 +4,11 @@ import sys
 import time
 
 sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
 import numpy as np  # noqa: E402
 
 import paper_2203_03732_b200 as otprg  # noqa: E402
-from tests.golden_util import pins_of  # noqa: E402
+from golden_util import pins_of  # noqa: E402
 
 golden = json.load(open("tests/golden/assign_pins.json"))
 solver = otprg.Solver(0)
