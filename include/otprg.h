@@ -103,6 +103,8 @@ typedef struct otprg_result {
   double build_ms;        /* cost build/rounding kernels (CUDA events) */
   double solve_ms;        /* phase loop + completion kernels (CUDA events) */
   double phase1_ms;       /* the first phase alone (its own launch) */
+  double loop_ms;         /* phases 2.. (the second phase-loop launch) */
+  double solve_d2h_ms;    /* solve_ms + D2H of the results into pinned staging */
   int64_t bytes_touched;  /* cost-matrix bytes the scan kernels loaded */
   int64_t bytes_alg;      /* sum_i n_i * n_a * width (Lemma-5 schedule) */
   int32_t width;          /* bytes per rounded cost entry on the device */
@@ -160,6 +162,18 @@ int otprg_uniform_square_points(int32_t n, uint64_t seed, double* pts_a, double*
 
 /* Writes a buffer larger than L2 on the context's stream (benchmark hygiene). */
 int otprg_flush_l2(otprg_ctx* ctx);
+
+/* Device timeline (tracing): when enabled, every phase-loop phase records 8
+ * u64 (%globaltimer ns) — phase start, t staged, last/first block done with
+ * the proposal step (first stored as ~t), after barrier 1, last block done
+ * with apply, after barrier 2, n_i — for up to max_phases phases (0 = off).
+ * otprg_get_trace copies them out (max_phases * 8 u64). */
+int otprg_set_trace(otprg_ctx* ctx, int64_t max_phases);
+int otprg_get_trace(otprg_ctx* ctx, uint64_t* out, int64_t max_phases);
+
+/* CUDA-event timer on the context's stream: start, ..., stop -> elapsed ms. */
+int otprg_timer_start(otprg_ctx* ctx);
+int otprg_timer_stop(otprg_ctx* ctx, double* ms);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,7 @@ class Result(C.Structure):
         ("swapped", C.c_int32), ("full_match_termination", C.c_int32),
         ("cost", C.c_double),
         ("build_ms", C.c_double), ("solve_ms", C.c_double), ("phase1_ms", C.c_double),
+        ("loop_ms", C.c_double), ("solve_d2h_ms", C.c_double),
         ("bytes_touched", C.c_int64), ("bytes_alg", C.c_int64),
         ("width", C.c_int32), ("gpu_launches", C.c_int32),
     ]
@@ -51,7 +52,8 @@ EXPORTS = [
     "otprg_create", "otprg_destroy", "otprg_last_error", "otprg_version", "otprg_scaled_floor",
     "otprg_solve_assignment", "otprg_prepare", "otprg_solve_prepared", "otprg_scale_round_costs",
     "otprg_uniform_square_points", "otprg_flush_l2", "otprg_begin", "otprg_step",
-    "otprg_snapshot", "otprg_finish",
+    "otprg_snapshot", "otprg_finish", "otprg_timer_start", "otprg_timer_stop",
+    "otprg_set_trace", "otprg_get_trace",
 ]
 
 _lib = None
@@ -91,6 +93,10 @@ def lib() -> C.CDLL:
     L.otprg_step.argtypes = [vp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.otprg_snapshot.argtypes = [vp, C.POINTER(Result)]
     L.otprg_finish.argtypes = [vp, C.POINTER(Result)]
+    L.otprg_timer_start.argtypes = [vp]
+    L.otprg_timer_stop.argtypes = [vp, C.POINTER(C.c_double)]
+    L.otprg_set_trace.argtypes = [vp, C.c_int64]
+    L.otprg_get_trace.argtypes = [vp, vp, C.c_int64]
     _lib = L
     return L
 

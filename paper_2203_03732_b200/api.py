@@ -311,7 +311,8 @@ class Solver:
             sum_ni=int(r.sum_ni), duals_final=DualState(bufs["y_a"], bufs["y_b"]),
             swapped=bool(r.swapped), full_match_termination=bool(r.full_match_termination),
             device=dict(cost=r.cost, build_ms=r.build_ms, solve_ms=r.solve_ms,
-                        phase1_ms=r.phase1_ms, bytes_touched=int(r.bytes_touched),
+                        phase1_ms=r.phase1_ms, loop_ms=r.loop_ms, solve_d2h_ms=r.solve_d2h_ms,
+                        bytes_touched=int(r.bytes_touched),
                         bytes_alg=int(r.bytes_alg), width=int(r.width),
                         gpu_launches=int(r.gpu_launches)))
         return m, stats
@@ -330,6 +331,31 @@ class Solver:
         st = self._L.otprg_flush_l2(self._ctx)
         if st:
             self._raise(st)
+
+    def set_trace(self, max_phases: int) -> None:
+        st = self._L.otprg_set_trace(self._ctx, max_phases)
+        if st:
+            self._raise(st)
+
+    def get_trace(self, phases: int) -> np.ndarray:
+        """(phases, 8) uint64 device timeline; see include/otprg.h."""
+        out = np.zeros((phases, 8), np.uint64)
+        st = self._L.otprg_get_trace(self._ctx, out.ctypes.data, phases)
+        if st:
+            self._raise(st)
+        return out
+
+    def timer_start(self) -> None:
+        st = self._L.otprg_timer_start(self._ctx)
+        if st:
+            self._raise(st)
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        st = self._L.otprg_timer_stop(self._ctx, C.byref(ms))
+        if st:
+            self._raise(st)
+        return float(ms.value)
 
 
 _solvers: dict[int, Solver] = {}

@@ -72,9 +72,15 @@ __device__ __forceinline__ void report(Ctl* ctl, int code, int e0, int e1 = 0, i
 // Sense-by-generation grid barrier.  Requires all blocks co-resident
 // (cooperative launch).  A wait longer than 4 s flags status 6 and returns
 // instead of hanging the device.
-__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned long long* arrive_max = nullptr,
+                                             unsigned long long* arrive_min_inv = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (arrive_max) {  // timeline: when this block finished its work
+      const unsigned long long now = globaltimer();
+      atomicMax(arrive_max, now);
+      if (arrive_min_inv) atomicMax(arrive_min_inv, ~now);
+    }
     const unsigned nblocks = gridDim.x;
     const unsigned gen = ld_acquire(&ctl->bar_gen);
     __threadfence();

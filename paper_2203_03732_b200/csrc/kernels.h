@@ -24,6 +24,10 @@ struct SolveArgs {
   int64_t* free_counts;         // [phase_cap + 1]
   Ctl* ctl;
   uint32_t max_phase;           // run phases up to and including this one
+  // Optional device timeline (%globaltimer ns), kTraceSlots u64 per phase,
+  // indexed by phase - 1; nullptr disables tracing.
+  unsigned long long* trace;
+  uint32_t trace_cap;           // phases the trace buffer holds
 };
 
 // Rounding kernels (K1/K2): write kT in the internal orientation.

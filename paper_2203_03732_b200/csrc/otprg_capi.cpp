@@ -67,7 +67,7 @@ int64_t host_scaled_floor(double c, double eps) {
 struct otprg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   int num_sms = 0;
   std::string err;
 
@@ -87,10 +87,15 @@ struct otprg_ctx {
 
   DevBuf kT, t, yb, ma, mb, holder, rowmin, list0, list1, mp0, mp1, fc, ctl, fa, fb;
   DevBuf stage, pts, flush;
+  void* hpin = nullptr;  // pinned D2H staging
+  size_t hpin_n = 0;
+  cudaEvent_t timer[2] = {};
   int64_t fc_cap = 0;
   int loop_grid = 0;
   bool smem_t = true;
   bool begun = false, completed = false;
+  DevBuf trace;            // device timeline, 8 u64 per phase (see solve_kernels.cu)
+  uint32_t trace_cap = 0;  // 0 = tracing off
 };
 
 namespace {
@@ -261,6 +266,8 @@ otprg::SolveArgs make_args(otprg_ctx* ctx) {
   A.mp[1] = ctx->mp1.as<int32_t>();
   A.free_counts = ctx->fc.as<int64_t>();
   A.ctl = ctx->ctl.as<Ctl>();
+  A.trace = ctx->trace_cap ? ctx->trace.as<unsigned long long>() : nullptr;
+  A.trace_cap = ctx->trace_cap;
   return A;
 }
 
@@ -282,6 +289,8 @@ int do_begin(otprg_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream), "H2D ctl");
   CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->stream),
      "init launch");
+  if (ctx->trace_cap)
+    CK(cudaMemsetAsync(ctx->trace.p, 0, ctx->trace_cap * 64ull, ctx->stream), "trace reset");
   ctx->begun = true;
   ctx->completed = false;
   return OTPRG_OK;
@@ -332,34 +341,60 @@ int check_status(otprg_ctx* ctx, const Ctl& h, bool need_done) {
 int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
   const int ia = ctx->ia, ib = ctx->ib;
   cudaStream_t s = ctx->stream;
-  Ctl h{};
-  std::vector<int32_t> ma(ia), mb(ib), yb(ib);
-  std::vector<uint8_t> tbytes(static_cast<size_t>(ia) * ctx->width);
-  CK(cudaMemcpyAsync(&h, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s), "D2H ctl");
-  CK(cudaMemcpyAsync(ma.data(), ctx->ma.p, ia * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaMemcpyAsync(mb.data(), ctx->mb.p, ib * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaMemcpyAsync(yb.data(), ctx->yb.p, ib * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaMemcpyAsync(tbytes.data(), ctx->t.p, tbytes.size(), cudaMemcpyDeviceToHost, s), "D2H");
+  // One batch of async copies into pinned staging, one sync.
+  const size_t o_ma = 256, o_mb = o_ma + ia * 4ull, o_yb = o_mb + ib * 4ull,
+               o_t = o_yb + ib * 4ull, o_fc = (o_t + static_cast<size_t>(ia) * ctx->width + 7) & ~7ull;
+  const int64_t fc_first = std::min<int64_t>(
+      std::min<int64_t>(ctx->fc_cap, r->free_counts ? r->free_cap : 0), 65536);
+  const size_t need = o_fc + static_cast<size_t>(fc_first) * 8;
+  if (ctx->hpin_n < need) {
+    if (ctx->hpin) cudaFreeHost(ctx->hpin);
+    ctx->hpin = nullptr;
+    ctx->hpin_n = 0;
+    CK(cudaMallocHost(&ctx->hpin, need), "pinned staging");
+    ctx->hpin_n = need;
+  }
+  char* hp = static_cast<char*>(ctx->hpin);
+  CK(cudaMemcpyAsync(hp, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s), "D2H ctl");
+  CK(cudaMemcpyAsync(hp + o_ma, ctx->ma.p, ia * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(hp + o_mb, ctx->mb.p, ib * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(hp + o_yb, ctx->yb.p, ib * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(hp + o_t, ctx->t.p, static_cast<size_t>(ia) * ctx->width,
+                     cudaMemcpyDeviceToHost, s), "D2H");
+  if (fc_first > 0)
+    CK(cudaMemcpyAsync(hp + o_fc, ctx->fc.p, fc_first * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaEventRecord(ctx->ev[3], s), "event");
   CK(cudaStreamSynchronize(s), "solve");
+  Ctl h;
+  std::memcpy(&h, hp, sizeof(Ctl));
+  const int32_t* ma = reinterpret_cast<const int32_t*>(hp + o_ma);
+  const int32_t* mb = reinterpret_cast<const int32_t*>(hp + o_mb);
+  const int32_t* yb = reinterpret_cast<const int32_t*>(hp + o_yb);
+  const uint8_t* tbytes = reinterpret_cast<const uint8_t*>(hp + o_t);
   if (hout) *hout = h;
   const int64_t phases = h.phase;
   if (r->free_counts && r->free_cap > 0 && phases > 0) {
     const int64_t nf = std::min<int64_t>(phases, r->free_cap);
-    CK(cudaMemcpyAsync(r->free_counts, ctx->fc.p, nf * 8, cudaMemcpyDeviceToHost, s), "D2H");
-    CK(cudaStreamSynchronize(s), "D2H free_counts");
+    const int64_t n1 = std::min<int64_t>(nf, fc_first);
+    std::memcpy(r->free_counts, hp + o_fc, n1 * 8);
+    if (nf > n1) {
+      CK(cudaMemcpyAsync(r->free_counts + n1, ctx->fc.as<int64_t>() + n1, (nf - n1) * 8,
+                         cudaMemcpyDeviceToHost, s), "D2H");
+      CK(cudaStreamSynchronize(s), "D2H free_counts");
+    }
   }
   // Back to the caller's orientation (assignment.cpp:395-399).
   if (!ctx->swapped) {
-    std::memcpy(r->match_of_a, ma.data(), ia * 4ull);
-    std::memcpy(r->match_of_b, mb.data(), ib * 4ull);
+    std::memcpy(r->match_of_a, ma, ia * 4ull);
+    std::memcpy(r->match_of_b, mb, ib * 4ull);
   } else {
-    std::memcpy(r->match_of_a, mb.data(), ib * 4ull);
-    std::memcpy(r->match_of_b, ma.data(), ia * 4ull);
+    std::memcpy(r->match_of_a, mb, ib * 4ull);
+    std::memcpy(r->match_of_b, ma, ia * 4ull);
   }
   if (r->y_a) {
     for (int i = 0; i < ia; ++i) {
       const int64_t t = ctx->width == 1 ? tbytes[i]
-                                        : reinterpret_cast<const uint16_t*>(tbytes.data())[i];
+                                        : reinterpret_cast<const uint16_t*>(tbytes)[i];
       r->y_a[i] = -t;
     }
   }
@@ -392,16 +427,22 @@ int do_solve(otprg_ctx* ctx, otprg_result* r) {
   if ((st = launch_loop(ctx, 1))) return st;  // phase 1 alone (full-width scan)
   CK(cudaEventRecord(ctx->ev[1], s), "event");
   if ((st = launch_loop(ctx, 0xffffffffu))) return st;
+  CK(cudaEventRecord(ctx->ev[6], s), "event");
   if ((st = launch_finish(ctx))) return st;
   CK(cudaEventRecord(ctx->ev[2], s), "event");
   Ctl h{};
   if ((st = export_state(ctx, r, &h))) return st;
   if ((st = check_status(ctx, h, true))) return st;
-  float ms_all = 0.f, ms_p1 = 0.f;
+  float ms_all = 0.f, ms_p1 = 0.f, ms_d2h = 0.f;
   cudaEventElapsedTime(&ms_all, ctx->ev[0], ctx->ev[2]);
   cudaEventElapsedTime(&ms_p1, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&ms_d2h, ctx->ev[0], ctx->ev[3]);
+  float ms_loop = 0.f;
+  cudaEventElapsedTime(&ms_loop, ctx->ev[1], ctx->ev[6]);
+  r->loop_ms = ms_loop;
   r->solve_ms = ms_all;
   r->phase1_ms = ms_p1;
+  r->solve_d2h_ms = ms_d2h;
   r->gpu_launches = 4;  // init, loop (phase 1), loop (rest), complete
   return OTPRG_OK;
 }
@@ -426,6 +467,7 @@ int otprg_create(int device, otprg_ctx** out) {
     return OTPRG_DEVICE;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  for (auto& e : ctx->timer) cudaEventCreate(&e);
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   *out = ctx;
   return OTPRG_OK;
@@ -436,9 +478,11 @@ void otprg_destroy(otprg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->kT, &ctx->t, &ctx->yb, &ctx->ma, &ctx->mb, &ctx->holder, &ctx->rowmin,
                     &ctx->list0, &ctx->list1, &ctx->mp0, &ctx->mp1, &ctx->fc, &ctx->ctl, &ctx->fa,
-                    &ctx->fb, &ctx->stage, &ctx->pts, &ctx->flush})
+                    &ctx->fb, &ctx->stage, &ctx->pts, &ctx->flush, &ctx->trace})
     b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
+  for (auto& e : ctx->timer) cudaEventDestroy(e);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -553,6 +597,44 @@ int otprg_finish(otprg_ctx* ctx, otprg_result* res) {
   Ctl h{};
   if ((st = export_state(ctx, res, &h))) return st;
   return check_status(ctx, h, true);
+}
+
+int otprg_set_trace(otprg_ctx* ctx, int64_t max_phases) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (max_phases <= 0) {
+    ctx->trace_cap = 0;
+    return OTPRG_OK;
+  }
+  const uint32_t cap = static_cast<uint32_t>(std::min<int64_t>(max_phases, 1 << 22));
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  CK(ctx->trace.ensure(cap * 64ull), "alloc trace");
+  ctx->trace_cap = cap;
+  return OTPRG_OK;
+}
+
+int otprg_get_trace(otprg_ctx* ctx, uint64_t* out, int64_t max_phases) {
+  if (!ctx || !out) return OTPRG_PARAMETER;
+  if (!ctx->trace_cap) return fail(ctx, OTPRG_PARAMETER, "tracing is off");
+  const int64_t n = std::min<int64_t>(max_phases, ctx->trace_cap);
+  CK(cudaMemcpyAsync(out, ctx->trace.p, n * 64, cudaMemcpyDeviceToHost, ctx->stream), "D2H trace");
+  CK(cudaStreamSynchronize(ctx->stream), "trace");
+  return OTPRG_OK;
+}
+
+int otprg_timer_start(otprg_ctx* ctx) {
+  if (!ctx) return OTPRG_PARAMETER;
+  CK(cudaEventRecord(ctx->timer[0], ctx->stream), "timer");
+  return OTPRG_OK;
+}
+
+int otprg_timer_stop(otprg_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return OTPRG_PARAMETER;
+  CK(cudaEventRecord(ctx->timer[1], ctx->stream), "timer");
+  CK(cudaEventSynchronize(ctx->timer[1]), "timer");
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, ctx->timer[0], ctx->timer[1]), "timer");
+  *ms = f;
+  return OTPRG_OK;
 }
 
 int otprg_flush_l2(otprg_ctx* ctx) {

@@ -230,9 +230,15 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       break;
     }
     phase += 1;
+    // Timeline slots (ns): 0 phase start, 1 t staged, 2/3 last/first block
+    // done with P (3 stores ~t), 4 after barrier 1, 5 last block done with A,
+    // 6 after barrier 2, 7 n_i.
+    unsigned long long* tr =
+        (A.trace && phase <= A.trace_cap) ? A.trace + (size_t)(phase - 1) * 8 : nullptr;
     if (leader) {
       A.free_counts[phase - 1] = n;
       ctl->sum_ni += n;
+      if (tr) tr[0] = globaltimer(), tr[7] = (unsigned long long)n;
     }
     if constexpr (kSmem) {
       const uint4* src = reinterpret_cast<const uint4*>(tg);
@@ -241,6 +247,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = __ldcg(src + i);
       __syncthreads();
     }
+    if (tr && leader) tr[1] = globaltimer();
     const T* tp = kSmem ? s_t : tg;
 
     // ---- P step: proposal chains ----
@@ -259,7 +266,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       const int b = __ldcg(list_cur + i);
       run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps);
     }
-    grid_barrier(ctl);
+    grid_barrier(ctl, tr ? tr + 2 : nullptr, tr ? tr + 3 : nullptr);
+    if (tr && leader) tr[4] = globaltimer();
 
     // ---- A step: apply M' ----
     const int m = ld_cg(&ctl->mp_cnt[cur]);
@@ -293,7 +301,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       if (nt > tmax) report(ctl, 12, (int)phase, a, (int)nt);
       tg[a] = (T)nt;
     }
-    grid_barrier(ctl);
+    grid_barrier(ctl, tr ? tr + 5 : nullptr);
+    if (tr && leader) tr[6] = globaltimer();
 #ifdef OTPRG_DEBUG_SCAN
     if (blockIdx.x == 0) {  // full state consistency after the phase
       __shared__ int s_free, s_bad;

@@ -1,0 +1,12 @@
+"""Short command for ncu: three config-2 solves (seed 1) through the C ABI."""
+import sys
+sys.path.insert(0, ".")
+import paper_2203_03732_b200 as otprg  # noqa: E402
+
+storage = sys.argv[1] if len(sys.argv) > 1 else "u8"
+S = otprg.Solver(0)
+S.prepare(otprg.gen_uniform_square(10000, 1), 0.01, storage)
+for _ in range(3):
+    m, s = S.solve_prepared()
+print("phases", s.phases, "solve_ms", s.device["solve_ms"], "loop_ms", s.device["loop_ms"],
+      "phase1_ms", s.device["phase1_ms"])
