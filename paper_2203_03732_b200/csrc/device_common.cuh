@@ -18,24 +18,26 @@ struct Ctl {
   int32_t n_a, n_b, lda;
   int32_t thresh;       // floor(eps * min(n_a, n_b)) : stop when n_i <= thresh
   int32_t phase_cap;    // phase_bound(eps) + 8  (assignment.cpp:326)
-  uint32_t tmax;        // dual bound ceil(1/eps)+2 (core.hpp:95) in units
+  uint32_t tmax;        // storage bound on |Y| (type max - 2)
   // loop state
   uint32_t phase;       // phases executed so far
-  int32_t cnt[2];       // free-b list sizes (ping-pong)
-  int32_t mp_cnt[2];    // newly-held-a list sizes (ping-pong)
-  int32_t work[2];      // dynamic chain-grab counters (ping-pong)
-  int32_t status;       // 0 ok, else otprg_status
+  uint32_t applied;     // last phase whose M' is applied to the global state
+  int32_t cnt[3];       // free-b list sizes (rotating over phases)
+  int32_t mp_cnt[3];    // first-held-a list sizes (rotating)
+  int32_t work[3];      // dynamic proposer-grab counters (rotating)
+  int32_t exh[3];       // b's that ended their chain unmatched (rotating)
+  int32_t status;       // 0 ok, else otprg_status / device diagnostic code
   int32_t done;         // 1 once the termination test passed
   int32_t full_match;   // n_i == 0 at termination
   int32_t pad0;
   int64_t sum_ni;
   unsigned long long bytes_touched;
   unsigned long long chain_steps;
-  // grid barrier
+  unsigned long long list_walks;
+  // grid barrier (monotone arrival count)
   unsigned int bar_count;
-  unsigned int bar_gen;
-  int32_t exh[2];        // b's that ended their chain unmatched (conservation check)
-  int32_t err[8];        // details of the first failure (written by its reporter only)
+  unsigned int pad1;
+  int32_t err[8];       // details of the first failure (written by its reporter only)
 };
 
 #ifdef __CUDACC__
@@ -69,10 +71,14 @@ __device__ __forceinline__ void report(Ctl* ctl, int code, int e0, int e1 = 0, i
   }
 }
 
-// Sense-by-generation grid barrier.  Requires all blocks co-resident
-// (cooperative launch).  A wait longer than 4 s flags status 6 and returns
-// instead of hanging the device.
-__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned long long* arrive_max = nullptr,
+// Counting grid barrier.  ctl->bar_count only grows: the j-th barrier of a
+// solve completes when it reaches j * gridDim.x, so each block derives its
+// target from how many barriers it has passed (no reset, no last-arriver
+// step; arrivals are fire-and-forget release reductions).  Requires all
+// blocks co-resident (cooperative launch).  A wait longer than 4 s flags
+// status 6 and returns instead of hanging the device.
+__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned target,
+                                             unsigned long long* arrive_max = nullptr,
                                              unsigned long long* arrive_min_inv = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -81,17 +87,11 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned long long* arriv
       atomicMax(arrive_max, now);
       if (arrive_min_inv) atomicMax(arrive_min_inv, ~now);
     }
-    const unsigned nblocks = gridDim.x;
-    const unsigned gen = ld_acquire(&ctl->bar_gen);
     __threadfence();
-    const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(&ctl->bar_count, 0u);
-      __threadfence();
-      st_release(&ctl->bar_gen, gen + 1);
-    } else {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->bar_count) : "memory");
+    if ((int)(ld_acquire(&ctl->bar_count) - target) < 0) {
       const unsigned long long t0 = globaltimer();
-      while (ld_acquire(&ctl->bar_gen) == gen) {
+      while ((int)(ld_acquire(&ctl->bar_count) - target) < 0) {
         if (globaltimer() - t0 > 4000000000ull) {
           report(ctl, 6, (int)blockIdx.x);
           break;
@@ -117,6 +117,12 @@ struct Simd<uint8_t> {
   __device__ static uint32_t add(uint32_t k, uint32_t t) { return __vaddus4(k, t); }
   __device__ static uint32_t eq(uint32_t s, uint32_t tg) { return __vcmpeq4(s, tg); }
   __device__ static uint32_t mn(uint32_t a, uint32_t b) { return __vminu4(a, b); }
+  __device__ static uint32_t le(uint32_t s, uint32_t up) { return __vcmpleu4(s, up); }
+  // per-element all-ones mask -> one bit per element (element 0 = bit 0)
+  __device__ static uint32_t bits(uint32_t m) {
+    return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+  }
+  __device__ static uint32_t elem(uint32_t w, int i) { return (w >> (8 * i)) & 0xffu; }
   __device__ static uint32_t hmin(uint32_t w) {
     uint32_t m = min(w & 0xffu, (w >> 8) & 0xffu);
     return min(m, min((w >> 16) & 0xffu, w >> 24));
@@ -131,6 +137,9 @@ struct Simd<uint16_t> {
   __device__ static uint32_t add(uint32_t k, uint32_t t) { return __vaddus2(k, t); }
   __device__ static uint32_t eq(uint32_t s, uint32_t tg) { return __vcmpeq2(s, tg); }
   __device__ static uint32_t mn(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+  __device__ static uint32_t le(uint32_t s, uint32_t up) { return __vcmpleu2(s, up); }
+  __device__ static uint32_t bits(uint32_t m) { return ((m >> 15) & 1u) | ((m >> 30) & 2u); }
+  __device__ static uint32_t elem(uint32_t w, int i) { return (w >> (16 * i)) & 0xffffu; }
   __device__ static uint32_t hmin(uint32_t w) { return min(w & 0xffffu, w >> 16); }
 };
 

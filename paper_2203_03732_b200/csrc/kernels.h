@@ -8,24 +8,35 @@
 
 namespace otprg {
 
+// Low-set cache per supply vertex b (see solve_kernels.cu): the ascending
+// positions a < cov with k(a,b) + t(a) <= upto at the time of the scan that
+// built it, up to kLowCap entries, each packed as (k << 32) | a.
+constexpr int kLowCap = 16;
+constexpr int kLowLevels = 2;  // upto = target + kLowLevels when (re)built
+
 // Device state of one prepared assignment problem, in the solver's internal
 // orientation (n_a >= n_b; rows of kT are supply vertices b, contiguous over
-// demand vertices a).
+// demand vertices a).  Lists rotate over three phases (written in phase p,
+// consumed in p+1, reset in p+2).
 struct SolveArgs {
   const void* kT;               // T[n_b][lda], pad entries = type max
   void* t;                      // T[lda]  : t(a) = -Y(a) >= 0, pad = 0
   int32_t* yb;                  // [n_b]   : Y(b) >= 1
   int32_t* match_a;             // [n_a]
   int32_t* match_b;             // [n_b]
-  unsigned long long* holder;   // [n_a]   : DA holder keys (~phase << 32 | b)
+  // [n_a] x2 : DA holder keys (~phase << 32 | b); phase p proposes into
+  // holder[p & 1] while the top of phase p+1 still reads phase p's winners.
+  unsigned long long* holder[2];
   void* rowmin;                 // T[n_b]  : lower bound on min_a k(a,b)+t(a)
-  int32_t* list[2];             // [n_b]   : free-b lists (ping-pong)
-  int32_t* mp[2];               // [n_b]   : newly-held-a lists (ping-pong)
+  int4* lmeta;                  // [n_b]   : low set (upto, cov, cnt, -)
+  unsigned long long* lent;     // [n_b * kLowCap] low-set entries
+  int32_t* list[3];             // [n_b]   : free b's of the next phase
+  int2* mp[3];                  // [n_b]   : (a, previous partner) first held this phase
   int64_t* free_counts;         // [phase_cap + 1]
   Ctl* ctl;
   uint32_t max_phase;           // run phases up to and including this one
-  // Optional device timeline (%globaltimer ns), kTraceSlots u64 per phase,
-  // indexed by phase - 1; nullptr disables tracing.
+  // Optional device timeline (%globaltimer ns), 8 u64 per phase, indexed by
+  // phase - 1; nullptr disables tracing.
   unsigned long long* trace;
   uint32_t trace_cap;           // phases the trace buffer holds
 };

@@ -85,7 +85,7 @@ struct otprg_ctx {
   double build_ms = 0.0;
   int build_launches = 0;
 
-  DevBuf kT, t, yb, ma, mb, holder, rowmin, list0, list1, mp0, mp1, fc, ctl, fa, fb;
+  DevBuf kT, t, yb, ma, mb, holder, rowmin, lmeta, lent, lists, mps, fc, ctl, fa, fb;
   DevBuf stage, pts, flush;
   void* hpin = nullptr;  // pinned D2H staging
   size_t hpin_n = 0;
@@ -177,12 +177,12 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   CK(ctx->yb.ensure(ib * 4), "alloc yb");
   CK(ctx->ma.ensure(ia * 4), "alloc match_a");
   CK(ctx->mb.ensure(ib * 4), "alloc match_b");
-  CK(ctx->holder.ensure(ia * 8), "alloc holder");
+  CK(ctx->holder.ensure(2 * ia * 8), "alloc holder");
   CK(ctx->rowmin.ensure(ib * width), "alloc rowmin");
-  CK(ctx->list0.ensure(ib * 4), "alloc list");
-  CK(ctx->list1.ensure(ib * 4), "alloc list");
-  CK(ctx->mp0.ensure(ib * 4), "alloc mp");
-  CK(ctx->mp1.ensure(ib * 4), "alloc mp");
+  CK(ctx->lmeta.ensure(ib * 16), "alloc low-set meta");
+  CK(ctx->lent.ensure(ib * 8 * otprg::kLowCap), "alloc low-set entries");
+  CK(ctx->lists.ensure(3 * ib * 4), "alloc lists");
+  CK(ctx->mps.ensure(3 * ib * 8), "alloc mp lists");
   CK(ctx->fa.ensure(ia * 4), "alloc scratch");
   CK(ctx->fb.ensure(ib * 4), "alloc scratch");
   CK(ctx->ctl.ensure(sizeof(Ctl)), "alloc ctl");
@@ -258,12 +258,15 @@ otprg::SolveArgs make_args(otprg_ctx* ctx) {
   A.yb = ctx->yb.as<int32_t>();
   A.match_a = ctx->ma.as<int32_t>();
   A.match_b = ctx->mb.as<int32_t>();
-  A.holder = ctx->holder.as<unsigned long long>();
+  A.holder[0] = ctx->holder.as<unsigned long long>();
+  A.holder[1] = A.holder[0] + ctx->ia;
   A.rowmin = ctx->rowmin.p;
-  A.list[0] = ctx->list0.as<int32_t>();
-  A.list[1] = ctx->list1.as<int32_t>();
-  A.mp[0] = ctx->mp0.as<int32_t>();
-  A.mp[1] = ctx->mp1.as<int32_t>();
+  A.lmeta = ctx->lmeta.as<int4>();
+  A.lent = ctx->lent.as<unsigned long long>();
+  for (int r = 0; r < 3; ++r) {
+    A.list[r] = ctx->lists.as<int32_t>() + static_cast<size_t>(r) * ctx->ib;
+    A.mp[r] = ctx->mps.as<int2>() + static_cast<size_t>(r) * ctx->ib;
+  }
   A.free_counts = ctx->fc.as<int64_t>();
   A.ctl = ctx->ctl.as<Ctl>();
   A.trace = ctx->trace_cap ? ctx->trace.as<unsigned long long>() : nullptr;
@@ -284,7 +287,7 @@ int do_begin(otprg_ctx* ctx) {
   h.thresh = static_cast<int32_t>(std::floor(threshold));
   h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
   h.tmax = ctx->width == 1 ? 253u : 65533u;
-  h.cnt[1] = ctx->ib;
+  h.cnt[0] = ctx->ib;  // phase 1 reads list 0 (all b)
   const otprg::SolveArgs A = make_args(ctx);
   CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream), "H2D ctl");
   CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->stream),
@@ -477,7 +480,7 @@ void otprg_destroy(otprg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->kT, &ctx->t, &ctx->yb, &ctx->ma, &ctx->mb, &ctx->holder, &ctx->rowmin,
-                    &ctx->list0, &ctx->list1, &ctx->mp0, &ctx->mp1, &ctx->fc, &ctx->ctl, &ctx->fa,
+                    &ctx->lmeta, &ctx->lent, &ctx->lists, &ctx->mps, &ctx->fc, &ctx->ctl, &ctx->fa,
                     &ctx->fb, &ctx->stage, &ctx->pts, &ctx->flush, &ctx->trace})
     b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);

@@ -1,29 +1,43 @@
 // solve_kernels.cu — the device-resident phase loop of the push-relabel
 // assignment solver (reference: src/assignment.cpp:316-364), for sm_100a.
 //
-// One persistent cooperative kernel runs whole phases with no host sync.
-// Per phase (phase p, free supply set B'_p):
+// One persistent cooperative kernel runs whole phases with no host sync and
+// ONE grid barrier per phase.  Phase p (free supply set B'_p, target
+// Y(b) - 1 for each free b):
 //
-//   P step  (reference collect_workset/scan_plain :107-147,65-75 and the
-//            sequential greedy :161-171)
-//     Every warp repeatedly grabs a free b and runs a deferred-acceptance
-//     proposal chain: it scans kT[b][*] (contiguous over a) for the first
-//     admissible a >= start (k(a,b) + t(a) == Y(b) - 1, i.e.
-//     Y(a)+Y(b) == k+1) and proposes with one 64-bit atomicMin on holder[a]
-//     (key = ~phase << 32 | b: lower b wins, stale phases lose).  Rejected ->
-//     continue the same row after a.  Winning over a same-phase holder b2 ->
-//     the warp takes over b2's chain from a+1.  No admissible a left -> b is
-//     unmatched this phase: Y(b) += 1 and b goes to the next free list.
-//     Deferred acceptance with a common priority (lower b first) converges to
-//     the serial-dictatorship matching regardless of proposal order, which is
-//     exactly the reference's sequential greedy M'.
-//   A step  (apply_phase :210-235)
-//     For every a first held this phase: drop its old partner (which becomes
-//     free), link (a, holder b), Y(a) -= 1 (t(a) += 1).
+//  top    Every block applies M'_{p-1} to its shared-memory copy of
+//         t(a) = -Y(a) (Y(a) -= 1 for a matched in M', apply_phase :210-235);
+//         all threads together apply M'_{p-1} to the global matching
+//         (link, drop the displaced partner) and to global t.  Termination
+//         (:330-334: n_i <= floor(eps*m)) and the phase cap (:326,356-358)
+//         are tested here, after the apply, so the state is consistent at
+//         every exit.
+//  P      Proposal chains (collect_workset/scan_plain :107-147,65-75 and the
+//         sequential greedy :161-171).  Every warp takes a free b and runs a
+//         deferred-acceptance chain: find the first admissible a >= start
+//         (k(a,b) + t(a) == Y(b) - 1, i.e. Y(a)+Y(b) == k+1) and propose with
+//         one 64-bit atomicMin on holder[a] (key = ~phase << 32 | b: lower b
+//         wins, older phases lose).  Rejected -> next admissible a of the same
+//         row.  Winning over a same-phase holder b2 -> the warp continues
+//         b2's chain after a.  No admissible a left -> b stays free:
+//         Y(b) += 1 and b joins the next free list.  The first proposal that
+//         takes an a this phase also frees a's previous partner (it joins the
+//         next free list) and records (a, partner) for the next phase's top.
+//         Deferred acceptance with a common priority (lower b first) reaches
+//         the serial-dictatorship matching in any proposal order, which is
+//         the reference's sequential greedy M' exactly.
+//  barrier
 //
-// Two grid barriers per phase.  Termination (:330-334) compares the free
-// count with floor(eps * min(n_a, n_b)) at the top of the loop; the phase cap
-// (:326,356-358) sets status 5.
+// Finding admissible edges.  A warp streams the row kT[b][*] (B-major, 1 or
+// 2 bytes per entry) with 128-bit loads against t in shared memory, using
+// packed saturating SIMD sums.  Each scan from position 0 also records the
+// row's "low set": the ascending positions with k + t <= target + 2 (up to
+// kLowCap entries, with k).  Since t(a) only grows and Y(b) only grows, the
+// admissible set of b at any later target <= that bound is a subset of the
+// low set, so later phases verify a handful of cached entries against the
+// current t instead of rescanning the row; a row is rescanned only when the
+// bound expires or the cache was truncated.  rowmin[b] (min of k + t at the
+// last full scan) skips rows that cannot have admissible edges at all.
 #include <climits>
 #include <cstdio>
 
@@ -34,8 +48,13 @@ namespace otprg {
 
 namespace {
 
-constexpr int kBlock = 1024;
+constexpr int kBlock = 768;
 constexpr int kUnroll = 4;
+#ifdef OTPRG_DEBUG_SCAN
+constexpr unsigned kDebugBarriers = 1;
+#else
+constexpr unsigned kDebugBarriers = 0;
+#endif
 
 __device__ __forceinline__ uint4 ldg_nc(const uint4* p) { return __ldg(p); }
 
@@ -45,19 +64,33 @@ __device__ __forceinline__ uint4 load_t(const uint4* p) {
   else return __ldcg(p);
 }
 
+// Low-set construction state of the current scan (uniform across the warp).
+struct LowBuild {
+  bool on = false;
+  int cnt = 0;                        // entries stored so far
+  int full_pos = -1;                  // position of the kLowCap-th entry once full
+  uint32_t up_rep = 0;                // packed upper level
+  unsigned long long* ent = nullptr;  // &lent[b * kLowCap]
+};
+
+template <typename S>
+__device__ __forceinline__ uint32_t pick_word(int i, uint32_t w0, uint32_t w1, uint32_t w2,
+                                              uint32_t w3) {
+  const int q = i / S::kEpw;
+  return q < 2 ? (q == 0 ? w0 : w1) : (q == 2 ? w2 : w3);
+}
+
 // First admissible a >= start in one kT row, or -1.  The warp streams the
 // row in 32 lanes x 16 B x kUnroll chunks (coalesced 128-bit loads, 4 in
-// flight per lane).  When track_min, folds min_a (k+t) of every loaded entry
-// into mnw (packed per-element minima) for the lazy-skip bound.
+// flight per lane).  track_min folds min_a (k + t) into mnw; lb appends the
+// low-set entries at positions <= the returned hit.
 template <typename T, bool kSmem>
-__device__ __forceinline__ int warp_find_first(const T* __restrict__ row,
-                                               const T* tvec, int lda, int start,
-                                               uint32_t target, bool track_min,
-                                               uint32_t& mnw, int lane,
-                                               unsigned long long& bytes) {
+__device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tvec, int lda,
+                                         int start, uint32_t target, bool track_min,
+                                         uint32_t& mnw, LowBuild& lb, int lane,
+                                         unsigned long long& bytes) {
   using S = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
-  constexpr int kBits = 8 * sizeof(T);
   const uint32_t tg = S::rep(target);
   const uint4* rv = reinterpret_cast<const uint4*>(row);
   const uint4* tv = reinterpret_cast<const uint4*>(tvec);
@@ -78,63 +111,155 @@ __device__ __forceinline__ int warp_find_first(const T* __restrict__ row,
     if (lane == 0) bytes += 16ull * (unsigned long long)min(nv - v, 32 * kUnroll);
 #pragma unroll
     for (int j = 0; j < kUnroll; ++j) {
-      const int vi = v + j * 32 + lane;
-      const uint32_t kw[4] = {kr[j].x, kr[j].y, kr[j].z, kr[j].w};
-      const uint32_t tw[4] = {tr[j].x, tr[j].y, tr[j].z, tr[j].w};
-      int hit = INT_MAX;
-#pragma unroll
-      for (int w = 3; w >= 0; --w) {  // descending so the lowest word wins
-        const uint32_t s = S::add(kw[w], tw[w]);
-        uint32_t e = S::eq(s, tg);
-        if (track_min) mnw = S::mn(mnw, s);
-        const int e0 = vi * kEpv + w * S::kEpw;
-        if (e0 < start) {
-          const int drop = start - e0;
-          e = drop >= S::kEpw ? 0u : (e & (~0u << (drop * kBits)));
-        }
-        if (e) hit = e0 + (__ffs(e) - 1) / kBits;
+      const int e0 = (v + j * 32 + lane) * kEpv;
+      const uint32_t k0 = kr[j].x, k1 = kr[j].y, k2 = kr[j].z, k3 = kr[j].w;
+      const uint32_t s0 = S::add(k0, tr[j].x), s1 = S::add(k1, tr[j].y);
+      const uint32_t s2 = S::add(k2, tr[j].z), s3 = S::add(k3, tr[j].w);
+      uint32_t eqb = S::bits(S::eq(s0, tg)) | (S::bits(S::eq(s1, tg)) << S::kEpw) |
+                     (S::bits(S::eq(s2, tg)) << (2 * S::kEpw)) |
+                     (S::bits(S::eq(s3, tg)) << (3 * S::kEpw));
+      if (track_min) mnw = S::mn(S::mn(mnw, S::mn(s0, s1)), S::mn(s2, s3));
+      uint32_t keep = ~0u;
+      if (e0 < start) {
+        const int drop = start - e0;
+        keep = drop >= kEpv ? 0u : (~0u << drop);
+        eqb &= keep;
       }
-      const unsigned bal = __ballot_sync(kFull, hit != INT_MAX);
-      if (bal) return __shfl_sync(kFull, hit, __ffs(bal) - 1);
+      const unsigned hb = __ballot_sync(kFull, eqb != 0);
+      int hit = INT_MAX;
+      if (hb) hit = __shfl_sync(kFull, e0 + __ffs(eqb) - 1, __ffs(hb) - 1);
+      if (lb.on) {
+        uint32_t leb = (S::bits(S::le(s0, lb.up_rep)) | (S::bits(S::le(s1, lb.up_rep)) << S::kEpw) |
+                        (S::bits(S::le(s2, lb.up_rep)) << (2 * S::kEpw)) |
+                        (S::bits(S::le(s3, lb.up_rep)) << (3 * S::kEpw))) & keep;
+        if (hit != INT_MAX) {  // entries up to and including the hit only
+          const int lim = hit - e0;
+          leb = lim < 0 ? 0u : (lim >= kEpv - 1 ? leb : (leb & ((2u << lim) - 1u)));
+        }
+        if (__ballot_sync(kFull, leb != 0)) {
+          const int c = __popc(leb);
+          int inc = c;  // inclusive warp scan of the per-lane counts
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += y;
+          }
+          const int tot = __shfl_sync(kFull, inc, 31);
+          int idx = lb.cnt + inc - c;
+          const int first_idx = idx;
+          uint32_t bm = leb;
+          int fp = -1;
+          while (bm) {
+            const int i = __ffs(bm) - 1;
+            bm &= bm - 1;
+            if (idx < kLowCap) {
+              const uint32_t kv = S::elem(pick_word<S>(i, k0, k1, k2, k3), i % S::kEpw);
+              lb.ent[idx] = ((unsigned long long)kv << 32) | (uint32_t)(e0 + i);
+              if (idx == kLowCap - 1) fp = e0 + i;
+            }
+            ++idx;
+          }
+          if (lb.cnt + tot >= kLowCap) {  // full: coverage ends at the last stored entry
+            const unsigned src = __ballot_sync(kFull, first_idx <= kLowCap - 1 &&
+                                                          kLowCap - 1 < first_idx + c);
+            lb.full_pos = __shfl_sync(kFull, fp, __ffs(src) - 1);
+            lb.cnt = kLowCap;
+            lb.on = false;
+          } else {
+            lb.cnt += tot;
+          }
+        }
+      }
+      if (hit != INT_MAX) return hit;
     }
   }
   return -1;
 }
 
-// Per-phase pointers (selected once so no parameter array is indexed
+// Per-phase list pointers (selected once so no parameter array is indexed
 // dynamically, which would spill the kernel parameters to local memory).
 struct PhasePtrs {
-  int32_t* list_nxt;  // free-b list of the next phase
-  int32_t* mp_cur;    // a's first held this phase
-  int* cnt_nxt;
-  int* mp_cnt_cur;
-  int* exh_cur;
+  int32_t* list_out;  // free b's of the next phase
+  int2* mp_out;       // (a, previous partner) first held this phase
+  int* cnt_out;
+  int* mp_cnt_out;
+  int* exh_out;
 };
 
 template <typename T, bool kSmem>
 __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const PhasePtrs& P,
                                           const T* tp, int lda, uint32_t phase, uint32_t tmax,
                                           int lane, unsigned long long& bytes,
-                                          unsigned long long& steps) {
+                                          unsigned long long& steps, unsigned long long& walks) {
   using S = Simd<T>;
   Ctl* ctl = A.ctl;
   const T* kT = static_cast<const T*>(A.kT);
   T* rowmin = static_cast<T*>(A.rowmin);
+  const uint32_t cur_tag = ~phase;
+  const uint32_t prev_tag = ~(phase - 1);
+  unsigned long long* H = (phase & 1) ? A.holder[1] : A.holder[0];             // this phase
+  const unsigned long long* Hprev = (phase & 1) ? A.holder[0] : A.holder[1];   // phase - 1
+
   uint32_t yb = (uint32_t)__ldcg(A.yb + b);
   uint32_t target = yb - 1;
   int start = 0;
-  bool fresh = true;
+  bool fresh = true;  // b came from the free list (owns its low-set cache)
   uint32_t mnw = 0xffffffffu;
-  const uint32_t cur_tag = ~phase;
-  // Lazy skip: the bound only grows (t only grows), so an empty row stays
-  // empty while target < bound.
-  bool skip = (uint32_t)__ldcg(rowmin + b) > target;
+  bool track_min = false, dirty = false;
+  LowBuild lb;
+  // low-set cache of b
+  int4 meta = __ldcg(A.lmeta + b);  // (upto, cov, cnt, -)
+  unsigned long long ent = 0;
+  if (lane < kLowCap) ent = __ldcg(A.lent + (size_t)b * kLowCap + lane);
+  bool walk = meta.y > 0 && target <= (uint32_t)meta.x;
+  bool skip = false;
+  if (!walk) {
+    if ((uint32_t)__ldcg(rowmin + b) > target) {
+      skip = true;  // row min too high: no admissible edge (min only grows)
+    } else {       // (re)build the low set with a full scan from position 0
+      meta = make_int4((int)(target + kLowLevels), 0, 0, 0);
+      lb.on = true;
+      lb.cnt = 0;
+      lb.up_rep = S::rep(target + kLowLevels);
+      lb.ent = A.lent + (size_t)b * kLowCap;
+      track_min = true;
+      dirty = true;
+    }
+  }
+  bool scanning = !walk && !skip;
+
   while (true) {
     int a = -1;
-    if (!skip) {
-      a = warp_find_first<T, kSmem>(kT + (size_t)b * lda, tp, lda, start, target, fresh, mnw,
-                                    lane, bytes);
+    if (walk) {
+      const int pos = (int)(uint32_t)ent;
+      const uint32_t kv = (uint32_t)(ent >> 32);
+      const bool ok = lane < meta.z && pos >= start && kv + (uint32_t)tp[pos] == target;
+      const unsigned bal = __ballot_sync(kFull, ok);
+      if (lane == 0) ++walks;
+      if (bal) {
+        a = __shfl_sync(kFull, pos, __ffs(bal) - 1);
+      } else if (meta.y < lda) {  // cache covers [0, cov) only: scan the rest
+        walk = false;
+        scanning = true;
+        start = max(start, meta.y);
+        if (meta.z < kLowCap && start == meta.y) {  // extend the cache
+          lb.on = true;
+          lb.cnt = meta.z;
+          lb.up_rep = S::rep((uint32_t)meta.x);
+          lb.ent = A.lent + (size_t)b * kLowCap;
+          dirty = true;
+        }
+      }
+    }
+    if (scanning) {
+      a = warp_scan<T, kSmem>(kT + (size_t)b * lda, tp, lda, start, target, track_min, mnw, lb,
+                              lane, bytes);
       if (lane == 0) ++steps;
+      if (dirty) {
+        meta.z = lb.cnt;
+        meta.y = lb.full_pos >= 0 ? lb.full_pos + 1 : (a >= 0 ? a + 1 : lda);
+        if (lb.full_pos >= 0) lb.on = false;
+      }
 #ifdef OTPRG_DEBUG_SCAN
       if (lane == 0) {  // serial re-check of the warp scan
         const T* row = kT + (size_t)b * lda;
@@ -150,41 +275,60 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     if (a < 0) {
       // b stays free this phase: Y(b) += 1 (apply_phase :233-235).
       uint32_t m = 0;
-      if (fresh && !skip) m = __reduce_min_sync(kFull, S::hmin(mnw));
+      if (track_min) m = __reduce_min_sync(kFull, S::hmin(mnw));
       if (lane == 0) {
-        if (fresh && !skip) rowmin[b] = (T)m;
+        if (track_min) rowmin[b] = (T)m;
+        if (fresh && dirty) A.lmeta[b] = meta;
         if (yb + 1 > tmax) report(ctl, 11, (int)phase, b, (int)yb);
         A.yb[b] = (int32_t)(yb + 1);
-        const int pos = atomicAdd(P.cnt_nxt, 1);
-        P.list_nxt[pos] = b;
-        atomicAdd(P.exh_cur, 1);
+        const int pos = atomicAdd(P.cnt_out, 1);
+        P.list_out[pos] = b;
+        atomicAdd(P.exh_out, 1);
       }
       return;
     }
     const unsigned long long key = ((unsigned long long)cur_tag << 32) | (uint32_t)b;
     unsigned long long old = 0;
-    if (lane == 0) old = atomicMin(A.holder + a, key);
+    if (lane == 0) old = atomicMin(H + a, key);
     old = __shfl_sync(kFull, old, 0);
+    const uint32_t old_tag = (uint32_t)(old >> 32);
 #ifdef OTPRG_DEBUG_SCAN
-    if (lane == 0 && (uint32_t)(old >> 32) < cur_tag)  // key from a later phase
-      report(ctl, 13, (int)phase, b, a, (int)~(uint32_t)(old >> 32), (int)(uint32_t)old);
+    if (lane == 0 && old_tag < cur_tag)  // key from a later phase
+      report(ctl, 13, (int)phase, b, a, (int)~old_tag, (int)(uint32_t)old);
 #endif
     if (old < key) {  // a is held by a lower b of this phase: next candidate
       start = a + 1;
       continue;
     }
-    if ((uint32_t)(old >> 32) == cur_tag) {  // displaced b2 continues after a
+    if (lane == 0 && fresh && dirty) A.lmeta[b] = meta;
+    if (old_tag == cur_tag) {  // displaced b2 continues after a (plain scan)
       b = (int)(uint32_t)old;
       yb = (uint32_t)__ldcg(A.yb + b);
       target = yb - 1;
       start = a + 1;
       fresh = false;
-      skip = false;
+      walk = false;
+      scanning = true;
+      track_min = false;
+      dirty = false;
+      lb.on = false;
       continue;
     }
-    if (lane == 0) {  // a newly held this phase
-      const int pos = atomicAdd(P.mp_cnt_cur, 1);
-      P.mp_cur[pos] = a;
+    if (lane == 0) {
+      // a is taken for the first time this phase: its partner before this
+      // phase is displaced (it is freed by apply_phase).  If a was matched in
+      // the previous phase, that partner is the previous phase's winner (the
+      // global matching is being updated concurrently at this phase's top);
+      // otherwise match_a, which is complete for all earlier phases.
+      const unsigned long long hp = __ldcg(Hprev + a);
+      const int ma = __ldcg(A.match_a + a);
+      const int partner = (uint32_t)(hp >> 32) == prev_tag ? (int)(uint32_t)hp : ma;
+      if (partner >= 0) {
+        const int pos = atomicAdd(P.cnt_out, 1);
+        P.list_out[pos] = partner;
+      }
+      const int pos = atomicAdd(P.mp_cnt_out, 1);
+      P.mp_out[pos] = make_int2(a, partner);
     }
     return;
   }
@@ -199,22 +343,80 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   const int thresh = ctl->thresh;
   const uint32_t cap = (uint32_t)ctl->phase_cap;
   const uint32_t tmax = ctl->tmax;
+  // Read once at launch; ctl->phase / ctl->applied are only written after
+  // this launch's first grid barrier, so late-starting blocks read the same.
   uint32_t phase = ld_cg(reinterpret_cast<const unsigned*>(&ctl->phase));
+  const uint32_t applied0 = ld_cg(reinterpret_cast<const unsigned*>(&ctl->applied));
   const int lane = threadIdx.x & 31;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  unsigned long long bytes = 0, steps = 0;
+  unsigned long long bytes = 0, steps = 0, walks = 0;
   T* tg = static_cast<T*>(A.t);
+  // Barrier targets: every executed phase passes exactly kBarriers grid
+  // barriers, so the arrival count after `phase` phases is known locally.
+  constexpr unsigned kBarriers = 1 + (kSmem ? 0u : 1u) + kDebugBarriers;
+  unsigned bar_target = phase * kBarriers * gridDim.x;
+  const int warps_per_block = blockDim.x >> 5;
+  const int total_warps = gridDim.x * warps_per_block;
+  // static proposer slot, striped across blocks so small phases spread over
+  // all SMs (slot i -> block i % grid, warp i / grid)
+  const int gwarp = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gthreads = gridDim.x * blockDim.x;
 
-  __shared__ int s_ctl[2];
+  if constexpr (kSmem) {  // global t is complete at launch (previous launch applied its M')
+    const uint4* src = reinterpret_cast<const uint4*>(tg);
+    uint4* dst = reinterpret_cast<uint4*>(s_t);
+    const int nvec = lda * (int)sizeof(T) / 16;
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = __ldcg(src + i);
+  }
+  __shared__ int s_ctl[4];
+  bool first = true;
+  int n_prev = -1;
   while (true) {
-    const int cur = (phase + 1) & 1, nxt = cur ^ 1;
-    // one read per block, broadcast: every thread must take the same branch
-    if (threadIdx.x == 0) {
+    const int r_prev = phase % 3, r_cur = (phase + 1) % 3, r_nxt = (phase + 2) % 3;
+    // apply M'_{phase} unless the previous launch already did
+    const bool apply = phase > 0 && !(first && applied0 == phase);
+    if (threadIdx.x == 0) {  // one read per block, broadcast: uniform branches
       s_ctl[0] = ld_cg(&ctl->status);
-      s_ctl[1] = ld_cg(&ctl->cnt[cur]);
+      s_ctl[1] = ld_cg(&ctl->cnt[r_prev]);
+      s_ctl[2] = apply ? ld_cg(&ctl->mp_cnt[r_prev]) : 0;
+      s_ctl[3] = ld_cg(&ctl->exh[r_prev]);
     }
     __syncthreads();
-    const int status = s_ctl[0], n = s_ctl[1];
+    const int status = s_ctl[0], n = s_ctl[1], m_prev = s_ctl[2], x_prev = s_ctl[3];
+    __syncthreads();
+    if (leader && !first) {
+      ctl->phase = phase;  // published only after a grid barrier of this launch
+      // conservation: every proposer of B' either holds an a or ended free
+      if (x_prev + m_prev != n_prev) report(ctl, 7, (int)phase, n_prev, m_prev, x_prev);
+    }
+    first = false;
+
+    // ---- apply M'_{phase}: shared t (every block) and the global state ----
+    const int2* mp_prev = A.mp[0];
+    if (r_prev == 1) mp_prev = A.mp[1];
+    if (r_prev == 2) mp_prev = A.mp[2];
+    const unsigned long long* Hq = (phase & 1) ? A.holder[1] : A.holder[0];  // phase's winners
+    if (m_prev > 0) {
+      if constexpr (kSmem) {
+        for (int i = threadIdx.x; i < m_prev; i += blockDim.x) {
+          const int a = __ldcg(&mp_prev[i].x);
+          s_t[a] = (T)(s_t[a] + 1);  // each a appears once
+        }
+      }
+      for (int i = gtid; i < m_prev; i += gthreads) {
+        const int2 e = __ldcg(mp_prev + i);
+        const int a = e.x, old_b = e.y;
+        const int b = (int)(uint32_t)__ldcg(Hq + a);
+        if (old_b >= 0) A.match_b[old_b] = -1;
+        A.match_a[a] = b;
+        A.match_b[b] = a;
+        const uint32_t nt = (uint32_t)__ldcg(tg + a) + 1u;
+        if (nt > tmax) report(ctl, 12, (int)phase, a, (int)nt);
+        tg[a] = (T)nt;
+      }
+      if (leader) ctl->applied = phase;
+    }
     __syncthreads();
     if (status != 0) break;
     if (n <= thresh) {  // (double)n_i <= eps*m  <=>  n_i <= floor(eps*m)
@@ -230,81 +432,17 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       break;
     }
     phase += 1;
-    // Timeline slots (ns): 0 phase start, 1 t staged, 2/3 last/first block
-    // done with P (3 stores ~t), 4 after barrier 1, 5 last block done with A,
-    // 6 after barrier 2, 7 n_i.
-    unsigned long long* tr =
-        (A.trace && phase <= A.trace_cap) ? A.trace + (size_t)(phase - 1) * 8 : nullptr;
-    if (leader) {
-      A.free_counts[phase - 1] = n;
-      ctl->sum_ni += n;
-      if (tr) tr[0] = globaltimer(), tr[7] = (unsigned long long)n;
+    n_prev = n;
+    // Barriers only in iterations that run a phase, so every executed phase
+    // passes exactly kBarriers of them (bar_target is derived from that).
+    if constexpr (!kSmem) {  // P reads global t: the apply must be complete
+      bar_target += gridDim.x;
+      grid_barrier(ctl, bar_target);
     }
-    if constexpr (kSmem) {
-      const uint4* src = reinterpret_cast<const uint4*>(tg);
-      uint4* dst = reinterpret_cast<uint4*>(s_t);
-      const int nvec = lda * (int)sizeof(T) / 16;
-      for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = __ldcg(src + i);
-      __syncthreads();
-    }
-    if (tr && leader) tr[1] = globaltimer();
-    const T* tp = kSmem ? s_t : tg;
-
-    // ---- P step: proposal chains ----
-    const int32_t* list_cur = cur ? A.list[1] : A.list[0];
-    PhasePtrs P;
-    P.list_nxt = cur ? A.list[0] : A.list[1];
-    P.mp_cur = cur ? A.mp[1] : A.mp[0];
-    P.cnt_nxt = &ctl->cnt[nxt];
-    P.mp_cnt_cur = &ctl->mp_cnt[cur];
-    P.exh_cur = &ctl->exh[cur];
-    while (true) {
-      int i = 0;
-      if (lane == 0) i = atomicAdd(&ctl->work[cur], 1);
-      i = __shfl_sync(kFull, i, 0);
-      if (i >= n) break;
-      const int b = __ldcg(list_cur + i);
-      run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps);
-    }
-    grid_barrier(ctl, tr ? tr + 2 : nullptr, tr ? tr + 3 : nullptr);
-    if (tr && leader) tr[4] = globaltimer();
-
-    // ---- A step: apply M' ----
-    const int m = ld_cg(&ctl->mp_cnt[cur]);
-    if (leader) {
-      // Conservation: every proposer of B' either holds an a (M') or ended
-      // unmatched.  A violation means the chains lost or duplicated a b.
-      const int x = ld_cg(&ctl->exh[cur]);
-      if (x + m != n) report(ctl, 7, (int)phase, n, m, x);
-      // Published only after a grid barrier: every block reads ctl->phase
-      // once at launch, and a block may start late (cooperative launch only
-      // guarantees co-residency, not a common start).
-      ctl->phase = phase;
-      ctl->work[nxt] = 0;
-      ctl->cnt[cur] = 0;
-      ctl->mp_cnt[nxt] = 0;
-      ctl->exh[nxt] = 0;
-    }
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-      const int a = __ldcg(P.mp_cur + i);
-      const unsigned long long key = __ldcg(A.holder + a);
-      const int b = (int)(uint32_t)key;
-      const int old_b = __ldcg(A.match_a + a);
-      if (old_b >= 0) {
-        A.match_b[old_b] = -1;
-        const int pos = atomicAdd(P.cnt_nxt, 1);
-        P.list_nxt[pos] = old_b;
-      }
-      A.match_a[a] = b;
-      A.match_b[b] = a;
-      const uint32_t nt = (uint32_t)__ldcg(tg + a) + 1u;
-      if (nt > tmax) report(ctl, 12, (int)phase, a, (int)nt);
-      tg[a] = (T)nt;
-    }
-    grid_barrier(ctl, tr ? tr + 5 : nullptr);
-    if (tr && leader) tr[6] = globaltimer();
 #ifdef OTPRG_DEBUG_SCAN
-    if (blockIdx.x == 0) {  // full state consistency after the phase
+    bar_target += gridDim.x;
+    grid_barrier(ctl, bar_target);
+    if (blockIdx.x == 0 && phase > 0) {  // full state consistency before the phase
       __shared__ int s_free, s_bad;
       if (threadIdx.x == 0) s_free = 0, s_bad = -1;
       __syncthreads();
@@ -314,17 +452,52 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
         else if (__ldcg(A.match_a + a) != b) atomicMax(&s_bad, b);
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        const int nn = ld_cg(&ctl->cnt[nxt]);
-        if (s_free != nn || s_bad >= 0) report(ctl, 10, (int)phase, nn, s_free, s_bad);
-      }
+      if (threadIdx.x == 0 && (s_free != n || s_bad >= 0))
+        report(ctl, 10, (int)phase, n, s_free, s_bad);
+      __syncthreads();
     }
-    grid_barrier(ctl);
 #endif
+    // Timeline slots (ns): 0 phase start, 1 apply done (block 0), 2/3 last /
+    // first block done with P (3 stores ~t), 4 after the barrier, 7 n_i.
+    unsigned long long* tr =
+        (A.trace && phase <= A.trace_cap) ? A.trace + (size_t)(phase - 1) * 8 : nullptr;
+    if (leader) {
+      A.free_counts[phase - 1] = n;
+      ctl->sum_ni += n;
+      ctl->cnt[r_nxt] = 0;  // r_nxt was last read at the top of phase - 1
+      ctl->mp_cnt[r_nxt] = 0;
+      ctl->work[r_nxt] = 0;
+      ctl->exh[r_nxt] = 0;
+      if (tr) tr[0] = globaltimer(), tr[7] = (unsigned long long)n;
+    }
+    const T* tp = kSmem ? s_t : tg;
+    if (tr && leader) tr[1] = globaltimer();
+
+    // ---- P step: proposal chains over the free list of phase `phase` ----
+    const int32_t* list_in = r_prev == 0 ? A.list[0] : (r_prev == 1 ? A.list[1] : A.list[2]);
+    PhasePtrs P;
+    P.list_out = r_cur == 0 ? A.list[0] : (r_cur == 1 ? A.list[1] : A.list[2]);
+    P.mp_out = r_cur == 0 ? A.mp[0] : (r_cur == 1 ? A.mp[1] : A.mp[2]);
+    P.cnt_out = &ctl->cnt[r_cur];
+    P.mp_cnt_out = &ctl->mp_cnt[r_cur];
+    P.exh_out = &ctl->exh[r_cur];
+    // First proposer of every warp is static (no contended grab when
+    // n_i <= #warps); the rest are grabbed from a counter.
+    int i = gwarp;
+    while (i < n) {
+      const int b = __ldcg(list_in + i);
+      run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks);
+      if (lane == 0) i = total_warps + atomicAdd(&ctl->work[r_cur], 1);
+      i = __shfl_sync(kFull, i, 0);
+    }
+    bar_target += gridDim.x;
+    grid_barrier(ctl, bar_target, tr ? tr + 2 : nullptr, tr ? tr + 3 : nullptr);
+    if (tr && leader) tr[4] = globaltimer();
   }
-  if (lane == 0 && (bytes | steps)) {
+  if (lane == 0 && (bytes | steps | walks)) {
     atomicAdd(&ctl->bytes_touched, bytes);
     atomicAdd(&ctl->chain_steps, steps);
+    atomicAdd(&ctl->list_walks, walks);
   }
 }
 
@@ -337,13 +510,15 @@ __global__ void init_state_kernel(SolveArgs A, int n_a, int n_b, int lda) {
     t[i] = 0;
     if (i < n_a) {
       A.match_a[i] = -1;
-      A.holder[i] = ~0ull;
+      A.holder[0][i] = ~0ull;
+      A.holder[1][i] = ~0ull;
     }
     if (i < n_b) {
       A.match_b[i] = -1;
       A.yb[i] = 1;  // init_state: Y(b) = 1, Y(a) = 0 (assignment.cpp:54-60)
       rowmin[i] = 0;
-      A.list[1][i] = i;  // phase 1 proposes every b
+      A.lmeta[i] = make_int4(0, 0, 0, 0);
+      A.list[0][i] = i;  // phase 1 proposes every b
     }
   }
 }
