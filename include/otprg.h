@@ -109,6 +109,10 @@ typedef struct otprg_result {
   int64_t bytes_alg;      /* sum_i n_i * n_a * width (Lemma-5 schedule) */
   int32_t width;          /* bytes per rounded cost entry on the device */
   int32_t gpu_launches;   /* kernels launched by this call */
+  /* proposal-chain statistics: fresh chains, takeovers, proposals from the
+   * low-set cache, exhaustions by a complete cache, scans past the cache,
+   * full rescans, rowmin skips, proposals (atomicMin) */
+  int64_t chain_stats[8];
 } otprg_result;
 
 typedef struct otprg_ctx otprg_ctx;

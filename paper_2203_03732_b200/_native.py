@@ -45,6 +45,7 @@ class Result(C.Structure):
         ("loop_ms", C.c_double), ("solve_d2h_ms", C.c_double),
         ("bytes_touched", C.c_int64), ("bytes_alg", C.c_int64),
         ("width", C.c_int32), ("gpu_launches", C.c_int32),
+        ("chain_stats", C.c_int64 * 8),
     ]
 
 

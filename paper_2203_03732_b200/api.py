@@ -314,6 +314,9 @@ class Solver:
                         phase1_ms=r.phase1_ms, loop_ms=r.loop_ms, solve_d2h_ms=r.solve_d2h_ms,
                         bytes_touched=int(r.bytes_touched),
                         bytes_alg=int(r.bytes_alg), width=int(r.width),
+                        chain_stats=dict(zip(
+                            ("fresh", "takeover", "cache_hit", "cache_exhaust", "scan_past_cache",
+                             "rescan", "rowmin_skip", "proposals"), list(r.chain_stats))),
                         gpu_launches=int(r.gpu_launches)))
         return m, stats
 

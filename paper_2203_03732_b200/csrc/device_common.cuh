@@ -34,6 +34,10 @@ struct Ctl {
   unsigned long long bytes_touched;
   unsigned long long chain_steps;
   unsigned long long list_walks;
+  // chain statistics: 0 fresh chains, 1 takeovers, 2 proposals from the
+  // low-set cache, 3 exhausted by a complete cache, 4 scans continuing past
+  // the cache, 5 full rescans (cache rebuilt), 6 rowmin skips, 7 proposals
+  unsigned long long stat[8];
   // grid barrier (monotone arrival count)
   unsigned int bar_count;
   unsigned int pad1;

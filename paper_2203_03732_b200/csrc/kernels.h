@@ -11,8 +11,14 @@ namespace otprg {
 // Low-set cache per supply vertex b (see solve_kernels.cu): the ascending
 // positions a < cov with k(a,b) + t(a) <= upto at the time of the scan that
 // built it, up to kLowCap entries, each packed as (k << 32) | a.
-constexpr int kLowCap = 16;
-constexpr int kLowLevels = 2;  // upto = target + kLowLevels when (re)built
+#ifndef OTPRG_LOWCAP
+#define OTPRG_LOWCAP 16
+#endif
+#ifndef OTPRG_LOWLEVELS
+#define OTPRG_LOWLEVELS 2
+#endif
+constexpr int kLowCap = OTPRG_LOWCAP;        // <= 32 (one entry per lane)
+constexpr int kLowLevels = OTPRG_LOWLEVELS;  // upto = target + kLowLevels when (re)built
 
 // Device state of one prepared assignment problem, in the solver's internal
 // orientation (n_a >= n_b; rows of kT are supply vertices b, contiguous over

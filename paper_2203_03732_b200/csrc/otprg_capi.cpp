@@ -417,6 +417,7 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
   r->bytes_touched = static_cast<int64_t>(h.bytes_touched);
   r->bytes_alg = h.sum_ni * static_cast<int64_t>(ia) * ctx->width;
   r->width = ctx->width;
+  for (int i = 0; i < 8; ++i) r->chain_stats[i] = static_cast<int64_t>(h.stat[i]);
   return OTPRG_OK;
 }
 

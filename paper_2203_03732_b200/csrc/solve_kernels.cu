@@ -48,8 +48,15 @@ namespace otprg {
 
 namespace {
 
-constexpr int kBlock = 768;
-constexpr int kUnroll = 4;
+#ifndef OTPRG_BLOCK
+#define OTPRG_BLOCK 768
+#endif
+constexpr int kBlock = OTPRG_BLOCK;
+constexpr int kUnroll = 4;       // 128-bit loads in flight per lane (global t)
+#ifndef OTPRG_UNROLL_SMEM
+#define OTPRG_UNROLL_SMEM 8
+#endif
+constexpr int kUnrollSmem = OTPRG_UNROLL_SMEM;  // (t in shared memory)
 #ifdef OTPRG_DEBUG_SCAN
 constexpr unsigned kDebugBarriers = 1;
 #else
@@ -95,26 +102,33 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
   const uint4* rv = reinterpret_cast<const uint4*>(row);
   const uint4* tv = reinterpret_cast<const uint4*>(tvec);
   const int nv = lda / kEpv;  // multiple of 32
-  for (int v = (start / kEpv) & ~31; v < nv; v += 32 * kUnroll) {
-    uint4 kr[kUnroll], tr[kUnroll];
+  constexpr int kU = kSmem ? kUnrollSmem : kUnroll;
+  for (int v = (start / kEpv) & ~31; v < nv; v += 32 * kU) {
+    // kT loads for the whole chunk are issued first (kU in flight per lane);
+    // t comes from shared memory at use (or is preloaded when it is global).
+    uint4 kr[kU], tr[kSmem ? 1 : kU];
 #pragma unroll
-    for (int j = 0; j < kUnroll; ++j) {
+    for (int j = 0; j < kU; ++j) {
       const int vi = v + j * 32 + lane;
       if (vi < nv) {
         kr[j] = ldg_nc(rv + vi);
-        tr[j] = load_t<kSmem>(tv + vi);
+        if constexpr (!kSmem) tr[j] = load_t<false>(tv + vi);
       } else {
         kr[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
-        tr[j] = make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (!kSmem) tr[j] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
-    if (lane == 0) bytes += 16ull * (unsigned long long)min(nv - v, 32 * kUnroll);
+    if (lane == 0) bytes += 16ull * (unsigned long long)min(nv - v, 32 * kU);
 #pragma unroll
-    for (int j = 0; j < kUnroll; ++j) {
-      const int e0 = (v + j * 32 + lane) * kEpv;
+    for (int j = 0; j < kU; ++j) {
+      const int vi = v + j * 32 + lane;
+      const int e0 = vi * kEpv;
+      uint4 tj;
+      if constexpr (kSmem) tj = vi < nv ? tv[vi] : make_uint4(0u, 0u, 0u, 0u);
+      else tj = tr[j];
       const uint32_t k0 = kr[j].x, k1 = kr[j].y, k2 = kr[j].z, k3 = kr[j].w;
-      const uint32_t s0 = S::add(k0, tr[j].x), s1 = S::add(k1, tr[j].y);
-      const uint32_t s2 = S::add(k2, tr[j].z), s3 = S::add(k3, tr[j].w);
+      const uint32_t s0 = S::add(k0, tj.x), s1 = S::add(k1, tj.y);
+      const uint32_t s2 = S::add(k2, tj.z), s3 = S::add(k3, tj.w);
       uint32_t eqb = S::bits(S::eq(s0, tg)) | (S::bits(S::eq(s1, tg)) << S::kEpw) |
                      (S::bits(S::eq(s2, tg)) << (2 * S::kEpw)) |
                      (S::bits(S::eq(s3, tg)) << (3 * S::kEpw));
@@ -190,7 +204,11 @@ template <typename T, bool kSmem>
 __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const PhasePtrs& P,
                                           const T* tp, int lda, uint32_t phase, uint32_t tmax,
                                           int lane, unsigned long long& bytes,
-                                          unsigned long long& steps, unsigned long long& walks) {
+                                          unsigned long long& steps, unsigned long long& walks,
+                                          unsigned* s_stat, unsigned long long* acc) {
+#define OTPRG_STAT(k) \
+  if (lane == 0) atomicAdd(&s_stat[k], 1u)
+  OTPRG_STAT(0);
   using S = Simd<T>;
   Ctl* ctl = A.ctl;
   const T* kT = static_cast<const T*>(A.kT);
@@ -216,8 +234,10 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
   if (!walk) {
     if ((uint32_t)__ldcg(rowmin + b) > target) {
       skip = true;  // row min too high: no admissible edge (min only grows)
+      OTPRG_STAT(6);
     } else {       // (re)build the low set with a full scan from position 0
       meta = make_int4((int)(target + kLowLevels), 0, 0, 0);
+      OTPRG_STAT(5);
       lb.on = true;
       lb.cnt = 0;
       lb.up_rep = S::rep(target + kLowLevels);
@@ -238,7 +258,11 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       if (lane == 0) ++walks;
       if (bal) {
         a = __shfl_sync(kFull, pos, __ffs(bal) - 1);
-      } else if (meta.y < lda) {  // cache covers [0, cov) only: scan the rest
+        OTPRG_STAT(2);
+      } else if (meta.y >= lda) {
+        OTPRG_STAT(3);
+      } else {  // cache covers [0, cov) only: scan the rest
+        OTPRG_STAT(4);
         walk = false;
         scanning = true;
         start = max(start, meta.y);
@@ -252,8 +276,10 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       }
     }
     if (scanning) {
+      const unsigned long long ts0 = acc ? globaltimer() : 0;
       a = warp_scan<T, kSmem>(kT + (size_t)b * lda, tp, lda, start, target, track_min, mnw, lb,
                               lane, bytes);
+      if (acc) acc[0] += globaltimer() - ts0;
       if (lane == 0) ++steps;
       if (dirty) {
         meta.z = lb.cnt;
@@ -289,8 +315,11 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     }
     const unsigned long long key = ((unsigned long long)cur_tag << 32) | (uint32_t)b;
     unsigned long long old = 0;
+    OTPRG_STAT(7);
+    const unsigned long long ta0 = acc ? globaltimer() : 0;
     if (lane == 0) old = atomicMin(H + a, key);
     old = __shfl_sync(kFull, old, 0);
+    if (acc) acc[1] += globaltimer() - ta0;
     const uint32_t old_tag = (uint32_t)(old >> 32);
 #ifdef OTPRG_DEBUG_SCAN
     if (lane == 0 && old_tag < cur_tag)  // key from a later phase
@@ -303,6 +332,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     if (lane == 0 && fresh && dirty) A.lmeta[b] = meta;
     if (old_tag == cur_tag) {  // displaced b2 continues after a (plain scan)
       b = (int)(uint32_t)old;
+      OTPRG_STAT(1);
       yb = (uint32_t)__ldcg(A.yb + b);
       target = yb - 1;
       start = a + 1;
@@ -370,6 +400,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = __ldcg(src + i);
   }
   __shared__ int s_ctl[4];
+  __shared__ unsigned s_stat[8];
+  if (threadIdx.x < 8) s_stat[threadIdx.x] = 0;
   bool first = true;
   int n_prev = -1;
   while (true) {
@@ -471,7 +503,6 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       if (tr) tr[0] = globaltimer(), tr[7] = (unsigned long long)n;
     }
     const T* tp = kSmem ? s_t : tg;
-    if (tr && leader) tr[1] = globaltimer();
 
     // ---- P step: proposal chains over the free list of phase `phase` ----
     const int32_t* list_in = r_prev == 0 ? A.list[0] : (r_prev == 1 ? A.list[1] : A.list[2]);
@@ -484,11 +515,20 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     // First proposer of every warp is static (no contended grab when
     // n_i <= #warps); the rest are grabbed from a counter.
     int i = gwarp;
+    unsigned long long acc[2] = {0ull, 0ull};
+    const unsigned long long tp0 = tr ? globaltimer() : 0;
+    const bool had_work = i < n;
     while (i < n) {
       const int b = __ldcg(list_in + i);
-      run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks);
+      run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
+                          tr ? acc : nullptr);
       if (lane == 0) i = total_warps + atomicAdd(&ctl->work[r_cur], 1);
       i = __shfl_sync(kFull, i, 0);
+    }
+    if (tr && had_work && lane == 0) {  // slowest warp: scan / atomic / total ns
+      atomicMax(tr + 1, acc[0]);
+      atomicMax(tr + 5, acc[1]);
+      atomicMax(tr + 6, globaltimer() - tp0);
     }
     bar_target += gridDim.x;
     grid_barrier(ctl, bar_target, tr ? tr + 2 : nullptr, tr ? tr + 3 : nullptr);
@@ -499,6 +539,9 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     atomicAdd(&ctl->chain_steps, steps);
     atomicAdd(&ctl->list_walks, walks);
   }
+  __syncthreads();
+  if (threadIdx.x < 8 && s_stat[threadIdx.x])
+    atomicAdd(&ctl->stat[threadIdx.x], (unsigned long long)s_stat[threadIdx.x]);
 }
 
 template <typename T>

@@ -1,4 +1,4 @@
-"""Per-phase device timeline of config-2 solves (tracing on)."""
+"""Per-phase device timeline of a solve (tracing on)."""
 import sys
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
@@ -14,19 +14,18 @@ for _ in range(3):
     m, s = S.solve_prepared()
 tr = S.get_trace(s.phases).astype(np.int64)
 t0 = tr[:, 0]
-start = t0
-staged = tr[:, 1] - t0
 p_last = tr[:, 2] - t0
 p_first = (~tr[:, 3].astype(np.uint64)).astype(np.int64) - t0
-b1 = tr[:, 4] - t0
-a_last = tr[:, 5] - t0
-b2 = tr[:, 6] - t0
+bar = tr[:, 4] - t0
 nxt = np.append(t0[1:] - t0[:-1], 0)
+scan, atom, warp = tr[:, 1], tr[:, 5], tr[:, 6]
 print(f"solve_ms={s.device['solve_ms']:.3f} loop_ms={s.device['loop_ms']:.3f} phases={s.phases}")
-print("phase  n_i  staged  Pfirst  Plast  bar1  Alast  bar2  next   (us from phase start)")
-for i in list(range(0, 8)) + list(range(8, s.phases, max(1, s.phases // 25))):
-    print(f"{i+1:5d} {tr[i,7]:5d} {staged[i]/1e3:7.2f} {p_first[i]/1e3:7.2f} {p_last[i]/1e3:6.2f} "
-          f"{b1[i]/1e3:6.2f} {a_last[i]/1e3:6.2f} {b2[i]/1e3:6.2f} {nxt[i]/1e3:6.2f}")
+print("phase   n_i  Pfirst  Plast   bar   next | slowest warp: total  scan  atomic (us)")
+rows = list(range(0, min(8, s.phases))) + list(range(8, s.phases, max(1, s.phases // 20)))
+for i in rows:
+    print(f"{i+1:5d} {tr[i,7]:5d} {p_first[i]/1e3:7.2f} {p_last[i]/1e3:6.2f} {bar[i]/1e3:6.2f} {nxt[i]/1e3:6.2f} |"
+          f" {warp[i]/1e3:6.2f} {scan[i]/1e3:6.2f} {atom[i]/1e3:6.2f}")
 sl = slice(1, s.phases - 1)
-print("means over phases 2..: staged %.2f Pfirst %.2f Plast %.2f bar1 %.2f Alast %.2f bar2 %.2f next %.2f" % tuple(
-    x[sl].mean() / 1e3 for x in (staged, p_first, p_last, b1, a_last, b2, nxt)))
+print("means over phases 2..: Pfirst %.2f Plast %.2f bar %.2f next %.2f | warp %.2f scan %.2f atomic %.2f" % tuple(
+    x[sl].mean() / 1e3 for x in (p_first, p_last, bar, nxt, warp, scan, atom)))
+print("chain stats", s.device["chain_stats"], "bytes_touched", s.device["bytes_touched"] / 1e6, "MB")

@@ -43,7 +43,7 @@ def test_struct_layouts_match_header(lib):
     def fields(struct):
         body = re.search(r"typedef struct " + struct + r" \{(.*?)\} " + struct, src, re.S).group(1)
         body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
-        return [m.group(1) for m in re.finditer(r"\b(\w+);", body)]
+        return [m.group(1) for m in re.finditer(r"\b(\w+)(?:\[\d+\])?;", body)]
 
     assert fields("otprg_problem") == [f for f, _ in _native.Problem._fields_]
     assert fields("otprg_result") == [f for f, _ in _native.Result._fields_]
