@@ -164,6 +164,16 @@ int otprg_scale_round_costs(otprg_ctx* ctx, const otprg_problem* prob, int32_t* 
  * uniforms.  Writes interleaved (x, y) pairs, n per side.  Host-only. */
 int otprg_uniform_square_points(int32_t n, uint64_t seed, double* pts_a, double* pts_b);
 
+/* The image pair of otpr::load_mnist_pair(path, n, seed)
+ * (src/instances.cpp:80-144): parses the IDX3 file, draws the seeded sample of
+ * 2n distinct images (mt19937_64(splitmix64(seed ^ 0xD1B54A32D192ED03)),
+ * partial Fisher-Yates) and writes the first n raw 28x28 images to img_a and
+ * the next n to img_b (n*784 bytes each).  The L1/2 cost of the pair is then
+ * computed on the device with OTPRG_COST_L1_U8.  Errors: 3 for unreadable /
+ * malformed files (FormatError / InputError), message in err.  Host-only. */
+int otprg_load_mnist_pair(const char* path, int32_t n, uint64_t seed, uint8_t* img_a,
+                          uint8_t* img_b, char* err, int32_t err_cap);
+
 /* Writes a buffer larger than L2 on the context's stream (benchmark hygiene). */
 int otprg_flush_l2(otprg_ctx* ctx);
 

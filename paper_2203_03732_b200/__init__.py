@@ -5,13 +5,14 @@ path.  See DESIGN.md for the device design and INTEGRATION.md for the C ABI.
 from .api import (  # noqa: F401
     AssignmentInstance, AssignmentOptions, DeviceError, DualState, FormatError, InputError,
     InvariantViolation, Matching, NumericalError, ParameterError, ScaledCosts, SolveStats, Solver,
-    gen_uniform_square, get_solver, matching_cost, points_cost, scale_round_costs, scaled_floor,
-    solve_assignment,
+    gen_uniform_square, get_solver, l1_cost, load_mnist_pair, matching_cost, points_cost,
+    scale_round_costs, scaled_floor, solve_assignment,
 )
 
 __all__ = [
     "AssignmentInstance", "AssignmentOptions", "DeviceError", "DualState", "FormatError",
     "InputError", "InvariantViolation", "Matching", "NumericalError", "ParameterError",
-    "ScaledCosts", "SolveStats", "Solver", "gen_uniform_square", "get_solver", "matching_cost",
-    "points_cost", "scale_round_costs", "scaled_floor", "solve_assignment",
+    "ScaledCosts", "SolveStats", "Solver", "gen_uniform_square", "get_solver", "l1_cost",
+    "load_mnist_pair", "matching_cost", "points_cost", "scale_round_costs", "scaled_floor",
+    "solve_assignment",
 ]

@@ -54,7 +54,7 @@ EXPORTS = [
     "otprg_solve_assignment", "otprg_prepare", "otprg_solve_prepared", "otprg_scale_round_costs",
     "otprg_uniform_square_points", "otprg_flush_l2", "otprg_begin", "otprg_step",
     "otprg_snapshot", "otprg_finish", "otprg_timer_start", "otprg_timer_stop",
-    "otprg_set_trace", "otprg_get_trace",
+    "otprg_set_trace", "otprg_get_trace", "otprg_load_mnist_pair",
 ]
 
 _lib = None
@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
     L.otprg_timer_stop.argtypes = [vp, C.POINTER(C.c_double)]
     L.otprg_set_trace.argtypes = [vp, C.c_int64]
     L.otprg_get_trace.argtypes = [vp, vp, C.c_int64]
+    L.otprg_load_mnist_pair.argtypes = [C.c_char_p, C.c_int32, C.c_uint64, vp, vp, C.c_char_p,
+                                        C.c_int32]
     _lib = L
     return L
 

@@ -67,6 +67,8 @@ class AssignmentInstance:
     pts_b: Optional[np.ndarray] = None     # (n_b, 2) float64
     norm_factor: float = 1.0
     seed: int = 0
+    img_a: Optional[np.ndarray] = None     # (n_a, dim) uint8: L1/2 cost of normalised images
+    img_b: Optional[np.ndarray] = None     # (n_b, dim) uint8   (load_mnist_pair, instances.cpp:80-144)
 
     def validate(self) -> None:
         """core.cpp:10-24."""
@@ -79,12 +81,14 @@ class AssignmentInstance:
             if bad.any():
                 a, b = np.argwhere(bad)[0]
                 raise ParameterError(f"cost entry outside [0,1] at ({a},{b}): {self.cost[a, b]:f}")
-        elif self.pts_a is None or self.pts_b is None:
-            raise ParameterError("instance has neither a cost matrix nor point sets")
+        elif (self.pts_a is None or self.pts_b is None) and (self.img_a is None or self.img_b is None):
+            raise ParameterError("instance has neither a cost matrix, point sets nor images")
 
     def dense_cost(self) -> np.ndarray:
         if self.cost is not None:
             return self.cost
+        if self.img_a is not None:
+            return l1_cost(self.img_a, self.img_b)
         return points_cost(self.pts_a, self.pts_b)
 
 
@@ -226,6 +230,14 @@ class Solver:
             p.cost_kind = N.COST_DENSE_F64
             p.cost = cost.ctypes.data
             self._keep = (cost,)
+        elif inst.img_a is not None and inst.img_b is not None:
+            ia = np.ascontiguousarray(inst.img_a, np.uint8).reshape(inst.n_a, -1)
+            ib = np.ascontiguousarray(inst.img_b, np.uint8).reshape(inst.n_b, -1)
+            if ia.shape[1] != ib.shape[1]:
+                raise ParameterError("image dimensions differ between the sides")
+            p.cost_kind = N.COST_L1_U8
+            p.img_a, p.img_b, p.dim = ia.ctypes.data, ib.ctypes.data, ia.shape[1]
+            self._keep = (ia, ib)
         elif inst.pts_a is not None and inst.pts_b is not None:
             pa = np.ascontiguousarray(inst.pts_a, np.float64).reshape(inst.n_a, 2)
             pb = np.ascontiguousarray(inst.pts_b, np.float64).reshape(inst.n_b, 2)
@@ -416,6 +428,8 @@ def matching_cost(m: Matching, inst: AssignmentInstance) -> float:
 def _pair_cost(inst: AssignmentInstance, a: int, b: int) -> float:
     if inst.cost is not None:
         return float(inst.cost[a, b])
+    if inst.img_a is not None:
+        return float(l1_cost(inst.img_a[a:a + 1], inst.img_b[b:b + 1])[0, 0])
     dx = float(inst.pts_a[a, 0]) - float(inst.pts_b[b, 0])
     dy = float(inst.pts_a[a, 1]) - float(inst.pts_b[b, 1])
     return math.sqrt(dx * dx + dy * dy) / math.sqrt(2.0)
@@ -443,3 +457,34 @@ def gen_uniform_square(n: int, seed: int, dense: bool = False) -> AssignmentInst
     if dense:
         inst.cost = points_cost(pa, pb)
     return inst
+
+
+def l1_cost(img_a: np.ndarray, img_b: np.ndarray) -> np.ndarray:
+    """Dense load_mnist_pair cost (instances.cpp:114-142): per-image
+    normalisation, then sum_p |x_p - y_p| in ascending p, / 2 (host, numpy;
+    the sequential sum is kept by accumulating pixel by pixel)."""
+    xa = img_a.astype(np.float64) / img_a.astype(np.float64).sum(axis=1, keepdims=True)
+    yb = img_b.astype(np.float64) / img_b.astype(np.float64).sum(axis=1, keepdims=True)
+    acc = np.zeros((xa.shape[0], yb.shape[0]), np.float64)
+    for p in range(xa.shape[1]):
+        acc += np.abs(xa[:, p:p + 1] - yb[None, :, p])
+    return acc / 2.0
+
+
+def load_mnist_pair(path: str, n: int, seed: int) -> AssignmentInstance:
+    """instances.cpp:80-144: seeded sample of 2n IDX3 images; the first n are A,
+    the next n B; cost = L1/2 of the normalised images (computed on the device
+    at solve time; norm_factor = 2)."""
+    img_a = np.empty((n, 784), np.uint8)
+    img_b = np.empty((n, 784), np.uint8)
+    err = C.create_string_buffer(256)
+    st = N.lib().otprg_load_mnist_pair(path.encode(), n, seed, img_a.ctypes.data,
+                                      img_b.ctypes.data, err, 256)
+    if st:
+        msg = err.value.decode()
+        if st == N.PARAMETER:
+            raise ParameterError(msg)
+        if "magic" in msg or "short" in msg or "truncated" in msg or "dimensions" in msg:
+            raise FormatError(msg)
+        raise InputError(msg)
+    return AssignmentInstance(n, n, None, img_a=img_a, img_b=img_b, norm_factor=2.0, seed=seed)

@@ -97,6 +97,95 @@ __global__ void round_points_kernel(const double2* __restrict__ pa,
   }
 }
 
+// K3a: per-image normalisation of load_mnist_pair (instances.cpp:114-126):
+// total = sum of the pixels (exact in double), pixel / total (IEEE RN).  One
+// block per image.  A zero total is the reference's InputError (status 3).
+__global__ void l1_normalize_kernel(const uint8_t* __restrict__ img, int count, int dim,
+                                    double* __restrict__ out, int* status) {
+  __shared__ unsigned s_sum;
+  for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    if (threadIdx.x == 0) s_sum = 0;
+    __syncthreads();
+    const uint8_t* src = img + (size_t)i * dim;
+    unsigned part = 0;
+    for (int p = threadIdx.x; p < dim; p += blockDim.x) part += src[p];
+    atomicAdd(&s_sum, part);
+    __syncthreads();
+    const double total = (double)s_sum;  // integer sum < 2^53: exact, any order
+    if (total == 0.0) {
+      if (threadIdx.x == 0) atomicCAS(status, 0, 3);
+    } else {
+      for (int p = threadIdx.x; p < dim; p += blockDim.x)
+        out[(size_t)i * dim + p] = __ddiv_rn((double)src[p], total);
+    }
+    __syncthreads();
+  }
+}
+
+// K3b: all-pairs L1 / 2 with rounding (instances.cpp:134-142 then
+// scale_round_costs).  c(a,b) = (sum_p |x_a[p] - y_b[p]|) / 2 summed in
+// ascending p exactly like the reference (no reassociation, no FMA), so the
+// bits match.  Block tile 64 a x 64 b, thread tile 4 x 4, pixels staged in
+// shared memory in chunks of kP, p-major.
+constexpr int kL1Tile = 64, kL1P = 16, kL1T = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) l1_round_kernel(const double* __restrict__ xa,
+                                                       const double* __restrict__ yb, int n_ai,
+                                                       int n_bi, int dim, double eps,
+                                                       T* __restrict__ kT, int lda, int* status) {
+  __shared__ __align__(16) double As[kL1P][kL1Tile];
+  __shared__ __align__(16) double Bs[kL1P][kL1Tile];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int a0 = blockIdx.x * kL1Tile, b0 = blockIdx.y * kL1Tile;
+  double acc[kL1T][kL1T];
+#pragma unroll
+  for (int i = 0; i < kL1T; ++i)
+#pragma unroll
+    for (int j = 0; j < kL1T; ++j) acc[i][j] = 0.0;
+  for (int p0 = 0; p0 < dim; p0 += kL1P) {
+    for (int e = threadIdx.x; e < kL1Tile * kL1P; e += blockDim.x) {
+      const int r = e / kL1P, pp = e % kL1P, p = p0 + pp;
+      const int a = a0 + r, b = b0 + r;
+      As[pp][r] = (a < n_ai && p < dim) ? xa[(size_t)a * dim + p] : 0.0;
+      Bs[pp][r] = (b < n_bi && p < dim) ? yb[(size_t)b * dim + p] : 0.0;
+    }
+    __syncthreads();
+    const int pend = min(kL1P, dim - p0);
+    for (int pp = 0; pp < pend; ++pp) {
+      double av[kL1T], bv[kL1T];
+#pragma unroll
+      for (int i = 0; i < kL1T; ++i) av[i] = As[pp][ty * kL1T + i];
+#pragma unroll
+      for (int j = 0; j < kL1T; ++j) bv[j] = Bs[pp][tx * kL1T + j];
+#pragma unroll
+      for (int i = 0; i < kL1T; ++i)
+#pragma unroll
+        for (int j = 0; j < kL1T; ++j) acc[i][j] = __dadd_rn(acc[i][j], fabs(__dsub_rn(av[i], bv[j])));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < kL1T; ++i) {
+    const int a = a0 + ty * kL1T + i;
+#pragma unroll
+    for (int j = 0; j < kL1T; ++j) {
+      const int b = b0 + tx * kL1T + j;
+      if (b >= n_bi) continue;
+      if (a < n_ai) {
+        const double c = __ddiv_rn(acc[i][j], 2.0);
+        if (!(c >= 0.0 && c <= 1.0)) {
+          atomicCAS(status, 0, 2);  // core.cpp:18-21 rejects it (ParameterError)
+          kT[(size_t)b * lda + a] = (T)type_max<T>();
+        } else {
+          kT[(size_t)b * lda + a] = clamp_store<T>(scaled_floor_dev(c, eps));
+        }
+      } else if (a < lda) {
+        kT[(size_t)b * lda + a] = (T)type_max<T>();
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void export_k_kernel(const T* __restrict__ kT, int n_ai, int n_bi, int lda,
                                 int swapped, int32_t* __restrict__ k) {
@@ -147,6 +236,25 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
   else
     round_points_kernel<uint16_t><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2,
                                                        static_cast<uint16_t*>(kT), lda);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l1_normalize(const uint8_t* img, int count, int dim, double* out, int* status,
+                                cudaStream_t s) {
+  l1_normalize_kernel<<<count < 4096 ? count : 4096, 256, 0, s>>>(img, count, dim, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_bi, int dim,
+                            double eps, void* kT, int lda, int width, int* status,
+                            cudaStream_t s) {
+  dim3 grid(lda / kL1Tile, (n_bi + kL1Tile - 1) / kL1Tile);
+  if (width == 1)
+    l1_round_kernel<uint8_t><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps,
+                                                  static_cast<uint8_t*>(kT), lda, status);
+  else
+    l1_round_kernel<uint16_t><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps,
+                                                   static_cast<uint16_t*>(kT), lda, status);
   return cudaGetLastError();
 }
 

@@ -54,6 +54,14 @@ cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swappe
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
                                   double eps, double sqrt2, void* kT, int lda, int width,
                                   cudaStream_t s);
+// K3: L1/2 cost of per-image-normalised uint8 vectors (load_mnist_pair).
+// normalize: out[i][p] = img[i][p] / sum_p img[i][p] (status 3 on a zero image);
+// round: kT[b][a] = scaled_floor(sum_p |xa[a][p] - yb[b][p]| / 2, eps) (status 2
+// when a cost leaves [0,1]).  lda must be a multiple of 64.
+cudaError_t launch_l1_normalize(const uint8_t* img, int count, int dim, double* out, int* status,
+                                cudaStream_t s);
+cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_bi, int dim,
+                            double eps, void* kT, int lda, int width, int* status, cudaStream_t s);
 // Rounded matrix back to int32 row-major in the ORIGINAL orientation (for
 // otprg_scale_round_costs).
 cudaError_t launch_export_k(const void* kT, int n_ai, int n_bi, int lda, int width, bool swapped,

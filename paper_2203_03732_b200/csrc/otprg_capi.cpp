@@ -82,6 +82,8 @@ struct otprg_ctx {
   int cost_kind = 0;
   const double* host_cost = nullptr;  // caller buffer (DENSE); valid until next prepare
   std::vector<double> pts_a, pts_b;   // original orientation (POINTS2D)
+  std::vector<uint8_t> img_a, img_b;  // original orientation (L1_U8)
+  int img_dim = 0;
   double build_ms = 0.0;
   int build_launches = 0;
 
@@ -132,6 +134,10 @@ int validate_problem(otprg_ctx* ctx, const otprg_problem* p) {
       break;
     case OTPRG_COST_POINTS2D:
       if (!p->pts_a || !p->pts_b) return fail(ctx, OTPRG_PARAMETER, "point pointers are null");
+      break;
+    case OTPRG_COST_L1_U8:
+      if (!p->img_a || !p->img_b || p->dim < 1)
+        return fail(ctx, OTPRG_PARAMETER, "image pointers are null or dim < 1");
       break;
     default:
       return fail(ctx, OTPRG_PARAMETER, "unsupported cost kind " + std::to_string(p->cost_kind));
@@ -207,6 +213,29 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
        "round_dense launch");
     ctx->build_launches = 1;
     ctx->host_cost = p->cost;
+  } else if (p->cost_kind == OTPRG_COST_L1_U8) {
+    // load_mnist_pair's cost (instances.cpp:114-142) from raw pixels
+    const size_t dim = static_cast<size_t>(p->dim);
+    const uint8_t* ia_img = ctx->swapped ? p->img_b : p->img_a;  // internal demand side
+    const uint8_t* ib_img = ctx->swapped ? p->img_a : p->img_b;
+    CK(ctx->pts.ensure((ia + ib) * dim * (sizeof(double) + 1)), "alloc images");
+    double* xa = ctx->pts.as<double>();
+    double* yb = xa + ia * dim;
+    uint8_t* raw = reinterpret_cast<uint8_t*>(yb + ib * dim);
+    CK(cudaMemcpyAsync(raw, ia_img, ia * dim, cudaMemcpyHostToDevice, ctx->stream), "H2D images");
+    CK(cudaMemcpyAsync(raw + ia * dim, ib_img, ib * dim, cudaMemcpyHostToDevice, ctx->stream),
+       "H2D images");
+    CK(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(Ctl), ctx->stream), "memset");
+    int* status = &ctx->ctl.as<Ctl>()->status;
+    CK(otprg::launch_l1_normalize(raw, static_cast<int>(ia + ib), p->dim, xa, status, ctx->stream),
+       "l1 normalize launch");
+    CK(otprg::launch_l1_round(xa, yb, ctx->ia, ctx->ib, p->dim, p->eps, ctx->kT.p, ctx->lda, width,
+                              status, ctx->stream),
+       "l1 round launch");
+    ctx->build_launches = 2;
+    ctx->img_dim = p->dim;
+    ctx->img_a.assign(p->img_a, p->img_a + dim * p->n_a);
+    ctx->img_b.assign(p->img_b, p->img_b + dim * p->n_b);
   } else {
     const double* pa = ctx->swapped ? p->pts_b : p->pts_a;  // internal demand points
     const double* pb = ctx->swapped ? p->pts_a : p->pts_b;
@@ -232,6 +261,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
      "D2H status");
   CK(cudaStreamSynchronize(ctx->stream), "cost build");
   if (dstatus == OTPRG_PARAMETER) return fail(ctx, OTPRG_PARAMETER, "cost entry outside [0,1]");
+  if (dstatus == OTPRG_INPUT) return fail(ctx, OTPRG_INPUT, "image has zero total intensity");
   if (dstatus) return fail(ctx, dstatus, "cost build failed");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]);
@@ -240,9 +270,23 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   return OTPRG_OK;
 }
 
+// L1/2 of two normalised images, ascending p (instances.cpp:116-126,134-141).
+double l1_cost(const uint8_t* x, const uint8_t* y, int dim) {
+  double tx = 0.0, ty = 0.0;
+  for (int p = 0; p < dim; ++p) tx += x[p];
+  for (int p = 0; p < dim; ++p) ty += y[p];
+  double l1 = 0.0;
+  for (int p = 0; p < dim; ++p)
+    l1 += std::abs(static_cast<double>(x[p]) / tx - static_cast<double>(y[p]) / ty);
+  return l1 / 2.0;
+}
+
 double pair_cost(const otprg_ctx* ctx, int32_t a, int32_t b) {
   if (ctx->cost_kind == OTPRG_COST_DENSE_F64)
     return ctx->host_cost[static_cast<size_t>(a) * ctx->n_b + b];
+  if (ctx->cost_kind == OTPRG_COST_L1_U8)
+    return l1_cost(ctx->img_a.data() + static_cast<size_t>(a) * ctx->img_dim,
+                   ctx->img_b.data() + static_cast<size_t>(b) * ctx->img_dim, ctx->img_dim);
   // instances.cpp:70-75, same expression, non-fused (-ffp-contract=off)
   const double sqrt2 = std::sqrt(2.0);
   const double dx = ctx->pts_a[2 * static_cast<size_t>(a)] - ctx->pts_b[2 * static_cast<size_t>(b)];
@@ -533,6 +577,76 @@ int otprg_scale_round_costs(otprg_ctx* ctx, const otprg_problem* prob, int32_t* 
   CK(cudaStreamSynchronize(ctx->stream), "export");
   if (unit_floor) *unit_floor = ctx->unit_floor;
   if (unit_ceil) *unit_ceil = ctx->unit_ceil;
+  return OTPRG_OK;
+}
+
+int otprg_load_mnist_pair(const char* path, int32_t n, uint64_t seed, uint8_t* img_a,
+                          uint8_t* img_b, char* err, int32_t err_cap) {
+  auto fail_msg = [&](int code, const std::string& m) {
+    if (err && err_cap > 0) {
+      std::strncpy(err, m.c_str(), static_cast<size_t>(err_cap) - 1);
+      err[err_cap - 1] = 0;
+    }
+    return code;
+  };
+  if (n < 1) return fail_msg(OTPRG_PARAMETER, "load_mnist_pair: n must be >= 1");
+  if (!path || !img_a || !img_b) return fail_msg(OTPRG_PARAMETER, "null argument");
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return fail_msg(OTPRG_INPUT, std::string("cannot open image file: ") + path);
+  std::vector<unsigned char> bytes;
+  {
+    unsigned char buf[1 << 16];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) bytes.insert(bytes.end(), buf, buf + got);
+    std::fclose(f);
+  }
+  auto be32 = [](const unsigned char* p) {
+    return (uint32_t(p[0]) << 24) | (uint32_t(p[1]) << 16) | (uint32_t(p[2]) << 8) | uint32_t(p[3]);
+  };
+  // instances.cpp:88-103
+  if (bytes.size() < 16) return fail_msg(OTPRG_INPUT, "image file too short for a header");
+  if (be32(bytes.data()) != 0x00000803) return fail_msg(OTPRG_INPUT, "bad IDX3 magic: expected 0x00000803");
+  const uint32_t count = be32(bytes.data() + 4);
+  if (be32(bytes.data() + 8) != 28 || be32(bytes.data() + 12) != 28)
+    return fail_msg(OTPRG_INPUT, "unexpected image dimensions: want 28x28");
+  const size_t pixels = 28 * 28;
+  if (bytes.size() < 16 + static_cast<size_t>(count) * pixels)
+    return fail_msg(OTPRG_INPUT, "image file truncated");
+  if (count < static_cast<uint32_t>(2 * n))
+    return fail_msg(OTPRG_INPUT, "not enough images: need " + std::to_string(2 * n) +
+                                     ", file has " + std::to_string(count));
+  // seeded sample of 2n distinct indices, partial Fisher-Yates (instances.cpp:105-112)
+  auto splitmix64 = [](uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+  };
+  std::mt19937_64 rng(splitmix64(seed ^ 0xD1B54A32D192ED03ULL));
+  auto bounded = [&](uint64_t m) {  // instances.cpp:25-32
+    const uint64_t limit = ~uint64_t{0} - (~uint64_t{0}) % m;
+    uint64_t x;
+    do {
+      x = rng();
+    } while (x >= limit);
+    return x % m;
+  };
+  std::vector<uint32_t> pool(count);
+  for (uint32_t i = 0; i < count; ++i) pool[i] = i;
+  for (int32_t i = 0; i < 2 * n; ++i) {
+    const uint64_t j = static_cast<uint64_t>(i) + bounded(count - static_cast<uint64_t>(i));
+    std::swap(pool[i], pool[j]);
+  }
+  for (int32_t i = 0; i < 2 * n; ++i) {
+    const unsigned char* src = bytes.data() + 16 + static_cast<size_t>(pool[i]) * pixels;
+    size_t total = 0;
+    for (size_t p = 0; p < pixels; ++p) total += src[p];
+    if (total == 0)  // instances.cpp:121-123
+      return fail_msg(OTPRG_INPUT, "image " + std::to_string(pool[i]) + " has zero total intensity");
+    std::memcpy((i < n ? img_a + static_cast<size_t>(i) * pixels
+                       : img_b + static_cast<size_t>(i - n) * pixels),
+                src, pixels);
+  }
   return OTPRG_OK;
 }
 
