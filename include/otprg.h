@@ -174,6 +174,56 @@ int otprg_uniform_square_points(int32_t n, uint64_t seed, double* pts_a, double*
 int otprg_load_mnist_pair(const char* path, int32_t n, uint64_t seed, uint8_t* img_a,
                           uint8_t* img_b, char* err, int32_t err_cap);
 
+/* ---- optimal transport (config 5) ---------------------------------------
+ * otprg_solve_ot replaces otpr::solve_ot (include/otpr/ot.hpp:161-163,
+ * src/ot.cpp:705-732): theta-scaling of the masses at eps/3
+ * (scale_and_round, ot.cpp:109-128), the copy/cluster phase algorithm
+ * (solve_copy_matching, ot.cpp:418-637) and plan_from_flow (ot.cpp:639-703).
+ * Plan entries are written row-major (as TransportPlan::entries) up to
+ * entry_cap; n_entries reports the full count.  Masses and costs as the
+ * reference sees them (no renormalisation here). */
+typedef struct otprg_ot_problem {
+  int32_t n_a, n_b;
+  double eps;
+  const double* mu;    /* n_a demand masses, host */
+  const double* nu;    /* n_b supply masses, host */
+  const double* cost;  /* n_a*n_b row-major in [0,1], host */
+  int32_t flags;       /* reserved, 0 */
+  int32_t pad;
+} otprg_ot_problem;
+
+typedef struct otprg_ot_result {
+  int32_t* ent_a;
+  int32_t* ent_b;
+  double* ent_mass;
+  int64_t entry_cap;
+  int64_t* free_counts; /* free supply copies per phase, or NULL */
+  int64_t free_cap;
+  /* outputs */
+  int64_t n_entries;
+  double cost;           /* TransportPlan::cost */
+  int64_t phases;
+  int64_t sum_ni;
+  int32_t full_match_termination;
+  int32_t gpu_launches;
+  double theta;          /* ScaledMasses::theta */
+  int64_t total_d, total_s;
+  double build_ms, loop_ms, scan_ms, solve_ms;  /* host-clock ms around the stages */
+  int64_t bytes_touched; /* kT bytes covered by the device scans */
+} otprg_ot_result;
+
+int otprg_solve_ot(otprg_ctx* ctx, const otprg_ot_problem* prob, otprg_ot_result* res);
+
+/* scale_and_round (ot.cpp:109-128): d = exact_ceil(mu*theta),
+ * s = exact_floor(nu*theta), theta = 4 max(n_a,n_b) / eps.  Host-only. */
+int otprg_ot_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const double* nu,
+                             double eps, int64_t* d, int64_t* s, double* theta);
+
+/* otpr::gen_random_ot_rational(n_a, n_b, seed) (instances.cpp:159-191)
+ * including OTInstance::renormalize (ot.cpp:91-100).  Host-only. */
+int otprg_random_ot_rational(int32_t n_a, int32_t n_b, uint64_t seed, double* mu, double* nu,
+                             double* cost);
+
 /* Writes a buffer larger than L2 on the context's stream (benchmark hygiene). */
 int otprg_flush_l2(otprg_ctx* ctx);
 

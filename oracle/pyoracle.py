@@ -281,6 +281,10 @@ class Reference:
         lib.ref_solve_ot_rational.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_double, _i32p, _i32p,
                                               _f64p, C.c_int64, _i64p, C.c_int64, C.POINTER(_RefOtStats)]
         lib.ref_gen_random_ot_rational.argtypes = [C.c_int32, C.c_int32, C.c_uint64, _f64p, _f64p, _f64p]
+        lib.ref_solve_ot.argtypes = [C.c_int32, C.c_int32, _f64p, _f64p, _f64p, C.c_double, _i32p, _i32p,
+                                     _f64p, C.c_int64, _i64p, C.c_int64, C.POINTER(_RefOtStats)]
+        lib.ref_scale_and_round.argtypes = [C.c_int32, C.c_int32, _f64p, _f64p, _f64p, C.c_double, _i64p,
+                                            _i64p, C.POINTER(C.c_double)]
 
     def _check(self, st):
         if st:
@@ -350,6 +354,34 @@ class Reference:
         cost = np.empty((n_a, n_b))
         self._check(self.lib.ref_gen_random_ot_rational(n_a, n_b, seed, mu, nu, cost))
         return mu, nu, cost
+
+    def solve_ot(self, mu, nu, cost, eps: float, entry_cap: int | None = None):
+        """otpr::solve_ot on the given instance (masses as given, no renormalisation)."""
+        mu = np.ascontiguousarray(mu, np.float64)
+        nu = np.ascontiguousarray(nu, np.float64)
+        cost = np.ascontiguousarray(cost, np.float64)
+        n_a, n_b = cost.shape
+        cap_e = entry_cap or (n_a + n_b) * 4 + 16
+        ea, eb, em = np.empty(cap_e, np.int32), np.empty(cap_e, np.int32), np.empty(cap_e)
+        fcap = phase_cap(eps / 3.0) + 1
+        fc = np.zeros(fcap, np.int64)
+        s = _RefOtStats()
+        self._check(self.lib.ref_solve_ot(n_a, n_b, mu, nu, cost, eps, ea, eb, em, cap_e, fc, fcap,
+                                          C.byref(s)))
+        ne = min(s.n_entries, cap_e)
+        return {"phases": s.phases, "sum_ni": s.sum_ni, "cost": s.cost, "theta": s.theta,
+                "solve_ms": s.solve_ms, "n_entries": s.n_entries, "total_d": s.total_d,
+                "total_s": s.total_s, "a": ea[:ne].copy(), "b": eb[:ne].copy(), "mass": em[:ne].copy(),
+                "free_counts": fc[: s.phases].copy()}
+
+    def scale_and_round(self, mu, nu, cost, eps: float):
+        mu = np.ascontiguousarray(mu, np.float64)
+        nu = np.ascontiguousarray(nu, np.float64)
+        cost = np.ascontiguousarray(cost, np.float64)
+        d, s = np.empty(len(mu), np.int64), np.empty(len(nu), np.int64)
+        th = C.c_double()
+        self._check(self.lib.ref_scale_and_round(len(mu), len(nu), mu, nu, cost, eps, d, s, C.byref(th)))
+        return d, s, th.value
 
     def solve_ot_rational(self, n_a: int, n_b: int, seed: int, eps: float, entry_cap: int | None = None):
         cap_e = entry_cap or (n_a + n_b) * 4

@@ -253,3 +253,61 @@ int ref_gen_random_ot_rational(int32_t n_a, int32_t n_b, uint64_t seed,
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// solve_ot on a caller-given instance (mu, nu, row-major cost); renormalize()
+// is NOT applied (the caller passes masses exactly as the reference would see
+// them).
+int ref_solve_ot(int32_t n_a, int32_t n_b, const double* mu, const double* nu,
+                 const double* cost, double eps, int32_t* ent_a, int32_t* ent_b,
+                 double* ent_mass, int64_t entry_cap, int64_t* free_counts,
+                 int64_t free_cap, RefOtStats* out) {
+  return guarded([&] {
+    otpr::OTInstance inst;
+    inst.mu.assign(mu, mu + n_a);
+    inst.nu.assign(nu, nu + n_b);
+    inst.cost = otpr::Matrix<double>(n_a, n_b);
+    std::memcpy(inst.cost.data(), cost, sizeof(double) * size_t(n_a) * n_b);
+    const auto sm = otpr::scale_and_round(inst, eps / 3.0);
+    out->theta = sm.theta;
+    out->total_d = sm.total_d();
+    out->total_s = sm.total_s();
+    const auto t0 = Clock::now();
+    auto [plan, stats] = otpr::solve_ot(inst, eps);
+    out->solve_ms = ms_since(t0);
+    out->phases = stats.phases;
+    out->sum_ni = stats.sum_ni;
+    out->cost = plan.cost;
+    out->n_entries = static_cast<int64_t>(plan.entries.size());
+    const int64_t ne = out->n_entries < entry_cap ? out->n_entries : entry_cap;
+    for (int64_t i = 0; i < ne; ++i) {
+      ent_a[i] = plan.entries[i].a;
+      ent_b[i] = plan.entries[i].b;
+      ent_mass[i] = plan.entries[i].mass;
+    }
+    const int64_t nf = static_cast<int64_t>(stats.free_counts.size());
+    if (free_counts)
+      std::memcpy(free_counts, stats.free_counts.data(),
+                  static_cast<size_t>(nf < free_cap ? nf : free_cap) * 8);
+  });
+}
+
+// scale_and_round(inst, eps): copy counts (ot.cpp:109-128).
+int ref_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const double* nu,
+                        const double* cost, double eps, int64_t* d, int64_t* s,
+                        double* theta) {
+  return guarded([&] {
+    otpr::OTInstance inst;
+    inst.mu.assign(mu, mu + n_a);
+    inst.nu.assign(nu, nu + n_b);
+    inst.cost = otpr::Matrix<double>(n_a, n_b);
+    std::memcpy(inst.cost.data(), cost, sizeof(double) * size_t(n_a) * n_b);
+    const auto sm = otpr::scale_and_round(inst, eps);
+    std::memcpy(d, sm.d.data(), 8 * sm.d.size());
+    std::memcpy(s, sm.s.data(), 8 * sm.s.size());
+    *theta = sm.theta;
+  });
+}
+
+}  // extern "C"

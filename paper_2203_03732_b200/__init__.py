@@ -6,7 +6,8 @@ from .api import (  # noqa: F401
     AssignmentInstance, AssignmentOptions, DeviceError, DualState, FormatError, InputError,
     InvariantViolation, Matching, NumericalError, ParameterError, ScaledCosts, SolveStats, Solver,
     gen_uniform_square, get_solver, l1_cost, load_mnist_pair, matching_cost, points_cost,
-    scale_round_costs, scaled_floor, solve_assignment,
+    scale_round_costs, scaled_floor, solve_assignment, OTInstance, TransportPlan, ScaledMasses,
+    gen_random_ot_rational, scale_and_round, solve_ot,
 )
 
 __all__ = [
@@ -14,5 +15,6 @@ __all__ = [
     "InputError", "InvariantViolation", "Matching", "NumericalError", "ParameterError",
     "ScaledCosts", "SolveStats", "Solver", "gen_uniform_square", "get_solver", "l1_cost",
     "load_mnist_pair", "matching_cost", "points_cost", "scale_round_costs", "scaled_floor",
-    "solve_assignment",
+    "solve_assignment", "OTInstance", "TransportPlan", "ScaledMasses", "gen_random_ot_rational",
+    "scale_and_round", "solve_ot",
 ]

@@ -54,7 +54,8 @@ EXPORTS = [
     "otprg_solve_assignment", "otprg_prepare", "otprg_solve_prepared", "otprg_scale_round_costs",
     "otprg_uniform_square_points", "otprg_flush_l2", "otprg_begin", "otprg_step",
     "otprg_snapshot", "otprg_finish", "otprg_timer_start", "otprg_timer_stop",
-    "otprg_set_trace", "otprg_get_trace", "otprg_load_mnist_pair",
+    "otprg_set_trace", "otprg_get_trace", "otprg_load_mnist_pair", "otprg_solve_ot",
+    "otprg_ot_scale_and_round", "otprg_random_ot_rational",
 ]
 
 _lib = None
@@ -100,6 +101,10 @@ def lib() -> C.CDLL:
     L.otprg_get_trace.argtypes = [vp, vp, C.c_int64]
     L.otprg_load_mnist_pair.argtypes = [C.c_char_p, C.c_int32, C.c_uint64, vp, vp, C.c_char_p,
                                         C.c_int32]
+    L.otprg_solve_ot.argtypes = [vp, vp, vp]
+    L.otprg_ot_scale_and_round.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp,
+                                           C.POINTER(C.c_double)]
+    L.otprg_random_ot_rational.argtypes = [C.c_int32, C.c_int32, C.c_uint64, vp, vp, vp]
     _lib = L
     return L
 

@@ -488,3 +488,145 @@ def load_mnist_pair(path: str, n: int, seed: int) -> AssignmentInstance:
             raise FormatError(msg)
         raise InputError(msg)
     return AssignmentInstance(n, n, None, img_a=img_a, img_b=img_b, norm_factor=2.0, seed=seed)
+
+
+# ---- optimal transport (include/otpr/ot.hpp) -------------------------------
+@dataclass
+class OTInstance:
+    """ot.hpp:24-37: demand masses mu (A), supply masses nu (B), costs in [0,1]."""
+    mu: np.ndarray
+    nu: np.ndarray
+    cost: np.ndarray
+    norm_factor: float = 1.0
+    seed: int = 0
+
+    def n_a(self) -> int:
+        return len(self.mu)
+
+    def n_b(self) -> int:
+        return len(self.nu)
+
+    def renormalize(self) -> None:  # ot.cpp:91-100
+        self.mu = self.mu / self.mu.sum()
+        self.nu = self.nu / self.nu.sum()
+
+
+@dataclass
+class TransportPlan:
+    """core.hpp:150-162 (entries row-major)."""
+    a: np.ndarray
+    b: np.ndarray
+    mass: np.ndarray
+    cost: float = 0.0
+
+    def row_sums(self, n_a: int) -> np.ndarray:
+        out = np.zeros(n_a)
+        for a, m in zip(self.a, self.mass):
+            out[a] += m
+        return out
+
+    def col_sums(self, n_b: int) -> np.ndarray:
+        out = np.zeros(n_b)
+        for b, m in zip(self.b, self.mass):
+            out[b] += m
+        return out
+
+    def total_mass(self) -> float:
+        s = 0.0
+        for m in self.mass:
+            s += float(m)
+        return s
+
+
+@dataclass
+class ScaledMasses:
+    """ot.hpp:42-49."""
+    theta: float
+    d: np.ndarray
+    s: np.ndarray
+
+    def total_d(self) -> int:
+        return int(self.d.sum())
+
+    def total_s(self) -> int:
+        return int(self.s.sum())
+
+
+class _OTProblem(C.Structure):
+    _fields_ = [("n_a", C.c_int32), ("n_b", C.c_int32), ("eps", C.c_double),
+                ("mu", C.c_void_p), ("nu", C.c_void_p), ("cost", C.c_void_p),
+                ("flags", C.c_int32), ("pad", C.c_int32)]
+
+
+class _OTResult(C.Structure):
+    _fields_ = [("ent_a", C.c_void_p), ("ent_b", C.c_void_p), ("ent_mass", C.c_void_p),
+                ("entry_cap", C.c_int64), ("free_counts", C.c_void_p), ("free_cap", C.c_int64),
+                ("n_entries", C.c_int64), ("cost", C.c_double), ("phases", C.c_int64),
+                ("sum_ni", C.c_int64), ("full_match_termination", C.c_int32),
+                ("gpu_launches", C.c_int32), ("theta", C.c_double), ("total_d", C.c_int64),
+                ("total_s", C.c_int64), ("build_ms", C.c_double), ("loop_ms", C.c_double),
+                ("scan_ms", C.c_double), ("solve_ms", C.c_double), ("bytes_touched", C.c_int64)]
+
+
+def gen_random_ot_rational(n_a: int, n_b: int, seed: int) -> OTInstance:
+    """instances.cpp:159-191 (weights 1..50 over their total, u01 costs), renormalised."""
+    if n_a < 1 or n_b < 1:
+        raise ParameterError("gen_random_ot_rational: sides must be >= 1")
+    mu, nu = np.empty(n_a), np.empty(n_b)
+    cost = np.empty((n_a, n_b))
+    st = N.lib().otprg_random_ot_rational(n_a, n_b, seed, mu.ctypes.data, nu.ctypes.data,
+                                          cost.ctypes.data)
+    if st:
+        raise ParameterError("gen_random_ot_rational failed")
+    return OTInstance(mu, nu, cost, seed=seed)
+
+
+def scale_and_round(inst: OTInstance, eps: float) -> ScaledMasses:
+    """ot.cpp:109-128."""
+    mu = np.ascontiguousarray(inst.mu, np.float64)
+    nu = np.ascontiguousarray(inst.nu, np.float64)
+    d, s = np.empty(len(mu), np.int64), np.empty(len(nu), np.int64)
+    th = C.c_double()
+    st = N.lib().otprg_ot_scale_and_round(len(mu), len(nu), mu.ctypes.data, nu.ctypes.data, eps,
+                                          d.ctypes.data, s.ctypes.data, C.byref(th))
+    if st:
+        raise _STATUS_EXC.get(st, DeviceError)("scale_and_round failed")
+    return ScaledMasses(th.value, d, s)
+
+
+def solve_ot(inst: OTInstance, eps: float, device: int = 0):
+    """ot.hpp:161-163 / ot.cpp:705-732 -> (TransportPlan, SolveStats)."""
+    mu = np.ascontiguousarray(inst.mu, np.float64)
+    nu = np.ascontiguousarray(inst.nu, np.float64)
+    cost = np.ascontiguousarray(inst.cost, np.float64)
+    if cost.shape != (len(mu), len(nu)):
+        raise ParameterError("OT cost matrix dimensions do not match mass vectors")
+    solver = get_solver(device)
+    p = _OTProblem(len(mu), len(nu), float(eps), mu.ctypes.data, nu.ctypes.data, cost.ctypes.data,
+                   0, 0)
+    cap = 4 * (len(mu) + len(nu)) + 64
+    fcap = SolveStats.phase_bound(eps / 3.0) + 16 if 0.0 < eps < 1.0 else 16  # C ABI validates eps
+    ea, eb, em = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap)
+    fc = np.zeros(fcap, np.int64)
+    r = _OTResult()
+    r.ent_a, r.ent_b, r.ent_mass, r.entry_cap = ea.ctypes.data, eb.ctypes.data, em.ctypes.data, cap
+    r.free_counts, r.free_cap = fc.ctypes.data, fcap
+    st = solver._L.otprg_solve_ot(solver._ctx, C.byref(p), C.byref(r))
+    if st:
+        solver._raise(st)
+    if r.n_entries > cap:  # rerun with room for every entry
+        cap = int(r.n_entries)
+        ea, eb, em = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap)
+        r.ent_a, r.ent_b, r.ent_mass, r.entry_cap = ea.ctypes.data, eb.ctypes.data, em.ctypes.data, cap
+        st = solver._L.otprg_solve_ot(solver._ctx, C.byref(p), C.byref(r))
+        if st:
+            solver._raise(st)
+    ne = int(r.n_entries)
+    plan = TransportPlan(ea[:ne].copy(), eb[:ne].copy(), em[:ne].copy(), float(r.cost))
+    stats = SolveStats(phases=int(r.phases), free_counts=fc[: r.phases].copy(), sum_ni=int(r.sum_ni),
+                       full_match_termination=bool(r.full_match_termination),
+                       device=dict(theta=r.theta, total_d=int(r.total_d), total_s=int(r.total_s),
+                                   build_ms=r.build_ms, loop_ms=r.loop_ms, scan_ms=r.scan_ms,
+                                   solve_ms=r.solve_ms, bytes_touched=int(r.bytes_touched),
+                                   gpu_launches=int(r.gpu_launches)))
+    return plan, stats

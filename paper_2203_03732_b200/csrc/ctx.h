@@ -1,0 +1,88 @@
+// ctx.h — the otprg_ctx behind the C ABI (internal to libotprg.so).
+#pragma once
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/otprg.h"
+
+namespace otprg {
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// scaled_floor, core.cpp:26-32 (host copy).
+inline int64_t host_scaled_floor(double c, double eps) {
+  auto k = static_cast<int64_t>(std::floor(c / eps));
+  while (static_cast<double>(k + 1) * eps <= c) ++k;
+  while (k > 0 && static_cast<double>(k) * eps > c) --k;
+  return k;
+}
+
+}  // namespace otprg
+
+struct otprg_ctx {
+  using DevBuf = otprg::DevBuf;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  int num_sms = 0;
+  std::string err;
+
+  // prepared assignment problem
+  bool prepared = false;
+  int32_t n_a = 0, n_b = 0;  // original orientation
+  int32_t ia = 0, ib = 0;    // internal: ia >= ib
+  bool swapped = false;
+  int width = 1, lda = 0;
+  double eps = 0.0;
+  int32_t unit_floor = 0, unit_ceil = 0;
+  int cost_kind = 0;
+  const double* host_cost = nullptr;  // caller buffer (DENSE); valid until next prepare
+  std::vector<double> pts_a, pts_b;   // original orientation (POINTS2D)
+  std::vector<uint8_t> img_a, img_b;  // original orientation (L1_U8)
+  int img_dim = 0;
+  double build_ms = 0.0;
+  int build_launches = 0;
+
+  DevBuf kT, t, yb, ma, mb, holder, rowmin, lmeta, lent, lists, mps, fc, ctl, fa, fb;
+  DevBuf stage, pts, flush;
+  void* hpin = nullptr;  // pinned D2H staging
+  size_t hpin_n = 0;
+  cudaEvent_t timer[2] = {};
+  int64_t fc_cap = 0;
+  int loop_grid = 0;
+  bool smem_t = true;
+  bool begun = false, completed = false;
+  DevBuf trace;            // device timeline, 8 u64 per phase (see solve_kernels.cu)
+  uint32_t trace_cap = 0;  // 0 = tracing off
+
+  // optimal transport (ot_host.cpp): per-phase scan inputs / outputs
+  DevBuf ot_t, ot_req, ot_out;
+  void* ot_hpin = nullptr;
+  size_t ot_hpin_n = 0;
+};

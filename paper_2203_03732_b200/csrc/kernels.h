@@ -67,6 +67,12 @@ cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_
 cudaError_t launch_export_k(const void* kT, int n_ai, int n_bi, int lda, int width, bool swapped,
                             int32_t* k_out, cudaStream_t s);
 
+// OT admissible-cluster scan (ot_kernels.cu): per request (b, target, start)
+// the first K admissible (a, ci), encoded a*2+ci, and (count, resume).
+cudaError_t launch_ot_scan(const void* kT, int lda, int width, const void* t0, const void* t1,
+                           const int4* req, int nreq, int K, int32_t* out, int2* meta,
+                           cudaStream_t s);
+
 // Phase loop.
 cudaError_t launch_init_state(const SolveArgs& a, int n_a, int n_b, int lda, int width,
                               cudaStream_t s);

@@ -1,0 +1,729 @@
+// ot_host.cpp — optimal transport through the copy/cluster phase algorithm
+// (reference: solve_ot, src/ot.cpp:705-732; scale_and_round :109-128;
+// solve_copy_matching :418-637; plan_from_flow :639-703).
+//
+// Division of labour:
+//   device  rounding of the dense cost at eps/3 into kT (K1, cost_kernels.cu)
+//           and, every phase, the admissible-cluster scan of every free
+//           supply vertex's row (ot_kernels.cu) — the O(n^2) work;
+//   host    the per-phase claim step over the scanned candidate lists and
+//           the per-vertex cluster bookkeeping (O(n + claims) per phase),
+//           completion and plan_from_flow on the sparse flow.
+// The claim order is the reference's: supply vertices ascending, each
+// consuming admissible demand clusters ascending by a; within a cluster, free
+// copies first, then matched copies ascending by current partner.  All
+// floating-point operations of plan_from_flow run in the reference's order
+// on the nonzero entries only, so the plan's masses and cost are bit-equal.
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <random>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ctx.h"
+#include "kernels.h"
+
+namespace {
+
+using otprg::DevBuf;
+using otprg::host_scaled_floor;
+
+constexpr double kMassTolerance = 1e-9;  // ot.cpp:15
+// Admissible clusters returned per scan request.  A free supply vertex walks
+// past clusters already used up by lower b's, so the list must usually cover
+// its whole admissible set (~n / (3/eps) entries for uniform costs); a list
+// that runs out while the row has more is extended by a rescan.
+constexpr int kCand = 256;
+
+struct OtError {
+  int code;
+  std::string msg;
+};
+
+int64_t exact_floor(double x) {  // ot.cpp:17-22
+  auto f = static_cast<int64_t>(std::floor(x));
+  while (static_cast<double>(f + 1) <= x) ++f;
+  while (static_cast<double>(f) > x) --f;
+  return f;
+}
+
+int64_t exact_ceil(double x) {  // ot.cpp:24-29
+  auto c = static_cast<int64_t>(std::ceil(x));
+  while (static_cast<double>(c - 1) >= x) --c;
+  while (static_cast<double>(c) < x) ++c;
+  return c;
+}
+
+using Flow = std::vector<std::pair<int32_t, int64_t>>;  // (b, copies), ascending b
+
+struct DemandC {
+  int64_t y = 0, free = 0;
+  Flow flow;
+  int64_t matched() const {
+    int64_t t = 0;
+    for (const auto& e : flow) t += e.second;
+    return t;
+  }
+  int64_t count() const { return free + matched(); }
+};
+
+struct SupplyC {
+  int64_t y = 0, free = 0, matched = 0;
+  int64_t count() const { return free + matched; }
+};
+
+void flow_add(Flow& f, int32_t b, int64_t cnt) {
+  if (cnt == 0) return;
+  auto it = std::lower_bound(f.begin(), f.end(), b,
+                             [](const std::pair<int32_t, int64_t>& e, int32_t k) { return e.first < k; });
+  if (it != f.end() && it->first == b)
+    it->second += cnt;
+  else
+    f.insert(it, {b, cnt});
+}
+
+void flow_sub(Flow& f, int32_t b, int64_t cnt) {
+  auto it = std::lower_bound(f.begin(), f.end(), b,
+                             [](const std::pair<int32_t, int64_t>& e, int32_t k) { return e.first < k; });
+  if (it == f.end() || it->first != b || it->second < cnt)
+    throw OtError{OTPRG_INVARIANT, "cluster flow underflow while rematching"};
+  it->second -= cnt;
+  if (it->second == 0) f.erase(it);
+}
+
+DemandC& demand_at(std::vector<DemandC>& cs, int64_t y) {
+  for (DemandC& c : cs)
+    if (c.y == y) return c;
+  cs.push_back(DemandC{y, 0, {}});
+  return cs.back();
+}
+
+SupplyC& supply_at(std::vector<SupplyC>& cs, int64_t y) {
+  for (SupplyC& c : cs)
+    if (c.y == y) return c;
+  cs.push_back(SupplyC{y, 0, 0});
+  return cs.back();
+}
+
+// Merge equal duals, drop empty clusters, descending dual order (ot.cpp:362-383).
+void normalize_demand(std::vector<DemandC>& cs, int32_t a) {
+  std::sort(cs.begin(), cs.end(), [](const DemandC& x, const DemandC& y) { return x.y > y.y; });
+  std::vector<DemandC> out;
+  for (DemandC& c : cs) {
+    if (c.count() == 0) continue;
+    if (!out.empty() && out.back().y == c.y) {
+      out.back().free += c.free;
+      for (const auto& e : c.flow) flow_add(out.back().flow, e.first, e.second);
+    } else {
+      out.push_back(std::move(c));
+    }
+  }
+  cs = std::move(out);
+  if (cs.size() > 2)
+    throw OtError{OTPRG_INVARIANT, "third dual value among copies of demand vertex " + std::to_string(a)};
+}
+
+// Lift free copies to the vertex maximum, merge, drop empty (ot.cpp:385-414).
+void normalize_supply(std::vector<SupplyC>& cs, int32_t b) {
+  int64_t max_y = std::numeric_limits<int64_t>::min(), total_free = 0;
+  for (const SupplyC& c : cs) {
+    if (c.count() == 0) continue;
+    max_y = std::max(max_y, c.y);
+    total_free += c.free;
+  }
+  for (SupplyC& c : cs) c.free = 0;
+  if (total_free > 0) supply_at(cs, max_y).free = total_free;
+  std::sort(cs.begin(), cs.end(), [](const SupplyC& x, const SupplyC& y) { return x.y > y.y; });
+  std::vector<SupplyC> out;
+  for (const SupplyC& c : cs) {
+    if (c.count() == 0) continue;
+    if (!out.empty() && out.back().y == c.y) {
+      out.back().free += c.free;
+      out.back().matched += c.matched;
+    } else {
+      out.push_back(c);
+    }
+  }
+  cs = std::move(out);
+  if (cs.size() > 2)
+    throw OtError{OTPRG_INVARIANT, "third dual value among copies of supply vertex " + std::to_string(b)};
+}
+
+struct Claim {
+  int32_t a, ci, b;
+  int64_t take_free;
+  int64_t total;
+  size_t disp_begin, disp_end;  // range in the displaced array
+};
+
+// Per-phase consumption cursor of one demand cluster (the reference's
+// "avail" snapshot, ot.cpp:459-469, kept as an offset into free + flow).
+struct Cursor {
+  int32_t stamp = -1;
+  int64_t used = 0;   // copies already claimed this phase
+  size_t fidx = 0;    // first flow entry not fully consumed
+  int64_t foff = 0;   // copies consumed from flow[fidx]
+};
+
+struct Timer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double ms() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
+#define OT_CK(expr, what)                                                          \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      throw OtError{OTPRG_DEVICE, std::string(what) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+void validate_ot(const otprg_ot_problem* p) {  // OTInstance::validate, ot.cpp:62-89 (masses)
+  if (!p || p->n_a < 1 || p->n_b < 1)
+    throw OtError{OTPRG_PARAMETER, "OT instance needs at least one point per side"};
+  if (!p->mu || !p->nu || !p->cost) throw OtError{OTPRG_PARAMETER, "null instance pointer"};
+  double sum_mu = 0.0, sum_nu = 0.0;
+  for (int32_t a = 0; a < p->n_a; ++a) {
+    if (!(p->mu[a] >= 0.0)) throw OtError{OTPRG_PARAMETER, "negative or NaN demand mass"};
+    sum_mu += p->mu[a];
+  }
+  for (int32_t b = 0; b < p->n_b; ++b) {
+    if (!(p->nu[b] >= 0.0)) throw OtError{OTPRG_PARAMETER, "negative or NaN supply mass"};
+    sum_nu += p->nu[b];
+  }
+  if (std::abs(sum_mu - 1.0) > kMassTolerance || std::abs(sum_nu - 1.0) > kMassTolerance)
+    throw OtError{OTPRG_INPUT, "masses must each sum to 1 within 1e-9 (got " + std::to_string(sum_mu) +
+                                   " and " + std::to_string(sum_nu) + ")"};
+}
+
+struct ScaledMasses {
+  double theta = 0.0;
+  std::vector<int64_t> d, s;
+  int64_t total_d = 0, total_s = 0;
+};
+
+ScaledMasses scale_and_round(const otprg_ot_problem* p, double eps) {  // ot.cpp:109-128
+  if (!(eps > 0.0 && eps < 1.0)) throw OtError{OTPRG_PARAMETER, "eps must lie in (0, 1)"};
+  const auto n = static_cast<double>(std::max(p->n_a, p->n_b));
+  ScaledMasses sm;
+  sm.theta = 4.0 * n / eps;
+  if (!(sm.theta < 4.0e15))
+    throw OtError{OTPRG_PARAMETER, "theta = 4n/eps too large: copy counts overflow"};
+  sm.d.resize(p->n_a);
+  sm.s.resize(p->n_b);
+  for (int32_t a = 0; a < p->n_a; ++a) sm.total_d += (sm.d[a] = exact_ceil(p->mu[a] * sm.theta));
+  for (int32_t b = 0; b < p->n_b; ++b) sm.total_s += (sm.s[b] = exact_floor(p->nu[b] * sm.theta));
+  if (sm.total_s > sm.total_d)
+    throw OtError{OTPRG_INVARIANT, "scaled supplies exceed scaled demands"};
+  return sm;
+}
+
+class OtSolver {
+ public:
+  OtSolver(otprg_ctx* ctx, const otprg_ot_problem* p, otprg_ot_result* r) : ctx_(ctx), p_(p), r_(r) {}
+
+  void run() {
+    Timer total;
+    validate_ot(p_);
+    if (!(p_->eps > 0.0 && p_->eps < 1.0)) throw OtError{OTPRG_PARAMETER, "eps must lie in (0, 1)"};
+    eps_in_ = p_->eps / 3.0;  // ot.cpp:710
+    sm_ = scale_and_round(p_, eps_in_);
+    n_a_ = p_->n_a;
+    n_b_ = p_->n_b;
+    build_costs();
+    solve_copy_matching();
+    plan_from_flow();
+    r_->theta = sm_.theta;
+    r_->total_d = sm_.total_d;
+    r_->total_s = sm_.total_s;
+    r_->solve_ms = total.ms();
+  }
+
+ private:
+  otprg_ctx* ctx_;
+  const otprg_ot_problem* p_;
+  otprg_ot_result* r_;
+  double eps_in_ = 0.0;
+  ScaledMasses sm_;
+  int32_t n_a_ = 0, n_b_ = 0;
+  int width_ = 2, lda_ = 0;
+  std::vector<std::vector<DemandC>> dem_;
+  std::vector<std::vector<SupplyC>> sup_;
+  std::vector<std::vector<std::pair<int32_t, int64_t>>> flow_;  // final sparse flow per a
+
+  int64_t k_of(int32_t a, int32_t b) const {
+    return host_scaled_floor(p_->cost[static_cast<size_t>(a) * n_b_ + b], eps_in_);
+  }
+
+  // scale_round_costs(costs, eps/3) on the device (core.cpp:34-53), kT[b][a].
+  void build_costs() {
+    Timer t;
+    if (!(eps_in_ > 0.0 && eps_in_ < 1.0)) throw OtError{OTPRG_PARAMETER, "eps must lie in (0, 1)"};
+    const int64_t uf = host_scaled_floor(1.0, eps_in_);
+    if (uf + 4 > std::numeric_limits<int32_t>::max())
+      throw OtError{OTPRG_PARAMETER, "eps too small: 1/eps overflows the cost unit type"};
+    const int64_t uc = static_cast<double>(uf) * eps_in_ == 1.0 ? uf : uf + 1;
+    if (uc + 2 > 65533) throw OtError{OTPRG_PARAMETER, "eps too small for the device cost storage"};
+    width_ = uc + 2 <= 253 ? 1 : 2;
+    const int align = 512 / width_;
+    lda_ = (n_a_ + align - 1) / align * align;
+    OT_CK(cudaSetDevice(ctx_->device), "cudaSetDevice");
+    const size_t bytes = static_cast<size_t>(n_a_) * n_b_ * sizeof(double);
+    OT_CK(ctx_->stage.ensure(bytes), "alloc cost staging");
+    OT_CK(ctx_->kT.ensure(static_cast<size_t>(n_b_) * lda_ * width_), "alloc kT");
+    OT_CK(ctx_->ctl.ensure(sizeof(otprg::Ctl)), "alloc ctl");
+    OT_CK(cudaMemcpyAsync(ctx_->stage.p, p_->cost, bytes, cudaMemcpyHostToDevice, ctx_->stream),
+          "H2D cost");
+    OT_CK(cudaMemsetAsync(ctx_->ctl.p, 0, sizeof(otprg::Ctl), ctx_->stream), "memset");
+    int* status = &ctx_->ctl.as<otprg::Ctl>()->status;
+    OT_CK(otprg::launch_round_dense(ctx_->stage.as<double>(), n_a_, n_b_, false, eps_in_, ctx_->kT.p,
+                                    lda_, width_, status, ctx_->stream),
+          "round_dense launch");
+    int dstatus = 0;
+    OT_CK(cudaMemcpyAsync(&dstatus, status, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream),
+          "D2H status");
+    OT_CK(cudaStreamSynchronize(ctx_->stream), "cost build");
+    if (dstatus) throw OtError{OTPRG_PARAMETER, "OT cost entry outside [0,1]"};
+    launches_ += 1;
+    r_->build_ms = t.ms();
+    // per-phase scan buffers: t0/t1 (2 x lda) + requests + candidates
+    OT_CK(ctx_->ot_t.ensure(2 * static_cast<size_t>(lda_) * width_), "alloc t");
+    OT_CK(ctx_->ot_req.ensure(static_cast<size_t>(n_b_) * sizeof(int4)), "alloc req");
+    OT_CK(ctx_->ot_out.ensure(static_cast<size_t>(n_b_) * (kCand * 4 + sizeof(int2))), "alloc out");
+    const size_t hp = static_cast<size_t>(lda_) * 2 * width_ + static_cast<size_t>(n_b_) * sizeof(int4) +
+                      static_cast<size_t>(n_b_) * (kCand * 4 + sizeof(int2)) + 64;
+    if (ctx_->ot_hpin_n < hp) {
+      if (ctx_->ot_hpin) cudaFreeHost(ctx_->ot_hpin);
+      ctx_->ot_hpin = nullptr;
+      ctx_->ot_hpin_n = 0;
+      OT_CK(cudaMallocHost(&ctx_->ot_hpin, hp), "pinned staging");
+      ctx_->ot_hpin_n = hp;
+    }
+  }
+
+  int launches_ = 0;
+  int64_t scan_bytes_ = 0;
+
+  // Scan requests on the device; results land in cand / meta (host views).
+  void scan(const std::vector<int4>& reqs, std::vector<int32_t>& cand, std::vector<int2>& meta) {
+    const int nreq = static_cast<int>(reqs.size());
+    cand.resize(static_cast<size_t>(nreq) * kCand);
+    meta.resize(nreq);
+    if (nreq == 0) return;
+    char* hp = static_cast<char*>(ctx_->ot_hpin);
+    const size_t tbytes = static_cast<size_t>(lda_) * 2 * width_;
+    int4* hreq = reinterpret_cast<int4*>(hp + ((tbytes + 15) & ~15ull));
+    int32_t* hcand = reinterpret_cast<int32_t*>(hreq + n_b_);
+    int2* hmeta = reinterpret_cast<int2*>(hcand + static_cast<size_t>(n_b_) * kCand);
+    std::memcpy(hreq, reqs.data(), nreq * sizeof(int4));
+    OT_CK(cudaMemcpyAsync(ctx_->ot_req.p, hreq, nreq * sizeof(int4), cudaMemcpyHostToDevice,
+                          ctx_->stream), "H2D requests");
+    int32_t* dcand = ctx_->ot_out.as<int32_t>();
+    int2* dmeta = reinterpret_cast<int2*>(dcand + static_cast<size_t>(n_b_) * kCand);
+    const void* t0 = ctx_->ot_t.p;
+    const void* t1 = static_cast<const char*>(ctx_->ot_t.p) + static_cast<size_t>(lda_) * width_;
+    OT_CK(otprg::launch_ot_scan(ctx_->kT.p, lda_, width_, t0, t1, ctx_->ot_req.as<int4>(), nreq, kCand,
+                                dcand, dmeta, ctx_->stream), "ot_scan launch");
+    launches_ += 1;
+    OT_CK(cudaMemcpyAsync(hcand, dcand, static_cast<size_t>(nreq) * kCand * 4, cudaMemcpyDeviceToHost,
+                          ctx_->stream), "D2H candidates");
+    OT_CK(cudaMemcpyAsync(hmeta, dmeta, nreq * sizeof(int2), cudaMemcpyDeviceToHost, ctx_->stream),
+          "D2H meta");
+    OT_CK(cudaStreamSynchronize(ctx_->stream), "ot scan");
+    std::memcpy(cand.data(), hcand, static_cast<size_t>(nreq) * kCand * 4);
+    std::memcpy(meta.data(), hmeta, nreq * sizeof(int2));
+    scan_bytes_ += static_cast<int64_t>(nreq) * lda_ * width_;
+  }
+
+  // Cluster duals of every demand vertex to the device: t_ci = -y (type max if absent).
+  void upload_cluster_duals() {
+    char* hp = static_cast<char*>(ctx_->ot_hpin);
+    const uint32_t none = width_ == 1 ? 0xffu : 0xffffu;
+    auto put = [&](size_t i, uint32_t v) {
+      if (width_ == 1) reinterpret_cast<uint8_t*>(hp)[i] = static_cast<uint8_t>(v);
+      else reinterpret_cast<uint16_t*>(hp)[i] = static_cast<uint16_t>(v);
+    };
+    for (int32_t a = 0; a < lda_; ++a) {
+      uint32_t v0 = none, v1 = none;
+      if (a < n_a_) {
+        const auto& cs = dem_[a];
+        if (cs.size() >= 1) v0 = static_cast<uint32_t>(-cs[0].y);
+        if (cs.size() >= 2) v1 = static_cast<uint32_t>(-cs[1].y);
+      }
+      put(a, v0);
+      put(static_cast<size_t>(lda_) + a, v1);
+    }
+    OT_CK(cudaMemcpyAsync(ctx_->ot_t.p, hp, static_cast<size_t>(lda_) * 2 * width_,
+                          cudaMemcpyHostToDevice, ctx_->stream), "H2D cluster duals");
+  }
+
+  // solve_copy_matching (ot.cpp:418-637).
+  void solve_copy_matching() {
+    dem_.assign(n_a_, {});
+    sup_.assign(n_b_, {});
+    for (int32_t a = 0; a < n_a_; ++a)
+      if (sm_.d[a] > 0) dem_[a].push_back(DemandC{0, sm_.d[a], {}});
+    for (int32_t b = 0; b < n_b_; ++b)
+      if (sm_.s[b] > 0) sup_[b].push_back(SupplyC{1, sm_.s[b], 0});
+    const double threshold = eps_in_ * static_cast<double>(sm_.total_s);
+    const int64_t phase_cap =
+        static_cast<int64_t>(std::ceil((1.0 + 2.0 * eps_in_) / (eps_in_ * eps_in_))) + 8;
+
+    std::vector<std::array<Cursor, 2>> cur(n_a_);
+    std::vector<int64_t> matched_from_b(n_b_), remaining_free(n_b_), free_dual(n_b_);
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> freed_at(n_b_);
+    std::vector<int32_t> free_bs;
+    std::vector<int4> reqs;
+    std::vector<int32_t> cand;
+    std::vector<int2> meta;
+    std::vector<Claim> claims;
+    std::vector<std::pair<int32_t, int64_t>> displaced;
+    int64_t phases = 0, sum_ni = 0;
+    std::vector<int64_t> free_counts;
+    Timer loop_t;
+    double scan_ms = 0.0;
+
+    while (true) {
+      int64_t n_i = 0;
+      for (const auto& cs : sup_)
+        for (const SupplyC& c : cs) n_i += c.free;
+      if (static_cast<double>(n_i) <= threshold) {
+        r_->full_match_termination = (n_i == 0);
+        break;
+      }
+      const int32_t stamp = static_cast<int32_t>(phases);
+
+      // free supply vertices (ascending) and their free-copy duals
+      free_bs.clear();
+      reqs.clear();
+      for (int32_t b = 0; b < n_b_; ++b) {
+        int64_t free_b = 0, y_b = 0;
+        for (const SupplyC& c : sup_[b])
+          if (c.free > 0) {
+            free_b += c.free;
+            y_b = c.y;
+          }
+        remaining_free[b] = free_b;
+        free_dual[b] = y_b;
+        matched_from_b[b] = 0;
+        freed_at[b].clear();
+        if (free_b == 0) continue;
+        free_bs.push_back(b);
+        reqs.push_back(make_int4(b, static_cast<int>(y_b - 1), 0, 0));
+      }
+      Timer st;
+      upload_cluster_duals();
+      scan(reqs, cand, meta);
+      scan_ms += st.ms();
+
+      // claim step (ot.cpp:471-522): b ascending, admissible clusters ascending a
+      claims.clear();
+      displaced.clear();
+      std::vector<int32_t> more;
+      std::vector<int2> more_meta;
+      for (size_t q = 0; q < free_bs.size(); ++q) {
+        const int32_t b = free_bs[q];
+        int64_t remaining = remaining_free[b];
+        const int32_t* list = cand.data() + q * kCand;
+        int cnt = meta[q].x, resume = meta[q].y;
+        int idx = 0;
+        while (remaining > 0) {
+          if (idx == cnt) {
+            if (resume < 0) break;  // row exhausted
+            std::vector<int4> one{make_int4(b, static_cast<int>(free_dual[b] - 1), resume, 0)};
+            scan(one, more, more_meta);
+            list = more.data();
+            cnt = more_meta[0].x;
+            resume = more_meta[0].y;
+            idx = 0;
+            continue;
+          }
+          const int32_t code = list[idx++];
+          const int32_t a = code >> 1, ci = code & 1;
+          DemandC& c = dem_[a][ci];
+          Cursor& cu = cur[a][ci];
+          if (cu.stamp != stamp) cu = Cursor{stamp, 0, 0, 0};
+          const int64_t total = c.free + c.matched() - cu.used;
+          if (total == 0) continue;
+          const int64_t take = std::min(remaining, total);
+          Claim cl{a, ci, b, 0, take, displaced.size(), 0};
+          const int64_t free_left = std::max<int64_t>(0, c.free - cu.used);
+          cl.take_free = std::min(take, free_left);
+          int64_t rest = take - cl.take_free;
+          while (rest > 0) {  // matched copies ascending by partner
+            const auto& e = c.flow[cu.fidx];
+            const int64_t use = std::min(e.second - cu.foff, rest);
+            if (use > 0) displaced.emplace_back(e.first, use);
+            cu.foff += use;
+            rest -= use;
+            if (cu.foff == e.second) {
+              ++cu.fidx;
+              cu.foff = 0;
+            }
+          }
+          cu.used += take;
+          cl.disp_end = displaced.size();
+          claims.push_back(cl);
+          remaining -= take;
+        }
+        matched_from_b[b] = remaining_free[b] - remaining;
+        remaining_free[b] = remaining;
+      }
+
+      // supply side: claimed copies become matched at their dual, the
+      // phase's leftover free copies go up a unit (ot.cpp:540-553)
+      for (int32_t b : free_bs) {
+        for (SupplyC& c : sup_[b]) {
+          if (c.free == 0) continue;
+          c.free = 0;
+          c.matched += matched_from_b[b];
+        }
+        if (remaining_free[b] > 0) supply_at(sup_[b], free_dual[b] + 1).free += remaining_free[b];
+      }
+      // demand side + displaced supply copies (ot.cpp:556-578)
+      for (const Claim& cl : claims) {
+        DemandC& src = dem_[cl.a][cl.ci];
+        src.free -= cl.take_free;
+        for (size_t i = cl.disp_begin; i < cl.disp_end; ++i) {
+          const int32_t b_old = displaced[i].first;
+          const int64_t cnt = displaced[i].second;
+          flow_sub(src.flow, b_old, cnt);
+          const int64_t y_old = k_of(cl.a, b_old) - src.y;
+          bool found = false;
+          for (SupplyC& c : sup_[b_old])
+            if (c.y == y_old && c.matched >= cnt) {
+              c.matched -= cnt;
+              found = true;
+              break;
+            }
+          if (!found) throw OtError{OTPRG_INVARIANT, "displaced supply copy has no cluster"};
+          freed_at[b_old].emplace_back(y_old, cnt);
+        }
+        const int64_t dst_y = src.y - 1;
+        flow_add(demand_at(dem_[cl.a], dst_y).flow, cl.b, cl.total);
+      }
+      for (int32_t b = 0; b < n_b_; ++b) {
+        for (const auto& [y_old, cnt] : freed_at[b]) supply_at(sup_[b], y_old).free += cnt;
+        normalize_supply(sup_[b], b);
+      }
+      for (int32_t a = 0; a < n_a_; ++a) normalize_demand(dem_[a], a);
+
+      phases += 1;
+      free_counts.push_back(n_i);
+      sum_ni += n_i;
+      if (phases > phase_cap)
+        throw OtError{OTPRG_INVARIANT, "phase count exceeded the proven bound; solver state is corrupt"};
+    }
+    r_->phases = phases;
+    r_->sum_ni = sum_ni;
+    if (r_->free_counts && r_->free_cap > 0)
+      std::memcpy(r_->free_counts, free_counts.data(),
+                  static_cast<size_t>(std::min<int64_t>(phases, r_->free_cap)) * 8);
+    r_->loop_ms = loop_t.ms();
+    r_->scan_ms = scan_ms;
+    r_->bytes_touched = scan_bytes_;
+    r_->gpu_launches = launches_;
+
+    // flow matrix (sparse, per a ascending b) + completion (ot.cpp:615-635)
+    flow_.assign(n_a_, {});
+    for (int32_t a = 0; a < n_a_; ++a)
+      for (const DemandC& c : dem_[a])
+        for (const auto& e : c.flow) flow_add(flow_[a], e.first, e.second);
+    int32_t a_cursor = 0;
+    auto free_demand_of = [&](int32_t a) {
+      int64_t t = 0;
+      for (const DemandC& c : dem_[a]) t += c.free;
+      return t;
+    };
+    int64_t a_spare = n_a_ > 0 ? free_demand_of(0) : 0;
+    for (int32_t b = 0; b < n_b_; ++b) {
+      int64_t need = 0;
+      for (const SupplyC& c : sup_[b]) need += c.free;
+      while (need > 0) {
+        while (a_spare == 0) {
+          ++a_cursor;
+          if (a_cursor >= n_a_) throw OtError{OTPRG_INVARIANT, "completion ran out of demand copies"};
+          a_spare = free_demand_of(a_cursor);
+        }
+        const int64_t take = std::min(need, a_spare);
+        flow_add(flow_[a_cursor], b, take);
+        need -= take;
+        a_spare -= take;
+      }
+    }
+  }
+
+  // plan_from_flow (ot.cpp:639-703) on the nonzero entries, reference order.
+  void plan_from_flow() {
+    const double* mu = p_->mu;
+    const double* nu = p_->nu;
+    std::vector<std::vector<std::pair<int32_t, double>>> sigma(n_a_);
+    std::vector<double> row_mass(n_a_, 0.0), col_mass(n_b_, 0.0);
+    for (int32_t a = 0; a < n_a_; ++a) {
+      for (const auto& [b, f] : flow_[a]) {
+        if (f < 0) throw OtError{OTPRG_PARAMETER, "negative flow entry"};
+        if (f == 0) continue;
+        const double m = static_cast<double>(f) / sm_.theta;
+        sigma[a].emplace_back(b, m);
+        row_mass[a] += m;
+        col_mass[b] += m;
+      }
+    }
+    std::vector<double> pool(n_b_, 0.0);
+    for (int32_t b = 0; b < n_b_; ++b) pool[b] = std::max(0.0, nu[b] - col_mass[b]);
+    for (int32_t a = 0; a < n_a_; ++a) {
+      double excess = row_mass[a] - mu[a];
+      if (excess <= 0.0) continue;
+      for (auto& [b, s] : sigma[a]) {
+        if (!(excess > 0.0)) break;
+        if (s <= 0.0) continue;
+        const double take = std::min(s, excess);
+        s -= take;
+        pool[b] += take;
+        excess -= take;
+        row_mass[a] -= take;
+      }
+    }
+    // Ship each pool to demands with spare capacity, ascending a.  The
+    // reference rescans a = 0.. for every b; capacities only shrink here, so
+    // a vertex whose capacity is gone is unlinked from an ascending list and
+    // the visit order (hence every addition) is unchanged.
+    std::vector<int32_t> nxt(n_a_, -1);
+    int32_t head = -1, tail = -1;
+    for (int32_t a = 0; a < n_a_; ++a) {
+      if (!(mu[a] - row_mass[a] > 0.0)) continue;
+      if (tail < 0) head = a;
+      else nxt[tail] = a;
+      tail = a;
+    }
+    for (int32_t b = 0; b < n_b_; ++b) {
+      double rest = pool[b];
+      int32_t prev = -1, a = head;
+      while (a >= 0 && rest > 0.0) {
+        const double cap = mu[a] - row_mass[a];
+        if (cap <= 0.0) {  // never positive again: unlink
+          const int32_t n = nxt[a];
+          if (prev < 0) head = n;
+          else nxt[prev] = n;
+          a = n;
+          continue;
+        }
+        const double add = std::min(cap, rest);
+        auto& row = sigma[a];
+        auto it = std::lower_bound(row.begin(), row.end(), b,
+                                   [](const std::pair<int32_t, double>& e, int32_t k) { return e.first < k; });
+        if (it != row.end() && it->first == b) it->second += add;
+        else row.insert(it, {b, add});
+        row_mass[a] += add;
+        rest -= add;
+        prev = a;
+        a = nxt[a];
+      }
+      if (rest > kMassTolerance)
+        throw OtError{OTPRG_INVARIANT, "residual supply could not be placed"};
+    }
+    // entries row-major with sigma > 0, cost summed in that order
+    int64_t ne = 0;
+    double cost = 0.0;
+    for (int32_t a = 0; a < n_a_; ++a)
+      for (const auto& [b, s] : sigma[a]) {
+        if (!(s > 0.0)) continue;
+        if (ne < r_->entry_cap) {
+          r_->ent_a[ne] = a;
+          r_->ent_b[ne] = b;
+          r_->ent_mass[ne] = s;
+        }
+        ++ne;
+        cost += s * p_->cost[static_cast<size_t>(a) * n_b_ + b];
+      }
+    r_->n_entries = ne;
+    r_->cost = cost;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int otprg_ot_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const double* nu,
+                             double eps, int64_t* d, int64_t* s, double* theta) {
+  otprg_ot_problem p{};
+  p.n_a = n_a;
+  p.n_b = n_b;
+  p.mu = mu;
+  p.nu = nu;
+  p.cost = mu;  // masses only: the cost is not inspected here
+  try {
+    validate_ot(&p);
+    const ScaledMasses sm = scale_and_round(&p, eps);
+    std::memcpy(d, sm.d.data(), sm.d.size() * 8);
+    std::memcpy(s, sm.s.data(), sm.s.size() * 8);
+    *theta = sm.theta;
+    return OTPRG_OK;
+  } catch (const OtError& e) {
+    return e.code;
+  }
+}
+
+int otprg_solve_ot(otprg_ctx* ctx, const otprg_ot_problem* prob, otprg_ot_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!res || (!res->ent_a && res->entry_cap > 0)) {
+    ctx->err = "result buffers are null";
+    return OTPRG_PARAMETER;
+  }
+  try {
+    OtSolver(ctx, prob, res).run();
+    return OTPRG_OK;
+  } catch (const OtError& e) {
+    ctx->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return OTPRG_DEVICE;
+  }
+}
+
+int otprg_random_ot_rational(int32_t n_a, int32_t n_b, uint64_t seed, double* mu, double* nu,
+                             double* cost) {
+  if (n_a < 1 || n_b < 1 || !mu || !nu || !cost) return OTPRG_PARAMETER;
+  auto splitmix64 = [](uint64_t x) {  // instances.cpp:41-46
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+  };
+  std::mt19937_64 rma(splitmix64(seed ^ 0x8BB84B93962EACC9ULL));
+  std::mt19937_64 rmb(splitmix64(seed ^ 0x2545F4914F6CDD1DULL));
+  std::mt19937_64 rc(splitmix64(seed));
+  auto bounded = [](std::mt19937_64& r, uint64_t m) {  // instances.cpp:25-32
+    const uint64_t limit = ~uint64_t{0} - (~uint64_t{0}) % m;
+    uint64_t x;
+    do {
+      x = r();
+    } while (x >= limit);
+    return x % m;
+  };
+  // gen_random_ot_rational (instances.cpp:159-191) + OTInstance::renormalize (ot.cpp:91-100)
+  std::vector<int64_t> wa(n_a), wb(n_b);
+  int64_t ta = 0, tb = 0;
+  for (auto& w : wa) ta += (w = static_cast<int64_t>(bounded(rma, 50)) + 1);
+  for (auto& w : wb) tb += (w = static_cast<int64_t>(bounded(rmb, 50)) + 1);
+  for (int32_t a = 0; a < n_a; ++a) mu[a] = static_cast<double>(wa[a]) / static_cast<double>(ta);
+  for (int32_t b = 0; b < n_b; ++b) nu[b] = static_cast<double>(wb[b]) / static_cast<double>(tb);
+  for (size_t i = 0; i < static_cast<size_t>(n_a) * n_b; ++i)
+    cost[i] = static_cast<double>(rc() >> 11) * 0x1.0p-53;
+  double sum_mu = 0.0, sum_nu = 0.0;
+  for (int32_t a = 0; a < n_a; ++a) sum_mu += mu[a];
+  for (int32_t b = 0; b < n_b; ++b) sum_nu += nu[b];
+  for (int32_t a = 0; a < n_a; ++a) mu[a] /= sum_mu;
+  for (int32_t b = 0; b < n_b; ++b) nu[b] /= sum_nu;
+  return OTPRG_OK;
+}
+
+}  // extern "C"

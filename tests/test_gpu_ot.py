@@ -1,0 +1,93 @@
+"""OT (config 5) on the GPU through the C ABI: otprg_solve_ot vs the
+unmodified reference's otpr::solve_ot (tests/golden/ot_pins.json, made by
+tests/golden/make_golden_ot.py).  Bar: identical plan (entries, masses bit
+for bit), identical cost bits, phases, free_counts and copy totals.
+Structure follows tests/test_ot.cpp."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+otprg = pytest.importorskip("paper_2203_03732_b200")
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ot_pins.json")
+KEYS = ("phases", "sum_ni", "cost_hex", "theta_hex", "total_d", "total_s", "n_entries", "fnv_a",
+        "fnv_b", "fnv_mass", "fnv_free")
+
+
+@pytest.fixture(scope="module")
+def pins():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+def _pins(plan, stats):
+    from oracle.pyoracle import fnv1a64
+    return {"phases": stats.phases, "sum_ni": stats.sum_ni, "cost_hex": float(plan.cost).hex(),
+            "theta_hex": float(stats.device["theta"]).hex(), "total_d": stats.device["total_d"],
+            "total_s": stats.device["total_s"], "n_entries": len(plan.a),
+            "fnv_a": "%016x" % fnv1a64(plan.a.astype(np.int32)),
+            "fnv_b": "%016x" % fnv1a64(plan.b.astype(np.int32)),
+            "fnv_mass": "%016x" % fnv1a64(plan.mass.astype(np.float64)),
+            "fnv_free": "%016x" % fnv1a64(np.asarray(stats.free_counts, np.int64))}
+
+
+def _check(key, w, plan, stats):
+    got = _pins(plan, stats)
+    bad = {k: (got[k], w[k]) for k in KEYS if got[k] != w[k]}
+    assert not bad, f"{key}: {bad}"
+
+
+def test_micro_instances(pins):
+    for key, w in sorted(pins.items()):
+        if w["kind"] != "micro":
+            continue
+        inst = otprg.OTInstance(np.array(w["mu"]), np.array(w["nu"]), np.array(w["cost"]))
+        plan, stats = otprg.solve_ot(inst, w["eps"])
+        _check(key, w, plan, stats)
+
+
+def test_one_by_one_ships_everything():  # test_ot.cpp:90-97
+    inst = otprg.OTInstance(np.array([1.0]), np.array([1.0]), np.array([[0.2]]))
+    plan, _ = otprg.solve_ot(inst, 0.1)
+    assert abs(plan.total_mass() - 1.0) <= 1e-12 and abs(plan.cost - 0.2) <= 1e-12
+
+
+def test_rational_instances_match_reference(pins):
+    keys = sorted(k for k, w in pins.items() if w["kind"] == "rational" and w["n_a"] * w["n_b"] <= 2_000_000)
+    assert keys
+    for key in keys:
+        w = pins[key]
+        inst = otprg.gen_random_ot_rational(w["n_a"], w["n_b"], w["seed"])
+        plan, stats = otprg.solve_ot(inst, w["eps"])
+        _check(key, w, plan, stats)
+
+
+def test_rational_5k(pins):
+    key = "ot_rational_5000x5000_s1_eps0.01"
+    w = pins[key]
+    inst = otprg.gen_random_ot_rational(5000, 5000, 1)
+    plan, stats = otprg.solve_ot(inst, 0.01)
+    _check(key, w, plan, stats)
+
+
+def test_config5_n20k(pins):
+    key = "ot_rational_20000x20000_s1_eps0.01"
+    w = pins[key]
+    inst = otprg.gen_random_ot_rational(20000, 20000, 1)
+    plan, stats = otprg.solve_ot(inst, 0.01)
+    _check(key, w, plan, stats)
+
+
+def test_validation_errors():  # test_ot.cpp:127-135
+    good = otprg.OTInstance(np.array([1.0]), np.array([1.0]), np.array([[0.2]]))
+    for eps in (0.0, 1.0):
+        with pytest.raises(otprg.ParameterError):
+            otprg.solve_ot(good, eps)
+    bad = otprg.OTInstance(np.array([1.0]), np.array([0.9]), np.array([[0.2]]))
+    with pytest.raises(otprg.InputError):
+        otprg.solve_ot(bad, 0.1)
+    with pytest.raises(otprg.ParameterError):
+        otprg.solve_ot(otprg.OTInstance(np.array([1.0]), np.array([1.0]), np.array([[1.5]])), 0.1)
