@@ -47,6 +47,21 @@ def test_struct_layouts_match_header(lib):
 
     assert fields("otprg_problem") == [f for f, _ in _native.Problem._fields_]
     assert fields("otprg_result") == [f for f, _ in _native.Result._fields_]
+    from paper_2203_03732_b200 import api
+
+    def flat(struct):  # "int32_t n_a, n_b;" declares two fields
+        body = re.search(r"typedef struct " + struct + r" \{(.*?)\} " + struct, src, re.S).group(1)
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        out = []
+        for decl in body.split(";"):
+            decl = decl.strip()
+            if not decl:
+                continue
+            out += re.findall(r"(\w+)\s*(?=,|$)", decl)
+        return out
+
+    assert flat("otprg_ot_problem") == [f for f, _ in api._OTProblem._fields_]
+    assert flat("otprg_ot_result") == [f for f, _ in api._OTResult._fields_]
 
 
 def test_scaled_floor_matches_oracle(lib, oracle):
