@@ -49,9 +49,13 @@ namespace otprg {
 namespace {
 
 #ifndef OTPRG_BLOCK
-#define OTPRG_BLOCK 768
+#define OTPRG_BLOCK 512  // 16 warps/SM: 128 registers, no spills (768/1024 spill)
 #endif
 constexpr int kBlock = OTPRG_BLOCK;
+#ifndef OTPRG_TEAMS
+#define OTPRG_TEAMS 1
+#endif
+constexpr bool kTeams = OTPRG_TEAMS != 0;  // multi-warp rows in small phases
 constexpr int kUnroll = 4;       // 128-bit loads in flight per lane (global t)
 #ifndef OTPRG_UNROLL_SMEM
 #define OTPRG_UNROLL_SMEM 8
@@ -87,14 +91,51 @@ __device__ __forceinline__ uint32_t pick_word(int i, uint32_t w0, uint32_t w1, u
   return q < 2 ? (q == 0 ? w0 : w1) : (q == 2 ? w2 : w3);
 }
 
-// First admissible a >= start in one kT row, or -1.  The warp streams the
-// row in 32 lanes x 16 B x kUnroll chunks (coalesced 128-bit loads, 4 in
-// flight per lane).  track_min folds min_a (k + t) into mnw; lb appends the
-// low-set entries at positions <= the returned hit.
+// A team of `size` consecutive warps of one block that works on one proposer
+// chain together (used when a phase has few proposers, so each row scan is
+// split across warps).  size == 1 is the plain warp-per-proposer mode.
+struct Team {
+  int size;                  // 1, 2, 4 or 8 warps
+  int rank;                  // warp index within the team
+  unsigned bar;              // named barrier id (1..15) when size > 1
+  unsigned long long* slot;  // shared-memory broadcast area (>= 9 words)
+};
+
+__device__ __forceinline__ void team_sync(const Team& tm) {
+  if (tm.size > 1) asm volatile("bar.sync %0, %1;" ::"r"(tm.bar), "r"(tm.size * 32) : "memory");
+}
+
+// value of the team leader (rank 0, lane 0), everywhere in the team
+__device__ __forceinline__ unsigned long long team_bcast(const Team& tm, unsigned long long v,
+                                                         int lane) {
+  if (tm.size == 1) return __shfl_sync(kFull, v, 0);
+  if (tm.rank == 0 && lane == 0) tm.slot[0] = v;
+  team_sync(tm);
+  const unsigned long long r = tm.slot[0];
+  team_sync(tm);
+  return r;
+}
+
+// min over the team of a warp-uniform value
+__device__ __forceinline__ int team_min(const Team& tm, int v, int lane) {
+  if (tm.size == 1) return v;
+  if (lane == 0) tm.slot[1 + tm.rank] = (unsigned long long)(unsigned)v;
+  team_sync(tm);
+  int m = INT_MAX;
+  for (int r = 0; r < tm.size; ++r) m = min(m, (int)(unsigned)tm.slot[1 + r]);
+  team_sync(tm);
+  return m;
+}
+
+// First admissible a >= start in one kT row, or -1.  Each warp streams its
+// part of the row in 32 lanes x 16 B x kU chunks (coalesced 128-bit loads,
+// kU in flight per lane); a team of warps covers consecutive chunks and
+// agrees on the first hit per step.  track_min folds min_a (k + t) into mnw;
+// lb (warp mode only) appends the low-set entries at positions <= the hit.
 template <typename T, bool kSmem>
 __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tvec, int lda,
                                          int start, uint32_t target, bool track_min,
-                                         uint32_t& mnw, LowBuild& lb, int lane,
+                                         uint32_t& mnw, LowBuild& lb, int lane, const Team& tm,
                                          unsigned long long& bytes) {
   using S = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
@@ -103,7 +144,10 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
   const uint4* tv = reinterpret_cast<const uint4*>(tvec);
   const int nv = lda / kEpv;  // multiple of 32
   constexpr int kU = kSmem ? kUnrollSmem : kUnroll;
-  for (int v = (start / kEpv) & ~31; v < nv; v += 32 * kU) {
+  const int tstride = tm.size * 32 * kU;
+  for (int vt = (start / kEpv) & ~31; vt < nv; vt += tstride) {
+    const int v = vt + tm.rank * 32 * kU;  // this warp's chunk of the team step
+    int first = INT_MAX;
     // kT loads for the whole chunk are issued first (kU in flight per lane);
     // t comes from shared memory at use (or is preloaded when it is global).
     uint4 kr[kU], tr[kSmem ? 1 : kU];
@@ -118,7 +162,7 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
         if constexpr (!kSmem) tr[j] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
-    if (lane == 0) bytes += 16ull * (unsigned long long)min(nv - v, 32 * kU);
+    if (lane == 0 && v < nv) bytes += 16ull * (unsigned long long)min(nv - v, 32 * kU);
 #pragma unroll
     for (int j = 0; j < kU; ++j) {
       const int vi = v + j * 32 + lane;
@@ -184,8 +228,13 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
           }
         }
       }
-      if (hit != INT_MAX) return hit;
+      if (hit != INT_MAX) {
+        first = hit;
+        break;
+      }
     }
+    const int h = team_min(tm, first, lane);
+    if (h != INT_MAX) return h;
   }
   return -1;
 }
@@ -205,9 +254,11 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
                                           const T* tp, int lda, uint32_t phase, uint32_t tmax,
                                           int lane, unsigned long long& bytes,
                                           unsigned long long& steps, unsigned long long& walks,
-                                          unsigned* s_stat, unsigned long long* acc) {
+                                          unsigned* s_stat, unsigned long long* acc,
+                                          const Team& tm) {
+  const bool lead = lane == 0 && tm.rank == 0;  // performs the chain's global side effects
 #define OTPRG_STAT(k) \
-  if (lane == 0) atomicAdd(&s_stat[k], 1u)
+  if (lead) atomicAdd(&s_stat[k], 1u)
   OTPRG_STAT(0);
   using S = Simd<T>;
   Ctl* ctl = A.ctl;
@@ -235,15 +286,17 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     if ((uint32_t)__ldcg(rowmin + b) > target) {
       skip = true;  // row min too high: no admissible edge (min only grows)
       OTPRG_STAT(6);
-    } else {       // (re)build the low set with a full scan from position 0
-      meta = make_int4((int)(target + kLowLevels), 0, 0, 0);
+    } else {  // full scan from position 0 (rebuilding the low set in warp mode)
       OTPRG_STAT(5);
-      lb.on = true;
-      lb.cnt = 0;
-      lb.up_rep = S::rep(target + kLowLevels);
-      lb.ent = A.lent + (size_t)b * kLowCap;
       track_min = true;
-      dirty = true;
+      if (tm.size == 1) {
+        meta = make_int4((int)(target + kLowLevels), 0, 0, 0);
+        lb.on = true;
+        lb.cnt = 0;
+        lb.up_rep = S::rep(target + kLowLevels);
+        lb.ent = A.lent + (size_t)b * kLowCap;
+        dirty = true;
+      }
     }
   }
   bool scanning = !walk && !skip;
@@ -255,7 +308,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       const uint32_t kv = (uint32_t)(ent >> 32);
       const bool ok = lane < meta.z && pos >= start && kv + (uint32_t)tp[pos] == target;
       const unsigned bal = __ballot_sync(kFull, ok);
-      if (lane == 0) ++walks;
+      if (lead) ++walks;
       if (bal) {
         a = __shfl_sync(kFull, pos, __ffs(bal) - 1);
         OTPRG_STAT(2);
@@ -266,7 +319,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
         walk = false;
         scanning = true;
         start = max(start, meta.y);
-        if (meta.z < kLowCap && start == meta.y) {  // extend the cache
+        if (tm.size == 1 && meta.z < kLowCap && start == meta.y) {  // extend the cache
           lb.on = true;
           lb.cnt = meta.z;
           lb.up_rep = S::rep((uint32_t)meta.x);
@@ -278,16 +331,16 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     if (scanning) {
       const unsigned long long ts0 = acc ? globaltimer() : 0;
       a = warp_scan<T, kSmem>(kT + (size_t)b * lda, tp, lda, start, target, track_min, mnw, lb,
-                              lane, bytes);
+                              lane, tm, bytes);
       if (acc) acc[0] += globaltimer() - ts0;
-      if (lane == 0) ++steps;
+      if (lead) ++steps;
       if (dirty) {
         meta.z = lb.cnt;
         meta.y = lb.full_pos >= 0 ? lb.full_pos + 1 : (a >= 0 ? a + 1 : lda);
         if (lb.full_pos >= 0) lb.on = false;
       }
 #ifdef OTPRG_DEBUG_SCAN
-      if (lane == 0) {  // serial re-check of the warp scan
+      if (lead) {  // serial re-check of the warp scan
         const T* row = kT + (size_t)b * lda;
         const int hi = a < 0 ? lda : a;
         for (int x = start; x < hi; ++x)
@@ -301,8 +354,8 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     if (a < 0) {
       // b stays free this phase: Y(b) += 1 (apply_phase :233-235).
       uint32_t m = 0;
-      if (track_min) m = __reduce_min_sync(kFull, S::hmin(mnw));
-      if (lane == 0) {
+      if (track_min) m = (uint32_t)team_min(tm, (int)__reduce_min_sync(kFull, S::hmin(mnw)), lane);
+      if (lead) {
         if (track_min) rowmin[b] = (T)m;
         if (fresh && dirty) A.lmeta[b] = meta;
         if (yb + 1 > tmax) report(ctl, 11, (int)phase, b, (int)yb);
@@ -317,19 +370,19 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     unsigned long long old = 0;
     OTPRG_STAT(7);
     const unsigned long long ta0 = acc ? globaltimer() : 0;
-    if (lane == 0) old = atomicMin(H + a, key);
-    old = __shfl_sync(kFull, old, 0);
+    if (lead) old = atomicMin(H + a, key);
+    old = team_bcast(tm, old, lane);
     if (acc) acc[1] += globaltimer() - ta0;
     const uint32_t old_tag = (uint32_t)(old >> 32);
 #ifdef OTPRG_DEBUG_SCAN
-    if (lane == 0 && old_tag < cur_tag)  // key from a later phase
+    if (lead && old_tag < cur_tag)  // key from a later phase
       report(ctl, 13, (int)phase, b, a, (int)~old_tag, (int)(uint32_t)old);
 #endif
     if (old < key) {  // a is held by a lower b of this phase: next candidate
       start = a + 1;
       continue;
     }
-    if (lane == 0 && fresh && dirty) A.lmeta[b] = meta;
+    if (lead && fresh && dirty) A.lmeta[b] = meta;
     if (old_tag == cur_tag) {  // displaced b2 continues after a (plain scan)
       b = (int)(uint32_t)old;
       OTPRG_STAT(1);
@@ -344,7 +397,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       lb.on = false;
       continue;
     }
-    if (lane == 0) {
+    if (lead) {
       // a is taken for the first time this phase: its partner before this
       // phase is displaced (it is freed by apply_phase).  If a was matched in
       // the previous phase, that partner is the previous phase's winner (the
@@ -387,9 +440,6 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   unsigned bar_target = phase * kBarriers * gridDim.x;
   const int warps_per_block = blockDim.x >> 5;
   const int total_warps = gridDim.x * warps_per_block;
-  // static proposer slot, striped across blocks so small phases spread over
-  // all SMs (slot i -> block i % grid, warp i / grid)
-  const int gwarp = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gthreads = gridDim.x * blockDim.x;
 
@@ -400,6 +450,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = __ldcg(src + i);
   }
   __shared__ int s_ctl[4];
+  __shared__ unsigned long long s_team[kBlock / 32][10];  // team broadcast slots
   __shared__ unsigned s_stat[8];
   if (threadIdx.x < 8) s_stat[threadIdx.x] = 0;
   bool first = true;
@@ -512,18 +563,31 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     P.cnt_out = &ctl->cnt[r_cur];
     P.mp_cnt_out = &ctl->mp_cnt[r_cur];
     P.exh_out = &ctl->exh[r_cur];
-    // First proposer of every warp is static (no contended grab when
-    // n_i <= #warps); the rest are grabbed from a counter.
-    int i = gwarp;
+    // Team size for this phase: few proposers -> several warps per row
+    // (uniform over the grid since n is).  First proposer of every team is
+    // static, striped across blocks; the rest are grabbed from a counter.
+    int tsize = 1;
+    if (kTeams) {
+      if (n * 8 <= total_warps) tsize = 8;
+      else if (n * 4 <= total_warps) tsize = 4;
+      else if (n * 2 <= total_warps) tsize = 2;
+    }
+    const int wib = threadIdx.x >> 5;
+    const int tib = wib / tsize;  // team index in the block
+    Team tm{tsize, wib % tsize, 1u + (unsigned)tib, s_team[tib]};
+    const int teams_per_block = warps_per_block / tsize;
+    const int total_teams = gridDim.x * teams_per_block;
+    int i = tib * (int)gridDim.x + (int)blockIdx.x;
     unsigned long long acc[2] = {0ull, 0ull};
     const unsigned long long tp0 = tr ? globaltimer() : 0;
     const bool had_work = i < n;
     while (i < n) {
       const int b = __ldcg(list_in + i);
       run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
-                          tr ? acc : nullptr);
-      if (lane == 0) i = total_warps + atomicAdd(&ctl->work[r_cur], 1);
-      i = __shfl_sync(kFull, i, 0);
+                          tr ? acc : nullptr, tm);
+      unsigned long long nx = 0;
+      if (lane == 0 && tm.rank == 0) nx = (unsigned long long)(total_teams + atomicAdd(&ctl->work[r_cur], 1));
+      i = (int)team_bcast(tm, nx, lane);
     }
     if (tr && had_work && lane == 0) {  // slowest warp: scan / atomic / total ns
       atomicMax(tr + 1, acc[0]);

@@ -3,7 +3,7 @@ import sys
 sys.path.insert(0, ".")
 import paper_2203_03732_b200 as otprg  # noqa: E402
 
-storage = sys.argv[1] if len(sys.argv) > 1 else "u8"
+storage = sys.argv[1] if len(sys.argv) > 1 else "u16"
 S = otprg.Solver(0)
 S.prepare(otprg.gen_uniform_square(10000, 1), 0.01, storage)
 for _ in range(3):
