@@ -227,11 +227,10 @@ int otprg_random_ot_rational(int32_t n_a, int32_t n_b, uint64_t seed, double* mu
 /* Writes a buffer larger than L2 on the context's stream (benchmark hygiene). */
 int otprg_flush_l2(otprg_ctx* ctx);
 
-/* Device timeline (tracing): when enabled, every phase-loop phase records 8
- * u64 (%globaltimer ns) — phase start, t staged, last/first block done with
- * the proposal step (first stored as ~t), after barrier 1, last block done
- * with apply, after barrier 2, n_i — for up to max_phases phases (0 = off).
- * otprg_get_trace copies them out (max_phases * 8 u64). */
+/* Device timeline (tracing): when enabled, every phase-loop phase records 16
+ * u64 (%globaltimer ns) per phase — see solve_kernels.cu for the slot map —
+ * for up to max_phases phases (0 = off).  otprg_get_trace copies them out
+ * (max_phases * 16 u64). */
 int otprg_set_trace(otprg_ctx* ctx, int64_t max_phases);
 int otprg_get_trace(otprg_ctx* ctx, uint64_t* out, int64_t max_phases);
 

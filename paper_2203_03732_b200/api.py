@@ -353,8 +353,8 @@ class Solver:
             self._raise(st)
 
     def get_trace(self, phases: int) -> np.ndarray:
-        """(phases, 8) uint64 device timeline; see include/otprg.h."""
-        out = np.zeros((phases, 8), np.uint64)
+        """(phases, 16) uint64 device timeline; see include/otprg.h."""
+        out = np.zeros((phases, 16), np.uint64)
         st = self._L.otprg_get_trace(self._ctx, out.ctypes.data, phases)
         if st:
             self._raise(st)

@@ -40,7 +40,7 @@ struct Ctl {
   unsigned long long stat[8];
   // grid barrier (monotone arrival count)
   unsigned int bar_count;
-  unsigned int pad1;
+  unsigned int bar_base;  // bar_count at the start of the next launch (written at exit)
   int32_t err[8];       // details of the first failure (written by its reporter only)
 };
 

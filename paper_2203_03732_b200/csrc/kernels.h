@@ -18,6 +18,7 @@ namespace otprg {
 #define OTPRG_LOWLEVELS 2
 #endif
 constexpr int kLowCap = OTPRG_LOWCAP;        // <= 32 (one entry per lane)
+constexpr int kTraceSlots = 16;  // u64 timeline slots per phase (see solve_kernels.cu)
 constexpr int kLowLevels = OTPRG_LOWLEVELS;  // upto = target + kLowLevels when (re)built
 
 // Device state of one prepared assignment problem, in the solver's internal
@@ -41,7 +42,7 @@ struct SolveArgs {
   int64_t* free_counts;         // [phase_cap + 1]
   Ctl* ctl;
   uint32_t max_phase;           // run phases up to and including this one
-  // Optional device timeline (%globaltimer ns), 8 u64 per phase, indexed by
+  // Optional device timeline (%globaltimer ns), kTraceSlots u64 per phase, indexed by
   // phase - 1; nullptr disables tracing.
   unsigned long long* trace;
   uint32_t trace_cap;           // phases the trace buffer holds

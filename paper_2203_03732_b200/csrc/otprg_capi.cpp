@@ -268,7 +268,7 @@ int do_begin(otprg_ctx* ctx) {
   CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->stream),
      "init launch");
   if (ctx->trace_cap)
-    CK(cudaMemsetAsync(ctx->trace.p, 0, ctx->trace_cap * 64ull, ctx->stream), "trace reset");
+    CK(cudaMemsetAsync(ctx->trace.p, 0, ctx->trace_cap * 8ull * otprg::kTraceSlots, ctx->stream), "trace reset");
   ctx->begun = true;
   ctx->completed = false;
   return OTPRG_OK;
@@ -656,7 +656,7 @@ int otprg_set_trace(otprg_ctx* ctx, int64_t max_phases) {
   }
   const uint32_t cap = static_cast<uint32_t>(std::min<int64_t>(max_phases, 1 << 22));
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-  CK(ctx->trace.ensure(cap * 64ull), "alloc trace");
+  CK(ctx->trace.ensure(cap * 8ull * otprg::kTraceSlots), "alloc trace");
   ctx->trace_cap = cap;
   return OTPRG_OK;
 }
@@ -665,7 +665,7 @@ int otprg_get_trace(otprg_ctx* ctx, uint64_t* out, int64_t max_phases) {
   if (!ctx || !out) return OTPRG_PARAMETER;
   if (!ctx->trace_cap) return fail(ctx, OTPRG_PARAMETER, "tracing is off");
   const int64_t n = std::min<int64_t>(max_phases, ctx->trace_cap);
-  CK(cudaMemcpyAsync(out, ctx->trace.p, n * 64, cudaMemcpyDeviceToHost, ctx->stream), "D2H trace");
+  CK(cudaMemcpyAsync(out, ctx->trace.p, n * 8 * otprg::kTraceSlots, cudaMemcpyDeviceToHost, ctx->stream), "D2H trace");
   CK(cudaStreamSynchronize(ctx->stream), "trace");
   return OTPRG_OK;
 }

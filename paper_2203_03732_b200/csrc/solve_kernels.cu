@@ -56,6 +56,10 @@ constexpr int kBlock = OTPRG_BLOCK;
 #define OTPRG_TEAMS 1
 #endif
 constexpr bool kTeams = OTPRG_TEAMS != 0;  // multi-warp rows in small phases
+#ifndef OTPRG_BULK
+#define OTPRG_BULK 1
+#endif
+constexpr bool kBulk = OTPRG_BULK != 0;  // streaming list build in large phases
 constexpr int kUnroll = 4;       // 128-bit loads in flight per lane (global t)
 #ifndef OTPRG_UNROLL_SMEM
 #define OTPRG_UNROLL_SMEM 8
@@ -136,7 +140,7 @@ template <typename T, bool kSmem>
 __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tvec, int lda,
                                          int start, uint32_t target, bool track_min,
                                          uint32_t& mnw, LowBuild& lb, int lane, const Team& tm,
-                                         unsigned long long& bytes) {
+                                         unsigned long long& bytes, bool full_row = false) {
   using S = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
   const uint32_t tg = S::rep(target);
@@ -173,10 +177,17 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
       const uint32_t k0 = kr[j].x, k1 = kr[j].y, k2 = kr[j].z, k3 = kr[j].w;
       const uint32_t s0 = S::add(k0, tj.x), s1 = S::add(k1, tj.y);
       const uint32_t s2 = S::add(k2, tj.z), s3 = S::add(k3, tj.w);
+      if (track_min) mnw = S::mn(S::mn(mnw, S::mn(s0, s1)), S::mn(s2, s3));
+      {  // fast path: nothing admissible (nor low) in this sub-chunk for the whole warp
+        uint32_t any = S::eq(s0, tg) | S::eq(s1, tg) | S::eq(s2, tg) | S::eq(s3, tg);
+        if (lb.on)
+          any |= S::le(s0, lb.up_rep) | S::le(s1, lb.up_rep) | S::le(s2, lb.up_rep) |
+                 S::le(s3, lb.up_rep);
+        if (!__any_sync(kFull, any != 0)) continue;
+      }
       uint32_t eqb = S::bits(S::eq(s0, tg)) | (S::bits(S::eq(s1, tg)) << S::kEpw) |
                      (S::bits(S::eq(s2, tg)) << (2 * S::kEpw)) |
                      (S::bits(S::eq(s3, tg)) << (3 * S::kEpw));
-      if (track_min) mnw = S::mn(S::mn(mnw, S::mn(s0, s1)), S::mn(s2, s3));
       uint32_t keep = ~0u;
       if (e0 < start) {
         const int drop = start - e0;
@@ -190,7 +201,7 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
         uint32_t leb = (S::bits(S::le(s0, lb.up_rep)) | (S::bits(S::le(s1, lb.up_rep)) << S::kEpw) |
                         (S::bits(S::le(s2, lb.up_rep)) << (2 * S::kEpw)) |
                         (S::bits(S::le(s3, lb.up_rep)) << (3 * S::kEpw))) & keep;
-        if (hit != INT_MAX) {  // entries up to and including the hit only
+        if (hit != INT_MAX && !full_row) {  // entries up to and including the hit only
           const int lim = hit - e0;
           leb = lim < 0 ? 0u : (lim >= kEpv - 1 ? leb : (leb & ((2u << lim) - 1u)));
         }
@@ -228,7 +239,7 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
           }
         }
       }
-      if (hit != INT_MAX) {
+      if (hit != INT_MAX && !full_row) {
         first = hit;
         break;
       }
@@ -434,15 +445,23 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long bytes = 0, steps = 0, walks = 0;
   T* tg = static_cast<T*>(A.t);
-  // Barrier targets: every executed phase passes exactly kBarriers grid
-  // barriers, so the arrival count after `phase` phases is known locally.
-  constexpr unsigned kBarriers = 1 + (kSmem ? 0u : 1u) + kDebugBarriers;
-  unsigned bar_target = phase * kBarriers * gridDim.x;
+  // Barrier targets: the arrival count at launch is ctl->bar_base (written by
+  // the previous launch at exit); every barrier adds gridDim.x.
+  unsigned bar_target = ld_cg(reinterpret_cast<const unsigned*>(&ctl->bar_base));
   const int warps_per_block = blockDim.x >> 5;
   const int total_warps = gridDim.x * warps_per_block;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gthreads = gridDim.x * blockDim.x;
 
+  if (phase == 0) {
+    // Touch every 2 MB page of kT once before the first full-width scan so
+    // the address translations are resident; a cold TLB otherwise serialises
+    // thousands of concurrent row scans on page walks.
+    const size_t bytes = (size_t)ctl->n_b * lda * sizeof(T);
+    const char* base = static_cast<const char*>(A.kT);
+    for (size_t off = (size_t)gtid << 21; off < bytes; off += (size_t)gthreads << 21)
+      (void)__ldcg(reinterpret_cast<const unsigned*>(base + off));
+  }
   if constexpr (kSmem) {  // global t is complete at launch (previous launch applied its M')
     const uint4* src = reinterpret_cast<const uint4*>(tg);
     uint4* dst = reinterpret_cast<uint4*>(s_t);
@@ -543,7 +562,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     // Timeline slots (ns): 0 phase start, 1 apply done (block 0), 2/3 last /
     // first block done with P (3 stores ~t), 4 after the barrier, 7 n_i.
     unsigned long long* tr =
-        (A.trace && phase <= A.trace_cap) ? A.trace + (size_t)(phase - 1) * 8 : nullptr;
+        (A.trace && phase <= A.trace_cap) ? A.trace + (size_t)(phase - 1) * kTraceSlots : nullptr;
     if (leader) {
       A.free_counts[phase - 1] = n;
       ctl->sum_ni += n;
@@ -573,6 +592,34 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       else if (n * 2 <= total_warps) tsize = 2;
     }
     const int wib = threadIdx.x >> 5;
+    if (kBulk && n >= total_warps) {
+      // Large phase: first stream every proposer's row once at full HBM
+      // bandwidth (warps in flight, no dependent atomics), recording its
+      // admissible positions (level 0 of the low-set cache) and row minimum;
+      // the chains below then mostly walk these lists.
+      Team solo{1, 0, 0u, s_team[wib]};
+      for (int q = wib * (int)gridDim.x + (int)blockIdx.x; q < n; q += total_warps) {
+        const int b = __ldcg(list_in + q);
+        const uint32_t target = (uint32_t)__ldcg(A.yb + b) - 1u;
+        const int4 meta0 = __ldcg(A.lmeta + b);
+        if (meta0.y >= lda && target <= (uint32_t)meta0.x) continue;  // complete & valid
+        LowBuild lb;
+        lb.on = true;
+        lb.up_rep = Simd<T>::rep(target);
+        lb.ent = A.lent + (size_t)b * kLowCap;
+        uint32_t mnw = 0xffffffffu;
+        warp_scan<T, kSmem>(static_cast<const T*>(A.kT) + (size_t)b * lda, tp, lda, 0, target, true,
+                            mnw, lb, lane, solo, bytes, true);
+        const uint32_t m = __reduce_min_sync(kFull, Simd<T>::hmin(mnw));
+        if (lane == 0) {
+          A.lmeta[b] = make_int4((int)target, lb.full_pos >= 0 ? lb.full_pos + 1 : lda, lb.cnt, 0);
+          static_cast<T*>(A.rowmin)[b] = (T)m;
+        }
+      }
+      bar_target += gridDim.x;
+      grid_barrier(ctl, bar_target, tr ? tr + 9 : nullptr);
+      if (tr && leader) tr[8] = globaltimer();
+    }
     const int tib = wib / tsize;  // team index in the block
     Team tm{tsize, wib % tsize, 1u + (unsigned)tib, s_team[tib]};
     const int teams_per_block = warps_per_block / tsize;
@@ -598,6 +645,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     grid_barrier(ctl, bar_target, tr ? tr + 2 : nullptr, tr ? tr + 3 : nullptr);
     if (tr && leader) tr[4] = globaltimer();
   }
+  if (leader) ctl->bar_base = bar_target;  // every block exits with the same count
   if (lane == 0 && (bytes | steps | walks)) {
     atomicAdd(&ctl->bytes_touched, bytes);
     atomicAdd(&ctl->chain_steps, steps);
