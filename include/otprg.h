@@ -174,6 +174,33 @@ int otprg_uniform_square_points(int32_t n, uint64_t seed, double* pts_a, double*
 int otprg_load_mnist_pair(const char* path, int32_t n, uint64_t seed, uint8_t* img_a,
                           uint8_t* img_b, char* err, int32_t err_cap);
 
+/* ---- A-row-sharded solve over several GPUs ---------------
+ * One context per rank (one process per GPU, or several contexts in one
+ * process for testing).  Rank `shard` of n_shards owns the demand range
+ * [bounds[shard], bounds[shard+1]) of every rounded-cost row (built from the
+ * 2-D point sets of the problem); matching, duals and DA holders are
+ * replicated and every rank computes the identical result.  Per phase:
+ *   otprg_shard_top    apply the previous phase's M' and test termination
+ *                      (returns n_i; finished when done);
+ *   otprg_shard_scan   write this rank's first-K admissible candidates of
+ *                      every free b into its slot of the exchange buffers
+ *                      cand[n_shards][cap][K] / meta[n_shards][cap] (device);
+ *   (all-gather the slots across ranks — NCCL, by the caller)
+ *   otprg_shard_da     deferred acceptance over the merged candidates;
+ *                      reports chains parked at a truncated list; while
+ *                      parked > 0: otprg_shard_scan(refill=1), all-gather,
+ *                      otprg_shard_da(resume=1).
+ * otprg_shard_finish completes the matching and returns the results (as
+ * otprg_solve_assignment).  Results are bit-identical for every n_shards. */
+int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* prob, int32_t n_shards,
+                        int32_t shard, int32_t K, int32_t* bounds_out);
+int otprg_shard_begin(otprg_ctx* ctx);
+int otprg_shard_top(otprg_ctx* ctx, int32_t* n_out, int32_t* finished);
+int otprg_shard_scan(otprg_ctx* ctx, int32_t* cand, int32_t* meta, int32_t cap, int32_t refill);
+int otprg_shard_da(otprg_ctx* ctx, const int32_t* cand, const int32_t* meta, int32_t cap,
+                   int32_t resume, int32_t* parked);
+int otprg_shard_finish(otprg_ctx* ctx, otprg_result* res);
+
 /* ---- optimal transport (config 5) ---------------------------------------
  * otprg_solve_ot replaces otpr::solve_ot (include/otpr/ot.hpp:161-163,
  * src/ot.cpp:705-732): theta-scaling of the masses at eps/3

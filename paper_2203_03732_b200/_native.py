@@ -55,7 +55,9 @@ EXPORTS = [
     "otprg_uniform_square_points", "otprg_flush_l2", "otprg_begin", "otprg_step",
     "otprg_snapshot", "otprg_finish", "otprg_timer_start", "otprg_timer_stop",
     "otprg_set_trace", "otprg_get_trace", "otprg_load_mnist_pair", "otprg_solve_ot",
-    "otprg_ot_scale_and_round", "otprg_random_ot_rational",
+    "otprg_ot_scale_and_round", "otprg_random_ot_rational", "otprg_shard_prepare",
+    "otprg_shard_begin", "otprg_shard_top", "otprg_shard_scan", "otprg_shard_da",
+    "otprg_shard_finish",
 ]
 
 _lib = None
@@ -105,6 +107,12 @@ def lib() -> C.CDLL:
     L.otprg_ot_scale_and_round.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp,
                                            C.POINTER(C.c_double)]
     L.otprg_random_ot_rational.argtypes = [C.c_int32, C.c_int32, C.c_uint64, vp, vp, vp]
+    L.otprg_shard_prepare.argtypes = [vp, C.POINTER(Problem), C.c_int32, C.c_int32, C.c_int32, vp]
+    L.otprg_shard_begin.argtypes = [vp]
+    L.otprg_shard_top.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.otprg_shard_scan.argtypes = [vp, vp, vp, C.c_int32, C.c_int32]
+    L.otprg_shard_da.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
+    L.otprg_shard_finish.argtypes = [vp, C.POINTER(Result)]
     _lib = L
     return L
 

@@ -81,6 +81,15 @@ struct otprg_ctx {
   DevBuf trace;            // device timeline, 8 u64 per phase (see solve_kernels.cu)
   uint32_t trace_cap = 0;  // 0 = tracing off
 
+  // A-row-sharded mode (shard_kernels.cu): this rank's slab [sh_lo, sh_hi)
+  bool sharded = false;
+  int sh_n_shards = 1, sh_shard = 0, sh_lo = 0, sh_hi = 0, sh_K = 16, sh_cap = 0;
+  uint32_t sh_phase = 0;     // phases completed
+  int sh_n = 0;              // proposers of the running phase
+  int sh_parked = 0;         // chains waiting for a rescan
+  int sh_park_cur = 0;       // which park buffer holds the waiting chains
+  DevBuf sh_bounds, sh_pos, sh_park[2], sh_list;
+
   // optimal transport (ot_host.cpp): per-phase scan inputs / outputs
   DevBuf ot_t, ot_req, ot_out;
   void* ot_hpin = nullptr;

@@ -68,6 +68,36 @@ cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_
 cudaError_t launch_export_k(const void* kT, int n_ai, int n_bi, int lda, int width, bool swapped,
                             int32_t* k_out, cudaStream_t s);
 
+// A-row-sharded phase step (shard_kernels.cu).  This rank owns demand range
+// [lo, hi) of every kT row; everything else is replicated.
+struct ShardArgs {
+  const void* kT;          // T[n_b][lda] : columns lo..hi-1 (local index a - lo)
+  int lda, lo, hi, shard, n_shards;
+  const int* bounds;       // [n_shards + 1] shard boundaries (device)
+  int K, cap;              // candidates per (shard, proposer); proposer capacity
+  void* t;                 // T[n_a] replicated t(a) = -Y(a)
+  int width;               // sizeof(T)
+  int32_t* yb;
+  int32_t* match_a;
+  int32_t* match_b;
+  unsigned long long* holder;  // [n_a] replicated DA holders
+  const int32_t* list_in;  // free b's of the phase being run
+  int32_t* list_out;       // free b's of the next phase
+  const int2* mp_prev;     // (a, partner) first held in the previous phase
+  int2* mp_out;            // (a, partner) first held in this phase
+  int32_t* pos_of_b;       // [n_b] b -> index in list_in
+  int4* park_out;          // parked chains (list index, b, restart)
+  int64_t* free_counts;
+  Ctl* ctl;
+};
+cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, cudaStream_t s);
+cudaError_t launch_shard_compact(const ShardArgs& a, cudaStream_t s);
+cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int32_t* cand,
+                              int2* meta, cudaStream_t s);
+cudaError_t launch_shard_da(const ShardArgs& a, uint32_t phase, const int32_t* cand,
+                            const int2* meta, int nchains, const int4* resume_list,
+                            cudaStream_t s);
+
 // OT admissible-cluster scan (ot_kernels.cu): per request (b, target, start)
 // the first K admissible (a, ci), encoded a*2+ci, and (count, resume).
 cudaError_t launch_ot_scan(const void* kT, int lda, int width, const void* t0, const void* t1,

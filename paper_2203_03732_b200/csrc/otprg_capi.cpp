@@ -696,3 +696,239 @@ int otprg_flush_l2(otprg_ctx* ctx) {
 }
 
 }  // extern "C"
+
+// ---- A-row-sharded mode --------------------------------------
+namespace {
+
+otprg::ShardArgs shard_args(otprg_ctx* ctx) {
+  otprg::ShardArgs S{};
+  S.kT = ctx->kT.p;
+  S.lda = ctx->lda;
+  S.lo = ctx->sh_lo;
+  S.hi = ctx->sh_hi;
+  S.shard = ctx->sh_shard;
+  S.n_shards = ctx->sh_n_shards;
+  S.bounds = ctx->sh_bounds.as<int>();
+  S.K = ctx->sh_K;
+  S.cap = ctx->sh_cap;
+  S.t = ctx->t.p;
+  S.width = ctx->width;
+  S.yb = ctx->yb.as<int32_t>();
+  S.match_a = ctx->ma.as<int32_t>();
+  S.match_b = ctx->mb.as<int32_t>();
+  S.holder = ctx->holder.as<unsigned long long>();
+  S.list_in = ctx->sh_list.as<int32_t>();
+  S.list_out = nullptr;
+  int2* mps = ctx->mps.as<int2>();
+  S.mp_prev = mps + static_cast<size_t>(ctx->sh_phase & 1) * ctx->ib;
+  S.mp_out = mps + static_cast<size_t>((ctx->sh_phase + 1) & 1) * ctx->ib;
+  S.pos_of_b = ctx->sh_pos.as<int32_t>();
+  S.park_out = ctx->sh_park[ctx->sh_park_cur ^ 1].as<int4>();
+  S.free_counts = ctx->fc.as<int64_t>();
+  S.ctl = ctx->ctl.as<Ctl>();
+  return S;
+}
+
+int read_ctl(otprg_ctx* ctx, Ctl* h) {
+  CK(cudaMemcpyAsync(h, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream), "D2H ctl");
+  CK(cudaStreamSynchronize(ctx->stream), "shard step");
+  return check_status(ctx, *h, false);
+}
+
+}  // namespace
+
+extern "C" {
+
+int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards, int32_t shard,
+                        int32_t K, int32_t* bounds_out) {
+  if (!ctx) return OTPRG_PARAMETER;
+  int st = validate_problem(ctx, p);
+  if (st) return st;
+  if (p->cost_kind != OTPRG_COST_POINTS2D)
+    return fail(ctx, OTPRG_PARAMETER, "sharded mode builds its slab from 2-D point sets");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards)
+    return fail(ctx, OTPRG_PARAMETER, "bad shard index");
+  if (K < 1 || K > 32) return fail(ctx, OTPRG_PARAMETER, "K must lie in [1, 32]");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  ctx->prepared = false;
+  ctx->n_a = p->n_a;
+  ctx->n_b = p->n_b;
+  ctx->swapped = p->n_b > p->n_a;
+  ctx->ia = ctx->swapped ? p->n_b : p->n_a;
+  ctx->ib = ctx->swapped ? p->n_a : p->n_b;
+  ctx->eps = p->eps;
+  ctx->cost_kind = p->cost_kind;
+  const int64_t uf = host_scaled_floor(1.0, p->eps);
+  ctx->unit_floor = static_cast<int32_t>(uf);
+  ctx->unit_ceil = static_cast<int32_t>(static_cast<double>(uf) * p->eps == 1.0 ? uf : uf + 1);
+  const int64_t need = static_cast<int64_t>(ctx->unit_ceil) + 2;
+  int width = -1;
+  if (p->storage == OTPRG_STORAGE_U8) width = need <= 253 ? 1 : -1;
+  else width = need <= 65533 ? 2 : -1;
+  if (width < 0) return fail(ctx, OTPRG_PARAMETER, "eps too small for the device cost storage");
+  ctx->width = width;
+  // shard boundaries: multiples of 512 elements (aligned t / kT vectors)
+  std::vector<int> bounds(n_shards + 1);
+  for (int g = 0; g < n_shards; ++g)
+    bounds[g] = static_cast<int>((static_cast<int64_t>(ctx->ia) * g / n_shards) / 512 * 512);
+  bounds[n_shards] = ctx->ia;
+  if (bounds_out)
+    for (int g = 0; g <= n_shards; ++g) bounds_out[g] = bounds[g];
+  ctx->sharded = true;
+  ctx->sh_n_shards = n_shards;
+  ctx->sh_shard = shard;
+  ctx->sh_lo = bounds[shard];
+  ctx->sh_hi = bounds[shard + 1];
+  ctx->sh_K = K;
+  ctx->sh_cap = ctx->ib;
+  const int align = 512 / width;
+  const size_t ia = ctx->ia, ib = ctx->ib;
+  const int local = std::max(ctx->sh_hi - ctx->sh_lo, 1);
+  ctx->lda = (local + align - 1) / align * align;
+  const size_t full = (ia + 511) / 512 * 512;
+  CK(ctx->kT.ensure(ib * ctx->lda * width), "alloc kT slab");
+  CK(ctx->t.ensure(full * width), "alloc t");
+  CK(ctx->yb.ensure(ib * 4), "alloc yb");
+  CK(ctx->ma.ensure(ia * 4), "alloc match_a");
+  CK(ctx->mb.ensure(ib * 4), "alloc match_b");
+  CK(ctx->holder.ensure(2 * ia * 8), "alloc holder");
+  CK(ctx->rowmin.ensure(ib * width), "alloc rowmin");
+  CK(ctx->lmeta.ensure(ib * 16), "alloc low-set meta");
+  CK(ctx->lists.ensure(3 * ib * 4), "alloc lists");
+  CK(ctx->mps.ensure(2 * ib * 8), "alloc mp lists");
+  CK(ctx->fa.ensure(ia * 4), "alloc scratch");
+  CK(ctx->fb.ensure(ib * 4), "alloc scratch");
+  CK(ctx->ctl.ensure(sizeof(Ctl)), "alloc ctl");
+  CK(ctx->sh_bounds.ensure((n_shards + 1) * sizeof(int)), "alloc bounds");
+  CK(ctx->sh_pos.ensure(ib * 4), "alloc pos");
+  CK(ctx->sh_list.ensure(ib * 4), "alloc list");
+  for (auto& pk : ctx->sh_park) CK(pk.ensure(ib * 16), "alloc park");
+  const double capd = std::ceil((1.0 + 2.0 * p->eps) / (p->eps * p->eps)) + 8.0;
+  ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(1 << 24)));
+  CK(ctx->fc.ensure(ctx->fc_cap * 8), "alloc free_counts");
+  CK(cudaMemcpyAsync(ctx->sh_bounds.p, bounds.data(), (n_shards + 1) * sizeof(int),
+                     cudaMemcpyHostToDevice, ctx->stream), "H2D bounds");
+  // this rank's slab of kT from the points (K2 on the demand range)
+  const double* pa = ctx->swapped ? p->pts_b : p->pts_a;
+  const double* pb = ctx->swapped ? p->pts_a : p->pts_b;
+  CK(ctx->pts.ensure((ia + ib) * 2 * sizeof(double)), "alloc points");
+  double* dpa = ctx->pts.as<double>();
+  double* dpb = dpa + ia * 2;
+  CK(cudaMemcpyAsync(dpa, pa, ia * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
+  if (ctx->sh_hi > ctx->sh_lo)
+    CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb,
+                                    ctx->sh_hi - ctx->sh_lo, ctx->ib, p->eps, std::sqrt(2.0),
+                                    ctx->kT.p, ctx->lda, width, ctx->stream),
+       "round_points launch");
+  CK(cudaEventRecord(ctx->ev[5], ctx->stream), "event");
+  CK(cudaStreamSynchronize(ctx->stream), "slab build");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]);
+  ctx->build_ms = ms;
+  ctx->pts_a.assign(p->pts_a, p->pts_a + 2 * static_cast<size_t>(p->n_a));
+  ctx->pts_b.assign(p->pts_b, p->pts_b + 2 * static_cast<size_t>(p->n_b));
+  ctx->prepared = true;
+  return OTPRG_OK;
+}
+
+int otprg_shard_begin(otprg_ctx* ctx) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!ctx->prepared || !ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_shard_prepare() first");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  Ctl h{};
+  h.n_a = ctx->ia;
+  h.n_b = ctx->ib;
+  h.lda = ctx->lda;
+  h.thresh = static_cast<int32_t>(std::floor(ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b))));
+  h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
+  h.tmax = ctx->width == 1 ? 253u : 65533u;
+  h.cnt[0] = ctx->ib;
+  CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream), "H2D ctl");
+  otprg::SolveArgs A{};
+  A.t = ctx->t.p;
+  A.yb = ctx->yb.as<int32_t>();
+  A.match_a = ctx->ma.as<int32_t>();
+  A.match_b = ctx->mb.as<int32_t>();
+  A.holder[0] = ctx->holder.as<unsigned long long>();
+  A.holder[1] = A.holder[0] + ctx->ia;
+  A.rowmin = ctx->rowmin.p;
+  A.lmeta = ctx->lmeta.as<int4>();
+  A.list[0] = ctx->lists.as<int32_t>();
+  const int full = (ctx->ia + 511) / 512 * 512;
+  CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, full, ctx->width, ctx->stream), "init launch");
+  ctx->sh_phase = 0;
+  ctx->sh_parked = 0;
+  ctx->sh_n = 0;
+  ctx->begun = true;
+  ctx->completed = false;
+  return OTPRG_OK;
+}
+
+int otprg_shard_top(otprg_ctx* ctx, int32_t* n_out, int32_t* finished) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!ctx->begun || !ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_shard_begin() first");
+  otprg::ShardArgs S = shard_args(ctx);
+  CK(otprg::launch_shard_top(S, ctx->sh_phase, ctx->sh_phase > 0, ctx->stream), "shard_top launch");
+  Ctl h{};
+  int st = read_ctl(ctx, &h);
+  if (st) return st;
+  ctx->sh_n = h.cnt[ctx->sh_phase & 1];
+  if (!h.done) {
+    CK(otprg::launch_shard_compact(S, ctx->stream), "shard_compact launch");
+    CK(cudaStreamSynchronize(ctx->stream), "compact");
+  }
+  if (n_out) *n_out = ctx->sh_n;
+  if (finished) *finished = h.done;
+  return OTPRG_OK;
+}
+
+int otprg_shard_scan(otprg_ctx* ctx, int32_t* cand, int32_t* meta_words, int32_t cap,
+                     int32_t refill) {
+  int2* meta = reinterpret_cast<int2*>(meta_words);
+  if (!ctx) return OTPRG_PARAMETER;
+  if (cap < ctx->sh_n || cap < ctx->sh_cap) return fail(ctx, OTPRG_PARAMETER, "exchange buffer too small");
+  otprg::ShardArgs S = shard_args(ctx);
+  S.cap = cap;
+  const int4* req = refill ? ctx->sh_park[ctx->sh_park_cur].as<int4>() : nullptr;
+  const int nreq = refill ? ctx->sh_parked : ctx->sh_n;
+  CK(otprg::launch_shard_scan(S, req, nreq, cand, meta, ctx->stream), "shard_scan launch");
+  CK(cudaStreamSynchronize(ctx->stream), "shard scan");
+  return OTPRG_OK;
+}
+
+int otprg_shard_da(otprg_ctx* ctx, const int32_t* cand, const int32_t* meta_words, int32_t cap,
+                   int32_t resume, int32_t* parked) {
+  const int2* meta = reinterpret_cast<const int2*>(meta_words);
+  if (!ctx) return OTPRG_PARAMETER;
+  otprg::ShardArgs S = shard_args(ctx);
+  S.cap = cap;
+  CK(cudaMemsetAsync(&ctx->ctl.as<Ctl>()->work[1], 0, sizeof(int32_t), ctx->stream), "memset");
+  const int4* resume_list = resume ? ctx->sh_park[ctx->sh_park_cur].as<int4>() : nullptr;
+  const int nchains = resume ? ctx->sh_parked : ctx->sh_n;
+  CK(otprg::launch_shard_da(S, ctx->sh_phase + 1, cand, meta, nchains, resume_list, ctx->stream),
+     "shard_da launch");
+  Ctl h{};
+  int st = read_ctl(ctx, &h);
+  if (st) return st;
+  ctx->sh_park_cur ^= 1;
+  ctx->sh_parked = h.work[1];
+  if (ctx->sh_parked == 0) ctx->sh_phase += 1;  // the phase is complete
+  if (parked) *parked = ctx->sh_parked;
+  return OTPRG_OK;
+}
+
+int otprg_shard_finish(otprg_ctx* ctx, otprg_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!res || !res->match_of_a || !res->match_of_b)
+    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
+  int st = launch_finish(ctx);
+  if (st) return st;
+  Ctl h{};
+  if ((st = export_state(ctx, res, &h))) return st;
+  res->build_ms = ctx->build_ms;
+  return check_status(ctx, h, true);
+}
+
+}  // extern "C"

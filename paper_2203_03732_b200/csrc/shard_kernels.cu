@@ -1,0 +1,321 @@
+// shard_kernels.cu — the A-row-sharded phase step for several GPUs
+// (SURVEY §8(e)).  Shard g owns the demand range [lo_g, hi_g) of every kT
+// row; the matching, duals and holders are replicated on every rank and every
+// rank runs the same deterministic deferred acceptance, so all ranks hold the
+// identical state after each phase and only candidate lists cross NVLink.
+//
+// Per phase (host-driven, one process per GPU; see shard_host in
+// otprg_capi.cpp and paper_2203_03732_b200/sharded.py):
+//   shard_top   apply M' of the previous phase (apply_phase,
+//               assignment.cpp:210-235), termination / phase cap
+//               (:324-334, :356-358), inverse map b -> list index;
+//   shard_scan  every rank scans its slab of each free b's row for the first
+//               K admissible a (global index) and its coverage end, into its
+//               slot of the exchange buffer;
+//   exchange    all-gather of the slots (NCCL over NVLink; nothing to do when
+//               all shards share one buffer);
+//   shard_da    deferred acceptance over the merged candidate lists (shards
+//               are ascending ranges, so concatenation is ascending); a chain
+//               that reaches a truncated shard's coverage end parks with a
+//               restart position, the parked rows are rescanned and
+//               exchanged, and the chains resume.  DA is order independent,
+//               so the result is the reference's sequential greedy M'
+//               whatever the shard count.
+#include <climits>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace otprg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t t_get(const ShardArgs& S, int a) {
+  return S.width == 1 ? (uint32_t)static_cast<const uint8_t*>(S.t)[a]
+                      : (uint32_t)static_cast<const uint16_t*>(S.t)[a];
+}
+__device__ __forceinline__ void t_set(const ShardArgs& S, int a, uint32_t v) {
+  if (S.width == 1) static_cast<uint8_t*>(S.t)[a] = (uint8_t)v;
+  else static_cast<uint16_t*>(S.t)[a] = (uint16_t)v;
+}
+
+// Scan request: (list index, b, start position (global a)).  req == nullptr:
+// every free b of the phase from position 0.
+template <typename T>
+__global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4* __restrict__ req,
+                                                         int nreq, int32_t* __restrict__ cand,
+                                                         int2* __restrict__ meta) {
+  using SD = Simd<T>;
+  constexpr int kEpv = 16 / sizeof(T);
+  constexpr int kU = 4;
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nreq) return;
+  int i, b, start;
+  if (req) {
+    const int4 r = req[w];
+    i = r.x;
+    b = r.y;
+    start = r.z;
+  } else {
+    i = w;
+    b = __ldcg(S.list_in + w);
+    start = 0;
+  }
+  const uint32_t tg = SD::rep((uint32_t)__ldcg(S.yb + b) - 1u);
+  const int lo = S.lo, hi = S.hi, K = S.K, width_local = hi - lo;
+  int32_t* o = cand + ((size_t)S.shard * S.cap + i) * K;
+  int cnt = 0, cov = hi;
+  const int lstart = max(start, lo) - lo;
+  if (start < hi) {
+    const uint4* rv = reinterpret_cast<const uint4*>(static_cast<const T*>(S.kT) + (size_t)b * S.lda);
+    const uint4* tv = reinterpret_cast<const uint4*>(static_cast<const T*>(S.t) + lo);
+    const int nv = (width_local + kEpv - 1) / kEpv;
+    bool full = false;
+    for (int v = (lstart / kEpv) & ~31; v < nv && !full; v += 32 * kU) {
+      uint4 kr[kU], tr[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const int vi = v + j * 32 + lane;
+        if (vi < nv) {
+          kr[j] = __ldg(rv + vi);
+          tr[j] = __ldcg(tv + vi);
+        } else {
+          kr[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
+          tr[j] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        if (full) break;
+        const int e0 = (v + j * 32 + lane) * kEpv;  // local element index
+        const uint32_t kw[4] = {kr[j].x, kr[j].y, kr[j].z, kr[j].w};
+        const uint32_t tw[4] = {tr[j].x, tr[j].y, tr[j].z, tr[j].w};
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) m |= SD::bits(SD::eq(SD::add(kw[q], tw[q]), tg)) << (q * SD::kEpw);
+        if (e0 < lstart) {
+          const int drop = lstart - e0;
+          m = drop >= kEpv ? 0u : (m & (~0u << drop));
+        }
+        if (e0 + kEpv > width_local) {  // t beyond the shard belongs to the next shard
+          const int keepn = width_local - e0;
+          m = keepn <= 0 ? 0u : (m & ((1u << keepn) - 1u));
+        }
+        if (!__ballot_sync(kFull, m != 0)) continue;
+        const int c = __popc(m);
+        int inc = c;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const int y = __shfl_up_sync(kFull, inc, s);
+          if (lane >= s) inc += y;
+        }
+        const int tot = __shfl_sync(kFull, inc, 31);
+        int idx = cnt + inc - c, last = -1;
+        uint32_t bm = m;
+        while (bm) {
+          const int e = __ffs(bm) - 1;
+          bm &= bm - 1;
+          if (idx < K) {
+            o[idx] = lo + e0 + e;
+            if (idx == K - 1) last = lo + e0 + e;
+          }
+          ++idx;
+        }
+        if (cnt + tot >= K) {
+          const unsigned src = __ballot_sync(kFull, last >= 0);
+          cov = __shfl_sync(kFull, last, __ffs(src) - 1) + 1;
+          cnt = K;
+          full = true;
+        } else {
+          cnt += tot;
+        }
+      }
+    }
+  }
+  if (lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+}
+
+// Top of the phase after `phase_done` phases: apply M' of phase phase_done
+// (replicated), termination test, counters for the next phase.
+__global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t phase_done,
+                                                         int apply) {
+  Ctl* ctl = S.ctl;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  const int par = phase_done & 1;
+  if (apply) {
+    const int m = ctl->mp_cnt[par];
+    for (int q = gtid; q < m; q += gthreads) {
+      const int2 e = S.mp_prev[q];
+      const int a = e.x, old_b = e.y;
+      const int b = (int)(uint32_t)S.holder[a];
+      if (old_b >= 0) S.match_b[old_b] = -1;
+      S.match_a[a] = b;
+      S.match_b[b] = a;
+      const uint32_t nt = t_get(S, a) + 1u;
+      if (nt > ctl->tmax) report(ctl, 12, (int)phase_done, a, (int)nt);
+      t_set(S, a, nt);
+    }
+  }
+  const int n = ctl->cnt[par];
+  if (gtid == 0) {
+    ctl->phase = phase_done;
+    if (apply) ctl->applied = phase_done;
+    if (n <= ctl->thresh) {  // (double)n_i <= eps*m  <=>  n_i <= floor(eps*m)
+      ctl->done = 1;
+      ctl->full_match = (n == 0);
+    } else if (phase_done + 1 > (uint32_t)ctl->phase_cap) {
+      report(ctl, 5, (int)phase_done);
+    } else {
+      S.free_counts[phase_done] = n;
+      ctl->sum_ni += n;
+      const int nx = par ^ 1;  // counters the coming phase appends to
+      ctl->cnt[nx] = 0;
+      ctl->mp_cnt[nx] = 0;
+      ctl->exh[nx] = 0;
+      ctl->work[1] = 0;  // parked chains
+    }
+  }
+}
+
+// The free list of the coming phase, ascending b (identical on every rank,
+// so list indices name the same b everywhere), and its inverse.  One block.
+__global__ void __launch_bounds__(1024) shard_compact_kernel(ShardArgs S) {
+  __shared__ int s_scan[1024];
+  const int n_b = S.ctl->n_b, tid = threadIdx.x, nt = blockDim.x;
+  int32_t* out = const_cast<int32_t*>(S.list_in);
+  const int chunk = (n_b + nt - 1) / nt;
+  const int lo = min(n_b, tid * chunk), hi = min(n_b, lo + chunk);
+  int c = 0;
+  for (int q = lo; q < hi; ++q) c += (S.match_b[q] == -1);
+  s_scan[tid] = c;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    const int v = tid >= off ? s_scan[tid - off] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  int pos = s_scan[tid] - c;
+  for (int q = lo; q < hi; ++q)
+    if (S.match_b[q] == -1) {
+      out[pos] = q;
+      S.pos_of_b[q] = pos;
+      ++pos;
+    }
+}
+
+// Deferred acceptance over merged candidate lists, one warp per chain.
+// resume_list == nullptr: a chain per free b; else per parked entry.
+__global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, uint32_t phase,
+                                                       const int32_t* __restrict__ cand,
+                                                       const int2* __restrict__ meta, int nchains,
+                                                       const int4* __restrict__ resume_list) {
+  Ctl* ctl = S.ctl;
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nchains) return;
+  const uint32_t cur_tag = ~phase;
+  const int par = phase & 1;
+  int i, b, start;
+  if (resume_list) {
+    const int4 r = resume_list[w];
+    i = r.x;
+    b = r.y;
+    start = r.z;
+  } else {
+    i = w;
+    b = __ldcg(S.list_in + w);
+    start = 0;
+  }
+  const int K = S.K, G = S.n_shards;
+  while (true) {
+    int a = -1, restart = -1;
+    for (int g = 0; g < G; ++g) {  // next candidate >= start, shard-ascending
+      const int ghi = S.bounds[g + 1];
+      if (start >= ghi) continue;
+      const int2 mt = __ldcg(meta + (size_t)g * S.cap + i);
+      int c = -1;
+      if (lane < mt.x && lane < K) c = __ldcg(cand + ((size_t)g * S.cap + i) * K + lane);
+      const unsigned bal = __ballot_sync(kFull, c >= start);
+      if (bal) {
+        a = __shfl_sync(kFull, c, __ffs(bal) - 1);
+        break;
+      }
+      if (mt.y < ghi) {  // truncated shard: [max(start, cov), hi) not yet scanned
+        restart = max(start, mt.y);
+        break;
+      }
+    }
+    if (a < 0 && restart >= 0) {  // park until the gap is rescanned
+      if (lane == 0) {
+        const int pos = atomicAdd(&ctl->work[1], 1);
+        S.park_out[pos] = make_int4(i, b, restart, 0);
+      }
+      return;
+    }
+    if (a < 0) {  // b stays free: Y(b) += 1 (apply_phase :233-235)
+      if (lane == 0) {
+        const uint32_t yb = (uint32_t)__ldcg(S.yb + b);
+        if (yb + 1 > ctl->tmax) report(ctl, 11, (int)phase, b, (int)yb);
+        S.yb[b] = (int32_t)(yb + 1);
+        atomicAdd(&ctl->cnt[par], 1);  // the next free list is rebuilt sorted
+        atomicAdd(&ctl->exh[par], 1);
+      }
+      return;
+    }
+    const unsigned long long key = ((unsigned long long)cur_tag << 32) | (uint32_t)b;
+    unsigned long long old = 0;
+    if (lane == 0) old = atomicMin(S.holder + a, key);
+    old = __shfl_sync(kFull, old, 0);
+    if (old < key) {  // held by a lower b of this phase
+      start = a + 1;
+      continue;
+    }
+    if ((uint32_t)(old >> 32) == cur_tag) {  // displaced b2 continues after a
+      b = (int)(uint32_t)old;
+      i = __ldcg(S.pos_of_b + b);
+      start = a + 1;
+      continue;
+    }
+    if (lane == 0) {  // first holder this phase: the previous partner is freed
+      const int partner = __ldcg(S.match_a + a);  // complete: applied at this phase's top
+      if (partner >= 0) atomicAdd(&ctl->cnt[par], 1);
+      const int pos = atomicAdd(&ctl->mp_cnt[par], 1);
+      S.mp_out[pos] = make_int2(a, partner);
+    }
+    return;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, cudaStream_t s) {
+  shard_top_kernel<<<148, 1024, 0, s>>>(a, phase_done, apply ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_compact(const ShardArgs& a, cudaStream_t s) {
+  shard_compact_kernel<<<1, 1024, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int32_t* cand,
+                              int2* meta, cudaStream_t s) {
+  if (nreq <= 0) return cudaSuccess;
+  const int blocks = (nreq * 32 + 255) / 256;
+  if (a.width == 1) shard_scan_kernel<uint8_t><<<blocks, 256, 0, s>>>(a, req, nreq, cand, meta);
+  else shard_scan_kernel<uint16_t><<<blocks, 256, 0, s>>>(a, req, nreq, cand, meta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_da(const ShardArgs& a, uint32_t phase, const int32_t* cand,
+                            const int2* meta, int nchains, const int4* resume_list,
+                            cudaStream_t s) {
+  if (nchains <= 0) return cudaSuccess;
+  const int blocks = (nchains * 32 + 255) / 256;
+  shard_da_kernel<<<blocks, 256, 0, s>>>(a, phase, cand, meta, nchains, resume_list);
+  return cudaGetLastError();
+}
+
+}  // namespace otprg

@@ -1,0 +1,194 @@
+"""A-row-sharded assignment solve over several GPUs.
+
+Rank g owns the demand range [bounds[g], bounds[g+1]) of every rounded-cost
+row (its slab of kT, built on its GPU from the point sets); the matching,
+the integer duals and the deferred-acceptance holders are replicated, and
+every rank runs the same deterministic phase, so only candidate lists cross
+NVLink.  Per phase (reference: solve_oriented, assignment.cpp:316-364):
+
+    top      apply the previous M', termination test      (every rank)
+    scan     first K admissible a >= start of every free b in the slab
+    gather   all-gather of the per-rank candidate slots   (NCCL / NVLink)
+    DA       deferred acceptance over the merged lists; chains that reach
+             a truncated slab park -> rescan -> gather -> resume
+
+Results are bit-identical for every shard count (and to the single-GPU
+solver / the reference): the merged candidate order is the row order and
+deferred acceptance with a common priority has one outcome.
+
+Backends (same driver): ``DeviceRank`` drives one otprg_ctx through the C
+ABI; the exchange is ``LocalExchange`` (all ranks in one process share one
+buffer: several logical shards on one GPU) or ``TorchDistExchange`` (one
+process per GPU, torch.distributed all_gather over NCCL).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .api import AssignmentInstance, AssignmentOptions, ParameterError, Solver, _check_options
+
+K_DEFAULT = 16
+
+
+class DeviceRank:
+    """One shard: an otprg_ctx prepared with the slab [lo, hi)."""
+
+    def __init__(self, device: int = 0):
+        self.solver = Solver(device)
+        self._L, self._ctx = self.solver._L, self.solver._ctx
+
+    def _ok(self, st):
+        if st:
+            self.solver._raise(st)
+
+    def prepare(self, inst: AssignmentInstance, eps: float, n_shards: int, shard: int,
+                K: int = K_DEFAULT, storage: str = "auto") -> np.ndarray:
+        p = self.solver._problem(inst, eps, storage)
+        bounds = np.zeros(n_shards + 1, np.int32)
+        self._ok(self._L.otprg_shard_prepare(self._ctx, C.byref(p), n_shards, shard, K,
+                                             bounds.ctypes.data))
+        self.n_shards, self.shard, self.K = n_shards, shard, K
+        self.cap = min(inst.n_a, inst.n_b)
+        self.shape = (inst.n_a, inst.n_b, eps)
+        self.bounds = bounds
+        return bounds
+
+    def begin(self):
+        self._ok(self._L.otprg_shard_begin(self._ctx))
+
+    def top(self) -> tuple[int, bool]:
+        n, fin = C.c_int32(), C.c_int32()
+        self._ok(self._L.otprg_shard_top(self._ctx, C.byref(n), C.byref(fin)))
+        return int(n.value), bool(fin.value)
+
+    def scan(self, cand_ptr: int, meta_ptr: int, cap: int, refill: bool):
+        self._ok(self._L.otprg_shard_scan(self._ctx, cand_ptr, meta_ptr, cap, int(refill)))
+
+    def da(self, cand_ptr: int, meta_ptr: int, cap: int, resume: bool) -> int:
+        parked = C.c_int32()
+        self._ok(self._L.otprg_shard_da(self._ctx, cand_ptr, meta_ptr, cap, int(resume),
+                                        C.byref(parked)))
+        return int(parked.value)
+
+    def finish(self):
+        n_a, n_b, eps = self.shape
+        r, bufs = self.solver._result(n_a, n_b, eps)
+        self._ok(self._L.otprg_shard_finish(self._ctx, C.byref(r)))
+        return Solver._pack(r, bufs)
+
+    def close(self):
+        self.solver.close()
+
+
+def _buffers(n_shards: int, cap: int, K: int, device: int):
+    import torch
+    cand = torch.full((n_shards * cap * K,), -1, dtype=torch.int32, device=f"cuda:{device}")
+    meta = torch.zeros((n_shards * cap * 2,), dtype=torch.int32, device=f"cuda:{device}")
+    return cand, meta
+
+
+class LocalExchange:
+    """All ranks in this process write their slots into one shared buffer."""
+
+    def gather(self, *tensors):
+        return None
+
+
+class TorchDistExchange:
+    """One process per GPU: all_gather of the rank slots (NCCL over NVLink)."""
+
+    def __init__(self, rank: int, world: int):
+        self.rank, self.world = rank, world
+
+    def gather(self, *tensors):
+        import torch
+        import torch.distributed as dist
+        for t in tensors:
+            slot = t.numel() // self.world
+            mine = t.narrow(0, self.rank * slot, slot).clone()
+            if t.is_cuda:
+                dist.all_gather_into_tensor(t, mine)
+            else:  # gloo (CPU tests of the protocol)
+                dist.all_gather(list(t.split(slot)), mine)
+        if tensors and tensors[0].is_cuda:
+            # the next C-ABI launch runs on the context's own stream
+            torch.cuda.current_stream().synchronize()
+
+
+def run_phases(ranks, exchange, cand_ptr: int, meta_ptr: int, cap: int, gather_args=()):
+    """The per-phase protocol over the ranks this process drives (one rank per
+    process with TorchDistExchange; every rank with LocalExchange)."""
+    for r in ranks:
+        r.begin()
+    rounds = 0
+    while True:
+        tops = [r.top() for r in ranks]
+        n, finished = tops[0]
+        if any(t != tops[0] for t in tops):
+            raise RuntimeError(f"ranks disagree at the phase top: {tops}")
+        if finished:
+            break
+        for r in ranks:
+            r.scan(cand_ptr, meta_ptr, cap, False)
+        exchange.gather(*gather_args)
+        parked = [r.da(cand_ptr, meta_ptr, cap, False) for r in ranks]
+        while parked[0] > 0:
+            rounds += 1
+            if any(p != parked[0] for p in parked):
+                raise RuntimeError(f"ranks disagree on parked chains: {parked}")
+            for r in ranks:
+                r.scan(cand_ptr, meta_ptr, cap, True)
+            exchange.gather(*gather_args)
+            parked = [r.da(cand_ptr, meta_ptr, cap, True) for r in ranks]
+    return rounds
+
+
+def solve_assignment_sharded(inst: AssignmentInstance, opt: AssignmentOptions, n_shards: int,
+                             K: int = K_DEFAULT):
+    """All shards in this process on opt.device (LocalExchange).  Returns the
+    (Matching, SolveStats) of rank 0 after checking every rank agrees."""
+    _check_options(inst, opt)
+    if inst.pts_a is None:
+        raise ParameterError("the sharded path builds slabs from 2-D point sets")
+    ranks = [DeviceRank(opt.device) for _ in range(n_shards)]
+    for g, r in enumerate(ranks):
+        r.prepare(inst, opt.eps, n_shards, g, K, opt.storage)
+    cap = ranks[0].cap
+    cand, meta = _buffers(n_shards, cap, K, opt.device)
+    rounds = run_phases(ranks, LocalExchange(), cand.data_ptr(), meta.data_ptr(), cap)
+    outs = [r.finish() for r in ranks]
+    m0, s0 = outs[0]
+    for m, s in outs[1:]:
+        if not (np.array_equal(m.match_of_a, m0.match_of_a)
+                and np.array_equal(s.duals_final.y_a, s0.duals_final.y_a)
+                and np.array_equal(s.duals_final.y_b, s0.duals_final.y_b)):
+            raise RuntimeError("shards ended in different states")
+    s0.device["refill_rounds"] = rounds
+    s0.device["n_shards"] = n_shards
+    for r in ranks:
+        r.close()
+    return m0, s0
+
+
+def solve_assignment_distributed(inst: AssignmentInstance, opt: AssignmentOptions,
+                                 K: int = K_DEFAULT):
+    """One rank per process/GPU under torch.distributed (NCCL): each process
+    calls this with the same instance; every rank returns the same result."""
+    import torch.distributed as dist
+    _check_options(inst, opt)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    device = int(os.environ.get("LOCAL_RANK", opt.device))
+    r = DeviceRank(device)
+    r.prepare(inst, opt.eps, world, rank, K, opt.storage)
+    cap = r.cap
+    cand, meta = _buffers(world, cap, K, device)
+    ex = TorchDistExchange(rank, world)
+    rounds = run_phases([r], ex, cand.data_ptr(), meta.data_ptr(), cap, (cand, meta))
+    m, s = r.finish()
+    s.device["refill_rounds"] = rounds
+    s.device["n_shards"] = world
+    r.close()
+    return m, s

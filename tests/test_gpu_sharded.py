@@ -1,0 +1,111 @@
+"""GPU parity of the A-row-sharded path: G logical shards on
+one device (each with its own context, slab and replicated state, exchanging
+candidate slots through one shared buffer) must give the reference's result
+bit for bit for every G and K, and the torch.distributed (NCCL) driver must
+agree with it."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from golden_util import PIN_KEYS, pins_of
+
+pytestmark = pytest.mark.gpu
+
+otprg = pytest.importorskip("paper_2203_03732_b200")
+from paper_2203_03732_b200 import sharded  # noqa: E402
+
+
+def _pins(m, s):
+    return pins_of(m.match_of_a, s.duals_final.y_a, s.duals_final.y_b, s.free_counts, s.phases,
+                   s.sum_ni, s.device["cost"])
+
+
+def _check_golden(golden, key, m, s):
+    want = golden[key]
+    got = _pins(m, s)
+    assert {k: got[k] for k in PIN_KEYS} == {k: want[k] for k in PIN_KEYS}, key
+    assert bool(s.full_match_termination) == bool(want["full_match_termination"])
+
+
+@pytest.mark.parametrize("key,G", [
+    ("square_n4000_eps0.01_s1", 1), ("square_n4000_eps0.01_s1", 2),
+    ("square_n4000_eps0.01_s1", 4), ("square_n4000_eps0.01_s1", 7),
+    ("square_n10000_eps0.01_s1", 2), ("square_n10000_eps0.01_s2", 4),
+    ("square_n10000_eps0.01_s3", 8), ("square_n3000_eps0.02_s1", 3),
+    ("square_n10000_eps0.1_s1", 8), ("square_n1000_eps0.01_s1", 2),
+])
+def test_sharded_matches_golden(golden, key, G):
+    v = golden[key]
+    inst = otprg.gen_uniform_square(v["n_a"], v["seed"])
+    m, s = sharded.solve_assignment_sharded(inst, otprg.AssignmentOptions(eps=v["eps"]), G)
+    _check_golden(golden, key, m, s)
+
+
+@pytest.mark.parametrize("K,G", [(1, 4), (2, 8), (5, 3)])
+def test_sharded_forced_rescans(golden, K, G):
+    key = "square_n4000_eps0.01_s1"
+    v = golden[key]
+    inst = otprg.gen_uniform_square(v["n_a"], v["seed"])
+    m, s = sharded.solve_assignment_sharded(inst, otprg.AssignmentOptions(eps=v["eps"]), G, K=K)
+    if K <= 2:
+        assert s.device["refill_rounds"] > 0  # truncated lists really forced rescans
+    _check_golden(golden, key, m, s)
+
+
+@pytest.mark.parametrize("storage", ["u8", "u16"])
+def test_sharded_storage(golden, storage):
+    key = "square_n2000_eps0.01_s3"
+    v = golden[key]
+    inst = otprg.gen_uniform_square(v["n_a"], v["seed"])
+    m, s = sharded.solve_assignment_sharded(
+        inst, otprg.AssignmentOptions(eps=v["eps"], storage=storage), 3)
+    _check_golden(golden, key, m, s)
+
+
+def test_sharded_rectangular_vs_single():
+    rng = np.random.default_rng(5)
+    for n_a, n_b in ((3000, 1700), (1500, 2600)):
+        inst = otprg.AssignmentInstance(n_a, n_b, pts_a=rng.random((n_a, 2)),
+                                        pts_b=rng.random((n_b, 2)))
+        opt = otprg.AssignmentOptions(eps=0.02)
+        m1, s1 = otprg.solve_assignment(inst, opt)
+        m2, s2 = sharded.solve_assignment_sharded(inst, opt, 3, K=4)
+        assert np.array_equal(m1.match_of_a, m2.match_of_a)
+        assert np.array_equal(m1.match_of_b, m2.match_of_b)
+        assert np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a)
+        assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b)
+        assert np.array_equal(s1.free_counts, s2.free_counts)
+        assert s1.device["cost"] == s2.device["cost"]
+        assert s1.swapped == s2.swapped
+
+
+@pytest.mark.slow
+def test_sharded_100k_vs_single():
+    inst = otprg.gen_uniform_square(100_000, 1)
+    opt = otprg.AssignmentOptions(eps=0.01)
+    m1, s1 = otprg.solve_assignment(inst, opt)
+    m2, s2 = sharded.solve_assignment_sharded(inst, opt, 8)
+    assert np.array_equal(m1.match_of_a, m2.match_of_a)
+    assert np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a)
+    assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b)
+    assert s1.phases == s2.phases and s1.sum_ni == s2.sum_ni
+
+
+def test_distributed_world1_nccl(golden):
+    import torch.distributed as dist
+    key = "square_n4000_eps0.01_s1"
+    v = golden[key]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("LOCAL_RANK", "0")
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        inst = otprg.gen_uniform_square(v["n_a"], v["seed"])
+        m, st = sharded.solve_assignment_distributed(inst, otprg.AssignmentOptions(eps=v["eps"]))
+        _check_golden(golden, key, m, st)
+    finally:
+        dist.destroy_process_group()
