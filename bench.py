@@ -46,6 +46,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "assignment solve time (ms) at n=10k, ε=0.01; propose-kernel HBM GB/s vs peak"
 N, EPS, SEEDS = 10000, 0.01, (1, 2, 3)
+N4 = 100_000  # config 4 (sharded rows)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -270,6 +271,9 @@ def run_ours(args, world, rank, local) -> None:
         line["e2e_points"] = e2e_points(otprg, local, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_ref(first)
+    if world == 1 and not args.no_config4:
+        # the 1-GPU point of the config-4 scaling curve (bench.py --gpus N runs it sharded)
+        line["config4_1gpu"] = run_sharded(args, world, rank, local, 3, 3)
     if rank == 0:
         print(json.dumps(line), flush=True)
     for sv in solvers:
@@ -323,6 +327,98 @@ def e2e_points(otprg, local, args) -> dict:
             "bit_exact": bool(ok)}
 
 
+def run_sharded(args, world, rank, local, steps: int, warmup: int) -> dict:
+    """Config 4: n=100k points, eps=0.01, A rows sharded across the ranks
+    (SURVEY §8(e)); one step = one full sharded solve with every rank's slab
+    resident (20 GB / N of uint16 kT: far larger than L2).  Timed with CUDA
+    events on each rank's solver stream, max over ranks."""
+    import paper_2203_03732_b200 as otprg
+    from paper_2203_03732_b200.sharded import ShardedSolver
+
+    inst = otprg.gen_uniform_square(N4, 1)
+    opt = otprg.AssignmentOptions(eps=EPS, storage=args.storage, device=local)
+    t0 = time.perf_counter()
+    sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1)
+    barrier(world)
+    prep_s = allreduce_max(time.perf_counter() - t0, world)
+    m, s = sv.solve()
+    for _ in range(warmup):
+        sv.solve()
+    times = []
+    barrier(world)
+    with ClockSampler(local) as clk:
+        for _ in range(steps):
+            sv.timer_start()
+            m, s = sv.solve()
+            times.append(sv.timer_stop())
+    barrier(world)
+    ms = allreduce_max(float(np.mean(times)), world)
+    P, R = int(s.phases), int(s.device["refill_rounds"])
+    out = {
+        "value": round(ms, 3), "unit": "ms", "n_gpus": world, "steps": steps, "warmup": warmup,
+        "phases": P, "sum_ni": int(s.sum_ni), "refill_rounds": R, "K": args.K,
+        "slab_build_ms": round(float(s.device["build_ms"]), 3),
+        "prepare_wall_s": round(prep_s, 3),
+        "gpu_launches_per_step": 4 + 4 * (P + R),
+        "clocks": clk.summary(),
+    }
+    sv.close()
+    if rank == 0 and not args.no_parity:
+        # bit-identity against the single-GPU fused solver (no CPU oracle
+        # finishes n=100k in bench time); outside the timed region
+        ref_m, ref_s = otprg.Solver(local).solve(inst, opt)
+        out["bit_identical_to_single_gpu_solver"] = bool(
+            np.array_equal(ref_m.match_of_a, m.match_of_a)
+            and np.array_equal(ref_s.duals_final.y_a, s.duals_final.y_a)
+            and np.array_equal(ref_s.duals_final.y_b, s.duals_final.y_b)
+            and np.array_equal(ref_s.free_counts, s.free_counts)
+            and ref_s.device["cost"] == s.device["cost"])
+        out["single_gpu_fused_solver_ms"] = round(float(ref_s.device["solve_ms"]), 3)
+    return out
+
+
+def run_config4(args, world, rank, local) -> None:
+    r = run_sharded(args, world, rank, local, args.steps, args.warmup)
+    # e2e: host point sets in, slab build + solve + results out, every step
+    import paper_2203_03732_b200 as otprg
+    from paper_2203_03732_b200.sharded import ShardedSolver
+    inst = otprg.gen_uniform_square(N4, 1)
+    opt = otprg.AssignmentOptions(eps=EPS, storage=args.storage, device=local)
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier(world)
+        import torch
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1)
+        sv.solve()
+        torch.cuda.synchronize()
+        e2e.append(allreduce_max(time.perf_counter() - t0, world) * 1e3)
+        sv.close()
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["value"],
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u16" if args.storage != "u8" else "u8", "data": "synthetic",
+        "config": {"workload": f"config 4: gen_uniform_square(n={N4}, seed 1) points, eps={EPS}, "
+                               f"A rows sharded across {world} GPU(s), per-rank uint16 kT slab "
+                               "built on the device from the points and resident",
+                   "l2": f"inputs larger than L2 ({N4 * N4 * 2 // world // 10**9} GB of kT per rank)",
+                   "parallelism": f"A-row shards x{world}, candidate all-gather per phase (NCCL)",
+                   "K": args.K},
+        "sharded": r,
+        "gpu_launches": r["gpu_launches_per_step"] * args.steps,
+        "clocks": r["clocks"],
+        "e2e": {"value": round(float(np.mean(e2e)), 3), "unit": "ms",
+                "h2d_bytes_per_step": N4 * 2 * 16,
+                "d2h_bytes_per_step": N4 * (4 + 4 + 8 + 8) + 8 * r["phases"],
+                "input": "2-D point sets in host memory; slab build, solve, D2H of matching/duals",
+                "timer": "wall clock between synchronised barriers, max over ranks"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_reference(args, world, rank) -> None:
     if rank != 0:
         return
@@ -372,12 +468,21 @@ def main() -> None:
     ap.add_argument("--storage", default="u16", choices=["u8", "u16", "auto"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--workload", default="auto", choices=["auto", "config2", "config4"],
+                    help="auto: config 2 on one GPU, config 4 (sharded n=100k) on N>1")
+    ap.add_argument("--K", type=int, default=16, help="candidates per shard per scan (config 4)")
+    ap.add_argument("--no-config4", action="store_true",
+                    help="skip the 1-GPU config-4 point in the config-2 line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup() if args.impl == "ours" or int(os.environ.get("WORLD_SIZE", "1")) == 1 \
         else (int(os.environ["WORLD_SIZE"]), int(os.environ.get("RANK", "0")), 0)
+    workload = args.workload if args.workload != "auto" else ("config2" if world == 1 else "config4")
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif workload == "config4":
+        run_config4(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

@@ -88,6 +88,8 @@ struct otprg_ctx {
   int sh_n = 0;              // proposers of the running phase
   int sh_parked = 0;         // chains waiting for a rescan
   int sh_park_cur = 0;       // which park buffer holds the waiting chains
+  bool sh_top_ready = false;  // the last DA call already ran the next phase's top
+  int sh_done = 0;
   DevBuf sh_bounds, sh_pos, sh_park[2], sh_list;
 
   // optimal transport (ot_host.cpp): per-phase scan inputs / outputs

@@ -90,8 +90,11 @@ struct ShardArgs {
   int64_t* free_counts;
   Ctl* ctl;
 };
-cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, cudaStream_t s);
-cudaError_t launch_shard_compact(const ShardArgs& a, cudaStream_t s);
+// cond: skip (both kernels) when the DA just before parked chains
+// (ctl->work[1] != 0), i.e. the phase is not complete yet.
+cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, bool cond,
+                             cudaStream_t s);
+cudaError_t launch_shard_compact(const ShardArgs& a, bool cond, cudaStream_t s);
 cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int32_t* cand,
                               int2* meta, cudaStream_t s);
 cudaError_t launch_shard_da(const ShardArgs& a, uint32_t phase, const int32_t* cand,

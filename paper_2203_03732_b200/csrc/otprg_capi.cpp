@@ -861,6 +861,7 @@ int otprg_shard_begin(otprg_ctx* ctx) {
   ctx->sh_phase = 0;
   ctx->sh_parked = 0;
   ctx->sh_n = 0;
+  ctx->sh_top_ready = false;
   ctx->begun = true;
   ctx->completed = false;
   return OTPRG_OK;
@@ -869,18 +870,20 @@ int otprg_shard_begin(otprg_ctx* ctx) {
 int otprg_shard_top(otprg_ctx* ctx, int32_t* n_out, int32_t* finished) {
   if (!ctx) return OTPRG_PARAMETER;
   if (!ctx->begun || !ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_shard_begin() first");
-  otprg::ShardArgs S = shard_args(ctx);
-  CK(otprg::launch_shard_top(S, ctx->sh_phase, ctx->sh_phase > 0, ctx->stream), "shard_top launch");
-  Ctl h{};
-  int st = read_ctl(ctx, &h);
-  if (st) return st;
-  ctx->sh_n = h.cnt[ctx->sh_phase & 1];
-  if (!h.done) {
-    CK(otprg::launch_shard_compact(S, ctx->stream), "shard_compact launch");
-    CK(cudaStreamSynchronize(ctx->stream), "compact");
+  if (!ctx->sh_top_ready) {  // (after a complete phase the DA call has run the top already)
+    otprg::ShardArgs S = shard_args(ctx);
+    CK(otprg::launch_shard_top(S, ctx->sh_phase, ctx->sh_phase > 0, false, ctx->stream),
+       "shard_top launch");
+    CK(otprg::launch_shard_compact(S, false, ctx->stream), "shard_compact launch");
+    Ctl h{};
+    int st = read_ctl(ctx, &h);
+    if (st) return st;
+    ctx->sh_n = h.cnt[ctx->sh_phase & 1];
+    ctx->sh_done = h.done;
   }
+  ctx->sh_top_ready = false;
   if (n_out) *n_out = ctx->sh_n;
-  if (finished) *finished = h.done;
+  if (finished) *finished = ctx->sh_done;
   return OTPRG_OK;
 }
 
@@ -909,12 +912,23 @@ int otprg_shard_da(otprg_ctx* ctx, const int32_t* cand, const int32_t* meta_word
   const int nchains = resume ? ctx->sh_parked : ctx->sh_n;
   CK(otprg::launch_shard_da(S, ctx->sh_phase + 1, cand, meta, nchains, resume_list, ctx->stream),
      "shard_da launch");
+  // If no chain parked the phase is complete: run the next top (apply M',
+  // termination, free list) in the same round trip; the kernels check.
+  otprg::ShardArgs T = S;
+  T.mp_prev = S.mp_out;
+  CK(otprg::launch_shard_top(T, ctx->sh_phase + 1, true, true, ctx->stream), "shard_top launch");
+  CK(otprg::launch_shard_compact(T, true, ctx->stream), "shard_compact launch");
   Ctl h{};
   int st = read_ctl(ctx, &h);
   if (st) return st;
   ctx->sh_park_cur ^= 1;
   ctx->sh_parked = h.work[1];
-  if (ctx->sh_parked == 0) ctx->sh_phase += 1;  // the phase is complete
+  if (ctx->sh_parked == 0) {  // the phase is complete
+    ctx->sh_phase += 1;
+    ctx->sh_n = h.cnt[ctx->sh_phase & 1];
+    ctx->sh_done = h.done;
+    ctx->sh_top_ready = true;
+  }
   if (parked) *parked = ctx->sh_parked;
   return OTPRG_OK;
 }

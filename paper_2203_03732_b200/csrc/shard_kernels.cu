@@ -139,8 +139,9 @@ __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4
 // Top of the phase after `phase_done` phases: apply M' of phase phase_done
 // (replicated), termination test, counters for the next phase.
 __global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t phase_done,
-                                                         int apply) {
+                                                         int apply, int cond) {
   Ctl* ctl = S.ctl;
+  if (cond && ctl->work[1] != 0) return;  // chains parked: the phase goes on
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
   const int par = phase_done & 1;
   if (apply) {
@@ -172,16 +173,16 @@ __global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t p
       const int nx = par ^ 1;  // counters the coming phase appends to
       ctl->cnt[nx] = 0;
       ctl->mp_cnt[nx] = 0;
-      ctl->exh[nx] = 0;
-      ctl->work[1] = 0;  // parked chains
+      ctl->exh[nx] = 0;  // (work[1], the parked count, is reset before every DA launch)
     }
   }
 }
 
 // The free list of the coming phase, ascending b (identical on every rank,
 // so list indices name the same b everywhere), and its inverse.  One block.
-__global__ void __launch_bounds__(1024) shard_compact_kernel(ShardArgs S) {
+__global__ void __launch_bounds__(1024) shard_compact_kernel(ShardArgs S, int cond) {
   __shared__ int s_scan[1024];
+  if (S.ctl->done || (cond && S.ctl->work[1] != 0)) return;
   const int n_b = S.ctl->n_b, tid = threadIdx.x, nt = blockDim.x;
   int32_t* out = const_cast<int32_t*>(S.list_in);
   const int chunk = (n_b + nt - 1) / nt;
@@ -290,13 +291,14 @@ __global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, uint32_t pha
 
 }  // namespace
 
-cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, cudaStream_t s) {
-  shard_top_kernel<<<148, 1024, 0, s>>>(a, phase_done, apply ? 1 : 0);
+cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, bool cond,
+                             cudaStream_t s) {
+  shard_top_kernel<<<148, 1024, 0, s>>>(a, phase_done, apply ? 1 : 0, cond ? 1 : 0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_shard_compact(const ShardArgs& a, cudaStream_t s) {
-  shard_compact_kernel<<<1, 1024, 0, s>>>(a);
+cudaError_t launch_shard_compact(const ShardArgs& a, bool cond, cudaStream_t s) {
+  shard_compact_kernel<<<1, 1024, 0, s>>>(a, cond ? 1 : 0);
   return cudaGetLastError();
 }
 

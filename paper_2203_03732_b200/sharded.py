@@ -146,49 +146,83 @@ def run_phases(ranks, exchange, cand_ptr: int, meta_ptr: int, cap: int, gather_a
     return rounds
 
 
+class ShardedSolver:
+    """Prepared sharded solve, reusable across solves of the same instance.
+
+    ``distributed=False``: all ``n_shards`` shards live in this process on
+    ``opt.device`` (LocalExchange).  ``distributed=True``: this process is
+    rank ``dist.get_rank()`` of ``dist.get_world_size()`` shards on GPU
+    LOCAL_RANK (TorchDistExchange over NCCL)."""
+
+    def __init__(self, inst: AssignmentInstance, opt: AssignmentOptions, n_shards: int = 1,
+                 K: int = K_DEFAULT, distributed: bool = False):
+        _check_options(inst, opt)
+        if inst.pts_a is None or inst.pts_b is None:
+            raise ParameterError("the sharded path builds slabs from 2-D point sets")
+        if distributed:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(), dist.get_world_size()
+            device = int(os.environ.get("LOCAL_RANK", opt.device))
+            self.ranks = [DeviceRank(device)]
+            self.ranks[0].prepare(inst, opt.eps, world, rank, K, opt.storage)
+            self.n_shards = world
+            self.exchange = TorchDistExchange(rank, world)
+        else:
+            device = opt.device
+            self.ranks = [DeviceRank(device) for _ in range(n_shards)]
+            for g, r in enumerate(self.ranks):
+                r.prepare(inst, opt.eps, n_shards, g, K, opt.storage)
+            self.n_shards = n_shards
+            self.exchange = LocalExchange()
+        self.cap = self.ranks[0].cap
+        self.cand, self.meta = _buffers(self.n_shards, self.cap, K, device)
+        self.gather_args = (self.cand, self.meta) if distributed else ()
+
+    def solve(self):
+        """One full solve (state re-initialised).  Returns (Matching,
+        SolveStats) of the first local rank after checking local ranks agree."""
+        rounds = run_phases(self.ranks, self.exchange, self.cand.data_ptr(), self.meta.data_ptr(),
+                            self.cap, self.gather_args)
+        outs = [r.finish() for r in self.ranks]
+        m0, s0 = outs[0]
+        for m, s in outs[1:]:
+            if not (np.array_equal(m.match_of_a, m0.match_of_a)
+                    and np.array_equal(s.duals_final.y_a, s0.duals_final.y_a)
+                    and np.array_equal(s.duals_final.y_b, s0.duals_final.y_b)):
+                raise RuntimeError("shards ended in different states")
+        s0.device["refill_rounds"] = rounds
+        s0.device["n_shards"] = self.n_shards
+        return m0, s0
+
+    def timer_start(self):
+        for r in self.ranks:
+            r.solver.timer_start()
+
+    def timer_stop(self) -> float:
+        return max(r.solver.timer_stop() for r in self.ranks)
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
+
+
 def solve_assignment_sharded(inst: AssignmentInstance, opt: AssignmentOptions, n_shards: int,
                              K: int = K_DEFAULT):
-    """All shards in this process on opt.device (LocalExchange).  Returns the
-    (Matching, SolveStats) of rank 0 after checking every rank agrees."""
-    _check_options(inst, opt)
-    if inst.pts_a is None:
-        raise ParameterError("the sharded path builds slabs from 2-D point sets")
-    ranks = [DeviceRank(opt.device) for _ in range(n_shards)]
-    for g, r in enumerate(ranks):
-        r.prepare(inst, opt.eps, n_shards, g, K, opt.storage)
-    cap = ranks[0].cap
-    cand, meta = _buffers(n_shards, cap, K, opt.device)
-    rounds = run_phases(ranks, LocalExchange(), cand.data_ptr(), meta.data_ptr(), cap)
-    outs = [r.finish() for r in ranks]
-    m0, s0 = outs[0]
-    for m, s in outs[1:]:
-        if not (np.array_equal(m.match_of_a, m0.match_of_a)
-                and np.array_equal(s.duals_final.y_a, s0.duals_final.y_a)
-                and np.array_equal(s.duals_final.y_b, s0.duals_final.y_b)):
-            raise RuntimeError("shards ended in different states")
-    s0.device["refill_rounds"] = rounds
-    s0.device["n_shards"] = n_shards
-    for r in ranks:
-        r.close()
-    return m0, s0
+    """All shards in this process on opt.device (LocalExchange): G logical
+    shards on one GPU.  Returns (Matching, SolveStats)."""
+    sv = ShardedSolver(inst, opt, n_shards, K)
+    try:
+        return sv.solve()
+    finally:
+        sv.close()
 
 
 def solve_assignment_distributed(inst: AssignmentInstance, opt: AssignmentOptions,
                                  K: int = K_DEFAULT):
     """One rank per process/GPU under torch.distributed (NCCL): each process
     calls this with the same instance; every rank returns the same result."""
-    import torch.distributed as dist
-    _check_options(inst, opt)
-    rank, world = dist.get_rank(), dist.get_world_size()
-    device = int(os.environ.get("LOCAL_RANK", opt.device))
-    r = DeviceRank(device)
-    r.prepare(inst, opt.eps, world, rank, K, opt.storage)
-    cap = r.cap
-    cand, meta = _buffers(world, cap, K, device)
-    ex = TorchDistExchange(rank, world)
-    rounds = run_phases([r], ex, cand.data_ptr(), meta.data_ptr(), cap, (cand, meta))
-    m, s = r.finish()
-    s.device["refill_rounds"] = rounds
-    s.device["n_shards"] = world
-    r.close()
-    return m, s
+    sv = ShardedSolver(inst, opt, K=K, distributed=True)
+    try:
+        return sv.solve()
+    finally:
+        sv.close()
