@@ -91,7 +91,8 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned target,
       atomicMax(arrive_max, now);
       if (arrive_min_inv) atomicMax(arrive_min_inv, ~now);
     }
-    __threadfence();
+    // release (cumulative: covers the block's writes ordered by the
+    // __syncthreads above) / acquire pair; no separate fences needed
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->bar_count) : "memory");
     if ((int)(ld_acquire(&ctl->bar_count) - target) < 0) {
       const unsigned long long t0 = globaltimer();
@@ -102,7 +103,6 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned target,
         }
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }

@@ -260,13 +260,24 @@ struct PhasePtrs {
   int* exh_out;
 };
 
+// A proposer's chain prologue (Y(b), low-set meta/entries, row min), loaded
+// at the top of the phase together with the phase counters so the first
+// chain of every warp starts without further dependent loads.
+struct Prefetch {
+  bool ok;
+  int i, b;
+  uint32_t yb, rowmin;
+  int4 meta;
+  unsigned long long ent;
+};
+
 template <typename T, bool kSmem>
 __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const PhasePtrs& P,
                                           const T* tp, int lda, uint32_t phase, uint32_t tmax,
                                           int lane, unsigned long long& bytes,
                                           unsigned long long& steps, unsigned long long& walks,
                                           unsigned* s_stat, unsigned long long* acc,
-                                          const Team& tm) {
+                                          const Team& tm, const Prefetch& pf, bool use_pf) {
   const bool lead = lane == 0 && tm.rank == 0;  // performs the chain's global side effects
 #define OTPRG_STAT(k) \
   if (lead) atomicAdd(&s_stat[k], 1u)
@@ -280,21 +291,33 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
   unsigned long long* H = (phase & 1) ? A.holder[1] : A.holder[0];             // this phase
   const unsigned long long* Hprev = (phase & 1) ? A.holder[0] : A.holder[1];   // phase - 1
 
-  uint32_t yb = (uint32_t)__ldcg(A.yb + b);
+  uint32_t yb;
+  int4 meta;  // low-set cache of b: (upto, cov, cnt, -)
+  unsigned long long ent = 0;
+  uint32_t rmin;
+  if (use_pf) {
+    yb = pf.yb;
+    meta = pf.meta;
+    ent = pf.ent;
+    rmin = pf.rowmin;
+  } else {
+    yb = (uint32_t)__ldcg(A.yb + b);
+    meta = __ldcg(A.lmeta + b);
+    if (lane < kLowCap) ent = __ldcg(A.lent + (size_t)b * kLowCap + lane);
+    rmin = (uint32_t)__ldcg(rowmin + b);
+    // every member has read b's state before the lead can update it
+    team_sync(tm);
+  }
   uint32_t target = yb - 1;
   int start = 0;
   bool fresh = true;  // b came from the free list (owns its low-set cache)
   uint32_t mnw = 0xffffffffu;
   bool track_min = false, dirty = false;
   LowBuild lb;
-  // low-set cache of b
-  int4 meta = __ldcg(A.lmeta + b);  // (upto, cov, cnt, -)
-  unsigned long long ent = 0;
-  if (lane < kLowCap) ent = __ldcg(A.lent + (size_t)b * kLowCap + lane);
   bool walk = meta.y > 0 && target <= (uint32_t)meta.x;
   bool skip = false;
   if (!walk) {
-    if ((uint32_t)__ldcg(rowmin + b) > target) {
+    if (rmin > target) {
       skip = true;  // row min too high: no admissible edge (min only grows)
       OTPRG_STAT(6);
     } else {  // full scan from position 0 (rebuilding the low set in warp mode)
@@ -378,10 +401,17 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       return;
     }
     const unsigned long long key = ((unsigned long long)cur_tag << 32) | (uint32_t)b;
-    unsigned long long old = 0;
+    unsigned long long old = 0, hp = 0;
+    int ma = -1;
     OTPRG_STAT(7);
     const unsigned long long ta0 = acc ? globaltimer() : 0;
-    if (lead) old = atomicMin(H + a, key);
+    if (lead) {
+      old = atomicMin(H + a, key);
+      // the partner lookup of a first take, issued with the atomic (both
+      // arrays are stable for entries it uses: see below)
+      hp = __ldcg(Hprev + a);
+      ma = __ldcg(A.match_a + a);
+    }
     old = team_bcast(tm, old, lane);
     if (acc) acc[1] += globaltimer() - ta0;
     const uint32_t old_tag = (uint32_t)(old >> 32);
@@ -413,9 +443,8 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       // phase is displaced (it is freed by apply_phase).  If a was matched in
       // the previous phase, that partner is the previous phase's winner (the
       // global matching is being updated concurrently at this phase's top);
-      // otherwise match_a, which is complete for all earlier phases.
-      const unsigned long long hp = __ldcg(Hprev + a);
-      const int ma = __ldcg(A.match_a + a);
+      // otherwise match_a, which is complete for all earlier phases (the
+      // apply of M'_{phase-1} only writes match_a of a in M'_{phase-1}).
       const int partner = (uint32_t)(hp >> 32) == prev_tag ? (int)(uint32_t)hp : ma;
       if (partner >= 0) {
         const int pos = atomicAdd(P.cnt_out, 1);
@@ -434,6 +463,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   T* s_t = reinterpret_cast<T*>(smem_raw);
   Ctl* ctl = A.ctl;
   const int lda = ctl->lda;
+  const int n_b = ctl->n_b;
   const int thresh = ctl->thresh;
   const uint32_t cap = (uint32_t)ctl->phase_cap;
   const uint32_t tmax = ctl->tmax;
@@ -474,15 +504,77 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   if (threadIdx.x < 8) s_stat[threadIdx.x] = 0;
   bool first = true;
   int n_prev = -1;
+  int tsize_prev = 1;  // team size of the previous phase: guess for the prefetch
+  const int wib = threadIdx.x >> 5;
+  const int n_a = ctl->n_a;
+  // Global part of apply M'_p (matching, global t), entries striped over the
+  // blocks (entry q = thread * grid + block).  The first entry of every
+  // thread is loaded speculatively at the top, in the same round trips as
+  // the phase counters and the chain prologue; only its stores wait.
+  auto apply_global = [&](const int2* mp_prev, const unsigned long long* Hq, int m_prev,
+                          uint32_t ph, int q0, int2 e0, int b0, uint32_t t0) {
+    for (int i = q0; i < m_prev; i += gthreads) {
+      int2 e;
+      int b;
+      uint32_t nt;
+      if (i == q0) {
+        e = e0;
+        b = b0;
+        nt = t0 + 1u;
+      } else {
+        e = __ldcg(mp_prev + i);
+        b = (int)(uint32_t)__ldcg(Hq + e.x);
+        nt = (uint32_t)__ldcg(tg + e.x) + 1u;
+      }
+      const int a = e.x, old_b = e.y;
+      if (old_b >= 0) A.match_b[old_b] = -1;
+      A.match_a[a] = b;
+      A.match_b[b] = a;
+      if (nt > tmax) report(ctl, 12, (int)ph, a, (int)nt);
+      tg[a] = (T)nt;
+    }
+  };
+  const int q0 = (int)threadIdx.x * (int)gridDim.x + (int)blockIdx.x;
   while (true) {
     const int r_prev = phase % 3, r_cur = (phase + 1) % 3, r_nxt = (phase + 2) % 3;
     // apply M'_{phase} unless the previous launch already did
     const bool apply = phase > 0 && !(first && applied0 == phase);
+    const int32_t* list_in = r_prev == 0 ? A.list[0] : (r_prev == 1 ? A.list[1] : A.list[2]);
+    const int2* mp_prev = A.mp[0];
+    if (r_prev == 1) mp_prev = A.mp[1];
+    if (r_prev == 2) mp_prev = A.mp[2];
+    const unsigned long long* Hq = (phase & 1) ? A.holder[1] : A.holder[0];  // phase's winners
     if (threadIdx.x == 0) {  // one read per block, broadcast: uniform branches
       s_ctl[0] = ld_cg(&ctl->status);
       s_ctl[1] = ld_cg(&ctl->cnt[r_prev]);
       s_ctl[2] = apply ? ld_cg(&ctl->mp_cnt[r_prev]) : 0;
       s_ctl[3] = ld_cg(&ctl->exh[r_prev]);
+    }
+    // Speculative loads in the same round trip as the counters: this warp's
+    // first proposer of the coming phase (static index under the previous
+    // team size; b is clamped, used only if the index is < n) and its chain
+    // prologue, and this thread's M' entry.
+    Prefetch pf;
+    pf.i = (wib / tsize_prev) * (int)gridDim.x + (int)blockIdx.x;
+    pf.ok = pf.i < n_b;
+    if (pf.ok) {
+      const int bb = min(max(__ldcg(list_in + pf.i), 0), n_b - 1);
+      pf.b = bb;
+      pf.yb = (uint32_t)__ldcg(A.yb + bb);
+      pf.meta = __ldcg(A.lmeta + bb);
+      pf.ent = lane < kLowCap ? __ldcg(A.lent + (size_t)bb * kLowCap + lane) : 0ull;
+      pf.rowmin = (uint32_t)__ldcg(static_cast<const T*>(A.rowmin) + bb);
+    }
+    int mp_a = -1;
+    if (kSmem && apply && (int)threadIdx.x < n_b) mp_a = __ldcg(&mp_prev[threadIdx.x].x);
+    int2 g_e = make_int2(0, -1);
+    int g_b = 0;
+    uint32_t g_t = 0;
+    if (apply && q0 < n_b) {
+      g_e = __ldcg(mp_prev + q0);
+      const int a = min(max(g_e.x, 0), n_a - 1);
+      g_b = (int)(uint32_t)__ldcg(Hq + a);
+      g_t = (uint32_t)__ldcg(tg + a);
     }
     __syncthreads();
     const int status = s_ctl[0], n = s_ctl[1], m_prev = s_ctl[2], x_prev = s_ctl[3];
@@ -495,28 +587,14 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     first = false;
 
     // ---- apply M'_{phase}: shared t (every block) and the global state ----
-    const int2* mp_prev = A.mp[0];
-    if (r_prev == 1) mp_prev = A.mp[1];
-    if (r_prev == 2) mp_prev = A.mp[2];
-    const unsigned long long* Hq = (phase & 1) ? A.holder[1] : A.holder[0];  // phase's winners
     if (m_prev > 0) {
       if constexpr (kSmem) {
         for (int i = threadIdx.x; i < m_prev; i += blockDim.x) {
-          const int a = __ldcg(&mp_prev[i].x);
+          const int a = i < n_b && i == (int)threadIdx.x ? mp_a : __ldcg(&mp_prev[i].x);
           s_t[a] = (T)(s_t[a] + 1);  // each a appears once
         }
       }
-      for (int i = gtid; i < m_prev; i += gthreads) {
-        const int2 e = __ldcg(mp_prev + i);
-        const int a = e.x, old_b = e.y;
-        const int b = (int)(uint32_t)__ldcg(Hq + a);
-        if (old_b >= 0) A.match_b[old_b] = -1;
-        A.match_a[a] = b;
-        A.match_b[b] = a;
-        const uint32_t nt = (uint32_t)__ldcg(tg + a) + 1u;
-        if (nt > tmax) report(ctl, 12, (int)phase, a, (int)nt);
-        tg[a] = (T)nt;
-      }
+      apply_global(mp_prev, Hq, m_prev, phase, q0, g_e, g_b, g_t);
       if (leader) ctl->applied = phase;
     }
     __syncthreads();
@@ -575,7 +653,6 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     const T* tp = kSmem ? s_t : tg;
 
     // ---- P step: proposal chains over the free list of phase `phase` ----
-    const int32_t* list_in = r_prev == 0 ? A.list[0] : (r_prev == 1 ? A.list[1] : A.list[2]);
     PhasePtrs P;
     P.list_out = r_cur == 0 ? A.list[0] : (r_cur == 1 ? A.list[1] : A.list[2]);
     P.mp_out = r_cur == 0 ? A.mp[0] : (r_cur == 1 ? A.mp[1] : A.mp[2]);
@@ -591,8 +668,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       else if (n * 4 <= total_warps) tsize = 4;
       else if (n * 2 <= total_warps) tsize = 2;
     }
-    const int wib = threadIdx.x >> 5;
-    if (kBulk && n >= total_warps) {
+    const bool bulk = kBulk && n >= total_warps;
+    if (bulk) {
       // Large phase: first stream every proposer's row once at full HBM
       // bandwidth (warps in flight, no dependent atomics), recording its
       // admissible positions (level 0 of the low-set cache) and row minimum;
@@ -628,10 +705,19 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     unsigned long long acc[2] = {0ull, 0ull};
     const unsigned long long tp0 = tr ? globaltimer() : 0;
     const bool had_work = i < n;
+    // The prefetched prologue is current unless the bulk build rewrote it.
+    // All warps of a team must take their prologue from the same place (a
+    // team's lead may update Y(b) / the cache of b before a late member
+    // reads them), hence the same-team-size condition.
+    bool use_pf = pf.ok && !bulk && i == pf.i && tsize == tsize_prev;
+    const bool single = n <= total_teams;  // every team has at most its static proposer
+    tsize_prev = tsize;
     while (i < n) {
-      const int b = __ldcg(list_in + i);
+      const int b = use_pf ? pf.b : __ldcg(list_in + i);
       run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
-                          tr ? acc : nullptr, tm);
+                          tr ? acc : nullptr, tm, pf, use_pf);
+      use_pf = false;
+      if (single) break;
       unsigned long long nx = 0;
       if (lane == 0 && tm.rank == 0) nx = (unsigned long long)(total_teams + atomicAdd(&ctl->work[r_cur], 1));
       i = (int)team_bcast(tm, nx, lane);
