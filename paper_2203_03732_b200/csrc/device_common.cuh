@@ -26,10 +26,10 @@ struct Ctl {
   int32_t mp_cnt[3];    // first-held-a list sizes (rotating)
   int32_t work[3];      // dynamic proposer-grab counters (rotating)
   int32_t exh[3];       // b's that ended their chain unmatched (rotating)
+  int32_t slots[3];     // output slots reserved (= chains run) per list (rotating)
   int32_t status;       // 0 ok, else otprg_status / device diagnostic code
   int32_t done;         // 1 once the termination test passed
   int32_t full_match;   // n_i == 0 at termination
-  int32_t pad0;
   int64_t sum_ni;
   unsigned long long bytes_touched;
   unsigned long long chain_steps;
@@ -38,6 +38,8 @@ struct Ctl {
   // low-set cache, 3 exhausted by a complete cache, 4 scans continuing past
   // the cache, 5 full rescans (cache rebuilt), 6 rowmin skips, 7 proposals
   unsigned long long stat[8];
+  // %globaltimer span of the phase-1 propose scan (first block start, last warp end)
+  unsigned long long prop_t0, prop_t1;
   // grid barrier (monotone arrival count)
   unsigned int bar_count;
   unsigned int bar_base;  // bar_count at the start of the next launch (written at exit)

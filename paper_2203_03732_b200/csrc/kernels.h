@@ -42,6 +42,7 @@ struct SolveArgs {
   int64_t* free_counts;         // [phase_cap + 1]
   Ctl* ctl;
   uint32_t max_phase;           // run phases up to and including this one
+  int32_t pre_scanned;          // phase-1 lists/rowmin built by launch_propose_stream
   // Optional device timeline (%globaltimer ns), kTraceSlots u64 per phase, indexed by
   // phase - 1; nullptr disables tracing.
   unsigned long long* trace;
@@ -114,6 +115,12 @@ cudaError_t launch_phase_loop(const SolveArgs& a, int width, bool smem_t, int ld
                               cudaStream_t s);
 int phase_loop_grid(int width, bool smem_t, int lda, int num_sms);
 size_t phase_loop_smem(int width, bool smem_t, int lda);
+// Phase-1 propose scan (propose_kernels.cu): every row's k == 0 positions
+// (low-set level 0) and row minimum, streamed once with TMA bulk copies.
+int propose_stream_chunk(int width, int lda);
+cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, int4* lmeta,
+                                  unsigned long long* lent, void* rowmin, Ctl* ctl, int num_sms,
+                                  cudaStream_t s);
 bool smem_t_fits(int width, int lda);
 cudaError_t launch_complete(int32_t* match_a, int32_t* match_b, int n_a, int n_b,
                             int32_t* scratch_a, int32_t* scratch_b, cudaStream_t s);

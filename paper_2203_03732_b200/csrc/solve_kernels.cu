@@ -255,9 +255,10 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
 struct PhasePtrs {
   int32_t* list_out;  // free b's of the next phase
   int2* mp_out;       // (a, previous partner) first held this phase
-  int* cnt_out;
-  int* mp_cnt_out;
-  int* exh_out;
+  int* cnt_out;       // free b's of the next phase (count only: red.add)
+  int* mp_cnt_out;    // first takes (count only)
+  int* exh_out;       // exhausted b's (count only)
+  int* slot_out;      // output slot reservations: one per chain
 };
 
 // A proposer's chain prologue (Y(b), low-set meta/entries, row min), loaded
@@ -282,6 +283,11 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
 #define OTPRG_STAT(k) \
   if (lead) atomicAdd(&s_stat[k], 1u)
   OTPRG_STAT(0);
+  // Every chain ends in exactly one event (b exhausted, or a first take of
+  // some a), written to its own output slot: the slot is reserved now, so
+  // the reservation's round trip overlaps the chain instead of ending it.
+  int slot = 0;
+  if (lead) slot = atomicAdd(P.slot_out, 1);
   using S = Simd<T>;
   Ctl* ctl = A.ctl;
   const T* kT = static_cast<const T*>(A.kT);
@@ -394,8 +400,9 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
         if (fresh && dirty) A.lmeta[b] = meta;
         if (yb + 1 > tmax) report(ctl, 11, (int)phase, b, (int)yb);
         A.yb[b] = (int32_t)(yb + 1);
-        const int pos = atomicAdd(P.cnt_out, 1);
-        P.list_out[pos] = b;
+        P.list_out[slot] = b;
+        P.mp_out[slot] = make_int2(-1, -1);
+        atomicAdd(P.cnt_out, 1);  // results unused: compiled to fire-and-forget reductions
         atomicAdd(P.exh_out, 1);
       }
       return;
@@ -447,11 +454,11 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       // apply of M'_{phase-1} only writes match_a of a in M'_{phase-1}).
       const int partner = (uint32_t)(hp >> 32) == prev_tag ? (int)(uint32_t)hp : ma;
       if (partner >= 0) {
-        const int pos = atomicAdd(P.cnt_out, 1);
-        P.list_out[pos] = partner;
+        atomicAdd(P.cnt_out, 1);
       }
-      const int pos = atomicAdd(P.mp_cnt_out, 1);
-      P.mp_out[pos] = make_int2(a, partner);
+      P.list_out[slot] = partner;  // -1: a hole in the next list
+      P.mp_out[slot] = make_int2(a, partner);
+      atomicAdd(P.mp_cnt_out, 1);
     }
     return;
   }
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     const int nvec = lda * (int)sizeof(T) / 16;
     for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = __ldcg(src + i);
   }
-  __shared__ int s_ctl[4];
+  __shared__ int s_ctl[5];
   __shared__ unsigned long long s_team[kBlock / 32][10];  // team broadcast slots
   __shared__ unsigned s_stat[8];
   if (threadIdx.x < 8) s_stat[threadIdx.x] = 0;
@@ -511,9 +518,9 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   // blocks (entry q = thread * grid + block).  The first entry of every
   // thread is loaded speculatively at the top, in the same round trips as
   // the phase counters and the chain prologue; only its stores wait.
-  auto apply_global = [&](const int2* mp_prev, const unsigned long long* Hq, int m_prev,
+  auto apply_global = [&](const int2* mp_prev, const unsigned long long* Hq, int m_slots,
                           uint32_t ph, int q0, int2 e0, int b0, uint32_t t0) {
-    for (int i = q0; i < m_prev; i += gthreads) {
+    for (int i = q0; i < m_slots; i += gthreads) {
       int2 e;
       int b;
       uint32_t nt;
@@ -523,10 +530,12 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
         nt = t0 + 1u;
       } else {
         e = __ldcg(mp_prev + i);
+        if (e.x < 0) continue;  // slot of an exhausted chain
         b = (int)(uint32_t)__ldcg(Hq + e.x);
         nt = (uint32_t)__ldcg(tg + e.x) + 1u;
       }
       const int a = e.x, old_b = e.y;
+      if (a < 0) continue;
       if (old_b >= 0) A.match_b[old_b] = -1;
       A.match_a[a] = b;
       A.match_b[b] = a;
@@ -549,6 +558,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       s_ctl[1] = ld_cg(&ctl->cnt[r_prev]);
       s_ctl[2] = apply ? ld_cg(&ctl->mp_cnt[r_prev]) : 0;
       s_ctl[3] = ld_cg(&ctl->exh[r_prev]);
+      s_ctl[4] = ld_cg(&ctl->slots[r_prev]);
     }
     // Speculative loads in the same round trip as the counters: this warp's
     // first proposer of the coming phase (static index under the previous
@@ -558,8 +568,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     pf.i = (wib / tsize_prev) * (int)gridDim.x + (int)blockIdx.x;
     pf.ok = pf.i < n_b;
     if (pf.ok) {
-      const int bb = min(max(__ldcg(list_in + pf.i), 0), n_b - 1);
-      pf.b = bb;
+      pf.b = __ldcg(list_in + pf.i);  // may be a hole (-1)
+      const int bb = min(max(pf.b, 0), n_b - 1);
       pf.yb = (uint32_t)__ldcg(A.yb + bb);
       pf.meta = __ldcg(A.lmeta + bb);
       pf.ent = lane < kLowCap ? __ldcg(A.lent + (size_t)bb * kLowCap + lane) : 0ull;
@@ -571,13 +581,14 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     int g_b = 0;
     uint32_t g_t = 0;
     if (apply && q0 < n_b) {
-      g_e = __ldcg(mp_prev + q0);
+      g_e = __ldcg(mp_prev + q0);  // may be a hole (a = -1)
       const int a = min(max(g_e.x, 0), n_a - 1);
       g_b = (int)(uint32_t)__ldcg(Hq + a);
       g_t = (uint32_t)__ldcg(tg + a);
     }
     __syncthreads();
     const int status = s_ctl[0], n = s_ctl[1], m_prev = s_ctl[2], x_prev = s_ctl[3];
+    const int n_slots = s_ctl[4];  // slots of list_in / mp_prev (holes are -1)
     __syncthreads();
     if (leader && !first) {
       ctl->phase = phase;  // published only after a grid barrier of this launch
@@ -589,12 +600,12 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     // ---- apply M'_{phase}: shared t (every block) and the global state ----
     if (m_prev > 0) {
       if constexpr (kSmem) {
-        for (int i = threadIdx.x; i < m_prev; i += blockDim.x) {
+        for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
           const int a = i < n_b && i == (int)threadIdx.x ? mp_a : __ldcg(&mp_prev[i].x);
-          s_t[a] = (T)(s_t[a] + 1);  // each a appears once
+          if (a >= 0) s_t[a] = (T)(s_t[a] + 1);  // each a appears once
         }
       }
-      apply_global(mp_prev, Hq, m_prev, phase, q0, g_e, g_b, g_t);
+      apply_global(mp_prev, Hq, n_slots, phase, q0, g_e, g_b, g_t);
       if (leader) ctl->applied = phase;
     }
     __syncthreads();
@@ -648,6 +659,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       ctl->mp_cnt[r_nxt] = 0;
       ctl->work[r_nxt] = 0;
       ctl->exh[r_nxt] = 0;
+      ctl->slots[r_nxt] = 0;
       if (tr) tr[0] = globaltimer(), tr[7] = (unsigned long long)n;
     }
     const T* tp = kSmem ? s_t : tg;
@@ -659,24 +671,27 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     P.cnt_out = &ctl->cnt[r_cur];
     P.mp_cnt_out = &ctl->mp_cnt[r_cur];
     P.exh_out = &ctl->exh[r_cur];
+    P.slot_out = &ctl->slots[r_cur];
     // Team size for this phase: few proposers -> several warps per row
     // (uniform over the grid since n is).  First proposer of every team is
     // static, striped across blocks; the rest are grabbed from a counter.
-    int tsize = 1;
+    int tsize = 1;  // (proposers are assigned by slot: size by the slot count)
     if (kTeams) {
-      if (n * 8 <= total_warps) tsize = 8;
-      else if (n * 4 <= total_warps) tsize = 4;
-      else if (n * 2 <= total_warps) tsize = 2;
+      if (n_slots * 8 <= total_warps) tsize = 8;
+      else if (n_slots * 4 <= total_warps) tsize = 4;
+      else if (n_slots * 2 <= total_warps) tsize = 2;
     }
-    const bool bulk = kBulk && n >= total_warps;
+    // (phase 1's lists come from the streaming propose kernel when it ran)
+    const bool bulk = kBulk && n >= total_warps && !(phase == 1 && A.pre_scanned);
     if (bulk) {
       // Large phase: first stream every proposer's row once at full HBM
       // bandwidth (warps in flight, no dependent atomics), recording its
       // admissible positions (level 0 of the low-set cache) and row minimum;
       // the chains below then mostly walk these lists.
       Team solo{1, 0, 0u, s_team[wib]};
-      for (int q = wib * (int)gridDim.x + (int)blockIdx.x; q < n; q += total_warps) {
+      for (int q = wib * (int)gridDim.x + (int)blockIdx.x; q < n_slots; q += total_warps) {
         const int b = __ldcg(list_in + q);
+        if (b < 0) continue;
         const uint32_t target = (uint32_t)__ldcg(A.yb + b) - 1u;
         const int4 meta0 = __ldcg(A.lmeta + b);
         if (meta0.y >= lda && target <= (uint32_t)meta0.x) continue;  // complete & valid
@@ -704,18 +719,19 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     int i = tib * (int)gridDim.x + (int)blockIdx.x;
     unsigned long long acc[2] = {0ull, 0ull};
     const unsigned long long tp0 = tr ? globaltimer() : 0;
-    const bool had_work = i < n;
+    const bool had_work = i < n_slots;
     // The prefetched prologue is current unless the bulk build rewrote it.
     // All warps of a team must take their prologue from the same place (a
     // team's lead may update Y(b) / the cache of b before a late member
     // reads them), hence the same-team-size condition.
     bool use_pf = pf.ok && !bulk && i == pf.i && tsize == tsize_prev;
-    const bool single = n <= total_teams;  // every team has at most its static proposer
+    const bool single = n_slots <= total_teams;  // every team has at most its static slot
     tsize_prev = tsize;
-    while (i < n) {
+    while (i < n_slots) {
       const int b = use_pf ? pf.b : __ldcg(list_in + i);
-      run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
-                          tr ? acc : nullptr, tm, pf, use_pf);
+      if (b >= 0)
+        run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
+                            tr ? acc : nullptr, tm, pf, use_pf);
       use_pf = false;
       if (single) break;
       unsigned long long nx = 0;
