@@ -152,6 +152,54 @@ int otprg_step(otprg_ctx* ctx, int64_t max_phases, int64_t* phases_done, int32_t
 int otprg_snapshot(otprg_ctx* ctx, otprg_result* res);
 int otprg_finish(otprg_ctx* ctx, otprg_result* res);
 
+/* ---- invariant suite (reference A12) ----------------
+ * verify_feasibility (assignment.cpp:264-312) evaluated on the device.  The
+ * result is the number of violations and the FIRST one in the reference's
+ * order of checks (Matching::validate core.cpp:69-86 a then b; per demand a:
+ * positive dual, free with nonzero dual, |Y| > dual_bound; per supply b:
+ * negative dual, |Y| > dual_bound; every edge a-major: matched edge not
+ * tight, else Y(a)+Y(b) > k+1), i.e. report.violations.front().  When the
+ * matching itself is inconsistent the reference stops there: violations = 1.
+ * Indices are in the orientation of the checked state (the solver's
+ * internal one for otprg_verify_feasibility). */
+enum {
+  OTPRG_VIOL_NONE = 0,
+  OTPRG_VIOL_MATCH_A = 1,         /* matching is not mutually consistent at a= */
+  OTPRG_VIOL_MATCH_B = 2,         /* ... at b= */
+  OTPRG_VIOL_DEMAND_POSITIVE = 3, /* demand dual positive at a= */
+  OTPRG_VIOL_FREE_NONZERO = 4,    /* free demand vertex with nonzero dual at a= */
+  OTPRG_VIOL_DEMAND_BOUND = 5,    /* demand dual magnitude exceeds bound at a= */
+  OTPRG_VIOL_SUPPLY_NEGATIVE = 6, /* supply dual negative at b= */
+  OTPRG_VIOL_SUPPLY_BOUND = 7,    /* supply dual magnitude exceeds bound at b= */
+  OTPRG_VIOL_NOT_TIGHT = 8,       /* matching edge not tight at (a,b) */
+  OTPRG_VIOL_EXCEEDS = 9          /* dual sum exceeds rounded cost allowance at (a,b) */
+};
+typedef struct otprg_feasibility {
+  int64_t violations;
+  int32_t kind;        /* OTPRG_VIOL_* of the first violation */
+  int32_t a, b;        /* its vertices (-1 when not applicable) */
+  int32_t pad;
+  int64_t sum;         /* Y(a)+Y(b) for edge kinds, else the offending dual */
+  int64_t k;           /* k(a,b) for edge kinds */
+} otprg_feasibility;
+
+/* The context's current solver state (between phases of the stepping API,
+ * i.e. what check_invariants sees after apply_phase, assignment.cpp:344-349). */
+int otprg_verify_feasibility(otprg_ctx* ctx, otprg_feasibility* out);
+/* Arbitrary state, the reference's verify_feasibility(sc, duals, m):
+ * k row-major n_a x n_b int32 (ScaledCosts::k), dual bound unit_ceil + 2. */
+int otprg_verify_host(otprg_ctx* ctx, int32_t n_a, int32_t n_b, const int32_t* k,
+                      int32_t unit_ceil, const int64_t* y_a, const int64_t* y_b,
+                      const int32_t* match_of_a, const int32_t* match_of_b,
+                      otprg_feasibility* out);
+/* collect_workset's B' and E' for the current state (assignment.cpp:107-147,
+ * internal orientation): b_free ascending (n_free entries, caller buffer of
+ * n_b), offsets[n_free + 1] and the admissible a of every free b ascending in
+ * a_list.  a_list == NULL or a_cap < n_edges: only n_free / n_edges / b_free
+ * / offsets are written (call again with a larger buffer). */
+int otprg_admissible(otprg_ctx* ctx, int32_t* b_free, int64_t* offsets, int32_t* a_list,
+                     int64_t a_cap, int64_t* n_free, int64_t* n_edges);
+
 /* Rounded costs k(a,b) = scaled_floor(c(a,b), eps) computed on the device
  * and returned row-major (n_a x n_b int32, like ScaledCosts::k), plus
  * unit_floor / unit_ceil (core.hpp:89-92).  Mirrors otpr::scale_round_costs. */

@@ -7,7 +7,8 @@ from .api import (  # noqa: F401
     InvariantViolation, Matching, NumericalError, ParameterError, ScaledCosts, SolveStats, Solver,
     gen_uniform_square, get_solver, l1_cost, load_mnist_pair, matching_cost, points_cost,
     scale_round_costs, scaled_floor, solve_assignment, OTInstance, TransportPlan, ScaledMasses,
-    gen_random_ot_rational, scale_and_round, solve_ot,
+    gen_random_ot_rational, scale_and_round, solve_ot, FeasibilityReport, PhaseSnapshot,
+    PhaseWorkset, verify_feasibility,
 )
 
 __all__ = [
@@ -16,5 +17,6 @@ __all__ = [
     "ScaledCosts", "SolveStats", "Solver", "gen_uniform_square", "get_solver", "l1_cost",
     "load_mnist_pair", "matching_cost", "points_cost", "scale_round_costs", "scaled_floor",
     "solve_assignment", "OTInstance", "TransportPlan", "ScaledMasses", "gen_random_ot_rational",
-    "scale_and_round", "solve_ot",
+    "scale_and_round", "solve_ot", "FeasibilityReport", "PhaseSnapshot", "PhaseWorkset",
+    "verify_feasibility",
 ]

@@ -49,6 +49,13 @@ class Result(C.Structure):
     ]
 
 
+class Feasibility(C.Structure):
+    _fields_ = [
+        ("violations", C.c_int64), ("kind", C.c_int32), ("a", C.c_int32), ("b", C.c_int32),
+        ("pad", C.c_int32), ("sum", C.c_int64), ("k", C.c_int64),
+    ]
+
+
 EXPORTS = [
     "otprg_create", "otprg_destroy", "otprg_last_error", "otprg_version", "otprg_scaled_floor",
     "otprg_solve_assignment", "otprg_prepare", "otprg_solve_prepared", "otprg_scale_round_costs",
@@ -57,7 +64,7 @@ EXPORTS = [
     "otprg_set_trace", "otprg_get_trace", "otprg_load_mnist_pair", "otprg_solve_ot",
     "otprg_ot_scale_and_round", "otprg_random_ot_rational", "otprg_shard_prepare",
     "otprg_shard_begin", "otprg_shard_top", "otprg_shard_scan", "otprg_shard_da",
-    "otprg_shard_finish",
+    "otprg_shard_finish", "otprg_verify_feasibility", "otprg_verify_host", "otprg_admissible",
 ]
 
 _lib = None
@@ -113,6 +120,11 @@ def lib() -> C.CDLL:
     L.otprg_shard_scan.argtypes = [vp, vp, vp, C.c_int32, C.c_int32]
     L.otprg_shard_da.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
     L.otprg_shard_finish.argtypes = [vp, C.POINTER(Result)]
+    L.otprg_verify_feasibility.argtypes = [vp, C.POINTER(Feasibility)]
+    L.otprg_verify_host.argtypes = [vp, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp, vp, vp,
+                                    C.POINTER(Feasibility)]
+    L.otprg_admissible.argtypes = [vp, vp, vp, vp, C.c_int64, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int64)]
     _lib = L
     return L
 

@@ -173,12 +173,80 @@ class SolveStats:
 
 
 @dataclass
+class PhaseWorkset:
+    """assignment.hpp:20-33 (internal orientation): B', E' (admissible a of
+    every free b, ascending), A', and the phase products M', A'', M''."""
+    b_free: np.ndarray
+    e_admissible: list
+    a_touched: np.ndarray
+    m_prime: list
+    a_double: list
+    m_double: list
+
+    def edge_count(self) -> int:
+        return int(sum(len(e) for e in self.e_admissible))
+
+
+@dataclass
+class PhaseSnapshot:
+    """assignment.hpp:57-67: handed to the observer after each phase, in the
+    solver's internal orientation."""
+    phase: int
+    costs: "ScaledCosts"
+    duals: DualState
+    matching: Matching
+    workset: PhaseWorkset
+    sum_abs_before: int
+    sum_abs_after: int
+
+
+@dataclass
+class FeasibilityReport:
+    """assignment.hpp:116-120.  The device suite reports the first violation
+    in the reference's order (the message check_invariants throws) and the
+    number of violations; ``violations`` holds that first message, ``count``
+    the total."""
+    violations: list = field(default_factory=list)
+    notes: list = field(default_factory=list)
+    count: int = 0
+    kind: int = 0
+    a: int = -1
+    b: int = -1
+
+    def ok(self) -> bool:
+        return not self.violations
+
+
+_VIOL_MSG = {
+    1: "matching is not mutually consistent at a={a}",
+    2: "matching is not mutually consistent at b={b}",
+    3: "demand dual positive at a={a}",
+    4: "free demand vertex with nonzero dual at a={a}",
+    5: "demand dual magnitude exceeds bound at a={a}",
+    6: "supply dual negative at b={b}",
+    7: "supply dual magnitude exceeds bound at b={b}",
+    8: "matching edge not tight at ({a},{b}): Y(a)+Y(b)={s} k={k}",
+    9: "dual sum exceeds rounded cost allowance at ({a},{b}): Y(a)+Y(b)={s} k={k}",
+}
+
+
+def _report(f: "N.Feasibility") -> FeasibilityReport:
+    """verify_feasibility's report strings (assignment.cpp:270-311, core.cpp:69-86)."""
+    if f.violations == 0:
+        return FeasibilityReport()
+    msg = _VIOL_MSG[f.kind].format(a=f.a, b=f.b, s=f.sum, k=f.k)
+    return FeasibilityReport(violations=[msg], count=int(f.violations), kind=int(f.kind), a=int(f.a),
+                             b=int(f.b))
+
+
+@dataclass
 class AssignmentOptions:
     """assignment.hpp:69-90.  ``threads`` is accepted and ignored: the device
     path always has threads=1 (deterministic) semantics.  ``observer`` and
-    ``check_invariants`` need the host-synced debug loop, which this round does
-    not provide; they raise ParameterError rather than being silently
-    ignored.  ``storage`` selects the device width of the rounded matrix."""
+    ``check_invariants`` switch to the host-synced stepping loop (one phase
+    per launch; the device invariant suite after every phase; the
+    PhaseSnapshot built from device exports), as the reference runs them
+    inside solve_oriented (assignment.cpp:344-355).  ``storage`` selects the device width of the rounded matrix."""
     eps: float = 0.1
     threads: int = 1
     check_invariants: bool = False
@@ -342,6 +410,52 @@ class Solver:
             self._raise(st)
         return ScaledCosts(eps, k, uf.value, uc.value)
 
+    # -- invariant suite / workset export --
+    def verify_feasibility(self) -> FeasibilityReport:
+        """verify_feasibility on the device state between phases (internal
+        orientation)."""
+        f = N.Feasibility()
+        st = self._L.otprg_verify_feasibility(self._ctx, C.byref(f))
+        if st:
+            self._raise(st)
+        return _report(f)
+
+    def verify_host(self, sc: "ScaledCosts", duals: DualState, m: Matching) -> FeasibilityReport:
+        k = np.ascontiguousarray(sc.k, np.int32)
+        n_a, n_b = k.shape
+        ya = np.ascontiguousarray(duals.y_a, np.int64)
+        yb = np.ascontiguousarray(duals.y_b, np.int64)
+        ma = np.ascontiguousarray(m.match_of_a, np.int32)
+        mb = np.ascontiguousarray(m.match_of_b, np.int32)
+        if len(ya) != n_a or len(yb) != n_b or len(ma) != n_a or len(mb) != n_b:
+            raise ParameterError("state sizes do not match the cost matrix")
+        f = N.Feasibility()
+        st = self._L.otprg_verify_host(self._ctx, n_a, n_b, k.ctypes.data, int(sc.unit_ceil),
+                                       ya.ctypes.data, yb.ctypes.data, ma.ctypes.data,
+                                       mb.ctypes.data, C.byref(f))
+        if st:
+            self._raise(st)
+        return _report(f)
+
+    def admissible(self, n_b: int):
+        """(B', E') of the current state: free b ascending and the admissible
+        a of each, ascending (collect_workset, assignment.cpp:107-147)."""
+        bfree = np.empty(n_b, np.int32)
+        offs = np.empty(n_b + 1, np.int64)
+        nf, ne = C.c_int64(), C.c_int64()
+        st = self._L.otprg_admissible(self._ctx, bfree.ctypes.data, offs.ctypes.data, None, 0,
+                                      C.byref(nf), C.byref(ne))
+        if st:
+            self._raise(st)
+        alist = np.empty(max(int(ne.value), 1), np.int32)
+        if ne.value:
+            st = self._L.otprg_admissible(self._ctx, bfree.ctypes.data, offs.ctypes.data,
+                                          alist.ctypes.data, alist.size, C.byref(nf), C.byref(ne))
+            if st:
+                self._raise(st)
+        n = int(nf.value)
+        return bfree[:n].copy(), [alist[offs[i]:offs[i + 1]].copy() for i in range(n)]
+
     def flush_l2(self) -> None:
         st = self._L.otprg_flush_l2(self._ctx)
         if st:
@@ -404,15 +518,83 @@ def _check_options(inst: AssignmentInstance, opt: AssignmentOptions) -> None:
         raise ParameterError("copy mode needs both demand and supply groups")
     if opt.demand_groups is not None:
         raise ParameterError("copy mode (demand/supply groups) is not provided by the device path")
-    if opt.observer is not None or opt.check_invariants:
-        raise ParameterError("observer/check_invariants need the host-synced debug loop, "
-                             "which the device path does not provide")
 
 
 def solve_assignment(inst: AssignmentInstance, opt: AssignmentOptions):
     """assignment.hpp:137-138 / assignment.cpp:368-400 -> (Matching, SolveStats)."""
     _check_options(inst, opt)
+    if opt.observer is not None or opt.check_invariants:
+        return _solve_debug(get_solver(opt.device), inst, opt)
     return get_solver(opt.device).solve(inst, opt)
+
+
+def _internal(m: Matching, swapped: bool) -> Matching:
+    return Matching(m.match_of_b, m.match_of_a) if swapped else m
+
+
+def _solve_debug(sv: Solver, inst: AssignmentInstance, opt: AssignmentOptions):
+    """The host-synced form of solve_oriented (assignment.cpp:316-364): one
+    device phase per step; after it the device invariant suite
+    (check_invariants, :344-349) and the observer (:350-355) see the state in
+    the internal orientation.  Results are those of the fused solve."""
+    swapped = inst.n_b > inst.n_a
+    n_b_int = min(inst.n_a, inst.n_b)
+    costs = None
+    if opt.observer is not None:  # ScaledCosts in the internal orientation (prepares too)
+        sc = sv.scale_round_costs(inst, opt.eps, opt.storage)
+        costs = ScaledCosts(sc.eps, np.ascontiguousarray(sc.k.T) if swapped else sc.k,
+                            sc.unit_floor, sc.unit_ceil)
+    else:
+        sv.prepare(inst, opt.eps, opt.storage)
+    sv._prepared = (inst.n_a, inst.n_b, opt.eps)
+    sv.begin()
+    threshold = opt.eps * float(min(inst.n_a, inst.n_b))
+    m0, s0 = sv.snapshot()
+    cur_m, cur_d = _internal(m0, swapped), s0.duals_final
+    phase = 0
+    while True:
+        if opt.observer is not None:
+            b_free, e_adm = sv.admissible(n_b_int)
+        else:
+            b_free = np.flatnonzero(cur_m.match_of_b == K_UNMATCHED).astype(np.int32)
+            e_adm = None
+        if float(len(b_free)) <= threshold:
+            break
+        before = int(np.abs(cur_d.y_a).sum() + np.abs(cur_d.y_b).sum())
+        done, _ = sv.step(phase + 1)
+        if done != phase + 1:
+            raise InvariantViolation(f"device loop stopped at phase {done}, expected {phase + 1}")
+        phase = done
+        prev_m = cur_m
+        m1, s1 = sv.snapshot()
+        cur_m, cur_d = _internal(m1, swapped), s1.duals_final
+        if opt.check_invariants:
+            rep = sv.verify_feasibility()
+            if not rep.ok():
+                raise InvariantViolation(f"phase {phase}: {rep.violations[0]}")
+        if opt.observer is not None:
+            m_prime, a_double, m_double = [], [], []
+            for b in b_free:  # M' in B' order (the sequential greedy's order)
+                a = int(cur_m.match_of_b[b])
+                if a == K_UNMATCHED:
+                    continue
+                m_prime.append((a, int(b)))
+                old_b = int(prev_m.match_of_a[a])
+                if old_b != K_UNMATCHED:
+                    a_double.append(a)
+                    m_double.append((a, old_b))
+            touched = np.unique(np.concatenate(e_adm)) if e_adm else np.zeros(0, np.int32)
+            ws = PhaseWorkset(b_free, e_adm, touched.astype(np.int32), m_prime, a_double, m_double)
+            after = int(np.abs(cur_d.y_a).sum() + np.abs(cur_d.y_b).sum())
+            opt.observer(PhaseSnapshot(phase, costs, cur_d, cur_m, ws, before, after))
+    return sv.finish()
+
+
+def verify_feasibility(sc: "ScaledCosts", duals: DualState, m: Matching,
+                       device: int = 0) -> FeasibilityReport:
+    """assignment.hpp:122-126 / assignment.cpp:264-312, evaluated on the
+    device (the first violation and the count; see FeasibilityReport)."""
+    return get_solver(device).verify_host(sc, duals, m)
 
 
 def matching_cost(m: Matching, inst: AssignmentInstance) -> float:

@@ -92,6 +92,9 @@ struct otprg_ctx {
   int sh_done = 0;
   DevBuf sh_bounds, sh_pos, sh_park[2], sh_list;
 
+  // invariant suite / workset export (verify_kernels.cu)
+  DevBuf v_out, v_k, v_ya, v_yb, v_ma, v_mb, adm_cnt, adm_off, adm_list;
+
   // optimal transport (ot_host.cpp): per-phase scan inputs / outputs
   DevBuf ot_t, ot_req, ot_out;
   void* ot_hpin = nullptr;

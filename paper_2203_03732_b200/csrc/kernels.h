@@ -122,6 +122,27 @@ cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, i
                                   unsigned long long* lent, void* rowmin, Ctl* ctl, int num_sms,
                                   cudaStream_t s);
 bool smem_t_fits(int width, int lda);
+
+// Device invariant suite (verify_kernels.cu): first violation key
+// (section << 60 | index << 4 | kind, minimum over the grid) and count.
+struct VerifyOut {
+  unsigned long long first;  // ~0 = none
+  unsigned long long count;
+};
+enum VerifyKind : unsigned {
+  kMatchA = 1, kMatchB = 2, kDemandPositive = 3, kFreeNonzero = 4, kDemandBound = 5,
+  kSupplyNegative = 6, kSupplyBound = 7, kNotTight = 8, kExceeds = 9
+};
+cudaError_t launch_verify_state(const void* kT, int lda, int width, const void* t,
+                                const int32_t* yb, const int32_t* ma, const int32_t* mb, int n_a,
+                                int n_b, long long bound, VerifyOut* out, cudaStream_t s);
+cudaError_t launch_verify_host(const int32_t* k, const long long* ya, const long long* yb,
+                               const int32_t* ma, const int32_t* mb, int n_a, int n_b,
+                               long long bound, VerifyOut* out, cudaStream_t s);
+cudaError_t launch_free_list(const int32_t* mb, int n_b, int32_t* out, int* count, cudaStream_t s);
+cudaError_t launch_admissible(const void* kT, int lda, int width, const void* t, const int32_t* yb,
+                              const int32_t* bfree, int nfree, int n_a, long long* counts,
+                              const long long* offs, int32_t* out, cudaStream_t s);
 cudaError_t launch_complete(int32_t* match_a, int32_t* match_b, int n_a, int n_b,
                             int32_t* scratch_a, int32_t* scratch_b, cudaStream_t s);
 cudaError_t launch_flush(void* buf, size_t bytes, cudaStream_t s);

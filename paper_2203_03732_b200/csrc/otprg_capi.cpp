@@ -469,11 +469,15 @@ void otprg_destroy(otprg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->kT, &ctx->t, &ctx->yb, &ctx->ma, &ctx->mb, &ctx->holder, &ctx->rowmin,
                     &ctx->lmeta, &ctx->lent, &ctx->lists, &ctx->mps, &ctx->fc, &ctx->ctl, &ctx->fa,
-                    &ctx->fb, &ctx->stage, &ctx->pts, &ctx->flush, &ctx->trace})
+                    &ctx->fb, &ctx->stage, &ctx->pts, &ctx->flush, &ctx->trace, &ctx->sh_bounds,
+                    &ctx->sh_pos, &ctx->sh_park[0], &ctx->sh_park[1], &ctx->sh_list, &ctx->v_out,
+                    &ctx->v_k, &ctx->v_ya, &ctx->v_yb, &ctx->v_ma, &ctx->v_mb, &ctx->adm_cnt,
+                    &ctx->adm_off, &ctx->adm_list, &ctx->ot_t, &ctx->ot_req, &ctx->ot_out})
     b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   for (auto& e : ctx->timer) cudaEventDestroy(e);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  if (ctx->ot_hpin) cudaFreeHost(ctx->ot_hpin);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -704,6 +708,190 @@ int otprg_flush_l2(otprg_ctx* ctx) {
   CK(ctx->flush.ensure(bytes), "alloc flush");
   CK(otprg::launch_flush(ctx->flush.p, bytes, ctx->stream), "flush launch");
   CK(cudaStreamSynchronize(ctx->stream), "flush");
+  return OTPRG_OK;
+}
+
+}  // extern "C"
+
+// ---- invariant suite --------------------------------
+namespace {
+
+struct VerifyResult {
+  unsigned long long first, count;
+};
+
+int run_verify(otprg_ctx* ctx, bool host_state, int n_a, int n_b, long long bound,
+               VerifyResult* r) {
+  CK(ctx->v_out.ensure(sizeof(otprg::VerifyOut)), "alloc verify");
+  otprg::VerifyOut init{~0ull, 0ull};
+  auto* out = ctx->v_out.as<otprg::VerifyOut>();
+  CK(cudaMemcpyAsync(out, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream), "H2D verify");
+  if (host_state)
+    CK(otprg::launch_verify_host(ctx->v_k.as<int32_t>(), ctx->v_ya.as<long long>(),
+                                 ctx->v_yb.as<long long>(), ctx->v_ma.as<int32_t>(),
+                                 ctx->v_mb.as<int32_t>(), n_a, n_b, bound, out, ctx->stream),
+       "verify launch");
+  else
+    CK(otprg::launch_verify_state(ctx->kT.p, ctx->lda, ctx->width, ctx->t.p, ctx->yb.as<int32_t>(),
+                                  ctx->ma.as<int32_t>(), ctx->mb.as<int32_t>(), n_a, n_b, bound, out,
+                                  ctx->stream),
+       "verify launch");
+  otprg::VerifyOut h{};
+  CK(cudaMemcpyAsync(&h, out, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream), "D2H verify");
+  CK(cudaStreamSynchronize(ctx->stream), "verify");
+  r->first = h.first;
+  r->count = h.count;
+  return OTPRG_OK;
+}
+
+// Splits the first-violation key; dual/edge values come from `get`.
+template <typename Get>
+void decode_violation(const VerifyResult& r, int n_a, int n_b, Get get, otprg_feasibility* f) {
+  f->violations = 0;
+  f->kind = OTPRG_VIOL_NONE;
+  f->a = f->b = -1;
+  f->pad = 0;
+  f->sum = f->k = 0;
+  if (r.first == ~0ull) return;
+  const unsigned section = static_cast<unsigned>(r.first >> 60);
+  const unsigned long long index = (r.first >> 4) & ((1ull << 56) - 1);
+  f->kind = static_cast<int32_t>(r.first & 15);
+  f->violations = section == 0 ? 1 : static_cast<int64_t>(r.count);  // validate() stops the check
+  if (section == 0) {
+    if (f->kind == OTPRG_VIOL_MATCH_A) f->a = static_cast<int32_t>(index);
+    else f->b = static_cast<int32_t>(index - n_a);
+  } else if (section == 1) {
+    f->a = static_cast<int32_t>(index);
+  } else if (section == 2) {
+    f->b = static_cast<int32_t>(index);
+  } else {
+    f->a = static_cast<int32_t>(index / n_b);
+    f->b = static_cast<int32_t>(index % n_b);
+  }
+  get(f);
+}
+
+}  // namespace
+
+extern "C" {
+
+int otprg_verify_feasibility(otprg_ctx* ctx, otprg_feasibility* out) {
+  if (!ctx || !out) return OTPRG_PARAMETER;
+  if (!ctx->begun || ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_begin() first");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  VerifyResult r{};
+  int st = run_verify(ctx, false, ctx->ia, ctx->ib, static_cast<long long>(ctx->unit_ceil) + 2, &r);
+  if (st) return st;
+  int err = 0;
+  decode_violation(r, ctx->ia, ctx->ib,
+                   [&](otprg_feasibility* f) {
+                     uint16_t tv = 0;
+                     int32_t ybv = 0;
+                     uint16_t kv = 0;
+                     const int w = ctx->width;
+                     if (f->a >= 0 && cudaMemcpy(&tv, static_cast<char*>(ctx->t.p) + static_cast<size_t>(f->a) * w, w,
+                                                 cudaMemcpyDeviceToHost) != cudaSuccess) err = 1;
+                     if (f->b >= 0 && cudaMemcpy(&ybv, ctx->yb.as<int32_t>() + f->b, 4,
+                                                 cudaMemcpyDeviceToHost) != cudaSuccess) err = 1;
+                     if (f->a >= 0 && f->b >= 0 &&
+                         cudaMemcpy(&kv, static_cast<char*>(ctx->kT.p) +
+                                             (static_cast<size_t>(f->b) * ctx->lda + f->a) * w,
+                                    w, cudaMemcpyDeviceToHost) != cudaSuccess) err = 1;
+                     const long long ya = -static_cast<long long>(w == 1 ? (tv & 0xff) : tv);
+                     const long long kk = w == 1 ? (kv & 0xff) : kv;
+                     if (f->kind >= OTPRG_VIOL_NOT_TIGHT) {
+                       f->sum = ya + ybv;
+                       f->k = kk;
+                     } else if (f->kind >= OTPRG_VIOL_SUPPLY_NEGATIVE) {
+                       f->sum = ybv;
+                     } else if (f->kind >= OTPRG_VIOL_DEMAND_POSITIVE) {
+                       f->sum = ya;
+                     }
+                   },
+                   out);
+  if (err) return fail(ctx, OTPRG_DEVICE, "D2H of the violation details failed");
+  return OTPRG_OK;
+}
+
+int otprg_verify_host(otprg_ctx* ctx, int32_t n_a, int32_t n_b, const int32_t* k, int32_t unit_ceil,
+                      const int64_t* y_a, const int64_t* y_b, const int32_t* match_of_a,
+                      const int32_t* match_of_b, otprg_feasibility* out) {
+  if (!ctx || !out) return OTPRG_PARAMETER;
+  if (n_a < 1 || n_b < 1 || !k || !y_a || !y_b || !match_of_a || !match_of_b)
+    return fail(ctx, OTPRG_PARAMETER, "null or empty state");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const size_t na = n_a, nb = n_b;
+  CK(ctx->v_k.ensure(na * nb * 4), "alloc");
+  CK(ctx->v_ya.ensure(na * 8), "alloc");
+  CK(ctx->v_yb.ensure(nb * 8), "alloc");
+  CK(ctx->v_ma.ensure(na * 4), "alloc");
+  CK(ctx->v_mb.ensure(nb * 4), "alloc");
+  CK(cudaMemcpyAsync(ctx->v_k.p, k, na * nb * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->v_ya.p, y_a, na * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->v_yb.p, y_b, nb * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->v_ma.p, match_of_a, na * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->v_mb.p, match_of_b, nb * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  VerifyResult r{};
+  int st = run_verify(ctx, true, n_a, n_b, static_cast<long long>(unit_ceil) + 2, &r);
+  if (st) return st;
+  decode_violation(r, n_a, n_b,
+                   [&](otprg_feasibility* f) {
+                     if (f->kind >= OTPRG_VIOL_NOT_TIGHT) {
+                       f->sum = y_a[f->a] + y_b[f->b];
+                       f->k = k[static_cast<size_t>(f->a) * nb + f->b];
+                     } else if (f->kind >= OTPRG_VIOL_SUPPLY_NEGATIVE) {
+                       f->sum = y_b[f->b];
+                     } else if (f->kind >= OTPRG_VIOL_DEMAND_POSITIVE) {
+                       f->sum = y_a[f->a];
+                     }
+                   },
+                   out);
+  return OTPRG_OK;
+}
+
+int otprg_admissible(otprg_ctx* ctx, int32_t* b_free, int64_t* offsets, int32_t* a_list,
+                     int64_t a_cap, int64_t* n_free, int64_t* n_edges) {
+  if (!ctx || !b_free || !offsets) return OTPRG_PARAMETER;
+  if (!ctx->begun || ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_begin() first");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int ib = ctx->ib;
+  CK(ctx->adm_cnt.ensure((static_cast<size_t>(ib) + 1) * 8), "alloc");
+  CK(ctx->adm_off.ensure((static_cast<size_t>(ib) + 1) * 8), "alloc");
+  int* d_count = reinterpret_cast<int*>(ctx->adm_cnt.as<long long>() + ib);
+  CK(otprg::launch_free_list(ctx->mb.as<int32_t>(), ib, ctx->fb.as<int32_t>(), d_count, ctx->stream),
+     "free list launch");
+  int nf = 0;
+  CK(cudaMemcpyAsync(&nf, d_count, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  CK(cudaStreamSynchronize(ctx->stream), "free list");
+  CK(otprg::launch_admissible(ctx->kT.p, ctx->lda, ctx->width, ctx->t.p, ctx->yb.as<int32_t>(),
+                              ctx->fb.as<int32_t>(), nf, ctx->ia, ctx->adm_cnt.as<long long>(), nullptr,
+                              nullptr, ctx->stream),
+     "admissible count launch");
+  std::vector<long long> cnt(static_cast<size_t>(nf));
+  if (nf > 0) {
+    CK(cudaMemcpyAsync(cnt.data(), ctx->adm_cnt.p, static_cast<size_t>(nf) * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream), "D2H");
+    CK(cudaMemcpyAsync(b_free, ctx->fb.p, static_cast<size_t>(nf) * 4, cudaMemcpyDeviceToHost,
+                       ctx->stream), "D2H");
+  }
+  CK(cudaStreamSynchronize(ctx->stream), "admissible count");
+  offsets[0] = 0;
+  for (int i = 0; i < nf; ++i) offsets[i + 1] = offsets[i] + cnt[i];
+  const int64_t total = offsets[nf];
+  if (n_free) *n_free = nf;
+  if (n_edges) *n_edges = total;
+  if (!a_list || a_cap < total || total == 0) return OTPRG_OK;
+  CK(ctx->adm_list.ensure(static_cast<size_t>(total) * 4), "alloc");
+  static_assert(sizeof(long long) == sizeof(int64_t), "offsets");
+  CK(cudaMemcpyAsync(ctx->adm_off.p, offsets, (static_cast<size_t>(nf) + 1) * 8, cudaMemcpyHostToDevice,
+                     ctx->stream), "H2D");
+  CK(otprg::launch_admissible(ctx->kT.p, ctx->lda, ctx->width, ctx->t.p, ctx->yb.as<int32_t>(),
+                              ctx->fb.as<int32_t>(), nf, ctx->ia, nullptr, ctx->adm_off.as<long long>(),
+                              ctx->adm_list.as<int32_t>(), ctx->stream),
+     "admissible fill launch");
+  CK(cudaMemcpyAsync(a_list, ctx->adm_list.p, static_cast<size_t>(total) * 4, cudaMemcpyDeviceToHost,
+                     ctx->stream), "D2H");
+  CK(cudaStreamSynchronize(ctx->stream), "admissible");
   return OTPRG_OK;
 }
 

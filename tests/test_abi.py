@@ -62,6 +62,7 @@ def test_struct_layouts_match_header(lib):
 
     assert flat("otprg_ot_problem") == [f for f, _ in api._OTProblem._fields_]
     assert flat("otprg_ot_result") == [f for f, _ in api._OTResult._fields_]
+    assert flat("otprg_feasibility") == [f for f, _ in _native.Feasibility._fields_]
 
 
 def test_scaled_floor_matches_oracle(lib, oracle):
@@ -91,8 +92,10 @@ def test_parameter_errors_before_device(lib):
     with pytest.raises(otprg.ParameterError):
         otprg.solve_assignment(otprg.AssignmentInstance(1, 1, np.array([[1.5]])),
                                otprg.AssignmentOptions(eps=0.1))
-    with pytest.raises(otprg.ParameterError):
-        otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=0.1, observer=lambda s: None))
+    with pytest.raises(otprg.ParameterError):  # copy mode is not on the device path
+        g = np.zeros(1, np.int64)
+        otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=0.1, demand_groups=g,
+                                                             supply_groups=g))
 
 
 def test_create_without_device_reports_status(lib):
