@@ -10,6 +10,6 @@ if [ "$1" == "ncu" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/launches.csv python scripts/profile_solve.py > gpurun_out/ncu_launch.log 2>&1
   timeout 300 python scripts/profile_solve.py > gpurun_out/plain2.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:phase_loop -s 4 -c 2 \
-      -o gpurun_out/prof_loop python scripts/profile_solve.py > gpurun_out/ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:propose_stream|phase_loop" \
+      -s 2 -c 2 -o gpurun_out/prof_loop python scripts/profile_solve.py > gpurun_out/ncu_full.log 2>&1
 fi

@@ -1,4 +1,4 @@
-"""Summarise an ncu capture of the two phase_loop launches of one solve
+"""Summarise an ncu capture of the propose-scan and phase-loop launches of one solve
 (gpurun_out/prof_loop.ncu-rep from scripts/gpu_round.sh) into
 profiles/ncu_summary.json and profiles/<tag>_ncu_phase_loop.txt."""
 import csv
@@ -19,7 +19,9 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size"]
 out, lines = {}, []
-for r, name in zip(rows[2:], ["phase1", "loop"]):
+for r in rows[2:]:
+    name = "propose" if "propose_stream" in r[hdr.index("Kernel Name")] else "loop"
+
     def g(k):
         return float(r[hdr.index(k)].replace(",", ""))
     rd = g("dram__bytes_read.sum") * scale[units[hdr.index("dram__bytes_read.sum")]]
