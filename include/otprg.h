@@ -102,8 +102,8 @@ typedef struct otprg_result {
   /* device-side measurements */
   double build_ms;        /* cost build/rounding kernels (CUDA events) */
   double solve_ms;        /* phase loop + completion kernels (CUDA events) */
-  double phase1_ms;       /* the first phase alone (its own launch) */
-  double loop_ms;         /* phases 2.. (the second phase-loop launch) */
+  double phase1_ms;       /* the phase-1 propose scan kernel (device %globaltimer span) */
+  double loop_ms;         /* the phase-loop launch (every phase's chains, phases >= 2 scans) */
   double solve_d2h_ms;    /* solve_ms + D2H of the results into pinned staging */
   int64_t bytes_touched;  /* cost-matrix bytes the scan kernels loaded */
   int64_t bytes_alg;      /* sum_i n_i * n_a * width (Lemma-5 schedule) */
@@ -121,6 +121,11 @@ int otprg_create(int device, otprg_ctx** out);
 void otprg_destroy(otprg_ctx* ctx);
 const char* otprg_last_error(const otprg_ctx* ctx);
 int otprg_version(void);
+
+/* Run this context's work on the caller's CUDA stream (NULL: its own stream
+ * again).  Used to put several contexts and an NCCL exchange on one stream so
+ * the sharded protocol needs no host sync between scan, exchange and DA. */
+int otprg_set_stream(otprg_ctx* ctx, void* stream);
 
 /* scaled_floor(c, eps) (core.cpp:26-32), evaluated on the host. */
 int64_t otprg_scaled_floor(double c, double eps);

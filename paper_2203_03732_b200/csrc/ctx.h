@@ -49,6 +49,7 @@ struct otprg_ctx {
   using DevBuf = otprg::DevBuf;
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;  // created by otprg_create (stream may be the caller's)
   cudaEvent_t ev[8] = {};
   int num_sms = 0;
   std::string err;

@@ -443,6 +443,14 @@ extern "C" {
 
 int otprg_version(void) { return 1; }
 
+int otprg_set_stream(otprg_ctx* ctx, void* stream) {
+  if (!ctx) return OTPRG_PARAMETER;
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  CK(cudaStreamSynchronize(ctx->stream), "stream switch");
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return OTPRG_OK;
+}
+
 int64_t otprg_scaled_floor(double c, double eps) { return host_scaled_floor(c, eps); }
 
 int otprg_create(int device, otprg_ctx** out) {
@@ -457,6 +465,7 @@ int otprg_create(int device, otprg_ctx** out) {
     delete ctx;
     return OTPRG_DEVICE;
   }
+  ctx->own_stream = ctx->stream;
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   for (auto& e : ctx->timer) cudaEventCreate(&e);
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -478,7 +487,7 @@ void otprg_destroy(otprg_ctx* ctx) {
   for (auto& e : ctx->timer) cudaEventDestroy(e);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
   if (ctx->ot_hpin) cudaFreeHost(ctx->ot_hpin);
-  cudaStreamDestroy(ctx->stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
 
@@ -1097,7 +1106,9 @@ int otprg_shard_scan(otprg_ctx* ctx, int32_t* cand, int32_t* meta_words, int32_t
   const int4* req = refill ? ctx->sh_park[ctx->sh_park_cur].as<int4>() : nullptr;
   const int nreq = refill ? ctx->sh_parked : ctx->sh_n;
   CK(otprg::launch_shard_scan(S, req, nreq, cand, meta, ctx->stream), "shard_scan launch");
-  CK(cudaStreamSynchronize(ctx->stream), "shard scan");
+  // no sync: the exchange and the DA are ordered after the scan on the
+  // context's stream (otprg_set_stream puts every rank of a process and the
+  // NCCL all-gather on one stream)
   return OTPRG_OK;
 }
 

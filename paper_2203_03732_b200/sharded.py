@@ -79,7 +79,11 @@ class DeviceRank:
         self._ok(self._L.otprg_shard_finish(self._ctx, C.byref(r)))
         return Solver._pack(r, bufs)
 
+    def set_stream(self, stream_handle: int):
+        self._ok(self._L.otprg_set_stream(self._ctx, stream_handle))
+
     def close(self):
+        self._L.otprg_set_stream(self._ctx, None)
         self.solver.close()
 
 
@@ -113,9 +117,9 @@ class TorchDistExchange:
                 dist.all_gather_into_tensor(t, mine)
             else:  # gloo (CPU tests of the protocol)
                 dist.all_gather(list(t.split(slot)), mine)
-        if tensors and tensors[0].is_cuda:
-            # the next C-ABI launch runs on the context's own stream
-            torch.cuda.current_stream().synchronize()
+        # (CUDA: the collective is ordered on the current stream, which the
+        # contexts share — otprg_set_stream — so the DA launch follows it
+        # without a host sync)
 
 
 def run_phases(ranks, exchange, cand_ptr: int, meta_ptr: int, cap: int, gather_args=()):
@@ -177,12 +181,20 @@ class ShardedSolver:
         self.cap = self.ranks[0].cap
         self.cand, self.meta = _buffers(self.n_shards, self.cap, K, device)
         self.gather_args = (self.cand, self.meta) if distributed else ()
+        # one stream for every context of this process and the exchange:
+        # scan -> all-gather -> DA are ordered on it without host syncs
+        import torch
+        self.stream = torch.cuda.Stream(device=device)
+        for r in self.ranks:
+            r.set_stream(self.stream.cuda_stream)
 
     def solve(self):
         """One full solve (state re-initialised).  Returns (Matching,
         SolveStats) of the first local rank after checking local ranks agree."""
-        rounds = run_phases(self.ranks, self.exchange, self.cand.data_ptr(), self.meta.data_ptr(),
-                            self.cap, self.gather_args)
+        import torch
+        with torch.cuda.stream(self.stream):
+            rounds = run_phases(self.ranks, self.exchange, self.cand.data_ptr(),
+                                self.meta.data_ptr(), self.cap, self.gather_args)
         outs = [r.finish() for r in self.ranks]
         m0, s0 = outs[0]
         for m, s in outs[1:]:
