@@ -13,6 +13,7 @@
 #include <string>
 
 #include "otpr/assignment.hpp"
+#include "otpr/bench.hpp"
 #include "otpr/core.hpp"
 #include "otpr/errors.hpp"
 #include "otpr/instances.hpp"
@@ -307,6 +308,54 @@ int ref_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const double
     std::memcpy(d, sm.d.data(), 8 * sm.d.size());
     std::memcpy(s, sm.s.data(), 8 * sm.s.size());
     *theta = sm.theta;
+  });
+}
+
+// format_double (bench.cpp:203-208): the CSV number format.
+int ref_format_double(double v, char* out, int32_t cap) {
+  const std::string f = otpr::format_double(v);
+  if (static_cast<int32_t>(f.size()) + 1 > cap) return 2;
+  std::memcpy(out, f.c_str(), f.size() + 1);
+  return 0;
+}
+
+// csv_row (bench.cpp:214-228) of one record (optional fields: has_* = 0 -> empty).
+int ref_csv_row(const char* solver, int32_t n, int32_t has_eps, double eps, int32_t has_reg,
+                double reg, uint64_t seed, double cost, int32_t has_oracle, double oracle,
+                double time_ms, int64_t phases, char* out, int32_t cap) {
+  return guarded([&] {
+    otpr::RunRecord r;
+    r.solver = solver;
+    r.n = n;
+    if (has_eps) r.eps = eps;
+    if (has_reg) r.reg = reg;
+    r.seed = seed;
+    r.cost = cost;
+    if (has_oracle) r.oracle_cost = oracle;
+    r.time_ms = time_ms;
+    r.phases = phases;
+    const std::string row = otpr::csv_row(r);
+    if (static_cast<int32_t>(row.size()) + 1 > cap) throw otpr::ParameterError("buffer");
+    std::memcpy(out, row.c_str(), row.size() + 1);
+  });
+}
+
+// save_instance (instances.cpp:209-222) of gen_uniform_square(n, seed).
+int ref_save_uniform_square(int32_t n, uint64_t seed, const char* path) {
+  return guarded([&] { otpr::save_instance(otpr::gen_uniform_square(n, seed), path); });
+}
+
+// load_instance (instances.cpp:224-246): header + cost.
+int ref_load_instance(const char* path, int32_t* n_a, int32_t* n_b, double* norm_factor,
+                      uint64_t* seed, double* cost, int64_t cost_cap) {
+  return guarded([&] {
+    const auto inst = otpr::load_instance(path);
+    *n_a = inst.n_a;
+    *n_b = inst.n_b;
+    *norm_factor = inst.norm_factor;
+    *seed = inst.seed;
+    if (cost && cost_cap >= static_cast<int64_t>(inst.cost.size()))
+      std::memcpy(cost, inst.cost.data(), inst.cost.size() * sizeof(double));
   });
 }
 
