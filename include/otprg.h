@@ -294,6 +294,39 @@ typedef struct otprg_ot_result {
 
 int otprg_solve_ot(otprg_ctx* ctx, const otprg_ot_problem* prob, otprg_ot_result* res);
 
+/* ---- Sinkhorn baseline -------------------------------
+ * otprg_sinkhorn replaces otpr::sinkhorn (include/otpr/sinkhorn.hpp:13-31,
+ * src/sinkhorn.cpp:69-151): kernel exp(-c/reg), alternating scaling until the
+ * L1 row-marginal violation <= tol (or max_iters / the time budget), then
+ * round_to_marginals (:12-66).  FP64 on the device; deterministic reductions
+ * (not the reference's sequential sums bit for bit).  Errors: 2 for reg/tol
+ * <= 0 or costs outside [0,1], 3 for masses not summing to 1, 4 when the
+ * kernel or a scaling vector underflows / diverges (NumericalError). */
+typedef struct otprg_sinkhorn_config {
+  double reg;            /* > 0 */
+  int32_t max_iters;
+  int32_t pad;
+  double tol;            /* > 0 */
+  double time_budget_ms; /* 0 = none */
+} otprg_sinkhorn_config;
+
+typedef struct otprg_sinkhorn_result {
+  int32_t* ent_a;        /* plan entries (p > 0, row-major) up to entry_cap, or NULL */
+  int32_t* ent_b;
+  double* ent_mass;
+  int64_t entry_cap;
+  /* outputs */
+  int64_t n_entries;
+  double cost;           /* SinkhornResult::cost = plan.cost */
+  int32_t iters;
+  int32_t converged;
+  double marginal_violation;
+  double build_ms, loop_ms, round_ms;
+} otprg_sinkhorn_result;
+
+int otprg_sinkhorn(otprg_ctx* ctx, const otprg_ot_problem* prob, const otprg_sinkhorn_config* cfg,
+                   otprg_sinkhorn_result* res);
+
 /* scale_and_round (ot.cpp:109-128): d = exact_ceil(mu*theta),
  * s = exact_floor(nu*theta), theta = 4 max(n_a,n_b) / eps.  Host-only. */
 int otprg_ot_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const double* nu,

@@ -18,6 +18,7 @@
 #include "otpr/errors.hpp"
 #include "otpr/instances.hpp"
 #include "otpr/ot.hpp"
+#include "otpr/sinkhorn.hpp"
 
 namespace {
 
@@ -356,6 +357,39 @@ int ref_load_instance(const char* path, int32_t* n_a, int32_t* n_b, double* norm
     *seed = inst.seed;
     if (cost && cost_cap >= static_cast<int64_t>(inst.cost.size()))
       std::memcpy(cost, inst.cost.data(), inst.cost.size() * sizeof(double));
+  });
+}
+
+// sinkhorn (sinkhorn.cpp:69-151): iters, converged, violation, cost and (when
+// cap allows) the plan entries.
+int ref_sinkhorn(int32_t n_a, int32_t n_b, const double* mu, const double* nu, const double* cost,
+                 double reg, int32_t max_iters, double tol, int32_t* iters, int32_t* converged,
+                 double* violation, double* plan_cost, int64_t* n_entries, int32_t* ea, int32_t* eb,
+                 double* em, int64_t cap, double* ms) {
+  return guarded([&] {
+    otpr::OTInstance inst;
+    inst.mu.assign(mu, mu + n_a);
+    inst.nu.assign(nu, nu + n_b);
+    inst.cost = otpr::Matrix<double>(n_a, n_b);
+    std::memcpy(inst.cost.data(), cost, sizeof(double) * size_t(n_a) * n_b);
+    otpr::SinkhornConfig cfg;
+    cfg.reg = reg;
+    cfg.max_iters = max_iters;
+    cfg.tol = tol;
+    const auto t0 = Clock::now();
+    const auto res = otpr::sinkhorn(inst, cfg);
+    *ms = ms_since(t0);
+    *iters = res.iters;
+    *converged = res.converged ? 1 : 0;
+    *violation = res.marginal_violation;
+    *plan_cost = res.cost;
+    *n_entries = static_cast<int64_t>(res.plan.entries.size());
+    if (ea && cap >= *n_entries)
+      for (size_t i = 0; i < res.plan.entries.size(); ++i) {
+        ea[i] = res.plan.entries[i].a;
+        eb[i] = res.plan.entries[i].b;
+        em[i] = res.plan.entries[i].mass;
+      }
   });
 }
 

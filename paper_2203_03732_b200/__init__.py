@@ -8,7 +8,7 @@ from .api import (  # noqa: F401
     gen_uniform_square, get_solver, l1_cost, load_mnist_pair, matching_cost, points_cost,
     scale_round_costs, scaled_floor, solve_assignment, OTInstance, TransportPlan, ScaledMasses,
     gen_random_ot_rational, scale_and_round, solve_ot, FeasibilityReport, PhaseSnapshot,
-    PhaseWorkset, verify_feasibility,
+    PhaseWorkset, verify_feasibility, SinkhornConfig, SinkhornResult, sinkhorn, reg_for_eps,
 )
 
 __all__ = [
@@ -18,5 +18,5 @@ __all__ = [
     "load_mnist_pair", "matching_cost", "points_cost", "scale_round_costs", "scaled_floor",
     "solve_assignment", "OTInstance", "TransportPlan", "ScaledMasses", "gen_random_ot_rational",
     "scale_and_round", "solve_ot", "FeasibilityReport", "PhaseSnapshot", "PhaseWorkset",
-    "verify_feasibility",
+    "verify_feasibility", "SinkhornConfig", "SinkhornResult", "sinkhorn", "reg_for_eps",
 ]

@@ -812,3 +812,74 @@ def solve_ot(inst: OTInstance, eps: float, device: int = 0):
                                    solve_ms=r.solve_ms, bytes_touched=int(r.bytes_touched),
                                    gpu_launches=int(r.gpu_launches)))
     return plan, stats
+
+
+# ---- Sinkhorn baseline (sinkhorn.hpp:13-31) ------------
+@dataclass
+class SinkhornConfig:
+    """sinkhorn.hpp:13-18."""
+    reg: float = 0.01
+    max_iters: int = 10000
+    tol: float = 1e-9
+    time_budget_ms: float = 0.0
+
+
+@dataclass
+class SinkhornResult:
+    """sinkhorn.hpp:20-26 (plan rounded to exact marginals), plus device timings."""
+    plan: Optional[TransportPlan]
+    iters: int
+    cost: float
+    converged: bool
+    marginal_violation: float
+    device: dict = field(default_factory=dict)
+
+
+class _SkConfig(C.Structure):
+    _fields_ = [("reg", C.c_double), ("max_iters", C.c_int32), ("pad", C.c_int32),
+                ("tol", C.c_double), ("time_budget_ms", C.c_double)]
+
+
+class _SkResult(C.Structure):
+    _fields_ = [("ent_a", C.c_void_p), ("ent_b", C.c_void_p), ("ent_mass", C.c_void_p),
+                ("entry_cap", C.c_int64), ("n_entries", C.c_int64), ("cost", C.c_double),
+                ("iters", C.c_int32), ("converged", C.c_int32), ("marginal_violation", C.c_double),
+                ("build_ms", C.c_double), ("loop_ms", C.c_double), ("round_ms", C.c_double)]
+
+
+def reg_for_eps(eps: float, n: int) -> float:
+    """bench.cpp:38-41: reg = eps / (4 ln n), n clamped to >= 2."""
+    return eps / (4.0 * math.log(max(float(n), 2.0)))
+
+
+def sinkhorn(inst: OTInstance, cfg: SinkhornConfig, device: int = 0,
+             entries: bool = True) -> SinkhornResult:
+    """sinkhorn.hpp:28-31 / sinkhorn.cpp:69-151 on the device (FP64).
+    ``entries=False`` skips the D2H of the dense plan (cost and counts only)."""
+    mu = np.ascontiguousarray(inst.mu, np.float64)
+    nu = np.ascontiguousarray(inst.nu, np.float64)
+    cost = np.ascontiguousarray(inst.cost, np.float64)
+    if cost.shape != (len(mu), len(nu)):
+        raise ParameterError("OT cost matrix dimensions do not match mass vectors")
+    solver = get_solver(device)
+    p = _OTProblem(len(mu), len(nu), 0.5, mu.ctypes.data, nu.ctypes.data, cost.ctypes.data, 0, 0)
+    c = _SkConfig(float(cfg.reg), int(cfg.max_iters), 0, float(cfg.tol), float(cfg.time_budget_ms))
+    r = _SkResult()
+    st = solver._L.otprg_sinkhorn(solver._ctx, C.byref(p), C.byref(c), C.byref(r))
+    if st:
+        solver._raise(st)
+    plan = None
+    if entries:
+        ne = int(r.n_entries)
+        ea, eb, em = np.empty(max(ne, 1), np.int32), np.empty(max(ne, 1), np.int32), np.empty(max(ne, 1))
+        r2 = _SkResult()
+        r2.ent_a, r2.ent_b, r2.ent_mass, r2.entry_cap = ea.ctypes.data, eb.ctypes.data, em.ctypes.data, ne
+        st = solver._L.otprg_sinkhorn(solver._ctx, C.byref(p), C.byref(c), C.byref(r2))
+        if st:
+            solver._raise(st)
+        plan = TransportPlan(ea[:ne].copy(), eb[:ne].copy(), em[:ne].copy(), float(r2.cost))
+        r = r2
+    return SinkhornResult(plan, int(r.iters), float(r.cost), bool(r.converged),
+                          float(r.marginal_violation),
+                          device=dict(build_ms=r.build_ms, loop_ms=r.loop_ms, round_ms=r.round_ms,
+                                      n_entries=int(r.n_entries)))

@@ -96,6 +96,9 @@ struct otprg_ctx {
   // invariant suite / workset export (verify_kernels.cu)
   DevBuf v_out, v_k, v_ya, v_yb, v_ma, v_mb, adm_cnt, adm_off, adm_list;
 
+  // Sinkhorn baseline (ot_host.cpp / sinkhorn_kernels.cu)
+  DevBuf sk_K, sk_P, sk_vec, sk_part, sk_int;
+
   // optimal transport (ot_host.cpp): per-phase scan inputs / outputs
   DevBuf ot_t, ot_req, ot_out;
   void* ot_hpin = nullptr;

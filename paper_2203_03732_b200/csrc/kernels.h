@@ -139,6 +139,28 @@ cudaError_t launch_verify_state(const void* kT, int lda, int width, const void* 
 cudaError_t launch_verify_host(const int32_t* k, const long long* ya, const long long* yb,
                                const int32_t* ma, const int32_t* mb, int n_a, int n_b,
                                long long bound, VerifyOut* out, cudaStream_t s);
+// Sinkhorn baseline (sinkhorn_kernels.cu).
+cudaError_t sk_build(const double* cost, int n_a, int n_b, double reg, double* K, int* row_ok,
+                     int* col_ok, int* bad_cost, cudaStream_t s);
+cudaError_t sk_row(const double* K, int n_a, int n_b, const double* u, const double* v,
+                   const double* mu, double* term, double* u_next, int* err, cudaStream_t s);
+cudaError_t sk_col(const double* K, int n_a, int n_b, const double* w, const double* nu, double* v,
+                   double* partial, int* err, cudaStream_t s);
+size_t sk_partial_elems(int n_a, int n_b);
+cudaError_t sk_sum(const double* x, int n, double* out, cudaStream_t s);
+cudaError_t sk_plan(const double* K, int n_a, int n_b, const double* u, const double* v,
+                    const double* rs, const double* cs, double* P, cudaStream_t s);
+cudaError_t sk_prow(const double* P, int n_a, int n_b, const double* mu, double* row, double* scale,
+                    cudaStream_t s);
+cudaError_t sk_pcol(const double* P, int n_a, int n_b, double* ones_a, double* partial, double* col,
+                    cudaStream_t s);
+cudaError_t sk_colscale(const double* col, const double* nu, int n_b, double* scale, cudaStream_t s);
+cudaError_t sk_adds(double* P, int n_b, const int2* ab, const double* add, int n, cudaStream_t s);
+cudaError_t sk_rowcost(const double* P, const double* cost, int n_a, int n_b, double* rcost,
+                       long long* rcnt, cudaStream_t s);
+cudaError_t sk_entries(const double* P, int n_a, int n_b, const long long* offs, int32_t* ea,
+                       int32_t* eb, double* em, cudaStream_t s);
+
 cudaError_t launch_free_list(const int32_t* mb, int n_b, int32_t* out, int* count, cudaStream_t s);
 cudaError_t launch_admissible(const void* kT, int lda, int width, const void* t, const int32_t* yb,
                               const int32_t* bfree, int nfree, int n_a, long long* counts,

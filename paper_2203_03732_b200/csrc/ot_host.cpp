@@ -647,6 +647,179 @@ class OtSolver {
   }
 };
 
+// ---- Sinkhorn baseline (sinkhorn.cpp:69-151, round_to_marginals :12-66) -----
+void run_sinkhorn(otprg_ctx* ctx, const otprg_ot_problem* p, const otprg_sinkhorn_config* cfg,
+                  otprg_sinkhorn_result* r) {
+  validate_ot(p);
+  if (!cfg || !(cfg->reg > 0.0)) throw OtError{OTPRG_PARAMETER, "sinkhorn: reg must be positive"};
+  if (!(cfg->tol > 0.0)) throw OtError{OTPRG_PARAMETER, "sinkhorn: tol must be positive"};
+  OT_CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int n_a = p->n_a, n_b = p->n_b;
+  const size_t nn = static_cast<size_t>(n_a) * n_b;
+  cudaStream_t s = ctx->stream;
+  Timer t_build;
+  OT_CK(ctx->stage.ensure(nn * 8), "alloc cost");
+  OT_CK(ctx->sk_K.ensure(nn * 8), "alloc kernel");
+  OT_CK(ctx->sk_P.ensure(nn * 8), "alloc plan");
+  // vectors: u, u_next, v, mu, nu, term, row, col, rs, cs, ones, rcost (12 x max n)
+  const size_t nm = static_cast<size_t>(std::max(n_a, n_b));
+  OT_CK(ctx->sk_vec.ensure(12 * nm * 8 + 64), "alloc vectors");
+  OT_CK(ctx->sk_part.ensure(otprg::sk_partial_elems(n_a, n_b) * 8), "alloc partials");
+  OT_CK(ctx->sk_int.ensure((nm * 3 + 16) * 8), "alloc flags");
+  double* V = ctx->sk_vec.as<double>();
+  double *u = V, *u_next = V + nm, *v = V + 2 * nm, *mu = V + 3 * nm, *nu = V + 4 * nm,
+         *term = V + 5 * nm, *row = V + 6 * nm, *col = V + 7 * nm, *rs = V + 8 * nm, *cs = V + 9 * nm,
+         *ones = V + 10 * nm, *rcost = V + 11 * nm, *scalar = V + 12 * nm;
+  int* I = ctx->sk_int.as<int>();
+  int *row_ok = I, *col_ok = I + nm, *err = I + 2 * nm, *bad = I + 2 * nm + 4;
+  long long* rcnt = reinterpret_cast<long long*>(I + 2 * nm + 16);
+  double* cost = ctx->stage.as<double>();
+  double* K = ctx->sk_K.as<double>();
+  double* P = ctx->sk_P.as<double>();
+  OT_CK(cudaMemcpyAsync(cost, p->cost, nn * 8, cudaMemcpyHostToDevice, s), "H2D cost");
+  OT_CK(cudaMemcpyAsync(mu, p->mu, n_a * 8ull, cudaMemcpyHostToDevice, s), "H2D mu");
+  OT_CK(cudaMemcpyAsync(nu, p->nu, n_b * 8ull, cudaMemcpyHostToDevice, s), "H2D nu");
+  OT_CK(cudaMemsetAsync(err, 0, 32, s), "memset");
+  OT_CK(otprg::sk_build(cost, n_a, n_b, cfg->reg, K, row_ok, col_ok, bad, s), "kernel build");
+  {
+    std::vector<int> rok(n_a), cok(n_b);
+    int hbad = 0;
+    OT_CK(cudaMemcpyAsync(rok.data(), row_ok, n_a * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(cok.data(), col_ok, n_b * 4ull, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaStreamSynchronize(s), "kernel build");
+    if (hbad) throw OtError{OTPRG_PARAMETER, "OT cost entry outside [0,1]"};
+    for (int a = 0; a < n_a; ++a)
+      if (!rok[a]) throw OtError{OTPRG_NUMERICAL, "regularization too small: kernel row underflowed"};
+    for (int b = 0; b < n_b; ++b)
+      if (!cok[b]) throw OtError{OTPRG_NUMERICAL, "regularization too small: kernel column underflowed"};
+  }
+  r->build_ms = t_build.ms();
+  Timer t_loop;
+  // u = v = 1 (sinkhorn.cpp:97); the first u-update reads K v0
+  std::vector<double> one(nm, 1.0);
+  OT_CK(cudaMemcpyAsync(u, one.data(), n_a * 8ull, cudaMemcpyHostToDevice, s), "H2D");
+  OT_CK(cudaMemcpyAsync(v, one.data(), n_b * 8ull, cudaMemcpyHostToDevice, s), "H2D");
+  OT_CK(otprg::sk_row(K, n_a, n_b, u, v, mu, nullptr, u_next, err, s), "row pass");
+  int iters = 0;
+  bool converged = false;
+  double violation = 0.0;
+  auto raise_err = [](int e) {
+    if (e & 1) throw OtError{OTPRG_NUMERICAL, "regularization too small: scaling underflowed"};
+    if (e & 2) throw OtError{OTPRG_NUMERICAL, "regularization too small: scaling diverged"};
+    if (e & 4) throw OtError{OTPRG_NUMERICAL, "regularization too small: scaling underflowed"};
+    if (e & 8) throw OtError{OTPRG_NUMERICAL, "regularization too small: scaling diverged"};
+  };
+  // pinned per-iteration readback: [0] u-update bits, [1] v-update bits, [2..3] violation
+  if (ctx->ot_hpin_n < 64) {
+    if (ctx->ot_hpin) cudaFreeHost(ctx->ot_hpin);
+    ctx->ot_hpin = nullptr;
+    ctx->ot_hpin_n = 0;
+    OT_CK(cudaMallocHost(&ctx->ot_hpin, 64), "pinned staging");
+    ctx->ot_hpin_n = 64;
+  }
+  int* hb = static_cast<int*>(ctx->ot_hpin);
+  while (iters < cfg->max_iters) {
+    iters += 1;
+    std::swap(u, u_next);  // u-update (computed by the previous row pass; its bits in err[0])
+    OT_CK(cudaMemcpyAsync(err + 2, err, 4, cudaMemcpyDeviceToDevice, s), "save bits");
+    OT_CK(cudaMemsetAsync(err, 0, 8, s), "memset");
+    OT_CK(otprg::sk_col(K, n_a, n_b, u, nu, v, ctx->sk_part.as<double>(), err + 1, s), "col pass");
+    // violation of (u, v) and the next u-update from the same K v (bits -> err[0])
+    OT_CK(otprg::sk_row(K, n_a, n_b, u, v, mu, term, u_next, err, s), "row pass");
+    OT_CK(otprg::sk_sum(term, n_a, scalar, s), "violation");
+    OT_CK(cudaMemcpyAsync(hb, err + 1, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(hb + 2, scalar, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaStreamSynchronize(s), "sinkhorn iteration");
+    raise_err(hb[1] & 3);   // this iteration's u-update (sinkhorn.cpp:110-118)
+    raise_err(hb[0] & 12);  // its v-update (:120-128)
+    double viol;
+    std::memcpy(&viol, hb + 2, 8);
+    violation = viol;
+    if (violation <= cfg->tol) {
+      converged = true;
+      break;
+    }
+    if (cfg->time_budget_ms > 0.0 && t_loop.ms() > cfg->time_budget_ms) break;
+  }
+  r->iters = iters;
+  r->converged = converged ? 1 : 0;
+  r->marginal_violation = violation;
+  r->loop_ms = t_loop.ms();
+
+  // round_to_marginals (sinkhorn.cpp:12-66) on P = u K v
+  Timer t_round;
+  OT_CK(otprg::sk_plan(K, n_a, n_b, u, v, nullptr, nullptr, P, s), "plan");
+  OT_CK(otprg::sk_prow(P, n_a, n_b, mu, row, rs, s), "row sums");
+  OT_CK(otprg::sk_plan(K, n_a, n_b, u, v, rs, nullptr, P, s), "plan");
+  OT_CK(otprg::sk_pcol(P, n_a, n_b, ones, ctx->sk_part.as<double>(), col, s), "col sums");
+  OT_CK(otprg::sk_colscale(col, nu, n_b, cs, s), "col scale");
+  OT_CK(otprg::sk_plan(K, n_a, n_b, u, v, rs, cs, P, s), "plan");
+  OT_CK(otprg::sk_prow(P, n_a, n_b, mu, row, nullptr, s), "row sums");
+  OT_CK(otprg::sk_pcol(P, n_a, n_b, ones, ctx->sk_part.as<double>(), col, s), "col sums");
+  std::vector<double> hrow(n_a), hcol(n_b);
+  OT_CK(cudaMemcpyAsync(hrow.data(), row, n_a * 8ull, cudaMemcpyDeviceToHost, s), "D2H");
+  OT_CK(cudaMemcpyAsync(hcol.data(), col, n_b * 8ull, cudaMemcpyDeviceToHost, s), "D2H");
+  OT_CK(cudaStreamSynchronize(s), "round");
+  // greedy placement of the missing mass by index (:50-62)
+  std::vector<double> err_a(n_a);
+  for (int a = 0; a < n_a; ++a) err_a[a] = std::max(0.0, p->mu[a] - hrow[a]);
+  std::vector<int2> add_ab;
+  std::vector<double> add_v;
+  int a0 = 0;
+  for (int b = 0; b < n_b; ++b) {
+    double rest = std::max(0.0, p->nu[b] - hcol[b]);
+    while (a0 < n_a && !(err_a[a0] > 0.0)) ++a0;
+    for (int a = a0; a < n_a && rest > 0.0; ++a) {
+      const double add = std::min(err_a[a], rest);
+      if (add <= 0.0) continue;
+      add_ab.push_back(make_int2(a, b));
+      add_v.push_back(add);
+      err_a[a] -= add;
+      rest -= add;
+    }
+  }
+  if (!add_ab.empty()) {
+    OT_CK(ctx->v_k.ensure(add_ab.size() * (sizeof(int2) + 8)), "alloc adds");
+    int2* d_ab = reinterpret_cast<int2*>(ctx->v_k.p);
+    double* d_add = reinterpret_cast<double*>(d_ab + add_ab.size());
+    OT_CK(cudaMemcpyAsync(d_ab, add_ab.data(), add_ab.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
+          "H2D");
+    OT_CK(cudaMemcpyAsync(d_add, add_v.data(), add_v.size() * 8, cudaMemcpyHostToDevice, s), "H2D");
+    OT_CK(otprg::sk_adds(P, n_b, d_ab, d_add, static_cast<int>(add_ab.size()), s), "adds");
+  }
+  // entries p > 0 (row-major) and the plan cost (:64-72)
+  OT_CK(otprg::sk_rowcost(P, cost, n_a, n_b, rcost, rcnt, s), "row cost");
+  std::vector<double> hrc(n_a);
+  std::vector<long long> hcnt(n_a);
+  OT_CK(cudaMemcpyAsync(hrc.data(), rcost, n_a * 8ull, cudaMemcpyDeviceToHost, s), "D2H");
+  OT_CK(cudaMemcpyAsync(hcnt.data(), rcnt, n_a * 8ull, cudaMemcpyDeviceToHost, s), "D2H");
+  OT_CK(cudaStreamSynchronize(s), "plan cost");
+  double total = 0.0;
+  std::vector<long long> offs(static_cast<size_t>(n_a) + 1, 0);
+  for (int a = 0; a < n_a; ++a) {
+    total += hrc[a];
+    offs[a + 1] = offs[a] + hcnt[a];
+  }
+  r->cost = total;
+  r->n_entries = offs[n_a];
+  if (r->ent_a && r->entry_cap >= r->n_entries && r->n_entries > 0) {
+    const size_t ne = static_cast<size_t>(r->n_entries);
+    OT_CK(ctx->adm_off.ensure((static_cast<size_t>(n_a) + 1) * 8), "alloc");
+    OT_CK(ctx->ot_out.ensure(ne * 16), "alloc entries");
+    int32_t* ea = ctx->ot_out.as<int32_t>();
+    int32_t* eb = ea + ne;
+    double* em = reinterpret_cast<double*>(eb + ne);
+    OT_CK(cudaMemcpyAsync(ctx->adm_off.p, offs.data(), (n_a + 1) * 8ull, cudaMemcpyHostToDevice, s), "H2D");
+    OT_CK(otprg::sk_entries(P, n_a, n_b, ctx->adm_off.as<long long>(), ea, eb, em, s), "entries");
+    OT_CK(cudaMemcpyAsync(r->ent_a, ea, ne * 4, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(r->ent_b, eb, ne * 4, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(r->ent_mass, em, ne * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaStreamSynchronize(s), "entries");
+  }
+  r->round_ms = t_round.ms();
+}
+
 }  // namespace
 
 extern "C" {
@@ -679,6 +852,25 @@ int otprg_solve_ot(otprg_ctx* ctx, const otprg_ot_problem* prob, otprg_ot_result
   }
   try {
     OtSolver(ctx, prob, res).run();
+    return OTPRG_OK;
+  } catch (const OtError& e) {
+    ctx->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return OTPRG_DEVICE;
+  }
+}
+
+int otprg_sinkhorn(otprg_ctx* ctx, const otprg_ot_problem* prob, const otprg_sinkhorn_config* cfg,
+                   otprg_sinkhorn_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!res || (!res->ent_a && res->entry_cap > 0)) {
+    ctx->err = "result buffers are null";
+    return OTPRG_PARAMETER;
+  }
+  try {
+    run_sinkhorn(ctx, prob, cfg, res);
     return OTPRG_OK;
   } catch (const OtError& e) {
     ctx->err = e.msg;

@@ -481,7 +481,8 @@ void otprg_destroy(otprg_ctx* ctx) {
                     &ctx->fb, &ctx->stage, &ctx->pts, &ctx->flush, &ctx->trace, &ctx->sh_bounds,
                     &ctx->sh_pos, &ctx->sh_park[0], &ctx->sh_park[1], &ctx->sh_list, &ctx->v_out,
                     &ctx->v_k, &ctx->v_ya, &ctx->v_yb, &ctx->v_ma, &ctx->v_mb, &ctx->adm_cnt,
-                    &ctx->adm_off, &ctx->adm_list, &ctx->ot_t, &ctx->ot_req, &ctx->ot_out})
+                    &ctx->adm_off, &ctx->adm_list, &ctx->ot_t, &ctx->ot_req, &ctx->ot_out,
+                    &ctx->sk_K, &ctx->sk_P, &ctx->sk_vec, &ctx->sk_part, &ctx->sk_int})
     b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   for (auto& e : ctx->timer) cudaEventDestroy(e);

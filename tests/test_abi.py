@@ -63,6 +63,8 @@ def test_struct_layouts_match_header(lib):
     assert flat("otprg_ot_problem") == [f for f, _ in api._OTProblem._fields_]
     assert flat("otprg_ot_result") == [f for f, _ in api._OTResult._fields_]
     assert flat("otprg_feasibility") == [f for f, _ in _native.Feasibility._fields_]
+    assert flat("otprg_sinkhorn_config") == [f for f, _ in api._SkConfig._fields_]
+    assert flat("otprg_sinkhorn_result") == [f for f, _ in api._SkResult._fields_]
 
 
 def test_scaled_floor_matches_oracle(lib, oracle):

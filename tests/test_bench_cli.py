@@ -90,7 +90,7 @@ def test_cache_format_errors(tmp_path):
 
 def test_exit_codes_without_device(tmp_path):
     # parameter error: a solver the device library does not provide -> 2
-    assert B.main(["solve", "--solver", "sinkhorn", "--n", "4"]) == 2
+    assert B.main(["solve", "--solver", "hungarian", "--n", "4"]) == 2
     # input/format errors -> 3
     assert B.main(["solve", "--solver", "pushrelabel", "--in", str(tmp_path / "none.bin")]) == 3
     bad = tmp_path / "bad.bin"
@@ -124,7 +124,7 @@ def test_cli_solve_verify_and_bench_on_gpu(golden, tmp_path):
     assert f[0] == "pushrelabel" and f[1] == "1000" and f[4] == "1"
     assert float(f[5]).hex() == w["cost_hex"] and int(f[8]) == w["phases"]
     out, agg = tmp_path / "b.csv", tmp_path / "a.csv"
-    assert B.main(["bench", "--solvers", "pushrelabel", "pushrelabel-ot", "--n", "200", "--eps",
-                   "0.1", "--runs", "2", "--out", str(out), "--aggregate", str(agg)]) == 0
-    assert len(out.read_text().splitlines()) == 1 + 4
-    assert len(agg.read_text().splitlines()) == 1 + 2
+    assert B.main(["bench", "--solvers", "pushrelabel", "pushrelabel-ot", "sinkhorn", "--n", "200",
+                   "--eps", "0.1", "--runs", "2", "--out", str(out), "--aggregate", str(agg)]) == 0
+    assert len(out.read_text().splitlines()) == 1 + 6
+    assert len(agg.read_text().splitlines()) == 1 + 3
