@@ -197,3 +197,30 @@ def test_adhoc_unbalanced_vs_oracle(oracle):
         np.testing.assert_array_equal(s.duals_final.y_b, want.y_b)
         np.testing.assert_array_equal(s.free_counts, want.free_counts)
         assert s.device["cost"] == want.cost and s.swapped == want.swapped
+
+
+# ---- unbalanced instances at scale (assignment.cpp:385-399)
+def _rect_pins():
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "assign_rect_pins.json")
+    with open(p) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("key", sorted(_rect_pins()))
+@pytest.mark.parametrize("form", ["points", "dense"])
+def test_unbalanced_at_scale_match_reference(key, form):
+    w = _rect_pins()[key]
+    big = otprg.gen_uniform_square(max(w["n_a"], w["n_b"]), w["seed"])
+    pa, pb = big.pts_a[: w["n_a"]], big.pts_b[: w["n_b"]]
+    if form == "points":
+        inst = otprg.AssignmentInstance(w["n_a"], w["n_b"], pts_a=pa, pts_b=pb,
+                                        norm_factor=big.norm_factor)
+    else:
+        inst = otprg.AssignmentInstance(w["n_a"], w["n_b"], otprg.points_cost(pa, pb))
+    m, s = _solve(inst, w["eps"])
+    got = _pins(m, s)
+    assert {k: got[k] for k in PIN_KEYS} == {k: w[k] for k in PIN_KEYS}, key
+    assert bool(s.swapped) == bool(w["swapped"])
+    assert m.size() == min(w["n_a"], w["n_b"])
