@@ -45,6 +45,13 @@ inline int64_t host_scaled_floor(double c, double eps) {
 
 }  // namespace otprg
 
+struct otprg_ctx;
+namespace otprg {
+// Large H2D from caller memory that may be pageable (h2d.cpp).
+cudaError_t h2d_large(otprg_ctx* ctx, void* dst, const void* src, size_t bytes);
+void release_bounce(otprg_ctx* ctx);
+}  // namespace otprg
+
 struct otprg_ctx {
   using DevBuf = otprg::DevBuf;
   int device = 0;
@@ -95,6 +102,10 @@ struct otprg_ctx {
 
   // invariant suite / workset export (verify_kernels.cu)
   DevBuf v_out, v_k, v_ya, v_yb, v_ma, v_mb, adm_cnt, adm_off, adm_list;
+
+  // pinned bounce buffers for large copies from pageable host memory (h2d.cpp)
+  void* bounce[2] = {nullptr, nullptr};
+  cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
 
   // Sinkhorn baseline (ot_host.cpp / sinkhorn_kernels.cu)
   DevBuf sk_K, sk_P, sk_vec, sk_part, sk_int;

@@ -278,8 +278,7 @@ class OtSolver {
     OT_CK(ctx_->stage.ensure(bytes), "alloc cost staging");
     OT_CK(ctx_->kT.ensure(static_cast<size_t>(n_b_) * lda_ * width_), "alloc kT");
     OT_CK(ctx_->ctl.ensure(sizeof(otprg::Ctl)), "alloc ctl");
-    OT_CK(cudaMemcpyAsync(ctx_->stage.p, p_->cost, bytes, cudaMemcpyHostToDevice, ctx_->stream),
-          "H2D cost");
+    OT_CK(otprg::h2d_large(ctx_, ctx_->stage.p, p_->cost, bytes), "H2D cost");
     OT_CK(cudaMemsetAsync(ctx_->ctl.p, 0, sizeof(otprg::Ctl), ctx_->stream), "memset");
     int* status = &ctx_->ctl.as<otprg::Ctl>()->status;
     OT_CK(otprg::launch_round_dense(ctx_->stage.as<double>(), n_a_, n_b_, false, eps_in_, ctx_->kT.p,
@@ -676,7 +675,7 @@ void run_sinkhorn(otprg_ctx* ctx, const otprg_ot_problem* p, const otprg_sinkhor
   double* cost = ctx->stage.as<double>();
   double* K = ctx->sk_K.as<double>();
   double* P = ctx->sk_P.as<double>();
-  OT_CK(cudaMemcpyAsync(cost, p->cost, nn * 8, cudaMemcpyHostToDevice, s), "H2D cost");
+  OT_CK(otprg::h2d_large(ctx, cost, p->cost, nn * 8), "H2D cost");
   OT_CK(cudaMemcpyAsync(mu, p->mu, n_a * 8ull, cudaMemcpyHostToDevice, s), "H2D mu");
   OT_CK(cudaMemcpyAsync(nu, p->nu, n_b * 8ull, cudaMemcpyHostToDevice, s), "H2D nu");
   OT_CK(cudaMemsetAsync(err, 0, 32, s), "memset");

@@ -135,8 +135,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   if (p->cost_kind == OTPRG_COST_DENSE_F64) {
     const size_t bytes = static_cast<size_t>(p->n_a) * p->n_b * sizeof(double);
     CK(ctx->stage.ensure(bytes), "alloc cost staging");
-    CK(cudaMemcpyAsync(ctx->stage.p, p->cost, bytes, cudaMemcpyHostToDevice, ctx->stream),
-       "H2D cost");
+    CK(otprg::h2d_large(ctx, ctx->stage.p, p->cost, bytes), "H2D cost");
     CK(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(Ctl), ctx->stream), "memset");
     int* status = &ctx->ctl.as<Ctl>()->status;
     CK(otprg::launch_round_dense(ctx->stage.as<double>(), p->n_a, p->n_b, ctx->swapped, p->eps,
@@ -488,6 +487,7 @@ void otprg_destroy(otprg_ctx* ctx) {
   for (auto& e : ctx->timer) cudaEventDestroy(e);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
   if (ctx->ot_hpin) cudaFreeHost(ctx->ot_hpin);
+  otprg::release_bounce(ctx);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
