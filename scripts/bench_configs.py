@@ -1,0 +1,139 @@
+"""Timings of BASELINE.json configs 1, 3, 4, 5 on one B200 (config 2 is bench.py),
+each with its parity check, next to the reference CPU solver.
+
+    python scripts/bench_configs.py > profiles/r01_configs.json
+
+Reference CPU times: config 1 is measured live here (oracle/_ref, 1 thread);
+configs 3 and 5 are the reference timings recorded when the golden fixtures
+were generated (tests/golden/*_pins.json, build container, 1 thread) because
+the reference needs minutes for them (cost build 119 s + solve 64 s for
+config 3 at eps = 0.01; 36 s for config 5).
+"""
+import json
+import os
+import statistics
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import numpy as np  # noqa: E402
+
+import paper_2203_03732_b200 as otprg  # noqa: E402
+from golden_util import PIN_KEYS, pins_of  # noqa: E402
+from paper_2203_03732_b200.instances import make_synthetic_mnist  # noqa: E402
+
+
+def pins(m, s):
+    return pins_of(m.match_of_a, s.duals_final.y_a, s.duals_final.y_b, s.free_counts, s.phases,
+                   s.sum_ni, s.device["cost"])
+
+
+def golden(name):
+    with open(os.path.join(ROOT, "tests", "golden", name)) as f:
+        return json.load(f)
+
+
+def wall(fn, reps):
+    out = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = fn()
+        out.append((time.perf_counter() - t0) * 1e3)
+    return statistics.median(out), r
+
+
+def config1():
+    g = golden("assign_pins.json")
+    sv = otprg.Solver(0)
+    ok, dev, e2e = True, [], []
+    for seed in range(1, 31):
+        inst = otprg.gen_uniform_square(1000, seed)
+        ms, (m, s) = wall(lambda: sv.solve(inst, otprg.AssignmentOptions(eps=0.1)), 3)
+        e2e.append(ms)
+        dev.append(s.device["solve_ms"])
+        w = g[f"square_n1000_eps0.1_s{seed}"]
+        ok &= all(pins(m, s)[k] == w[k] for k in PIN_KEYS)
+    ref = None
+    try:
+        from oracle.pyoracle import Reference
+        if Reference.available():
+            R = Reference.get()
+            ref = statistics.median(R.solve_uniform_square(1000, s, 0.1, threads=1).solve_ms
+                                    for s in range(1, 6))
+    except Exception:  # noqa: BLE001
+        pass
+    return {"workload": "config 1: gen_uniform_square(1000, seeds 1..30), eps=0.1, points in",
+            "gpu_device_solve_ms_median": round(statistics.median(dev), 4),
+            "gpu_e2e_ms_median": round(statistics.median(e2e), 3),
+            "bit_exact_all_30_seeds": bool(ok),
+            "reference_cpu_ms_median_seeds_1_5": None if ref is None else round(ref, 3),
+            "reference_note": "measured live, oracle/_ref, 1 thread, incl. its rounding"}
+
+
+def config3():
+    g = golden("mnist_pins.json")
+    d = tempfile.mkdtemp()
+    path = make_synthetic_mnist(os.path.join(d, "synth-images-idx3-ubyte"), 20000, 0)
+    inst = otprg.load_mnist_pair(path, 10000, 1)
+    sv = otprg.Solver(0)
+    rows = []
+    for eps in (0.1, 0.05, 0.01):
+        ms, (m, s) = wall(lambda: sv.solve(inst, otprg.AssignmentOptions(eps=eps)), 3)
+        key = f"mnist_n10000_eps{eps!r}_s1"
+        w = g.get(key)
+        rows.append({"eps": eps, "gpu_e2e_ms": round(ms, 3),
+                     "gpu_cost_build_ms": round(s.device["build_ms"], 3),
+                     "gpu_solve_ms": round(s.device["solve_ms"], 3), "phases": s.phases,
+                     "bit_exact": None if w is None else all(pins(m, s)[k] == w[k] for k in PIN_KEYS),
+                     "reference_cpu_ms": None if w is None else
+                     round(w["ref_load_s"] * 1e3 + w["ref_solve_ms"], 1)})
+    return {"workload": "config 3: synthetic MNIST-shaped IDX3 (20000 images, seed 0), "
+                        "load_mnist_pair(n=10000, seed=1), L1/2 cost built on the device",
+            "runs": rows,
+            "reference_note": "reference = load_mnist_pair cost build + solve_assignment, recorded "
+                              "at golden generation (build container, 1 thread)"}
+
+
+def config4():
+    from paper_2203_03732_b200.sharded import ShardedSolver
+    inst = otprg.gen_uniform_square(100_000, 1)
+    sv = otprg.Solver(0)
+    ms, (m1, s1) = wall(lambda: sv.solve(inst, otprg.AssignmentOptions(eps=0.01)), 2)
+    sh = ShardedSolver(inst, otprg.AssignmentOptions(eps=0.01), 1)
+    sms, (m2, s2) = wall(sh.solve, 2)
+    same = bool(np.array_equal(m1.match_of_a, m2.match_of_a)
+                and np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a))
+    sh.close()
+    sv.close()
+    return {"workload": "config 4: gen_uniform_square(100000, 1) points, eps=0.01 (uint16 kT 20 GB)",
+            "single_gpu_fused": {"e2e_ms": round(ms, 2), "build_ms": round(s1.device["build_ms"], 2),
+                                 "solve_ms": round(s1.device["solve_ms"], 3), "phases": s1.phases},
+            "sharded_g1_wall_ms": round(sms, 2), "sharded_bit_identical": same,
+            "note": "no CPU reference at this size (the reference needs hours); parity through the "
+                    "sharded/fused bit-identity and the sharded golden tests"}
+
+
+def config5():
+    g = golden("ot_pins.json")["ot_rational_20000x20000_s1_eps0.01"]
+    inst = otprg.gen_random_ot_rational(20000, 20000, 1)
+    ms, (plan, st) = wall(lambda: otprg.solve_ot(inst, 0.01), 2)
+    return {"workload": "config 5: gen_random_ot_rational(20000, 20000, 1), solve_ot eps=0.01",
+            "gpu_e2e_ms": round(ms, 2), "gpu_build_ms": round(st.device["build_ms"], 2),
+            "gpu_loop_ms": round(st.device["loop_ms"], 2), "phases": st.phases,
+            "cost_bits_match_reference": float(plan.cost).hex() == g["cost_hex"],
+            "entries_match_reference": len(plan.a) == g["n_entries"],
+            "reference_cpu_ms": g["ref_solve_ms"],
+            "reference_note": "recorded at golden generation (build container, 1 thread)"}
+
+
+if __name__ == "__main__":
+    out = {}
+    for name, fn in (("config1", config1), ("config3", config3), ("config4", config4),
+                     ("config5", config5)):
+        t0 = time.time()
+        out[name] = fn()
+        print(f"{name} done in {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
+    print(json.dumps(out, indent=1))
