@@ -411,6 +411,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     unsigned long long old = 0, hp = 0;
     int ma = -1;
     OTPRG_STAT(7);
+    if (acc && lead) acc[2] += 1;  // proposals of this warp's chains (timeline)
     const unsigned long long ta0 = acc ? globaltimer() : 0;
     if (lead) {
       old = atomicMin(H + a, key);
@@ -717,7 +718,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     const int teams_per_block = warps_per_block / tsize;
     const int total_teams = gridDim.x * teams_per_block;
     int i = tib * (int)gridDim.x + (int)blockIdx.x;
-    unsigned long long acc[2] = {0ull, 0ull};
+    unsigned long long acc[3] = {0ull, 0ull, 0ull};
+    const unsigned long long steps0 = steps, walks0 = walks;
     const unsigned long long tp0 = tr ? globaltimer() : 0;
     const bool had_work = i < n_slots;
     // The prefetched prologue is current unless the bulk build rewrote it.
@@ -742,6 +744,10 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       atomicMax(tr + 1, acc[0]);
       atomicMax(tr + 5, acc[1]);
       atomicMax(tr + 6, globaltimer() - tp0);
+      // chain structure maxima over warps: row scans, cache walks, proposals
+      atomicMax(tr + 10, steps - steps0);
+      atomicMax(tr + 11, walks - walks0);
+      atomicMax(tr + 12, acc[2]);
     }
     bar_target += gridDim.x;
     grid_barrier(ctl, bar_target, tr ? tr + 2 : nullptr, tr ? tr + 3 : nullptr);

@@ -30,12 +30,15 @@ scan, atom, warp = tr[:, 1], tr[:, 5], tr[:, 6]
 bulk = np.where(tr[:, 8] > 0, tr[:, 8] - t0, 0)
 print(f"solve_ms={s.device['solve_ms']:.3f} phase1_ms={s.device['phase1_ms']:.3f} "
       f"loop_ms={s.device['loop_ms']:.3f} phases={s.phases} width={s.device['width']}")
-print("phase   n_i   bulk  Pfirst  Plast   bar   next | slowest warp: total  scan  atomic (us)")
+print("phase   n_i   bulk  Pfirst  Plast   bar   next | slowest warp: total  scan  atomic (us) | max/warp: scans walks props")
 rows = list(range(0, min(8, s.phases))) + list(range(8, s.phases, max(1, s.phases // 20)))
 for i in rows:
     print(f"{i+1:5d} {tr[i,7]:5d} {bulk[i]/1e3:6.2f} {p_first[i]/1e3:7.2f} {p_last[i]/1e3:6.2f} "
-          f"{bar[i]/1e3:6.2f} {nxt[i]/1e3:6.2f} | {warp[i]/1e3:6.2f} {scan[i]/1e3:6.2f} {atom[i]/1e3:6.2f}")
+          f"{bar[i]/1e3:6.2f} {nxt[i]/1e3:6.2f} | {warp[i]/1e3:6.2f} {scan[i]/1e3:6.2f} {atom[i]/1e3:6.2f} | "
+          f"{tr[i,10]:4d} {tr[i,11]:4d} {tr[i,12]:4d}")
 sl = slice(1, s.phases - 1)
 print("means over phases 2..: Pfirst %.2f Plast %.2f bar %.2f next %.2f | warp %.2f scan %.2f atomic %.2f" % tuple(
     x[sl].mean() / 1e3 for x in (p_first, p_last, bar, nxt, warp, scan, atom)))
+print("means over phases 2..: max scans/warp %.2f walks %.2f props %.2f" % tuple(
+    tr[sl, j].mean() for j in (10, 11, 12)))
 print("chain stats", s.device["chain_stats"], "bytes_touched", s.device["bytes_touched"] / 1e6, "MB")
