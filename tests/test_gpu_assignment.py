@@ -224,3 +224,31 @@ def test_unbalanced_at_scale_match_reference(key, form):
     assert {k: got[k] for k in PIN_KEYS} == {k: w[k] for k in PIN_KEYS}, key
     assert bool(s.swapped) == bool(w["swapped"])
     assert m.size() == min(w["n_a"], w["n_b"])
+
+
+# ---- degenerate inputs (ties, exact multiples of eps, extreme shapes) ------
+@pytest.mark.parametrize("case", ["zeros", "ones", "multiples", "two_values", "single_row",
+                                  "single_col"])
+def test_degenerate_costs_match_oracle(oracle, case):
+    rng = np.random.default_rng(17)
+    eps = 0.05
+    if case == "zeros":
+        cost = np.zeros((300, 300))          # every edge admissible: maximal contention
+    elif case == "ones":
+        cost = np.ones((257, 200))
+    elif case == "multiples":                 # exact multiples of eps (scaled_floor boundaries)
+        cost = rng.integers(0, 21, (256, 256)) * eps
+        cost = np.minimum(cost, 1.0)
+    elif case == "two_values":
+        cost = np.where(rng.random((400, 333)) < 0.5, 0.25, 0.75)
+    elif case == "single_row":
+        cost = rng.random((1, 500))
+    else:
+        cost = rng.random((500, 1))
+    want = oracle.solve_assignment(cost, eps)
+    m, s = _solve(otprg.AssignmentInstance(*cost.shape, cost), eps)
+    np.testing.assert_array_equal(m.match_of_a, want.match_of_a)
+    np.testing.assert_array_equal(s.duals_final.y_a, want.y_a)
+    np.testing.assert_array_equal(s.duals_final.y_b, want.y_b)
+    np.testing.assert_array_equal(s.free_counts, want.free_counts)
+    assert s.device["cost"] == want.cost
