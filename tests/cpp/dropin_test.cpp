@@ -1,0 +1,229 @@
+// dropin_test.cpp — the C++ drop-in check: the same calls against the
+// UNMODIFIED reference (namespace otpr, oracle/_ref/libotpr_ref.so) and
+// against this library (namespace otprg, libotprg.so), side by side in one
+// program, results compared field by field.  Needs a GPU (run by
+// tests/test_gpu_cpp_dropin.py).  Built by tests/cpp/Makefile (needs the
+// reference headers, i.e. the build container).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "otpr/assignment.hpp"
+#include "otpr/core.hpp"
+#include "otpr/instances.hpp"
+#include "otpr/ot.hpp"
+#include "otpr/sinkhorn.hpp"
+#include "otprg.hpp"
+
+static int g_fail = 0;
+#define EXPECT(cond, what)                                       \
+  do {                                                           \
+    if (!(cond)) {                                               \
+      std::printf("FAIL %s (%s:%d)\n", what, __FILE__, __LINE__); \
+      ++g_fail;                                                  \
+    }                                                            \
+  } while (0)
+
+static otprg::AssignmentInstance to_g(const otpr::AssignmentInstance& r) {
+  otprg::AssignmentInstance g;
+  g.n_a = r.n_a;
+  g.n_b = r.n_b;
+  g.cost = otprg::Matrix<double>(r.n_a, r.n_b);
+  std::memcpy(g.cost.data(), r.cost.data(), r.cost.size() * sizeof(double));
+  g.norm_factor = r.norm_factor;
+  g.seed = r.seed;
+  return g;
+}
+
+static otpr::AssignmentInstance random_instance(int n_a, int n_b, uint64_t seed) {  // test_util.hpp
+  std::mt19937_64 rng(seed);
+  otpr::AssignmentInstance inst;
+  inst.n_a = n_a;
+  inst.n_b = n_b;
+  inst.cost = otpr::Matrix<double>(n_a, n_b);
+  for (int a = 0; a < n_a; ++a)
+    for (int b = 0; b < n_b; ++b) inst.cost(a, b) = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+  return inst;
+}
+
+template <typename MR, typename SR, typename MG, typename SG>
+static void same_result(const MR& mr, const SR& sr, const MG& mg, const SG& sg, const char* name) {
+  EXPECT(mr.match_of_a == mg.match_of_a, name);
+  EXPECT(mr.match_of_b == mg.match_of_b, name);
+  EXPECT(sr.phases == sg.phases, name);
+  EXPECT(sr.free_counts == sg.free_counts, name);
+  EXPECT(sr.sum_ni == sg.sum_ni, name);
+  EXPECT(sr.duals_final.y_a == sg.duals_final.y_a, name);
+  EXPECT(sr.duals_final.y_b == sg.duals_final.y_b, name);
+  EXPECT(sr.swapped == sg.swapped, name);
+  EXPECT(sr.full_match_termination == sg.full_match_termination, name);
+}
+
+static void assignment_cases() {
+  for (uint64_t seed : {1, 2, 3}) {
+    const otpr::AssignmentInstance r = otpr::gen_uniform_square(1000, seed);
+    otpr::AssignmentOptions ro;
+    ro.eps = 0.01;
+    auto [mr, sr] = otpr::solve_assignment(r, ro);
+    otprg::AssignmentOptions go;
+    go.eps = 0.01;
+    const otprg::AssignmentInstance g = to_g(r);
+    auto [mg, sg] = otprg::solve_assignment(g, go);
+    same_result(mr, sr, mg, sg, "square dense");
+    EXPECT(otpr::matching_cost(mr, r) == otprg::matching_cost(mg, g), "matching_cost bits");
+    // the point-set form (cost built on the device)
+    otprg::AssignmentInstance gp = otprg::gen_uniform_square(1000, seed);
+    gp.cost = otprg::Matrix<double>();
+    auto [mp, sp] = otprg::solve_assignment(gp, go);
+    same_result(mr, sr, mp, sp, "square points");
+    EXPECT(otpr::matching_cost(mr, r) == otprg::matching_cost(mp, gp), "points matching_cost bits");
+  }
+  for (auto [na, nb] : {std::pair{300, 170}, std::pair{170, 300}}) {
+    const otpr::AssignmentInstance r = random_instance(na, nb, 40 + na);
+    otpr::AssignmentOptions ro;
+    ro.eps = 0.03;
+    otprg::AssignmentOptions go;
+    go.eps = 0.03;
+    auto [mr, sr] = otpr::solve_assignment(r, ro);
+    auto [mg, sg] = otprg::solve_assignment(to_g(r), go);
+    same_result(mr, sr, mg, sg, "rectangular");
+  }
+  // rounding
+  {
+    const otpr::AssignmentInstance r = random_instance(200, 150, 9);
+    const auto kr = otpr::scale_round_costs(r, 0.007);
+    const auto kg = otprg::scale_round_costs(to_g(r), 0.007);
+    EXPECT(kr.unit_floor == kg.unit_floor && kr.unit_ceil == kg.unit_ceil, "units");
+    EXPECT(std::memcmp(kr.k.data(), kg.k.data(), kr.k.size() * 4) == 0, "rounded costs");
+    EXPECT(otpr::scaled_floor(0.57, 0.1) == otprg::scaled_floor(0.57, 0.1), "scaled_floor");
+  }
+  // errors
+  {
+    const otpr::AssignmentInstance r = random_instance(4, 4, 1);
+    otprg::AssignmentOptions go;
+    go.eps = 1.0;
+    bool thrown = false;
+    try {
+      otprg::solve_assignment(to_g(r), go);
+    } catch (const otprg::ParameterError&) {
+      thrown = true;
+    }
+    EXPECT(thrown, "eps = 1 -> ParameterError");
+  }
+}
+
+struct PhaseRec {
+  int phase;
+  std::vector<otpr::Index> b_free, m_prime_a, m_prime_b, a_double, a_touched;
+  std::vector<std::vector<otpr::Index>> e_admissible;
+  std::vector<otpr::DualUnits> y_a, y_b;
+  otpr::DualUnits before, after;
+};
+
+static void observer_cases() {
+  for (uint64_t seed : {131, 262}) {
+    const otpr::AssignmentInstance r = random_instance(30, 30, seed);
+    std::vector<PhaseRec> ref;
+    otpr::AssignmentOptions ro;
+    ro.eps = 0.08;
+    ro.check_invariants = true;
+    ro.observer = [&](const otpr::PhaseSnapshot& s) {
+      PhaseRec p{s.phase, s.workset.b_free, {}, {}, s.workset.a_double, s.workset.a_touched,
+                 s.workset.e_admissible, s.duals.y_a, s.duals.y_b, s.sum_abs_before, s.sum_abs_after};
+      for (auto [a, b] : s.workset.m_prime) {
+        p.m_prime_a.push_back(a);
+        p.m_prime_b.push_back(b);
+      }
+      ref.push_back(std::move(p));
+    };
+    auto [mr, sr] = otpr::solve_assignment(r, ro);
+    size_t i = 0;
+    otprg::AssignmentOptions go;
+    go.eps = 0.08;
+    go.check_invariants = true;
+    go.observer = [&](const otprg::PhaseSnapshot& s) {
+      if (i >= ref.size()) {
+        EXPECT(false, "more phases than the reference");
+        return;
+      }
+      const PhaseRec& p = ref[i++];
+      EXPECT(p.phase == s.phase, "phase");
+      EXPECT(p.b_free == s.workset.b_free, "B'");
+      EXPECT(p.e_admissible == s.workset.e_admissible, "E'");
+      EXPECT(p.a_touched == s.workset.a_touched, "A'");
+      EXPECT(p.a_double == s.workset.a_double, "A''");
+      std::vector<otpr::Index> ma, mb;
+      for (auto [a, b] : s.workset.m_prime) {
+        ma.push_back(a);
+        mb.push_back(b);
+      }
+      EXPECT(p.m_prime_a == ma && p.m_prime_b == mb, "M'");
+      EXPECT(p.y_a == s.duals.y_a && p.y_b == s.duals.y_b, "duals");
+      EXPECT(p.before == s.sum_abs_before && p.after == s.sum_abs_after, "sum_abs");
+    };
+    auto [mg, sg] = otprg::solve_assignment(to_g(r), go);
+    EXPECT(i == ref.size(), "phase count seen by the observer");
+    same_result(mr, sr, mg, sg, "observer run");
+  }
+  // verify_feasibility on a corrupted state: same first message and count
+  const otpr::AssignmentInstance r = random_instance(4, 4, 9);
+  const auto sc = otpr::scale_round_costs(r, 0.2);
+  auto [m, d] = otpr::init_state(sc);
+  d.y_b[2] += 10;
+  const auto rr = otpr::verify_feasibility(sc, d, m);
+  otprg::ScaledCosts gsc;
+  gsc.eps = sc.eps;
+  gsc.unit_floor = sc.unit_floor;
+  gsc.unit_ceil = sc.unit_ceil;
+  gsc.k = otprg::Matrix<std::int32_t>(4, 4);
+  std::memcpy(gsc.k.data(), sc.k.data(), 16 * 4);
+  otprg::DualState gd{d.y_a, d.y_b};
+  otprg::Matching gm(4, 4);
+  const auto gr = otprg::verify_feasibility(gsc, gd, gm);
+  EXPECT(!rr.ok() && !gr.ok(), "violations found");
+  EXPECT(rr.violations.front() == gr.violations.front(), "first violation message");
+  EXPECT(static_cast<int64_t>(rr.violations.size()) == gr.count, "violation count");
+}
+
+static void ot_cases() {
+  const otpr::OTInstance r = otpr::gen_random_ot_rational(300, 200, 3);
+  otprg::OTInstance g;
+  g.mu = r.mu;
+  g.nu = r.nu;
+  g.cost = otprg::Matrix<double>(300, 200);
+  std::memcpy(g.cost.data(), r.cost.data(), r.cost.size() * sizeof(double));
+  auto [pr, sr] = otpr::solve_ot(r, 0.01);
+  auto [pg, sg] = otprg::solve_ot(g, 0.01);
+  EXPECT(pr.cost == pg.cost, "OT cost bits");
+  EXPECT(pr.entries.size() == pg.entries.size(), "OT entry count");
+  bool same = pr.entries.size() == pg.entries.size();
+  for (size_t i = 0; same && i < pr.entries.size(); ++i)
+    same = pr.entries[i].a == pg.entries[i].a && pr.entries[i].b == pg.entries[i].b &&
+           pr.entries[i].mass == pg.entries[i].mass;
+  EXPECT(same, "OT plan entries");
+  EXPECT(sr.phases == sg.phases && sr.free_counts == sg.free_counts, "OT phases");
+  otpr::SinkhornConfig rc;
+  rc.reg = 0.05;
+  otprg::SinkhornConfig gc;
+  gc.reg = 0.05;
+  const auto kr = otpr::sinkhorn(r, rc);
+  const auto kg = otprg::sinkhorn(g, gc);
+  EXPECT(std::abs(kr.iters - kg.iters) <= 1, "sinkhorn iterations");
+  EXPECT(std::abs(kr.cost - kg.cost) <= 1e-9 * std::abs(kr.cost), "sinkhorn cost");
+}
+
+int main() {
+  assignment_cases();
+  observer_cases();
+  ot_cases();
+  if (g_fail) {
+    std::printf("dropin: %d failures\n", g_fail);
+    return 1;
+  }
+  std::printf("dropin: all checks passed\n");
+  return 0;
+}

@@ -106,3 +106,27 @@ def test_create_without_device_reports_status(lib):
         pytest.skip("a device is present")
     ctx = C.c_void_p()
     assert lib.otprg_create(0, C.byref(ctx)) == 6
+
+
+def test_cpp_api_header_compiles_and_links(lib, tmp_path):
+    """include/otprg.hpp (the reference's C++ API in namespace otprg) compiles
+    as C++17 and links against libotprg.so; host-only calls run without a GPU."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "otprg.hpp"\n'
+                   'int main() {\n'
+                   '  if (otprg::scaled_floor(0.57, 0.1) != 5) return 1;\n'
+                   '  otprg::Matching m(3, 2); m.link(1, 0); m.validate();\n'
+                   '  if (m.size() != 1) return 2;\n'
+                   '  try { otprg::AssignmentInstance i; i.validate(); return 3; }\n'
+                   '  catch (const otprg::ParameterError&) {}\n'
+                   '  return 0;\n'
+                   '}\n')
+    exe = tmp_path / "t"
+    libdir = os.path.join(root, "paper_2203_03732_b200", "lib")
+    r = subprocess.run(["g++", "-std=c++17", "-I", os.path.join(root, "include"), str(src), "-o", str(exe),
+                        "-L", libdir, "-lotprg", f"-Wl,-rpath,{libdir}", "-Wl,-rpath,/usr/local/cuda/lib64"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(exe)]).returncode == 0
