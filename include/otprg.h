@@ -157,6 +157,24 @@ int otprg_step(otprg_ctx* ctx, int64_t max_phases, int64_t* phases_done, int32_t
 int otprg_snapshot(otprg_ctx* ctx, otprg_result* res);
 int otprg_finish(otprg_ctx* ctx, otprg_result* res);
 
+/* ---- copy mode ---------------------------------------
+ * solve_assignment with AssignmentOptions::demand_groups / supply_groups
+ * (assignment.hpp:81-89; scan order assignment.cpp:81-103, supply-copy dual
+ * lift :241-250): every phase visits the admissible demand copies of a free
+ * b in group order (free copies first, then matched copies by their
+ * partner's supply group), and free supply copies are raised to their
+ * group's maximum dual.  Requires n_b <= n_a (ParameterError otherwise, as
+ * the reference).  Host-synced phases (copy mode serves the reference's
+ * OT-equivalence checks, not the benchmark path):
+ *   otprg_groups_begin   prepare + init_state with the group maps
+ *   otprg_groups_step    run one phase (finished once the termination test passed)
+ *   otprg_snapshot / otprg_verify_feasibility / otprg_admissible work between steps
+ *   otprg_groups_finish  remaining phases, completion, results (as otprg_solve_assignment) */
+int otprg_groups_begin(otprg_ctx* ctx, const otprg_problem* prob, const int32_t* demand_groups,
+                       const int32_t* supply_groups);
+int otprg_groups_step(otprg_ctx* ctx, int64_t* phases_done, int32_t* finished);
+int otprg_groups_finish(otprg_ctx* ctx, otprg_result* res);
+
 /* ---- invariant suite (reference A12) ----------------
  * verify_feasibility (assignment.cpp:264-312) evaluated on the device.  The
  * result is the number of violations and the FIRST one in the reference's

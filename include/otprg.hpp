@@ -8,9 +8,9 @@
 // libraries side by side (tests/cpp/dropin_test.cpp does).  C++17.
 //
 // Device path: results equal the reference's threads = 1 results bit for bit
-// (the Sinkhorn baseline to a floating-point tolerance).  Not provided:
-// copy mode (AssignmentOptions::demand_groups / supply_groups) and the OT
-// observer / check_invariants -> ParameterError.  AssignmentOptions::threads
+// (the Sinkhorn baseline to a floating-point tolerance), copy mode
+// (AssignmentOptions::demand_groups / supply_groups) included.  Not provided:
+// the OT observer / check_invariants (OTOptions).  AssignmentOptions::threads
 // is accepted and ignored (the device path is always deterministic).
 #pragma once
 

@@ -275,6 +275,8 @@ class Reference:
         outs = [_i32p, _i32p, _i64p, _i64p, _i64p, C.c_int64, C.POINTER(_RefStats)]
         lib.ref_solve_assignment.argtypes = [C.c_int32, C.c_int32, _f64p, C.c_double, C.c_int] + outs
         lib.ref_solve_uniform_square.argtypes = [C.c_int32, C.c_uint64, C.c_double, C.c_int, C.c_int] + outs
+        lib.ref_solve_assignment_groups.argtypes = ([C.c_int32, C.c_int32, _f64p, C.c_double, _i32p, _i32p,
+                                                     C.c_int32] + outs)
         lib.ref_load_mnist_pair.argtypes = [C.c_char_p, C.c_int32, C.c_uint64, _f64p]
         lib.ref_solve_mnist.argtypes = ([C.c_char_p, C.c_int32, C.c_uint64, C.c_double, C.c_int] + outs
                                         + [C.POINTER(C.c_double)])
@@ -324,6 +326,19 @@ class Reference:
         s = _RefStats()
         self._check(self.lib.ref_solve_assignment(n_a, n_b, cost, eps, threads, ma, mb, ya, yb, fc, cap,
                                                   C.byref(s)))
+        return self._result(ma, mb, ya, yb, fc, s)
+
+    def solve_assignment_groups(self, cost: np.ndarray, eps: float, demand_groups, supply_groups,
+                                check_invariants: bool = False) -> AssignResult:
+        """Copy mode (assignment.cpp:81-103, :241-250), threads = 1."""
+        cost = np.ascontiguousarray(cost, np.float64)
+        n_a, n_b = cost.shape
+        ma, mb, ya, yb, fc, cap = self._outs(n_a, n_b, eps)
+        s = _RefStats()
+        dg = np.ascontiguousarray(demand_groups, np.int32)
+        sg = np.ascontiguousarray(supply_groups, np.int32)
+        self._check(self.lib.ref_solve_assignment_groups(n_a, n_b, cost, eps, dg, sg, int(check_invariants),
+                                                         ma, mb, ya, yb, fc, cap, C.byref(s)))
         return self._result(ma, mb, ya, yb, fc, s)
 
     def solve_uniform_square(self, n: int, seed: int, eps: float, threads: int = 1,

@@ -393,4 +393,30 @@ int ref_sinkhorn(int32_t n_a, int32_t n_b, const double* mu, const double* nu, c
   });
 }
 
+// solve_assignment in copy mode (AssignmentOptions::demand_groups /
+// supply_groups, assignment.cpp:81-103, :241-250), threads = 1; with
+// check_invariants when asked.
+int ref_solve_assignment_groups(int32_t n_a, int32_t n_b, const double* cost, double eps,
+                                const int32_t* demand_groups, const int32_t* supply_groups,
+                                int32_t check_invariants, int32_t* match_of_a, int32_t* match_of_b,
+                                int64_t* y_a, int64_t* y_b, int64_t* free_counts, int64_t free_cap,
+                                RefStats* out) {
+  return guarded([&] {
+    const otpr::AssignmentInstance inst = wrap(n_a, n_b, cost);
+    const std::vector<otpr::Index> dg(demand_groups, demand_groups + n_a);
+    const std::vector<otpr::Index> sg(supply_groups, supply_groups + n_b);
+    otpr::AssignmentOptions opt;
+    opt.eps = eps;
+    opt.demand_groups = &dg;
+    opt.supply_groups = &sg;
+    opt.check_invariants = check_invariants != 0;
+    const auto t0 = Clock::now();
+    auto [m, s] = otpr::solve_assignment(inst, opt);
+    out->solve_ms = ms_since(t0);
+    out->cost = otpr::matching_cost(m, inst);
+    out->round_ms = 0.0;
+    export_result(m, s, match_of_a, match_of_b, y_a, y_b, free_counts, free_cap, out);
+  });
+}
+
 }  // extern "C"

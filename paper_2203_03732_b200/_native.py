@@ -64,7 +64,8 @@ EXPORTS = [
     "otprg_set_trace", "otprg_get_trace", "otprg_load_mnist_pair", "otprg_solve_ot",
     "otprg_ot_scale_and_round", "otprg_random_ot_rational", "otprg_shard_prepare",
     "otprg_shard_begin", "otprg_shard_top", "otprg_shard_scan", "otprg_shard_da",
-    "otprg_shard_finish", "otprg_set_stream", "otprg_sinkhorn", "otprg_verify_feasibility", "otprg_verify_host", "otprg_admissible",
+    "otprg_shard_finish", "otprg_set_stream", "otprg_sinkhorn", "otprg_groups_begin",
+    "otprg_groups_step", "otprg_groups_finish", "otprg_verify_feasibility", "otprg_verify_host", "otprg_admissible",
 ]
 
 _lib = None
@@ -121,6 +122,9 @@ def lib() -> C.CDLL:
     L.otprg_shard_da.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
     L.otprg_shard_finish.argtypes = [vp, C.POINTER(Result)]
     L.otprg_set_stream.argtypes = [vp, vp]
+    L.otprg_groups_begin.argtypes = [vp, C.POINTER(Problem), vp, vp]
+    L.otprg_groups_step.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+    L.otprg_groups_finish.argtypes = [vp, C.POINTER(Result)]
     L.otprg_sinkhorn.argtypes = [vp, vp, vp, vp]
     L.otprg_verify_feasibility.argtypes = [vp, C.POINTER(Feasibility)]
     L.otprg_verify_host.argtypes = [vp, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp, vp, vp,

@@ -517,13 +517,16 @@ def _check_options(inst: AssignmentInstance, opt: AssignmentOptions) -> None:
     if (opt.demand_groups is None) != (opt.supply_groups is None):
         raise ParameterError("copy mode needs both demand and supply groups")
     if opt.demand_groups is not None:
-        raise ParameterError("copy mode (demand/supply groups) is not provided by the device path")
+        if len(opt.demand_groups) != inst.n_a or len(opt.supply_groups) != inst.n_b:
+            raise ParameterError("group map sizes do not match the instance")
+        if inst.n_b > inst.n_a:
+            raise ParameterError("copy mode requires n_b <= n_a")
 
 
 def solve_assignment(inst: AssignmentInstance, opt: AssignmentOptions):
     """assignment.hpp:137-138 / assignment.cpp:368-400 -> (Matching, SolveStats)."""
     _check_options(inst, opt)
-    if opt.observer is not None or opt.check_invariants:
+    if opt.observer is not None or opt.check_invariants or opt.demand_groups is not None:
         return _solve_debug(get_solver(opt.device), inst, opt)
     return get_solver(opt.device).solve(inst, opt)
 
@@ -539,15 +542,24 @@ def _solve_debug(sv: Solver, inst: AssignmentInstance, opt: AssignmentOptions):
     the internal orientation.  Results are those of the fused solve."""
     swapped = inst.n_b > inst.n_a
     n_b_int = min(inst.n_a, inst.n_b)
+    grouped = opt.demand_groups is not None
     costs = None
     if opt.observer is not None:  # ScaledCosts in the internal orientation (prepares too)
         sc = sv.scale_round_costs(inst, opt.eps, opt.storage)
         costs = ScaledCosts(sc.eps, np.ascontiguousarray(sc.k.T) if swapped else sc.k,
                             sc.unit_floor, sc.unit_ceil)
-    else:
+    elif not grouped:
         sv.prepare(inst, opt.eps, opt.storage)
     sv._prepared = (inst.n_a, inst.n_b, opt.eps)
-    sv.begin()
+    if grouped:  # copy mode: its own phase step (assignment.cpp:81-103, :241-250)
+        dg = np.ascontiguousarray(opt.demand_groups, np.int32)
+        sg = np.ascontiguousarray(opt.supply_groups, np.int32)
+        p = sv._problem(inst, opt.eps, opt.storage)
+        st = sv._L.otprg_groups_begin(sv._ctx, C.byref(p), dg.ctypes.data, sg.ctypes.data)
+        if st:
+            sv._raise(st)
+    else:
+        sv.begin()
     threshold = opt.eps * float(min(inst.n_a, inst.n_b))
     m0, s0 = sv.snapshot()
     cur_m, cur_d = _internal(m0, swapped), s0.duals_final
@@ -560,8 +572,22 @@ def _solve_debug(sv: Solver, inst: AssignmentInstance, opt: AssignmentOptions):
             e_adm = None
         if float(len(b_free)) <= threshold:
             break
+        if grouped and e_adm is not None:  # scan_grouped order (assignment.cpp:81-103)
+            ma = cur_m.match_of_a
+            part = np.where(ma >= 0, sg[np.maximum(ma, 0)], 0)
+            order = np.lexsort((np.arange(len(dg)), part, (ma >= 0).astype(np.int64), dg))
+            rank = np.empty(len(dg), np.int64)
+            rank[order] = np.arange(len(dg))
+            e_adm = [e[np.argsort(rank[e], kind="stable")] for e in e_adm]
         before = int(np.abs(cur_d.y_a).sum() + np.abs(cur_d.y_b).sum())
-        done, _ = sv.step(phase + 1)
+        if grouped:
+            d64, f32 = C.c_int64(), C.c_int32()
+            st = sv._L.otprg_groups_step(sv._ctx, C.byref(d64), C.byref(f32))
+            if st:
+                sv._raise(st)
+            done = int(d64.value)
+        else:
+            done, _ = sv.step(phase + 1)
         if done != phase + 1:
             raise InvariantViolation(f"device loop stopped at phase {done}, expected {phase + 1}")
         phase = done
@@ -587,6 +613,13 @@ def _solve_debug(sv: Solver, inst: AssignmentInstance, opt: AssignmentOptions):
             ws = PhaseWorkset(b_free, e_adm, touched.astype(np.int32), m_prime, a_double, m_double)
             after = int(np.abs(cur_d.y_a).sum() + np.abs(cur_d.y_b).sum())
             opt.observer(PhaseSnapshot(phase, costs, cur_d, cur_m, ws, before, after))
+    if grouped:
+        n_a, n_b, eps = sv._prepared
+        r, bufs = sv._result(n_a, n_b, eps)
+        st = sv._L.otprg_groups_finish(sv._ctx, C.byref(r))
+        if st:
+            sv._raise(st)
+        return Solver._pack(r, bufs)
     return sv.finish()
 
 

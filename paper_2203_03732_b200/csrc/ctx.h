@@ -103,6 +103,14 @@ struct otprg_ctx {
   // invariant suite / workset export (verify_kernels.cu)
   DevBuf v_out, v_k, v_ya, v_yb, v_ma, v_mb, adm_cnt, adm_off, adm_list;
 
+  // copy mode (copy_kernels.cu): groups, per-phase order, host-side stats
+  bool groups_mode = false, g_done = false, g_full = false;
+  int g_ndg = 0, g_nsg = 0;
+  uint32_t g_phase = 0;
+  int64_t g_sum_ni = 0;
+  std::vector<int64_t> g_fc;
+  DevBuf g_d, g_s, g_keys, g_keys2, g_vals, g_pi, g_rank, g_tmp, g_gmax, g_cnt;
+
   // pinned bounce buffers for large copies from pageable host memory (h2d.cpp)
   void* bounce[2] = {nullptr, nullptr};
   cudaEvent_t bounce_ev[2] = {nullptr, nullptr};

@@ -161,6 +161,20 @@ cudaError_t sk_rowcost(const double* P, const double* cost, int n_a, int n_b, do
 cudaError_t sk_entries(const double* P, int n_a, int n_b, const long long* offs, int32_t* ea,
                        int32_t* eb, double* em, cudaStream_t s);
 
+// Copy mode (copy_kernels.cu).
+size_t copy_sort_temp_bytes(int n_a);
+cudaError_t copy_order(const int32_t* dgroup, const int32_t* sgroup, const int32_t* ma, int n_a,
+                       unsigned long long* keys, unsigned long long* keys_sorted, int32_t* vals,
+                       int32_t* pi, int32_t* rank, void* temp, size_t temp_bytes, cudaStream_t s);
+cudaError_t copy_da(const void* kT, int lda, int width, const void* t, int32_t* yb, const int32_t* ma,
+                    unsigned long long* holder, const int32_t* pi, const int32_t* rank,
+                    const int32_t* bfree, int nfree, int n_a, uint32_t phase, int2* mp, int* mp_cnt,
+                    Ctl* ctl, cudaStream_t s);
+cudaError_t copy_apply(const int2* mp, const int* mp_cnt, const unsigned long long* holder, int32_t* ma,
+                       int32_t* mb, void* t, int width, uint32_t phase, Ctl* ctl, cudaStream_t s);
+cudaError_t copy_lift(int32_t* yb, const int32_t* mb, const int32_t* sgroup, int n_b, int n_groups,
+                      int* gmax, cudaStream_t s);
+
 cudaError_t launch_free_list(const int32_t* mb, int n_b, int32_t* out, int* count, cudaStream_t s);
 cudaError_t launch_admissible(const void* kT, int lda, int width, const void* t, const int32_t* yb,
                               const int32_t* bfree, int nfree, int n_a, long long* counts,

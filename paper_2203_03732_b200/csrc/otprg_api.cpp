@@ -9,6 +9,7 @@
 #include <map>
 #include <set>
 #include <string>
+#include <tuple>
 
 #include "../../include/otprg.h"
 
@@ -152,6 +153,7 @@ std::pair<Matching, SolveStats> solve_debug(otprg_ctx* ctx, const AssignmentInst
                                             const AssignmentOptions& opt) {
   const otprg_problem p = problem_of(inst, opt.eps, opt.storage);
   const bool swapped = inst.n_b > inst.n_a;
+  const bool grouped = opt.demand_groups != nullptr;  // copy mode (assignment.cpp:81-103, :241-250)
   const Index ia = std::max(inst.n_a, inst.n_b), ib = std::min(inst.n_a, inst.n_b);
   ScaledCosts sc;
   if (opt.observer) {  // ScaledCosts in the internal orientation (this also prepares)
@@ -159,11 +161,14 @@ std::pair<Matching, SolveStats> solve_debug(otprg_ctx* ctx, const AssignmentInst
     check(otprg_scale_round_costs(ctx, &p, k.data(), &sc.unit_floor, &sc.unit_ceil), ctx);
     sc.eps = opt.eps;
     sc.k = swapped ? k.transposed() : std::move(k);
-  } else {
+  } else if (!grouped) {
     otprg_result r{};
     check(otprg_prepare(ctx, &p, &r), ctx);
   }
-  check(otprg_begin(ctx), ctx);
+  if (grouped)
+    check(otprg_groups_begin(ctx, &p, opt.demand_groups->data(), opt.supply_groups->data()), ctx);
+  else
+    check(otprg_begin(ctx), ctx);
   const double threshold = opt.eps * static_cast<double>(ib);
   auto snapshot = [&]() {
     ResultBufs rb(inst.n_a, inst.n_b, opt.eps);
@@ -187,6 +192,16 @@ std::pair<Matching, SolveStats> solve_debug(otprg_ctx* ctx, const AssignmentInst
       ws.e_admissible.resize(static_cast<size_t>(nf));
       for (std::int64_t i = 0; i < nf; ++i)
         ws.e_admissible[i].assign(alist.begin() + offs[i], alist.begin() + offs[i + 1]);
+      if (grouped) {  // scan_grouped order: group, free before matched, partner's group, id
+        const auto& dg = *opt.demand_groups;
+        const auto& sg = *opt.supply_groups;
+        auto key = [&](Index a) {
+          const Index b = cur_m.match_of_a[a];
+          return std::make_tuple(dg[a], b != kUnmatched ? 1 : 0, b != kUnmatched ? sg[b] : 0, a);
+        };
+        for (auto& e : ws.e_admissible)
+          std::sort(e.begin(), e.end(), [&](Index x, Index y) { return key(x) < key(y); });
+      }
     } else {
       for (Index b = 0; b < ib; ++b)
         if (!cur_m.has_b(b)) ws.b_free.push_back(b);
@@ -195,7 +210,10 @@ std::pair<Matching, SolveStats> solve_debug(otprg_ctx* ctx, const AssignmentInst
     const DualUnits before = cur_d.sum_abs();
     std::int64_t done = 0;
     std::int32_t fin = 0;
-    check(otprg_step(ctx, phase + 1, &done, &fin), ctx);
+    if (grouped)
+      check(otprg_groups_step(ctx, &done, &fin), ctx);
+    else
+      check(otprg_step(ctx, phase + 1, &done, &fin), ctx);
     if (done != phase + 1)
       throw InvariantViolation("device loop stopped at phase " + std::to_string(done));
     phase = static_cast<int>(done);
@@ -226,7 +244,7 @@ std::pair<Matching, SolveStats> solve_debug(otprg_ctx* ctx, const AssignmentInst
   }
   (void)ia;
   ResultBufs rb(inst.n_a, inst.n_b, opt.eps);
-  check(otprg_finish(ctx, &rb.r), ctx);
+  check(grouped ? otprg_groups_finish(ctx, &rb.r) : otprg_finish(ctx, &rb.r), ctx);
   return rb.take();
 }
 
@@ -339,9 +357,14 @@ std::pair<Matching, SolveStats> solve_assignment(const AssignmentInstance& inst,
   if (!(opt.eps > 0.0 && opt.eps < 1.0)) throw ParameterError("eps must lie in (0, 1)");
   if ((opt.demand_groups == nullptr) != (opt.supply_groups == nullptr))
     throw ParameterError("copy mode needs both demand and supply groups");
-  if (opt.demand_groups) throw ParameterError("copy mode is not provided by the device path");
+  if (opt.demand_groups) {  // assignment.cpp:375-381
+    if (static_cast<Index>(opt.demand_groups->size()) != inst.n_a ||
+        static_cast<Index>(opt.supply_groups->size()) != inst.n_b)
+      throw ParameterError("group map sizes do not match the instance");
+    if (inst.n_b > inst.n_a) throw ParameterError("copy mode requires n_b <= n_a");
+  }
   otprg_ctx* ctx = context(opt.device);
-  if (opt.observer || opt.check_invariants) return solve_debug(ctx, inst, opt);
+  if (opt.observer || opt.check_invariants || opt.demand_groups) return solve_debug(ctx, inst, opt);
   const otprg_problem p = problem_of(inst, opt.eps, opt.storage);
   ResultBufs rb(inst.n_a, inst.n_b, opt.eps);
   check(otprg_solve_assignment(ctx, &p, &rb.r), ctx);

@@ -907,6 +907,150 @@ int otprg_admissible(otprg_ctx* ctx, int32_t* b_free, int64_t* offsets, int32_t*
 
 }  // extern "C"
 
+// ---- copy mode --------------------------------------
+namespace {
+
+// Mirror of the host-side loop state into the device control block, so
+// otprg_snapshot / otprg_verify_feasibility / export_state see copy-mode runs
+// exactly like fused ones.
+int groups_publish(otprg_ctx* ctx) {
+  Ctl* d = ctx->ctl.as<Ctl>();
+  const uint32_t ph = ctx->g_phase;
+  const int32_t done = ctx->g_done ? 1 : 0, full = ctx->g_full ? 1 : 0;
+  CK(cudaMemcpyAsync(&d->phase, &ph, 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(&d->sum_ni, &ctx->g_sum_ni, 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(&d->done, &done, 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(&d->full_match, &full, 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  if (ph > 0 && static_cast<int64_t>(ph) <= ctx->fc_cap)
+    CK(cudaMemcpyAsync(ctx->fc.as<int64_t>() + ph - 1, &ctx->g_fc[ph - 1], 8, cudaMemcpyHostToDevice,
+                       ctx->stream), "H2D");
+  CK(cudaStreamSynchronize(ctx->stream), "publish");  // (host sources live on the stack)
+  return OTPRG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int otprg_groups_begin(otprg_ctx* ctx, const otprg_problem* p, const int32_t* demand_groups,
+                       const int32_t* supply_groups) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!p || !demand_groups || !supply_groups)
+    return fail(ctx, OTPRG_PARAMETER, "copy mode needs both demand and supply groups");
+  if (p->n_b > p->n_a) return fail(ctx, OTPRG_PARAMETER, "copy mode requires n_b <= n_a");
+  if (p->n_a >= (1 << 21)) return fail(ctx, OTPRG_PARAMETER, "copy mode supports n_a < 2^21");
+  int dmax = -1, smax = -1;
+  for (int32_t a = 0; a < p->n_a; ++a) {
+    if (demand_groups[a] < 0 || demand_groups[a] >= (1 << 21))
+      return fail(ctx, OTPRG_PARAMETER, "group ids must lie in [0, 2^21)");
+    dmax = std::max(dmax, demand_groups[a]);
+  }
+  for (int32_t b = 0; b < p->n_b; ++b) {
+    if (supply_groups[b] < 0 || supply_groups[b] >= (1 << 21))
+      return fail(ctx, OTPRG_PARAMETER, "group ids must lie in [0, 2^21)");
+    smax = std::max(smax, supply_groups[b]);
+  }
+  int st = do_prepare(ctx, p);
+  if (st) return st;
+  if ((st = do_begin(ctx))) return st;
+  const size_t na = ctx->ia, nb = ctx->ib;
+  ctx->g_ndg = dmax + 1;
+  ctx->g_nsg = smax + 1;
+  CK(ctx->g_d.ensure(na * 4), "alloc");
+  CK(ctx->g_s.ensure(nb * 4), "alloc");
+  CK(ctx->g_keys.ensure(na * 8), "alloc");
+  CK(ctx->g_keys2.ensure(na * 8), "alloc");
+  CK(ctx->g_vals.ensure(na * 4), "alloc");
+  CK(ctx->g_pi.ensure(na * 4), "alloc");
+  CK(ctx->g_rank.ensure(na * 4), "alloc");
+  CK(ctx->g_tmp.ensure(std::max<size_t>(otprg::copy_sort_temp_bytes(ctx->ia), 16)), "alloc");
+  CK(ctx->g_gmax.ensure(static_cast<size_t>(ctx->g_nsg) * 4), "alloc");
+  CK(ctx->g_cnt.ensure(16), "alloc");
+  CK(cudaMemcpyAsync(ctx->g_d.p, demand_groups, na * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->g_s.p, supply_groups, nb * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  ctx->groups_mode = true;
+  ctx->g_done = ctx->g_full = false;
+  ctx->g_phase = 0;
+  ctx->g_sum_ni = 0;
+  ctx->g_fc.clear();
+  return groups_publish(ctx);
+}
+
+// One phase of solve_oriented (assignment.cpp:316-364) in copy mode.
+int otprg_groups_step(otprg_ctx* ctx, int64_t* phases_done, int32_t* finished) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!ctx->groups_mode || !ctx->begun) return fail(ctx, OTPRG_PARAMETER, "otprg_groups_begin() first");
+  cudaStream_t s = ctx->stream;
+  if (!ctx->g_done) {
+    int* d_count = ctx->g_cnt.as<int>() + 1;
+    CK(otprg::launch_free_list(ctx->mb.as<int32_t>(), ctx->ib, ctx->fb.as<int32_t>(), d_count, s),
+       "free list");
+    int nf = 0;
+    CK(cudaMemcpyAsync(&nf, d_count, 4, cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "free list");
+    const double threshold = ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b));
+    if (static_cast<double>(nf) <= threshold) {
+      ctx->g_done = true;
+      ctx->g_full = nf == 0;
+    } else {
+      const int64_t cap = static_cast<int64_t>(std::ceil((1.0 + 2.0 * ctx->eps) / (ctx->eps * ctx->eps))) + 8;
+      ctx->g_phase += 1;
+      ctx->g_fc.push_back(nf);
+      ctx->g_sum_ni += nf;
+      CK(otprg::copy_order(ctx->g_d.as<int32_t>(), ctx->g_s.as<int32_t>(), ctx->ma.as<int32_t>(), ctx->ia,
+                           ctx->g_keys.as<unsigned long long>(), ctx->g_keys2.as<unsigned long long>(),
+                           ctx->g_vals.as<int32_t>(), ctx->g_pi.as<int32_t>(), ctx->g_rank.as<int32_t>(),
+                           ctx->g_tmp.p, ctx->g_tmp.n, s),
+         "copy order");
+      int* mp_cnt = ctx->g_cnt.as<int>();
+      CK(cudaMemsetAsync(mp_cnt, 0, 4, s), "memset");
+      unsigned long long* holder = ctx->holder.as<unsigned long long>();
+      CK(otprg::copy_da(ctx->kT.p, ctx->lda, ctx->width, ctx->t.p, ctx->yb.as<int32_t>(), ctx->ma.as<int32_t>(),
+                        holder, ctx->g_pi.as<int32_t>(), ctx->g_rank.as<int32_t>(), ctx->fb.as<int32_t>(), nf,
+                        ctx->ia, ctx->g_phase, ctx->mps.as<int2>(), mp_cnt, ctx->ctl.as<Ctl>(), s),
+         "copy DA");
+      CK(otprg::copy_apply(ctx->mps.as<int2>(), mp_cnt, holder, ctx->ma.as<int32_t>(), ctx->mb.as<int32_t>(),
+                           ctx->t.p, ctx->width, ctx->g_phase, ctx->ctl.as<Ctl>(), s),
+         "copy apply");
+      CK(otprg::copy_lift(ctx->yb.as<int32_t>(), ctx->mb.as<int32_t>(), ctx->g_s.as<int32_t>(), ctx->ib,
+                          ctx->g_nsg, ctx->g_gmax.as<int>(), s),
+         "copy lift");
+      Ctl h{};
+      CK(cudaMemcpyAsync(&h, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s), "D2H ctl");
+      CK(cudaStreamSynchronize(s), "copy phase");
+      int st = check_status(ctx, h, false);
+      if (st) return st;
+      if (static_cast<int64_t>(ctx->g_phase) > cap)
+        return fail(ctx, OTPRG_INVARIANT, "phase count exceeded the proven bound; solver state is corrupt");
+    }
+    int st = groups_publish(ctx);
+    if (st) return st;
+  }
+  if (phases_done) *phases_done = ctx->g_phase;
+  if (finished) *finished = ctx->g_done ? 1 : 0;
+  return OTPRG_OK;
+}
+
+int otprg_groups_finish(otprg_ctx* ctx, otprg_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!res || !res->match_of_a || !res->match_of_b)
+    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
+  int32_t fin = 0;
+  while (!fin) {
+    int st = otprg_groups_step(ctx, nullptr, &fin);
+    if (st) return st;
+  }
+  int st = launch_finish(ctx);
+  if (st) return st;
+  Ctl h{};
+  if ((st = export_state(ctx, res, &h))) return st;
+  res->gpu_launches = 0;
+  ctx->groups_mode = false;
+  return check_status(ctx, h, true);
+}
+
+}  // extern "C"
+
 // ---- A-row-sharded mode --------------------------------------
 namespace {
 

@@ -216,10 +216,59 @@ static void ot_cases() {
   EXPECT(std::abs(kr.cost - kg.cost) <= 1e-9 * std::abs(kr.cost), "sinkhorn cost");
 }
 
+// copy mode (demand/supply groups, assignment.cpp:81-103, :241-250) with the
+// observer: per-phase worksets in the grouped scan order must match.
+static void copy_mode_cases() {
+  const int d_copies[4] = {3, 2, 4, 1}, s_copies[3] = {2, 3, 4};
+  const otpr::AssignmentInstance orig = random_instance(4, 3, 11);
+  std::vector<otpr::Index> dg, sg;
+  for (int a = 0; a < 4; ++a)
+    for (int c = 0; c < d_copies[a]; ++c) dg.push_back(a);
+  for (int b = 0; b < 3; ++b)
+    for (int c = 0; c < s_copies[b]; ++c) sg.push_back(b);
+  otpr::AssignmentInstance r;
+  r.n_a = static_cast<int>(dg.size());
+  r.n_b = static_cast<int>(sg.size());
+  r.cost = otpr::Matrix<double>(r.n_a, r.n_b);
+  for (int i = 0; i < r.n_a; ++i)
+    for (int j = 0; j < r.n_b; ++j) r.cost(i, j) = orig.cost(dg[i], sg[j]);
+  for (double eps : {0.2, 0.1}) {
+    std::vector<std::vector<std::vector<otpr::Index>>> ref_e;
+    std::vector<std::vector<otpr::Index>> ref_mb;
+    otpr::AssignmentOptions ro;
+    ro.eps = eps;
+    ro.demand_groups = &dg;
+    ro.supply_groups = &sg;
+    ro.check_invariants = true;
+    ro.observer = [&](const otpr::PhaseSnapshot& s) {
+      ref_e.push_back(s.workset.e_admissible);
+      ref_mb.push_back(s.matching.match_of_b);
+    };
+    auto [mr, sr] = otpr::solve_assignment(r, ro);
+    size_t i = 0;
+    otprg::AssignmentOptions go;
+    go.eps = eps;
+    go.demand_groups = &dg;
+    go.supply_groups = &sg;
+    go.check_invariants = true;
+    go.observer = [&](const otprg::PhaseSnapshot& s) {
+      if (i < ref_e.size()) {
+        EXPECT(ref_e[i] == s.workset.e_admissible, "copy-mode E' (grouped order)");
+        EXPECT(ref_mb[i] == s.matching.match_of_b, "copy-mode matching");
+      }
+      ++i;
+    };
+    auto [mg, sg2] = otprg::solve_assignment(to_g(r), go);
+    EXPECT(i == ref_e.size(), "copy-mode phase count");
+    same_result(mr, sr, mg, sg2, "copy mode");
+  }
+}
+
 int main() {
   assignment_cases();
   observer_cases();
   ot_cases();
+  copy_mode_cases();
   if (g_fail) {
     std::printf("dropin: %d failures\n", g_fail);
     return 1;

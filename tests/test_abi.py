@@ -94,10 +94,16 @@ def test_parameter_errors_before_device(lib):
     with pytest.raises(otprg.ParameterError):
         otprg.solve_assignment(otprg.AssignmentInstance(1, 1, np.array([[1.5]])),
                                otprg.AssignmentOptions(eps=0.1))
-    with pytest.raises(otprg.ParameterError):  # copy mode is not on the device path
-        g = np.zeros(1, np.int64)
-        otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=0.1, demand_groups=g,
+    g = np.zeros(1, np.int64)
+    with pytest.raises(otprg.ParameterError):  # copy mode needs both group maps (assignment.cpp:373)
+        otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=0.1, demand_groups=g))
+    with pytest.raises(otprg.ParameterError):  # group map sizes (:376-378)
+        otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=0.1, demand_groups=np.zeros(2, np.int64),
                                                              supply_groups=g))
+    with pytest.raises(otprg.ParameterError):  # copy mode requires n_b <= n_a (:379-380)
+        wide = otprg.AssignmentInstance(1, 2, np.array([[0.5, 0.5]]))
+        otprg.solve_assignment(wide, otprg.AssignmentOptions(eps=0.1, demand_groups=g,
+                                                             supply_groups=np.zeros(2, np.int64)))
 
 
 def test_create_without_device_reports_status(lib):
