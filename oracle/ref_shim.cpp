@@ -17,6 +17,7 @@
 #include "otpr/core.hpp"
 #include "otpr/errors.hpp"
 #include "otpr/instances.hpp"
+#include "otpr/oracles.hpp"
 #include "otpr/ot.hpp"
 #include "otpr/sinkhorn.hpp"
 
@@ -416,6 +417,24 @@ int ref_solve_assignment_groups(int32_t n_a, int32_t n_b, const double* cost, do
     out->cost = otpr::matching_cost(m, inst);
     out->round_ms = 0.0;
     export_result(m, s, match_of_a, match_of_b, y_a, y_b, free_counts, free_cap, out);
+  });
+}
+
+// The reference's exact oracles (oracles.hpp:18-37), used by the acceptance
+// checks as the optimum to bound against (test infrastructure only).
+int ref_hungarian_exact(int32_t n_a, int32_t n_b, const double* cost, double* opt_cost) {
+  return guarded([&] { *opt_cost = otpr::hungarian_exact(wrap(n_a, n_b, cost), 4096).second; });
+}
+
+int ref_exact_ot(int32_t n_a, int32_t n_b, const double* mu, const double* nu, const double* cost,
+                 double* opt_cost) {
+  return guarded([&] {
+    otpr::OTInstance inst;
+    inst.mu.assign(mu, mu + n_a);
+    inst.nu.assign(nu, nu + n_b);
+    inst.cost = otpr::Matrix<double>(n_a, n_b);
+    std::memcpy(inst.cost.data(), cost, sizeof(double) * size_t(n_a) * n_b);
+    *opt_cost = otpr::exact_ot(inst, 256).second;
   });
 }
 

@@ -1,0 +1,125 @@
+"""The reference's acceptance criteria (tests/acceptance.cpp) on the device
+path, with the reference's own exact oracles (oracles.hpp: hungarian_exact,
+exact_ot via oracle/_ref) as the optimum:
+
+  1  assignment additive error <= 3 eps n           (acceptance.cpp:190-225)
+  2  unbalanced additive error <= 3 eps |B|          (:227-250)
+  3  transport cost <= optimal + eps, complete plans (:252-291)
+  4  per-phase invariant suite over 1-3              (device verify + observer)
+  5  phase and free-count bounds                     (:213-224)
+ 10  sequential runs bit-for-bit deterministic       (:451-479)
+(Criterion 9 is a CPU-scaling statement about the reference itself.)  Seed
+ranges are thinned from 30 to keep the GPU suite short."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+otprg = pytest.importorskip("paper_2203_03732_b200")
+
+
+@pytest.fixture(scope="module")
+def oracles(reference):
+    L = reference.lib
+    L.ref_hungarian_exact.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_double)]
+    L.ref_exact_ot.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.POINTER(C.c_double)]
+
+    def hungarian(cost):
+        cost = np.ascontiguousarray(cost)
+        out = C.c_double()
+        assert L.ref_hungarian_exact(*cost.shape, cost.ctypes.data, C.byref(out)) == 0
+        return out.value
+
+    def exact_ot(mu, nu, cost):
+        cost = np.ascontiguousarray(cost)
+        out = C.c_double()
+        assert L.ref_exact_ot(len(mu), len(nu), np.ascontiguousarray(mu).ctypes.data,
+                              np.ascontiguousarray(nu).ctypes.data, cost.ctypes.data, C.byref(out)) == 0
+        return out.value
+
+    return hungarian, exact_ot
+
+
+class _Obs:
+    """verified_options (acceptance.cpp:74-124): signs, free-demand zero,
+    magnitude bound, feasibility (device), monotone matched set, dual
+    progress, greedy maximality."""
+
+    def __init__(self):
+        self.prev, self.checks = 0, 0
+
+    def __call__(self, snap):
+        bound = snap.costs.unit_ceil + 2
+        ya, yb = snap.duals.y_a, snap.duals.y_b
+        assert (ya <= 0).all() and (yb >= 0).all()
+        assert (ya[snap.matching.match_of_a == -1] == 0).all()
+        assert (np.abs(ya) <= bound).all() and (np.abs(yb) <= bound).all()
+        assert snap.matching.size() >= self.prev
+        self.prev = snap.matching.size()
+        assert snap.sum_abs_after - snap.sum_abs_before >= len(snap.workset.b_free)
+        prime_a = {a for a, _ in snap.workset.m_prime}
+        prime_b = {b for _, b in snap.workset.m_prime}
+        for i, b in enumerate(snap.workset.b_free):
+            if int(b) not in prime_b:
+                assert all(int(a) in prime_a for a in snap.workset.e_admissible[i])
+        self.checks += 1
+
+
+def test_criteria_1_4_5(oracles):
+    hungarian, _ = oracles
+    for n in (50, 100, 200):
+        for seed in range(1, 31, 6):
+            inst = otprg.gen_uniform_square(n, seed, dense=True)
+            opt_cost = hungarian(inst.cost)
+            for eps in (0.2, 0.1, 0.05):
+                obs = _Obs()
+                m, s = otprg.solve_assignment(inst, otprg.AssignmentOptions(
+                    eps=eps, check_invariants=True, observer=obs))
+                assert otprg.matching_cost(m, inst) <= opt_cost + 3.0 * eps * n  # criterion 1
+                assert s.phases <= s.phase_bound(eps)                              # criterion 5
+                assert s.sum_ni <= s.sum_ni_bound(eps, n)
+                assert obs.checks == s.phases                                       # criterion 4
+
+
+def test_criterion_2_unbalanced(oracles):
+    hungarian, _ = oracles
+    for n_b in (50, 100):
+        for seed in range(1, 31, 6):
+            full = otprg.gen_uniform_square(2 * n_b, seed, dense=True)
+            cost = np.ascontiguousarray(full.cost[:, :n_b])
+            inst = otprg.AssignmentInstance(2 * n_b, n_b, cost)
+            opt_cost = hungarian(cost)
+            for eps in (0.2, 0.1, 0.05):
+                m, s = otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=eps, check_invariants=True))
+                assert m.size() == n_b
+                assert otprg.matching_cost(m, inst) <= opt_cost + 3.0 * eps * n_b
+
+
+def test_criterion_3_transport(oracles):
+    _, exact_ot = oracles
+    for n in (5, 10, 20):
+        for seed in range(1, 31, 5):
+            inst = otprg.gen_random_ot_rational(n, n, seed * 1009 + n)
+            opt_cost = exact_ot(inst.mu, inst.nu, inst.cost)
+            for eps in (0.25, 0.1):
+                plan, s = otprg.solve_ot(inst, eps)
+                assert plan.cost <= opt_cost + eps
+                assert np.abs(plan.col_sums(n) - inst.nu).max() <= 1e-12   # complete plans
+
+
+def test_criterion_10_determinism():
+    inst = otprg.gen_uniform_square(200, 31337, dense=True)
+    opt = otprg.AssignmentOptions(eps=0.1)
+    m1, s1 = otprg.solve_assignment(inst, opt)
+    m2, s2 = otprg.solve_assignment(inst, opt)
+    assert np.array_equal(m1.match_of_a, m2.match_of_a) and np.array_equal(m1.match_of_b, m2.match_of_b)
+    assert np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a)
+    assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b)
+    assert s1.phases == s2.phases and np.array_equal(s1.free_counts, s2.free_counts)
+    from paper_2203_03732_b200.bench_cli import SolveRequest, format_double, run_solver
+    r1 = run_solver(inst, SolveRequest("pushrelabel", eps=0.1)).record
+    r2 = run_solver(inst, SolveRequest("pushrelabel", eps=0.1)).record
+    assert format_double(r1.cost) == format_double(r2.cost)
