@@ -113,7 +113,7 @@ class TorchDistExchange:
         for t in tensors:
             slot = t.numel() // self.world
             mine = t.narrow(0, self.rank * slot, slot).clone()
-            if t.is_cuda:
+            if t.is_cuda and dist.get_backend() == "nccl":
                 dist.all_gather_into_tensor(t, mine)
             else:  # gloo (CPU tests of the protocol)
                 dist.all_gather(list(t.split(slot)), mine)
@@ -166,7 +166,8 @@ class ShardedSolver:
         if distributed:
             import torch.distributed as dist
             rank, world = dist.get_rank(), dist.get_world_size()
-            device = int(os.environ.get("LOCAL_RANK", opt.device))
+            # this rank's GPU: OTPRG_DEVICE, else LOCAL_RANK (one process per GPU)
+            device = int(os.environ.get("OTPRG_DEVICE", os.environ.get("LOCAL_RANK", opt.device)))
             self.ranks = [DeviceRank(device)]
             self.ranks[0].prepare(inst, opt.eps, world, rank, K, opt.storage)
             self.n_shards = world

@@ -109,3 +109,23 @@ def test_distributed_world1_nccl(golden):
         _check_golden(golden, key, m, st)
     finally:
         dist.destroy_process_group()
+
+
+def test_two_processes_one_gpu_gloo():
+    """The multi-process protocol end to end on real kernels: two
+    torch.distributed ranks (gloo exchange, both contexts on cuda:0) — golden
+    pins and bit-identity with the fused solver at n = 100k
+    (scripts/dist_on_one_gpu.py)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, OTPRG_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        "scripts/dist_on_one_gpu.py"], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and "DIST OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
