@@ -112,6 +112,15 @@ SupplyC& supply_at(std::vector<SupplyC>& cs, int64_t y) {
 
 // Merge equal duals, drop empty clusters, descending dual order (ot.cpp:362-383).
 void normalize_demand(std::vector<DemandC>& cs, int32_t a) {
+  // fast paths (most vertices, every phase): nothing to merge
+  if (cs.size() == 1) {
+    if (cs[0].count() == 0) cs.clear();
+    return;
+  }
+  if (cs.size() == 2 && cs[0].y != cs[1].y && cs[0].count() > 0 && cs[1].count() > 0) {
+    if (cs[0].y < cs[1].y) std::swap(cs[0], cs[1]);
+    return;
+  }
   std::sort(cs.begin(), cs.end(), [](const DemandC& x, const DemandC& y) { return x.y > y.y; });
   std::vector<DemandC> out;
   for (DemandC& c : cs) {
@@ -130,6 +139,10 @@ void normalize_demand(std::vector<DemandC>& cs, int32_t a) {
 
 // Lift free copies to the vertex maximum, merge, drop empty (ot.cpp:385-414).
 void normalize_supply(std::vector<SupplyC>& cs, int32_t b) {
+  if (cs.size() == 1) {  // fast path: free copies already sit at the only dual
+    if (cs[0].count() == 0) cs.clear();
+    return;
+  }
   int64_t max_y = std::numeric_limits<int64_t>::min(), total_free = 0;
   for (const SupplyC& c : cs) {
     if (c.count() == 0) continue;
