@@ -65,11 +65,6 @@ constexpr int kUnroll = 4;       // 128-bit loads in flight per lane (global t)
 #define OTPRG_UNROLL_SMEM 8
 #endif
 constexpr int kUnrollSmem = OTPRG_UNROLL_SMEM;  // (t in shared memory)
-#ifdef OTPRG_DEBUG_SCAN
-constexpr unsigned kDebugBarriers = 1;
-#else
-constexpr unsigned kDebugBarriers = 0;
-#endif
 
 __device__ __forceinline__ uint4 ldg_nc(const uint4* p) { return __ldg(p); }
 
@@ -491,15 +486,6 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gthreads = gridDim.x * blockDim.x;
 
-  if (phase == 0) {
-    // Touch every 2 MB page of kT once before the first full-width scan so
-    // the address translations are resident; a cold TLB otherwise serialises
-    // thousands of concurrent row scans on page walks.
-    const size_t bytes = (size_t)ctl->n_b * lda * sizeof(T);
-    const char* base = static_cast<const char*>(A.kT);
-    for (size_t off = (size_t)gtid << 21; off < bytes; off += (size_t)gthreads << 21)
-      (void)__ldcg(reinterpret_cast<const unsigned*>(base + off));
-  }
   if constexpr (kSmem) {  // global t is complete at launch (previous launch applied its M')
     const uint4* src = reinterpret_cast<const uint4*>(tg);
     uint4* dst = reinterpret_cast<uint4*>(s_t);
