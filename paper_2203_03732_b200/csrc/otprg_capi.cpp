@@ -1245,7 +1245,9 @@ int otprg_shard_scan(otprg_ctx* ctx, int32_t* cand, int32_t* meta_words, int32_t
                      int32_t refill) {
   int2* meta = reinterpret_cast<int2*>(meta_words);
   if (!ctx) return OTPRG_PARAMETER;
-  if (cap < ctx->sh_n || cap < ctx->sh_cap) return fail(ctx, OTPRG_PARAMETER, "exchange buffer too small");
+  // cap = slots per rank in the exchange buffers: >= the phase's proposers
+  // (the driver passes n_i so the all-gather moves only the used prefix)
+  if (cap < ctx->sh_n || cap > ctx->sh_cap) return fail(ctx, OTPRG_PARAMETER, "bad exchange slot count");
   otprg::ShardArgs S = shard_args(ctx);
   S.cap = cap;
   const int4* req = refill ? ctx->sh_park[ctx->sh_park_cur].as<int4>() : nullptr;

@@ -97,34 +97,38 @@ def _buffers(n_shards: int, cap: int, K: int, device: int):
 class LocalExchange:
     """All ranks in this process write their slots into one shared buffer."""
 
-    def gather(self, *tensors):
+    def gather(self, n, *args):
         return None
 
 
 class TorchDistExchange:
-    """One process per GPU: all_gather of the rank slots (NCCL over NVLink)."""
+    """One process per GPU: all_gather of the rank slots (NCCL over NVLink).
+    Only the used prefix moves: with n proposers in the phase the kernels
+    index the buffers as [world][n][K] / [world][n][2]."""
 
     def __init__(self, rank: int, world: int):
         self.rank, self.world = rank, world
 
-    def gather(self, *tensors):
-        import torch
+    def gather(self, n, cand=None, meta=None, K=0):
         import torch.distributed as dist
-        for t in tensors:
-            slot = t.numel() // self.world
-            mine = t.narrow(0, self.rank * slot, slot).clone()
+        for t, per in ((cand, n * K), (meta, n * 2)):
+            if t is None:
+                continue
+            view = t.narrow(0, 0, self.world * per)
+            mine = view.narrow(0, self.rank * per, per).clone()
             if t.is_cuda and dist.get_backend() == "nccl":
-                dist.all_gather_into_tensor(t, mine)
-            else:  # gloo (CPU tests of the protocol)
-                dist.all_gather(list(t.split(slot)), mine)
+                dist.all_gather_into_tensor(view, mine)
+            else:  # gloo (CPU tests of the protocol; one-GPU multi-process checks)
+                dist.all_gather(list(view.split(per)), mine)
         # (CUDA: the collective is ordered on the current stream, which the
         # contexts share — otprg_set_stream — so the DA launch follows it
         # without a host sync)
 
 
-def run_phases(ranks, exchange, cand_ptr: int, meta_ptr: int, cap: int, gather_args=()):
+def run_phases(ranks, exchange, cand_ptr, meta_ptr, cap: int, gather_args=()):
     """The per-phase protocol over the ranks this process drives (one rank per
-    process with TorchDistExchange; every rank with LocalExchange)."""
+    process with TorchDistExchange; every rank with LocalExchange).  The
+    exchange buffers hold `cap` slots per rank; each phase uses n of them."""
     for r in ranks:
         r.begin()
     rounds = 0
@@ -135,18 +139,19 @@ def run_phases(ranks, exchange, cand_ptr: int, meta_ptr: int, cap: int, gather_a
             raise RuntimeError(f"ranks disagree at the phase top: {tops}")
         if finished:
             break
+        assert n <= cap
         for r in ranks:
-            r.scan(cand_ptr, meta_ptr, cap, False)
-        exchange.gather(*gather_args)
-        parked = [r.da(cand_ptr, meta_ptr, cap, False) for r in ranks]
+            r.scan(cand_ptr, meta_ptr, n, False)
+        exchange.gather(n, *gather_args)
+        parked = [r.da(cand_ptr, meta_ptr, n, False) for r in ranks]
         while parked[0] > 0:
             rounds += 1
             if any(p != parked[0] for p in parked):
                 raise RuntimeError(f"ranks disagree on parked chains: {parked}")
             for r in ranks:
-                r.scan(cand_ptr, meta_ptr, cap, True)
-            exchange.gather(*gather_args)
-            parked = [r.da(cand_ptr, meta_ptr, cap, True) for r in ranks]
+                r.scan(cand_ptr, meta_ptr, n, True)
+            exchange.gather(n, *gather_args)
+            parked = [r.da(cand_ptr, meta_ptr, n, True) for r in ranks]
     return rounds
 
 
@@ -181,7 +186,7 @@ class ShardedSolver:
             self.exchange = LocalExchange()
         self.cap = self.ranks[0].cap
         self.cand, self.meta = _buffers(self.n_shards, self.cap, K, device)
-        self.gather_args = (self.cand, self.meta) if distributed else ()
+        self.gather_args = (self.cand, self.meta, K) if distributed else ()
         # one stream for every context of this process and the exchange:
         # scan -> all-gather -> DA are ordered on it without host syncs
         import torch

@@ -86,7 +86,7 @@ def _worker(rank, world, port, kT, eps, K, align, q):
         cand = torch.full((world * cap * K,), -1, dtype=torch.int32)
         meta = torch.zeros((world * cap * 2,), dtype=torch.int32)
         rounds = run_phases([r], TorchDistExchange(rank, world), cand.numpy(), meta.numpy(), cap,
-                            (cand, meta))
+                            (cand, meta, K))
         out = r.finish()
         q.put((rank, rounds, {k: np.asarray(v) for k, v in out.items()}))
     finally:
