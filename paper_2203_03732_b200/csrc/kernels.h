@@ -90,6 +90,7 @@ struct ShardArgs {
   int4* park_out;          // parked chains (list index, b, restart)
   int64_t* free_counts;
   Ctl* ctl;
+  int* scratch;            // [>= 148] compaction block counts
 };
 // cond: skip (both kernels) when the DA just before parked chains
 // (ctl->work[1] != 0), i.e. the phase is not complete yet.

@@ -1080,6 +1080,7 @@ otprg::ShardArgs shard_args(otprg_ctx* ctx) {
   S.park_out = ctx->sh_park[ctx->sh_park_cur ^ 1].as<int4>();
   S.free_counts = ctx->fc.as<int64_t>();
   S.ctl = ctx->ctl.as<Ctl>();
+  S.scratch = ctx->fa.as<int>();  // (completion scratch, free during the phases)
   return S;
 }
 

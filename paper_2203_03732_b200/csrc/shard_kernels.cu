@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4
                                                          int2* __restrict__ meta) {
   using SD = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
-  constexpr int kU = 4;
+  constexpr int kU = 8;  // 4 KB per warp step (long rows: n = 100k rows are 200 KB)
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= nreq) return;
@@ -179,31 +179,63 @@ __global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t p
 }
 
 // The free list of the coming phase, ascending b (identical on every rank,
-// so list indices name the same b everywhere), and its inverse.  One block.
-__global__ void __launch_bounds__(1024) shard_compact_kernel(ShardArgs S, int cond) {
-  __shared__ int s_scan[1024];
+// so list indices name the same b everywhere), and its inverse.  Two passes
+// over kCompactBlocks contiguous ranges: per-range counts, then ordered writes
+// at the range's offset (block-wide scans per 1024-entry tile).
+constexpr int kCompactBlocks = 148;
+
+__global__ void __launch_bounds__(1024) shard_compact_count_kernel(ShardArgs S, int cond, int* counts) {
   if (S.ctl->done || (cond && S.ctl->work[1] != 0)) return;
-  const int n_b = S.ctl->n_b, tid = threadIdx.x, nt = blockDim.x;
-  int32_t* out = const_cast<int32_t*>(S.list_in);
-  const int chunk = (n_b + nt - 1) / nt;
-  const int lo = min(n_b, tid * chunk), hi = min(n_b, lo + chunk);
+  const int n_b = S.ctl->n_b;
+  const int chunk = (n_b + gridDim.x - 1) / gridDim.x;
+  const int lo = min(n_b, (int)blockIdx.x * chunk), hi = min(n_b, lo + chunk);
   int c = 0;
-  for (int q = lo; q < hi; ++q) c += (S.match_b[q] == -1);
-  s_scan[tid] = c;
+  for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) c += (S.match_b[q] == -1);
+  __shared__ int s_sum;
+  if (threadIdx.x == 0) s_sum = 0;
   __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    const int v = tid >= off ? s_scan[tid - off] : 0;
-    __syncthreads();
-    s_scan[tid] += v;
-    __syncthreads();
+  c = __reduce_add_sync(kFull, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_sum, c);
+  __syncthreads();
+  if (threadIdx.x == 0) counts[blockIdx.x] = s_sum;
+}
+
+__global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, int cond,
+                                                                   const int* counts) {
+  if (S.ctl->done || (cond && S.ctl->work[1] != 0)) return;
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int n_b = S.ctl->n_b;
+  const int chunk = (n_b + gridDim.x - 1) / gridDim.x;
+  const int lo = min(n_b, (int)blockIdx.x * chunk), hi = min(n_b, lo + chunk);
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int g = 0; g < (int)blockIdx.x; ++g) off += counts[g];
+    s_base = off;
   }
-  int pos = s_scan[tid] - c;
-  for (int q = lo; q < hi; ++q)
-    if (S.match_b[q] == -1) {
+  __syncthreads();
+  int32_t* out = const_cast<int32_t*>(S.list_in);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int t0 = lo; t0 < hi; t0 += blockDim.x) {  // one tile: block-wide ordered scan of the flags
+    const int q = t0 + threadIdx.x;
+    const bool f = q < hi && S.match_b[q] == -1;
+    const unsigned bal = __ballot_sync(kFull, f);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      if (w < warp) before += s_warp[w];
+      total += s_warp[w];
+    }
+    if (f) {
+      const int pos = s_base + before + __popc(bal & ((1u << lane) - 1u));
       out[pos] = q;
       S.pos_of_b[q] = pos;
-      ++pos;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
 }
 
 // Deferred acceptance over merged candidate lists, one warp per chain.
@@ -298,7 +330,8 @@ cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply
 }
 
 cudaError_t launch_shard_compact(const ShardArgs& a, bool cond, cudaStream_t s) {
-  shard_compact_kernel<<<1, 1024, 0, s>>>(a, cond ? 1 : 0);
+  shard_compact_count_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, cond ? 1 : 0, a.scratch);
+  shard_compact_write_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, cond ? 1 : 0, a.scratch);
   return cudaGetLastError();
 }
 
