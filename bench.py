@@ -364,7 +364,9 @@ def run_sharded(args, world, rank, local, steps: int, warmup: int) -> dict:
         "phases": P, "sum_ni": int(s.sum_ni), "refill_rounds": R, "K": args.K,
         "slab_build_ms": round(float(s.device["build_ms"]), 3),
         "prepare_wall_s": round(prep_s, 3),
-        "gpu_launches_per_step": 4 + 4 * (P + R),
+        # init + first top (top, 2 compaction passes) + per DA round (scan, DA, top,
+        # 2 compaction passes) + completion
+        "gpu_launches_per_step": 5 + 5 * (P + R),
         "clocks": clk.summary(),
     }
     sv.close()
