@@ -64,8 +64,15 @@ enum otprg_cost_kind {
   OTPRG_COST_L1_U8 = 2
 };
 
-/* Storage width of the rounded cost matrix on the device. */
-enum otprg_storage { OTPRG_STORAGE_AUTO = 0, OTPRG_STORAGE_U8 = 1, OTPRG_STORAGE_U16 = 2 };
+/* Storage width of the rounded cost matrix on the device.  AUTO: uint16 when
+ * ceil(1/eps) + 2 <= 65533, else uint32 (eps down to the reference's own
+ * limit, unit_floor + 4 <= INT32_MAX, core.cpp:36-41). */
+enum otprg_storage {
+  OTPRG_STORAGE_AUTO = 0,
+  OTPRG_STORAGE_U8 = 1,
+  OTPRG_STORAGE_U16 = 2,
+  OTPRG_STORAGE_U32 = 3
+};
 
 typedef struct otprg_problem {
   int32_t n_a; /* demand side A (rows)   */
@@ -86,6 +93,11 @@ typedef struct otprg_problem {
  * core.hpp:117-138).  Duals are reported like SolveStats::duals_final: in
  * the solver's internal orientation (swapped when n_b > n_a), before the
  * completion step. */
+/* The device keeps free_counts for at most this many phases; a solve that
+ * reaches it (only possible for eps below ~2.4e-4, where the reference's own
+ * phase cap ceil((1+2eps)/eps^2)+8 is larger) stops with OTPRG_INVARIANT. */
+#define OTPRG_MAX_PHASES (1 << 24)
+
 typedef struct otprg_result {
   int32_t* match_of_a;   /* n_a entries, -1 = unmatched (kUnmatched) */
   int32_t* match_of_b;   /* n_b entries */

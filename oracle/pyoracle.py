@@ -214,7 +214,7 @@ class Oracle:
     # -- solver --
     def _outs(self, n_a, n_b, eps):
         ia, ib = max(n_a, n_b), min(n_a, n_b)
-        cap = phase_cap(eps) + 1
+        cap = min(phase_cap(eps) + 1, 1 << 22)  # free_counts kept for the first 4M phases
         return (np.empty(n_a, np.int32), np.empty(n_b, np.int32), np.empty(ia, np.int64),
                 np.empty(ib, np.int64), np.zeros(cap, np.int64), cap)
 
@@ -310,7 +310,7 @@ class Reference:
 
     def _outs(self, n_a, n_b, eps):
         ia, ib = max(n_a, n_b), min(n_a, n_b)
-        cap = phase_cap(eps) + 1
+        cap = min(phase_cap(eps) + 1, 1 << 22)  # free_counts kept for the first 4M phases
         return (np.empty(n_a, np.int32), np.empty(n_b, np.int32), np.empty(ia, np.int64),
                 np.empty(ib, np.int64), np.zeros(cap, np.int64), cap)
 
@@ -378,7 +378,7 @@ class Reference:
         n_a, n_b = cost.shape
         cap_e = entry_cap or (n_a + n_b) * 4 + 16
         ea, eb, em = np.empty(cap_e, np.int32), np.empty(cap_e, np.int32), np.empty(cap_e)
-        fcap = phase_cap(eps / 3.0) + 1
+        fcap = min(phase_cap(eps / 3.0) + 1, 1 << 22)
         fc = np.zeros(fcap, np.int64)
         s = _RefOtStats()
         self._check(self.lib.ref_solve_ot(n_a, n_b, mu, nu, cost, eps, ea, eb, em, cap_e, fc, fcap,
@@ -401,7 +401,7 @@ class Reference:
     def solve_ot_rational(self, n_a: int, n_b: int, seed: int, eps: float, entry_cap: int | None = None):
         cap_e = entry_cap or (n_a + n_b) * 4
         ea, eb, em = np.empty(cap_e, np.int32), np.empty(cap_e, np.int32), np.empty(cap_e)
-        fcap = phase_cap(eps / 3.0) + 1
+        fcap = min(phase_cap(eps / 3.0) + 1, 1 << 22)
         fc = np.zeros(fcap, np.int64)
         s = _RefOtStats()
         self._check(self.lib.ref_solve_ot_rational(n_a, n_b, seed, eps, ea, eb, em, cap_e, fc, fcap,

@@ -20,7 +20,8 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 
 OK, PARAMETER, INPUT, NUMERICAL, INVARIANT, DEVICE = 0, 2, 3, 4, 5, 6
 COST_DENSE_F64, COST_POINTS2D, COST_L1_U8 = 0, 1, 2
-STORAGE = {"auto": 0, "u8": 1, "u16": 2}
+STORAGE = {"auto": 0, "u8": 1, "u16": 2, "u32": 3}
+MAX_PHASES = 1 << 24  # OTPRG_MAX_PHASES
 
 
 class Problem(C.Structure):

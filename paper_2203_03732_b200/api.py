@@ -318,7 +318,7 @@ class Solver:
 
     def _result(self, n_a: int, n_b: int, eps: float):
         ia, ib = max(n_a, n_b), min(n_a, n_b)
-        cap = SolveStats.phase_bound(eps) + 10
+        cap = min(SolveStats.phase_bound(eps) + 10, N.MAX_PHASES + 2)
         bufs = dict(match_of_a=np.empty(n_a, np.int32), match_of_b=np.empty(n_b, np.int32),
                     y_a=np.empty(ia, np.int64), y_b=np.empty(ib, np.int64),
                     free_counts=np.zeros(cap, np.int64))
@@ -820,7 +820,8 @@ def solve_ot(inst: OTInstance, eps: float, device: int = 0):
     p = _OTProblem(len(mu), len(nu), float(eps), mu.ctypes.data, nu.ctypes.data, cost.ctypes.data,
                    0, 0)
     cap = 4 * (len(mu) + len(nu)) + 64
-    fcap = SolveStats.phase_bound(eps / 3.0) + 16 if 0.0 < eps < 1.0 else 16  # C ABI validates eps
+    fcap = (min(SolveStats.phase_bound(eps / 3.0) + 16, N.MAX_PHASES + 2)
+            if 0.0 < eps < 1.0 else 16)  # C ABI validates eps
     ea, eb, em = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap)
     fc = np.zeros(fcap, np.int64)
     r = _OTResult()

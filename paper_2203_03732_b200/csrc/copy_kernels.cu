@@ -166,25 +166,23 @@ cudaError_t copy_da(const void* kT, int lda, int width, const void* t, int32_t* 
                     Ctl* ctl, cudaStream_t s) {
   if (nfree <= 0) return cudaSuccess;
   const int blocks = (nfree * 32 + 255) / 256;
-  if (width == 1)
-    copy_da_kernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(kT), lda,
-                                                   static_cast<const uint8_t*>(t), yb, ma, holder, pi,
-                                                   rank, bfree, nfree, n_a, phase, mp, mp_cnt, ctl);
-  else
-    copy_da_kernel<uint16_t><<<blocks, 256, 0, s>>>(static_cast<const uint16_t*>(kT), lda,
-                                                    static_cast<const uint16_t*>(t), yb, ma, holder, pi,
-                                                    rank, bfree, nfree, n_a, phase, mp, mp_cnt, ctl);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    copy_da_kernel<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(kT), lda, static_cast<const T*>(t), yb,
+                                             ma, holder, pi, rank, bfree, nfree, n_a, phase, mp, mp_cnt,
+                                             ctl);
+    return 0;
+  });
   return cudaGetLastError();
 }
 
 cudaError_t copy_apply(const int2* mp, const int* mp_cnt, const unsigned long long* holder, int32_t* ma,
                        int32_t* mb, void* t, int width, uint32_t phase, Ctl* ctl, cudaStream_t s) {
-  if (width == 1)
-    copy_apply_kernel<uint8_t><<<148, 256, 0, s>>>(mp, mp_cnt, holder, ma, mb, static_cast<uint8_t*>(t),
-                                                   phase, ctl);
-  else
-    copy_apply_kernel<uint16_t><<<148, 256, 0, s>>>(mp, mp_cnt, holder, ma, mb, static_cast<uint16_t*>(t),
-                                                    phase, ctl);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    copy_apply_kernel<T><<<148, 256, 0, s>>>(mp, mp_cnt, holder, ma, mb, static_cast<T*>(t), phase, ctl);
+    return 0;
+  });
   return cudaGetLastError();
 }
 

@@ -214,12 +214,11 @@ cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swappe
     grid = dim3((lda + 31) / 32, (n_b + 31) / 32);
   else
     grid = dim3((lda + 31) / 32, (n_a + 31) / 32);
-  if (width == 1)
-    round_dense_kernel<uint8_t><<<grid, block, 0, s>>>(cost, n_a, n_b, swapped, eps,
-                                                       static_cast<uint8_t*>(kT), lda, status);
-  else
-    round_dense_kernel<uint16_t><<<grid, block, 0, s>>>(cost, n_a, n_b, swapped, eps,
-                                                        static_cast<uint16_t*>(kT), lda, status);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    round_dense_kernel<T><<<grid, block, 0, s>>>(cost, n_a, n_b, swapped, eps, static_cast<T*>(kT), lda, status);
+    return 0;
+  });
   return cudaGetLastError();
 }
 
@@ -230,12 +229,11 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
   dim3 grid(bx < 8 ? bx : 8, n_bi < 65535 ? n_bi : 65535);
   const double2* a2 = reinterpret_cast<const double2*>(pa);
   const double2* b2 = reinterpret_cast<const double2*>(pb);
-  if (width == 1)
-    round_points_kernel<uint8_t><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2,
-                                                      static_cast<uint8_t*>(kT), lda);
-  else
-    round_points_kernel<uint16_t><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2,
-                                                       static_cast<uint16_t*>(kT), lda);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    round_points_kernel<T><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2, static_cast<T*>(kT), lda);
+    return 0;
+  });
   return cudaGetLastError();
 }
 
@@ -249,23 +247,21 @@ cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_
                             double eps, void* kT, int lda, int width, int* status,
                             cudaStream_t s) {
   dim3 grid(lda / kL1Tile, (n_bi + kL1Tile - 1) / kL1Tile);
-  if (width == 1)
-    l1_round_kernel<uint8_t><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps,
-                                                  static_cast<uint8_t*>(kT), lda, status);
-  else
-    l1_round_kernel<uint16_t><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps,
-                                                   static_cast<uint16_t*>(kT), lda, status);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    l1_round_kernel<T><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps, static_cast<T*>(kT), lda, status);
+    return 0;
+  });
   return cudaGetLastError();
 }
 
 cudaError_t launch_export_k(const void* kT, int n_ai, int n_bi, int lda, int width, bool swapped,
                             int32_t* k_out, cudaStream_t s) {
-  if (width == 1)
-    export_k_kernel<uint8_t><<<1184, 256, 0, s>>>(static_cast<const uint8_t*>(kT), n_ai, n_bi,
-                                                  lda, swapped, k_out);
-  else
-    export_k_kernel<uint16_t><<<1184, 256, 0, s>>>(static_cast<const uint16_t*>(kT), n_ai, n_bi,
-                                                   lda, swapped, k_out);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    export_k_kernel<T><<<1184, 256, 0, s>>>(static_cast<const T*>(kT), n_ai, n_bi, lda, swapped, k_out);
+    return 0;
+  });
   return cudaGetLastError();
 }
 

@@ -149,13 +149,39 @@ struct Simd<uint16_t> {
   __device__ static uint32_t hmin(uint32_t w) { return min(w & 0xffffu, w >> 16); }
 };
 
+// One element per word (eps below ~1/65531: unit_floor beyond uint16).
+template <>
+struct Simd<uint32_t> {
+  static constexpr int kEpw = 1;
+  static constexpr uint32_t kPadWord = 0xffffffffu;
+  __device__ static uint32_t rep(uint32_t v) { return v; }
+  __device__ static uint32_t add(uint32_t k, uint32_t t) {
+    const uint32_t s = k + t;
+    return s < k ? 0xffffffffu : s;
+  }
+  __device__ static uint32_t eq(uint32_t s, uint32_t tg) { return s == tg ? 0xffffffffu : 0u; }
+  __device__ static uint32_t mn(uint32_t a, uint32_t b) { return min(a, b); }
+  __device__ static uint32_t le(uint32_t s, uint32_t up) { return s <= up ? 0xffffffffu : 0u; }
+  __device__ static uint32_t bits(uint32_t m) { return m & 1u; }
+  __device__ static uint32_t elem(uint32_t w, int) { return w; }
+  __device__ static uint32_t hmin(uint32_t w) { return w; }
+};
+
 #endif  // __CUDACC__
 
 // Largest representable entry of T: the pad value of kT rows, and the
 // saturation value of k + t.  Targets are always strictly below it.
 template <typename T>
 __host__ __device__ constexpr uint32_t type_max() {
-  return sizeof(T) == 1 ? 0xffu : 0xffffu;
+  return sizeof(T) == 1 ? 0xffu : sizeof(T) == 2 ? 0xffffu : 0xffffffffu;
+}
+
+// Calls f(T{}) with T the kT storage type of `width` bytes (1, 2 or 4).
+template <typename F>
+inline auto with_width(int width, F&& f) {
+  if (width == 1) return f(uint8_t{});
+  if (width == 2) return f(uint16_t{});
+  return f(uint32_t{});
 }
 
 }  // namespace otprg

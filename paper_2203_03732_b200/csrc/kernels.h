@@ -124,6 +124,26 @@ cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, i
                                   cudaStream_t s);
 bool smem_t_fits(int width, int lda);
 
+// Largest t(a) / Y(b) the device state may hold: below the saturation value
+// of the packed k + t sums (u8/u16) and inside int32 (u32).
+inline uint32_t storage_tmax(int width) {
+  return width == 1 ? 253u : width == 2 ? 65533u : 0x7ffffff0u;
+}
+// Bytes per kT entry for |Y| <= need (= unit_ceil + 2, core.hpp:94-95), or -1
+// when the requested storage cannot hold it.  storage: 0 auto, 1 u8, 2 u16,
+// 3 u32 (otprg_storage).  Auto picks uint16 whenever it fits (measured faster
+// than uint8 end to end on B200 for config 2, profiles/r01_variants.txt, even
+// though a phase-1 scan reads twice the bytes), else uint32.
+inline int storage_width(int64_t need, int storage) {
+  auto fits = [&](int w) { return need <= (int64_t)storage_tmax(w) ? w : -1; };
+  switch (storage) {
+    case 1: return fits(1);
+    case 2: return fits(2);
+    case 3: return fits(4);
+    default: return fits(2) > 0 ? 2 : fits(4);
+  }
+}
+
 // Device invariant suite (verify_kernels.cu): first violation key
 // (section << 60 | index << 4 | kind, minimum over the grid) and count.
 struct VerifyOut {

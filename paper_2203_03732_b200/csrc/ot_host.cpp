@@ -282,8 +282,8 @@ class OtSolver {
     if (uf + 4 > std::numeric_limits<int32_t>::max())
       throw OtError{OTPRG_PARAMETER, "eps too small: 1/eps overflows the cost unit type"};
     const int64_t uc = static_cast<double>(uf) * eps_in_ == 1.0 ? uf : uf + 1;
-    if (uc + 2 > 65533) throw OtError{OTPRG_PARAMETER, "eps too small for the device cost storage"};
-    width_ = uc + 2 <= 253 ? 1 : 2;
+    width_ = otprg::storage_width(uc + 2, OTPRG_STORAGE_AUTO);
+    if (width_ < 0) throw OtError{OTPRG_PARAMETER, "eps too small for the device cost storage"};
     const int align = 512 / width_;
     lda_ = (n_a_ + align - 1) / align * align;
     OT_CK(cudaSetDevice(ctx_->device), "cudaSetDevice");
@@ -356,10 +356,11 @@ class OtSolver {
   // Cluster duals of every demand vertex to the device: t_ci = -y (type max if absent).
   void upload_cluster_duals() {
     char* hp = static_cast<char*>(ctx_->ot_hpin);
-    const uint32_t none = width_ == 1 ? 0xffu : 0xffffu;
+    const uint32_t none = width_ == 1 ? 0xffu : width_ == 2 ? 0xffffu : 0xffffffffu;
     auto put = [&](size_t i, uint32_t v) {
       if (width_ == 1) reinterpret_cast<uint8_t*>(hp)[i] = static_cast<uint8_t>(v);
-      else reinterpret_cast<uint16_t*>(hp)[i] = static_cast<uint16_t>(v);
+      else if (width_ == 2) reinterpret_cast<uint16_t*>(hp)[i] = static_cast<uint16_t>(v);
+      else reinterpret_cast<uint32_t*>(hp)[i] = v;
     };
     for (int32_t a = 0; a < lda_; ++a) {
       uint32_t v0 = none, v1 = none;

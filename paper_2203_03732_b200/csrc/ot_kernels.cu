@@ -117,16 +117,11 @@ cudaError_t launch_ot_scan(const void* kT, int lda, int width, const void* t0, c
                            cudaStream_t s) {
   if (nreq <= 0) return cudaSuccess;
   const int blocks = (nreq * 32 + 255) / 256;
-  if (width == 1)
-    ot_scan_kernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(kT), lda,
-                                                   static_cast<const uint8_t*>(t0),
-                                                   static_cast<const uint8_t*>(t1), req, nreq, K,
-                                                   out, meta);
-  else
-    ot_scan_kernel<uint16_t><<<blocks, 256, 0, s>>>(static_cast<const uint16_t*>(kT), lda,
-                                                    static_cast<const uint16_t*>(t0),
-                                                    static_cast<const uint16_t*>(t1), req, nreq, K,
-                                                    out, meta);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    ot_scan_kernel<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(kT), lda, static_cast<const T*>(t0), static_cast<const T*>(t1), req, nreq, K, out, meta);
+    return 0;
+  });
   return cudaGetLastError();
 }
 

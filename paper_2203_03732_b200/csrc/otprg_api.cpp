@@ -93,7 +93,7 @@ struct ResultBufs {
     ya.assign(ia, 0);
     yb.assign(ib, 0);
     SolveStats s;
-    fc.assign(static_cast<size_t>(s.phase_bound(eps) + 10), 0);
+    fc.assign(static_cast<size_t>(std::min<std::int64_t>(s.phase_bound(eps) + 10, OTPRG_MAX_PHASES + 2)), 0);
     r.match_of_a = m.match_of_a.data();
     r.match_of_b = m.match_of_b.data();
     r.y_a = ya.data();

@@ -93,13 +93,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   // Storage: |Y| <= unit_ceil + 2 (core.hpp:94-95) must stay below the
   // saturation value of the packed k + t sums.
   const int64_t need = static_cast<int64_t>(ctx->unit_ceil) + 2;
-  const bool fits8 = need <= 253, fits16 = need <= 65533;
-  int width = 0;
-  if (p->storage == OTPRG_STORAGE_U8) width = fits8 ? 1 : -1;
-  else if (p->storage == OTPRG_STORAGE_U16) width = fits16 ? 2 : -1;
-  // AUTO: uint16, measured faster than uint8 end to end on B200 for config 2
-  // (profiles/r01_variants.txt) even though a phase-1 scan reads twice the bytes.
-  else width = fits16 ? 2 : -1;
+  const int width = otprg::storage_width(need, p->storage);
   if (width < 0)
     return fail(ctx, OTPRG_PARAMETER,
                 "eps too small for the device cost storage (ceil(1/eps)+2 = " +
@@ -124,7 +118,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   CK(ctx->fb.ensure(ib * 4), "alloc scratch");
   CK(ctx->ctl.ensure(sizeof(Ctl)), "alloc ctl");
   const double capd = std::ceil((1.0 + 2.0 * p->eps) / (p->eps * p->eps)) + 8.0;
-  ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(1 << 24)));
+  ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(OTPRG_MAX_PHASES)));
   CK(ctx->fc.ensure(ctx->fc_cap * 8), "alloc free_counts");
   ctx->smem_t = otprg::smem_t_fits(width, ctx->lda);
   ctx->loop_grid = otprg::phase_loop_grid(width, ctx->smem_t, ctx->lda, ctx->num_sms);
@@ -263,7 +257,7 @@ int do_begin(otprg_ctx* ctx, cudaEvent_t ev_init = nullptr, cudaEvent_t ev_scan0
   const double threshold = ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b));
   h.thresh = static_cast<int32_t>(std::floor(threshold));
   h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
-  h.tmax = ctx->width == 1 ? 253u : 65533u;
+  h.tmax = otprg::storage_tmax(ctx->width);
   h.cnt[0] = ctx->ib;  // phase 1 reads list 0 (all b)
   h.slots[0] = ctx->ib;
   h.prop_t0 = ~0ull;
@@ -381,8 +375,9 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
   }
   if (r->y_a) {
     for (int i = 0; i < ia; ++i) {
-      const int64_t t = ctx->width == 1 ? tbytes[i]
-                                        : reinterpret_cast<const uint16_t*>(tbytes)[i];
+      const int64_t t = ctx->width == 1   ? tbytes[i]
+                        : ctx->width == 2 ? reinterpret_cast<const uint16_t*>(tbytes)[i]
+                                          : reinterpret_cast<const uint32_t*>(tbytes)[i];
       r->y_a[i] = -t;
     }
   }
@@ -795,9 +790,9 @@ int otprg_verify_feasibility(otprg_ctx* ctx, otprg_feasibility* out) {
   int err = 0;
   decode_violation(r, ctx->ia, ctx->ib,
                    [&](otprg_feasibility* f) {
-                     uint16_t tv = 0;
+                     uint32_t tv = 0;  // w low bytes (little endian), rest zero
                      int32_t ybv = 0;
-                     uint16_t kv = 0;
+                     uint32_t kv = 0;
                      const int w = ctx->width;
                      if (f->a >= 0 && cudaMemcpy(&tv, static_cast<char*>(ctx->t.p) + static_cast<size_t>(f->a) * w, w,
                                                  cudaMemcpyDeviceToHost) != cudaSuccess) err = 1;
@@ -807,8 +802,8 @@ int otprg_verify_feasibility(otprg_ctx* ctx, otprg_feasibility* out) {
                          cudaMemcpy(&kv, static_cast<char*>(ctx->kT.p) +
                                              (static_cast<size_t>(f->b) * ctx->lda + f->a) * w,
                                     w, cudaMemcpyDeviceToHost) != cudaSuccess) err = 1;
-                     const long long ya = -static_cast<long long>(w == 1 ? (tv & 0xff) : tv);
-                     const long long kk = w == 1 ? (kv & 0xff) : kv;
+                     const long long ya = -static_cast<long long>(tv);
+                     const long long kk = kv;
                      if (f->kind >= OTPRG_VIOL_NOT_TIGHT) {
                        f->sum = ya + ybv;
                        f->k = kk;
@@ -1117,9 +1112,7 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   ctx->unit_floor = static_cast<int32_t>(uf);
   ctx->unit_ceil = static_cast<int32_t>(static_cast<double>(uf) * p->eps == 1.0 ? uf : uf + 1);
   const int64_t need = static_cast<int64_t>(ctx->unit_ceil) + 2;
-  int width = -1;
-  if (p->storage == OTPRG_STORAGE_U8) width = need <= 253 ? 1 : -1;
-  else width = need <= 65533 ? 2 : -1;
+  const int width = otprg::storage_width(need, p->storage);
   if (width < 0) return fail(ctx, OTPRG_PARAMETER, "eps too small for the device cost storage");
   ctx->width = width;
   // shard boundaries: multiples of 512 elements (aligned t / kT vectors)
@@ -1159,7 +1152,7 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   CK(ctx->sh_list.ensure(ib * 4), "alloc list");
   for (auto& pk : ctx->sh_park) CK(pk.ensure(ib * 16), "alloc park");
   const double capd = std::ceil((1.0 + 2.0 * p->eps) / (p->eps * p->eps)) + 8.0;
-  ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(1 << 24)));
+  ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(OTPRG_MAX_PHASES)));
   CK(ctx->fc.ensure(ctx->fc_cap * 8), "alloc free_counts");
   CK(cudaMemcpyAsync(ctx->sh_bounds.p, bounds.data(), (n_shards + 1) * sizeof(int),
                      cudaMemcpyHostToDevice, ctx->stream), "H2D bounds");
@@ -1198,7 +1191,7 @@ int otprg_shard_begin(otprg_ctx* ctx) {
   h.lda = ctx->lda;
   h.thresh = static_cast<int32_t>(std::floor(ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b))));
   h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
-  h.tmax = ctx->width == 1 ? 253u : 65533u;
+  h.tmax = otprg::storage_tmax(ctx->width);
   h.cnt[0] = ctx->ib;
   CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream), "H2D ctl");
   otprg::SolveArgs A{};

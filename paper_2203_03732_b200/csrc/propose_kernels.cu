@@ -221,23 +221,19 @@ cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, i
   const int warps = (n_b + rpw - 1) / rpw;
   const int grid = (warps + kWarps - 1) / kWarps;
   // raise the opt-in shared-memory limit once per device and width
-  static size_t smem_set[64][2] = {};
+  static size_t smem_set[64][3] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   size_t* smem_set_dev = smem_set[dev & 63];
-  if (width == 1) {
-    auto fn = propose_stream_kernel<uint8_t>;
-    if (smem_set_dev[0] < smem)
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_set_dev[0] = smem));
-    fn<<<grid, kStreamThreads, smem, s>>>(static_cast<const uint8_t*>(kT), lda, n_b, chunk, cpr, rpw,
-                                          lmeta, lent, static_cast<uint8_t*>(rowmin), ctl);
-  } else {
-    auto fn = propose_stream_kernel<uint16_t>;
-    if (smem_set_dev[1] < smem)
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_set_dev[1] = smem));
-    fn<<<grid, kStreamThreads, smem, s>>>(static_cast<const uint16_t*>(kT), lda, n_b, chunk, cpr, rpw,
-                                          lmeta, lent, static_cast<uint16_t*>(rowmin), ctl);
-  }
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    auto fn = propose_stream_kernel<T>;
+    size_t& set = smem_set_dev[sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : 2];
+    if (set < smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(set = smem));
+    fn<<<grid, kStreamThreads, smem, s>>>(static_cast<const T*>(kT), lda, n_b, chunk, cpr, rpw, lmeta,
+                                          lent, static_cast<T*>(rowmin), ctl);
+    return 0;
+  });
   return cudaGetLastError();
 }
 

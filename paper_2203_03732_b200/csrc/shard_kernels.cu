@@ -31,12 +31,14 @@ namespace otprg {
 namespace {
 
 __device__ __forceinline__ uint32_t t_get(const ShardArgs& S, int a) {
-  return S.width == 1 ? (uint32_t)static_cast<const uint8_t*>(S.t)[a]
-                      : (uint32_t)static_cast<const uint16_t*>(S.t)[a];
+  return S.width == 1   ? (uint32_t)static_cast<const uint8_t*>(S.t)[a]
+         : S.width == 2 ? (uint32_t)static_cast<const uint16_t*>(S.t)[a]
+                        : static_cast<const uint32_t*>(S.t)[a];
 }
 __device__ __forceinline__ void t_set(const ShardArgs& S, int a, uint32_t v) {
   if (S.width == 1) static_cast<uint8_t*>(S.t)[a] = (uint8_t)v;
-  else static_cast<uint16_t*>(S.t)[a] = (uint16_t)v;
+  else if (S.width == 2) static_cast<uint16_t*>(S.t)[a] = (uint16_t)v;
+  else static_cast<uint32_t*>(S.t)[a] = v;
 }
 
 // Scan request: (list index, b, start position (global a)).  req == nullptr:
@@ -339,8 +341,10 @@ cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int
                               int2* meta, cudaStream_t s) {
   if (nreq <= 0) return cudaSuccess;
   const int blocks = (nreq * 32 + 255) / 256;
-  if (a.width == 1) shard_scan_kernel<uint8_t><<<blocks, 256, 0, s>>>(a, req, nreq, cand, meta);
-  else shard_scan_kernel<uint16_t><<<blocks, 256, 0, s>>>(a, req, nreq, cand, meta);
+  with_width(a.width, [&](auto tag) {
+    shard_scan_kernel<decltype(tag)><<<blocks, 256, 0, s>>>(a, req, nreq, cand, meta);
+    return 0;
+  });
   return cudaGetLastError();
 }
 

@@ -389,7 +389,9 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     if (a < 0) {
       // b stays free this phase: Y(b) += 1 (apply_phase :233-235).
       uint32_t m = 0;
-      if (track_min) m = (uint32_t)team_min(tm, (int)__reduce_min_sync(kFull, S::hmin(mnw)), lane);
+      // (clamped into int: a uint32 pad sum 0xffffffff must not read as -1)
+      if (track_min)
+        m = (uint32_t)team_min(tm, (int)min(__reduce_min_sync(kFull, S::hmin(mnw)), 0x7fffffffu), lane);
       if (lead) {
         if (track_min) rowmin[b] = (T)m;
         if (fresh && dirty) A.lmeta[b] = meta;
@@ -821,8 +823,10 @@ void* loop_fn() {
 }
 
 void* pick_loop(int width, bool smem_t) {
-  if (width == 1) return smem_t ? loop_fn<uint8_t, true>() : loop_fn<uint8_t, false>();
-  return smem_t ? loop_fn<uint16_t, true>() : loop_fn<uint16_t, false>();
+  return with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    return smem_t ? loop_fn<T, true>() : loop_fn<T, false>();
+  });
 }
 
 }  // namespace
@@ -856,10 +860,10 @@ cudaError_t launch_phase_loop(const SolveArgs& a, int width, bool smem_t, int ld
 cudaError_t launch_init_state(const SolveArgs& a, int n_a, int n_b, int lda, int width,
                               cudaStream_t s) {
   const int blocks = (lda + 255) / 256;
-  if (width == 1)
-    init_state_kernel<uint8_t><<<blocks, 256, 0, s>>>(a, n_a, n_b, lda);
-  else
-    init_state_kernel<uint16_t><<<blocks, 256, 0, s>>>(a, n_a, n_b, lda);
+  with_width(width, [&](auto tag) {
+    init_state_kernel<decltype(tag)><<<blocks, 256, 0, s>>>(a, n_a, n_b, lda);
+    return 0;
+  });
   return cudaGetLastError();
 }
 

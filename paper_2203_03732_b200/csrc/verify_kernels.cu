@@ -254,19 +254,13 @@ cudaError_t launch_verify_state(const void* kT, int lda, int width, const void* 
                                 int n_b, long long bound, VerifyOut* out, cudaStream_t s) {
   const int blocks = 148 * 4;
   verify_match_kernel<<<blocks, 256, 0, s>>>(ma, mb, n_a, n_b, out);
-  if (width == 1) {
-    verify_duals_kernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(t), yb, ma, n_a,
-                                                        n_b, bound, out);
-    verify_edges_kernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(kT), lda,
-                                                        static_cast<const uint8_t*>(t), yb, mb, n_a,
-                                                        n_b, out);
-  } else {
-    verify_duals_kernel<uint16_t><<<blocks, 256, 0, s>>>(static_cast<const uint16_t*>(t), yb, ma,
-                                                         n_a, n_b, bound, out);
-    verify_edges_kernel<uint16_t><<<blocks, 256, 0, s>>>(static_cast<const uint16_t*>(kT), lda,
-                                                         static_cast<const uint16_t*>(t), yb, mb,
-                                                         n_a, n_b, out);
-  }
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    verify_duals_kernel<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(t), yb, ma, n_a, n_b, bound, out);
+    verify_edges_kernel<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(kT), lda, static_cast<const T*>(t),
+                                                  yb, mb, n_a, n_b, out);
+    return 0;
+  });
   return cudaGetLastError();
 }
 
@@ -290,14 +284,11 @@ cudaError_t launch_admissible(const void* kT, int lda, int width, const void* t,
                               const long long* offs, int32_t* out, cudaStream_t s) {
   if (nfree <= 0) return cudaSuccess;
   const int blocks = (nfree * 32 + 255) / 256;
-  if (width == 1)
-    admissible_kernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(kT), lda,
-                                                      static_cast<const uint8_t*>(t), yb, bfree,
-                                                      nfree, n_a, counts, offs, out);
-  else
-    admissible_kernel<uint16_t><<<blocks, 256, 0, s>>>(static_cast<const uint16_t*>(kT), lda,
-                                                       static_cast<const uint16_t*>(t), yb, bfree,
-                                                       nfree, n_a, counts, offs, out);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    admissible_kernel<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(kT), lda, static_cast<const T*>(t), yb, bfree, nfree, n_a, counts, offs, out);
+    return 0;
+  });
   return cudaGetLastError();
 }
 

@@ -150,7 +150,7 @@ def test_config2_n10k_eps001_seeds_1_2_3(golden):
         key = f"square_n10000_eps0.01_s{seed}"
         w = golden[key]
         inst = otprg.gen_uniform_square(10000, seed)
-        for storage in ("u8", "u16"):
+        for storage in ("u8", "u16", "u32"):
             m, s = _solve(inst, 0.01, storage)
             _assert_matches_golden(key, w, m, s)
 
@@ -177,7 +177,9 @@ def test_storage_widths_agree_and_repeat_is_deterministic():
     m2, s2 = solver.solve_prepared()
     solver.prepare(inst, 0.02, "u16")
     m3, s3 = solver.solve_prepared()
-    for m, s in ((m2, s2), (m3, s3)):
+    solver.prepare(inst, 0.02, "u32")
+    m4, s4 = solver.solve_prepared()
+    for m, s in ((m2, s2), (m3, s3), (m4, s4)):
         np.testing.assert_array_equal(m.match_of_a, m1.match_of_a)
         np.testing.assert_array_equal(s.duals_final.y_a, s1.duals_final.y_a)
         np.testing.assert_array_equal(s.duals_final.y_b, s1.duals_final.y_b)
@@ -252,3 +254,43 @@ def test_degenerate_costs_match_oracle(oracle, case):
     np.testing.assert_array_equal(s.duals_final.y_b, want.y_b)
     np.testing.assert_array_equal(s.free_counts, want.free_counts)
     assert s.device["cost"] == want.cost
+
+
+# ---- uint32 storage: eps below ~1/65531 ------------------
+# The reference accepts any eps with unit_floor + 4 <= INT32_MAX
+# (core.cpp:36-41); below uint16's range the device stores kT / t as uint32.
+
+def _assert_same_as_oracle(m, s, want):
+    np.testing.assert_array_equal(m.match_of_a, want.match_of_a)
+    np.testing.assert_array_equal(m.match_of_b, want.match_of_b)
+    np.testing.assert_array_equal(s.duals_final.y_a, want.y_a)
+    np.testing.assert_array_equal(s.duals_final.y_b, want.y_b)
+    assert s.phases == want.phases and s.sum_ni == want.sum_ni
+    np.testing.assert_array_equal(s.free_counts, want.free_counts)
+    assert s.device["cost"] == want.cost and s.swapped == want.swapped
+
+
+def test_one_by_one_tiny_eps_u32():
+    eps = 1e-5  # unit_floor 100000: beyond uint16
+    m, s = _solve(_single(0.375), eps)
+    assert s.device["width"] == 4
+    k = otprg.scale_round_costs(_single(0.375), eps).k[0, 0]
+    assert s.phases == k + 1 and m.match_of_a[0] == 0
+    assert s.duals_final.y_b[0] == k + 1 and s.duals_final.y_a[0] == -1
+
+
+@pytest.mark.parametrize("n_a,n_b,eps,seed", [(48, 40, 1.0 / 70000.0, 1), (30, 45, 1e-5, 2),
+                                              (64, 64, 2e-6, 3)])
+def test_tiny_eps_u32_vs_oracle(oracle, n_a, n_b, eps, seed):
+    cost = np.random.default_rng(seed).random((n_a, n_b))
+    want = oracle.solve_assignment(cost, eps)
+    m, s = _solve(otprg.AssignmentInstance(n_a, n_b, cost), eps)
+    assert s.device["width"] == 4
+    _assert_same_as_oracle(m, s, want)
+
+
+def test_explicit_storage_too_narrow_is_parameter_error():
+    with pytest.raises(otprg.ParameterError):
+        _solve(_single(0.5), 1e-5, "u16")
+    with pytest.raises(otprg.ParameterError):
+        _solve(_single(0.5), 0.001, "u8")

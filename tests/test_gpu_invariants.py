@@ -213,7 +213,7 @@ def test_swapped_orientation_observer():
     assert s.swapped and m.size() == 5 and seen == list(range(1, s.phases + 1))
 
 
-@pytest.mark.parametrize("storage", ["u8", "u16"])
+@pytest.mark.parametrize("storage", ["u8", "u16", "u32"])
 @pytest.mark.parametrize("shape", [(60, 60), (70, 45), (45, 70)])
 def test_state_verify_matches_restatement_after_completion(storage, shape):
     """The solver-state kernels (packed SIMD over the B-major kT) against the

@@ -54,7 +54,7 @@ def test_sharded_forced_rescans(golden, K, G):
     _check_golden(golden, key, m, s)
 
 
-@pytest.mark.parametrize("storage", ["u8", "u16"])
+@pytest.mark.parametrize("storage", ["u8", "u16", "u32"])
 def test_sharded_storage(golden, storage):
     key = "square_n2000_eps0.01_s3"
     v = golden[key]
