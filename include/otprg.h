@@ -46,7 +46,8 @@ enum otprg_status {
   OTPRG_INPUT = 3,
   OTPRG_NUMERICAL = 4,
   OTPRG_INVARIANT = 5,
-  OTPRG_DEVICE = 6
+  OTPRG_DEVICE = 6,
+  OTPRG_ABORTED = 7 /* an observer callback returned nonzero (its exception, in a wrapper) */
 };
 
 /* How the cost of edge (a, b) is given. */
@@ -323,6 +324,105 @@ typedef struct otprg_ot_result {
 } otprg_ot_result;
 
 int otprg_solve_ot(otprg_ctx* ctx, const otprg_ot_problem* prob, otprg_ot_result* res);
+
+/* ---- OT phase primitives and debug mode ----------------------------------
+ * The copy/cluster solver's types (include/otpr/ot.hpp:52-95) in flat form.
+ * A CopyInstance: rounded costs over the original vertices plus a copy count
+ * per vertex (ot.hpp:52-63).  unit_ceil is ScaledCosts::unit_ceil, so the
+ * dual bound of the checks is unit_ceil + 2 (core.hpp:95). */
+typedef struct otprg_copy_instance {
+  int32_t n_a, n_b;
+  const int32_t* k;              /* n_a*n_b row-major ScaledCosts::k */
+  int64_t unit_ceil;
+  const int64_t* demand_copies;  /* n_a */
+  const int64_t* supply_copies;  /* n_b */
+} otprg_copy_instance;
+
+/* ClusterState (ot.hpp:65-95): demand vertex a owns clusters
+ * [dem_off[a], dem_off[a+1]) (dual, free copies, flow entries
+ * [flow_off[c], flow_off[c+1]) of (b, copies) ascending b); supply vertex b
+ * owns [sup_off[b], sup_off[b+1]).  Clusters are in descending dual order, as
+ * normalize_demand / normalize_supply leave them (ot.cpp:362-414). */
+typedef struct otprg_cluster_state {
+  int32_t n_a, n_b;
+  const int32_t* dem_off;   /* n_a + 1 */
+  const int64_t* dem_y;
+  const int64_t* dem_free;
+  const int64_t* flow_off;  /* clusters + 1 */
+  const int32_t* flow_b;
+  const int64_t* flow_cnt;
+  const int32_t* sup_off;   /* n_b + 1 */
+  const int64_t* sup_y;
+  const int64_t* sup_free;
+  const int64_t* sup_matched;
+} otprg_cluster_state;
+
+/* ClusterPhaseSnapshot (ot.hpp:115-122); every pointer is valid only during
+ * the observer call (the reference's references have the same lifetime). */
+typedef struct otprg_cluster_snapshot {
+  int64_t phase; /* 1-based */
+  int64_t n_i;   /* free supply copies at phase start */
+  int64_t sum_abs_before, sum_abs_after;
+  otprg_copy_instance inst;
+  otprg_cluster_state state;
+} otprg_cluster_snapshot;
+
+typedef int (*otprg_cluster_observer)(const otprg_cluster_snapshot* snap, void* user);
+
+/* OTOptions / ClusterOptions (ot.hpp:124-129, 153-156).  check_invariants:
+ * after every phase the greedy-maximality, cluster-invariant and
+ * cluster-feasibility checks of ot.cpp:524-533, 594-603 (host; the first
+ * violation is OTPRG_INVARIANT with the reference's message).  observer:
+ * called after every phase; a nonzero return stops the solve (OTPRG_ABORTED). */
+typedef struct otprg_ot_options {
+  int32_t check_invariants;
+  int32_t pad;
+  otprg_cluster_observer observer;
+  void* user;
+} otprg_ot_options;
+
+/* solve_ot with options (opt may be NULL = otprg_solve_ot). */
+int otprg_solve_ot_opts(otprg_ctx* ctx, const otprg_ot_problem* prob, const otprg_ot_options* opt,
+                        otprg_ot_result* res);
+
+/* solve_copy_matching (ot.hpp:135-141, ot.cpp:418-637) on a copy instance:
+ * the k matrix goes to the device as the scan's kT, the claim step and the
+ * cluster bookkeeping are those of otprg_solve_ot.  eps is the solve's
+ * accuracy (termination eps * total supply copies, phase cap).  Errors as
+ * CopyInstance::validate (ot.cpp:142-152) -> OTPRG_PARAMETER; in addition k
+ * must lie in [0, 2^31 - 16) (device storage).  flow: the n_a*n_b dense
+ * ClusterSolveResult::flow (completion included) or NULL.  The final state
+ * before completion stays readable through otprg_copy_state until the next
+ * solve on the context. */
+typedef struct otprg_copy_result {
+  int64_t* flow;
+  int64_t* free_counts;  /* n_i per phase, up to free_cap entries, or NULL */
+  int64_t free_cap;
+  int64_t phases;
+  int64_t sum_ni;
+  int32_t full_match_termination;
+  int32_t gpu_launches;
+} otprg_copy_result;
+
+int otprg_solve_copy_matching(otprg_ctx* ctx, const otprg_copy_instance* inst, double eps,
+                              const otprg_ot_options* opt, otprg_copy_result* res);
+/* ClusterSolveResult::state of the last otprg_solve_copy_matching /
+ * otprg_solve_ot_opts on ctx (pointers owned by ctx). */
+int otprg_copy_state(otprg_ctx* ctx, otprg_cluster_state* out);
+
+/* check_cluster_invariant (which = 0, ot.cpp:190-265) and
+ * check_cluster_feasibility (which = 1, ot.cpp:267-315) on a flat state:
+ * *count = number of violations (ClusterReport::violations.size()), their
+ * messages newline-separated into msgs (NUL-terminated, truncated to
+ * msgs_cap).  Host-only. */
+int otprg_check_cluster_state(const otprg_cluster_state* state, const otprg_copy_instance* inst,
+                              int32_t which, int64_t* count, char* msgs, int32_t msgs_cap);
+
+/* plan_from_flow (ot.hpp:143-151, ot.cpp:639-703): dense integer copy flow
+ * (n_a*n_b row-major) + ScaledMasses (theta, d, s) + the OT instance ->
+ * plan entries / cost in res (the plan fields of otprg_ot_result).  Host-only. */
+int otprg_plan_from_flow(const otprg_ot_problem* prob, const int64_t* flow, double theta,
+                         const int64_t* d, const int64_t* s, otprg_ot_result* res);
 
 /* ---- Sinkhorn baseline -------------------------------
  * otprg_sinkhorn replaces otpr::sinkhorn (include/otpr/sinkhorn.hpp:13-31,

@@ -287,6 +287,13 @@ class Reference:
                                      _f64p, C.c_int64, _i64p, C.c_int64, C.POINTER(_RefOtStats)]
         lib.ref_scale_and_round.argtypes = [C.c_int32, C.c_int32, _f64p, _f64p, _f64p, C.c_double, _i64p,
                                             _i64p, C.POINTER(C.c_double)]
+        flat = [_i32p, _i64p, _i64p, _i64p, _i32p, _i64p, _i32p, _i64p, _i64p, _i64p]
+        lib.ref_solve_copy_matching.argtypes = ([C.c_int32, C.c_int32, _i32p, C.c_double, C.c_int32,
+                                                 C.c_int32, _i64p, _i64p, C.c_double, C.c_int32, _i64p,
+                                                 _i64p, C.c_int64, _i64p, C.c_int64, _i64p, _i64p]
+                                                + flat + [C.c_int64, _i64p])
+        lib.ref_check_cluster.argtypes = ([C.c_int32, C.c_int32, _i32p, C.c_int32, _i64p, _i64p] + flat
+                                          + [C.c_int32, C.POINTER(C.c_int64), C.c_char_p, C.c_int32])
 
     def _check(self, st):
         if st:
@@ -411,3 +418,62 @@ class Reference:
                 "solve_ms": s.solve_ms, "n_entries": s.n_entries, "total_d": s.total_d,
                 "total_s": s.total_s, "a": ea[:ne].copy(), "b": eb[:ne].copy(), "mass": em[:ne].copy(),
                 "free_counts": fc[: s.phases].copy()}
+
+
+# ---- copy/cluster solver of the reference (ot.hpp:52-151) -------------------
+FLAT_KEYS = ("dem_off", "dem_y", "dem_free", "flow_off", "flow_b", "flow_cnt", "sup_off", "sup_y",
+             "sup_free", "sup_matched")
+
+
+def _ref_copy_matching(self, k, ceps, uf, uc, d, s, eps, check=True, phase_cap=4096):
+    """otpr::solve_copy_matching on CopyInstance{k, d, s}: final flow,
+    free_counts, stats, the per-phase flow matrices (observer) and the final
+    ClusterState in the flat layout of include/otprg.h."""
+    k = np.ascontiguousarray(k, np.int32)
+    d = np.ascontiguousarray(d, np.int64)
+    s = np.ascontiguousarray(s, np.int64)
+    n_a, n_b = k.shape
+    flow = np.zeros((n_a, n_b), np.int64)
+    fc = np.zeros(1 << 16, np.int64)
+    pf = np.zeros((phase_cap, n_a, n_b), np.int64)
+    pni = np.zeros(phase_cap, np.int64)
+    st3 = np.zeros(3, np.int64)
+    cap = int(d.sum() + s.sum()) * 2 + 4 * (n_a + n_b) + 16
+    fl = dict(dem_off=np.zeros(n_a + 1, np.int32), dem_y=np.zeros(cap, np.int64),
+              dem_free=np.zeros(cap, np.int64), flow_off=np.zeros(cap + 1, np.int64),
+              flow_b=np.zeros(cap, np.int32), flow_cnt=np.zeros(cap, np.int64),
+              sup_off=np.zeros(n_b + 1, np.int32), sup_y=np.zeros(cap, np.int64),
+              sup_free=np.zeros(cap, np.int64), sup_matched=np.zeros(cap, np.int64))
+    sizes = np.zeros(3, np.int64)
+    self._check(self.lib.ref_solve_copy_matching(n_a, n_b, k, ceps, uf, uc, d, s, eps, int(check), flow,
+                                                 fc, len(fc), pf, phase_cap, pni, st3,
+                                                 *[fl[x] for x in FLAT_KEYS], cap, sizes))
+    nd, nf, ns = (int(x) for x in sizes)
+    assert max(nd, nf, ns) <= cap
+    state = dict(dem_off=fl["dem_off"], dem_y=fl["dem_y"][:nd], dem_free=fl["dem_free"][:nd],
+                 flow_off=fl["flow_off"][: nd + 1], flow_b=fl["flow_b"][:nf], flow_cnt=fl["flow_cnt"][:nf],
+                 sup_off=fl["sup_off"], sup_y=fl["sup_y"][:ns], sup_free=fl["sup_free"][:ns],
+                 sup_matched=fl["sup_matched"][:ns])
+    ph = int(st3[0])
+    return dict(flow=flow, free_counts=fc[:ph].copy(), phases=ph, sum_ni=int(st3[1]),
+                full_match_termination=bool(st3[2]), phase_flows=pf[: min(ph, phase_cap)].copy(),
+                phase_ni=pni[: min(ph, phase_cap)].copy(), state=state)
+
+
+def _ref_check_cluster(self, k, uc, d, s, state: dict, which: int):
+    """otpr::check_cluster_invariant (0) / check_cluster_feasibility (1)."""
+    k = np.ascontiguousarray(k, np.int32)
+    n_a, n_b = k.shape
+    cnt = C.c_int64()
+    buf = C.create_string_buffer(1 << 16)
+    arrs = [np.ascontiguousarray(state[x], np.int32 if x in ("dem_off", "flow_b", "sup_off") else np.int64)
+            for x in FLAT_KEYS]
+    self._check(self.lib.ref_check_cluster(n_a, n_b, k, uc, np.ascontiguousarray(d, np.int64),
+                                           np.ascontiguousarray(s, np.int64), *arrs, which, C.byref(cnt),
+                                           buf, len(buf)))
+    msgs = buf.value.decode().split("\n") if cnt.value else []
+    return msgs[: cnt.value]
+
+
+Reference.solve_copy_matching = _ref_copy_matching
+Reference.check_cluster = _ref_check_cluster

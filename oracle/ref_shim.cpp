@@ -6,6 +6,7 @@
 // generator and bench.py's reference arm call the reference's own public API
 // (otpr::solve_assignment, otpr::solve_ot, ...) through ctypes.  This file is
 // ours; no reference source is copied into the repo.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -435,6 +436,124 @@ int ref_exact_ot(int32_t n_a, int32_t n_b, const double* mu, const double* nu, c
     inst.cost = otpr::Matrix<double>(n_a, n_b);
     std::memcpy(inst.cost.data(), cost, sizeof(double) * size_t(n_a) * n_b);
     *opt_cost = otpr::exact_ot(inst, 256).second;
+  });
+}
+
+
+// ---- copy/cluster solver (ot.hpp:52-151), for the OT phase-primitive tests --
+static otpr::CopyInstance make_copy(int32_t n_a, int32_t n_b, const int32_t* k, double ceps,
+                                    int32_t unit_floor, int32_t unit_ceil, const int64_t* d,
+                                    const int64_t* s) {
+  otpr::CopyInstance ci;
+  ci.costs.eps = ceps;
+  ci.costs.unit_floor = unit_floor;
+  ci.costs.unit_ceil = unit_ceil;
+  ci.costs.k = otpr::Matrix<int32_t>(n_a, n_b);
+  std::memcpy(ci.costs.k.data(), k, sizeof(int32_t) * size_t(n_a) * n_b);
+  ci.demand_copies.assign(d, d + n_a);
+  ci.supply_copies.assign(s, s + n_b);
+  return ci;
+}
+
+// Flat ClusterState (include/otprg.h otprg_cluster_state layout, counts first):
+// sizes[0..2] = clusters (demand), flow entries, clusters (supply).
+static void flatten(const otpr::ClusterState& st, int32_t* dem_off, int64_t* dem_y, int64_t* dem_free,
+                    int64_t* flow_off, int32_t* flow_b, int64_t* flow_cnt, int32_t* sup_off,
+                    int64_t* sup_y, int64_t* sup_free, int64_t* sup_matched, int64_t cap,
+                    int64_t* sizes) {
+  int64_t nd = 0, nf = 0, ns = 0;
+  dem_off[0] = 0;
+  flow_off[0] = 0;
+  for (size_t a = 0; a < st.demand.size(); ++a) {
+    for (const auto& c : st.demand[a]) {
+      if (nd < cap) dem_y[nd] = c.y, dem_free[nd] = c.free_count;
+      for (const auto& [b, cnt] : c.flow) {
+        if (nf < cap) flow_b[nf] = b, flow_cnt[nf] = cnt;
+        ++nf;
+      }
+      ++nd;
+      if (nd < cap + 1) flow_off[nd] = nf;
+    }
+    dem_off[a + 1] = static_cast<int32_t>(nd);
+  }
+  sup_off[0] = 0;
+  for (size_t b = 0; b < st.supply.size(); ++b) {
+    for (const auto& c : st.supply[b]) {
+      if (ns < cap) sup_y[ns] = c.y, sup_free[ns] = c.free_count, sup_matched[ns] = c.matched_count;
+      ++ns;
+    }
+    sup_off[b + 1] = static_cast<int32_t>(ns);
+  }
+  sizes[0] = nd, sizes[1] = nf, sizes[2] = ns;
+}
+
+// otpr::solve_copy_matching: final flow (completion included), free_counts,
+// phases / sum_ni / full_match_termination in stats6[0..2], the per-phase flow
+// matrices (observer, up to phase_cap of them) and the final state, flat.
+int ref_solve_copy_matching(int32_t n_a, int32_t n_b, const int32_t* k, double ceps,
+                            int32_t unit_floor, int32_t unit_ceil, const int64_t* d,
+                            const int64_t* s, double eps, int32_t check, int64_t* flow,
+                            int64_t* free_counts, int64_t free_cap, int64_t* phase_flows,
+                            int64_t phase_cap, int64_t* phase_ni, int64_t* stats3,
+                            int32_t* dem_off, int64_t* dem_y, int64_t* dem_free, int64_t* flow_off,
+                            int32_t* flow_b, int64_t* flow_cnt, int32_t* sup_off, int64_t* sup_y,
+                            int64_t* sup_free, int64_t* sup_matched, int64_t cap, int64_t* sizes) {
+  return guarded([&] {
+    const otpr::CopyInstance ci = make_copy(n_a, n_b, k, ceps, unit_floor, unit_ceil, d, s);
+    otpr::ClusterOptions opt;
+    opt.check_invariants = check != 0;
+    const size_t nn = size_t(n_a) * n_b;
+    opt.observer = [&](const otpr::ClusterPhaseSnapshot& snap) {
+      if (snap.phase <= phase_cap) {
+        const auto f = snap.state.flow_matrix(n_a, n_b);
+        std::memcpy(phase_flows + (snap.phase - 1) * nn, f.data(), nn * 8);
+        phase_ni[snap.phase - 1] = snap.n_i;
+      }
+    };
+    const otpr::ClusterSolveResult r = otpr::solve_copy_matching(ci, eps, opt);
+    std::memcpy(flow, r.flow.data(), nn * 8);
+    const int64_t nf = static_cast<int64_t>(r.stats.free_counts.size());
+    std::memcpy(free_counts, r.stats.free_counts.data(), size_t(nf < free_cap ? nf : free_cap) * 8);
+    stats3[0] = r.stats.phases;
+    stats3[1] = r.stats.sum_ni;
+    stats3[2] = r.stats.full_match_termination ? 1 : 0;
+    flatten(r.state, dem_off, dem_y, dem_free, flow_off, flow_b, flow_cnt, sup_off, sup_y, sup_free,
+            sup_matched, cap, sizes);
+  });
+}
+
+// otpr::check_cluster_invariant (which 0) / check_cluster_feasibility (1) on a
+// flat state: violation count and the messages, newline-separated.
+int ref_check_cluster(int32_t n_a, int32_t n_b, const int32_t* k, int32_t unit_ceil,
+                      const int64_t* d, const int64_t* s, const int32_t* dem_off,
+                      const int64_t* dem_y, const int64_t* dem_free, const int64_t* flow_off,
+                      const int32_t* flow_b, const int64_t* flow_cnt, const int32_t* sup_off,
+                      const int64_t* sup_y, const int64_t* sup_free, const int64_t* sup_matched,
+                      int32_t which, int64_t* count, char* msgs, int32_t msgs_cap) {
+  return guarded([&] {
+    const otpr::CopyInstance ci = make_copy(n_a, n_b, k, 0.5, unit_ceil, unit_ceil, d, s);
+    otpr::ClusterState st;
+    st.demand.resize(n_a);
+    st.supply.resize(n_b);
+    for (int32_t a = 0; a < n_a; ++a)
+      for (int32_t c = dem_off[a]; c < dem_off[a + 1]; ++c) {
+        otpr::DemandCluster dc;
+        dc.y = dem_y[c];
+        dc.free_count = dem_free[c];
+        for (int64_t f = flow_off[c]; f < flow_off[c + 1]; ++f) dc.flow.emplace_back(flow_b[f], flow_cnt[f]);
+        st.demand[a].push_back(std::move(dc));
+      }
+    for (int32_t b = 0; b < n_b; ++b)
+      for (int32_t c = sup_off[b]; c < sup_off[b + 1]; ++c)
+        st.supply[b].push_back(otpr::SupplyCluster{sup_y[c], sup_free[c], sup_matched[c]});
+    const otpr::ClusterReport rep =
+        which == 0 ? otpr::check_cluster_invariant(st, ci) : otpr::check_cluster_feasibility(st, ci);
+    *count = static_cast<int64_t>(rep.violations.size());
+    std::string m;
+    for (const auto& x : rep.violations) m += (m.empty() ? "" : "\n") + x;
+    const size_t n = std::min(m.size(), static_cast<size_t>(msgs_cap - 1));
+    std::memcpy(msgs, m.data(), n);
+    msgs[n] = 0;
   });
 }
 

@@ -9,6 +9,9 @@ from .api import (  # noqa: F401
     scale_round_costs, scaled_floor, solve_assignment, OTInstance, TransportPlan, ScaledMasses,
     gen_random_ot_rational, scale_and_round, solve_ot, FeasibilityReport, PhaseSnapshot,
     PhaseWorkset, verify_feasibility, SinkhornConfig, SinkhornResult, sinkhorn, reg_for_eps,
+    CopyInstance, DemandCluster, SupplyCluster, ClusterState, ClusterReport, ClusterPhaseSnapshot,
+    ClusterOptions, OTOptions, ClusterSolveResult, check_cluster_invariant, check_cluster_feasibility,
+    solve_copy_matching, plan_from_flow, last_cluster_state,
 )
 
 __all__ = [
@@ -19,4 +22,8 @@ __all__ = [
     "solve_assignment", "OTInstance", "TransportPlan", "ScaledMasses", "gen_random_ot_rational",
     "scale_and_round", "solve_ot", "FeasibilityReport", "PhaseSnapshot", "PhaseWorkset",
     "verify_feasibility", "SinkhornConfig", "SinkhornResult", "sinkhorn", "reg_for_eps",
+    "CopyInstance", "DemandCluster", "SupplyCluster", "ClusterState", "ClusterReport",
+    "ClusterPhaseSnapshot", "ClusterOptions", "OTOptions", "ClusterSolveResult",
+    "check_cluster_invariant", "check_cluster_feasibility", "solve_copy_matching", "plan_from_flow",
+    "last_cluster_state",
 ]

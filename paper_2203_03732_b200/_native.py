@@ -18,7 +18,7 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "lib", os.environ.get("OTPRG_LIB", "libotprg.so"))
 CSRC = os.path.join(PKG_DIR, "csrc")
 
-OK, PARAMETER, INPUT, NUMERICAL, INVARIANT, DEVICE = 0, 2, 3, 4, 5, 6
+OK, PARAMETER, INPUT, NUMERICAL, INVARIANT, DEVICE, ABORTED = 0, 2, 3, 4, 5, 6, 7
 COST_DENSE_F64, COST_POINTS2D, COST_L1_U8 = 0, 1, 2
 STORAGE = {"auto": 0, "u8": 1, "u16": 2, "u32": 3}
 MAX_PHASES = 1 << 24  # OTPRG_MAX_PHASES
@@ -57,6 +57,37 @@ class Feasibility(C.Structure):
     ]
 
 
+class CopyInstance(C.Structure):
+    _fields_ = [("n_a", C.c_int32), ("n_b", C.c_int32), ("k", C.c_void_p), ("unit_ceil", C.c_int64),
+                ("demand_copies", C.c_void_p), ("supply_copies", C.c_void_p)]
+
+
+class ClusterState(C.Structure):
+    _fields_ = [("n_a", C.c_int32), ("n_b", C.c_int32), ("dem_off", C.c_void_p),
+                ("dem_y", C.c_void_p), ("dem_free", C.c_void_p), ("flow_off", C.c_void_p),
+                ("flow_b", C.c_void_p), ("flow_cnt", C.c_void_p), ("sup_off", C.c_void_p),
+                ("sup_y", C.c_void_p), ("sup_free", C.c_void_p), ("sup_matched", C.c_void_p)]
+
+
+class ClusterSnapshot(C.Structure):
+    _fields_ = [("phase", C.c_int64), ("n_i", C.c_int64), ("sum_abs_before", C.c_int64),
+                ("sum_abs_after", C.c_int64), ("inst", CopyInstance), ("state", ClusterState)]
+
+
+CLUSTER_OBSERVER = C.CFUNCTYPE(C.c_int, C.POINTER(ClusterSnapshot), C.c_void_p)
+
+
+class OTOptions(C.Structure):
+    _fields_ = [("check_invariants", C.c_int32), ("pad", C.c_int32),
+                ("observer", CLUSTER_OBSERVER), ("user", C.c_void_p)]
+
+
+class CopyResult(C.Structure):
+    _fields_ = [("flow", C.c_void_p), ("free_counts", C.c_void_p), ("free_cap", C.c_int64),
+                ("phases", C.c_int64), ("sum_ni", C.c_int64), ("full_match_termination", C.c_int32),
+                ("gpu_launches", C.c_int32)]
+
+
 EXPORTS = [
     "otprg_create", "otprg_destroy", "otprg_last_error", "otprg_version", "otprg_scaled_floor",
     "otprg_solve_assignment", "otprg_prepare", "otprg_solve_prepared", "otprg_scale_round_costs",
@@ -67,6 +98,8 @@ EXPORTS = [
     "otprg_shard_begin", "otprg_shard_top", "otprg_shard_scan", "otprg_shard_da",
     "otprg_shard_finish", "otprg_set_stream", "otprg_sinkhorn", "otprg_groups_begin",
     "otprg_groups_step", "otprg_groups_finish", "otprg_verify_feasibility", "otprg_verify_host", "otprg_admissible",
+    "otprg_solve_ot_opts", "otprg_solve_copy_matching", "otprg_copy_state",
+    "otprg_check_cluster_state", "otprg_plan_from_flow",
 ]
 
 _lib = None
@@ -113,6 +146,13 @@ def lib() -> C.CDLL:
     L.otprg_load_mnist_pair.argtypes = [C.c_char_p, C.c_int32, C.c_uint64, vp, vp, C.c_char_p,
                                         C.c_int32]
     L.otprg_solve_ot.argtypes = [vp, vp, vp]
+    L.otprg_solve_ot_opts.argtypes = [vp, vp, C.POINTER(OTOptions), vp]
+    L.otprg_solve_copy_matching.argtypes = [vp, C.POINTER(CopyInstance), C.c_double,
+                                            C.POINTER(OTOptions), C.POINTER(CopyResult)]
+    L.otprg_copy_state.argtypes = [vp, C.POINTER(ClusterState)]
+    L.otprg_check_cluster_state.argtypes = [C.POINTER(ClusterState), C.POINTER(CopyInstance),
+                                            C.c_int32, C.POINTER(C.c_int64), C.c_char_p, C.c_int32]
+    L.otprg_plan_from_flow.argtypes = [vp, vp, C.c_double, vp, vp, vp]
     L.otprg_ot_scale_and_round.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp,
                                            C.POINTER(C.c_double)]
     L.otprg_random_ot_rational.argtypes = [C.c_int32, C.c_int32, C.c_uint64, vp, vp, vp]

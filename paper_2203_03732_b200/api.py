@@ -50,7 +50,8 @@ class DeviceError(RuntimeError):
 
 
 _STATUS_EXC = {N.PARAMETER: ParameterError, N.INPUT: InputError, N.NUMERICAL: NumericalError,
-               N.INVARIANT: InvariantViolation, N.DEVICE: DeviceError}
+               N.INVARIANT: InvariantViolation, N.DEVICE: DeviceError,
+               N.ABORTED: DeviceError}  # (an observer's own exception is re-raised instead)
 
 
 # ---- data model (include/otpr/core.hpp) ----------------------------------
@@ -809,7 +810,295 @@ def scale_and_round(inst: OTInstance, eps: float) -> ScaledMasses:
     return ScaledMasses(th.value, d, s)
 
 
-def solve_ot(inst: OTInstance, eps: float, device: int = 0):
+# ---- copy/cluster solver types and hooks (ot.hpp:52-156) --------------------
+@dataclass
+class CopyInstance:
+    """ot.hpp:52-63: rounded costs over the original vertices + copy counts."""
+    costs: ScaledCosts
+    demand_copies: np.ndarray
+    supply_copies: np.ndarray
+
+    def total_demand(self) -> int:
+        return int(np.sum(self.demand_copies))
+
+    def total_supply(self) -> int:
+        return int(np.sum(self.supply_copies))
+
+    def _c(self):
+        k = np.ascontiguousarray(self.costs.k, np.int32)
+        d = np.ascontiguousarray(self.demand_copies, np.int64)
+        s = np.ascontiguousarray(self.supply_copies, np.int64)
+        if k.shape != (len(d), len(s)):
+            raise ParameterError("copy counts do not match the cost matrix")
+        ci = N.CopyInstance(k.shape[0], k.shape[1], k.ctypes.data, int(self.costs.unit_ceil),
+                            d.ctypes.data, s.ctypes.data)
+        return ci, (k, d, s)
+
+
+@dataclass
+class DemandCluster:
+    """ot.hpp:65-75: copies of a demand vertex at one dual; matched copies as
+    flow (b, copies), ascending b."""
+    y: int = 0
+    free_count: int = 0
+    flow: list = field(default_factory=list)
+
+    def matched(self) -> int:
+        return sum(c for _, c in self.flow)
+
+    def count(self) -> int:
+        return self.free_count + self.matched()
+
+
+@dataclass
+class SupplyCluster:
+    """ot.hpp:77-83."""
+    y: int = 0
+    free_count: int = 0
+    matched_count: int = 0
+
+    def count(self) -> int:
+        return self.free_count + self.matched_count
+
+
+@dataclass
+class ClusterState:
+    """ot.hpp:85-95: per vertex at most two live clusters."""
+    demand: list
+    supply: list
+
+    def flow_matrix(self, n_a: int, n_b: int) -> np.ndarray:
+        f = np.zeros((n_a, n_b), np.int64)
+        for a, cs in enumerate(self.demand):
+            for c in cs:
+                for b, cnt in c.flow:
+                    f[a, b] += cnt
+        return f
+
+    def free_supply_total(self) -> int:
+        return sum(c.free_count for cs in self.supply for c in cs)
+
+    def free_demand_of(self, a: int) -> int:
+        return sum(c.free_count for c in self.demand[a])
+
+    def sum_abs_duals(self) -> int:
+        return (sum(abs(c.y) * c.count() for cs in self.demand for c in cs)
+                + sum(abs(c.y) * c.count() for cs in self.supply for c in cs))
+
+    @staticmethod
+    def _from_c(st) -> "ClusterState":
+        n_a, n_b = st.n_a, st.n_b
+
+        def arr(ptr, n, ct):
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), (n,)).copy() if n else np.zeros(0)
+
+        dem_off = arr(st.dem_off, n_a + 1, C.c_int32)
+        nd = int(dem_off[-1])
+        dem_y, dem_free = arr(st.dem_y, nd, C.c_int64), arr(st.dem_free, nd, C.c_int64)
+        flow_off = arr(st.flow_off, nd + 1, C.c_int64)
+        nf = int(flow_off[-1])
+        flow_b, flow_cnt = arr(st.flow_b, nf, C.c_int32), arr(st.flow_cnt, nf, C.c_int64)
+        sup_off = arr(st.sup_off, n_b + 1, C.c_int32)
+        ns = int(sup_off[-1])
+        sup_y, sup_free = arr(st.sup_y, ns, C.c_int64), arr(st.sup_free, ns, C.c_int64)
+        sup_matched = arr(st.sup_matched, ns, C.c_int64)
+        demand = [[DemandCluster(int(dem_y[c]), int(dem_free[c]),
+                                 [(int(flow_b[f]), int(flow_cnt[f]))
+                                  for f in range(int(flow_off[c]), int(flow_off[c + 1]))])
+                   for c in range(int(dem_off[a]), int(dem_off[a + 1]))] for a in range(n_a)]
+        supply = [[SupplyCluster(int(sup_y[c]), int(sup_free[c]), int(sup_matched[c]))
+                   for c in range(int(sup_off[b]), int(sup_off[b + 1]))] for b in range(n_b)]
+        return ClusterState(demand, supply)
+
+    def _c(self):
+        dem_off, dem_y, dem_free, flow_off, flow_b, flow_cnt = [0], [], [], [0], [], []
+        for cs in self.demand:
+            for c in cs:
+                dem_y.append(c.y)
+                dem_free.append(c.free_count)
+                for b, cnt in c.flow:
+                    flow_b.append(b)
+                    flow_cnt.append(cnt)
+                flow_off.append(len(flow_b))
+            dem_off.append(len(dem_y))
+        sup_off, sup_y, sup_free, sup_matched = [0], [], [], []
+        for cs in self.supply:
+            for c in cs:
+                sup_y.append(c.y)
+                sup_free.append(c.free_count)
+                sup_matched.append(c.matched_count)
+            sup_off.append(len(sup_y))
+        keep = [np.asarray(dem_off, np.int32), np.asarray(dem_y, np.int64), np.asarray(dem_free, np.int64),
+                np.asarray(flow_off, np.int64), np.asarray(flow_b, np.int32), np.asarray(flow_cnt, np.int64),
+                np.asarray(sup_off, np.int32), np.asarray(sup_y, np.int64), np.asarray(sup_free, np.int64),
+                np.asarray(sup_matched, np.int64)]
+        st = N.ClusterState(len(self.demand), len(self.supply), *[x.ctypes.data for x in keep])
+        return st, keep
+
+
+@dataclass
+class ClusterReport:
+    """ot.hpp:97-100."""
+    violations: list = field(default_factory=list)
+
+    def ok(self) -> bool:
+        return not self.violations
+
+
+def _check_cluster(state: ClusterState, inst: CopyInstance, which: int) -> ClusterReport:
+    st, keep = state._c()
+    ci, keep2 = inst._c()
+    cnt = C.c_int64()
+    buf = C.create_string_buffer(1 << 16)
+    rc = N.lib().otprg_check_cluster_state(C.byref(st), C.byref(ci), which, C.byref(cnt), buf, len(buf))
+    if rc:
+        raise ParameterError("cluster state does not match the copy instance")
+    msgs = buf.value.decode().split("\n") if cnt.value else []
+    return ClusterReport(msgs[: cnt.value])
+
+
+def check_cluster_invariant(state: ClusterState, inst: CopyInstance) -> ClusterReport:
+    """ot.hpp:102-107 / ot.cpp:190-265."""
+    return _check_cluster(state, inst, 0)
+
+
+def check_cluster_feasibility(state: ClusterState, inst: CopyInstance) -> ClusterReport:
+    """ot.hpp:109-113 / ot.cpp:267-315."""
+    return _check_cluster(state, inst, 1)
+
+
+@dataclass
+class ClusterPhaseSnapshot:
+    """ot.hpp:115-122 (a copy: valid after the callback too)."""
+    phase: int
+    inst: CopyInstance
+    state: ClusterState
+    n_i: int
+    sum_abs_before: int
+    sum_abs_after: int
+
+
+@dataclass
+class ClusterOptions:
+    """ot.hpp:124-129 (and OTOptions, ot.hpp:153-156): after every phase the
+    greedy-maximality / cluster-invariant / feasibility checks (host), and an
+    observer called with a ClusterPhaseSnapshot."""
+    check_invariants: bool = False
+    observer: Optional[Callable] = None
+
+
+OTOptions = ClusterOptions
+
+
+@dataclass
+class ClusterSolveResult:
+    """ot.hpp:131-135: final state before completion, flow with completion."""
+    state: ClusterState
+    flow: np.ndarray
+    stats: SolveStats
+
+
+def _c_options(opt: Optional[ClusterOptions]):
+    """(N.OTOptions or None, the callback keep-alive, the error box)."""
+    if opt is None or (not opt.check_invariants and opt.observer is None):
+        return None, None, None
+    err = []
+    cb = N.CLUSTER_OBSERVER()  # NULL
+    if opt.observer is not None:
+        cache = {}
+
+        def _obs(snap_p, _user):
+            try:
+                sn = snap_p.contents
+                if "inst" not in cache:  # the copy instance does not change between phases
+                    ci = sn.inst
+                    k = np.ctypeslib.as_array(C.cast(ci.k, C.POINTER(C.c_int32)), (ci.n_a, ci.n_b)).copy()
+                    d = np.ctypeslib.as_array(C.cast(ci.demand_copies, C.POINTER(C.c_int64)), (ci.n_a,)).copy()
+                    s = np.ctypeslib.as_array(C.cast(ci.supply_copies, C.POINTER(C.c_int64)), (ci.n_b,)).copy()
+                    cache["inst"] = CopyInstance(ScaledCosts(0.0, k, int(ci.unit_ceil), int(ci.unit_ceil)), d, s)
+                opt.observer(ClusterPhaseSnapshot(int(sn.phase), cache["inst"], ClusterState._from_c(sn.state),
+                                                  int(sn.n_i), int(sn.sum_abs_before), int(sn.sum_abs_after)))
+                return 0
+            except BaseException as e:  # re-raised by the caller after the C call returns
+                err.append(e)
+                return 1
+
+        cb = N.CLUSTER_OBSERVER(_obs)
+    o = N.OTOptions(int(bool(opt.check_invariants)), 0, cb, None)
+    return o, cb, err
+
+
+def _raise_opts(solver, st: int, err):
+    if st == N.ABORTED and err:
+        raise err[0]
+    solver._raise(st)
+
+
+def solve_copy_matching(inst: CopyInstance, eps: float, opt: Optional[ClusterOptions] = None,
+                        device: int = 0) -> ClusterSolveResult:
+    """ot.hpp:135-141 / ot.cpp:418-637 on the device (admissible-cluster
+    scans) with the claim step and cluster bookkeeping on the host."""
+    ci, keep = inst._c()
+    n_a, n_b = ci.n_a, ci.n_b
+    solver = get_solver(device)
+    o, cb, err = _c_options(opt)
+    fcap = min(SolveStats.phase_bound(eps) + 16, N.MAX_PHASES + 2) if 0.0 < eps < 1.0 else 16
+    fc = np.zeros(fcap, np.int64)
+    flow = np.zeros((n_a, n_b), np.int64)
+    r = N.CopyResult(flow.ctypes.data, fc.ctypes.data, fcap, 0, 0, 0, 0)
+    st = solver._L.otprg_solve_copy_matching(solver._ctx, C.byref(ci), float(eps),
+                                             C.byref(o) if o is not None else None, C.byref(r))
+    if st:
+        _raise_opts(solver, st, err)
+    cs = N.ClusterState()
+    st = solver._L.otprg_copy_state(solver._ctx, C.byref(cs))
+    if st:
+        solver._raise(st)
+    stats = SolveStats(phases=int(r.phases), free_counts=fc[: r.phases].copy(), sum_ni=int(r.sum_ni),
+                       full_match_termination=bool(r.full_match_termination),
+                       device=dict(gpu_launches=int(r.gpu_launches)))
+    return ClusterSolveResult(ClusterState._from_c(cs), flow, stats)
+
+
+def plan_from_flow(flow: np.ndarray, sm: ScaledMasses, inst: OTInstance) -> TransportPlan:
+    """ot.hpp:143-151 / ot.cpp:639-703 (host, the reference's FP64 order)."""
+    mu = np.ascontiguousarray(inst.mu, np.float64)
+    nu = np.ascontiguousarray(inst.nu, np.float64)
+    cost = np.ascontiguousarray(inst.cost, np.float64)
+    f = np.ascontiguousarray(flow, np.int64)
+    if f.shape != (len(mu), len(nu)) or cost.shape != f.shape:
+        raise ParameterError("flow matrix dimensions do not match the instance")
+    p = _OTProblem(len(mu), len(nu), 0.5, mu.ctypes.data, nu.ctypes.data, cost.ctypes.data, 0, 0)
+    cap = int(np.count_nonzero(f)) + len(mu) + len(nu) + 16
+    while True:
+        ea, eb, em = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap)
+        r = _OTResult()
+        r.ent_a, r.ent_b, r.ent_mass, r.entry_cap = ea.ctypes.data, eb.ctypes.data, em.ctypes.data, cap
+        d = np.ascontiguousarray(sm.d, np.int64)
+        s = np.ascontiguousarray(sm.s, np.int64)
+        st = N.lib().otprg_plan_from_flow(C.byref(p), f.ctypes.data, float(sm.theta), d.ctypes.data,
+                                          s.ctypes.data, C.byref(r))
+        if st:
+            raise _STATUS_EXC.get(st, DeviceError)("plan_from_flow failed")
+        if r.n_entries <= cap:
+            break
+        cap = int(r.n_entries)
+    ne = int(r.n_entries)
+    return TransportPlan(ea[:ne].copy(), eb[:ne].copy(), em[:ne].copy(), float(r.cost))
+
+
+def last_cluster_state(device: int = 0) -> ClusterState:
+    """ClusterSolveResult::state of the last solve_ot / solve_copy_matching on
+    this device's shared solver (the state before completion)."""
+    solver = get_solver(device)
+    cs = N.ClusterState()
+    st = solver._L.otprg_copy_state(solver._ctx, C.byref(cs))
+    if st:
+        solver._raise(st)
+    return ClusterState._from_c(cs)
+
+
+def solve_ot(inst: OTInstance, eps: float, opt: Optional[OTOptions] = None, device: int = 0):
     """ot.hpp:161-163 / ot.cpp:705-732 -> (TransportPlan, SolveStats)."""
     mu = np.ascontiguousarray(inst.mu, np.float64)
     nu = np.ascontiguousarray(inst.nu, np.float64)
@@ -819,7 +1108,10 @@ def solve_ot(inst: OTInstance, eps: float, device: int = 0):
     solver = get_solver(device)
     p = _OTProblem(len(mu), len(nu), float(eps), mu.ctypes.data, nu.ctypes.data, cost.ctypes.data,
                    0, 0)
+    o, cb, err = _c_options(opt)
     cap = 4 * (len(mu) + len(nu)) + 64
+    if o is not None:  # hooks run once: room for any plan (debug sizes)
+        cap = max(cap, len(mu) * len(nu))
     fcap = (min(SolveStats.phase_bound(eps / 3.0) + 16, N.MAX_PHASES + 2)
             if 0.0 < eps < 1.0 else 16)  # C ABI validates eps
     ea, eb, em = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap)
@@ -827,9 +1119,10 @@ def solve_ot(inst: OTInstance, eps: float, device: int = 0):
     r = _OTResult()
     r.ent_a, r.ent_b, r.ent_mass, r.entry_cap = ea.ctypes.data, eb.ctypes.data, em.ctypes.data, cap
     r.free_counts, r.free_cap = fc.ctypes.data, fcap
-    st = solver._L.otprg_solve_ot(solver._ctx, C.byref(p), C.byref(r))
+    st = solver._L.otprg_solve_ot_opts(solver._ctx, C.byref(p), C.byref(o) if o is not None else None,
+                                       C.byref(r))
     if st:
-        solver._raise(st)
+        _raise_opts(solver, st, err)
     if r.n_entries > cap:  # rerun with room for every entry
         cap = int(r.n_entries)
         ea, eb, em = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap)

@@ -186,6 +186,25 @@ __global__ void __launch_bounds__(256) l1_round_kernel(const double* __restrict_
   }
 }
 
+// A given rounded-cost matrix (copy instances, ot.hpp:52-63): k[a][b]
+// row-major int32 -> kT[b][a] (32x32 shared-memory transpose), pads = type max.
+template <typename T>
+__global__ void k_to_kT_kernel(const int32_t* __restrict__ k, int n_a, int n_b, T* __restrict__ kT,
+                               int lda) {
+  __shared__ T tile[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const int a0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  for (int r = ty; r < 32; r += 8) {
+    const int a = a0 + r, b = b0 + tx;
+    tile[r][tx] = (a < n_a && b < n_b) ? (T)k[(size_t)a * n_b + b] : (T)type_max<T>();
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int b = b0 + r, a = a0 + tx;
+    if (b < n_b && a < lda) kT[(size_t)b * lda + a] = tile[tx][r];
+  }
+}
+
 template <typename T>
 __global__ void export_k_kernel(const T* __restrict__ kT, int n_ai, int n_bi, int lda,
                                 int swapped, int32_t* __restrict__ k) {
@@ -250,6 +269,17 @@ cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_
   with_width(width, [&](auto tag) {
     using T = decltype(tag);
     l1_round_kernel<T><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps, static_cast<T*>(kT), lda, status);
+    return 0;
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k_to_kT(const int32_t* k, int n_a, int n_b, void* kT, int lda, int width,
+                           cudaStream_t s) {
+  dim3 block(32, 8), grid((lda + 31) / 32, (n_b + 31) / 32);
+  with_width(width, [&](auto tag) {
+    using T = decltype(tag);
+    k_to_kT_kernel<T><<<grid, block, 0, s>>>(k, n_a, n_b, static_cast<T*>(kT), lda);
     return 0;
   });
   return cudaGetLastError();

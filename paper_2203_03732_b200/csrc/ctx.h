@@ -2,6 +2,7 @@
 #pragma once
 #include <cmath>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -121,5 +122,6 @@ struct otprg_ctx {
   // optimal transport (ot_host.cpp): per-phase scan inputs / outputs
   DevBuf ot_t, ot_req, ot_out;
   void* ot_hpin = nullptr;
+  std::shared_ptr<void> ot_state;  // flat ClusterState of the last copy/cluster solve (ot_host.cpp)
   size_t ot_hpin_n = 0;
 };

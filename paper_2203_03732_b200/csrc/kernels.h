@@ -66,6 +66,8 @@ cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_
                             double eps, void* kT, int lda, int width, int* status, cudaStream_t s);
 // Rounded matrix back to int32 row-major in the ORIGINAL orientation (for
 // otprg_scale_round_costs).
+cudaError_t launch_k_to_kT(const int32_t* k, int n_a, int n_b, void* kT, int lda, int width,
+                           cudaStream_t s);
 cudaError_t launch_export_k(const void* kT, int n_ai, int n_bi, int lda, int width, bool swapped,
                             int32_t* k_out, cudaStream_t s);
 

@@ -237,9 +237,177 @@ ScaledMasses scale_and_round(const otprg_ot_problem* p, double eps) {  // ot.cpp
   return sm;
 }
 
+// ---- flat ClusterState (otprg_cluster_state) and the reference's checks ----
+
+struct FlatState {
+  int32_t n_a = 0, n_b = 0;
+  std::vector<int32_t> dem_off, flow_b, sup_off;
+  std::vector<int64_t> dem_y, dem_free, flow_off, flow_cnt, sup_y, sup_free, sup_matched;
+
+  void build(const std::vector<std::vector<DemandC>>& dem, const std::vector<std::vector<SupplyC>>& sup) {
+    n_a = static_cast<int32_t>(dem.size());
+    n_b = static_cast<int32_t>(sup.size());
+    dem_off.assign(1, 0);
+    sup_off.assign(1, 0);
+    flow_off.assign(1, 0);
+    dem_y.clear(), dem_free.clear(), flow_b.clear(), flow_cnt.clear();
+    sup_y.clear(), sup_free.clear(), sup_matched.clear();
+    for (const auto& cs : dem) {
+      for (const DemandC& c : cs) {
+        dem_y.push_back(c.y);
+        dem_free.push_back(c.free);
+        for (const auto& e : c.flow) flow_b.push_back(e.first), flow_cnt.push_back(e.second);
+        flow_off.push_back(static_cast<int64_t>(flow_b.size()));
+      }
+      dem_off.push_back(static_cast<int32_t>(dem_y.size()));
+    }
+    for (const auto& cs : sup) {
+      for (const SupplyC& c : cs) sup_y.push_back(c.y), sup_free.push_back(c.free), sup_matched.push_back(c.matched);
+      sup_off.push_back(static_cast<int32_t>(sup_y.size()));
+    }
+  }
+  otprg_cluster_state view() const {
+    return otprg_cluster_state{n_a,          n_b,          dem_off.data(), dem_y.data(),  dem_free.data(),
+                               flow_off.data(), flow_b.data(), flow_cnt.data(), sup_off.data(), sup_y.data(),
+                               sup_free.data(), sup_matched.data()};
+  }
+};
+
+int64_t sum_abs_duals(const std::vector<std::vector<DemandC>>& dem,
+                      const std::vector<std::vector<SupplyC>>& sup) {  // ot.cpp:181-188
+  int64_t t = 0;
+  for (const auto& cs : dem)
+    for (const DemandC& c : cs) t += std::llabs(c.y) * c.count();
+  for (const auto& cs : sup)
+    for (const SupplyC& c : cs) t += std::llabs(c.y) * c.count();
+  return t;
+}
+
+// check_cluster_invariant (ot.cpp:190-265) on the flat form.
+std::vector<std::string> check_invariant(const otprg_cluster_state& st, const otprg_copy_instance& in) {
+  std::vector<std::string> v;
+  auto fail = [&](std::string m) { v.push_back(std::move(m)); };
+  const int64_t bound = in.unit_ceil + 2;
+  auto dem_count = [&](int32_t c) {
+    int64_t t = st.dem_free[c];
+    for (int64_t f = st.flow_off[c]; f < st.flow_off[c + 1]; ++f) t += st.flow_cnt[f];
+    return t;
+  };
+  for (int32_t a = 0; a < st.n_a; ++a) {
+    std::vector<int64_t> values;
+    int64_t total = 0;
+    const std::string at = std::to_string(a);
+    for (int32_t c = st.dem_off[a]; c < st.dem_off[a + 1]; ++c) {
+      const int64_t cnt = dem_count(c), y = st.dem_y[c];
+      if (cnt == 0) continue;
+      values.push_back(y);
+      total += cnt;
+      if (y > 0) fail("demand cluster with positive dual at a=" + at);
+      if (std::llabs(y) > bound) fail("demand cluster dual exceeds magnitude bound at a=" + at);
+      if (st.dem_free[c] > 0 && y != 0) fail("free demand copies away from dual zero at a=" + at);
+      for (int64_t f = st.flow_off[c]; f < st.flow_off[c + 1]; ++f)
+        if (st.flow_b[f] < 0 || st.flow_b[f] >= st.n_b || st.flow_cnt[f] <= 0)
+          fail("bad flow entry at a=" + at);
+    }
+    std::sort(values.begin(), values.end());
+    values.erase(std::unique(values.begin(), values.end()), values.end());
+    if (values.size() > 2) fail("more than two distinct duals among copies of a=" + at);
+    if (total != in.demand_copies[a]) fail("demand copy count mismatch at a=" + at);
+  }
+  for (int32_t b = 0; b < st.n_b; ++b) {
+    std::vector<int64_t> values;
+    int64_t total = 0, free_clusters = 0;
+    int64_t max_y = std::numeric_limits<int64_t>::min();
+    const std::string at = std::to_string(b);
+    for (int32_t c = st.sup_off[b]; c < st.sup_off[b + 1]; ++c) {
+      const int64_t cnt = st.sup_free[c] + st.sup_matched[c], y = st.sup_y[c];
+      if (cnt == 0) continue;
+      values.push_back(y);
+      total += cnt;
+      max_y = std::max(max_y, y);
+      if (y < 0) fail("supply cluster with negative dual at b=" + at);
+      if (std::llabs(y) > bound) fail("supply cluster dual exceeds magnitude bound at b=" + at);
+      if (st.sup_free[c] > 0) ++free_clusters;
+    }
+    std::sort(values.begin(), values.end());
+    values.erase(std::unique(values.begin(), values.end()), values.end());
+    if (values.size() > 2) fail("more than two distinct duals among copies of b=" + at);
+    if (total != in.supply_copies[b]) fail("supply copy count mismatch at b=" + at);
+    if (free_clusters > 1) fail("free supply copies split across duals at b=" + at);
+    for (int32_t c = st.sup_off[b]; c < st.sup_off[b + 1]; ++c)
+      if (st.sup_free[c] + st.sup_matched[c] > 0 && st.sup_free[c] > 0 && st.sup_y[c] != max_y)
+        fail("free supply copies below their vertex maximum dual at b=" + at);
+  }
+  std::vector<int64_t> inbound(st.n_b, 0);
+  for (int32_t c = 0; c < st.dem_off[st.n_a]; ++c)
+    for (int64_t f = st.flow_off[c]; f < st.flow_off[c + 1]; ++f)
+      if (st.flow_b[f] >= 0 && st.flow_b[f] < st.n_b) inbound[st.flow_b[f]] += st.flow_cnt[f];
+  for (int32_t b = 0; b < st.n_b; ++b) {
+    int64_t matched = 0;
+    for (int32_t c = st.sup_off[b]; c < st.sup_off[b + 1]; ++c) matched += st.sup_matched[c];
+    if (inbound[b] != matched)
+      fail("flow into b=" + std::to_string(b) + " disagrees with matched supply count");
+  }
+  return v;
+}
+
+// check_cluster_feasibility (ot.cpp:267-315) on the flat form.
+std::vector<std::string> check_feasibility(const otprg_cluster_state& st, const otprg_copy_instance& in) {
+  std::vector<std::string> v;
+  auto k = [&](int32_t a, int32_t b) { return static_cast<int64_t>(in.k[static_cast<size_t>(a) * in.n_b + b]); };
+  // matched copy pairs are tight: expected[b][partner dual] from the flows
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> expected(st.n_b), actual(st.n_b);
+  auto add = [](std::vector<std::pair<int64_t, int64_t>>& m, int64_t y, int64_t c) {
+    for (auto& e : m)
+      if (e.first == y) {
+        e.second += c;
+        return;
+      }
+    m.emplace_back(y, c);
+  };
+  for (int32_t a = 0; a < st.n_a; ++a)
+    for (int32_t c = st.dem_off[a]; c < st.dem_off[a + 1]; ++c)
+      for (int64_t f = st.flow_off[c]; f < st.flow_off[c + 1]; ++f)
+        add(expected[st.flow_b[f]], k(a, st.flow_b[f]) - st.dem_y[c], st.flow_cnt[f]);
+  for (int32_t b = 0; b < st.n_b; ++b) {
+    for (int32_t c = st.sup_off[b]; c < st.sup_off[b + 1]; ++c)
+      if (st.sup_matched[c] > 0) add(actual[b], st.sup_y[c], st.sup_matched[c]);
+    auto& e = expected[b];
+    auto& x = actual[b];
+    std::sort(e.begin(), e.end());
+    std::sort(x.begin(), x.end());
+    if (e != x) v.push_back("matched copies of b=" + std::to_string(b) + " are not tight against their partners");
+  }
+  // unmatched cross pairs respect the dual-sum allowance
+  for (int32_t a = 0; a < st.n_a; ++a)
+    for (int32_t c = st.dem_off[a]; c < st.dem_off[a + 1]; ++c) {
+      int64_t cnt_a = st.dem_free[c];
+      for (int64_t f = st.flow_off[c]; f < st.flow_off[c + 1]; ++f) cnt_a += st.flow_cnt[f];
+      if (cnt_a == 0) continue;
+      const int64_t ya = st.dem_y[c];
+      for (int32_t b = 0; b < st.n_b; ++b) {
+        const int64_t kk = k(a, b);
+        for (int32_t d = st.sup_off[b]; d < st.sup_off[b + 1]; ++d) {
+          const int64_t cnt_b = st.sup_free[d] + st.sup_matched[d];
+          if (cnt_b == 0) continue;
+          int64_t cross = 0;
+          if (kk - ya == st.sup_y[d])
+            for (int64_t f = st.flow_off[c]; f < st.flow_off[c + 1]; ++f)
+              if (st.flow_b[f] == b) cross = st.flow_cnt[f];
+          if (cnt_a * cnt_b > cross && ya + st.sup_y[d] > kk + 1)
+            v.push_back("dual-sum allowance violated between copies of a=" + std::to_string(a) +
+                        " and b=" + std::to_string(b));
+        }
+      }
+    }
+  return v;
+}
+
 class OtSolver {
  public:
-  OtSolver(otprg_ctx* ctx, const otprg_ot_problem* p, otprg_ot_result* r) : ctx_(ctx), p_(p), r_(r) {}
+  OtSolver(otprg_ctx* ctx, const otprg_ot_problem* p, otprg_ot_result* r,
+           const otprg_ot_options* opt = nullptr)
+      : ctx_(ctx), p_(p), r_(r), opt_(opt) {}
 
   void run() {
     Timer total;
@@ -250,7 +418,14 @@ class OtSolver {
     n_a_ = p_->n_a;
     n_b_ = p_->n_b;
     build_costs();
+    if (debug()) {  // the CopyInstance the hooks see: k at eps/3 on the host
+      hk_store_.resize(static_cast<size_t>(n_a_) * n_b_);
+      for (size_t i = 0; i < hk_store_.size(); ++i)
+        hk_store_[i] = static_cast<int32_t>(host_scaled_floor(p_->cost[i], eps_in_));
+      hk_ = hk_store_.data();
+    }
     solve_copy_matching();
+    save_state();
     plan_from_flow();
     r_->theta = sm_.theta;
     r_->total_d = sm_.total_d;
@@ -258,20 +433,105 @@ class OtSolver {
     r_->solve_ms = total.ms();
   }
 
+  // solve_copy_matching on a given copy instance (ot.cpp:418-637).
+  void run_copy(const otprg_copy_instance* ci, double eps, otprg_copy_result* cr) {
+    if (!ci || !ci->k || !ci->demand_copies || !ci->supply_copies || ci->n_a < 0 || ci->n_b < 0)
+      throw OtError{OTPRG_PARAMETER, "copy counts do not match the cost matrix"};
+    int64_t td = 0, ts = 0;
+    for (int32_t a = 0; a < ci->n_a; ++a) {
+      if (ci->demand_copies[a] < 0) throw OtError{OTPRG_PARAMETER, "negative demand copy count"};
+      td += ci->demand_copies[a];
+    }
+    for (int32_t b = 0; b < ci->n_b; ++b) {
+      if (ci->supply_copies[b] < 0) throw OtError{OTPRG_PARAMETER, "negative supply copy count"};
+      ts += ci->supply_copies[b];
+    }
+    if (ts > td) throw OtError{OTPRG_PARAMETER, "copy instance needs total supply <= total demand"};
+    if (!(eps > 0.0 && eps < 1.0)) throw OtError{OTPRG_PARAMETER, "eps must lie in (0, 1)"};
+    n_a_ = ci->n_a;
+    n_b_ = ci->n_b;
+    eps_in_ = eps;
+    sm_.theta = 0.0;
+    sm_.d.assign(ci->demand_copies, ci->demand_copies + n_a_);
+    sm_.s.assign(ci->supply_copies, ci->supply_copies + n_b_);
+    sm_.total_d = td;
+    sm_.total_s = ts;
+    hk_ = ci->k;
+    unit_ceil_ = ci->unit_ceil;
+    otprg_ot_result tmp{};
+    tmp.free_counts = cr->free_counts;
+    tmp.free_cap = cr->free_cap;
+    r_ = &tmp;
+    if (n_a_ > 0 && n_b_ > 0) {
+      build_costs_from_k();
+      solve_copy_matching();
+    } else {  // nothing to match: the loop ends at once (n_i = 0)
+      dem_.assign(n_a_, {});
+      sup_.assign(n_b_, {});
+      flow_.assign(n_a_, {});
+      tmp.full_match_termination = 1;
+    }
+    save_state();
+    cr->phases = tmp.phases;
+    cr->sum_ni = tmp.sum_ni;
+    cr->full_match_termination = tmp.full_match_termination;
+    cr->gpu_launches = tmp.gpu_launches;
+    if (cr->flow) {
+      std::memset(cr->flow, 0, static_cast<size_t>(n_a_) * n_b_ * 8);
+      for (int32_t a = 0; a < n_a_; ++a)
+        for (const auto& [b, f] : flow_[a]) cr->flow[static_cast<size_t>(a) * n_b_ + b] = f;
+    }
+  }
+
+  // plan_from_flow alone on a dense flow (ot.cpp:639-703).
+  void run_plan(const int64_t* flow, double theta) {
+    if (!p_->mu || !p_->nu || !p_->cost || p_->n_a < 0 || p_->n_b < 0)
+      throw OtError{OTPRG_PARAMETER, "flow matrix dimensions do not match the instance"};
+    n_a_ = p_->n_a;
+    n_b_ = p_->n_b;
+    sm_.theta = theta;
+    flow_.assign(n_a_, {});
+    for (int32_t a = 0; a < n_a_; ++a)
+      for (int32_t b = 0; b < n_b_; ++b) {
+        const int64_t f = flow[static_cast<size_t>(a) * n_b_ + b];
+        if (f < 0) throw OtError{OTPRG_PARAMETER, "negative flow entry"};
+        if (f > 0) flow_[a].emplace_back(b, f);
+      }
+    plan_from_flow();
+  }
+
  private:
   otprg_ctx* ctx_;
   const otprg_ot_problem* p_;
   otprg_ot_result* r_;
+  const otprg_ot_options* opt_;
   double eps_in_ = 0.0;
   ScaledMasses sm_;
   int32_t n_a_ = 0, n_b_ = 0;
   int width_ = 2, lda_ = 0;
+  int64_t unit_ceil_ = 0;                // dual bound - 2 of the hooks' CopyInstance
+  const int32_t* hk_ = nullptr;          // host k (copy instance / debug mode), row-major
+  std::vector<int32_t> hk_store_;
   std::vector<std::vector<DemandC>> dem_;
   std::vector<std::vector<SupplyC>> sup_;
   std::vector<std::vector<std::pair<int32_t, int64_t>>> flow_;  // final sparse flow per a
 
+  bool debug() const { return opt_ && (opt_->check_invariants || opt_->observer); }
+
   int64_t k_of(int32_t a, int32_t b) const {
+    if (hk_) return hk_[static_cast<size_t>(a) * n_b_ + b];
     return host_scaled_floor(p_->cost[static_cast<size_t>(a) * n_b_ + b], eps_in_);
+  }
+
+  otprg_copy_instance copy_instance() const {
+    return otprg_copy_instance{n_a_, n_b_, hk_, unit_ceil_, sm_.d.data(), sm_.s.data()};
+  }
+
+  // ClusterSolveResult::state (before completion) kept on the context.
+  void save_state() {
+    auto fs = std::make_shared<FlatState>();
+    fs->build(dem_, sup_);
+    ctx_->ot_state = fs;
   }
 
   // scale_round_costs(costs, eps/3) on the device (core.cpp:34-53), kT[b][a].
@@ -282,6 +542,7 @@ class OtSolver {
     if (uf + 4 > std::numeric_limits<int32_t>::max())
       throw OtError{OTPRG_PARAMETER, "eps too small: 1/eps overflows the cost unit type"};
     const int64_t uc = static_cast<double>(uf) * eps_in_ == 1.0 ? uf : uf + 1;
+    unit_ceil_ = uc;
     width_ = otprg::storage_width(uc + 2, OTPRG_STORAGE_AUTO);
     if (width_ < 0) throw OtError{OTPRG_PARAMETER, "eps too small for the device cost storage"};
     const int align = 512 / width_;
@@ -304,6 +565,36 @@ class OtSolver {
     if (dstatus) throw OtError{OTPRG_PARAMETER, "OT cost entry outside [0,1]"};
     launches_ += 1;
     r_->build_ms = t.ms();
+    alloc_scan_buffers();
+  }
+
+  // The copy instance's k (host int32, row-major) -> kT on the device.
+  void build_costs_from_k() {
+    Timer t;
+    int64_t kmax = 0;
+    const size_t nn = static_cast<size_t>(n_a_) * n_b_;
+    for (size_t i = 0; i < nn; ++i) {
+      if (hk_[i] < 0) throw OtError{OTPRG_PARAMETER, "negative rounded cost in the copy instance"};
+      kmax = std::max<int64_t>(kmax, hk_[i]);
+    }
+    width_ = otprg::storage_width(std::max(kmax, unit_ceil_) + 2, OTPRG_STORAGE_AUTO);
+    if (width_ < 0) throw OtError{OTPRG_PARAMETER, "rounded costs beyond the device cost storage"};
+    const int align = 512 / width_;
+    lda_ = (n_a_ + align - 1) / align * align;
+    OT_CK(cudaSetDevice(ctx_->device), "cudaSetDevice");
+    OT_CK(ctx_->stage.ensure(nn * 4), "alloc k staging");
+    OT_CK(ctx_->kT.ensure(static_cast<size_t>(n_b_) * lda_ * width_), "alloc kT");
+    OT_CK(ctx_->ctl.ensure(sizeof(otprg::Ctl)), "alloc ctl");
+    OT_CK(otprg::h2d_large(ctx_, ctx_->stage.p, hk_, nn * 4), "H2D k");
+    OT_CK(otprg::launch_k_to_kT(ctx_->stage.as<int32_t>(), n_a_, n_b_, ctx_->kT.p, lda_, width_, ctx_->stream),
+          "k_to_kT launch");
+    OT_CK(cudaStreamSynchronize(ctx_->stream), "k upload");
+    launches_ += 1;
+    r_->build_ms = t.ms();
+    alloc_scan_buffers();
+  }
+
+  void alloc_scan_buffers() {
     // per-phase scan buffers: t0/t1 (2 x lda) + requests + candidates
     OT_CK(ctx_->ot_t.ensure(2 * static_cast<size_t>(lda_) * width_), "alloc t");
     OT_CK(ctx_->ot_req.ensure(static_cast<size_t>(n_b_) * sizeof(int4)), "alloc req");
@@ -357,6 +648,7 @@ class OtSolver {
   void upload_cluster_duals() {
     char* hp = static_cast<char*>(ctx_->ot_hpin);
     const uint32_t none = width_ == 1 ? 0xffu : width_ == 2 ? 0xffffu : 0xffffffffu;
+    const int64_t tmax = otprg::storage_tmax(width_);
     auto put = [&](size_t i, uint32_t v) {
       if (width_ == 1) reinterpret_cast<uint8_t*>(hp)[i] = static_cast<uint8_t>(v);
       else if (width_ == 2) reinterpret_cast<uint16_t*>(hp)[i] = static_cast<uint16_t>(v);
@@ -368,6 +660,8 @@ class OtSolver {
         const auto& cs = dem_[a];
         if (cs.size() >= 1) v0 = static_cast<uint32_t>(-cs[0].y);
         if (cs.size() >= 2) v1 = static_cast<uint32_t>(-cs[1].y);
+        if ((cs.size() >= 1 && -cs[0].y > tmax) || (cs.size() >= 2 && -cs[1].y > tmax))
+          throw OtError{OTPRG_INVARIANT, "demand dual beyond the device storage at a=" + std::to_string(a)};
       }
       put(a, v0);
       put(static_cast<size_t>(lda_) + a, v1);
@@ -411,6 +705,7 @@ class OtSolver {
         break;
       }
       const int32_t stamp = static_cast<int32_t>(phases);
+      const int64_t sum_before = opt_ && opt_->observer ? sum_abs_duals(dem_, sup_) : 0;
 
       // free supply vertices (ascending) and their free-copy duals
       free_bs.clear();
@@ -488,6 +783,21 @@ class OtSolver {
         matched_from_b[b] = remaining_free[b] - remaining;
         remaining_free[b] = remaining;
       }
+      if (opt_ && opt_->check_invariants) {
+        // greedy maximality (ot.cpp:524-533): a supply vertex keeps free
+        // copies only when every admissible demand cluster was used up
+        for (int32_t b : free_bs) {
+          if (remaining_free[b] == 0) continue;
+          for (int32_t a = 0; a < n_a_; ++a)
+            for (size_t ci = 0; ci < dem_[a].size() && ci < 2; ++ci) {
+              const DemandC& c = dem_[a][ci];
+              const Cursor& cu = cur[a][ci];
+              const int64_t avail = c.free + c.matched() - (cu.stamp == stamp ? cu.used : 0);
+              if (c.y == k_of(a, b) + 1 - free_dual[b] && avail > 0)
+                throw OtError{OTPRG_INVARIANT, "greedy step left an admissible pair unmatched"};
+            }
+        }
+      }
 
       // supply side: claimed copies become matched at their dual, the
       // phase's leftover free copies go up a unit (ot.cpp:540-553)
@@ -530,6 +840,7 @@ class OtSolver {
       phases += 1;
       free_counts.push_back(n_i);
       sum_ni += n_i;
+      if (debug()) phase_hooks(phases, n_i, sum_before);
       if (phases > phase_cap)
         throw OtError{OTPRG_INVARIANT, "phase count exceeded the proven bound; solver state is corrupt"};
     }
@@ -569,6 +880,25 @@ class OtSolver {
         need -= take;
         a_spare -= take;
       }
+    }
+  }
+
+  // check_invariants / observer after a phase (ot.cpp:594-608).
+  void phase_hooks(int64_t phase, int64_t n_i, int64_t sum_before) {
+    FlatState fs;
+    fs.build(dem_, sup_);
+    const otprg_cluster_state st = fs.view();
+    const otprg_copy_instance in = copy_instance();
+    if (opt_->check_invariants) {
+      for (int which = 0; which < 2; ++which) {
+        const auto v = which == 0 ? check_invariant(st, in) : check_feasibility(st, in);
+        if (!v.empty()) throw OtError{OTPRG_INVARIANT, "phase " + std::to_string(phase) + ": " + v.front()};
+      }
+    }
+    if (opt_->observer) {
+      const otprg_cluster_snapshot snap{phase, n_i, sum_before, sum_abs_duals(dem_, sup_), in, st};
+      if (opt_->observer(&snap, opt_->user) != 0)
+        throw OtError{OTPRG_ABORTED, "observer stopped the solve at phase " + std::to_string(phase)};
     }
   }
 
@@ -835,6 +1165,22 @@ void run_sinkhorn(otprg_ctx* ctx, const otprg_ot_problem* p, const otprg_sinkhor
 
 }  // namespace
 
+namespace {
+template <typename F>
+int guarded(otprg_ctx* ctx, F&& f) {
+  try {
+    f();
+    return OTPRG_OK;
+  } catch (const OtError& e) {
+    ctx->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return OTPRG_DEVICE;
+  }
+}
+}  // namespace
+
 extern "C" {
 
 int otprg_ot_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const double* nu,
@@ -858,20 +1204,66 @@ int otprg_ot_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const d
 }
 
 int otprg_solve_ot(otprg_ctx* ctx, const otprg_ot_problem* prob, otprg_ot_result* res) {
+  return otprg_solve_ot_opts(ctx, prob, nullptr, res);
+}
+
+int otprg_solve_ot_opts(otprg_ctx* ctx, const otprg_ot_problem* prob, const otprg_ot_options* opt,
+                        otprg_ot_result* res) {
   if (!ctx) return OTPRG_PARAMETER;
   if (!res || (!res->ent_a && res->entry_cap > 0)) {
     ctx->err = "result buffers are null";
     return OTPRG_PARAMETER;
   }
+  return guarded(ctx, [&] { OtSolver(ctx, prob, res, opt).run(); });
+}
+
+int otprg_solve_copy_matching(otprg_ctx* ctx, const otprg_copy_instance* inst, double eps,
+                              const otprg_ot_options* opt, otprg_copy_result* res) {
+  if (!ctx) return OTPRG_PARAMETER;
+  if (!res) {
+    ctx->err = "result is null";
+    return OTPRG_PARAMETER;
+  }
+  return guarded(ctx, [&] { OtSolver(ctx, nullptr, nullptr, opt).run_copy(inst, eps, res); });
+}
+
+int otprg_copy_state(otprg_ctx* ctx, otprg_cluster_state* out) {
+  if (!ctx || !out) return OTPRG_PARAMETER;
+  if (!ctx->ot_state) {
+    ctx->err = "no copy/cluster solve on this context yet";
+    return OTPRG_PARAMETER;
+  }
+  *out = static_cast<const FlatState*>(ctx->ot_state.get())->view();
+  return OTPRG_OK;
+}
+
+int otprg_check_cluster_state(const otprg_cluster_state* state, const otprg_copy_instance* inst,
+                              int32_t which, int64_t* count, char* msgs, int32_t msgs_cap) {
+  if (!state || !inst || !inst->k || (which != 0 && which != 1) || state->n_a != inst->n_a ||
+      state->n_b != inst->n_b)
+    return OTPRG_PARAMETER;
+  const auto v = which == 0 ? check_invariant(*state, *inst) : check_feasibility(*state, *inst);
+  if (count) *count = static_cast<int64_t>(v.size());
+  if (msgs && msgs_cap > 0) {
+    std::string m;
+    for (const auto& x : v) m += (m.empty() ? "" : "\n") + x;
+    const size_t n = std::min(m.size(), static_cast<size_t>(msgs_cap - 1));
+    std::memcpy(msgs, m.data(), n);
+    msgs[n] = 0;
+  }
+  return OTPRG_OK;
+}
+
+int otprg_plan_from_flow(const otprg_ot_problem* prob, const int64_t* flow, double theta,
+                         const int64_t* d, const int64_t* s, otprg_ot_result* res) {
+  (void)d;
+  (void)s;  // ScaledMasses' counts: plan_from_flow reads theta only (ot.cpp:639-703)
+  if (!prob || !flow || !res || !(theta > 0.0) || (!res->ent_a && res->entry_cap > 0)) return OTPRG_PARAMETER;
   try {
-    OtSolver(ctx, prob, res).run();
+    OtSolver(nullptr, prob, res).run_plan(flow, theta);
     return OTPRG_OK;
   } catch (const OtError& e) {
-    ctx->err = e.msg;
     return e.code;
-  } catch (const std::exception& e) {
-    ctx->err = e.what();
-    return OTPRG_DEVICE;
   }
 }
 
