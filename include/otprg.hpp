@@ -9,9 +9,11 @@
 //
 // Device path: results equal the reference's threads = 1 results bit for bit
 // (the Sinkhorn baseline to a floating-point tolerance), copy mode
-// (AssignmentOptions::demand_groups / supply_groups) included.  Not provided:
-// the OT observer / check_invariants (OTOptions).  AssignmentOptions::threads
-// is accepted and ignored (the device path is always deterministic).
+// (AssignmentOptions::demand_groups / supply_groups) and the copy/cluster
+// solver's primitives and hooks (solve_copy_matching, plan_from_flow,
+// ClusterOptions / OTOptions, check_cluster_*) included.
+// AssignmentOptions::threads is accepted and ignored (the device path is
+// always deterministic).
 #pragma once
 
 #include <cstdint>
@@ -202,8 +204,87 @@ struct TransportPlan {  // core.hpp:150-162
   double cost = 0.0;
 };
 
-std::pair<TransportPlan, SolveStats> solve_ot(const OTInstance& inst, double eps);
 OTInstance gen_random_ot_rational(Index n_a, Index n_b, std::uint64_t seed);
+
+struct ScaledMasses {  // ot.hpp:40-49
+  double theta = 0.0;
+  std::vector<std::int64_t> d;
+  std::vector<std::int64_t> s;
+  std::int64_t total_d() const;
+  std::int64_t total_s() const;
+};
+ScaledMasses scale_and_round(const OTInstance& inst, double eps);
+
+struct CopyInstance {  // ot.hpp:52-63
+  ScaledCosts costs;
+  std::vector<std::int64_t> demand_copies;
+  std::vector<std::int64_t> supply_copies;
+  std::int64_t total_demand() const;
+  std::int64_t total_supply() const;
+};
+
+struct DemandCluster {  // ot.hpp:65-75
+  DualUnits y = 0;
+  std::int64_t free_count = 0;
+  std::vector<std::pair<Index, std::int64_t>> flow;  // (b, copies), sorted
+  std::int64_t matched() const;
+  std::int64_t count() const { return free_count + matched(); }
+};
+
+struct SupplyCluster {  // ot.hpp:77-83
+  DualUnits y = 0;
+  std::int64_t free_count = 0;
+  std::int64_t matched_count = 0;
+  std::int64_t count() const { return free_count + matched_count; }
+};
+
+struct ClusterState {  // ot.hpp:85-95
+  std::vector<std::vector<DemandCluster>> demand;
+  std::vector<std::vector<SupplyCluster>> supply;
+  Matrix<std::int64_t> flow_matrix(Index n_a, Index n_b) const;
+  std::int64_t free_supply_total() const;
+  std::int64_t free_demand_of(Index a) const;
+  DualUnits sum_abs_duals() const;
+};
+
+struct ClusterReport {  // ot.hpp:97-100
+  std::vector<std::string> violations;
+  bool ok() const { return violations.empty(); }
+};
+ClusterReport check_cluster_invariant(const ClusterState& state, const CopyInstance& inst);
+ClusterReport check_cluster_feasibility(const ClusterState& state, const CopyInstance& inst);
+
+struct ClusterPhaseSnapshot {  // ot.hpp:115-122 (valid during the callback)
+  int phase;
+  const CopyInstance& inst;
+  const ClusterState& state;
+  std::int64_t n_i;
+  DualUnits sum_abs_before;
+  DualUnits sum_abs_after;
+};
+
+struct ClusterOptions {  // ot.hpp:124-129
+  bool check_invariants = false;
+  std::function<void(const ClusterPhaseSnapshot&)> observer;
+};
+
+struct ClusterSolveResult {  // ot.hpp:131-135
+  ClusterState state;
+  Matrix<std::int64_t> flow;
+  SolveStats stats;
+};
+
+ClusterSolveResult solve_copy_matching(const CopyInstance& inst, double eps,
+                                       const ClusterOptions& opt = {});
+TransportPlan plan_from_flow(const Matrix<std::int64_t>& flow, const ScaledMasses& sm,
+                             const OTInstance& inst);
+
+struct OTOptions {  // ot.hpp:153-156
+  bool check_invariants = false;
+  std::function<void(const ClusterPhaseSnapshot&)> observer;
+};
+std::pair<TransportPlan, SolveStats> solve_ot(const OTInstance& inst, double eps,
+                                              const OTOptions& opt = {});
 
 // ---- Sinkhorn baseline (sinkhorn.hpp) ---------------------------------------------
 struct SinkhornConfig {

@@ -4,6 +4,7 @@
 #include "../../include/otprg.hpp"
 
 #include <algorithm>
+#include <exception>
 #include <cmath>
 #include <cstdlib>
 #include <map>
@@ -387,7 +388,252 @@ AssignmentInstance gen_uniform_square(Index n, std::uint64_t seed) {  // instanc
 }
 
 // ---- OT ---------------------------------------------------------------------------
-std::pair<TransportPlan, SolveStats> solve_ot(const OTInstance& inst, double eps) {
+namespace {
+
+// Flat ClusterState (otprg_cluster_state) <-> the reference-shaped types.
+ClusterState state_of(const otprg_cluster_state& st) {
+  ClusterState s;
+  s.demand.resize(st.n_a);
+  s.supply.resize(st.n_b);
+  for (Index a = 0; a < st.n_a; ++a)
+    for (std::int32_t c = st.dem_off[a]; c < st.dem_off[a + 1]; ++c) {
+      DemandCluster d;
+      d.y = st.dem_y[c];
+      d.free_count = st.dem_free[c];
+      for (std::int64_t f = st.flow_off[c]; f < st.flow_off[c + 1]; ++f) d.flow.emplace_back(st.flow_b[f], st.flow_cnt[f]);
+      s.demand[a].push_back(std::move(d));
+    }
+  for (Index b = 0; b < st.n_b; ++b)
+    for (std::int32_t c = st.sup_off[b]; c < st.sup_off[b + 1]; ++c)
+      s.supply[b].push_back(SupplyCluster{st.sup_y[c], st.sup_free[c], st.sup_matched[c]});
+  return s;
+}
+
+struct FlatOf {
+  std::vector<std::int32_t> dem_off{0}, flow_b, sup_off{0};
+  std::vector<std::int64_t> dem_y, dem_free, flow_off{0}, flow_cnt, sup_y, sup_free, sup_matched;
+  otprg_cluster_state v{};
+  explicit FlatOf(const ClusterState& s) {
+    for (const auto& cs : s.demand) {
+      for (const auto& c : cs) {
+        dem_y.push_back(c.y);
+        dem_free.push_back(c.free_count);
+        for (const auto& [b, n] : c.flow) flow_b.push_back(b), flow_cnt.push_back(n);
+        flow_off.push_back(static_cast<std::int64_t>(flow_b.size()));
+      }
+      dem_off.push_back(static_cast<std::int32_t>(dem_y.size()));
+    }
+    for (const auto& cs : s.supply) {
+      for (const auto& c : cs) sup_y.push_back(c.y), sup_free.push_back(c.free_count), sup_matched.push_back(c.matched_count);
+      sup_off.push_back(static_cast<std::int32_t>(sup_y.size()));
+    }
+    v = otprg_cluster_state{static_cast<std::int32_t>(s.demand.size()), static_cast<std::int32_t>(s.supply.size()),
+                            dem_off.data(), dem_y.data(), dem_free.data(), flow_off.data(), flow_b.data(),
+                            flow_cnt.data(), sup_off.data(), sup_y.data(), sup_free.data(), sup_matched.data()};
+  }
+};
+
+otprg_copy_instance flat_instance(const CopyInstance& ci) {
+  return otprg_copy_instance{ci.costs.k.rows(), ci.costs.k.cols(), ci.costs.k.data(), ci.costs.unit_ceil,
+                             ci.demand_copies.data(), ci.supply_copies.data()};
+}
+
+CopyInstance instance_of(const otprg_copy_instance& in) {
+  CopyInstance ci;
+  ci.costs.k = Matrix<std::int32_t>(in.n_a, in.n_b);
+  std::copy(in.k, in.k + static_cast<size_t>(in.n_a) * in.n_b, ci.costs.k.data());
+  ci.costs.unit_floor = ci.costs.unit_ceil = static_cast<std::int32_t>(in.unit_ceil);
+  ci.demand_copies.assign(in.demand_copies, in.demand_copies + in.n_a);
+  ci.supply_copies.assign(in.supply_copies, in.supply_copies + in.n_b);
+  return ci;
+}
+
+// The observer trampoline: C callback -> std::function, exceptions parked and
+// rethrown once the C call has returned (OTPRG_ABORTED).
+struct Hooks {
+  std::function<void(const ClusterPhaseSnapshot&)> fn;
+  const CopyInstance* inst = nullptr;  // the caller's (solve_copy_matching) or built once
+  CopyInstance built;
+  std::exception_ptr err;
+  static int call(const otprg_cluster_snapshot* sn, void* user) {
+    Hooks* h = static_cast<Hooks*>(user);
+    try {
+      if (!h->inst) {
+        h->built = instance_of(sn->inst);
+        h->inst = &h->built;
+      }
+      const ClusterState st = state_of(sn->state);
+      const ClusterPhaseSnapshot snap{static_cast<int>(sn->phase), *h->inst, st, sn->n_i, sn->sum_abs_before,
+                                      sn->sum_abs_after};
+      h->fn(snap);
+      return 0;
+    } catch (...) {
+      h->err = std::current_exception();
+      return 1;
+    }
+  }
+};
+
+void check_hooks(int st, otprg_ctx* ctx, const Hooks& h) {
+  if (st == OTPRG_ABORTED && h.err) std::rethrow_exception(h.err);
+  check(st, ctx);
+}
+
+std::int64_t free_cap_for(double eps) {
+  if (!(eps > 0.0 && eps < 1.0)) return 16;
+  SolveStats s;
+  return std::min<std::int64_t>(s.phase_bound(eps) + 16, OTPRG_MAX_PHASES + 2);
+}
+
+}  // namespace
+
+std::int64_t ScaledMasses::total_d() const {
+  std::int64_t t = 0;
+  for (auto v : d) t += v;
+  return t;
+}
+std::int64_t ScaledMasses::total_s() const {
+  std::int64_t t = 0;
+  for (auto v : s) t += v;
+  return t;
+}
+std::int64_t CopyInstance::total_demand() const {
+  std::int64_t t = 0;
+  for (auto v : demand_copies) t += v;
+  return t;
+}
+std::int64_t CopyInstance::total_supply() const {
+  std::int64_t t = 0;
+  for (auto v : supply_copies) t += v;
+  return t;
+}
+std::int64_t DemandCluster::matched() const {
+  std::int64_t t = 0;
+  for (const auto& e : flow) t += e.second;
+  return t;
+}
+Matrix<std::int64_t> ClusterState::flow_matrix(Index n_a, Index n_b) const {
+  Matrix<std::int64_t> f(n_a, n_b, 0);
+  for (Index a = 0; a < n_a; ++a)
+    for (const DemandCluster& c : demand[a])
+      for (const auto& [b, cnt] : c.flow) f(a, b) += cnt;
+  return f;
+}
+std::int64_t ClusterState::free_supply_total() const {
+  std::int64_t t = 0;
+  for (const auto& cs : supply)
+    for (const auto& c : cs) t += c.free_count;
+  return t;
+}
+std::int64_t ClusterState::free_demand_of(Index a) const {
+  std::int64_t t = 0;
+  for (const auto& c : demand[a]) t += c.free_count;
+  return t;
+}
+DualUnits ClusterState::sum_abs_duals() const {
+  DualUnits t = 0;
+  for (const auto& cs : demand)
+    for (const auto& c : cs) t += std::llabs(c.y) * c.count();
+  for (const auto& cs : supply)
+    for (const auto& c : cs) t += std::llabs(c.y) * c.count();
+  return t;
+}
+
+ScaledMasses scale_and_round(const OTInstance& inst, double eps) {
+  ScaledMasses sm;
+  sm.d.resize(inst.n_a());
+  sm.s.resize(inst.n_b());
+  const int st = otprg_ot_scale_and_round(inst.n_a(), inst.n_b(), inst.mu.data(), inst.nu.data(), eps,
+                                          sm.d.data(), sm.s.data(), &sm.theta);
+  if (st == OTPRG_PARAMETER) throw ParameterError("scale_and_round: bad masses or eps");
+  if (st == OTPRG_INPUT) throw InputError("scale_and_round: masses do not sum to one");
+  if (st) throw InvariantViolation("scale_and_round failed");
+  return sm;
+}
+
+static ClusterReport check_flat(const ClusterState& state, const CopyInstance& inst, int which) {
+  const FlatOf f(state);
+  const otprg_copy_instance in = flat_instance(inst);
+  std::int64_t n = 0;
+  std::vector<char> buf(1 << 16);
+  if (otprg_check_cluster_state(&f.v, &in, which, &n, buf.data(), static_cast<std::int32_t>(buf.size())) != OTPRG_OK)
+    throw ParameterError("cluster state does not match the copy instance");
+  ClusterReport r;
+  std::string all(buf.data());
+  size_t pos = 0;
+  for (std::int64_t i = 0; i < n; ++i) {
+    const size_t e = all.find('\n', pos);
+    r.violations.push_back(all.substr(pos, e == std::string::npos ? std::string::npos : e - pos));
+    if (e == std::string::npos) break;
+    pos = e + 1;
+  }
+  while (static_cast<std::int64_t>(r.violations.size()) < n) r.violations.emplace_back("(truncated)");
+  return r;
+}
+ClusterReport check_cluster_invariant(const ClusterState& state, const CopyInstance& inst) {
+  return check_flat(state, inst, 0);
+}
+ClusterReport check_cluster_feasibility(const ClusterState& state, const CopyInstance& inst) {
+  return check_flat(state, inst, 1);
+}
+
+ClusterSolveResult solve_copy_matching(const CopyInstance& inst, double eps, const ClusterOptions& opt) {
+  otprg_ctx* ctx = context(0);
+  const otprg_copy_instance in = flat_instance(inst);
+  if (inst.costs.k.rows() != static_cast<Index>(inst.demand_copies.size()) ||
+      inst.costs.k.cols() != static_cast<Index>(inst.supply_copies.size()))
+    throw ParameterError("copy counts do not match the cost matrix");
+  Hooks h;
+  h.fn = opt.observer;
+  h.inst = &inst;
+  otprg_ot_options o{opt.check_invariants ? 1 : 0, 0, opt.observer ? &Hooks::call : nullptr, &h};
+  ClusterSolveResult res;
+  res.flow = Matrix<std::int64_t>(in.n_a, in.n_b, 0);
+  std::vector<std::int64_t> fc(static_cast<size_t>(free_cap_for(eps)));
+  otprg_copy_result r{};
+  r.flow = res.flow.data();
+  r.free_counts = fc.data();
+  r.free_cap = static_cast<std::int64_t>(fc.size());
+  check_hooks(otprg_solve_copy_matching(ctx, &in, eps, &o, &r), ctx, h);
+  otprg_cluster_state st{};
+  check(otprg_copy_state(ctx, &st), ctx);
+  res.state = state_of(st);
+  res.stats.phases = static_cast<int>(r.phases);
+  res.stats.free_counts.assign(fc.begin(), fc.begin() + std::min<std::int64_t>(r.phases, fc.size()));
+  res.stats.sum_ni = r.sum_ni;
+  res.stats.full_match_termination = r.full_match_termination != 0;
+  return res;
+}
+
+TransportPlan plan_from_flow(const Matrix<std::int64_t>& flow, const ScaledMasses& sm, const OTInstance& inst) {
+  if (flow.rows() != inst.n_a() || flow.cols() != inst.n_b())
+    throw ParameterError("flow matrix dimensions do not match the instance");
+  otprg_ot_problem p{};
+  p.n_a = inst.n_a();
+  p.n_b = inst.n_b();
+  p.eps = 0.5;
+  p.mu = inst.mu.data();
+  p.nu = inst.nu.data();
+  p.cost = inst.cost.data();
+  std::int64_t cap = static_cast<std::int64_t>(flow.size()) + p.n_a + p.n_b + 16;
+  std::vector<std::int32_t> ea(cap), eb(cap);
+  std::vector<double> em(cap);
+  otprg_ot_result r{};
+  r.ent_a = ea.data();
+  r.ent_b = eb.data();
+  r.ent_mass = em.data();
+  r.entry_cap = cap;
+  const int st = otprg_plan_from_flow(&p, flow.data(), sm.theta, sm.d.data(), sm.s.data(), &r);
+  if (st == OTPRG_PARAMETER) throw ParameterError("plan_from_flow: bad flow or instance");
+  if (st) throw InvariantViolation("plan_from_flow: residual supply could not be placed");
+  TransportPlan plan;
+  plan.cost = r.cost;
+  plan.entries.resize(static_cast<size_t>(r.n_entries));
+  for (std::int64_t i = 0; i < r.n_entries; ++i) plan.entries[i] = {ea[i], eb[i], em[i]};
+  return plan;
+}
+
+std::pair<TransportPlan, SolveStats> solve_ot(const OTInstance& inst, double eps, const OTOptions& opt) {
   if (inst.cost.rows() != inst.n_a() || inst.cost.cols() != inst.n_b())
     throw ParameterError("OT cost matrix dimensions do not match mass vectors");
   otprg_ctx* ctx = context(0);
@@ -398,8 +644,13 @@ std::pair<TransportPlan, SolveStats> solve_ot(const OTInstance& inst, double eps
   p.mu = inst.mu.data();
   p.nu = inst.nu.data();
   p.cost = inst.cost.data();
+  Hooks h;
+  h.fn = opt.observer;
+  const bool hooks = opt.check_invariants || opt.observer;
+  otprg_ot_options o{opt.check_invariants ? 1 : 0, 0, opt.observer ? &Hooks::call : nullptr, &h};
   std::int64_t cap = 4 * (static_cast<std::int64_t>(p.n_a) + p.n_b) + 64;
-  std::vector<std::int64_t> fc(1 << 16);
+  if (hooks) cap = std::max<std::int64_t>(cap, static_cast<std::int64_t>(p.n_a) * p.n_b);  // hooks run once
+  std::vector<std::int64_t> fc(static_cast<size_t>(free_cap_for(eps / 3.0)));
   for (int attempt = 0; attempt < 2; ++attempt) {
     std::vector<std::int32_t> ea(cap), eb(cap);
     std::vector<double> em(cap);
@@ -410,7 +661,7 @@ std::pair<TransportPlan, SolveStats> solve_ot(const OTInstance& inst, double eps
     r.entry_cap = cap;
     r.free_counts = fc.data();
     r.free_cap = static_cast<std::int64_t>(fc.size());
-    check(otprg_solve_ot(ctx, &p, &r), ctx);
+    check_hooks(otprg_solve_ot_opts(ctx, &p, hooks && attempt == 0 ? &o : nullptr, &r), ctx, h);
     if (r.n_entries > cap) {  // room for every entry, then once more
       cap = r.n_entries;
       continue;

@@ -264,11 +264,116 @@ static void copy_mode_cases() {
   }
 }
 
+// copy/cluster solver primitives (ot.hpp:97-156): solve_copy_matching with
+// check_invariants and an observer (flow after every phase), the final state,
+// check_cluster_* on it, plan_from_flow, and solve_ot with OTOptions.
+static void cluster_cases() {
+  std::mt19937_64 rng(777);
+  for (int trial = 0; trial < 12; ++trial) {
+    const double eps = 0.1 + 0.05 * static_cast<double>(rng() % 5);
+    const int n_a = static_cast<int>(rng() % 5) + 2, n_b = static_cast<int>(rng() % 5) + 2;
+    const otpr::AssignmentInstance orig = random_instance(n_a, n_b, rng());
+    otpr::CopyInstance rc;
+    rc.costs = otpr::scale_round_costs(orig, eps);
+    std::int64_t td = 0, ts = 0;
+    for (int a = 0; a < n_a; ++a) rc.demand_copies.push_back(static_cast<std::int64_t>(rng() % 12) + 1), td += rc.demand_copies.back();
+    for (int b = 0; b < n_b; ++b) {
+      const std::int64_t room = td - ts;
+      rc.supply_copies.push_back(room > 0 ? static_cast<std::int64_t>(rng() % (room + 1)) : 0);
+      ts += rc.supply_copies.back();
+    }
+    otprg::CopyInstance gc;
+    gc.costs.eps = rc.costs.eps;
+    gc.costs.unit_floor = rc.costs.unit_floor;
+    gc.costs.unit_ceil = rc.costs.unit_ceil;
+    gc.costs.k = otprg::Matrix<std::int32_t>(n_a, n_b);
+    std::memcpy(gc.costs.k.data(), rc.costs.k.data(), rc.costs.k.size() * 4);
+    gc.demand_copies = rc.demand_copies;
+    gc.supply_copies = rc.supply_copies;
+    std::vector<std::vector<std::int64_t>> rflows, gflows;
+    otpr::ClusterOptions ro;
+    ro.check_invariants = true;
+    ro.observer = [&](const otpr::ClusterPhaseSnapshot& sn) {
+      const auto f = sn.state.flow_matrix(n_a, n_b);
+      rflows.emplace_back(f.data(), f.data() + f.size());
+    };
+    otprg::ClusterOptions go;
+    go.check_invariants = true;
+    go.observer = [&](const otprg::ClusterPhaseSnapshot& sn) {
+      const auto f = sn.state.flow_matrix(n_a, n_b);
+      gflows.emplace_back(f.data(), f.data() + f.size());
+    };
+    const auto rr = otpr::solve_copy_matching(rc, eps, ro);
+    const auto gr = otprg::solve_copy_matching(gc, eps, go);
+    EXPECT(rr.stats.phases == gr.stats.phases && rr.stats.free_counts == gr.stats.free_counts, "copy matching phases");
+    EXPECT(rflows == gflows, "copy matching flow after every phase");
+    EXPECT(std::memcmp(rr.flow.data(), gr.flow.data(), rr.flow.size() * 8) == 0, "copy matching final flow");
+    bool same_state = rr.state.demand.size() == gr.state.demand.size();
+    for (size_t a = 0; same_state && a < rr.state.demand.size(); ++a) {
+      same_state = rr.state.demand[a].size() == gr.state.demand[a].size();
+      for (size_t c = 0; same_state && c < rr.state.demand[a].size(); ++c)
+        same_state = rr.state.demand[a][c].y == gr.state.demand[a][c].y &&
+                     rr.state.demand[a][c].free_count == gr.state.demand[a][c].free_count &&
+                     rr.state.demand[a][c].flow == gr.state.demand[a][c].flow;
+    }
+    for (size_t b = 0; same_state && b < rr.state.supply.size(); ++b) {
+      same_state = rr.state.supply[b].size() == gr.state.supply[b].size();
+      for (size_t c = 0; same_state && c < rr.state.supply[b].size(); ++c)
+        same_state = rr.state.supply[b][c].y == gr.state.supply[b][c].y &&
+                     rr.state.supply[b][c].free_count == gr.state.supply[b][c].free_count &&
+                     rr.state.supply[b][c].matched_count == gr.state.supply[b][c].matched_count;
+    }
+    EXPECT(same_state, "copy matching final ClusterState");
+    EXPECT(otprg::check_cluster_invariant(gr.state, gc).ok() && otprg::check_cluster_feasibility(gr.state, gc).ok(),
+           "cluster checks pass on the final state");
+    // a corrupted state: the same violation list as the reference
+    otpr::ClusterState rbad = rr.state;
+    otprg::ClusterState gbad = gr.state;
+    if (!rbad.supply.empty() && !rbad.supply[0].empty()) {
+      rbad.supply[0][0].y += 3;
+      gbad.supply[0][0].y += 3;
+    }
+    EXPECT(otpr::check_cluster_invariant(rbad, rc).violations == otprg::check_cluster_invariant(gbad, gc).violations,
+           "cluster invariant messages");
+    EXPECT(otpr::check_cluster_feasibility(rbad, rc).violations ==
+               otprg::check_cluster_feasibility(gbad, gc).violations,
+           "cluster feasibility messages");
+  }
+  // solve_ot = scale_and_round -> solve_copy_matching(eps/3) -> plan_from_flow, with hooks
+  const otpr::OTInstance r = otpr::gen_random_ot_rational(40, 30, 9);
+  otprg::OTInstance g;
+  g.mu = r.mu;
+  g.nu = r.nu;
+  g.cost = otprg::Matrix<double>(40, 30);
+  std::memcpy(g.cost.data(), r.cost.data(), r.cost.size() * sizeof(double));
+  int phases_seen = 0;
+  otprg::OTOptions oo;
+  oo.check_invariants = true;
+  oo.observer = [&](const otprg::ClusterPhaseSnapshot& sn) { phases_seen = sn.phase; };
+  auto [pr, sr] = otpr::solve_ot(r, 0.1);
+  auto [pg, sg] = otprg::solve_ot(g, 0.1, oo);
+  EXPECT(pr.cost == pg.cost && sr.free_counts == sg.free_counts, "solve_ot with OTOptions");
+  EXPECT(phases_seen == sg.phases, "OT observer saw every phase");
+  const auto smg = otprg::scale_and_round(g, 0.1 / 3.0);
+  const auto smr = otpr::scale_and_round(r, 0.1 / 3.0);
+  EXPECT(smg.d == smr.d && smg.s == smr.s && smg.theta == smr.theta, "scale_and_round");
+  otpr::CopyInstance rc;
+  rc.costs = otpr::scale_round_costs(otpr::AssignmentInstance{40, 30, r.cost}, 0.1 / 3.0);
+  rc.demand_copies = smr.d;
+  rc.supply_copies = smr.s;
+  const auto rr = otpr::solve_copy_matching(rc, 0.1 / 3.0);
+  otprg::Matrix<std::int64_t> gf(40, 30);
+  std::memcpy(gf.data(), rr.flow.data(), rr.flow.size() * 8);
+  const auto plan = otprg::plan_from_flow(gf, smg, g);
+  EXPECT(plan.cost == pr.cost && plan.entries.size() == pr.entries.size(), "plan_from_flow");
+}
+
 int main() {
   assignment_cases();
   observer_cases();
   ot_cases();
   copy_mode_cases();
+  cluster_cases();
   if (g_fail) {
     std::printf("dropin: %d failures\n", g_fail);
     return 1;
