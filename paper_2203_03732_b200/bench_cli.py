@@ -10,7 +10,8 @@ this library provides.
   timing boundary (the whole solve incl. cost rounding; instance generation
   and verification outside the timer), the same ``--verify`` checks (per phase:
   verify_feasibility, matched-set monotonicity, dual progress, greedy
-  maximality; phase / Σn_i bounds), ``--no-normalize`` semantics.  The
+  maximality; phase / Σn_i bounds; ``pushrelabel-ot``: a rerun with
+  OTOptions::check_invariants), ``--no-normalize`` semantics.  The
   solvers ``pushrelabel``, ``pushrelabel-ot`` and ``sinkhorn`` run on the GPU
   through this package; the exact oracles ``hungarian`` and ``exact-ot`` are
   not on the device path (ParameterError, exit 2), so the oracle-gap check of
@@ -275,8 +276,12 @@ def run_solver(inst: A.AssignmentInstance, req: SolveRequest) -> SolveOutcome:
         rec.time_ms = (time.perf_counter() - t0) * 1e3
         rec.cost = plan.cost * scale
         rec.phases = st.phases
-        if req.verify:
-            out.notes.append("OT check_invariants / exact-ot gap are not on the device path")
+        if req.verify:  # bench.cpp:141-156: an untimed rerun with OTOptions::check_invariants
+            try:
+                A.solve_ot(ot, eps, A.OTOptions(check_invariants=True), device=req.device)
+            except A.InvariantViolation as err:
+                out.verify_violations.append(str(err))
+            out.notes.append("oracle gap not checked: exact-ot is not on the device path")
         return out
 
     if req.solver == "sinkhorn":

@@ -128,3 +128,10 @@ def test_cli_solve_verify_and_bench_on_gpu(golden, tmp_path):
                    "--eps", "0.1", "--runs", "2", "--out", str(out), "--aggregate", str(agg)]) == 0
     assert len(out.read_text().splitlines()) == 1 + 6
     assert len(agg.read_text().splitlines()) == 1 + 3
+
+
+@pytest.mark.gpu
+def test_cli_ot_verify_runs_check_invariants():
+    """pushrelabel-ot --verify: the OTOptions::check_invariants rerun passes (exit 0)."""
+    assert B.main(["solve", "--solver", "pushrelabel-ot", "--n", "60", "--seed", "2", "--eps", "0.1",
+                   "--verify"]) == 0
