@@ -643,7 +643,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
         (A.trace && phase <= A.trace_cap) ? A.trace + (size_t)(phase - 1) * kTraceSlots : nullptr;
     if (leader) {
       A.free_counts[phase - 1] = n;
-      ctl->sum_ni += n;
+      // (a reduction, not a load + store: block 0 must not wait a round trip here)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->sum_ni), (unsigned long long)n);
       ctl->cnt[r_nxt] = 0;  // r_nxt was last read at the top of phase - 1
       ctl->mp_cnt[r_nxt] = 0;
       ctl->work[r_nxt] = 0;
