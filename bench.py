@@ -281,6 +281,8 @@ def run_ours(args, world, rank, local) -> None:
     if world == 1 and not args.no_config4:
         # the 1-GPU point of the config-4 scaling curve (bench.py --gpus N runs it sharded)
         line["config4_1gpu"] = run_sharded(args, world, rank, local, 3, 3)
+        line["scaling_series"] = ("bench.py --gpus N>1 reports config 4 (n=100k) sharded across N GPUs; "
+                                  "its N=1 point is config4_1gpu.value, not this line's config-2 value")
     if rank == 0:
         print(json.dumps(line), flush=True)
     for sv in solvers:
@@ -414,6 +416,9 @@ def run_config4(args, world, rank, local) -> None:
                    "parallelism": f"A-row shards x{world}, candidate all-gather per phase (NCCL)",
                    "K": args.K},
         "sharded": r,
+        "scaling_series": "config 4 (n=100k, eps=0.01) strong scaling: this line is its N-GPU point; the "
+                          "N=1 point is the N=1 line's config4_1gpu (that line's headline value is "
+                          "config 2, the metric's n=10k workload)",
         "gpu_launches": r["gpu_launches_per_step"] * args.steps,
         "clocks": r["clocks"],
         "e2e": {"value": round(float(np.mean(e2e)), 3), "unit": "ms",
