@@ -93,7 +93,15 @@ struct ShardArgs {
   int64_t* free_counts;
   Ctl* ctl;
   int* scratch;            // [>= 148] compaction block counts
+  // Segmented scans (few requests): per-warp first hits [kSegWarps][K],
+  // per-warp hit counts [kSegWarps], per-request arrival counters [n_b]
+  // (zero between launches).  seg_hits == nullptr: one warp per request.
+  int32_t* seg_hits;
+  int32_t* seg_cnt;
+  int32_t* row_cnt;
 };
+constexpr int kSegWarps = 8192;
+constexpr int kMaxSegs = 32;
 // cond: skip (both kernels) when the DA just before parked chains
 // (ctl->work[1] != 0), i.e. the phase is not complete yet.
 cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, bool cond,

@@ -1076,6 +1076,9 @@ otprg::ShardArgs shard_args(otprg_ctx* ctx) {
   S.free_counts = ctx->fc.as<int64_t>();
   S.ctl = ctx->ctl.as<Ctl>();
   S.scratch = ctx->fa.as<int>();  // (completion scratch, free during the phases)
+  S.seg_hits = ctx->sh_seg.as<int32_t>();
+  S.seg_cnt = S.seg_hits + static_cast<size_t>(otprg::kSegWarps) * ctx->sh_K;
+  S.row_cnt = S.seg_cnt + otprg::kSegWarps;
   return S;
 }
 
@@ -1151,6 +1154,11 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   CK(ctx->sh_pos.ensure(ib * 4), "alloc pos");
   CK(ctx->sh_list.ensure(ib * 4), "alloc list");
   for (auto& pk : ctx->sh_park) CK(pk.ensure(ib * 16), "alloc park");
+  {  // segmented-scan merge buffers; the per-request counters start (and stay) zero
+    const size_t seg_words = static_cast<size_t>(otprg::kSegWarps) * (K + 1) + ib;
+    CK(ctx->sh_seg.ensure(seg_words * 4), "alloc segment buffers");
+    CK(cudaMemsetAsync(ctx->sh_seg.p, 0, seg_words * 4, ctx->stream), "memset segment buffers");
+  }
   const double capd = std::ceil((1.0 + 2.0 * p->eps) / (p->eps * p->eps)) + 8.0;
   ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(OTPRG_MAX_PHASES)));
   CK(ctx->fc.ensure(ctx->fc_cap * 8), "alloc free_counts");

@@ -21,6 +21,7 @@
 //               exchanged, and the chains resume.  DA is order independent,
 //               so the result is the reference's sequential greedy M'
 //               whatever the shard count.
+#include <algorithm>
 #include <climits>
 
 #include "device_common.cuh"
@@ -43,43 +44,57 @@ __device__ __forceinline__ void t_set(const ShardArgs& S, int a, uint32_t v) {
 
 // Scan request: (list index, b, start position (global a)).  req == nullptr:
 // every free b of the phase from position 0.
+//
+// segs == 1: one warp per request scans the slab row from `start` in 4 KB
+// steps and writes the first K admissible a (ascending) and the resume
+// position straight to the exchange slots.  segs > 1 (few requests, long
+// rows: the tail phases): the row range [start, hi) is split into segs
+// contiguous pieces, one warp each; every warp keeps the first K hits of its
+// piece in S.seg_hits, and the last warp of the request to finish merges the
+// pieces in order (the first K hits overall; resume after the K-th), so a
+// 200 KB row costs a few dependent steps instead of ~50.
 template <typename T>
 __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4* __restrict__ req,
-                                                         int nreq, int32_t* __restrict__ cand,
+                                                         int nreq, int segs, int32_t* __restrict__ cand,
                                                          int2* __restrict__ meta) {
   using SD = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
   constexpr int kU = 8;  // 4 KB per warp step (long rows: n = 100k rows are 200 KB)
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= nreq) return;
+  if (w >= nreq * segs) return;
+  const int r = w / segs, sg = w - r * segs;
   int i, b, start;
   if (req) {
-    const int4 r = req[w];
-    i = r.x;
-    b = r.y;
-    start = r.z;
+    const int4 q = req[r];
+    i = q.x;
+    b = q.y;
+    start = q.z;
   } else {
-    i = w;
-    b = __ldcg(S.list_in + w);
+    i = r;
+    b = __ldcg(S.list_in + r);
     start = 0;
   }
   const uint32_t tg = SD::rep((uint32_t)__ldcg(S.yb + b) - 1u);
   const int lo = S.lo, hi = S.hi, K = S.K, width_local = hi - lo;
-  int32_t* o = cand + ((size_t)S.shard * S.cap + i) * K;
+  int32_t* o = segs == 1 ? cand + ((size_t)S.shard * S.cap + i) * K : S.seg_hits + (size_t)w * K;
   int cnt = 0, cov = hi;
   const int lstart = max(start, lo) - lo;
   if (start < hi) {
     const uint4* rv = reinterpret_cast<const uint4*>(static_cast<const T*>(S.kT) + (size_t)b * S.lda);
     const uint4* tv = reinterpret_cast<const uint4*>(static_cast<const T*>(S.t) + lo);
     const int nv = (width_local + kEpv - 1) / kEpv;
+    // this warp's piece, in 32-vector units
+    const int u0 = (lstart / kEpv) >> 5, units = (nv + 31) >> 5;
+    const int per = (units - u0 + segs - 1) / segs;
+    const int vb = (u0 + sg * per) * 32, ve = min(nv, (u0 + (sg + 1) * per) * 32);
     bool full = false;
-    for (int v = (lstart / kEpv) & ~31; v < nv && !full; v += 32 * kU) {
+    for (int v = vb; v < ve && !full; v += 32 * kU) {
       uint4 kr[kU], tr[kU];
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
         const int vi = v + j * 32 + lane;
-        if (vi < nv) {
+        if (vi < ve) {
           kr[j] = __ldg(rv + vi);
           tr[j] = __ldcg(tv + vi);
         } else {
@@ -135,7 +150,34 @@ __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4
       }
     }
   }
-  if (lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+  if (segs == 1) {
+    if (lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+    return;
+  }
+  // publish this piece, then the request's last piece merges (first K overall)
+  int prev = 0;
+  if (lane == 0) {
+    S.seg_cnt[w] = cnt;
+    __threadfence();
+    prev = atomicAdd(S.row_cnt + r, 1);
+  }
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != segs - 1) return;
+  __threadfence();
+  int32_t* out = cand + ((size_t)S.shard * S.cap + i) * K;
+  const int wb = r * segs;
+  int tot = 0, rcov = hi;
+  for (int p = 0; p < segs && tot < K; ++p) {
+    const int c = __ldcg(S.seg_cnt + wb + p);
+    const int32_t* src = S.seg_hits + (size_t)(wb + p) * K;
+    if (lane < c && tot + lane < K) out[tot + lane] = __ldcg(src + lane);
+    if (tot + c >= K) rcov = __ldcg(src + (K - 1 - tot)) + 1;
+    tot = min(K, tot + c);
+  }
+  if (lane == 0) {
+    meta[(size_t)S.shard * S.cap + i] = make_int2(tot, rcov);
+    S.row_cnt[r] = 0;  // ready for the next launch
+  }
 }
 
 // Top of the phase after `phase_done` phases: apply M' of phase phase_done
@@ -340,9 +382,19 @@ cudaError_t launch_shard_compact(const ShardArgs& a, bool cond, cudaStream_t s) 
 cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int32_t* cand,
                               int2* meta, cudaStream_t s) {
   if (nreq <= 0) return cudaSuccess;
-  const int blocks = (nreq * 32 + 255) / 256;
+  // Pieces per request: enough warps to cover the GPU (~16 resident per SM at
+  // this kernel's register use) when requests are few, each piece >= one
+  // 4 KB warp step, at most kMaxSegs, within the merge buffers.
+  const int units = ((a.hi - a.lo) * a.width + 511) / 512;  // 32-vector units of a slab row
+  const int target = 148 * 16;
+  int segs = 1;
+  if (a.seg_hits && nreq * 2 <= target) {
+    segs = std::min(std::min(kMaxSegs, target / nreq), std::max(1, units / 8));
+    segs = std::max(1, std::min(segs, kSegWarps / nreq));
+  }
+  const int blocks = (nreq * segs * 32 + 255) / 256;
   with_width(a.width, [&](auto tag) {
-    shard_scan_kernel<decltype(tag)><<<blocks, 256, 0, s>>>(a, req, nreq, cand, meta);
+    shard_scan_kernel<decltype(tag)><<<blocks, 256, 0, s>>>(a, req, nreq, segs, cand, meta);
     return 0;
   });
   return cudaGetLastError();
