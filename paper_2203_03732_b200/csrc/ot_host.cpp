@@ -19,6 +19,8 @@
 #include <chrono>
 #include <random>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -64,12 +66,9 @@ using Flow = std::vector<std::pair<int32_t, int64_t>>;  // (b, copies), ascendin
 struct DemandC {
   int64_t y = 0, free = 0;
   Flow flow;
-  int64_t matched() const {
-    int64_t t = 0;
-    for (const auto& e : flow) t += e.second;
-    return t;
-  }
-  int64_t count() const { return free + matched(); }
+  int64_t mt = 0;  // sum of the flow counts, kept in step by dflow_add / dflow_sub
+  int64_t matched() const { return mt; }
+  int64_t count() const { return free + mt; }
 };
 
 struct SupplyC {
@@ -94,6 +93,16 @@ void flow_sub(Flow& f, int32_t b, int64_t cnt) {
     throw OtError{OTPRG_INVARIANT, "cluster flow underflow while rematching"};
   it->second -= cnt;
   if (it->second == 0) f.erase(it);
+}
+
+void dflow_add(DemandC& c, int32_t b, int64_t cnt) {
+  flow_add(c.flow, b, cnt);
+  c.mt += cnt;
+}
+
+void dflow_sub(DemandC& c, int32_t b, int64_t cnt) {
+  flow_sub(c.flow, b, cnt);
+  c.mt -= cnt;
 }
 
 DemandC& demand_at(std::vector<DemandC>& cs, int64_t y) {
@@ -127,7 +136,7 @@ void normalize_demand(std::vector<DemandC>& cs, int32_t a) {
     if (c.count() == 0) continue;
     if (!out.empty() && out.back().y == c.y) {
       out.back().free += c.free;
-      for (const auto& e : c.flow) flow_add(out.back().flow, e.first, e.second);
+      for (const auto& e : c.flow) dflow_add(out.back(), e.first, e.second);
     } else {
       out.push_back(std::move(c));
     }
@@ -612,6 +621,7 @@ class OtSolver {
 
   int launches_ = 0;
   int64_t scan_bytes_ = 0;
+  double prof_[4] = {0, 0, 0, 0};  // host ms: claim walk, state updates (OTPRG_OT_PROFILE)
 
   // Scan requests on the device; results land in cand / meta (host views).
   void scan(const std::vector<int4>& reqs, std::vector<int32_t>& cand, std::vector<int2>& meta) {
@@ -683,6 +693,7 @@ class OtSolver {
         static_cast<int64_t>(std::ceil((1.0 + 2.0 * eps_in_) / (eps_in_ * eps_in_))) + 8;
 
     std::vector<std::array<Cursor, 2>> cur(n_a_);
+    std::vector<int64_t> avail(2 * static_cast<size_t>(n_a_));
     std::vector<int64_t> matched_from_b(n_b_), remaining_free(n_b_), free_dual(n_b_);
     std::vector<std::vector<std::pair<int64_t, int64_t>>> freed_at(n_b_);
     std::vector<int32_t> free_bs;
@@ -730,6 +741,13 @@ class OtSolver {
       scan(reqs, cand, meta);
       scan_ms += st.ms();
 
+      Timer tc;
+      // copies of every demand cluster still claimable this phase, by scan code 2a + ci
+      for (int32_t a = 0; a < n_a_; ++a) {
+        const auto& cs = dem_[a];
+        avail[2 * a] = cs.size() >= 1 ? cs[0].count() : 0;
+        avail[2 * a + 1] = cs.size() >= 2 ? cs[1].count() : 0;
+      }
       // claim step (ot.cpp:471-522): b ascending, admissible clusters ascending a
       claims.clear();
       displaced.clear();
@@ -753,6 +771,7 @@ class OtSolver {
             continue;
           }
           const int32_t code = list[idx++];
+          if (avail[code] == 0) continue;  // used up this phase (flat filter: no cluster access)
           const int32_t a = code >> 1, ci = code & 1;
           DemandC& c = dem_[a][ci];
           Cursor& cu = cur[a][ci];
@@ -776,6 +795,7 @@ class OtSolver {
             }
           }
           cu.used += take;
+          avail[code] -= take;
           cl.disp_end = displaced.size();
           claims.push_back(cl);
           remaining -= take;
@@ -799,6 +819,8 @@ class OtSolver {
         }
       }
 
+      prof_[0] += tc.ms();
+      Timer tu;
       // supply side: claimed copies become matched at their dual, the
       // phase's leftover free copies go up a unit (ot.cpp:540-553)
       for (int32_t b : free_bs) {
@@ -816,7 +838,7 @@ class OtSolver {
         for (size_t i = cl.disp_begin; i < cl.disp_end; ++i) {
           const int32_t b_old = displaced[i].first;
           const int64_t cnt = displaced[i].second;
-          flow_sub(src.flow, b_old, cnt);
+          dflow_sub(src, b_old, cnt);
           const int64_t y_old = k_of(cl.a, b_old) - src.y;
           bool found = false;
           for (SupplyC& c : sup_[b_old])
@@ -829,13 +851,14 @@ class OtSolver {
           freed_at[b_old].emplace_back(y_old, cnt);
         }
         const int64_t dst_y = src.y - 1;
-        flow_add(demand_at(dem_[cl.a], dst_y).flow, cl.b, cl.total);
+        dflow_add(demand_at(dem_[cl.a], dst_y), cl.b, cl.total);
       }
       for (int32_t b = 0; b < n_b_; ++b) {
         for (const auto& [y_old, cnt] : freed_at[b]) supply_at(sup_[b], y_old).free += cnt;
         normalize_supply(sup_[b], b);
       }
       for (int32_t a = 0; a < n_a_; ++a) normalize_demand(dem_[a], a);
+      prof_[1] += tu.ms();
 
       phases += 1;
       free_counts.push_back(n_i);
@@ -850,6 +873,9 @@ class OtSolver {
       std::memcpy(r_->free_counts, free_counts.data(),
                   static_cast<size_t>(std::min<int64_t>(phases, r_->free_cap)) * 8);
     r_->loop_ms = loop_t.ms();
+    if (std::getenv("OTPRG_OT_PROFILE"))
+      std::fprintf(stderr, "ot loop %.2f ms: scan %.2f claim %.2f update %.2f\n", r_->loop_ms, scan_ms, prof_[0],
+                   prof_[1]);
     r_->scan_ms = scan_ms;
     r_->bytes_touched = scan_bytes_;
     r_->gpu_launches = launches_;
