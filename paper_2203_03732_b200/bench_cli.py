@@ -234,6 +234,13 @@ def _warm_up(device: int) -> None:
     _warmed.add(device)
 
 
+# The GPU solver names SURVEY §8(b) proposes for a GPU-aware run_solver; they
+# run the same device paths as the reference's own names (and keep their own
+# name in the CSV).
+ALIASES = {"pushrelabel-gpu": "pushrelabel", "pushrelabel-ot-gpu": "pushrelabel-ot",
+           "sinkhorn-gpu": "sinkhorn"}
+
+
 def run_solver(inst: A.AssignmentInstance, req: SolveRequest) -> SolveOutcome:
     inst.validate()
     rec = RunRecord(req.solver, n=min(inst.n_a, inst.n_b), seed=inst.seed)
@@ -241,8 +248,9 @@ def run_solver(inst: A.AssignmentInstance, req: SolveRequest) -> SolveOutcome:
     scale = inst.norm_factor if req.no_normalize else 1.0
     eps = req.eps / inst.norm_factor if req.no_normalize else req.eps
     m_side = min(inst.n_a, inst.n_b)
+    solver = ALIASES.get(req.solver, req.solver)
 
-    if req.solver == "pushrelabel":
+    if solver == "pushrelabel":
         rec.eps = req.eps
         opt = A.AssignmentOptions(eps=eps, threads=req.threads, device=req.device)
         _warm_up(req.device)
@@ -263,7 +271,7 @@ def run_solver(inst: A.AssignmentInstance, req: SolveRequest) -> SolveOutcome:
             out.notes.append("oracle gap not checked: hungarian is not on the device path")
         return out
 
-    if req.solver == "pushrelabel-ot":
+    if solver == "pushrelabel-ot":
         if inst.n_a != inst.n_b:
             raise A.InputError("assignment_to_ot needs a balanced instance")
         rec.eps = req.eps
@@ -284,7 +292,7 @@ def run_solver(inst: A.AssignmentInstance, req: SolveRequest) -> SolveOutcome:
             out.notes.append("oracle gap not checked: exact-ot is not on the device path")
         return out
 
-    if req.solver == "sinkhorn":
+    if solver == "sinkhorn":
         if inst.n_a != inst.n_b:
             raise A.InputError("assignment_to_ot needs a balanced instance")
         rec.eps = req.eps
@@ -361,7 +369,7 @@ def _run(argv) -> int:
     s = sub.add_parser("solve", help="run one solver on one instance")
     _instance_flags(s)
     s.add_argument("--solver", required=True,
-                   choices=["pushrelabel", "pushrelabel-ot", "sinkhorn", "hungarian", "exact-ot"])
+                   choices=["pushrelabel", "pushrelabel-ot", "sinkhorn", "hungarian", "exact-ot"] + list(ALIASES))
     s.add_argument("--eps", type=float, default=0.1)
     s.add_argument("--reg", type=float, default=None)
     s.add_argument("--threads", type=int, default=1)

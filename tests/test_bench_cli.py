@@ -135,3 +135,13 @@ def test_cli_ot_verify_runs_check_invariants():
     """pushrelabel-ot --verify: the OTOptions::check_invariants rerun passes (exit 0)."""
     assert B.main(["solve", "--solver", "pushrelabel-ot", "--n", "60", "--seed", "2", "--eps", "0.1",
                    "--verify"]) == 0
+
+
+@pytest.mark.gpu
+def test_cli_gpu_solver_aliases(tmp_path):
+    """pushrelabel-gpu / pushrelabel-ot-gpu name the device paths in the CSV."""
+    csv = tmp_path / "alias.csv"
+    assert B.main(["solve", "--solver", "pushrelabel-gpu", "--n", "200", "--seed", "1", "--eps", "0.1",
+                   "--csv", str(csv)]) == 0
+    assert csv.read_text().splitlines()[1].split(",")[0] == "pushrelabel-gpu"
+    assert B.main(["solve", "--solver", "pushrelabel-ot-gpu", "--n", "50", "--seed", "1", "--eps", "0.1"]) == 0
