@@ -87,7 +87,7 @@ typedef struct otprg_problem {
   const uint8_t* img_a; /* L1_U8: n_a*dim */
   const uint8_t* img_b; /* L1_U8: n_b*dim */
   int32_t dim;          /* L1_U8 pixels per image */
-  int32_t flags;        /* reserved, 0 */
+  int32_t flags;        /* OTPRG_FLAG_* (0 = none) */
 } otprg_problem;
 
 /* Caller-allocated results (SolveStats, assignment.hpp:35-53 + Matching,
@@ -142,6 +142,19 @@ int otprg_set_stream(otprg_ctx* ctx, void* stream);
 
 /* scaled_floor(c, eps) (core.cpp:26-32), evaluated on the host. */
 int64_t otprg_scaled_floor(double c, double eps);
+
+/* Exact threshold table of the 2-D point cost: for the cost
+ * c = sqrt(d2) / sqrt(2) of gen_uniform_square (instances.cpp:70-75, IEEE
+ * round-to-nearest, no FMA) and k = scaled_floor(c, eps), thr[j] is the
+ * smallest double d2 >= 0 with k(d2) >= j, j = 0..unit_floor+1 (thr[0] = 0,
+ * +inf where unreachable for d2 <= 2): k(d2) = max{j : thr[j] <= d2}, so
+ * k(a,b) needs no sqrt or division.  Writes unit_floor + 2 doubles (cap
+ * permitting) and returns that count, or -1 for a bad eps.  Host-only. */
+int32_t otprg_points_threshold_table(double eps, double* thr, int32_t cap);
+
+/* otprg_problem.flags */
+#define OTPRG_FLAG_ON_THE_FLY 1 /* sharded 2-D points: no kT slab; the scans compute k(a,b) from
+                                 * the points with the threshold table above */
 
 /* Full solve: H2D of the problem's host buffers, cost build + rounding on
  * the device, device-resident phase loop, completion, D2H of the results,

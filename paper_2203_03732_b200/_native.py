@@ -22,6 +22,7 @@ OK, PARAMETER, INPUT, NUMERICAL, INVARIANT, DEVICE, ABORTED = 0, 2, 3, 4, 5, 6, 
 COST_DENSE_F64, COST_POINTS2D, COST_L1_U8 = 0, 1, 2
 STORAGE = {"auto": 0, "u8": 1, "u16": 2, "u32": 3}
 MAX_PHASES = 1 << 24  # OTPRG_MAX_PHASES
+FLAG_ON_THE_FLY = 1  # OTPRG_FLAG_ON_THE_FLY
 
 
 class Problem(C.Structure):
@@ -99,7 +100,7 @@ EXPORTS = [
     "otprg_shard_finish", "otprg_set_stream", "otprg_sinkhorn", "otprg_groups_begin",
     "otprg_groups_step", "otprg_groups_finish", "otprg_verify_feasibility", "otprg_verify_host", "otprg_admissible",
     "otprg_solve_ot_opts", "otprg_solve_copy_matching", "otprg_copy_state",
-    "otprg_check_cluster_state", "otprg_plan_from_flow",
+    "otprg_check_cluster_state", "otprg_plan_from_flow", "otprg_points_threshold_table",
 ]
 
 _lib = None
@@ -146,6 +147,8 @@ def lib() -> C.CDLL:
     L.otprg_load_mnist_pair.argtypes = [C.c_char_p, C.c_int32, C.c_uint64, vp, vp, C.c_char_p,
                                         C.c_int32]
     L.otprg_solve_ot.argtypes = [vp, vp, vp]
+    L.otprg_points_threshold_table.restype = C.c_int32
+    L.otprg_points_threshold_table.argtypes = [C.c_double, vp, C.c_int32]
     L.otprg_solve_ot_opts.argtypes = [vp, vp, C.POINTER(OTOptions), vp]
     L.otprg_solve_copy_matching.argtypes = [vp, C.POINTER(CopyInstance), C.c_double,
                                             C.POINTER(OTOptions), C.POINTER(CopyResult)]

@@ -651,6 +651,18 @@ def _pair_cost(inst: AssignmentInstance, a: int, b: int) -> float:
     return math.sqrt(dx * dx + dy * dy) / math.sqrt(2.0)
 
 
+def points_threshold_table(eps: float) -> np.ndarray:
+    """thr[j] = smallest d2 with scaled_floor(sqrt(d2)/sqrt(2), eps) >= j
+    (j = 0..unit_floor+1), so k = searchsorted(thr, d2, 'right') - 1."""
+    L = N.lib()
+    n = L.otprg_points_threshold_table(float(eps), None, 0)
+    if n < 0:
+        raise ParameterError("eps must lie in (0, 1)")
+    thr = np.empty(n, np.float64)
+    L.otprg_points_threshold_table(float(eps), thr.ctypes.data, n)
+    return thr
+
+
 def points_cost(pts_a: np.ndarray, pts_b: np.ndarray) -> np.ndarray:
     """Dense instances.cpp:70-75 cost from point sets (numpy, non-fused)."""
     dx = pts_a[:, None, 0] - pts_b[None, :, 0]

@@ -99,7 +99,9 @@ struct otprg_ctx {
   int sh_park_cur = 0;       // which park buffer holds the waiting chains
   bool sh_top_ready = false;  // the last DA call already ran the next phase's top
   int sh_done = 0;
-  DevBuf sh_bounds, sh_pos, sh_park[2], sh_list, sh_seg;
+  DevBuf sh_bounds, sh_pos, sh_park[2], sh_list, sh_seg, sh_thr;
+  bool sh_otf = false;  // OTPRG_FLAG_ON_THE_FLY: no kT slab, threshold-table scans
+  int sh_thr_n = 0;
 
   // invariant suite / workset export (verify_kernels.cu)
   DevBuf v_out, v_k, v_ya, v_yb, v_ma, v_mb, adm_cnt, adm_off, adm_list;

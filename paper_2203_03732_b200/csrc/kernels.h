@@ -99,6 +99,12 @@ struct ShardArgs {
   int32_t* seg_hits;
   int32_t* seg_cnt;
   int32_t* row_cnt;
+  // On-the-fly costs (thr != nullptr): demand / supply points (global
+  // indices) and the exact threshold table of thr_n doubles.
+  const double2* pa;
+  const double2* pb;
+  const double* thr;
+  int thr_n;
 };
 constexpr int kSegWarps = 8192;
 constexpr int kMaxSegs = 32;

@@ -447,6 +447,36 @@ int otprg_set_stream(otprg_ctx* ctx, void* stream) {
 
 int64_t otprg_scaled_floor(double c, double eps) { return host_scaled_floor(c, eps); }
 
+int32_t otprg_points_threshold_table(double eps, double* thr, int32_t cap) {
+  if (!(eps > 0.0 && eps < 1.0)) return -1;
+  const int64_t uf = host_scaled_floor(1.0, eps);
+  if (uf + 4 > std::numeric_limits<int32_t>::max()) return -1;
+  const int32_t n = static_cast<int32_t>(uf + 2);
+  if (!thr || cap < n) return n;
+  const double sqrt2 = std::sqrt(2.0);
+  // k(d2) = scaled_floor(sqrt(d2) / sqrt(2), eps) is monotone in d2, and d2 >= 0
+  // is monotone in its bit pattern: bisect the bits for the first d2 at each level.
+  auto k_of = [&](double d2) { return host_scaled_floor(std::sqrt(d2) / sqrt2, eps); };
+  auto bits = [](double x) { uint64_t u; std::memcpy(&u, &x, 8); return u; };
+  auto from = [](uint64_t u) { double x; std::memcpy(&x, &u, 8); return x; };
+  const uint64_t top = bits(2.0);  // |a - b|^2 <= 2 for points of the unit square
+  thr[0] = 0.0;
+  for (int32_t j = 1; j < n; ++j) {
+    if (k_of(from(top)) < j) {  // unreachable level
+      thr[j] = std::numeric_limits<double>::infinity();
+      continue;
+    }
+    uint64_t lo = 0, hi = top;  // k(from(hi)) >= j
+    while (lo < hi) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      if (k_of(from(mid)) >= j) hi = mid;
+      else lo = mid + 1;
+    }
+    thr[j] = from(lo);
+  }
+  return n;
+}
+
 int otprg_create(int device, otprg_ctx** out) {
   if (!out) return OTPRG_PARAMETER;
   *out = nullptr;
@@ -1079,6 +1109,12 @@ otprg::ShardArgs shard_args(otprg_ctx* ctx) {
   S.seg_hits = ctx->sh_seg.as<int32_t>();
   S.seg_cnt = S.seg_hits + static_cast<size_t>(otprg::kSegWarps) * ctx->sh_K;
   S.row_cnt = S.seg_cnt + otprg::kSegWarps;
+  if (ctx->sh_otf) {
+    S.pa = ctx->pts.as<double2>();
+    S.pb = S.pa + ctx->ia;
+    S.thr = ctx->sh_thr.as<double>();
+    S.thr_n = ctx->sh_thr_n;
+  }
   return S;
 }
 
@@ -1137,7 +1173,8 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   const int local = std::max(ctx->sh_hi - ctx->sh_lo, 1);
   ctx->lda = (local + align - 1) / align * align;
   const size_t full = (ia + 511) / 512 * 512;
-  CK(ctx->kT.ensure(ib * ctx->lda * width), "alloc kT slab");
+  ctx->sh_otf = (p->flags & OTPRG_FLAG_ON_THE_FLY) != 0;
+  if (!ctx->sh_otf) CK(ctx->kT.ensure(ib * ctx->lda * width), "alloc kT slab");
   CK(ctx->t.ensure(full * width), "alloc t");
   CK(ctx->yb.ensure(ib * 4), "alloc yb");
   CK(ctx->ma.ensure(ia * 4), "alloc match_a");
@@ -1173,7 +1210,17 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   CK(cudaMemcpyAsync(dpa, pa, ia * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
   CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
   CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
-  if (ctx->sh_hi > ctx->sh_lo)
+  if (ctx->sh_otf) {  // the exact threshold table replaces the slab
+    const int32_t n = otprg_points_threshold_table(p->eps, nullptr, 0);
+    if (n < 0 || n > 8192)
+      return fail(ctx, OTPRG_PARAMETER, "on-the-fly costs need 1/eps <= 8190 (threshold table in shared memory)");
+    std::vector<double> thr(n);
+    otprg_points_threshold_table(p->eps, thr.data(), n);
+    CK(ctx->sh_thr.ensure(n * sizeof(double)), "alloc threshold table");
+    CK(cudaMemcpyAsync(ctx->sh_thr.p, thr.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
+       "H2D threshold table");
+    ctx->sh_thr_n = n;
+  } else if (ctx->sh_hi > ctx->sh_lo)
     CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb,
                                     ctx->sh_hi - ctx->sh_lo, ctx->ib, p->eps, std::sqrt(2.0),
                                     ctx->kT.p, ctx->lda, width, ctx->stream),

@@ -365,6 +365,248 @@ __global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, uint32_t pha
   }
 }
 
+
+// On-the-fly variant (OTPRG_FLAG_ON_THE_FLY): no kT slab.  Each lane
+// takes one demand point per 32-element group, forms d2 = dx*dx + dy*dy in
+// IEEE round-to-nearest (the reference's bits, instances.cpp:70-75) and tests
+// admissibility k(a,b) + t(a) == target as thr[m] <= d2 < thr[m+1] with
+// m = target - t(a), against the exact threshold table staged in shared
+// memory: no sqrt, no division, 16 B of point per element instead of w B of kT.
+// Outputs, pieces and the merge as shard_scan_kernel.
+template <typename T>
+__global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const int4* __restrict__ req,
+                                                             int nreq, int segs, int32_t* __restrict__ cand,
+                                                             int2* __restrict__ meta) {
+  extern __shared__ double s_thr[];
+  for (int j = threadIdx.x; j < S.thr_n; j += blockDim.x) s_thr[j] = S.thr[j];
+  __syncthreads();
+  constexpr int kG = 8;  // 32-element groups per warp step
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nreq * segs) return;
+  const int r = w / segs, sg = w - r * segs;
+  int i, b, start;
+  if (req) {
+    const int4 q = req[r];
+    i = q.x;
+    b = q.y;
+    start = q.z;
+  } else {
+    i = r;
+    b = __ldcg(S.list_in + r);
+    start = 0;
+  }
+  const int64_t target = (int64_t)(uint32_t)__ldcg(S.yb + b) - 1;
+  const int lo = S.lo, hi = S.hi, K = S.K, width_local = hi - lo, mmax = S.thr_n - 2;
+  int32_t* o = segs == 1 ? cand + ((size_t)S.shard * S.cap + i) * K : S.seg_hits + (size_t)w * K;
+  int cnt = 0, cov = hi;
+  const int lstart = max(start, lo) - lo;
+  if (start < hi) {
+    const double2 q = S.pb[b];
+    const double2* pa = S.pa + lo;
+    const T* tl = static_cast<const T*>(S.t) + lo;
+    const int groups = (width_local + 31) >> 5, g0 = lstart >> 5;
+    const int per = (groups - g0 + segs - 1) / segs;
+    const int gb = g0 + sg * per, ge = min(groups, g0 + (sg + 1) * per);
+    bool full = false;
+    for (int g = gb; g < ge && !full; g += kG) {
+      double2 p[kG];
+      uint32_t tt[kG];
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        const int e = (g + j) * 32 + lane;
+        const bool ok = g + j < ge && e < width_local;
+        p[j] = ok ? __ldg(pa + e) : make_double2(0.0, 0.0);
+        tt[j] = ok ? (uint32_t)__ldcg(tl + e) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        if (full || g + j >= ge) break;
+        const int e = (g + j) * 32 + lane;
+        bool hit = false;
+        if (e < width_local && e >= lstart) {
+          const double dx = __dsub_rn(p[j].x, q.x), dy = __dsub_rn(p[j].y, q.y);
+          const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+          const int64_t m = target - (int64_t)tt[j];
+          hit = m >= 0 && m <= mmax && s_thr[m] <= d2 && d2 < s_thr[m + 1];
+        }
+        const unsigned bal = __ballot_sync(kFull, hit);
+        if (!bal) continue;
+        const int idx = cnt + __popc(bal & ((1u << lane) - 1u));
+        if (hit && idx < K) o[idx] = lo + e;
+        const int c = __popc(bal);
+        if (cnt + c >= K) {
+          unsigned bm = bal;  // lane of the K-th hit overall: the (K - cnt)-th set bit
+          for (int t2 = 1; t2 < K - cnt; ++t2) bm &= bm - 1;
+          const int src = __ffs(bm) - 1;
+          cov = lo + (g + j) * 32 + src + 1;
+          cnt = K;
+          full = true;
+        } else {
+          cnt += c;
+        }
+      }
+    }
+  }
+  if (segs == 1) {
+    if (lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+    return;
+  }
+  int prev = 0;
+  if (lane == 0) {
+    S.seg_cnt[w] = cnt;
+    __threadfence();
+    prev = atomicAdd(S.row_cnt + r, 1);
+  }
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != segs - 1) return;
+  __threadfence();
+  int32_t* out = cand + ((size_t)S.shard * S.cap + i) * K;
+  const int wb = r * segs;
+  int tot = 0, rcov = hi;
+  for (int pc = 0; pc < segs && tot < K; ++pc) {
+    const int c = __ldcg(S.seg_cnt + wb + pc);
+    const int32_t* src = S.seg_hits + (size_t)(wb + pc) * K;
+    if (lane < c && tot + lane < K) out[tot + lane] = __ldcg(src + lane);
+    if (tot + c >= K) rcov = __ldcg(src + (K - 1 - tot)) + 1;
+    tot = min(K, tot + c);
+  }
+  if (lane == 0) {
+    meta[(size_t)S.shard * S.cap + i] = make_int2(tot, rcov);
+    S.row_cnt[r] = 0;
+  }
+}
+
+
+// On-the-fly, many requests: a block takes kOtfRows requests (one warp
+// each) and streams the slab's demand points and t through shared memory in
+// kOtfChunk-point chunks (two stages filled by 1-D TMA bulk copies, the next
+// chunk landing while the current one is scanned), so each 16-byte point
+// leaves L2 once per block rather than once per row; warps whose row already
+// has K hits idle until every row of the block is done.  Outputs as
+// shard_scan_otf_kernel with segs == 1.
+constexpr int kOtfRows = 16, kOtfChunk = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(ShardArgs S,
+                                                                            const int4* __restrict__ req,
+                                                                            int nreq, int32_t* __restrict__ cand,
+                                                                            int2* __restrict__ meta) {
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  // stage st: points [kOtfChunk] double2 then t [kOtfChunk] T; the table after both stages
+  constexpr size_t kStage = (size_t)kOtfChunk * (sizeof(double2) + sizeof(T));
+  double* s_thr = reinterpret_cast<double*>(s_dyn + 2 * kStage);
+  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ int s_lo_start, s_act[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * kOtfRows + warp;
+  const bool has = r < nreq;
+  int i = 0, b = 0, start = 0;
+  if (has) {
+    if (req) {
+      const int4 q = req[r];
+      i = q.x;
+      b = q.y;
+      start = q.z;
+    } else {
+      i = r;
+      b = __ldcg(S.list_in + r);
+    }
+  }
+  const int lo = S.lo, hi = S.hi, K = S.K, width_local = hi - lo, mmax = S.thr_n - 2;
+  const int lstart = has ? max(start, lo) - lo : width_local;
+  bool done = !has || start >= hi;
+  if (threadIdx.x == 0) {
+    s_lo_start = width_local;
+    s_act[0] = s_act[1] = s_act[2] = 0;
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < S.thr_n; j += blockDim.x) s_thr[j] = S.thr[j];
+  __syncthreads();
+  if (lane == 0 && !done) atomicMin(&s_lo_start, lstart);
+  int64_t target = 0;
+  double2 q = make_double2(0.0, 0.0);
+  if (has) {
+    target = (int64_t)(uint32_t)__ldcg(S.yb + b) - 1;
+    q = S.pb[b];
+  }
+  int32_t* o = cand + ((size_t)S.shard * S.cap + i) * K;
+  int cnt = 0, cov = hi;
+  __syncthreads();
+  const int c_begin = (s_lo_start / kOtfChunk) * kOtfChunk;
+  const int nchunk = c_begin < width_local ? (width_local - c_begin + kOtfChunk - 1) / kOtfChunk : 0;
+  const double2* pa = S.pa + lo;
+  const T* tl = static_cast<const T*>(S.t) + lo;
+  auto issue = [&](int k) {  // thread 0: chunk k into stage k & 1
+    const int c0 = c_begin + k * kOtfChunk;
+    const int len = min(kOtfChunk, width_local - c0);
+    unsigned char* st = s_dyn + (size_t)(k & 1) * kStage;
+    const unsigned pb_bytes = (unsigned)len * 16u;
+    const unsigned tb = (unsigned)(((size_t)len * sizeof(T) + 15) & ~(size_t)15);
+    mbar_expect_tx(&bar[k & 1], pb_bytes + tb);
+    bulk_g2s(st, pa + c0, pb_bytes, &bar[k & 1]);
+    bulk_g2s(st + (size_t)kOtfChunk * sizeof(double2), tl + c0, tb, &bar[k & 1]);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < min(2, nchunk); ++k) issue(k);
+  unsigned par = 0;
+  int k = 0;
+  for (; k < nchunk; ++k) {
+    mbar_wait(&bar[k & 1], (par >> (k & 1)) & 1u);
+    par ^= 1u << (k & 1);
+    const int c0 = c_begin + k * kOtfChunk;
+    const int len = min(kOtfChunk, width_local - c0);
+    const double2* sp = reinterpret_cast<const double2*>(s_dyn + (size_t)(k & 1) * kStage);
+    const T* stt = reinterpret_cast<const T*>(s_dyn + (size_t)(k & 1) * kStage + (size_t)kOtfChunk * sizeof(double2));
+    for (int g = 0; g < len && !done; g += 32) {
+      const int e = c0 + g + lane;
+      bool hit = false;
+      if (g + lane < len && e >= lstart) {
+        const double2 p = sp[g + lane];
+        const double dx = __dsub_rn(p.x, q.x), dy = __dsub_rn(p.y, q.y);
+        const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        const int64_t m = target - (int64_t)(uint32_t)stt[g + lane];
+        hit = m >= 0 && m <= mmax && s_thr[m] <= d2 && d2 < s_thr[m + 1];
+      }
+      const unsigned bal = __ballot_sync(kFull, hit);
+      if (!bal) continue;
+      const int idx = cnt + __popc(bal & ((1u << lane) - 1u));
+      if (hit && idx < K) o[idx] = lo + e;
+      const int cc = __popc(bal);
+      if (cnt + cc >= K) {
+        unsigned bm = bal;
+        for (int t2 = 1; t2 < K - cnt; ++t2) bm &= bm - 1;
+        cov = lo + c0 + g + __ffs(bm);  // (position of the K-th hit) + 1
+        cnt = K;
+        done = true;
+      } else {
+        cnt += cc;
+      }
+    }
+    // rows still open after this chunk; three counters so that a reset never
+    // races with a read (counter k % 3 is read after this barrier, reset after
+    // the next one, and counted into again only after the one after that)
+    if (lane == 0 && !done) atomicAdd(&s_act[k % 3], 1);
+    __syncthreads();  // stage k & 1 consumed by every warp
+    const int open = s_act[k % 3];
+    if (threadIdx.x == 0) s_act[(k + 2) % 3] = 0;
+    if (open == 0) {
+      ++k;
+      break;
+    }
+    if (threadIdx.x == 0 && k + 2 < nchunk) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + 2);
+    }
+  }
+  // an early stop leaves chunk k (issued as k-1+2... i.e. the one after the
+  // last consumed) in flight: it must land before the block exits
+  if (threadIdx.x == 0 && k < nchunk) mbar_wait(&bar[k & 1], (par >> (k & 1)) & 1u);
+  if (has && lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+}
+
 }  // namespace
 
 cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, bool cond,
@@ -385,7 +627,8 @@ cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int
   // Pieces per request: enough warps to cover the GPU (~16 resident per SM at
   // this kernel's register use) when requests are few, each piece >= one
   // 4 KB warp step, at most kMaxSegs, within the merge buffers.
-  const int units = ((a.hi - a.lo) * a.width + 511) / 512;  // 32-vector units of a slab row
+  const int units = a.thr ? ((a.hi - a.lo) + 31) / 32  // 32-element groups (on the fly)
+                          : ((a.hi - a.lo) * a.width + 511) / 512;  // 32-vector units of a slab row
   const int target = 148 * 16;
   int segs = 1;
   if (a.seg_hits && nreq * 2 <= target) {
@@ -393,6 +636,28 @@ cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int
     segs = std::max(1, std::min(segs, kSegWarps / nreq));
   }
   const int blocks = (nreq * segs * 32 + 255) / 256;
+  if (a.thr && segs == 1) {  // many rows: tile kOtfRows rows over shared point chunks
+    const size_t smem = 2 * (size_t)kOtfChunk * (sizeof(double2) + (size_t)a.width) +
+                        (size_t)a.thr_n * sizeof(double);
+    const int tblocks = (nreq + kOtfRows - 1) / kOtfRows;
+    with_width(a.width, [&](auto tag) {
+      auto fn = shard_scan_otf_tiled_kernel<decltype(tag)>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      fn<<<tblocks, kOtfRows * 32, smem, s>>>(a, req, nreq, cand, meta);
+      return 0;
+    });
+    return cudaGetLastError();
+  }
+  if (a.thr) {
+    const size_t smem = (size_t)a.thr_n * sizeof(double);
+    with_width(a.width, [&](auto tag) {
+      auto fn = shard_scan_otf_kernel<decltype(tag)>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      fn<<<blocks, 256, smem, s>>>(a, req, nreq, segs, cand, meta);
+      return 0;
+    });
+    return cudaGetLastError();
+  }
   with_width(a.width, [&](auto tag) {
     shard_scan_kernel<decltype(tag)><<<blocks, 256, 0, s>>>(a, req, nreq, segs, cand, meta);
     return 0;

@@ -45,8 +45,11 @@ class DeviceRank:
             self.solver._raise(st)
 
     def prepare(self, inst: AssignmentInstance, eps: float, n_shards: int, shard: int,
-                K: int = K_DEFAULT, storage: str = "auto") -> np.ndarray:
+                K: int = K_DEFAULT, storage: str = "auto", on_the_fly: bool = False) -> np.ndarray:
         p = self.solver._problem(inst, eps, storage)
+        if on_the_fly:  # no kT slab: scans compute k from the points (threshold table)
+            from . import _native as N
+            p.flags |= N.FLAG_ON_THE_FLY
         bounds = np.zeros(n_shards + 1, np.int32)
         self._ok(self._L.otprg_shard_prepare(self._ctx, C.byref(p), n_shards, shard, K,
                                              bounds.ctypes.data))
@@ -164,7 +167,7 @@ class ShardedSolver:
     LOCAL_RANK (TorchDistExchange over NCCL)."""
 
     def __init__(self, inst: AssignmentInstance, opt: AssignmentOptions, n_shards: int = 1,
-                 K: int = K_DEFAULT, distributed: bool = False):
+                 K: int = K_DEFAULT, distributed: bool = False, on_the_fly: bool = False):
         _check_options(inst, opt)
         if inst.pts_a is None or inst.pts_b is None:
             raise ParameterError("the sharded path builds slabs from 2-D point sets")
@@ -174,14 +177,14 @@ class ShardedSolver:
             # this rank's GPU: OTPRG_DEVICE, else LOCAL_RANK (one process per GPU)
             device = int(os.environ.get("OTPRG_DEVICE", os.environ.get("LOCAL_RANK", opt.device)))
             self.ranks = [DeviceRank(device)]
-            self.ranks[0].prepare(inst, opt.eps, world, rank, K, opt.storage)
+            self.ranks[0].prepare(inst, opt.eps, world, rank, K, opt.storage, on_the_fly)
             self.n_shards = world
             self.exchange = TorchDistExchange(rank, world)
         else:
             device = opt.device
             self.ranks = [DeviceRank(device) for _ in range(n_shards)]
             for g, r in enumerate(self.ranks):
-                r.prepare(inst, opt.eps, n_shards, g, K, opt.storage)
+                r.prepare(inst, opt.eps, n_shards, g, K, opt.storage, on_the_fly)
             self.n_shards = n_shards
             self.exchange = LocalExchange()
         self.cap = self.ranks[0].cap
@@ -225,10 +228,11 @@ class ShardedSolver:
 
 
 def solve_assignment_sharded(inst: AssignmentInstance, opt: AssignmentOptions, n_shards: int,
-                             K: int = K_DEFAULT):
+                             K: int = K_DEFAULT, on_the_fly: bool = False):
     """All shards in this process on opt.device (LocalExchange): G logical
-    shards on one GPU.  Returns (Matching, SolveStats)."""
-    sv = ShardedSolver(inst, opt, n_shards, K)
+    shards on one GPU.  ``on_the_fly``: no kT slabs, costs from the points in
+    the scans (OTPRG_FLAG_ON_THE_FLY).  Returns (Matching, SolveStats)."""
+    sv = ShardedSolver(inst, opt, n_shards, K, on_the_fly=on_the_fly)
     try:
         return sv.solve()
     finally:
@@ -236,10 +240,10 @@ def solve_assignment_sharded(inst: AssignmentInstance, opt: AssignmentOptions, n
 
 
 def solve_assignment_distributed(inst: AssignmentInstance, opt: AssignmentOptions,
-                                 K: int = K_DEFAULT):
+                                 K: int = K_DEFAULT, on_the_fly: bool = False):
     """One rank per process/GPU under torch.distributed (NCCL): each process
     calls this with the same instance; every rank returns the same result."""
-    sv = ShardedSolver(inst, opt, K=K, distributed=True)
+    sv = ShardedSolver(inst, opt, K=K, distributed=True, on_the_fly=on_the_fly)
     try:
         return sv.solve()
     finally:

@@ -129,3 +129,43 @@ def test_two_processes_one_gpu_gloo():
                         "scripts/dist_on_one_gpu.py"], cwd=root, env=env, capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0 and "DIST OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+# ---- on-the-fly costs (OTPRG_FLAG_ON_THE_FLY) ----
+
+@pytest.mark.parametrize("key,G,K", [
+    ("square_n10000_eps0.01_s1", 1, 16), ("square_n10000_eps0.01_s2", 3, 16),
+    ("square_n4000_eps0.01_s1", 2, 1), ("square_n10000_eps0.1_s1", 4, 4),
+    ("square_n3000_eps0.02_s1", 5, 2), ("square_n1000_eps0.01_s1", 1, 16),
+])
+def test_on_the_fly_matches_golden(golden, key, G, K):
+    """No kT slab: the scans round the 2-D point costs themselves through the
+    exact threshold table; results equal the reference's bit for bit."""
+    v = golden[key]
+    m, s = sharded.solve_assignment_sharded(otprg.gen_uniform_square(v["n_a"], v["seed"]),
+                                            otprg.AssignmentOptions(eps=v["eps"]), G, K=K, on_the_fly=True)
+    _check_golden(golden, key, m, s)
+
+
+@pytest.mark.parametrize("storage", ["u8", "u16", "u32"])
+def test_on_the_fly_rectangular_and_storage(storage):
+    rng = np.random.default_rng(17)
+    for n_a, n_b, eps in ((2500, 1300, 0.02), (900, 2100, 0.05), (64, 64, 0.003)):
+        inst = otprg.AssignmentInstance(n_a, n_b, pts_a=rng.random((n_a, 2)), pts_b=rng.random((n_b, 2)))
+        opt = otprg.AssignmentOptions(eps=eps, storage=storage)
+        try:
+            m1, s1 = otprg.solve_assignment(inst, opt)
+        except otprg.ParameterError:
+            continue  # storage too narrow for eps
+        m2, s2 = sharded.solve_assignment_sharded(inst, opt, 3, K=4, on_the_fly=True)
+        assert np.array_equal(m1.match_of_a, m2.match_of_a)
+        assert np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a)
+        assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b)
+        assert np.array_equal(s1.free_counts, s2.free_counts)
+        assert s1.device["cost"] == s2.device["cost"] and s1.swapped == s2.swapped
+
+
+def test_on_the_fly_rejects_tiny_eps():
+    inst = otprg.gen_uniform_square(50, 1)
+    with pytest.raises(otprg.ParameterError):
+        sharded.solve_assignment_sharded(inst, otprg.AssignmentOptions(eps=1e-4), 1, on_the_fly=True)
