@@ -281,6 +281,7 @@ def run_ours(args, world, rank, local) -> None:
     if world == 1 and not args.no_config4:
         # the 1-GPU point of the config-4 scaling curve (bench.py --gpus N runs it sharded)
         line["config4_1gpu"] = run_sharded(args, world, rank, local, 3, 3)
+        line["config4_1gpu_on_the_fly"] = run_sharded(args, world, rank, local, 3, 3, on_the_fly=True)
         line["scaling_series"] = ("bench.py --gpus N>1 reports config 4 (n=100k) sharded across N GPUs; "
                                   "its N=1 point is config4_1gpu.value, not this line's config-2 value")
     if rank == 0:
@@ -334,18 +335,20 @@ def e2e_points(otprg, local, args) -> dict:
             "bit_exact": bool(ok)}
 
 
-def run_sharded(args, world, rank, local, steps: int, warmup: int) -> dict:
+def run_sharded(args, world, rank, local, steps: int, warmup: int, on_the_fly: bool = False) -> dict:
     """Config 4: n=100k points, eps=0.01, A rows sharded across the ranks
     (SURVEY §8(e)); one step = one full sharded solve with every rank's slab
-    resident (20 GB / N of uint16 kT: far larger than L2).  Timed with CUDA
-    events on each rank's solver stream, max over ranks."""
+    resident (20 GB / N of uint16 kT: far larger than L2), or with
+    ``on_the_fly`` no slab at all (the scans round the point costs through the
+    exact threshold table).  Timed with CUDA events on each rank's
+    solver stream, max over ranks."""
     import paper_2203_03732_b200 as otprg
     from paper_2203_03732_b200.sharded import ShardedSolver
 
     inst = otprg.gen_uniform_square(N4, 1)
     opt = otprg.AssignmentOptions(eps=EPS, storage=args.storage, device=local)
     t0 = time.perf_counter()
-    sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1)
+    sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1, on_the_fly=on_the_fly)
     barrier(world)
     prep_s = allreduce_max(time.perf_counter() - t0, world)
     m, s = sv.solve()
@@ -364,6 +367,8 @@ def run_sharded(args, world, rank, local, steps: int, warmup: int) -> dict:
     out = {
         "value": round(ms, 3), "unit": "ms", "n_gpus": world, "steps": steps, "warmup": warmup,
         "phases": P, "sum_ni": int(s.sum_ni), "refill_rounds": R, "K": args.K,
+        "costs": "on the fly from the points (threshold table, no kT slab)" if on_the_fly
+                 else "precomputed uint16 kT slab",
         "slab_build_ms": round(float(s.device["build_ms"]), 3),
         "prepare_wall_s": round(prep_s, 3),
         # init + first top (top, 2 compaction passes) + per DA round (scan, DA, top,
@@ -388,6 +393,7 @@ def run_sharded(args, world, rank, local, steps: int, warmup: int) -> dict:
 
 def run_config4(args, world, rank, local) -> None:
     r = run_sharded(args, world, rank, local, args.steps, args.warmup)
+    r_otf = run_sharded(args, world, rank, local, min(args.steps, 3), min(args.warmup, 3), on_the_fly=True)
     # e2e: host point sets in, slab build + solve + results out, every step
     import paper_2203_03732_b200 as otprg
     from paper_2203_03732_b200.sharded import ShardedSolver
@@ -416,6 +422,7 @@ def run_config4(args, world, rank, local) -> None:
                    "parallelism": f"A-row shards x{world}, candidate all-gather per phase (NCCL)",
                    "K": args.K},
         "sharded": r,
+        "on_the_fly": r_otf,
         "scaling_series": "config 4 (n=100k, eps=0.01) strong scaling: this line is its N-GPU point; the "
                           "N=1 point is the N=1 line's config4_1gpu (that line's headline value is "
                           "config 2, the metric's n=10k workload)",
