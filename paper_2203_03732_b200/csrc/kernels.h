@@ -106,7 +106,7 @@ struct ShardArgs {
   const double* thr;
   int thr_n;
 };
-constexpr int kSegWarps = 8192;
+constexpr int kSegWarps = 32768;
 constexpr int kMaxSegs = 32;
 // cond: skip (both kernels) when the DA just before parked chains
 // (ctl->work[1] != 0), i.e. the phase is not complete yet.

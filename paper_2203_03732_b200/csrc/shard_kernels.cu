@@ -483,23 +483,27 @@ __global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const 
 // kOtfChunk-point chunks (two stages filled by 1-D TMA bulk copies, the next
 // chunk landing while the current one is scanned), so each 16-byte point
 // leaves L2 once per block rather than once per row; warps whose row already
-// has K hits idle until every row of the block is done.  Outputs as
-// shard_scan_otf_kernel with segs == 1.
+// has K hits idle until every row of the block is done.  segs > 1 (tail
+// phases: few row groups) splits the chunk range of a row group into pieces
+// on separate blocks, merged per row like shard_scan_kernel's pieces.  The
+// threshold table is staged as pairs (thr[m], thr[m+1]): one 16-byte load.
 constexpr int kOtfRows = 16, kOtfChunk = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(ShardArgs S,
                                                                             const int4* __restrict__ req,
-                                                                            int nreq, int32_t* __restrict__ cand,
+                                                                            int nreq, int segs,
+                                                                            int32_t* __restrict__ cand,
                                                                             int2* __restrict__ meta) {
   extern __shared__ __align__(128) unsigned char s_dyn[];
-  // stage st: points [kOtfChunk] double2 then t [kOtfChunk] T; the table after both stages
+  // stage st: points [kOtfChunk] double2 then t [kOtfChunk] T; the pair table after both stages
   constexpr size_t kStage = (size_t)kOtfChunk * (sizeof(double2) + sizeof(T));
-  double* s_thr = reinterpret_cast<double*>(s_dyn + 2 * kStage);
+  double2* s_pair = reinterpret_cast<double2*>(s_dyn + 2 * kStage);
   __shared__ __align__(8) unsigned long long bar[2];
   __shared__ int s_lo_start, s_act[3];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = blockIdx.x * kOtfRows + warp;
+  const int grp = blockIdx.x / segs, sg = blockIdx.x - grp * segs;
+  const int r = grp * kOtfRows + warp;
   const bool has = r < nreq;
   int i = 0, b = 0, start = 0;
   if (has) {
@@ -513,7 +517,8 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
       b = __ldcg(S.list_in + r);
     }
   }
-  const int lo = S.lo, hi = S.hi, K = S.K, width_local = hi - lo, mmax = S.thr_n - 2;
+  const int lo = S.lo, hi = S.hi, K = S.K, width_local = hi - lo;
+  const unsigned mmax = (unsigned)(S.thr_n - 2);
   const int lstart = has ? max(start, lo) - lo : width_local;
   bool done = !has || start >= hi;
   if (threadIdx.x == 0) {
@@ -523,24 +528,27 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int j = threadIdx.x; j < S.thr_n; j += blockDim.x) s_thr[j] = S.thr[j];
+  for (int j = threadIdx.x; j + 1 < S.thr_n; j += blockDim.x) s_pair[j] = make_double2(S.thr[j], S.thr[j + 1]);
   __syncthreads();
   if (lane == 0 && !done) atomicMin(&s_lo_start, lstart);
-  int64_t target = 0;
+  int target = 0;  // (the table has <= 8192 levels: int is exact)
   double2 q = make_double2(0.0, 0.0);
   if (has) {
-    target = (int64_t)(uint32_t)__ldcg(S.yb + b) - 1;
+    target = __ldcg(S.yb + b) - 1;
     q = S.pb[b];
   }
-  int32_t* o = cand + ((size_t)S.shard * S.cap + i) * K;
+  int32_t* o = segs == 1 ? cand + ((size_t)S.shard * S.cap + i) * K : S.seg_hits + ((size_t)r * segs + sg) * K;
   int cnt = 0, cov = hi;
   __syncthreads();
-  const int c_begin = (s_lo_start / kOtfChunk) * kOtfChunk;
-  const int nchunk = c_begin < width_local ? (width_local - c_begin + kOtfChunk - 1) / kOtfChunk : 0;
+  // this block's piece of the row group's chunk range
+  const int c_first = s_lo_start / kOtfChunk, c_total = (width_local + kOtfChunk - 1) / kOtfChunk;
+  const int per = c_total > c_first ? (c_total - c_first + segs - 1) / segs : 0;
+  const int k_lo = c_first + sg * per, k_hi = min(c_total, c_first + (sg + 1) * per);
+  const int nchunk = max(0, k_hi - k_lo);
   const double2* pa = S.pa + lo;
   const T* tl = static_cast<const T*>(S.t) + lo;
-  auto issue = [&](int k) {  // thread 0: chunk k into stage k & 1
-    const int c0 = c_begin + k * kOtfChunk;
+  auto issue = [&](int k) {  // thread 0: chunk k_lo + k into stage k & 1
+    const int c0 = (k_lo + k) * kOtfChunk;
     const int len = min(kOtfChunk, width_local - c0);
     unsigned char* st = s_dyn + (size_t)(k & 1) * kStage;
     const unsigned pb_bytes = (unsigned)len * 16u;
@@ -556,24 +564,23 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
   for (; k < nchunk; ++k) {
     mbar_wait(&bar[k & 1], (par >> (k & 1)) & 1u);
     par ^= 1u << (k & 1);
-    const int c0 = c_begin + k * kOtfChunk;
+    const int c0 = (k_lo + k) * kOtfChunk;
     const int len = min(kOtfChunk, width_local - c0);
     const double2* sp = reinterpret_cast<const double2*>(s_dyn + (size_t)(k & 1) * kStage);
     const T* stt = reinterpret_cast<const T*>(s_dyn + (size_t)(k & 1) * kStage + (size_t)kOtfChunk * sizeof(double2));
-    for (int g = 0; g < len && !done; g += 32) {
-      const int e = c0 + g + lane;
-      bool hit = false;
-      if (g + lane < len && e >= lstart) {
-        const double2 p = sp[g + lane];
-        const double dx = __dsub_rn(p.x, q.x), dy = __dsub_rn(p.y, q.y);
-        const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-        const int64_t m = target - (int64_t)(uint32_t)stt[g + lane];
-        hit = m >= 0 && m <= mmax && s_thr[m] <= d2 && d2 < s_thr[m + 1];
-      }
-      const unsigned bal = __ballot_sync(kFull, hit);
-      if (!bal) continue;
+    const int g_begin = max(0, ((lstart - c0) >> 5) << 5);  // groups before lstart hold nothing
+    auto test = [&](int g) -> bool {  // is element c0 + g + lane admissible?
+      const unsigned m = (unsigned)(target - (int)stt[g + lane]);
+      if (g + lane >= len || c0 + g + lane < lstart || m > mmax) return false;
+      const double2 p = sp[g + lane];
+      const double dx = __dsub_rn(p.x, q.x), dy = __dsub_rn(p.y, q.y);
+      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+      const double2 tw = s_pair[m];
+      return tw.x <= d2 && d2 < tw.y;
+    };
+    auto take = [&](int g, unsigned bal, bool hit) {  // append a group's hits in lane order
       const int idx = cnt + __popc(bal & ((1u << lane) - 1u));
-      if (hit && idx < K) o[idx] = lo + e;
+      if (hit && idx < K) o[idx] = lo + c0 + g + lane;
       const int cc = __popc(bal);
       if (cnt + cc >= K) {
         unsigned bm = bal;
@@ -584,6 +591,21 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
       } else {
         cnt += cc;
       }
+    };
+    constexpr int kGU = 4;  // groups per step (independent loads and DP ops in flight)
+    for (int g = g_begin; g < len && !done; g += 32 * kGU) {
+      bool h[kGU];
+      unsigned bl[kGU], any = 0;
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        h[u] = test(g + 32 * u);
+        bl[u] = __ballot_sync(kFull, h[u]);
+        any |= bl[u];
+      }
+      if (!any) continue;
+#pragma unroll
+      for (int u = 0; u < kGU; ++u)
+        if (bl[u] && !done) take(g + 32 * u, bl[u], h[u]);
     }
     // rows still open after this chunk; three counters so that a reset never
     // races with a read (counter k % 3 is read after this barrier, reset after
@@ -601,10 +623,39 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
       issue(k + 2);
     }
   }
-  // an early stop leaves chunk k (issued as k-1+2... i.e. the one after the
-  // last consumed) in flight: it must land before the block exits
+  // an early stop leaves the chunk after the last consumed one in flight:
+  // it must land before the block exits
   if (threadIdx.x == 0 && k < nchunk) mbar_wait(&bar[k & 1], (par >> (k & 1)) & 1u);
-  if (has && lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+  if (!has) return;
+  if (segs == 1) {
+    if (lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+    return;
+  }
+  // publish this piece; the row's last piece merges (first K overall)
+  const int w = r * segs + sg;
+  int prev = 0;
+  if (lane == 0) {
+    S.seg_cnt[w] = cnt;
+    __threadfence();
+    prev = atomicAdd(S.row_cnt + r, 1);
+  }
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != segs - 1) return;
+  __threadfence();
+  int32_t* out = cand + ((size_t)S.shard * S.cap + i) * K;
+  const int wb = r * segs;
+  int tot = 0, rcov = hi;
+  for (int pc = 0; pc < segs && tot < K; ++pc) {
+    const int c = __ldcg(S.seg_cnt + wb + pc);
+    const int32_t* src = S.seg_hits + (size_t)(wb + pc) * K;
+    if (lane < c && tot + lane < K) out[tot + lane] = __ldcg(src + lane);
+    if (tot + c >= K) rcov = __ldcg(src + (K - 1 - tot)) + 1;
+    tot = min(K, tot + c);
+  }
+  if (lane == 0) {
+    meta[(size_t)S.shard * S.cap + i] = make_int2(tot, rcov);
+    S.row_cnt[r] = 0;
+  }
 }
 
 }  // namespace
@@ -636,14 +687,18 @@ cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int
     segs = std::max(1, std::min(segs, kSegWarps / nreq));
   }
   const int blocks = (nreq * segs * 32 + 255) / 256;
-  if (a.thr && segs == 1) {  // many rows: tile kOtfRows rows over shared point chunks
+  if (a.thr && nreq >= 64) {  // many rows: tile kOtfRows rows over shared point chunks
     const size_t smem = 2 * (size_t)kOtfChunk * (sizeof(double2) + (size_t)a.width) +
-                        (size_t)a.thr_n * sizeof(double);
-    const int tblocks = (nreq + kOtfRows - 1) / kOtfRows;
+                        (size_t)a.thr_n * sizeof(double2);
+    const int groups = (nreq + kOtfRows - 1) / kOtfRows;
+    const int chunks = (a.hi - a.lo + kOtfChunk - 1) / kOtfChunk;
+    // enough blocks for ~4 per SM, pieces of >= 4 chunks, within the merge buffers
+    int tsegs = std::max(1, std::min({kMaxSegs, (148 * 4) / groups, chunks / 4, kSegWarps / nreq}));
+    if (!a.seg_hits) tsegs = 1;
     with_width(a.width, [&](auto tag) {
       auto fn = shard_scan_otf_tiled_kernel<decltype(tag)>;
       if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fn<<<tblocks, kOtfRows * 32, smem, s>>>(a, req, nreq, cand, meta);
+      fn<<<groups * tsegs, kOtfRows * 32, smem, s>>>(a, req, nreq, tsegs, cand, meta);
       return 0;
     });
     return cudaGetLastError();
