@@ -247,7 +247,10 @@ class AssignmentOptions:
     ``check_invariants`` switch to the host-synced stepping loop (one phase
     per launch; the device invariant suite after every phase; the
     PhaseSnapshot built from device exports), as the reference runs them
-    inside solve_oriented (assignment.cpp:344-355).  ``storage`` selects the device width of the rounded matrix."""
+    inside solve_oriented (assignment.cpp:344-355).  ``storage`` selects the device width of the rounded matrix.
+    ``costs`` (2-D point instances): "matrix" materialises the rounded kT in HBM, "on_the_fly" never
+    does (the scans round the point costs through the exact threshold table; the
+    sharded driver with one shard), "auto" picks the matrix when it fits in free HBM."""
     eps: float = 0.1
     threads: int = 1
     check_invariants: bool = False
@@ -256,6 +259,7 @@ class AssignmentOptions:
     supply_groups: Optional[np.ndarray] = None
     storage: str = "auto"
     device: int = 0
+    costs: str = "auto"
 
 
 # ---- device context ------------------------------------------------------
@@ -524,11 +528,29 @@ def _check_options(inst: AssignmentInstance, opt: AssignmentOptions) -> None:
             raise ParameterError("copy mode requires n_b <= n_a")
 
 
+def _matrix_fits(inst: AssignmentInstance, opt: AssignmentOptions) -> bool:
+    """Whether the rounded matrix (uint16 rows padded to 256 entries, or
+    uint32 for tiny eps) fits in the device's free memory with a 10 % margin."""
+    import torch
+    ia, ib = max(inst.n_a, inst.n_b), min(inst.n_a, inst.n_b)
+    width = 4 if opt.storage == "u32" or (0 < opt.eps < 1 and math.ceil(1.0 / opt.eps) + 2 > 65533) \
+        else (1 if opt.storage == "u8" else 2)
+    need = ib * ((ia + 511) // 512 * 512) * width
+    free, _ = torch.cuda.mem_get_info(opt.device)
+    return need <= 0.9 * free
+
+
 def solve_assignment(inst: AssignmentInstance, opt: AssignmentOptions):
     """assignment.hpp:137-138 / assignment.cpp:368-400 -> (Matching, SolveStats)."""
     _check_options(inst, opt)
+    if opt.costs not in ("auto", "matrix", "on_the_fly"):
+        raise ParameterError(f"unknown costs mode {opt.costs!r}")
     if opt.observer is not None or opt.check_invariants or opt.demand_groups is not None:
         return _solve_debug(get_solver(opt.device), inst, opt)
+    if inst.pts_a is not None and inst.cost is None and (
+            opt.costs == "on_the_fly" or (opt.costs == "auto" and not _matrix_fits(inst, opt))):
+        from .sharded import solve_assignment_sharded  # one shard, no kT anywhere
+        return solve_assignment_sharded(inst, opt, 1, on_the_fly=True)
     return get_solver(opt.device).solve(inst, opt)
 
 

@@ -294,3 +294,17 @@ def test_explicit_storage_too_narrow_is_parameter_error():
         _solve(_single(0.5), 1e-5, "u16")
     with pytest.raises(otprg.ParameterError):
         _solve(_single(0.5), 0.001, "u8")
+
+
+# ---- costs="on_the_fly" through the public API (north star: costs from the
+# point coordinates when the matrix would not fit in HBM) ---------------------
+
+def test_public_api_on_the_fly_costs(golden):
+    for key in ("square_n10000_eps0.01_s1", "square_n1000_eps0.1_s2", "square_n3000_eps0.02_s1"):
+        w = golden[key]
+        inst = otprg.gen_uniform_square(w["n_a"], w["seed"])
+        m, s = otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=w["eps"], costs="on_the_fly"))
+        _assert_matches_golden(key, w, m, s)
+        assert s.device.get("n_shards") == 1
+    with pytest.raises(otprg.ParameterError):
+        otprg.solve_assignment(_single(0.5), otprg.AssignmentOptions(eps=0.1, costs="bogus"))
