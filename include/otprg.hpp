@@ -169,6 +169,10 @@ struct AssignmentOptions {
   const std::vector<Index>* supply_groups = nullptr;
   int device = 0;   // CUDA device
   int storage = 0;  // otprg_storage (0 = auto)
+  // 2-D point instances (cost empty): 0 auto (on the fly when the rounded
+  // matrix would not fit in free device memory), 1 matrix, 2 on the fly (the
+  // scans round the point costs through the exact threshold table; no kT).
+  int costs = 0;
 };
 
 struct FeasibilityReport {

@@ -14,6 +14,8 @@
 
 #include "../../include/otprg.h"
 
+#include <cuda_runtime.h>
+
 namespace otprg {
 
 namespace {
@@ -352,6 +354,60 @@ FeasibilityReport verify_feasibility(const ScaledCosts& sc, const DualState& dua
   return report_of(f);
 }
 
+namespace {
+// costs = auto: the rounded matrix (uint16, or uint32 below uint16's eps
+// range; rows padded to 256 entries) against the free device memory.
+bool on_the_fly(const AssignmentInstance& inst, const AssignmentOptions& opt) {
+  if (opt.costs == 2) return true;
+  if (opt.costs == 1) return false;
+  const size_t ia = std::max(inst.n_a, inst.n_b), ib = std::min(inst.n_a, inst.n_b);
+  const double need_units = std::ceil(1.0 / opt.eps) + 2.0;
+  const size_t width = opt.storage == OTPRG_STORAGE_U32 || need_units > 65533.0 ? 4 : (opt.storage == OTPRG_STORAGE_U8 ? 1 : 2);
+  const size_t need = ib * ((ia + 511) / 512 * 512) * width;
+  size_t free_b = 0, total_b = 0;
+  if (cudaSetDevice(opt.device) != cudaSuccess || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess)
+    return false;
+  return static_cast<double>(need) > 0.9 * static_cast<double>(free_b);
+}
+
+// One shard, no kT (OTPRG_FLAG_ON_THE_FLY): the per-phase protocol of
+// paper_2203_03732_b200/sharded.py run_phases with a local "exchange".
+void solve_on_the_fly(otprg_ctx* ctx, otprg_problem p, otprg_result* r, int device) {
+  p.flags |= OTPRG_FLAG_ON_THE_FLY;
+  if (cudaSetDevice(device) != cudaSuccess) throw DeviceError("cudaSetDevice");
+  const int32_t K = 16, cap = std::min(p.n_a, p.n_b);
+  std::int32_t bounds[2];
+  check(otprg_shard_prepare(ctx, &p, 1, 0, K, bounds), ctx);
+  int32_t *cand = nullptr, *meta = nullptr;
+  if (cudaMalloc(&cand, static_cast<size_t>(cap) * K * 4) != cudaSuccess ||
+      cudaMalloc(&meta, static_cast<size_t>(cap) * 2 * 4) != cudaSuccess) {
+    cudaFree(cand);
+    throw DeviceError("on-the-fly solve: candidate buffers");
+  }
+  struct Free {
+    int32_t *c, *m;
+    ~Free() {
+      cudaFree(c);
+      cudaFree(m);
+    }
+  } guard{cand, meta};
+  check(otprg_shard_begin(ctx), ctx);
+  while (true) {
+    int32_t n = 0, fin = 0;
+    check(otprg_shard_top(ctx, &n, &fin), ctx);
+    if (fin) break;
+    check(otprg_shard_scan(ctx, cand, meta, n, 0), ctx);
+    int32_t parked = 0;
+    check(otprg_shard_da(ctx, cand, meta, n, 0, &parked), ctx);
+    while (parked > 0) {
+      check(otprg_shard_scan(ctx, cand, meta, n, 1), ctx);
+      check(otprg_shard_da(ctx, cand, meta, n, 1, &parked), ctx);
+    }
+  }
+  check(otprg_shard_finish(ctx, r), ctx);
+}
+}  // namespace
+
 std::pair<Matching, SolveStats> solve_assignment(const AssignmentInstance& inst,
                                                  const AssignmentOptions& opt) {
   inst.validate();
@@ -366,8 +422,12 @@ std::pair<Matching, SolveStats> solve_assignment(const AssignmentInstance& inst,
   }
   otprg_ctx* ctx = context(opt.device);
   if (opt.observer || opt.check_invariants || opt.demand_groups) return solve_debug(ctx, inst, opt);
-  const otprg_problem p = problem_of(inst, opt.eps, opt.storage);
+  otprg_problem p = problem_of(inst, opt.eps, opt.storage);
   ResultBufs rb(inst.n_a, inst.n_b, opt.eps);
+  if (p.cost_kind == OTPRG_COST_POINTS2D && on_the_fly(inst, opt)) {
+    solve_on_the_fly(ctx, p, &rb.r, opt.device);
+    return rb.take();
+  }
   check(otprg_solve_assignment(ctx, &p, &rb.r), ctx);
   return rb.take();
 }

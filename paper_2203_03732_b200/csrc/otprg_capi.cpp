@@ -79,6 +79,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   if (st) return st;
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   ctx->prepared = false;
+  ctx->sharded = false;  // (a shard_prepare on this context is superseded)
   ctx->n_a = p->n_a;
   ctx->n_b = p->n_b;
   ctx->swapped = p->n_b > p->n_a;  // assignment.cpp:385-399

@@ -81,6 +81,11 @@ static void assignment_cases() {
     auto [mp, sp] = otprg::solve_assignment(gp, go);
     same_result(mr, sr, mp, sp, "square points");
     EXPECT(otpr::matching_cost(mr, r) == otprg::matching_cost(mp, gp), "points matching_cost bits");
+    // costs on the fly (no rounded matrix anywhere; threshold table)
+    otprg::AssignmentOptions gf = go;
+    gf.costs = 2;
+    auto [mf, sf] = otprg::solve_assignment(gp, gf);
+    same_result(mr, sr, mf, sf, "square points, costs on the fly");
   }
   for (auto [na, nb] : {std::pair{300, 170}, std::pair{170, 300}}) {
     const otpr::AssignmentInstance r = random_instance(na, nb, 40 + na);
