@@ -13,9 +13,13 @@
 namespace otprg {
 
 // Grow-only device buffer.
-struct DevBuf {
+struct DevBuf {  // owning, move-free device buffer (freed with its context)
   void* p = nullptr;
   size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
   cudaError_t ensure(size_t bytes) {
     if (bytes <= n) return cudaSuccess;
     if (p) cudaFree(p);

@@ -14,6 +14,7 @@ from paper_2203_03732_b200 import sharded  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 600.0
 seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+verbose = len(sys.argv) > 3 and sys.argv[3] == "-v"
 orc = Oracle.get()
 t_end = time.time() + budget
 case = 0
@@ -36,11 +37,21 @@ def family_cost(rng, n_a, n_b, fam):
     raise ValueError(fam)
 
 
+only = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else None
 while time.time() < t_end:
     case += 1
+    if only is not None:
+        if not only:
+            break
+        case = only.pop(0)
     seed = seed0 * 1_000_003 + case
     rng = np.random.default_rng(seed)
-    kind = rng.choice(["dense", "dense", "dense", "points", "sharded"])
+    if verbose:
+        print(f"start case {case} seed {seed}", flush=True)
+    if case % 1000 == 0:
+        import torch
+        print(f"case {case}: free device memory {torch.cuda.mem_get_info(0)[0] / 2**30:.2f} GiB", flush=True)
+    kind = rng.choice(["dense", "dense", "dense", "points", "sharded", "otf"])
     if kind == "dense":
         n_a, n_b = int(rng.integers(1, 1500)), int(rng.integers(1, 1500))
         fam = str(rng.choice(["uniform", "levels", "lowrank", "tiny"]))
@@ -77,13 +88,16 @@ while time.time() < t_end:
                   and np.array_equal(ref_s.duals_final.y_b, want.y_b) and ref_s.device["cost"] == want.cost)
             tag = f"points {n}x{n_b} eps={eps:.3g}"
         else:
-            G, K = int(rng.integers(2, 6)), int(rng.choice([1, 2, 4, 16]))
-            m2, s2 = sharded.solve_assignment_sharded(inst, otprg.AssignmentOptions(eps=eps), G, K=K)
+            G, K = int(rng.integers(1 if kind == "otf" else 2, 6)), int(rng.choice([1, 2, 4, 16]))
+            m2, s2 = sharded.solve_assignment_sharded(inst, otprg.AssignmentOptions(eps=eps), G, K=K,
+                                                      on_the_fly=kind == "otf")
             ok = (np.array_equal(ref_m.match_of_a, m2.match_of_a) and s2.phases == ref_s.phases
                   and np.array_equal(ref_s.duals_final.y_a, s2.duals_final.y_a)
                   and np.array_equal(ref_s.duals_final.y_b, s2.duals_final.y_b))
-            tag = f"sharded {n}x{n_b} eps={eps:.3g} G={G} K={K}"
+            tag = f"{kind} {n}x{n_b} eps={eps:.3g} G={G} K={K}"
     counts[kind] = counts.get(kind, 0) + 1
+    if verbose:
+        print(f"ok case {case} seed {seed}: {tag}", flush=True)
     if not ok:
         bad += 1
         print(f"MISMATCH case {case} seed {seed}: {tag}", flush=True)
