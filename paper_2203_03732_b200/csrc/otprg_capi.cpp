@@ -1185,7 +1185,8 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   CK(ctx->lmeta.ensure(ib * 16), "alloc low-set meta");
   CK(ctx->lists.ensure(3 * ib * 4), "alloc lists");
   CK(ctx->mps.ensure(2 * ib * 8), "alloc mp lists");
-  CK(ctx->fa.ensure(ia * 4), "alloc scratch");
+  // completion scratch, and the compaction's per-block counts during the phases (>= 148 ints)
+  CK(ctx->fa.ensure(std::max<size_t>(ia, 1024) * 4), "alloc scratch");
   CK(ctx->fb.ensure(ib * 4), "alloc scratch");
   CK(ctx->ctl.ensure(sizeof(Ctl)), "alloc ctl");
   CK(ctx->sh_bounds.ensure((n_shards + 1) * sizeof(int)), "alloc bounds");
