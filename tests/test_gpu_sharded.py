@@ -169,3 +169,20 @@ def test_on_the_fly_rejects_tiny_eps():
     inst = otprg.gen_uniform_square(50, 1)
     with pytest.raises(otprg.ParameterError):
         sharded.solve_assignment_sharded(inst, otprg.AssignmentOptions(eps=1e-4), 1, on_the_fly=True)
+
+
+@pytest.mark.parametrize("otf", [False, True])
+def test_tiny_instances_with_empty_shards(otf):
+    """n below the 512-element shard granularity (all but the last shard
+    empty) and below the compaction's 148 blocks, many times over."""
+    rng = np.random.default_rng(23)
+    for trial in range(40):
+        n_a, n_b = int(rng.integers(1, 150)), int(rng.integers(1, 150))
+        inst = otprg.AssignmentInstance(n_a, n_b, pts_a=rng.random((n_a, 2)), pts_b=rng.random((n_b, 2)))
+        opt = otprg.AssignmentOptions(eps=float(rng.choice([0.01, 0.05, 0.2])))
+        m1, s1 = otprg.solve_assignment(inst, opt)
+        m2, s2 = sharded.solve_assignment_sharded(inst, opt, int(rng.integers(1, 5)), K=int(rng.choice([1, 16])),
+                                                  on_the_fly=otf)
+        assert np.array_equal(m1.match_of_a, m2.match_of_a), trial
+        assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b), trial
+        assert s1.phases == s2.phases, trial
