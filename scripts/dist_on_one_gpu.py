@@ -26,10 +26,12 @@ rank, world = dist.get_rank(), dist.get_world_size()
 torch.cuda.set_device(0)
 golden = json.load(open("tests/golden/assign_pins.json"))
 ok = True
-for key in ("square_n4000_eps0.01_s1", "square_n10000_eps0.01_s2", "square_n10000_eps0.1_s1"):
+for key, otf in (("square_n4000_eps0.01_s1", False), ("square_n10000_eps0.01_s2", False),
+                 ("square_n10000_eps0.1_s1", False), ("square_n4000_eps0.01_s1", True),
+                 ("square_n10000_eps0.01_s2", True)):
     w = golden[key]
     inst = otprg.gen_uniform_square(w["n_a"], w["seed"])
-    sv = ShardedSolver(inst, otprg.AssignmentOptions(eps=w["eps"]), distributed=True, K=4)
+    sv = ShardedSolver(inst, otprg.AssignmentOptions(eps=w["eps"]), distributed=True, K=4, on_the_fly=otf)
     t0 = time.perf_counter()
     m, s = sv.solve()
     ms = (time.perf_counter() - t0) * 1e3
@@ -39,7 +41,7 @@ for key in ("square_n4000_eps0.01_s1", "square_n10000_eps0.01_s2", "square_n1000
     same = all(got[k] == w[k] for k in PIN_KEYS)
     ok &= same
     if rank == 0:
-        print(f"{key}: world={world} bit-exact={same} phases={s.phases} refills={s.device['refill_rounds']} "
+        print(f"{key} otf={otf}: world={world} bit-exact={same} phases={s.phases} refills={s.device['refill_rounds']} "
               f"wall={ms:.1f} ms", flush=True)
 # n = 100k: the two-rank result equals the fused single-GPU solver
 inst = otprg.gen_uniform_square(100_000, 1)
