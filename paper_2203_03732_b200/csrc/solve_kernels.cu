@@ -56,6 +56,12 @@ constexpr int kBlock = OTPRG_BLOCK;
 #define OTPRG_TEAMS 1
 #endif
 constexpr bool kTeams = OTPRG_TEAMS != 0;  // multi-warp rows in small phases
+#ifndef OTPRG_TEAM_OVERSUB
+#define OTPRG_TEAM_OVERSUB 1
+#endif
+#ifndef OTPRG_TEAM_DEN
+#define OTPRG_TEAM_DEN 1
+#endif
 #ifndef OTPRG_BULK
 #define OTPRG_BULK 1
 #endif
@@ -667,9 +673,10 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     // static, striped across blocks; the rest are grabbed from a counter.
     int tsize = 1;  // (proposers are assigned by slot: size by the slot count)
     if (kTeams) {
-      if (n_slots * 8 <= total_warps) tsize = 8;
-      else if (n_slots * 4 <= total_warps) tsize = 4;
-      else if (n_slots * 2 <= total_warps) tsize = 2;
+      const int tw = total_warps * OTPRG_TEAM_OVERSUB / OTPRG_TEAM_DEN;  // (team size vs the warps)
+      if (n_slots * 8 <= tw) tsize = 8;
+      else if (n_slots * 4 <= tw) tsize = 4;
+      else if (n_slots * 2 <= tw) tsize = 2;
     }
     // (phase 1's lists come from the streaming propose kernel when it ran)
     const bool bulk = kBulk && n >= total_warps && !(phase == 1 && A.pre_scanned);
