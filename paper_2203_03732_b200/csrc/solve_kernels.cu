@@ -68,7 +68,7 @@ constexpr bool kTeams = OTPRG_TEAMS != 0;  // multi-warp rows in small phases
 constexpr bool kBulk = OTPRG_BULK != 0;  // streaming list build in large phases
 constexpr int kUnroll = 4;       // 128-bit loads in flight per lane (global t)
 #ifndef OTPRG_UNROLL_SMEM
-#define OTPRG_UNROLL_SMEM 8
+#define OTPRG_UNROLL_SMEM 4  // A/B (scripts/ab_unroll.sh): 2 / 4 / 6 / 8 / 16 -> 3.44 / 3.34 / 3.46 / 3.72 / 5.21 ms
 #endif
 constexpr int kUnrollSmem = OTPRG_UNROLL_SMEM;  // (t in shared memory)
 
