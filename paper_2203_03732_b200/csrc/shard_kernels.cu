@@ -31,6 +31,10 @@ namespace otprg {
 
 namespace {
 
+#ifndef OTPRG_SHARD_UNROLL
+#define OTPRG_SHARD_UNROLL 12  // A/B (scripts/ab_shard_unroll.sh): 4 / 8 / 12 / 16 / 24 -> 13.6 / 13.5 / 12.1 / 15.8 / 18.3 ms
+#endif
+
 __device__ __forceinline__ uint32_t t_get(const ShardArgs& S, int a) {
   return S.width == 1   ? (uint32_t)static_cast<const uint8_t*>(S.t)[a]
          : S.width == 2 ? (uint32_t)static_cast<const uint16_t*>(S.t)[a]
@@ -59,7 +63,7 @@ __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4
                                                          int2* __restrict__ meta) {
   using SD = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
-  constexpr int kU = 8;  // 4 KB per warp step (long rows: n = 100k rows are 200 KB)
+  constexpr int kU = OTPRG_SHARD_UNROLL;  // 16-byte loads in flight per lane (12: 6 KB per warp step)
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= nreq * segs) return;
