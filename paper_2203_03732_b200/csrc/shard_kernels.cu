@@ -491,7 +491,13 @@ __global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const 
 // phases: few row groups) splits the chunk range of a row group into pieces
 // on separate blocks, merged per row like shard_scan_kernel's pieces.  The
 // threshold table is staged as pairs (thr[m], thr[m+1]): one 16-byte load.
-constexpr int kOtfRows = 16, kOtfChunk = 1024;
+#ifndef OTPRG_OTF_ROWS
+#define OTPRG_OTF_ROWS 16
+#endif
+#ifndef OTPRG_OTF_GU
+#define OTPRG_OTF_GU 4
+#endif
+constexpr int kOtfRows = OTPRG_OTF_ROWS, kOtfChunk = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(ShardArgs S,
@@ -596,7 +602,7 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
         cnt += cc;
       }
     };
-    constexpr int kGU = 4;  // groups per step (independent loads and DP ops in flight)
+    constexpr int kGU = OTPRG_OTF_GU;  // groups per step (independent loads and DP ops in flight)
     for (int g = g_begin; g < len && !done; g += 32 * kGU) {
       bool h[kGU];
       unsigned bl[kGU], any = 0;
