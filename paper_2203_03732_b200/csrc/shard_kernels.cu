@@ -578,15 +578,20 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
     const int len = min(kOtfChunk, width_local - c0);
     const double2* sp = reinterpret_cast<const double2*>(s_dyn + (size_t)(k & 1) * kStage);
     const T* stt = reinterpret_cast<const T*>(s_dyn + (size_t)(k & 1) * kStage + (size_t)kOtfChunk * sizeof(double2));
-    const int g_begin = max(0, ((lstart - c0) >> 5) << 5);  // groups before lstart hold nothing
+    // steps of 32 * kGU elements from a multiple of 32 * kGU (elements
+    // before lstart are masked), so every index stays inside the stage
+    const int g_begin = max(0, ((lstart - c0) / (32 * OTPRG_OTF_GU)) * (32 * OTPRG_OTF_GU));
     auto test = [&](int g) -> bool {  // is element c0 + g + lane admissible?
-      const unsigned m = (unsigned)(target - (int)stt[g + lane]);
-      if (g + lane >= len || c0 + g + lane < lstart || m > mmax) return false;
-      const double2 p = sp[g + lane];
+      // branch-free: the kernel is issue-bound, and an early return costs a
+      // reconvergence region (BSSY/BSYNC + a divergence check) per element;
+      // out-of-range lanes compute on stale stage data and are masked
+      const int e = g + lane;
+      const unsigned m = (unsigned)(target - (int)stt[e]);
+      const double2 p = sp[e];
       const double dx = __dsub_rn(p.x, q.x), dy = __dsub_rn(p.y, q.y);
       const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-      const double2 tw = s_pair[m];
-      return tw.x <= d2 && d2 < tw.y;
+      const double2 tw = s_pair[min(m, mmax)];
+      return (e < len) & (c0 + e >= lstart) & (m <= mmax) & (tw.x <= d2) & (d2 < tw.y);
     };
     auto take = [&](int g, unsigned bal, bool hit) {  // append a group's hits in lane order
       const int idx = cnt + __popc(bal & ((1u << lane) - 1u));

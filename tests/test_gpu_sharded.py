@@ -186,3 +186,36 @@ def test_tiny_instances_with_empty_shards(otf):
         assert np.array_equal(m1.match_of_a, m2.match_of_a), trial
         assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b), trial
         assert s1.phases == s2.phases, trial
+
+
+@pytest.mark.parametrize("shift,scale", [(0.0, 1.0), (1000.0, 1.0), (-3.5e4, 0.7), (0.25, 1e-3)])
+def test_on_the_fly_float_prefilter_bounds(shift, scale):
+    """The tiled on-the-fly scan rejects most elements with a float test
+    widened by E (from the sets' half-extent after centring); only the
+    double test decides admissibility.  Shifted / scaled point sets (costs
+    still in [0, 1]) must give the dense solver's result bit for bit."""
+    rng = np.random.default_rng(31)
+    n = 3000
+    pa = shift + scale * rng.random((n, 2))
+    pb = shift + scale * rng.random((n, 2))
+    inst = otprg.AssignmentInstance(n, n, pts_a=pa, pts_b=pb)
+    opt = otprg.AssignmentOptions(eps=0.01)
+    m1, s1 = otprg.solve_assignment(inst, opt)
+    m2, s2 = sharded.solve_assignment_sharded(inst, opt, 2, K=16, on_the_fly=True)
+    assert np.array_equal(m1.match_of_a, m2.match_of_a)
+    assert np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a)
+    assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b)
+    assert np.array_equal(s1.free_counts, s2.free_counts)
+    assert s1.device["cost"] == s2.device["cost"]
+
+
+@pytest.mark.slow
+def test_on_the_fly_100k_vs_single():
+    inst = otprg.gen_uniform_square(100_000, 1)
+    opt = otprg.AssignmentOptions(eps=0.01)
+    m1, s1 = otprg.solve_assignment(inst, opt)
+    m2, s2 = sharded.solve_assignment_sharded(inst, opt, 1, on_the_fly=True)
+    assert np.array_equal(m1.match_of_a, m2.match_of_a)
+    assert np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a)
+    assert np.array_equal(s1.duals_final.y_b, s2.duals_final.y_b)
+    assert s1.phases == s2.phases and s1.sum_ni == s2.sum_ni
