@@ -105,6 +105,7 @@ struct ShardArgs {
   const double2* pb;
   const double* thr;
   int thr_n;
+  bool first_phase;  // scans of phase 1 (t == 0, every target 0): picks the level-0 scan
 };
 constexpr int kSegWarps = 32768;
 constexpr int kMaxSegs = 32;

@@ -1303,6 +1303,7 @@ int otprg_shard_scan(otprg_ctx* ctx, int32_t* cand, int32_t* meta_words, int32_t
   S.cap = cap;
   const int4* req = refill ? ctx->sh_park[ctx->sh_park_cur].as<int4>() : nullptr;
   const int nreq = refill ? ctx->sh_parked : ctx->sh_n;
+  S.first_phase = ctx->sh_phase == 0;  // init_state: Y == 0 on A, 1 on B
   CK(otprg::launch_shard_scan(S, req, nreq, cand, meta, ctx->stream), "shard_scan launch");
   // no sync: the exchange and the DA are ordered after the scan on the
   // context's stream (otprg_set_stream puts every rank of a process and the

@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const 
 #endif
 constexpr int kOtfRows = OTPRG_OTF_ROWS, kOtfChunk = 1024;
 
-template <typename T>
+template <typename T, bool kP1>
 __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(ShardArgs S,
                                                                             const int4* __restrict__ req,
                                                                             int nreq, int segs,
@@ -563,9 +563,9 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
     unsigned char* st = s_dyn + (size_t)(k & 1) * kStage;
     const unsigned pb_bytes = (unsigned)len * 16u;
     const unsigned tb = (unsigned)(((size_t)len * sizeof(T) + 15) & ~(size_t)15);
-    mbar_expect_tx(&bar[k & 1], pb_bytes + tb);
+    mbar_expect_tx(&bar[k & 1], pb_bytes + (kP1 ? 0u : tb));
     bulk_g2s(st, pa + c0, pb_bytes, &bar[k & 1]);
-    bulk_g2s(st + (size_t)kOtfChunk * sizeof(double2), tl + c0, tb, &bar[k & 1]);
+    if (!kP1) bulk_g2s(st + (size_t)kOtfChunk * sizeof(double2), tl + c0, tb, &bar[k & 1]);
   };
   if (threadIdx.x == 0)
     for (int k = 0; k < min(2, nchunk); ++k) issue(k);
@@ -580,18 +580,23 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
     const T* stt = reinterpret_cast<const T*>(s_dyn + (size_t)(k & 1) * kStage + (size_t)kOtfChunk * sizeof(double2));
     // steps of 32 * kGU elements from a multiple of 32 * kGU (elements
     // before lstart are masked), so every index stays inside the stage
+    const double thr1 = s_pair[0].y;
     const int g_begin = max(0, ((lstart - c0) / (32 * OTPRG_OTF_GU)) * (32 * OTPRG_OTF_GU));
     auto test = [&](int g) -> bool {  // is element c0 + g + lane admissible?
       // branch-free: the kernel is issue-bound, and an early return costs a
       // reconvergence region (BSSY/BSYNC + a divergence check) per element;
       // out-of-range lanes compute on stale stage data and are masked
       const int e = g + lane;
-      const unsigned m = (unsigned)(target - (int)stt[e]);
       const double2 p = sp[e];
       const double dx = __dsub_rn(p.x, q.x), dy = __dsub_rn(p.y, q.y);
       const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-      const double2 tw = s_pair[min(m, mmax)];
-      return (e < len) & (c0 + e >= lstart) & (m <= mmax) & (tw.x <= d2) & (d2 < tw.y);
+      if constexpr (kP1) {  // phase 1: t == 0 and target == 0, so level 0: d2 < thr[1]
+        return (e < len) & (c0 + e >= lstart) & (d2 < thr1);
+      } else {
+        const unsigned m = (unsigned)(target - (int)stt[e]);
+        const double2 tw = s_pair[min(m, mmax)];
+        return (e < len) & (c0 + e >= lstart) & (m <= mmax) & (tw.x <= d2) & (d2 < tw.y);
+      }
     };
     auto take = [&](int g, unsigned bal, bool hit) {  // append a group's hits in lane order
       const int idx = cnt + __popc(bal & ((1u << lane) - 1u));
@@ -710,8 +715,11 @@ cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int
     // enough blocks for ~4 per SM, pieces of >= 4 chunks, within the merge buffers
     int tsegs = std::max(1, std::min({kMaxSegs, (148 * 4) / groups, chunks / 4, kSegWarps / nreq}));
     if (!a.seg_hits) tsegs = 1;
+    // phase 1 (every t(a) == 0 and every target == 0 after init_state): the
+    // level-0 test d2 < thr[1] alone, no t stage
     with_width(a.width, [&](auto tag) {
-      auto fn = shard_scan_otf_tiled_kernel<decltype(tag)>;
+      auto fn = a.first_phase ? shard_scan_otf_tiled_kernel<decltype(tag), true>
+                              : shard_scan_otf_tiled_kernel<decltype(tag), false>;
       if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       fn<<<groups * tsegs, kOtfRows * 32, smem, s>>>(a, req, nreq, tsegs, cand, meta);
       return 0;
