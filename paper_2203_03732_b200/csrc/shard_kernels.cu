@@ -57,7 +57,7 @@ __device__ __forceinline__ void t_set(const ShardArgs& S, int a, uint32_t v) {
 // piece in S.seg_hits, and the last warp of the request to finish merges the
 // pieces in order (the first K hits overall; resume after the K-th), so a
 // 200 KB row costs a few dependent steps instead of ~50.
-template <typename T>
+template <typename T, bool kP1>
 __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4* __restrict__ req,
                                                          int nreq, int segs, int32_t* __restrict__ cand,
                                                          int2* __restrict__ meta) {
@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4
         const int vi = v + j * 32 + lane;
         if (vi < ve) {
           kr[j] = __ldg(rv + vi);
-          tr[j] = __ldcg(tv + vi);
+          // phase 1: t == 0 everywhere (init_state), no t traffic
+          tr[j] = kP1 ? make_uint4(0u, 0u, 0u, 0u) : __ldcg(tv + vi);
         } else {
           kr[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
           tr[j] = make_uint4(0u, 0u, 0u, 0u);
@@ -737,7 +738,10 @@ cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int
     return cudaGetLastError();
   }
   with_width(a.width, [&](auto tag) {
-    shard_scan_kernel<decltype(tag)><<<blocks, 256, 0, s>>>(a, req, nreq, segs, cand, meta);
+    if (a.first_phase)
+      shard_scan_kernel<decltype(tag), true><<<blocks, 256, 0, s>>>(a, req, nreq, segs, cand, meta);
+    else
+      shard_scan_kernel<decltype(tag), false><<<blocks, 256, 0, s>>>(a, req, nreq, segs, cand, meta);
     return 0;
   });
   return cudaGetLastError();
