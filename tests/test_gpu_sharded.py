@@ -189,11 +189,11 @@ def test_tiny_instances_with_empty_shards(otf):
 
 
 @pytest.mark.parametrize("shift,scale", [(0.0, 1.0), (1000.0, 1.0), (-3.5e4, 0.7), (0.25, 1e-3)])
-def test_on_the_fly_float_prefilter_bounds(shift, scale):
-    """The tiled on-the-fly scan rejects most elements with a float test
-    widened by E (from the sets' half-extent after centring); only the
-    double test decides admissibility.  Shifted / scaled point sets (costs
-    still in [0, 1]) must give the dense solver's result bit for bit."""
+def test_on_the_fly_shifted_scaled_points(shift, scale):
+    """The on-the-fly scans test thr[m] <= d2 < thr[m+1] on the double
+    points (branch-free, out-of-range lanes masked).  Shifted / scaled point
+    sets (costs still in [0, 1]) must give the dense solver's result bit for
+    bit."""
     rng = np.random.default_rng(31)
     n = 3000
     pa = shift + scale * rng.random((n, 2))
