@@ -498,7 +498,10 @@ __global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const 
 #ifndef OTPRG_OTF_GU
 #define OTPRG_OTF_GU 4
 #endif
-constexpr int kOtfRows = OTPRG_OTF_ROWS, kOtfChunk = 1024;
+#ifndef OTPRG_OTF_CHUNK
+#define OTPRG_OTF_CHUNK 2048
+#endif
+constexpr int kOtfRows = OTPRG_OTF_ROWS, kOtfChunk = OTPRG_OTF_CHUNK;
 
 template <typename T, bool kP1>
 __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(ShardArgs S,
