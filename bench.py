@@ -57,6 +57,15 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
            0x100: "display_clock_setting"}
 
 
+def ctype(width: int) -> str:
+    """C type of a kT entry of `width` bytes (labels of kernels and storage)."""
+    return {1: "uint8_t", 2: "uint16_t", 4: "uint32_t"}[width]
+
+
+def dtype_of(width: int) -> str:
+    return {1: "u8", 2: "u16", 4: "u32"}[width]
+
+
 def peaks() -> tuple[float, str]:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -110,16 +119,68 @@ class ClockSampler:
                 "reasons": sorted(reasons - {"gpu_idle"}), "samples": len(sm), "source": "nvml"}
 
 
+SHARE_GPU_ENV = "OTPRG_BENCH_SHARE_GPU"  # documented one-GPU override (see relaunch())
+
+
+def share_gpu() -> bool:
+    return os.environ.get(SHARE_GPU_ENV, "") not in ("", "0")
+
+
 def dist_setup():
+    """One rank per GPU (RANK/LOCAL_RANK/WORLD_SIZE from torchrun), NCCL.
+    With OTPRG_BENCH_SHARE_GPU=1 every rank runs on GPU OTPRG_DEVICE (default
+    0) and the process group is gloo: a functional check of the N-rank path
+    on a one-GPU box (timings are then not a scaling point)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if share_gpu():
+        local = int(os.environ.get("OTPRG_DEVICE", "0"))
+        os.environ["OTPRG_DEVICE"] = str(local)
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu():
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def visible_gpus() -> int:
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        n = pynvml.nvmlDeviceGetCount()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis is not None:
+            n = min(n, len([v for v in vis.split(",") if v.strip() != ""]))
+        return n
+    except Exception:
+        import torch
+        return torch.cuda.device_count()
+
+
+def relaunch(n: int) -> None:
+    """`bench.py --gpus N` (N > 1) started without torchrun: re-execute under
+    torch.distributed.run with one process per GPU (the driver's own launch
+    form).  Fewer than N visible GPUs is an error (exit 2) unless
+    OTPRG_BENCH_SHARE_GPU=1 puts every rank on one GPU (gloo exchange)."""
+    have = visible_gpus()
+    if have < n and not share_gpu():
+        print(json.dumps({"error": f"--gpus {n} needs {n} visible GPUs, found {have} "
+                                   f"(set {SHARE_GPU_ENV}=1 to run every rank on one GPU)"}),
+              file=sys.stderr, flush=True)
+        sys.exit(2)
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def allreduce_max(x: float, world: int) -> float:
@@ -229,7 +290,7 @@ def run_ours(args, world, rank, local) -> None:
     a_loop = float(np.mean(loop_ach))
     roofline = {
         "bound": "hbm",
-        "kernel": f"phase_loop_kernel<{'uint8_t' if width == 1 else 'uint16_t'},true> "
+        "kernel": f"phase_loop_kernel<{ctype(width)},true> "
                   "(all phases' proposal chains + phases >= 2 scans, one launch)",
         "achieved": round(a_loop, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
         "frac": round(a_loop / peak, 4),
@@ -238,7 +299,7 @@ def run_ours(args, world, rank, local) -> None:
         "launch_ms": round(loop_ms, 4),
         "share_of_step": round(loop_ms / float(np.mean(steps)), 3),
         "propose_scan": {
-            "kernel": f"propose_stream_kernel<{'uint8_t' if width == 1 else 'uint16_t'}> "
+            "kernel": f"propose_stream_kernel<{ctype(width)}> "
                       "(phase-1 propose scan, n_i = n, one launch per step)",
             "achieved": round(float(np.mean(p1_ach)), 1),
             "frac": round(float(np.mean(p1_ach)) / peak, 4),
@@ -254,9 +315,9 @@ def run_ours(args, world, rank, local) -> None:
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8" if width == 1 else "u16", "data": "synthetic",
+        "dtype": dtype_of(width), "data": "synthetic",
         "config": {"workload": f"config 2: gen_uniform_square(n={N}, seeds 1/2/3 rotating), "
-                               f"eps={EPS}, rounded cost matrix resident ({'uint8' if width == 1 else 'uint16'} "
+                               f"eps={EPS}, rounded cost matrix resident ({ctype(width)[:-2]} "
                                "B-major kT)",
                    "l2": f"inputs larger than L2: each step's kT is {N * N * width // 10**6} MB "
                          f"(> 126 MB L2) and 3 instances rotate ({3 * N * N * width // 10**6} MB), "
@@ -500,6 +561,14 @@ def main() -> None:
     ap.add_argument("--no-config4", action="store_true",
                     help="skip the 1-GPU config-4 point in the config-2 line")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args.gpus)  # does not return
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}"}),
+              file=sys.stderr, flush=True)
+        sys.exit(2)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup() if args.impl == "ours" or int(os.environ.get("WORLD_SIZE", "1")) == 1 \
         else (int(os.environ["WORLD_SIZE"]), int(os.environ.get("RANK", "0")), 0)

@@ -241,6 +241,12 @@ int otprg_verify_host(otprg_ctx* ctx, int32_t n_a, int32_t n_b, const int32_t* k
                       int32_t unit_ceil, const int64_t* y_a, const int64_t* y_b,
                       const int32_t* match_of_a, const int32_t* match_of_b,
                       otprg_feasibility* out);
+/* verify_feasibility of a solver result (internal orientation, pre-completion
+ * matching, e.g. from otprg_snapshot of another context — a sharded or
+ * on-the-fly solve of the same instance) against this context's prepared
+ * rounded costs: the check for sizes where no host k matrix fits (n = 100k). */
+int otprg_verify_result(otprg_ctx* ctx, const int64_t* y_a, const int64_t* y_b,
+                        const int32_t* match_of_a, const int32_t* match_of_b, otprg_feasibility* out);
 /* collect_workset's B' and E' for the current state (assignment.cpp:107-147,
  * internal orientation): b_free ascending (n_free entries, caller buffer of
  * n_b), offsets[n_free + 1] and the admissible a of every free b ascending in
@@ -479,6 +485,11 @@ int otprg_ot_scale_and_round(int32_t n_a, int32_t n_b, const double* mu, const d
  * including OTInstance::renormalize (ot.cpp:91-100).  Host-only. */
 int otprg_random_ot_rational(int32_t n_a, int32_t n_b, uint64_t seed, double* mu, double* nu,
                              double* cost);
+
+/* Free and total device memory of `device` (cudaMemGetInfo), for callers that
+ * choose between the materialised matrix and on-the-fly costs
+ * (AssignmentOptions costs = auto) without a CUDA runtime of their own. */
+int otprg_mem_info(int device, uint64_t* free_bytes, uint64_t* total_bytes);
 
 /* Writes a buffer larger than L2 on the context's stream (benchmark hygiene). */
 int otprg_flush_l2(otprg_ctx* ctx);

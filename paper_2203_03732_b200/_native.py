@@ -101,6 +101,7 @@ EXPORTS = [
     "otprg_groups_step", "otprg_groups_finish", "otprg_verify_feasibility", "otprg_verify_host", "otprg_admissible",
     "otprg_solve_ot_opts", "otprg_solve_copy_matching", "otprg_copy_state",
     "otprg_check_cluster_state", "otprg_plan_from_flow", "otprg_points_threshold_table",
+    "otprg_mem_info", "otprg_verify_result",
 ]
 
 _lib = None
@@ -136,6 +137,7 @@ def lib() -> C.CDLL:
                                           C.POINTER(C.c_int32)]
     L.otprg_uniform_square_points.argtypes = [C.c_int32, C.c_uint64, vp, vp]
     L.otprg_flush_l2.argtypes = [vp]
+    L.otprg_mem_info.argtypes = [C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
     L.otprg_begin.argtypes = [vp]
     L.otprg_step.argtypes = [vp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.otprg_snapshot.argtypes = [vp, C.POINTER(Result)]
@@ -173,6 +175,7 @@ def lib() -> C.CDLL:
     L.otprg_verify_feasibility.argtypes = [vp, C.POINTER(Feasibility)]
     L.otprg_verify_host.argtypes = [vp, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp, vp, vp,
                                     C.POINTER(Feasibility)]
+    L.otprg_verify_result.argtypes = [vp, vp, vp, vp, vp, C.POINTER(Feasibility)]
     L.otprg_admissible.argtypes = [vp, vp, vp, vp, C.c_int64, C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int64)]
     _lib = L

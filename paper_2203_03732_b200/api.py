@@ -425,6 +425,21 @@ class Solver:
             self._raise(st)
         return _report(f)
 
+    def verify_result(self, duals: DualState, m: Matching) -> FeasibilityReport:
+        """verify_feasibility of a result state (internal orientation,
+        pre-completion matching) against this solver's prepared rounded costs
+        on the device (no host k matrix: the n = 100k check)."""
+        ya = np.ascontiguousarray(duals.y_a, np.int64)
+        yb = np.ascontiguousarray(duals.y_b, np.int64)
+        ma = np.ascontiguousarray(m.match_of_a, np.int32)
+        mb = np.ascontiguousarray(m.match_of_b, np.int32)
+        f = N.Feasibility()
+        st = self._L.otprg_verify_result(self._ctx, ya.ctypes.data, yb.ctypes.data, ma.ctypes.data,
+                                         mb.ctypes.data, C.byref(f))
+        if st:
+            self._raise(st)
+        return _report(f)
+
     def verify_host(self, sc: "ScaledCosts", duals: DualState, m: Matching) -> FeasibilityReport:
         k = np.ascontiguousarray(sc.k, np.int32)
         n_a, n_b = k.shape
@@ -531,13 +546,14 @@ def _check_options(inst: AssignmentInstance, opt: AssignmentOptions) -> None:
 def _matrix_fits(inst: AssignmentInstance, opt: AssignmentOptions) -> bool:
     """Whether the rounded matrix (uint16 rows padded to 256 entries, or
     uint32 for tiny eps) fits in the device's free memory with a 10 % margin."""
-    import torch
     ia, ib = max(inst.n_a, inst.n_b), min(inst.n_a, inst.n_b)
     width = 4 if opt.storage == "u32" or (0 < opt.eps < 1 and math.ceil(1.0 / opt.eps) + 2 > 65533) \
         else (1 if opt.storage == "u8" else 2)
     need = ib * ((ia + 511) // 512 * 512) * width
-    free, _ = torch.cuda.mem_get_info(opt.device)
-    return need <= 0.9 * free
+    free, total = C.c_uint64(), C.c_uint64()
+    if N.lib().otprg_mem_info(opt.device, C.byref(free), C.byref(total)) != 0:
+        raise DeviceError(f"cannot query the memory of device {opt.device}")
+    return need <= 0.9 * free.value
 
 
 def solve_assignment(inst: AssignmentInstance, opt: AssignmentOptions):

@@ -5,7 +5,10 @@
 // All FP64 arithmetic uses explicit round-to-nearest intrinsics so no FMA
 // contraction can change bits: the reference is built without
 // -march and its cost formulas are plain IEEE double expressions.
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -72,14 +75,16 @@ __global__ void round_dense_kernel(const double* __restrict__ cost, int n_a, int
   }
 }
 
-// K2: 2-D points -> kT with c = sqrt(dx*dx + dy*dy) / sqrt(2)
-// (gen_uniform_square, instances.cpp:70-75).  Internal orientation: pa are
-// the n_ai demand points, pb the n_bi supply points; the formula is exactly
-// symmetric under swapping the roles of the two points.
+// K2 (exact-division form): 2-D points -> kT with c = sqrt(dx*dx + dy*dy) /
+// sqrt(2) (gen_uniform_square, instances.cpp:70-75).  Internal orientation:
+// pa are the n_ai demand points, pb the n_bi supply points; the formula is
+// exactly symmetric under swapping the roles of the two points.  Used only
+// when the threshold table below would not fit in shared memory
+// (unit_floor > kThrSmemMax - 2, i.e. eps < 1/8190).
 template <typename T>
-__global__ void round_points_kernel(const double2* __restrict__ pa,
-                                    const double2* __restrict__ pb, int n_ai, int n_bi,
-                                    double eps, double sqrt2, T* __restrict__ kT, int lda) {
+__global__ void round_points_div_kernel(const double2* __restrict__ pa,
+                                        const double2* __restrict__ pb, int n_ai, int n_bi,
+                                        double eps, double sqrt2, T* __restrict__ kT, int lda) {
   for (int b = blockIdx.y; b < n_bi; b += gridDim.y) {
     const double2 q = pb[b];
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < lda; a += gridDim.x * blockDim.x) {
@@ -93,6 +98,76 @@ __global__ void round_points_kernel(const double2* __restrict__ pa,
         v = clamp_store<T>(scaled_floor_dev(c, eps));
       }
       kT[(size_t)b * lda + a] = v;
+    }
+  }
+}
+
+// K2 on the exact threshold table (otprg_points_threshold_table):
+// k(a,b) = max{j : thr[j] <= d2} with d2 = dx*dx + dy*dy in IEEE RN (the
+// reference's bits up to the sqrt), so no FP64 sqrt or division.  The float
+// estimate e = floor(sqrt(d2 / 2) / eps) (approximate sqrt, relative error
+// ~2^-21, so |e - x| < 0.004 for the real x = sqrt(d2/2)/eps <= 8190) and the
+// exact k = scaled_floor(c, eps) both lie in {floor(x) - 1, floor(x),
+// floor(x) + 1} and cannot sit on opposite ends of it, so |e - k| <= 1: one
+// upward and one downward exact comparison against the table (shared
+// memory) settle k.  Every thread owns 16 B of a kT row (kV consecutive demand
+// points, held in registers) and walks a strided set of supply rows, storing
+// one 16-byte vector per row: the build is bound by its HBM writes.
+constexpr int kThrSmemMax = 8192;
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+template <typename T>
+__global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __restrict__ pa,
+                                                               const double2* __restrict__ pb,
+                                                               int n_ai, int n_bi, const double* __restrict__ thr,
+                                                               int thr_n, float inv_step, T* __restrict__ kT,
+                                                               int lda) {
+  constexpr int kV = 16 / sizeof(T), kPer = 4 / sizeof(T);  // entries per 16 B / per 32-bit word
+  extern __shared__ double s_thr[];
+  for (int j = threadIdx.x; j < thr_n; j += blockDim.x) s_thr[j] = thr[j];
+  __syncthreads();
+  const int uf = thr_n - 2;  // unit_floor: thr[uf + 1] = +inf
+  const int a0 = (blockIdx.x * blockDim.x + threadIdx.x) * kV;
+  if (a0 >= lda) return;
+  double2 p[kV];
+#pragma unroll
+  for (int j = 0; j < kV; ++j) p[j] = a0 + j < n_ai ? pa[a0 + j] : make_double2(0.0, 0.0);
+  for (int b = blockIdx.y; b < n_bi; b += gridDim.y) {
+    const double2 q = pb[b];
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+      const double dx = __dsub_rn(p[j].x, q.x), dy = __dsub_rn(p[j].y, q.y);
+      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+      int k = min(uf, (int)(sqrt_approx(__double2float_rn(d2)) * inv_step));
+      k += s_thr[k + 1] <= d2;
+      k -= s_thr[k] > d2;
+      const uint32_t v = a0 + j < n_ai ? (uint32_t)k : type_max<T>();
+      w[j / kPer] |= v << (8 * sizeof(T) * (j % kPer));
+    }
+    *reinterpret_cast<uint4*>(kT + (size_t)b * lda + a0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Range check of a point instance (AssignmentInstance::validate,
+// core.cpp:15-21): the first (a, b) in the reference's row-major order whose
+// cost sqrt(d2)/sqrt(2) is not in [0, 1] — d2 above d2_max (the largest d2
+// with cost <= 1) or NaN — as atomicMin of a * n_b + b (original
+// orientation).  Only launched when the host's bounding-box bound does not
+// already prove every cost <= 1.
+__global__ void points_range_kernel(const double2* __restrict__ pa, const double2* __restrict__ pb,
+                                    int n_a, int n_b, double d2_max,
+                                    unsigned long long* __restrict__ first) {
+  for (int a = blockIdx.y; a < n_a; a += gridDim.y) {
+    const double2 p = pa[a];
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n_b; b += gridDim.x * blockDim.x) {
+      const double2 q = pb[b];
+      const double dx = __dsub_rn(p.x, q.x), dy = __dsub_rn(p.y, q.y);
+      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+      if (!(d2 <= d2_max)) atomicMin(first, (unsigned long long)a * n_b + b);
     }
   }
 }
@@ -242,17 +317,43 @@ cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swappe
 }
 
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
-                                  double eps, double sqrt2, void* kT, int lda, int width,
-                                  cudaStream_t s) {
-  const int bx = (lda + 255) / 256;
-  dim3 grid(bx < 8 ? bx : 8, n_bi < 65535 ? n_bi : 65535);
+                                  double eps, double sqrt2, const double* thr, int thr_n, void* kT,
+                                  int lda, int width, cudaStream_t s) {
   const double2* a2 = reinterpret_cast<const double2*>(pa);
   const double2* b2 = reinterpret_cast<const double2*>(pb);
+  if (thr && thr_n >= 2 && thr_n <= kThrSmemMax) {
+    // threads own 16 B of a row (lda is a multiple of 512 B / width); ~8 resident
+    // blocks per SM over the columns, the supply rows strided over grid.y
+    const int threads_x = lda * width / 16;
+    const int bx = (threads_x + 255) / 256;
+    const int by = std::max(1, std::min(n_bi, (148 * 8 + bx - 1) / bx * 4));
+    const float inv_step = (float)(1.0 / (std::sqrt(2.0) * eps));
+    const size_t smem = (size_t)thr_n * sizeof(double);
+    with_width(width, [&](auto tag) {
+      using T = decltype(tag);
+      auto fn = round_points_thr_kernel<T>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      fn<<<dim3(bx, std::min(by, 65535)), 256, smem, s>>>(a2, b2, n_ai, n_bi, thr, thr_n, inv_step,
+                                                           static_cast<T*>(kT), lda);
+      return 0;
+    });
+    return cudaGetLastError();
+  }
+  const int bx = (lda + 255) / 256;
+  dim3 grid(bx < 8 ? bx : 8, n_bi < 65535 ? n_bi : 65535);
   with_width(width, [&](auto tag) {
     using T = decltype(tag);
-    round_points_kernel<T><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2, static_cast<T*>(kT), lda);
+    round_points_div_kernel<T><<<grid, 256, 0, s>>>(a2, b2, n_ai, n_bi, eps, sqrt2, static_cast<T*>(kT), lda);
     return 0;
   });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_points_range(const double* pa, const double* pb, int n_a, int n_b, double d2_max,
+                                unsigned long long* first, cudaStream_t s) {
+  const int bx = std::min(8, (n_b + 255) / 256);
+  points_range_kernel<<<dim3(bx, std::min(n_a, 4096)), 256, 0, s>>>(
+      reinterpret_cast<const double2*>(pa), reinterpret_cast<const double2*>(pb), n_a, n_b, d2_max, first);
   return cudaGetLastError();
 }
 

@@ -84,6 +84,13 @@ struct otprg_ctx {
 
   DevBuf kT, t, yb, ma, mb, holder, rowmin, lmeta, lent, lists, mps, fc, ctl, fa, fb;
   DevBuf stage, pts, flush;
+  DevBuf prop_scratch, prop_rowcnt;  // phase-1 scan: split-row pieces and arrival counters
+  // exact threshold table of the 2-D point cost for eps = thr_eps (K2 and the
+  // on-the-fly scans; otprg_points_threshold_table), cached across prepares
+  DevBuf thr_dev, range_first;
+  std::vector<double> thr_host;
+  double thr_eps = -1.0;
+  int thr_n = 0;
   void* hpin = nullptr;  // pinned D2H staging
   size_t hpin_n = 0;
   cudaEvent_t timer[2] = {};

@@ -54,8 +54,12 @@ struct SolveArgs {
 cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swapped, double eps,
                                void* kT, int lda, int width, int* status, cudaStream_t s);
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
-                                  double eps, double sqrt2, void* kT, int lda, int width,
-                                  cudaStream_t s);
+                                  double eps, double sqrt2, const double* thr, int thr_n, void* kT,
+                                  int lda, int width, cudaStream_t s);
+// First (a, b) (row-major, original orientation) whose point cost is outside
+// [0, 1]: atomicMin into *first (initialise to ~0).
+cudaError_t launch_points_range(const double* pa, const double* pb, int n_a, int n_b, double d2_max,
+                                unsigned long long* first, cudaStream_t s);
 // K3: L1/2 cost of per-image-normalised uint8 vectors (load_mnist_pair).
 // normalize: out[i][p] = img[i][p] / sum_p img[i][p] (status 3 on a zero image);
 // round: kT[b][a] = scaled_floor(sum_p |xa[a][p] - yb[b][p]| / 2, eps) (status 2
@@ -136,9 +140,12 @@ size_t phase_loop_smem(int width, bool smem_t, int lda);
 // Phase-1 propose scan (propose_kernels.cu): every row's k == 0 positions
 // (low-set level 0) and row minimum, streamed once with TMA bulk copies.
 int propose_stream_chunk(int width, int lda);
+// Phase-1 propose scan; scratch = propose_stream_scratch_bytes(num_sms) bytes,
+// row_cnt = n_b ints, zero before the first launch (kept zero by the kernel).
+size_t propose_stream_scratch_bytes(int num_sms);
 cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, int4* lmeta,
-                                  unsigned long long* lent, void* rowmin, Ctl* ctl, int num_sms,
-                                  cudaStream_t s);
+                                  unsigned long long* lent, void* rowmin, void* scratch, int* row_cnt,
+                                  Ctl* ctl, int num_sms, cudaStream_t s);
 bool smem_t_fits(int width, int lda);
 
 // Largest t(a) / Y(b) the device state may hold: below the saturation value

@@ -74,6 +74,84 @@ int validate_problem(otprg_ctx* ctx, const otprg_problem* p) {
   return OTPRG_OK;
 }
 
+// Largest d2 whose point cost RN(RN(sqrt(d2)) / sqrt(2)) is <= 1 (bisection
+// over the bit patterns; the cost is monotone in d2).
+double points_d2_max() {
+  static const double v = [] {
+    const double sqrt2 = std::sqrt(2.0);
+    auto bits = [](double x) { uint64_t u; std::memcpy(&u, &x, 8); return u; };
+    auto from = [](uint64_t u) { double x; std::memcpy(&x, &u, 8); return x; };
+    uint64_t lo = bits(2.0), hi = bits(8.0);  // cost(lo) <= 1 < cost(hi)
+    while (hi - lo > 1) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      if (std::sqrt(from(mid)) / sqrt2 <= 1.0) lo = mid;
+      else hi = mid;
+    }
+    return from(lo);
+  }();
+  return v;
+}
+
+// AssignmentInstance::validate (core.cpp:15-21) for a point instance: every
+// cost sqrt(dx*dx+dy*dy)/sqrt(2) must lie in [0, 1].  The bounding box of both
+// sets bounds every pair's d2 (RN arithmetic is monotone), which settles it
+// for any points inside the unit square; otherwise a device pass finds the
+// first violating (a, b) in row-major order, reported with the reference's
+// message.  dpa_orig / dpb_orig: device copies of the original A / B points.
+int check_points_range(otprg_ctx* ctx, const otprg_problem* p, const double* dpa_orig,
+                       const double* dpb_orig) {
+  double lo[2] = {INFINITY, INFINITY}, hi[2] = {-INFINITY, -INFINITY};
+  bool nan = false;
+  for (int side = 0; side < 2; ++side) {
+    const double* q = side ? p->pts_b : p->pts_a;
+    const int64_t n = side ? p->n_b : p->n_a;
+    for (int64_t i = 0; i < 2 * n; ++i) {
+      const double x = q[i];
+      if (x != x) nan = true;
+      lo[i & 1] = std::min(lo[i & 1], x);
+      hi[i & 1] = std::max(hi[i & 1], x);
+    }
+  }
+  if (!nan) {
+    const double dx = hi[0] - lo[0], dy = hi[1] - lo[1];
+    if (dx * dx + dy * dy <= points_d2_max()) return OTPRG_OK;
+  }
+  CK(ctx->range_first.ensure(8), "alloc range flag");
+  CK(cudaMemsetAsync(ctx->range_first.p, 0xff, 8, ctx->stream), "memset");
+  CK(otprg::launch_points_range(dpa_orig, dpb_orig, p->n_a, p->n_b, points_d2_max(),
+                                ctx->range_first.as<unsigned long long>(), ctx->stream),
+     "range check launch");
+  unsigned long long first = 0;
+  CK(cudaMemcpyAsync(&first, ctx->range_first.p, 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  CK(cudaStreamSynchronize(ctx->stream), "range check");
+  if (first == ~0ull) return OTPRG_OK;
+  const int64_t a = static_cast<int64_t>(first / p->n_b), b = static_cast<int64_t>(first % p->n_b);
+  const double dx = p->pts_a[2 * a] - p->pts_b[2 * b], dy = p->pts_a[2 * a + 1] - p->pts_b[2 * b + 1];
+  const double c = std::sqrt(dx * dx + dy * dy) / std::sqrt(2.0);
+  return fail(ctx, OTPRG_PARAMETER, "cost entry outside [0,1] at (" + std::to_string(a) + "," +
+                                        std::to_string(b) + "): " + std::to_string(c));
+}
+
+// The exact threshold table for eps on the device (cached per eps).  Returns
+// its length, 0 when it is too large for the shared-memory kernels.
+int points_table(otprg_ctx* ctx, double eps, int* n_out) {
+  *n_out = 0;
+  const int32_t n = otprg_points_threshold_table(eps, nullptr, 0);
+  if (n < 2 || n > 8192) return OTPRG_OK;
+  if (ctx->thr_eps != eps || ctx->thr_n != n) {
+    ctx->thr_host.assign(n, 0.0);
+    otprg_points_threshold_table(eps, ctx->thr_host.data(), n);
+    CK(ctx->thr_dev.ensure(n * sizeof(double)), "alloc threshold table");
+    CK(cudaMemcpyAsync(ctx->thr_dev.p, ctx->thr_host.data(), n * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream),
+       "H2D threshold table");
+    ctx->thr_eps = eps;
+    ctx->thr_n = n;
+  }
+  *n_out = n;
+  return OTPRG_OK;
+}
+
 int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   int st = validate_problem(ctx, p);
   if (st) return st;
@@ -172,7 +250,12 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
     CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
        "H2D points");
     CK(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(Ctl), ctx->stream), "memset");
-    CK(otprg::launch_round_points2d(dpa, dpb, ctx->ia, ctx->ib, p->eps, std::sqrt(2.0), ctx->kT.p,
+    st = check_points_range(ctx, p, ctx->swapped ? dpb : dpa, ctx->swapped ? dpa : dpb);
+    if (st) return st;
+    int thr_n = 0;
+    if ((st = points_table(ctx, p->eps, &thr_n))) return st;
+    CK(otprg::launch_round_points2d(dpa, dpb, ctx->ia, ctx->ib, p->eps, std::sqrt(2.0),
+                                    thr_n ? ctx->thr_dev.as<double>() : nullptr, thr_n, ctx->kT.p,
                                     ctx->lda, width, ctx->stream),
        "round_points launch");
     ctx->build_launches = 1;
@@ -268,8 +351,14 @@ int do_begin(otprg_ctx* ctx, cudaEvent_t ev_init = nullptr, cudaEvent_t ev_scan0
   CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->stream),
      "init launch");
   if (ev_scan0) CK(cudaEventRecord(ev_scan0, ctx->stream), "event");
+  if (ctx->prop_rowcnt.n < static_cast<size_t>(ctx->ib) * 4) {
+    CK(ctx->prop_rowcnt.ensure(static_cast<size_t>(ctx->ib) * 4), "alloc propose counters");
+    CK(cudaMemsetAsync(ctx->prop_rowcnt.p, 0, ctx->prop_rowcnt.n, ctx->stream), "memset");
+  }
+  CK(ctx->prop_scratch.ensure(otprg::propose_stream_scratch_bytes(ctx->num_sms)), "alloc propose scratch");
   CK(otprg::launch_propose_stream(ctx->kT.p, ctx->lda, ctx->ib, ctx->width, A.lmeta, A.lent,
-                                  ctx->rowmin.p, A.ctl, ctx->num_sms, ctx->stream),
+                                  ctx->rowmin.p, ctx->prop_scratch.p, ctx->prop_rowcnt.as<int>(), A.ctl,
+                                  ctx->num_sms, ctx->stream),
      "propose scan launch");
   if (ev_scan1) CK(cudaEventRecord(ev_scan1, ctx->stream), "event");
   if (ctx->trace_cap)
@@ -476,6 +565,18 @@ int32_t otprg_points_threshold_table(double eps, double* thr, int32_t cap) {
     thr[j] = from(lo);
   }
   return n;
+}
+
+int otprg_mem_info(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) return OTPRG_DEVICE;
+  size_t f = 0, t = 0;
+  const cudaError_t e = cudaMemGetInfo(&f, &t);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return OTPRG_DEVICE;
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = t;
+  return OTPRG_OK;
 }
 
 int otprg_create(int device, otprg_ctx** out) {
@@ -849,6 +950,70 @@ int otprg_verify_feasibility(otprg_ctx* ctx, otprg_feasibility* out) {
   return OTPRG_OK;
 }
 
+int otprg_verify_result(otprg_ctx* ctx, const int64_t* y_a, const int64_t* y_b, const int32_t* match_of_a,
+                        const int32_t* match_of_b, otprg_feasibility* out) {
+  if (!ctx || !out) return OTPRG_PARAMETER;
+  if (!ctx->prepared || ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_prepare() first");
+  if (!y_a || !y_b || !match_of_a || !match_of_b) return fail(ctx, OTPRG_PARAMETER, "null state");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int ia = ctx->ia, ib = ctx->ib, w = ctx->width;
+  // the solver's own representation: t(a) = -Y(a) in the storage type, Y(b) int32
+  const int64_t tmax = otprg::storage_tmax(w);
+  std::vector<uint8_t> t(static_cast<size_t>(ctx->lda) * w, 0);
+  std::vector<int32_t> yb(ib);
+  for (int a = 0; a < ia; ++a) {
+    if (y_a[a] > 0 || -y_a[a] > tmax)
+      return fail(ctx, OTPRG_PARAMETER, "demand dual outside the device representation at a=" + std::to_string(a));
+    const uint32_t v = static_cast<uint32_t>(-y_a[a]);
+    std::memcpy(t.data() + static_cast<size_t>(a) * w, &v, w);  // little endian: low w bytes
+  }
+  for (int b = 0; b < ib; ++b) {
+    if (y_b[b] < 0 || y_b[b] > tmax)
+      return fail(ctx, OTPRG_PARAMETER, "supply dual outside the device representation at b=" + std::to_string(b));
+    yb[b] = static_cast<int32_t>(y_b[b]);
+  }
+  CK(ctx->v_ya.ensure(t.size()), "alloc");
+  CK(ctx->v_yb.ensure(ib * 4ull), "alloc");
+  CK(ctx->v_ma.ensure(ia * 4ull), "alloc");
+  CK(ctx->v_mb.ensure(ib * 4ull), "alloc");
+  CK(cudaMemcpyAsync(ctx->v_ya.p, t.data(), t.size(), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->v_yb.p, yb.data(), ib * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->v_ma.p, match_of_a, ia * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(cudaMemcpyAsync(ctx->v_mb.p, match_of_b, ib * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CK(ctx->v_out.ensure(sizeof(otprg::VerifyOut)), "alloc verify");
+  otprg::VerifyOut init{~0ull, 0ull};
+  auto* vo = ctx->v_out.as<otprg::VerifyOut>();
+  CK(cudaMemcpyAsync(vo, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream), "H2D verify");
+  CK(otprg::launch_verify_state(ctx->kT.p, ctx->lda, w, ctx->v_ya.p, ctx->v_yb.as<int32_t>(),
+                                ctx->v_ma.as<int32_t>(), ctx->v_mb.as<int32_t>(), ia, ib,
+                                static_cast<long long>(ctx->unit_ceil) + 2, vo, ctx->stream),
+     "verify launch");
+  otprg::VerifyOut h{};
+  CK(cudaMemcpyAsync(&h, vo, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream), "D2H verify");
+  CK(cudaStreamSynchronize(ctx->stream), "verify");
+  VerifyResult r{h.first, h.count};
+  int err = 0;
+  decode_violation(r, ia, ib,
+                   [&](otprg_feasibility* f) {
+                     uint32_t kv = 0;
+                     if (f->a >= 0 && f->b >= 0 &&
+                         cudaMemcpy(&kv, static_cast<char*>(ctx->kT.p) +
+                                             (static_cast<size_t>(f->b) * ctx->lda + f->a) * w,
+                                    w, cudaMemcpyDeviceToHost) != cudaSuccess) err = 1;
+                     if (f->kind >= OTPRG_VIOL_NOT_TIGHT) {
+                       f->sum = y_a[f->a] + y_b[f->b];
+                       f->k = kv;
+                     } else if (f->kind >= OTPRG_VIOL_SUPPLY_NEGATIVE) {
+                       f->sum = y_b[f->b];
+                     } else if (f->kind >= OTPRG_VIOL_DEMAND_POSITIVE) {
+                       f->sum = y_a[f->a];
+                     }
+                   },
+                   out);
+  if (err) return fail(ctx, OTPRG_DEVICE, "D2H of the violation details failed");
+  return OTPRG_OK;
+}
+
 int otprg_verify_host(otprg_ctx* ctx, int32_t n_a, int32_t n_b, const int32_t* k, int32_t unit_ceil,
                       const int64_t* y_a, const int64_t* y_b, const int32_t* match_of_a,
                       const int32_t* match_of_b, otprg_feasibility* out) {
@@ -1113,7 +1278,7 @@ otprg::ShardArgs shard_args(otprg_ctx* ctx) {
   if (ctx->sh_otf) {
     S.pa = ctx->pts.as<double2>();
     S.pb = S.pa + ctx->ia;
-    S.thr = ctx->sh_thr.as<double>();
+    S.thr = ctx->thr_dev.as<double>();
     S.thr_n = ctx->sh_thr_n;
   }
   return S;
@@ -1212,19 +1377,23 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   CK(cudaMemcpyAsync(dpa, pa, ia * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
   CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
   CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
+  {
+    const int rst = check_points_range(ctx, p, ctx->swapped ? dpb : dpa, ctx->swapped ? dpa : dpb);
+    if (rst) return rst;
+  }
+  int thr_n = 0;
+  {
+    const int tst = points_table(ctx, p->eps, &thr_n);
+    if (tst) return tst;
+  }
   if (ctx->sh_otf) {  // the exact threshold table replaces the slab
-    const int32_t n = otprg_points_threshold_table(p->eps, nullptr, 0);
-    if (n < 0 || n > 8192)
+    if (thr_n == 0)
       return fail(ctx, OTPRG_PARAMETER, "on-the-fly costs need 1/eps <= 8190 (threshold table in shared memory)");
-    std::vector<double> thr(n);
-    otprg_points_threshold_table(p->eps, thr.data(), n);
-    CK(ctx->sh_thr.ensure(n * sizeof(double)), "alloc threshold table");
-    CK(cudaMemcpyAsync(ctx->sh_thr.p, thr.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
-       "H2D threshold table");
-    ctx->sh_thr_n = n;
+    ctx->sh_thr_n = thr_n;
   } else if (ctx->sh_hi > ctx->sh_lo)
     CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb,
                                     ctx->sh_hi - ctx->sh_lo, ctx->ib, p->eps, std::sqrt(2.0),
+                                    thr_n ? ctx->thr_dev.as<double>() : nullptr, thr_n,
                                     ctx->kT.p, ctx->lda, width, ctx->stream),
        "round_points launch");
   CK(cudaEventRecord(ctx->ev[5], ctx->stream), "event");

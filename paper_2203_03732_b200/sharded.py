@@ -76,6 +76,14 @@ class DeviceRank:
                                         C.byref(parked)))
         return int(parked.value)
 
+    def snapshot(self):
+        """The replicated state before completion (otprg_snapshot): matching
+        (caller orientation), duals (internal), phases, free_counts."""
+        n_a, n_b, eps = self.shape
+        r, bufs = self.solver._result(n_a, n_b, eps)
+        self._ok(self._L.otprg_snapshot(self._ctx, C.byref(r)))
+        return Solver._pack(r, bufs)
+
     def finish(self):
         n_a, n_b, eps = self.shape
         r, bufs = self.solver._result(n_a, n_b, eps)
@@ -197,13 +205,16 @@ class ShardedSolver:
         for r in self.ranks:
             r.set_stream(self.stream.cuda_stream)
 
-    def solve(self):
+    def solve(self, keep_state: bool = False):
         """One full solve (state re-initialised).  Returns (Matching,
-        SolveStats) of the first local rank after checking local ranks agree."""
+        SolveStats) of the first local rank after checking local ranks agree.
+        ``keep_state``: also return the state before completion (rank 0's
+        snapshot) as a third element, for verify_feasibility."""
         import torch
         with torch.cuda.stream(self.stream):
             rounds = run_phases(self.ranks, self.exchange, self.cand.data_ptr(),
                                 self.meta.data_ptr(), self.cap, self.gather_args)
+        pre = self.ranks[0].snapshot() if keep_state else None
         outs = [r.finish() for r in self.ranks]
         m0, s0 = outs[0]
         for m, s in outs[1:]:
@@ -213,7 +224,7 @@ class ShardedSolver:
                 raise RuntimeError("shards ended in different states")
         s0.device["refill_rounds"] = rounds
         s0.device["n_shards"] = self.n_shards
-        return m0, s0
+        return (m0, s0, pre) if keep_state else (m0, s0)
 
     def timer_start(self):
         for r in self.ranks:

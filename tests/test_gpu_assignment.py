@@ -9,6 +9,8 @@ for ad-hoc instances, with the C oracle restatement.  Bar: bit-exact.
 Structure mirrors the reference's tests/test_assignment.cpp and
 tests/test_core.cpp.
 """
+import re
+
 import numpy as np
 import pytest
 
@@ -70,6 +72,31 @@ def test_cost_outside_unit_interval_is_parameter_error():
     inst = otprg.AssignmentInstance(2, 2, np.array([[0.1, 0.2], [0.3, 1.5]]))
     with pytest.raises(otprg.ParameterError):
         otprg.Solver(0).solve(inst, otprg.AssignmentOptions(eps=0.1))
+
+
+@pytest.mark.parametrize("costs", ["matrix", "on_the_fly"])
+def test_point_cost_outside_unit_interval_is_parameter_error(costs):
+    """core.cpp:15-21 for point instances: scaled points give
+    costs above 1 and must be rejected on both cost paths with the reference's
+    message (first offending (a, b) in row-major order), never truncated."""
+    inst = otprg.gen_uniform_square(300, 4)
+    big = otprg.AssignmentInstance(300, 300, pts_a=inst.pts_a * 2.0, pts_b=inst.pts_b * 2.0)
+    want = None
+    dense = otprg.points_cost(big.pts_a, big.pts_b)
+    bad = np.argwhere(~((dense >= 0.0) & (dense <= 1.0)))[0]
+    want = f"cost entry outside [0,1] at ({bad[0]},{bad[1]}): {dense[bad[0], bad[1]]:f}"
+    with pytest.raises(otprg.ParameterError, match=re.escape(want)):
+        otprg.solve_assignment(big, otprg.AssignmentOptions(eps=0.01, costs=costs))
+    nan_a = inst.pts_a.copy()
+    nan_a[7, 1] = np.nan
+    with pytest.raises(otprg.ParameterError, match=re.escape("at (7,0)")):
+        otprg.solve_assignment(otprg.AssignmentInstance(300, 300, pts_a=nan_a, pts_b=inst.pts_b),
+                               otprg.AssignmentOptions(eps=0.01, costs=costs))
+    # the boundary itself is legal: the corners of the unit square are at cost 1
+    corners = otprg.AssignmentInstance(2, 2, pts_a=np.array([[0.0, 0.0], [1.0, 1.0]]),
+                                       pts_b=np.array([[1.0, 1.0], [0.0, 0.0]]))
+    m, s = otprg.solve_assignment(corners, otprg.AssignmentOptions(eps=0.1, costs=costs))
+    assert m.size() == 2
 
 
 def test_one_by_one_phase_counts():
