@@ -140,12 +140,9 @@ size_t phase_loop_smem(int width, bool smem_t, int lda);
 // Phase-1 propose scan (propose_kernels.cu): every row's k == 0 positions
 // (low-set level 0) and row minimum, streamed once with TMA bulk copies.
 int propose_stream_chunk(int width, int lda);
-// Phase-1 propose scan; scratch = propose_stream_scratch_bytes(num_sms) bytes,
-// row_cnt = n_b ints, zero before the first launch (kept zero by the kernel).
-size_t propose_stream_scratch_bytes(int num_sms);
 cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, int4* lmeta,
-                                  unsigned long long* lent, void* rowmin, void* scratch, int* row_cnt,
-                                  Ctl* ctl, int num_sms, cudaStream_t s);
+                                  unsigned long long* lent, void* rowmin, Ctl* ctl, int num_sms,
+                                  cudaStream_t s);
 bool smem_t_fits(int width, int lda);
 
 // Largest t(a) / Y(b) the device state may hold: below the saturation value

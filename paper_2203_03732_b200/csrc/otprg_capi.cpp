@@ -351,14 +351,8 @@ int do_begin(otprg_ctx* ctx, cudaEvent_t ev_init = nullptr, cudaEvent_t ev_scan0
   CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->stream),
      "init launch");
   if (ev_scan0) CK(cudaEventRecord(ev_scan0, ctx->stream), "event");
-  if (ctx->prop_rowcnt.n < static_cast<size_t>(ctx->ib) * 4) {
-    CK(ctx->prop_rowcnt.ensure(static_cast<size_t>(ctx->ib) * 4), "alloc propose counters");
-    CK(cudaMemsetAsync(ctx->prop_rowcnt.p, 0, ctx->prop_rowcnt.n, ctx->stream), "memset");
-  }
-  CK(ctx->prop_scratch.ensure(otprg::propose_stream_scratch_bytes(ctx->num_sms)), "alloc propose scratch");
   CK(otprg::launch_propose_stream(ctx->kT.p, ctx->lda, ctx->ib, ctx->width, A.lmeta, A.lent,
-                                  ctx->rowmin.p, ctx->prop_scratch.p, ctx->prop_rowcnt.as<int>(), A.ctl,
-                                  ctx->num_sms, ctx->stream),
+                                  ctx->rowmin.p, A.ctl, ctx->num_sms, ctx->stream),
      "propose scan launch");
   if (ev_scan1) CK(cudaEventRecord(ev_scan1, ctx->stream), "event");
   if (ctx->trace_cap)

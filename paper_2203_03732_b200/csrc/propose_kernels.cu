@@ -13,19 +13,17 @@
 // loop.  The algorithmic traffic is n_b * lda * width bytes (SURVEY §8(d):
 // n_i = n in phase 1).
 //
-// B200 structure: one CTA of kWarps warps per SM (grid = number of SMs) and
-// the n_b * chunks_per_row (row, chunk) items of kT split into equal
-// contiguous ranges, one per warp, so every SM streams the same number of
-// bytes.  Each warp pulls its items through its own ring of kDepth chunk
-// buffers in shared memory, filled by 1-D TMA bulk copies
-// (cp.async.bulk ... mbarrier::complete_tx); its lane 0 refills a stage as
-// soon as the warp has read it; no cross-warp synchronisation.  A row whose
-// chunks span several warps ("split row") is finished by the last of those
-// warps to arrive: each piece publishes its ordered k = 0 positions (up to
-// kLowCap) and its minimum, and the last arriver concatenates the pieces in
-// chunk order.
+// B200 structure: one CTA of kWarps warps per SM on every SM; every warp owns
+// a contiguous range of whole rows (so each row's positions are produced in
+// order by one warp) and streams them through its own ring of
+// kDepth chunk buffers in shared memory, filled by 1-D TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx).  The warp's lane 0 refills a
+// stage as soon as the warp has read it; there is no cross-warp
+// synchronisation at all.  Row chunks are sized so kWarps * kDepth chunks
+// fit in shared memory (rows above the limit are split evenly).
 #include "device_common.cuh"
 #include "kernels.h"
+#include <algorithm>
 
 namespace otprg {
 
@@ -43,49 +41,33 @@ constexpr int kStreamThreads = kWarps * 32;
 constexpr int kMaxChunk = (192 * 1024 / (kWarps * kDepth)) / 512 * 512;  // ring <= 192 KB
 constexpr int kVec = 4;              // 16-byte vectors per lane per step
 
-// One piece of a split row (2 slots per warp: its first and its last row).
-struct PropPiece {
-  int32_t cnt, full_pos;
-  uint32_t mn, pad;
-  int32_t pos[kLowCap];
-};
-
-// Item range of warp w: [w * total / W, (w + 1) * total / W).
-__device__ __forceinline__ long long item_start(long long w, long long total, long long W) {
-  return w * total / W;
-}
-__device__ __forceinline__ long long warp_of_item(long long i, long long total, long long W) {
-  long long w = i * W / total;
-  while (w + 1 < W && item_start(w + 1, total, W) <= i) ++w;
-  while (w > 0 && item_start(w, total, W) > i) --w;
-  return w;
-}
 
 template <typename T>
 __global__ void __launch_bounds__(kStreamThreads, 1)
     propose_stream_kernel(const T* __restrict__ kT, int lda, int n_b, int chunk_bytes,
-                          int chunks_per_row, int4* __restrict__ lmeta,
-                          unsigned long long* __restrict__ lent, T* __restrict__ rowmin,
-                          PropPiece* __restrict__ pieces, int* __restrict__ row_cnt, Ctl* ctl) {
+                          int chunks_per_row, int rows_per_warp, int4* __restrict__ lmeta,
+                          unsigned long long* __restrict__ lent, T* __restrict__ rowmin, Ctl* ctl) {
   using SD = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);  // elements per 16-byte vector
   extern __shared__ __align__(128) unsigned char ring[];  // kWarps * kDepth * chunk_bytes
   __shared__ __align__(8) unsigned long long full_bar[kWarps][kDepth];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long W = (long long)gridDim.x * kWarps;
-  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  // warps interleaved over the SMs (warp slot `warp` of block x is global warp
+  // warp * gridDim.x + x): the active warps spread evenly over every SM
+  const int gw = warp * (int)gridDim.x + (int)blockIdx.x;
   const size_t row_bytes = (size_t)lda * sizeof(T);
-  const long long total = (long long)n_b * chunks_per_row;
-  const long long it0 = item_start(gw, total, W), it1 = item_start(gw + 1, total, W);
-  const int items = (int)(it1 - it0);
+  // contiguous, equal row ranges per warp (the last may be shorter)
+  const int row0 = gw * rows_per_warp;
+  const int rows = max(0, min(n_b - row0, rows_per_warp));
+  const int items = rows * chunks_per_row;  // this warp's (row, chunk) pairs, in order
   const int chunk_elems = chunk_bytes / (int)sizeof(T);
   unsigned char* my_ring = ring + (size_t)warp * kDepth * chunk_bytes;
   unsigned long long* bars = full_bar[warp];
 
   if (threadIdx.x == 0) atomicMin(&ctl->prop_t0, globaltimer());
   if (lane == 0) {
-    for (int st = 0; st < kDepth; ++st) mbar_init(&bars[st], 1);
+    for (int s = 0; s < kDepth; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -93,38 +75,33 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   auto chunk_len = [&](int c) -> unsigned {
     return (unsigned)min((size_t)chunk_bytes, row_bytes - (size_t)c * chunk_bytes);
   };
-  auto issue = [&](int k) {  // lane 0: load this warp's k-th item into stage k % kDepth
-    const long long it = it0 + k;
-    const int st = k % kDepth;
-    const int b = (int)(it / chunks_per_row), c = (int)(it % chunks_per_row);
+  auto issue = [&](int it) {  // lane 0: load item `it` into stage it % kDepth
+    const int s = it % kDepth;
+    const int b = row0 + it / chunks_per_row;
+    const int c = it % chunks_per_row;
     const unsigned len = chunk_len(c);
     const char* src = reinterpret_cast<const char*>(kT) + (size_t)b * row_bytes + (size_t)c * chunk_bytes;
-    mbar_expect_tx(&bars[st], len);
-    bulk_g2s(my_ring + (size_t)st * chunk_bytes, src, len, &bars[st]);
+    mbar_expect_tx(&bars[s], len);
+    bulk_g2s(my_ring + (size_t)s * chunk_bytes, src, len, &bars[s]);
   };
   if (lane == 0)
-    for (int k = 0; k < min(kDepth, items); ++k) issue(k);
+    for (int it = 0; it < min(kDepth, items); ++it) issue(it);
 
   int cnt = 0, full_pos = -1;
   uint32_t mn = 0xffffffffu;
   unsigned long long bytes = 0;
-  int b = items ? (int)(it0 / chunks_per_row) : 0, c = items ? (int)(it0 % chunks_per_row) : 0;
-  int st = 0;
+  int b = row0, c = 0, s = 0;
   unsigned parity = 0;
-  bool whole = false, first_row = true;
-  int32_t* piece_pos = nullptr;
-  for (int k = 0; k < items; ++k) {
-    if (k == 0 || c == 0) {  // a row (piece) starts
+  for (int it = 0; it < items; ++it) {
+    if (c == 0) {
       cnt = 0;
       full_pos = -1;
       mn = 0xffffffffu;
-      whole = c == 0 && (long long)(b + 1) * chunks_per_row <= it1;
-      piece_pos = pieces[2 * gw + (first_row ? 0 : 1)].pos;
     }
-    mbar_wait(&bars[st], parity);
+    mbar_wait(&bars[s], parity);
     const unsigned len = chunk_len(c);
     const int nv = (int)len / 16;
-    const uint4* src = reinterpret_cast<const uint4*>(my_ring + (size_t)st * chunk_bytes);
+    const uint4* src = reinterpret_cast<const uint4*>(my_ring + (size_t)s * chunk_bytes);
     const int base = c * chunk_elems;
     for (int v0 = 0; v0 < nv; v0 += 32 * kVec) {  // warp-uniform trip count
       uint4 x[kVec];
@@ -159,70 +136,30 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           while (mj && cnt < kLowCap) {
             const int pos = e0 + __ffs(mj) - 1;
             mj &= mj - 1;
-            if (lane == 0) {
-              if (whole) lent[(size_t)b * kLowCap + cnt] = (unsigned long long)(uint32_t)pos;  // (k=0)<<32|a
-              else piece_pos[cnt] = pos;
-            }
+            if (lane == 0) lent[(size_t)b * kLowCap + cnt] = (unsigned long long)(uint32_t)pos;  // (k=0)<<32|a
             if (cnt == kLowCap - 1) full_pos = pos;
             ++cnt;
           }
         }
       }
     }
-    __syncwarp();  // the warp is done reading stage st
+    __syncwarp();  // the warp is done reading stage s
     if (lane == 0) {
       bytes += len;
-      if (k + kDepth < items) {
+      if (it + kDepth < items) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(k + kDepth);
+        issue(it + kDepth);
       }
     }
-    if (c == chunks_per_row - 1 || k == items - 1) {  // this warp's piece of row b ends
+    if (c == chunks_per_row - 1) {
       const uint32_t m = __reduce_min_sync(kFull, SD::hmin(mn));
-      if (whole) {
-        if (lane == 0) {
-          lmeta[b] = make_int4(0, full_pos >= 0 ? full_pos + 1 : lda, cnt, 0);
-          rowmin[b] = (T)m;
-        }
-      } else {
-        // split row: publish the piece; the last of the row's warps merges
-        const long long ws = warp_of_item((long long)b * chunks_per_row, total, W);
-        const long long we = warp_of_item((long long)(b + 1) * chunks_per_row - 1, total, W);
-        int prev = 0;
-        if (lane == 0) {
-          PropPiece* pc = &pieces[2 * gw + (first_row ? 0 : 1)];
-          pc->cnt = cnt;
-          pc->mn = m;
-          __threadfence();
-          prev = atomicAdd(row_cnt + b, 1);
-        }
-        prev = __shfl_sync(kFull, prev, 0);
-        if (prev == (int)(we - ws)) {
-          __threadfence();
-          if (lane == 0) {
-            int tot = 0, fpos = -1;
-            uint32_t rmin = 0xffffffffu;
-            for (long long w = ws; w <= we; ++w) {
-              const bool w_first = item_start(w, total, W) / chunks_per_row == b;
-              const PropPiece* pc = &pieces[2 * w + (w_first ? 0 : 1)];
-              const int pcnt = __ldcg(&pc->cnt);
-              rmin = min(rmin, __ldcg(&pc->mn));
-              for (int q = 0; q < pcnt && tot < kLowCap; ++q, ++tot) {
-                const int pos = __ldcg(&pc->pos[q]);
-                lent[(size_t)b * kLowCap + tot] = (unsigned long long)(uint32_t)pos;
-                if (tot == kLowCap - 1) fpos = pos;
-              }
-            }
-            lmeta[b] = make_int4(0, fpos >= 0 ? fpos + 1 : lda, tot, 0);
-            rowmin[b] = (T)rmin;
-            row_cnt[b] = 0;  // ready for the next launch
-          }
-        }
+      if (lane == 0) {
+        lmeta[b] = make_int4(0, full_pos >= 0 ? full_pos + 1 : lda, cnt, 0);
+        rowmin[b] = (T)m;
       }
-      first_row = false;
     }
     if (++c == chunks_per_row) c = 0, ++b;
-    if (++st == kDepth) st = 0, parity ^= 1u;
+    if (++s == kDepth) s = 0, parity ^= 1u;
   }
   if (lane == 0) {
     if (bytes) atomicAdd(&ctl->bytes_touched, bytes);
@@ -238,18 +175,24 @@ int propose_stream_chunk(int width, int lda) {
   return ((row_bytes / 512 + cpr - 1) / cpr) * 512;  // even split, 512 B granules
 }
 
-size_t propose_stream_scratch_bytes(int num_sms) {
-  return (size_t)num_sms * kWarps * 2 * sizeof(PropPiece);
-}
-
 cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, int4* lmeta,
-                                  unsigned long long* lent, void* rowmin, void* scratch, int* row_cnt,
-                                  Ctl* ctl, int num_sms, cudaStream_t s) {
+                                  unsigned long long* lent, void* rowmin, Ctl* ctl, int num_sms,
+                                  cudaStream_t s) {
   const int chunk = propose_stream_chunk(width, lda);
   const int cpr = (lda * width + chunk - 1) / chunk;
   const size_t smem = (size_t)kWarps * kDepth * chunk;
-  // one CTA per SM, equal item ranges per warp (every SM streams the same bytes)
-  const int grid = num_sms;
+  // Balance: every warp gets the same number of rows (a warp's throughput
+  // is set by its own ring depth, so equal shares matter more than equal
+  // warps per SM).
+  // Whole rows per warp, rows_per_warp = ceil(n_b / (SMs * kWarps)), and the
+  // warps spread over EVERY SM: global warp `warp * grid + block`, so each SM
+  // runs n_warps / grid or one more (grid = SM count).  A/B (profiles/
+  // r02_prop_ab.txt): equal row counts per warp matter (a warp is bound by its
+  // own ring), the SM count does not once the memory system is saturated.
+  const int max_warps = num_sms * kWarps;
+  const int rpw = (n_b + max_warps - 1) / max_warps;
+  const int warps = (n_b + rpw - 1) / rpw;
+  const int grid = std::min(num_sms, warps);
   // raise the opt-in shared-memory limit once per device and width
   static size_t smem_set[64][3] = {};
   int dev = 0;
@@ -260,9 +203,8 @@ cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, i
     auto fn = propose_stream_kernel<T>;
     size_t& set = smem_set_dev[sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : 2];
     if (set < smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(set = smem));
-    fn<<<grid, kStreamThreads, smem, s>>>(static_cast<const T*>(kT), lda, n_b, chunk, cpr, lmeta, lent,
-                                          static_cast<T*>(rowmin), static_cast<PropPiece*>(scratch),
-                                          row_cnt, ctl);
+    fn<<<grid, kStreamThreads, smem, s>>>(static_cast<const T*>(kT), lda, n_b, chunk, cpr, rpw, lmeta,
+                                          lent, static_cast<T*>(rowmin), ctl);
     return 0;
   });
   return cudaGetLastError();

@@ -255,6 +255,38 @@ def test_unbalanced_at_scale_match_reference(key, form):
     assert m.size() == min(w["n_a"], w["n_b"])
 
 
+# ---- the phase-1 scan's split rows (propose_kernels.cu) ---------------------
+@pytest.mark.parametrize("storage", ["u8", "u16", "u32"])
+def test_phase1_split_rows_match_oracle(oracle, storage):
+    """Few long rows: the phase-1 scan splits every row over several warps,
+    with warps of empty item ranges in between (n_b * chunks < warps), and the
+    last arriver of each row merges the pieces.  Repeated solves on one
+    context reuse the arrival counters.  Bit-exact vs the C oracle."""
+    rng = np.random.default_rng(99)
+    sv = otprg.Solver(0)
+    try:
+        for n_a, n_b, eps in ((30000, 40, 0.05), (12000, 300, 0.02), (9000, 2, 0.1), (30000, 40, 0.05)):
+            pa, pb = rng.random((n_a, 2)), rng.random((n_b, 2))
+            cost = otprg.points_cost(pa, pb)
+            cost[:, 0] = np.where(rng.random(n_a) < 0.002, 0.0, cost[:, 0])  # zeros spread over row 0
+            want = oracle.solve_assignment(cost, eps)
+            for inst in (otprg.AssignmentInstance(n_a, n_b, cost),
+                         otprg.AssignmentInstance(n_b, n_a, np.ascontiguousarray(cost.T))):
+                m, s = sv.solve(inst, otprg.AssignmentOptions(eps=eps, storage=storage))
+                if inst.n_a == n_a:
+                    np.testing.assert_array_equal(m.match_of_a, want.match_of_a)
+                    np.testing.assert_array_equal(s.duals_final.y_a, want.y_a)
+                    np.testing.assert_array_equal(s.duals_final.y_b, want.y_b)
+                    np.testing.assert_array_equal(s.free_counts, want.free_counts)
+                    assert s.device["cost"] == want.cost
+                else:  # transposed instance: the same internal orientation (swapped)
+                    want_t = oracle.solve_assignment(inst.cost, eps)
+                    np.testing.assert_array_equal(m.match_of_a, want_t.match_of_a)
+                    np.testing.assert_array_equal(s.free_counts, want_t.free_counts)
+    finally:
+        sv.close()
+
+
 # ---- degenerate inputs (ties, exact multiples of eps, extreme shapes) ------
 @pytest.mark.parametrize("case", ["zeros", "ones", "multiples", "two_values", "single_row",
                                   "single_col"])
