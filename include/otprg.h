@@ -126,6 +126,10 @@ typedef struct otprg_result {
    * low-set cache, exhaustions by a complete cache, scans past the cache,
    * full rescans, rowmin skips, proposals (atomicMin) */
   int64_t chain_stats[8];
+  /* sharded solves: refill rounds (rescans of truncated candidate lists) and
+   * the shard count; 0 for the single-GPU solver */
+  int32_t refill_rounds;
+  int32_t n_shards;
 } otprg_result;
 
 typedef struct otprg_ctx otprg_ctx;
@@ -278,25 +282,65 @@ int otprg_load_mnist_pair(const char* path, int32_t n, uint64_t seed, uint8_t* i
                           uint8_t* img_b, char* err, int32_t err_cap);
 
 /* ---- A-row-sharded solve over several GPUs ---------------
- * One context per rank (one process per GPU, or several contexts in one
- * process for testing).  Rank `shard` of n_shards owns the demand range
- * [bounds[shard], bounds[shard+1]) of every rounded-cost row (built from the
- * 2-D point sets of the problem); matching, duals and DA holders are
- * replicated and every rank computes the identical result.  Per phase:
- *   otprg_shard_top    apply the previous phase's M' and test termination
- *                      (returns n_i; finished when done);
- *   otprg_shard_scan   write this rank's first-K admissible candidates of
- *                      every free b into its slot of the exchange buffers
- *                      cand[n_shards][cap][K] / meta[n_shards][cap] (device);
- *   (all-gather the slots across ranks — NCCL, by the caller)
- *   otprg_shard_da     deferred acceptance over the merged candidates;
- *                      reports chains parked at a truncated list; while
- *                      parked > 0: otprg_shard_scan(refill=1), all-gather,
- *                      otprg_shard_da(resume=1).
- * otprg_shard_finish completes the matching and returns the results (as
- * otprg_solve_assignment).  Results are bit-identical for every n_shards. */
+ * Shard g of G owns the demand range [bounds[g], bounds[g+1]) of every
+ * rounded-cost row (built from the problem's 2-D point sets on its GPU, or no
+ * slab at all with OTPRG_FLAG_ON_THE_FLY); matching, duals and DA holders are
+ * replicated and every shard computes the identical result, bit-identical for
+ * every G (and to otprg_solve_assignment / the reference).  A round is: scan
+ * (first K admissible a of every proposer in the slab) -> exchange of the
+ * candidate slots -> deferred acceptance over the merged lists; chains that
+ * reach a truncated list park and the next round rescans them; a phase ends
+ * with its top (apply M', termination, next free list).
+ *
+ * Easiest: a multi-device context.  otprg_create_multi(devices, n) makes one
+ * shard per listed device (the same device may be listed several times:
+ * logical shards sharing it); otprg_solve_assignment / otprg_prepare +
+ * otprg_solve_prepared on it run the resident loop below for point instances
+ * (other cost kinds run on the first device).  K: otprg_set_shard_k (16). */
+int otprg_create_multi(const int32_t* devices, int32_t ndev, otprg_ctx** out);
+int otprg_set_shard_k(otprg_ctx* ctx, int32_t K);
+
+/* Shard contexts (one per shard and device; created with otprg_create): */
 int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* prob, int32_t n_shards,
                         int32_t shard, int32_t K, int32_t* bounds_out);
+/* Resident solve of the shards this process holds: every round of every phase
+ * runs inside one CUDA graph per device (a conditional WHILE node: scan ->
+ * NVLink peer push of the candidate slots + epoch flags -> DA -> top ->
+ * round bookkeeping, which sets the loop condition), one host sync per solve.
+ * Shards on one device run in stream order and exchange nothing; each device
+ * appears once (its shards consecutive).  When the shards do not cover all
+ * n_shards (one process per GPU), attach the other processes' exchange blocks
+ * first with otprg_shard_ipc_export / otprg_shard_ipc_attach.  Results as
+ * otprg_solve_assignment (from the lowest local shard; all must agree). */
+int otprg_shard_solve_resident(otprg_ctx** shards, int32_t n, otprg_result* res);
+/* Multi-process resident mode (one process per GPU; this process's shard
+ * forms group my_group of n_groups): export writes the CUDA IPC handle
+ * (OTPRG_IPC_HANDLE_BYTES) of this shard's exchange block; the caller
+ * all-gathers the handles (e.g. torch.distributed) and attaches them all
+ * (handles[q] of group q, group q holding shards [group_shard_lo[q],
+ * group_shard_lo[q+1])).  Then otprg_shard_solve_resident(&ctx, 1, res). */
+#define OTPRG_IPC_HANDLE_BYTES 64
+/* Self-test of the resident loop's peer exchange on one device: n_groups
+ * groups (shards_per_group shards each) push varying round slots into each
+ * other's exchange blocks and wait on the epoch flags, emulated as one
+ * cooperative grid (co-resident blocks; the multi-GPU push proper needs one
+ * GPU per group).  *mismatches counts wrong slots / flags over `rounds`. */
+int otprg_selftest_exchange(int32_t device, int32_t n_groups, int32_t shards_per_group, int32_t ib,
+                            int32_t K, int32_t rounds, int64_t* mismatches);
+int otprg_shard_ipc_export(otprg_ctx* ctx, int32_t n_groups, int32_t my_group, void* handle_out);
+int otprg_shard_ipc_attach(otprg_ctx* ctx, const void* handles, int32_t n_groups,
+                           const int32_t* group_shard_lo);
+/* Host-driven protocol (the caller exchanges the slots between scan and DA,
+ * e.g. with an NCCL / gloo all-gather; one host sync per round):
+ *   otprg_shard_begin  init_state + the phase-0 top;
+ *   otprg_shard_top    n_i of the coming phase and whether the solve finished;
+ *   otprg_shard_scan   this shard's first-K candidates of every proposer into
+ *                      its slot of cand[n_shards][cap][K] / meta[n_shards][cap]
+ *                      (device buffers; refill = 1 for a rescan round);
+ *   otprg_shard_da     deferred acceptance over the merged slots; reports the
+ *                      parked chains (> 0: scan(refill=1), exchange,
+ *                      da(resume=1) again);
+ *   otprg_shard_finish completes the matching and returns the results. */
 int otprg_shard_begin(otprg_ctx* ctx);
 int otprg_shard_top(otprg_ctx* ctx, int32_t* n_out, int32_t* finished);
 int otprg_shard_scan(otprg_ctx* ctx, int32_t* cand, int32_t* meta, int32_t cap, int32_t refill);

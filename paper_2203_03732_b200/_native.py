@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(PKG_DIR, "lib", os.environ.get("OTPRG_LIB", "libotprg.so
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 OK, PARAMETER, INPUT, NUMERICAL, INVARIANT, DEVICE, ABORTED = 0, 2, 3, 4, 5, 6, 7
+IPC_HANDLE_BYTES = 64  # OTPRG_IPC_HANDLE_BYTES
 COST_DENSE_F64, COST_POINTS2D, COST_L1_U8 = 0, 1, 2
 STORAGE = {"auto": 0, "u8": 1, "u16": 2, "u32": 3}
 MAX_PHASES = 1 << 24  # OTPRG_MAX_PHASES
@@ -48,6 +49,7 @@ class Result(C.Structure):
         ("bytes_touched", C.c_int64), ("bytes_alg", C.c_int64),
         ("width", C.c_int32), ("gpu_launches", C.c_int32),
         ("chain_stats", C.c_int64 * 8),
+        ("refill_rounds", C.c_int32), ("n_shards", C.c_int32),
     ]
 
 
@@ -101,7 +103,9 @@ EXPORTS = [
     "otprg_groups_step", "otprg_groups_finish", "otprg_verify_feasibility", "otprg_verify_host", "otprg_admissible",
     "otprg_solve_ot_opts", "otprg_solve_copy_matching", "otprg_copy_state",
     "otprg_check_cluster_state", "otprg_plan_from_flow", "otprg_points_threshold_table",
-    "otprg_mem_info", "otprg_verify_result",
+    "otprg_mem_info", "otprg_verify_result", "otprg_create_multi", "otprg_set_shard_k",
+    "otprg_shard_solve_resident", "otprg_shard_ipc_export", "otprg_shard_ipc_attach",
+    "otprg_selftest_exchange",
 ]
 
 _lib = None
@@ -163,6 +167,12 @@ def lib() -> C.CDLL:
     L.otprg_random_ot_rational.argtypes = [C.c_int32, C.c_int32, C.c_uint64, vp, vp, vp]
     L.otprg_shard_prepare.argtypes = [vp, C.POINTER(Problem), C.c_int32, C.c_int32, C.c_int32, vp]
     L.otprg_shard_begin.argtypes = [vp]
+    L.otprg_create_multi.argtypes = [vp, C.c_int32, C.POINTER(vp)]
+    L.otprg_set_shard_k.argtypes = [vp, C.c_int32]
+    L.otprg_shard_solve_resident.argtypes = [vp, C.c_int32, C.POINTER(Result)]
+    L.otprg_shard_ipc_export.argtypes = [vp, C.c_int32, C.c_int32, vp]
+    L.otprg_shard_ipc_attach.argtypes = [vp, vp, C.c_int32, vp]
+    L.otprg_selftest_exchange.argtypes = [C.c_int32] * 6 + [C.POINTER(C.c_int64)]
     L.otprg_shard_top.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.otprg_shard_scan.argtypes = [vp, vp, vp, C.c_int32, C.c_int32]
     L.otprg_shard_da.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]

@@ -402,7 +402,8 @@ class Solver:
                         chain_stats=dict(zip(
                             ("fresh", "takeover", "cache_hit", "cache_exhaust", "scan_past_cache",
                              "rescan", "rowmin_skip", "proposals"), list(r.chain_stats))),
-                        gpu_launches=int(r.gpu_launches)))
+                        gpu_launches=int(r.gpu_launches), refill_rounds=int(r.refill_rounds),
+                        n_shards=int(r.n_shards)))
         return m, stats
 
     def scale_round_costs(self, inst: AssignmentInstance, eps: float, storage: str = "auto") -> ScaledCosts:

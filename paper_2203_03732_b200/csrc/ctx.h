@@ -100,18 +100,24 @@ struct otprg_ctx {
   DevBuf trace;            // device timeline, 8 u64 per phase (see solve_kernels.cu)
   uint32_t trace_cap = 0;  // 0 = tracing off
 
-  // A-row-sharded mode (shard_kernels.cu): this rank's slab [sh_lo, sh_hi)
+  // A-row-sharded mode (shard_kernels.cu, shard_host.cpp): this shard's slab [sh_lo, sh_hi)
   bool sharded = false;
   int sh_n_shards = 1, sh_shard = 0, sh_lo = 0, sh_hi = 0, sh_K = 16, sh_cap = 0;
-  uint32_t sh_phase = 0;     // phases completed
-  int sh_n = 0;              // proposers of the running phase
-  int sh_parked = 0;         // chains waiting for a rescan
-  int sh_park_cur = 0;       // which park buffer holds the waiting chains
-  bool sh_top_ready = false;  // the last DA call already ran the next phase's top
-  int sh_done = 0;
-  DevBuf sh_bounds, sh_pos, sh_park[2], sh_list, sh_seg, sh_thr;
+  int sh_grid = 0, sh_da_grid = 0;  // resident-sized grids of the scan / DA kernels
+  uint64_t sh_gen = 0;              // bumped by every shard prepare (invalidates resident plans)
+  // host-driven protocol: the round state last read back from the device
+  bool sh_have = false;
+  int sh_n = 0, sh_parked = 0, sh_done = 0;
+  uint32_t sh_epoch = 0;            // exchange epochs used so far (flags only grow)
+  DevBuf sh_bounds, sh_pos, sh_park[2], sh_list, sh_seg;
   bool sh_otf = false;  // OTPRG_FLAG_ON_THE_FLY: no kT slab, threshold-table scans
+  bool sh_otf_tiled = true;
   int sh_thr_n = 0;
+  std::shared_ptr<void> sh_plan;    // resident loop (graphs, exchange blocks, peers): shard_host.cpp
+  // multi-device context (otprg_create_multi): one shard context per device
+  std::vector<otprg_ctx*> multi;
+  int multi_K = 16;
+  bool multi_prepared = false;
 
   // invariant suite / workset export (verify_kernels.cu)
   DevBuf v_out, v_k, v_ya, v_yb, v_ma, v_mb, adm_cnt, adm_off, adm_list;

@@ -44,6 +44,14 @@ struct Ctl {
   unsigned int bar_count;
   unsigned int bar_base;  // bar_count at the start of the next launch (written at exit)
   int32_t err[8];       // details of the first failure (written by its reporter only)
+  // A-row-sharded rounds (shard_kernels.cu): the round state lives on the device so
+  // the resident loop needs no host.  A round is (scan, exchange, DA[, top]).
+  int32_t sh_mode;      // 0: first round of a phase (every free b), 1: rescan/resume of parked chains
+  int32_t sh_nreq;      // requests (= chains) of the current round
+  int32_t sh_park_cur;  // park buffer holding the current round's chains (mode 1)
+  int32_t sh_rounds;    // refill rounds so far
+  uint32_t sh_epoch;    // exchange rounds completed (the value peers' flags reach)
+  int32_t sh_live;      // 1 while rounds remain (set by the ctl kernel at the end of a round)
 };
 
 #ifdef __CUDACC__

@@ -81,24 +81,23 @@ struct ShardArgs {
   const void* kT;          // T[n_b][lda] : columns lo..hi-1 (local index a - lo)
   int lda, lo, hi, shard, n_shards;
   const int* bounds;       // [n_shards + 1] shard boundaries (device)
-  int K, cap;              // candidates per (shard, proposer); proposer capacity
+  int K, cap;              // candidates per (shard, proposer); slot stride of the exchange buffers
+  int ib;                  // supply vertices (stride of the mps halves)
   void* t;                 // T[n_a] replicated t(a) = -Y(a)
   int width;               // sizeof(T)
   int32_t* yb;
   int32_t* match_a;
   int32_t* match_b;
   unsigned long long* holder;  // [n_a] replicated DA holders
-  const int32_t* list_in;  // free b's of the phase being run
-  int32_t* list_out;       // free b's of the next phase
-  const int2* mp_prev;     // (a, partner) first held in the previous phase
-  int2* mp_out;            // (a, partner) first held in this phase
+  const int32_t* list_in;  // free b's of the running phase (ascending)
+  int2* mps;               // [2][ib] (a, partner) first held in phase p, half p & 1
   int32_t* pos_of_b;       // [n_b] b -> index in list_in
-  int4* park_out;          // parked chains (list index, b, restart)
+  int4* park[2];           // parked chains (list index, b, restart); ctl->sh_park_cur holds the current
   int64_t* free_counts;
   Ctl* ctl;
   int* scratch;            // [>= 148] compaction block counts
-  // Segmented scans (few requests): per-warp first hits [kSegWarps][K],
-  // per-warp hit counts [kSegWarps], per-request arrival counters [n_b]
+  // Segmented scans (few requests): per-work-item first hits [kSegWarps][K],
+  // per-item hit counts [kSegWarps], per-request arrival counters [n_b]
   // (zero between launches).  seg_hits == nullptr: one warp per request.
   int32_t* seg_hits;
   int32_t* seg_cnt;
@@ -109,20 +108,49 @@ struct ShardArgs {
   const double2* pb;
   const double* thr;
   int thr_n;
-  bool first_phase;  // scans of phase 1 (t == 0, every target 0): picks the level-0 scan
+  int otf_tiled;           // the tiled on-the-fly kernel fits shared memory (else the per-row kernel)
 };
 constexpr int kSegWarps = 32768;
 constexpr int kMaxSegs = 32;
-// cond: skip (both kernels) when the DA just before parked chains
-// (ctl->work[1] != 0), i.e. the phase is not complete yet.
-cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, bool cond,
-                             cudaStream_t s);
-cudaError_t launch_shard_compact(const ShardArgs& a, bool cond, cudaStream_t s);
-cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int32_t* cand,
-                              int2* meta, cudaStream_t s);
-cudaError_t launch_shard_da(const ShardArgs& a, uint32_t phase, const int32_t* cand,
-                            const int2* meta, int nchains, const int4* resume_list,
+constexpr int kMaxShardPeers = 8;  // device groups one group pushes to (<= 8 GPUs per node + slack)
+
+// Peer exchange of a device group (one resident loop per device): after the
+// local scans, the group's slots are pushed into every other group's exchange
+// buffers over NVLink peer memory and each group signals its flag there; a
+// group proceeds to DA once every peer's flag reached this round's epoch.
+struct ShardPeers {
+  int n;                              // peer groups
+  int32_t* cand[kMaxShardPeers];      // their exchange buffers (same layout as ours)
+  int2* meta[kMaxShardPeers];
+  uint32_t* flag[kMaxShardPeers];     // their flag arrays, indexed by group
+  uint32_t* my_flags;                 // ours, written by the peers
+  int my_group, n_groups;
+  int shard_lo, shard_hi;             // local shards [lo, hi): their slots are pushed
+  unsigned* arrive;                   // block arrival counter (zero between launches)
+};
+
+// Device-driven round kernels: every per-round quantity (mode, request count,
+// phase, park buffer, segment split) is read from ctl, so the same launches
+// serve the host-driven protocol and the resident graph loop.
+// grid: resident-sized (shard_scan_grid); cap = slot stride (S.cap).
+int shard_scan_grid(const ShardArgs& a, int num_sms);
+bool shard_otf_tiled_fits(int width, int thr_n, int device);
+cudaError_t launch_shard_scan(const ShardArgs& a, int32_t* cand, int2* meta, int grid, cudaStream_t s);
+cudaError_t launch_shard_push(const ShardArgs& a, const int32_t* cand, const int2* meta,
+                              const ShardPeers& p, cudaStream_t s);
+// Self-test: n_groups pushes (device arrays of their args) as one cooperative grid.
+cudaError_t launch_shard_push_emulated(const ShardArgs* a, const int32_t* const* cand, const int2* const* meta,
+                                       const ShardPeers* p, int n_groups, int nblk, cudaStream_t s);
+cudaError_t launch_shard_da(const ShardArgs& a, const int32_t* cand, const int2* meta, int grid,
                             cudaStream_t s);
+// After the DA: when no chain parked, apply M' / termination / next free
+// list (top + compaction); then the round bookkeeping (ctl kernel), which
+// sets the resident loop's condition `cond` when use_cond.
+cudaError_t launch_shard_after_da(const ShardArgs& a, cudaStream_t s);
+cudaError_t launch_shard_ctl(const ShardArgs& a, cudaGraphConditionalHandle cond, bool use_cond,
+                             cudaStream_t s);
+// Before the first round: phase 0 top (termination test, first free list) and ctl.
+cudaError_t launch_shard_first_top(const ShardArgs& a, cudaStream_t s);
 
 // OT admissible-cluster scan (ot_kernels.cu): per request (b, target, start)
 // the first K admissible (a, ci), encoded a*2+ci, and (count, resume).

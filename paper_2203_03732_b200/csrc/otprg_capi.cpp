@@ -25,11 +25,12 @@
 using otprg::Ctl;
 
 #include "ctx.h"
+#include "capi_internal.h"
 
 using otprg::DevBuf;
 using otprg::host_scaled_floor;
 
-namespace {
+namespace otprg_capi {
 
 int fail(otprg_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
@@ -40,11 +41,6 @@ int cuda_fail(otprg_ctx* ctx, cudaError_t e, const char* what) {
   return fail(ctx, OTPRG_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define CK(expr, what)                                \
-  do {                                                \
-    cudaError_t _e = (expr);                          \
-    if (_e != cudaSuccess) return cuda_fail(ctx, _e, what); \
-  } while (0)
 
 // Validation of solve_assignment (assignment.cpp:370-372) and
 // scale_round_costs (core.cpp:35-47) that does not need the cost values.
@@ -515,7 +511,9 @@ int do_solve(otprg_ctx* ctx, otprg_result* r) {
   r->gpu_launches = 4;  // init, phase-1 propose scan, phase loop, complete
   return OTPRG_OK;
 }
-}  // namespace
+}  // namespace otprg_capi
+
+using namespace otprg_capi;
 
 extern "C" {
 
@@ -595,6 +593,9 @@ int otprg_create(int device, otprg_ctx** out) {
 
 void otprg_destroy(otprg_ctx* ctx) {
   if (!ctx) return;
+  for (otprg_ctx* c : ctx->multi) otprg_destroy(c);
+  ctx->multi.clear();
+  ctx->sh_plan.reset();  // graphs, exchange blocks and IPC mappings of a resident plan
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->kT, &ctx->t, &ctx->yb, &ctx->ma, &ctx->mb, &ctx->holder, &ctx->rowmin,
                     &ctx->lmeta, &ctx->lent, &ctx->lists, &ctx->mps, &ctx->fc, &ctx->ctl, &ctx->fa,
@@ -617,7 +618,18 @@ const char* otprg_last_error(const otprg_ctx* ctx) { return ctx ? ctx->err.c_str
 
 int otprg_prepare(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res) {
   if (!ctx) return OTPRG_PARAMETER;
-  int st = do_prepare(ctx, prob);
+  int st = OTPRG_OK;
+  if (!ctx->multi.empty()) {  // multi-device context: shard point instances
+    if ((st = multi_prepare(ctx, prob))) return st;
+    if (ctx->multi_prepared) {
+      if (res) {
+        res->build_ms = ctx->build_ms;
+        res->width = ctx->multi[0]->width;
+      }
+      return OTPRG_OK;
+    }
+  }
+  st = do_prepare(ctx, prob);
   if (st == OTPRG_OK && res) {
     res->build_ms = ctx->build_ms;
     res->width = ctx->width;
@@ -627,11 +639,17 @@ int otprg_prepare(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res) 
 
 int otprg_solve_prepared(otprg_ctx* ctx, otprg_result* res) {
   if (!ctx) return OTPRG_PARAMETER;
+  if (ctx->multi_prepared) return multi_solve(ctx, res);
   return do_solve(ctx, res);
 }
 
 int otprg_solve_assignment(otprg_ctx* ctx, const otprg_problem* prob, otprg_result* res) {
   if (!ctx) return OTPRG_PARAMETER;
+  if (!ctx->multi.empty()) {
+    int st = multi_prepare(ctx, prob);
+    if (st) return st;
+    if (ctx->multi_prepared) return multi_solve(ctx, res);
+  }
   int st = do_prepare(ctx, prob);
   if (st) return st;
   st = do_solve(ctx, res);
@@ -1236,286 +1254,3 @@ int otprg_groups_finish(otprg_ctx* ctx, otprg_result* res) {
 
 }  // extern "C"
 
-// ---- A-row-sharded mode --------------------------------------
-namespace {
-
-otprg::ShardArgs shard_args(otprg_ctx* ctx) {
-  otprg::ShardArgs S{};
-  S.kT = ctx->kT.p;
-  S.lda = ctx->lda;
-  S.lo = ctx->sh_lo;
-  S.hi = ctx->sh_hi;
-  S.shard = ctx->sh_shard;
-  S.n_shards = ctx->sh_n_shards;
-  S.bounds = ctx->sh_bounds.as<int>();
-  S.K = ctx->sh_K;
-  S.cap = ctx->sh_cap;
-  S.t = ctx->t.p;
-  S.width = ctx->width;
-  S.yb = ctx->yb.as<int32_t>();
-  S.match_a = ctx->ma.as<int32_t>();
-  S.match_b = ctx->mb.as<int32_t>();
-  S.holder = ctx->holder.as<unsigned long long>();
-  S.list_in = ctx->sh_list.as<int32_t>();
-  S.list_out = nullptr;
-  int2* mps = ctx->mps.as<int2>();
-  S.mp_prev = mps + static_cast<size_t>(ctx->sh_phase & 1) * ctx->ib;
-  S.mp_out = mps + static_cast<size_t>((ctx->sh_phase + 1) & 1) * ctx->ib;
-  S.pos_of_b = ctx->sh_pos.as<int32_t>();
-  S.park_out = ctx->sh_park[ctx->sh_park_cur ^ 1].as<int4>();
-  S.free_counts = ctx->fc.as<int64_t>();
-  S.ctl = ctx->ctl.as<Ctl>();
-  S.scratch = ctx->fa.as<int>();  // (completion scratch, free during the phases)
-  S.seg_hits = ctx->sh_seg.as<int32_t>();
-  S.seg_cnt = S.seg_hits + static_cast<size_t>(otprg::kSegWarps) * ctx->sh_K;
-  S.row_cnt = S.seg_cnt + otprg::kSegWarps;
-  if (ctx->sh_otf) {
-    S.pa = ctx->pts.as<double2>();
-    S.pb = S.pa + ctx->ia;
-    S.thr = ctx->thr_dev.as<double>();
-    S.thr_n = ctx->sh_thr_n;
-  }
-  return S;
-}
-
-int read_ctl(otprg_ctx* ctx, Ctl* h) {
-  CK(cudaMemcpyAsync(h, ctx->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream), "D2H ctl");
-  CK(cudaStreamSynchronize(ctx->stream), "shard step");
-  return check_status(ctx, *h, false);
-}
-
-}  // namespace
-
-extern "C" {
-
-int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards, int32_t shard,
-                        int32_t K, int32_t* bounds_out) {
-  if (!ctx) return OTPRG_PARAMETER;
-  int st = validate_problem(ctx, p);
-  if (st) return st;
-  if (p->cost_kind != OTPRG_COST_POINTS2D)
-    return fail(ctx, OTPRG_PARAMETER, "sharded mode builds its slab from 2-D point sets");
-  if (n_shards < 1 || shard < 0 || shard >= n_shards)
-    return fail(ctx, OTPRG_PARAMETER, "bad shard index");
-  if (K < 1 || K > 32) return fail(ctx, OTPRG_PARAMETER, "K must lie in [1, 32]");
-  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-  ctx->prepared = false;
-  ctx->n_a = p->n_a;
-  ctx->n_b = p->n_b;
-  ctx->swapped = p->n_b > p->n_a;
-  ctx->ia = ctx->swapped ? p->n_b : p->n_a;
-  ctx->ib = ctx->swapped ? p->n_a : p->n_b;
-  ctx->eps = p->eps;
-  ctx->cost_kind = p->cost_kind;
-  const int64_t uf = host_scaled_floor(1.0, p->eps);
-  ctx->unit_floor = static_cast<int32_t>(uf);
-  ctx->unit_ceil = static_cast<int32_t>(static_cast<double>(uf) * p->eps == 1.0 ? uf : uf + 1);
-  const int64_t need = static_cast<int64_t>(ctx->unit_ceil) + 2;
-  const int width = otprg::storage_width(need, p->storage);
-  if (width < 0) return fail(ctx, OTPRG_PARAMETER, "eps too small for the device cost storage");
-  ctx->width = width;
-  // shard boundaries: multiples of 512 elements (aligned t / kT vectors)
-  std::vector<int> bounds(n_shards + 1);
-  for (int g = 0; g < n_shards; ++g)
-    bounds[g] = static_cast<int>((static_cast<int64_t>(ctx->ia) * g / n_shards) / 512 * 512);
-  bounds[n_shards] = ctx->ia;
-  if (bounds_out)
-    for (int g = 0; g <= n_shards; ++g) bounds_out[g] = bounds[g];
-  ctx->sharded = true;
-  ctx->sh_n_shards = n_shards;
-  ctx->sh_shard = shard;
-  ctx->sh_lo = bounds[shard];
-  ctx->sh_hi = bounds[shard + 1];
-  ctx->sh_K = K;
-  ctx->sh_cap = ctx->ib;
-  const int align = 512 / width;
-  const size_t ia = ctx->ia, ib = ctx->ib;
-  const int local = std::max(ctx->sh_hi - ctx->sh_lo, 1);
-  ctx->lda = (local + align - 1) / align * align;
-  const size_t full = (ia + 511) / 512 * 512;
-  ctx->sh_otf = (p->flags & OTPRG_FLAG_ON_THE_FLY) != 0;
-  if (!ctx->sh_otf) CK(ctx->kT.ensure(ib * ctx->lda * width), "alloc kT slab");
-  CK(ctx->t.ensure(full * width), "alloc t");
-  CK(ctx->yb.ensure(ib * 4), "alloc yb");
-  CK(ctx->ma.ensure(ia * 4), "alloc match_a");
-  CK(ctx->mb.ensure(ib * 4), "alloc match_b");
-  CK(ctx->holder.ensure(2 * ia * 8), "alloc holder");
-  CK(ctx->rowmin.ensure(ib * width), "alloc rowmin");
-  CK(ctx->lmeta.ensure(ib * 16), "alloc low-set meta");
-  CK(ctx->lists.ensure(3 * ib * 4), "alloc lists");
-  CK(ctx->mps.ensure(2 * ib * 8), "alloc mp lists");
-  // completion scratch, and the compaction's per-block counts during the phases (>= 148 ints)
-  CK(ctx->fa.ensure(std::max<size_t>(ia, 1024) * 4), "alloc scratch");
-  CK(ctx->fb.ensure(ib * 4), "alloc scratch");
-  CK(ctx->ctl.ensure(sizeof(Ctl)), "alloc ctl");
-  CK(ctx->sh_bounds.ensure((n_shards + 1) * sizeof(int)), "alloc bounds");
-  CK(ctx->sh_pos.ensure(ib * 4), "alloc pos");
-  CK(ctx->sh_list.ensure(ib * 4), "alloc list");
-  for (auto& pk : ctx->sh_park) CK(pk.ensure(ib * 16), "alloc park");
-  {  // segmented-scan merge buffers; the per-request counters start (and stay) zero
-    const size_t seg_words = static_cast<size_t>(otprg::kSegWarps) * (K + 1) + ib;
-    CK(ctx->sh_seg.ensure(seg_words * 4), "alloc segment buffers");
-    CK(cudaMemsetAsync(ctx->sh_seg.p, 0, seg_words * 4, ctx->stream), "memset segment buffers");
-  }
-  const double capd = std::ceil((1.0 + 2.0 * p->eps) / (p->eps * p->eps)) + 8.0;
-  ctx->fc_cap = static_cast<int64_t>(std::min(capd + 1.0, double(OTPRG_MAX_PHASES)));
-  CK(ctx->fc.ensure(ctx->fc_cap * 8), "alloc free_counts");
-  CK(cudaMemcpyAsync(ctx->sh_bounds.p, bounds.data(), (n_shards + 1) * sizeof(int),
-                     cudaMemcpyHostToDevice, ctx->stream), "H2D bounds");
-  // this rank's slab of kT from the points (K2 on the demand range)
-  const double* pa = ctx->swapped ? p->pts_b : p->pts_a;
-  const double* pb = ctx->swapped ? p->pts_a : p->pts_b;
-  CK(ctx->pts.ensure((ia + ib) * 2 * sizeof(double)), "alloc points");
-  double* dpa = ctx->pts.as<double>();
-  double* dpb = dpa + ia * 2;
-  CK(cudaMemcpyAsync(dpa, pa, ia * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-  CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-  CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
-  {
-    const int rst = check_points_range(ctx, p, ctx->swapped ? dpb : dpa, ctx->swapped ? dpa : dpb);
-    if (rst) return rst;
-  }
-  int thr_n = 0;
-  {
-    const int tst = points_table(ctx, p->eps, &thr_n);
-    if (tst) return tst;
-  }
-  if (ctx->sh_otf) {  // the exact threshold table replaces the slab
-    if (thr_n == 0)
-      return fail(ctx, OTPRG_PARAMETER, "on-the-fly costs need 1/eps <= 8190 (threshold table in shared memory)");
-    ctx->sh_thr_n = thr_n;
-  } else if (ctx->sh_hi > ctx->sh_lo)
-    CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb,
-                                    ctx->sh_hi - ctx->sh_lo, ctx->ib, p->eps, std::sqrt(2.0),
-                                    thr_n ? ctx->thr_dev.as<double>() : nullptr, thr_n,
-                                    ctx->kT.p, ctx->lda, width, ctx->stream),
-       "round_points launch");
-  CK(cudaEventRecord(ctx->ev[5], ctx->stream), "event");
-  CK(cudaStreamSynchronize(ctx->stream), "slab build");
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]);
-  ctx->build_ms = ms;
-  ctx->pts_a.assign(p->pts_a, p->pts_a + 2 * static_cast<size_t>(p->n_a));
-  ctx->pts_b.assign(p->pts_b, p->pts_b + 2 * static_cast<size_t>(p->n_b));
-  ctx->prepared = true;
-  return OTPRG_OK;
-}
-
-int otprg_shard_begin(otprg_ctx* ctx) {
-  if (!ctx) return OTPRG_PARAMETER;
-  if (!ctx->prepared || !ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_shard_prepare() first");
-  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-  Ctl h{};
-  h.n_a = ctx->ia;
-  h.n_b = ctx->ib;
-  h.lda = ctx->lda;
-  h.thresh = static_cast<int32_t>(std::floor(ctx->eps * static_cast<double>(std::min(ctx->n_a, ctx->n_b))));
-  h.phase_cap = static_cast<int32_t>(ctx->fc_cap - 1);
-  h.tmax = otprg::storage_tmax(ctx->width);
-  h.cnt[0] = ctx->ib;
-  CK(cudaMemcpyAsync(ctx->ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream), "H2D ctl");
-  otprg::SolveArgs A{};
-  A.t = ctx->t.p;
-  A.yb = ctx->yb.as<int32_t>();
-  A.match_a = ctx->ma.as<int32_t>();
-  A.match_b = ctx->mb.as<int32_t>();
-  A.holder[0] = ctx->holder.as<unsigned long long>();
-  A.holder[1] = A.holder[0] + ctx->ia;
-  A.rowmin = ctx->rowmin.p;
-  A.lmeta = ctx->lmeta.as<int4>();
-  A.list[0] = ctx->lists.as<int32_t>();
-  const int full = (ctx->ia + 511) / 512 * 512;
-  CK(otprg::launch_init_state(A, ctx->ia, ctx->ib, full, ctx->width, ctx->stream), "init launch");
-  ctx->sh_phase = 0;
-  ctx->sh_parked = 0;
-  ctx->sh_n = 0;
-  ctx->sh_top_ready = false;
-  ctx->begun = true;
-  ctx->completed = false;
-  return OTPRG_OK;
-}
-
-int otprg_shard_top(otprg_ctx* ctx, int32_t* n_out, int32_t* finished) {
-  if (!ctx) return OTPRG_PARAMETER;
-  if (!ctx->begun || !ctx->sharded) return fail(ctx, OTPRG_PARAMETER, "otprg_shard_begin() first");
-  if (!ctx->sh_top_ready) {  // (after a complete phase the DA call has run the top already)
-    otprg::ShardArgs S = shard_args(ctx);
-    CK(otprg::launch_shard_top(S, ctx->sh_phase, ctx->sh_phase > 0, false, ctx->stream),
-       "shard_top launch");
-    CK(otprg::launch_shard_compact(S, false, ctx->stream), "shard_compact launch");
-    Ctl h{};
-    int st = read_ctl(ctx, &h);
-    if (st) return st;
-    ctx->sh_n = h.cnt[ctx->sh_phase & 1];
-    ctx->sh_done = h.done;
-  }
-  ctx->sh_top_ready = false;
-  if (n_out) *n_out = ctx->sh_n;
-  if (finished) *finished = ctx->sh_done;
-  return OTPRG_OK;
-}
-
-int otprg_shard_scan(otprg_ctx* ctx, int32_t* cand, int32_t* meta_words, int32_t cap,
-                     int32_t refill) {
-  int2* meta = reinterpret_cast<int2*>(meta_words);
-  if (!ctx) return OTPRG_PARAMETER;
-  // cap = slots per rank in the exchange buffers: >= the phase's proposers
-  // (the driver passes n_i so the all-gather moves only the used prefix)
-  if (cap < ctx->sh_n || cap > ctx->sh_cap) return fail(ctx, OTPRG_PARAMETER, "bad exchange slot count");
-  otprg::ShardArgs S = shard_args(ctx);
-  S.cap = cap;
-  const int4* req = refill ? ctx->sh_park[ctx->sh_park_cur].as<int4>() : nullptr;
-  const int nreq = refill ? ctx->sh_parked : ctx->sh_n;
-  S.first_phase = ctx->sh_phase == 0;  // init_state: Y == 0 on A, 1 on B
-  CK(otprg::launch_shard_scan(S, req, nreq, cand, meta, ctx->stream), "shard_scan launch");
-  // no sync: the exchange and the DA are ordered after the scan on the
-  // context's stream (otprg_set_stream puts every rank of a process and the
-  // NCCL all-gather on one stream)
-  return OTPRG_OK;
-}
-
-int otprg_shard_da(otprg_ctx* ctx, const int32_t* cand, const int32_t* meta_words, int32_t cap,
-                   int32_t resume, int32_t* parked) {
-  const int2* meta = reinterpret_cast<const int2*>(meta_words);
-  if (!ctx) return OTPRG_PARAMETER;
-  otprg::ShardArgs S = shard_args(ctx);
-  S.cap = cap;
-  CK(cudaMemsetAsync(&ctx->ctl.as<Ctl>()->work[1], 0, sizeof(int32_t), ctx->stream), "memset");
-  const int4* resume_list = resume ? ctx->sh_park[ctx->sh_park_cur].as<int4>() : nullptr;
-  const int nchains = resume ? ctx->sh_parked : ctx->sh_n;
-  CK(otprg::launch_shard_da(S, ctx->sh_phase + 1, cand, meta, nchains, resume_list, ctx->stream),
-     "shard_da launch");
-  // If no chain parked the phase is complete: run the next top (apply M',
-  // termination, free list) in the same round trip; the kernels check.
-  otprg::ShardArgs T = S;
-  T.mp_prev = S.mp_out;
-  CK(otprg::launch_shard_top(T, ctx->sh_phase + 1, true, true, ctx->stream), "shard_top launch");
-  CK(otprg::launch_shard_compact(T, true, ctx->stream), "shard_compact launch");
-  Ctl h{};
-  int st = read_ctl(ctx, &h);
-  if (st) return st;
-  ctx->sh_park_cur ^= 1;
-  ctx->sh_parked = h.work[1];
-  if (ctx->sh_parked == 0) {  // the phase is complete
-    ctx->sh_phase += 1;
-    ctx->sh_n = h.cnt[ctx->sh_phase & 1];
-    ctx->sh_done = h.done;
-    ctx->sh_top_ready = true;
-  }
-  if (parked) *parked = ctx->sh_parked;
-  return OTPRG_OK;
-}
-
-int otprg_shard_finish(otprg_ctx* ctx, otprg_result* res) {
-  if (!ctx) return OTPRG_PARAMETER;
-  if (!res || !res->match_of_a || !res->match_of_b)
-    return fail(ctx, OTPRG_PARAMETER, "result buffers are null");
-  int st = launch_finish(ctx);
-  if (st) return st;
-  Ctl h{};
-  if ((st = export_state(ctx, res, &h))) return st;
-  res->build_ms = ctx->build_ms;
-  return check_status(ctx, h, true);
-}
-
-}  // extern "C"

@@ -4,8 +4,12 @@
 // rank runs the same deterministic deferred acceptance, so all ranks hold the
 // identical state after each phase and only candidate lists cross NVLink.
 //
-// Per phase (host-driven, one process per GPU; see shard_host in
-// otprg_capi.cpp and paper_2203_03732_b200/sharded.py):
+// Every kernel reads its round parameters (mode, request count, phase, park
+// buffer) from the control block, so the same launches run host-driven (one
+// host sync per round, torch.distributed exchange: sharded.py) or as the body
+// of a CUDA-graph WHILE loop that never returns to the host (resident mode,
+// otprg_shard_solve_resident: the exchange is a peer-memory push + flags).
+// Per round:
 //   shard_top   apply M' of the previous phase (apply_phase,
 //               assignment.cpp:210-235), termination / phase cap
 //               (:324-334, :356-358), inverse map b -> list index;
@@ -35,6 +39,8 @@ namespace {
 #define OTPRG_SHARD_UNROLL 12  // A/B (scripts/ab_shard_unroll.sh): 4 / 8 / 12 / 16 / 24 -> 13.6 / 13.5 / 12.1 / 15.8 / 18.3 ms
 #endif
 
+constexpr int kOtfTiledMin = 64;  // requests from which the tiled on-the-fly kernel runs
+
 __device__ __forceinline__ uint32_t t_get(const ShardArgs& S, int a) {
   return S.width == 1   ? (uint32_t)static_cast<const uint8_t*>(S.t)[a]
          : S.width == 2 ? (uint32_t)static_cast<const uint16_t*>(S.t)[a]
@@ -44,6 +50,44 @@ __device__ __forceinline__ void t_set(const ShardArgs& S, int a, uint32_t v) {
   if (S.width == 1) static_cast<uint8_t*>(S.t)[a] = (uint8_t)v;
   else if (S.width == 2) static_cast<uint16_t*>(S.t)[a] = (uint16_t)v;
   else static_cast<uint32_t*>(S.t)[a] = v;
+}
+
+// Round parameters, read by every kernel at its start (written by the ctl
+// kernel of the previous round; ld.cg: never from a stale L1 line).
+struct Round {
+  int mode, nreq;
+  uint32_t phase;     // phases completed (the running phase is phase + 1)
+  const int4* req;    // mode 1: the parked chains (list index, b, restart)
+  int4* park_out;     // chains parked by this round's DA
+  bool stop;          // finished or failed: nothing to do
+};
+__device__ __forceinline__ Round round_of(const ShardArgs& S) {
+  const Ctl* c = S.ctl;
+  Round r;
+  // (sh_live, not done: done is set by the top kernel inside a round)
+  r.stop = __ldcg(&c->sh_live) == 0 || __ldcg(&c->status) != 0;
+  r.mode = __ldcg(&c->sh_mode);
+  r.nreq = r.stop ? 0 : __ldcg(&c->sh_nreq);
+  r.phase = __ldcg(&c->phase);
+  const int pc = __ldcg(&c->sh_park_cur);
+  r.req = r.mode ? S.park[pc] : nullptr;
+  r.park_out = S.park[pc ^ 1];
+  return r;
+}
+
+// Pieces per request of the slab / per-row on-the-fly scans: enough warps to
+// cover the GPU (~16 resident per SM) when requests are few, each piece >=
+// one 4 KB warp step, at most kMaxSegs, within the merge buffers.
+__device__ __forceinline__ int scan_segs(const ShardArgs& S, int nreq) {
+  const int units = S.thr ? ((S.hi - S.lo) + 31) / 32                 // 32-element groups (on the fly)
+                          : ((S.hi - S.lo) * S.width + 511) / 512;    // 32-vector units of a slab row
+  const int target = 148 * 16;
+  int segs = 1;
+  if (S.seg_hits && nreq > 0 && nreq * 2 <= target) {
+    segs = min(min(kMaxSegs, target / nreq), max(1, units / 8));
+    segs = max(1, min(segs, kSegWarps / nreq));
+  }
+  return segs;
 }
 
 // Scan request: (list index, b, start position (global a)).  req == nullptr:
@@ -58,15 +102,12 @@ __device__ __forceinline__ void t_set(const ShardArgs& S, int a, uint32_t v) {
 // pieces in order (the first K hits overall; resume after the K-th), so a
 // 200 KB row costs a few dependent steps instead of ~50.
 template <typename T, bool kP1>
-__global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4* __restrict__ req,
-                                                         int nreq, int segs, int32_t* __restrict__ cand,
-                                                         int2* __restrict__ meta) {
+__device__ __forceinline__ void scan_slab_item(const ShardArgs& S, const int4* __restrict__ req, int segs,
+                                               int w, int32_t* __restrict__ cand, int2* __restrict__ meta) {
   using SD = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
   constexpr int kU = OTPRG_SHARD_UNROLL;  // 16-byte loads in flight per lane (12: 6 KB per warp step)
   const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= nreq * segs) return;
   const int r = w / segs, sg = w - r * segs;
   int i, b, start;
   if (req) {
@@ -185,20 +226,42 @@ __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, const int4
   }
 }
 
-// Top of the phase after `phase_done` phases: apply M' of phase phase_done
-// (replicated), termination test, counters for the next phase.
-__global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t phase_done,
-                                                         int apply, int cond) {
+template <typename T>
+__global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, int32_t* __restrict__ cand,
+                                                         int2* __restrict__ meta) {
+  const Round rd = round_of(S);
+  if (rd.stop) return;
+  const int segs = scan_segs(S, rd.nreq);
+  const int work = rd.nreq * segs;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < work; w += nwarps) {
+    if (rd.phase == 0)  // phase 1: t == 0 everywhere (init_state), no t traffic
+      scan_slab_item<T, true>(S, rd.req, segs, w, cand, meta);
+    else
+      scan_slab_item<T, false>(S, rd.req, segs, w, cand, meta);
+  }
+}
+
+// Top of a phase: apply M' of the phase the DA just completed (replicated;
+// apply_phase, assignment.cpp:210-235), termination / phase cap (:324-334,
+// :356-358), counters of the next phase.  first: the top before phase 1
+// (nothing to apply).  Skipped while chains are parked (the phase goes on).
+// Reads only what earlier kernels wrote (ctl->phase is advanced by the ctl
+// kernel), so its blocks never race with its own thread 0.
+__global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, int first) {
   Ctl* ctl = S.ctl;
-  if (cond && ctl->work[1] != 0) return;  // chains parked: the phase goes on
+  if (__ldcg(&ctl->status)) return;
+  if (!first && (__ldcg(&ctl->work[1]) != 0 || __ldcg(&ctl->sh_live) == 0)) return;
+  const uint32_t phase_done = first ? 0u : __ldcg(&ctl->phase) + 1u;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
   const int par = phase_done & 1;
-  if (apply) {
-    const int m = ctl->mp_cnt[par];
+  if (!first) {
+    const int2* mp_prev = S.mps + (size_t)par * S.ib;
+    const int m = __ldcg(&ctl->mp_cnt[par]);
     for (int q = gtid; q < m; q += gthreads) {
-      const int2 e = S.mp_prev[q];
+      const int2 e = __ldcg(mp_prev + q);
       const int a = e.x, old_b = e.y;
-      const int b = (int)(uint32_t)S.holder[a];
+      const int b = (int)(uint32_t)__ldcg(S.holder + a);
       if (old_b >= 0) S.match_b[old_b] = -1;
       S.match_a[a] = b;
       S.match_b[b] = a;
@@ -207,10 +270,8 @@ __global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t p
       t_set(S, a, nt);
     }
   }
-  const int n = ctl->cnt[par];
+  const int n = __ldcg(&ctl->cnt[par]);
   if (gtid == 0) {
-    ctl->phase = phase_done;
-    if (apply) ctl->applied = phase_done;
     if (n <= ctl->thresh) {  // (double)n_i <= eps*m  <=>  n_i <= floor(eps*m)
       ctl->done = 1;
       ctl->full_match = (n == 0);
@@ -222,7 +283,7 @@ __global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t p
       const int nx = par ^ 1;  // counters the coming phase appends to
       ctl->cnt[nx] = 0;
       ctl->mp_cnt[nx] = 0;
-      ctl->exh[nx] = 0;  // (work[1], the parked count, is reset before every DA launch)
+      ctl->exh[nx] = 0;
     }
   }
 }
@@ -233,13 +294,17 @@ __global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, uint32_t p
 // at the range's offset (block-wide scans per 1024-entry tile).
 constexpr int kCompactBlocks = 148;
 
-__global__ void __launch_bounds__(1024) shard_compact_count_kernel(ShardArgs S, int cond, int* counts) {
-  if (S.ctl->done || (cond && S.ctl->work[1] != 0)) return;
+__device__ __forceinline__ bool compact_skip(const Ctl* c) {
+  return __ldcg(&c->done) || __ldcg(&c->status) || __ldcg(&c->work[1]) != 0;
+}
+
+__global__ void __launch_bounds__(1024) shard_compact_count_kernel(ShardArgs S, int* counts) {
+  if (compact_skip(S.ctl)) return;
   const int n_b = S.ctl->n_b;
   const int chunk = (n_b + gridDim.x - 1) / gridDim.x;
   const int lo = min(n_b, (int)blockIdx.x * chunk), hi = min(n_b, lo + chunk);
   int c = 0;
-  for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) c += (S.match_b[q] == -1);
+  for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) c += (__ldcg(S.match_b + q) == -1);
   __shared__ int s_sum;
   if (threadIdx.x == 0) s_sum = 0;
   __syncthreads();
@@ -249,9 +314,8 @@ __global__ void __launch_bounds__(1024) shard_compact_count_kernel(ShardArgs S, 
   if (threadIdx.x == 0) counts[blockIdx.x] = s_sum;
 }
 
-__global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, int cond,
-                                                                   const int* counts) {
-  if (S.ctl->done || (cond && S.ctl->work[1] != 0)) return;
+__global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, const int* counts) {
+  if (compact_skip(S.ctl)) return;
   __shared__ int s_warp[32];
   __shared__ int s_base;
   const int n_b = S.ctl->n_b;
@@ -259,7 +323,7 @@ __global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, 
   const int lo = min(n_b, (int)blockIdx.x * chunk), hi = min(n_b, lo + chunk);
   if (threadIdx.x == 0) {
     int off = 0;
-    for (int g = 0; g < (int)blockIdx.x; ++g) off += counts[g];
+    for (int g = 0; g < (int)blockIdx.x; ++g) off += __ldcg(counts + g);
     s_base = off;
   }
   __syncthreads();
@@ -267,7 +331,7 @@ __global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int t0 = lo; t0 < hi; t0 += blockDim.x) {  // one tile: block-wide ordered scan of the flags
     const int q = t0 + threadIdx.x;
-    const bool f = q < hi && S.match_b[q] == -1;
+    const bool f = q < hi && __ldcg(S.match_b + q) == -1;
     const unsigned bal = __ballot_sync(kFull, f);
     if (lane == 0) s_warp[warp] = __popc(bal);
     __syncthreads();
@@ -287,21 +351,50 @@ __global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, 
   }
 }
 
-// Deferred acceptance over merged candidate lists, one warp per chain.
-// resume_list == nullptr: a chain per free b; else per parked entry.
-__global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, uint32_t phase,
-                                                       const int32_t* __restrict__ cand,
-                                                       const int2* __restrict__ meta, int nchains,
-                                                       const int4* __restrict__ resume_list) {
+// Round bookkeeping (one thread), after the DA (and the top when the phase
+// completed): parked chains -> a refill round over them; else the phase is
+// complete -> the next phase's first round over its free list.  Sets the
+// resident loop's WHILE condition (continue while not finished and no error).
+__global__ void shard_ctl_kernel(ShardArgs S, int first, cudaGraphConditionalHandle cond, int use_cond) {
+  Ctl* c = S.ctl;
+  if (!first && !c->sh_live) {  // a loop entered after the solve had finished: nothing ran
+    if (use_cond) cudaGraphSetConditional(cond, 0u);
+    return;
+  }
+  const int parked = first ? 0 : c->work[1];
+  if (parked > 0) {
+    c->sh_mode = 1;
+    c->sh_nreq = parked;
+    c->sh_rounds += 1;
+  } else {
+    if (!first) c->phase += 1;  // the DA's phase is complete (its top ran)
+    c->applied = c->phase;
+    c->sh_mode = 0;
+    c->sh_nreq = c->done ? 0 : c->cnt[c->phase & 1];
+  }
+  if (!first) {
+    c->sh_park_cur ^= 1;
+    c->sh_epoch += 1;
+  }
+  c->work[1] = 0;
+  const int go = !c->done && !c->status;
+  c->sh_live = go;
+  if (use_cond) cudaGraphSetConditional(cond, go ? 1u : 0u);
+}
+
+// Deferred acceptance over merged candidate lists, one warp per chain
+// (grid-stride over the round's chains).  Mode 0: a chain per free b of the
+// phase; mode 1: the parked chains resume.
+__device__ __forceinline__ void da_chain(const ShardArgs& S, const Round& rd, int w,
+                                         const int32_t* __restrict__ cand, const int2* __restrict__ meta) {
   Ctl* ctl = S.ctl;
   const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= nchains) return;
+  const uint32_t phase = rd.phase + 1u;
   const uint32_t cur_tag = ~phase;
   const int par = phase & 1;
   int i, b, start;
-  if (resume_list) {
-    const int4 r = resume_list[w];
+  if (rd.req) {
+    const int4 r = __ldcg(rd.req + w);
     i = r.x;
     b = r.y;
     start = r.z;
@@ -332,7 +425,7 @@ __global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, uint32_t pha
     if (a < 0 && restart >= 0) {  // park until the gap is rescanned
       if (lane == 0) {
         const int pos = atomicAdd(&ctl->work[1], 1);
-        S.park_out[pos] = make_int4(i, b, restart, 0);
+        rd.park_out[pos] = make_int4(i, b, restart, 0);
       }
       return;
     }
@@ -364,12 +457,90 @@ __global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, uint32_t pha
       const int partner = __ldcg(S.match_a + a);  // complete: applied at this phase's top
       if (partner >= 0) atomicAdd(&ctl->cnt[par], 1);
       const int pos = atomicAdd(&ctl->mp_cnt[par], 1);
-      S.mp_out[pos] = make_int2(a, partner);
+      S.mps[(size_t)par * S.ib + pos] = make_int2(a, partner);
     }
     return;
   }
 }
 
+__global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, const int32_t* __restrict__ cand,
+                                                       const int2* __restrict__ meta) {
+  const Round rd = round_of(S);
+  if (rd.stop) return;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rd.nreq; w += nwarps)
+    da_chain(S, rd, w, cand, meta);
+}
+
+// Peer exchange of a device group (resident multi-GPU loop): push the local
+// shards' slots of this round (nreq rows) into every peer group's exchange
+// buffers over NVLink peer memory, then — last block — release this round's
+// epoch into every peer's flag array and wait (acquire, system scope) until
+// every peer's flag in ours reached it.  Epochs only grow (never reset), so a
+// peer that runs ahead can never be missed.  A wait longer than 20 s reports
+// status 6 (device) and the loop ends instead of hanging.
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// blk / nblk: this block's index among the blocks pushing for the group.
+__device__ __forceinline__ void push_body(const ShardArgs& S, const int32_t* __restrict__ cand,
+                                          const int2* __restrict__ meta, const ShardPeers& P, int blk, int nblk) {
+  const Round rd = round_of(S);
+  if (rd.stop) return;
+  const uint32_t epoch = __ldcg(&S.ctl->sh_epoch) + 1u;
+  const int nreq = rd.nreq, K = S.K;
+  const size_t tid = (size_t)blk * blockDim.x + threadIdx.x, nthr = (size_t)nblk * blockDim.x;
+  for (int g = P.shard_lo; g < P.shard_hi; ++g) {
+    const size_t c0 = (size_t)g * S.cap * K, m0 = (size_t)g * S.cap;
+    const size_t nc = (size_t)nreq * K;
+    for (int p = 0; p < P.n; ++p) {
+      for (size_t q = tid; q < nc; q += nthr) P.cand[p][c0 + q] = __ldcg(cand + c0 + q);
+      for (size_t q = tid; q < (size_t)nreq; q += nthr) P.meta[p][m0 + q] = __ldcg(meta + m0 + q);
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(P.arrive, 1u) == (unsigned)nblk - 1u;
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  *P.arrive = 0;  // ready for the next round
+  __threadfence_system();
+  for (int p = 0; p < P.n; ++p) st_release_sys(P.flag[p] + P.my_group, epoch);
+  const unsigned long long t0 = globaltimer();
+  for (int q = 0; q < P.n_groups; ++q) {
+    if (q == P.my_group) continue;
+    while ((int)(ld_acquire_sys(P.my_flags + q) - epoch) < 0) {
+      if (globaltimer() - t0 > 20000000000ull) {
+        report(S.ctl, 6, -2, q, (int)epoch);
+        return;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) shard_push_kernel(ShardArgs S, const int32_t* __restrict__ cand,
+                                                         const int2* __restrict__ meta, ShardPeers P) {
+  push_body(S, cand, meta, P, blockIdx.x, gridDim.x);
+}
+
+// Self-test of the exchange protocol on ONE device: every group's push runs
+// as a slice of one cooperative grid (all blocks co-resident), so the groups'
+// flag waits are satisfied by blocks that are guaranteed to run — the
+// emulation the multi-GPU push needs on a single GPU.
+__global__ void __launch_bounds__(256) shard_push_emulate_kernel(const ShardArgs* __restrict__ S,
+                                                                 const int32_t* const* __restrict__ cand,
+                                                                 const int2* const* __restrict__ meta,
+                                                                 const ShardPeers* __restrict__ P, int nblk) {
+  const int g = blockIdx.x / nblk;
+  push_body(S[g], cand[g], meta[g], P[g], blockIdx.x - g * nblk, nblk);
+}
 
 // On-the-fly variant (OTPRG_FLAG_ON_THE_FLY): no kT slab.  Each lane
 // takes one demand point per 32-element group, forms d2 = dx*dx + dy*dy in
@@ -379,16 +550,11 @@ __global__ void __launch_bounds__(256) shard_da_kernel(ShardArgs S, uint32_t pha
 // memory: no sqrt, no division, 16 B of point per element instead of w B of kT.
 // Outputs, pieces and the merge as shard_scan_kernel.
 template <typename T>
-__global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const int4* __restrict__ req,
-                                                             int nreq, int segs, int32_t* __restrict__ cand,
-                                                             int2* __restrict__ meta) {
-  extern __shared__ double s_thr[];
-  for (int j = threadIdx.x; j < S.thr_n; j += blockDim.x) s_thr[j] = S.thr[j];
-  __syncthreads();
+__device__ __forceinline__ void scan_otf_item(const ShardArgs& S, const double* __restrict__ s_thr,
+                                              const int4* __restrict__ req, int segs, int w,
+                                              int32_t* __restrict__ cand, int2* __restrict__ meta) {
   constexpr int kG = 8;  // 32-element groups per warp step
   const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= nreq * segs) return;
   const int r = w / segs, sg = w - r * segs;
   int i, b, start;
   if (req) {
@@ -483,6 +649,22 @@ __global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const 
 }
 
 
+// Few requests (or no room for the tiled kernel): a warp per (request, piece).
+template <typename T>
+__global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, int32_t* __restrict__ cand,
+                                                             int2* __restrict__ meta) {
+  const Round rd = round_of(S);
+  if (rd.stop || (S.otf_tiled && rd.nreq >= kOtfTiledMin)) return;
+  extern __shared__ double s_thr[];
+  for (int j = threadIdx.x; j < S.thr_n; j += blockDim.x) s_thr[j] = S.thr[j];
+  __syncthreads();
+  const int segs = scan_segs(S, rd.nreq);
+  const int work = rd.nreq * segs;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < work; w += nwarps)
+    scan_otf_item<T>(S, s_thr, rd.req, segs, w, cand, meta);
+}
+
 // On-the-fly, many requests: a block takes kOtfRows requests (one warp
 // each) and streams the slab's demand points and t through shared memory in
 // kOtfChunk-point chunks (two stages filled by 1-D TMA bulk copies, the next
@@ -503,20 +685,28 @@ __global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, const 
 #endif
 constexpr int kOtfRows = OTPRG_OTF_ROWS, kOtfChunk = OTPRG_OTF_CHUNK;
 
+struct OtfTileSmem {
+  unsigned long long* bar;  // [2] stage barriers
+  int* lo_start;
+  int* act;                 // [3]
+  const double2* pair;      // (thr[m], thr[m+1])
+};
+
+// One work item of the tiled on-the-fly scan: row group grp's piece sg.
+// `par` carries the stage barriers' phase bits across items.
 template <typename T, bool kP1>
-__global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(ShardArgs S,
-                                                                            const int4* __restrict__ req,
-                                                                            int nreq, int segs,
-                                                                            int32_t* __restrict__ cand,
-                                                                            int2* __restrict__ meta) {
-  extern __shared__ __align__(128) unsigned char s_dyn[];
+__device__ __forceinline__ void otf_tile_item(const ShardArgs& S, unsigned char* s_dyn, const OtfTileSmem& sm,
+                                              const int4* __restrict__ req, int nreq, int segs, int item,
+                                              unsigned& par, int32_t* __restrict__ cand,
+                                              int2* __restrict__ meta) {
   // stage st: points [kOtfChunk] double2 then t [kOtfChunk] T; the pair table after both stages
   constexpr size_t kStage = (size_t)kOtfChunk * (sizeof(double2) + sizeof(T));
-  double2* s_pair = reinterpret_cast<double2*>(s_dyn + 2 * kStage);
-  __shared__ __align__(8) unsigned long long bar[2];
-  __shared__ int s_lo_start, s_act[3];
+  const double2* s_pair = sm.pair;
+  unsigned long long* bar = sm.bar;
+  int& s_lo_start = *sm.lo_start;
+  int* s_act = sm.act;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = blockIdx.x / segs, sg = blockIdx.x - grp * segs;
+  const int grp = item / segs, sg = item - grp * segs;
   const int r = grp * kOtfRows + warp;
   const bool has = r < nreq;
   int i = 0, b = 0, start = 0;
@@ -538,11 +728,7 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
   if (threadIdx.x == 0) {
     s_lo_start = width_local;
     s_act[0] = s_act[1] = s_act[2] = 0;
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int j = threadIdx.x; j + 1 < S.thr_n; j += blockDim.x) s_pair[j] = make_double2(S.thr[j], S.thr[j + 1]);
   __syncthreads();
   if (lane == 0 && !done) atomicMin(&s_lo_start, lstart);
   int target = 0;  // (the table has <= 8192 levels: int is exact)
@@ -571,9 +757,10 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
     bulk_g2s(st, pa + c0, pb_bytes, &bar[k & 1]);
     if (!kP1) bulk_g2s(st + (size_t)kOtfChunk * sizeof(double2), tl + c0, tb, &bar[k & 1]);
   };
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    fence_proxy_async_smem();  // the stages were read (generic proxy) by the previous item
     for (int k = 0; k < min(2, nchunk); ++k) issue(k);
-  unsigned par = 0;
+  }
   int k = 0;
   for (; k < nchunk; ++k) {
     mbar_wait(&bar[k & 1], (par >> (k & 1)) & 1u);
@@ -649,7 +836,10 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
   }
   // an early stop leaves the chunk after the last consumed one in flight:
   // it must land before the block exits
-  if (threadIdx.x == 0 && k < nchunk) mbar_wait(&bar[k & 1], (par >> (k & 1)) & 1u);
+  if (k < nchunk) {
+    if (threadIdx.x == 0) mbar_wait(&bar[k & 1], (par >> (k & 1)) & 1u);
+    par ^= 1u << (k & 1);
+  }
   if (!has) return;
   if (segs == 1) {
     if (lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
@@ -682,80 +872,149 @@ __global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(Sha
   }
 }
 
-}  // namespace
-
-cudaError_t launch_shard_top(const ShardArgs& a, uint32_t phase_done, bool apply, bool cond,
-                             cudaStream_t s) {
-  shard_top_kernel<<<148, 1024, 0, s>>>(a, phase_done, apply ? 1 : 0, cond ? 1 : 0);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_shard_compact(const ShardArgs& a, bool cond, cudaStream_t s) {
-  shard_compact_count_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, cond ? 1 : 0, a.scratch);
-  shard_compact_write_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, cond ? 1 : 0, a.scratch);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_shard_scan(const ShardArgs& a, const int4* req, int nreq, int32_t* cand,
-                              int2* meta, cudaStream_t s) {
-  if (nreq <= 0) return cudaSuccess;
-  // Pieces per request: enough warps to cover the GPU (~16 resident per SM at
-  // this kernel's register use) when requests are few, each piece >= one
-  // 4 KB warp step, at most kMaxSegs, within the merge buffers.
-  const int units = a.thr ? ((a.hi - a.lo) + 31) / 32  // 32-element groups (on the fly)
-                          : ((a.hi - a.lo) * a.width + 511) / 512;  // 32-vector units of a slab row
-  const int target = 148 * 16;
-  int segs = 1;
-  if (a.seg_hits && nreq * 2 <= target) {
-    segs = std::min(std::min(kMaxSegs, target / nreq), std::max(1, units / 8));
-    segs = std::max(1, std::min(segs, kSegWarps / nreq));
+template <typename T>
+__global__ void __launch_bounds__(kOtfRows * 32) shard_scan_otf_tiled_kernel(ShardArgs S, int32_t* __restrict__ cand,
+                                                                            int2* __restrict__ meta) {
+  const Round rd = round_of(S);
+  if (rd.stop || !S.otf_tiled || rd.nreq < kOtfTiledMin) return;
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  constexpr size_t kStage = (size_t)kOtfChunk * (sizeof(double2) + sizeof(T));
+  double2* s_pair = reinterpret_cast<double2*>(s_dyn + 2 * kStage);
+  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ int s_lo_start, s_act[3];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int blocks = (nreq * segs * 32 + 255) / 256;
-  if (a.thr && nreq >= 64) {  // many rows: tile kOtfRows rows over shared point chunks
-    const size_t smem = 2 * (size_t)kOtfChunk * (sizeof(double2) + (size_t)a.width) +
-                        (size_t)a.thr_n * sizeof(double2);
-    const int groups = (nreq + kOtfRows - 1) / kOtfRows;
-    const int chunks = (a.hi - a.lo + kOtfChunk - 1) / kOtfChunk;
-    // enough blocks for ~4 per SM, pieces of >= 4 chunks, within the merge buffers
-    int tsegs = std::max(1, std::min({kMaxSegs, (148 * 4) / groups, chunks / 4, kSegWarps / nreq}));
-    if (!a.seg_hits) tsegs = 1;
+  for (int j = threadIdx.x; j + 1 < S.thr_n; j += blockDim.x) s_pair[j] = make_double2(S.thr[j], S.thr[j + 1]);
+  __syncthreads();
+  const OtfTileSmem sm{bar, &s_lo_start, s_act, s_pair};
+  const int nreq = rd.nreq;
+  const int groups = (nreq + kOtfRows - 1) / kOtfRows;
+  const int chunks = (S.hi - S.lo + kOtfChunk - 1) / kOtfChunk;
+  // pieces per row group: the grid's blocks over the groups, pieces of >= 4
+  // chunks, within the merge buffers
+  int segs = max(1, min(min(kMaxSegs, (int)gridDim.x / groups), min(chunks / 4, kSegWarps / nreq)));
+  if (!S.seg_hits) segs = 1;
+  unsigned par = 0;
+  for (int item = blockIdx.x; item < groups * segs; item += gridDim.x) {
     // phase 1 (every t(a) == 0 and every target == 0 after init_state): the
     // level-0 test d2 < thr[1] alone, no t stage
-    with_width(a.width, [&](auto tag) {
-      auto fn = a.first_phase ? shard_scan_otf_tiled_kernel<decltype(tag), true>
-                              : shard_scan_otf_tiled_kernel<decltype(tag), false>;
-      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fn<<<groups * tsegs, kOtfRows * 32, smem, s>>>(a, req, nreq, tsegs, cand, meta);
-      return 0;
-    });
-    return cudaGetLastError();
+    if (rd.phase == 0) otf_tile_item<T, true>(S, s_dyn, sm, rd.req, nreq, segs, item, par, cand, meta);
+    else otf_tile_item<T, false>(S, s_dyn, sm, rd.req, nreq, segs, item, par, cand, meta);
+    __syncthreads();
   }
-  if (a.thr) {
-    const size_t smem = (size_t)a.thr_n * sizeof(double);
-    with_width(a.width, [&](auto tag) {
-      auto fn = shard_scan_otf_kernel<decltype(tag)>;
-      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fn<<<blocks, 256, smem, s>>>(a, req, nreq, segs, cand, meta);
-      return 0;
-    });
-    return cudaGetLastError();
-  }
+}
+
+}  // namespace
+
+namespace {
+size_t otf_tiled_smem(int width, int thr_n) {
+  return 2 * (size_t)kOtfChunk * (sizeof(double2) + (size_t)width) + (size_t)thr_n * sizeof(double2);
+}
+// Resident blocks per SM of a kernel at its launch shape (>= 1).
+template <typename K>
+int blocks_per_sm(K fn, int threads, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess || n < 1) n = 1;
+  return n;
+}
+}  // namespace
+
+static_assert(kOtfChunk % (32 * OTPRG_OTF_GU) == 0, "OTPRG_OTF_CHUNK must be a multiple of 32 * OTPRG_OTF_GU");
+static_assert((kOtfChunk * 16) % 16 == 0 && kOtfChunk % 16 == 0, "OTPRG_OTF_CHUNK must keep 16-byte stages");
+
+// Grid of the scan kernels: every SM filled with resident blocks (the
+// kernels loop over their work items, whose count is only known on the device).
+int shard_scan_grid(const ShardArgs& a, int num_sms) {
+  int g = 0;
   with_width(a.width, [&](auto tag) {
-    if (a.first_phase)
-      shard_scan_kernel<decltype(tag), true><<<blocks, 256, 0, s>>>(a, req, nreq, segs, cand, meta);
-    else
-      shard_scan_kernel<decltype(tag), false><<<blocks, 256, 0, s>>>(a, req, nreq, segs, cand, meta);
+    using T = decltype(tag);
+    if (a.thr) {
+      const int simple = blocks_per_sm(shard_scan_otf_kernel<T>, 256, (size_t)a.thr_n * sizeof(double));
+      g = num_sms * simple;
+      if (a.otf_tiled) {
+        const size_t smem = otf_tiled_smem(a.width, a.thr_n);
+        cudaFuncSetAttribute(shard_scan_otf_tiled_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        g = std::max(g, num_sms * blocks_per_sm(shard_scan_otf_tiled_kernel<T>, kOtfRows * 32, smem));
+      }
+    } else {
+      g = num_sms * blocks_per_sm(shard_scan_kernel<T>, 256, 0);
+    }
+    return 0;
+  });
+  return g;
+}
+
+// Whether the tiled on-the-fly kernel's stages + pair table fit the opt-in
+// shared-memory limit (else the per-row kernel serves every request count).
+bool shard_otf_tiled_fits(int width, int thr_n, int device) {
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  return otf_tiled_smem(width, thr_n) <= (size_t)optin;
+}
+
+cudaError_t launch_shard_scan(const ShardArgs& a, int32_t* cand, int2* meta, int grid, cudaStream_t s) {
+  with_width(a.width, [&](auto tag) {
+    using T = decltype(tag);
+    if (a.thr) {
+      const size_t smem1 = (size_t)a.thr_n * sizeof(double);
+      auto fn1 = shard_scan_otf_kernel<T>;
+      if (smem1 > 48 * 1024) cudaFuncSetAttribute(fn1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+      // each of the two exits at once unless the round's request count is its regime
+      fn1<<<grid, 256, smem1, s>>>(a, cand, meta);
+      if (a.otf_tiled) {
+        const size_t smem = otf_tiled_smem(a.width, a.thr_n);
+        auto fn = shard_scan_otf_tiled_kernel<T>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        fn<<<grid, kOtfRows * 32, smem, s>>>(a, cand, meta);
+      }
+    } else {
+      shard_scan_kernel<T><<<grid, 256, 0, s>>>(a, cand, meta);
+    }
     return 0;
   });
   return cudaGetLastError();
 }
 
-cudaError_t launch_shard_da(const ShardArgs& a, uint32_t phase, const int32_t* cand,
-                            const int2* meta, int nchains, const int4* resume_list,
+cudaError_t launch_shard_push(const ShardArgs& a, const int32_t* cand, const int2* meta,
+                              const ShardPeers& p, cudaStream_t s) {
+  shard_push_kernel<<<148, 256, 0, s>>>(a, cand, meta, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_push_emulated(const ShardArgs* a, const int32_t* const* cand, const int2* const* meta,
+                                       const ShardPeers* p, int n_groups, int nblk, cudaStream_t s) {
+  void* args[] = {(void*)&a, (void*)&cand, (void*)&meta, (void*)&p, (void*)&nblk};
+  return cudaLaunchCooperativeKernel((const void*)shard_push_emulate_kernel, dim3(n_groups * nblk), dim3(256),
+                                     args, 0, s);
+}
+
+cudaError_t launch_shard_da(const ShardArgs& a, const int32_t* cand, const int2* meta, int grid,
                             cudaStream_t s) {
-  if (nchains <= 0) return cudaSuccess;
-  const int blocks = (nchains * 32 + 255) / 256;
-  shard_da_kernel<<<blocks, 256, 0, s>>>(a, phase, cand, meta, nchains, resume_list);
+  shard_da_kernel<<<grid, 256, 0, s>>>(a, cand, meta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_after_da(const ShardArgs& a, cudaStream_t s) {
+  shard_top_kernel<<<148, 1024, 0, s>>>(a, 0);
+  shard_compact_count_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, a.scratch);
+  shard_compact_write_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, a.scratch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_ctl(const ShardArgs& a, cudaGraphConditionalHandle cond, bool use_cond,
+                             cudaStream_t s) {
+  shard_ctl_kernel<<<1, 1, 0, s>>>(a, 0, cond, use_cond ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_first_top(const ShardArgs& a, cudaStream_t s) {
+  shard_top_kernel<<<148, 1024, 0, s>>>(a, 1);
+  shard_compact_count_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, a.scratch);
+  shard_compact_write_kernel<<<kCompactBlocks, 1024, 0, s>>>(a, a.scratch);
+  shard_ctl_kernel<<<1, 1, 0, s>>>(a, 1, cudaGraphConditionalHandle{}, 0);
   return cudaGetLastError();
 }
 

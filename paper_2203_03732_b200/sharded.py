@@ -16,10 +16,17 @@ Results are bit-identical for every shard count (and to the single-GPU
 solver / the reference): the merged candidate order is the row order and
 deferred acceptance with a common priority has one outcome.
 
-Backends (same driver): ``DeviceRank`` drives one otprg_ctx through the C
-ABI; the exchange is ``LocalExchange`` (all ranks in one process share one
-buffer: several logical shards on one GPU) or ``TorchDistExchange`` (one
-process per GPU, torch.distributed all_gather over NCCL).
+Drivers: ``resident=True`` (default) runs every round on the device — one
+CUDA graph per GPU with a conditional WHILE node (otprg_shard_solve_resident):
+the shards of this process on one GPU run in stream order, and shards on other
+GPUs (other processes: CUDA IPC handles exchanged over torch.distributed) get
+the candidate slots pushed into their exchange blocks over NVLink peer memory
+with epoch flags; one host sync per solve.  ``resident=False`` is the
+host-driven protocol (one host sync per round): ``DeviceRank`` drives one
+otprg_ctx through the C ABI and the exchange is ``LocalExchange`` (all ranks
+of the process share one buffer) or ``TorchDistExchange`` (torch.distributed
+all_gather: NCCL, or gloo when several ranks share one GPU — the resident
+loop's cross-process flag waits need distinct GPUs).
 """
 from __future__ import annotations
 
@@ -89,6 +96,17 @@ class DeviceRank:
         r, bufs = self.solver._result(n_a, n_b, eps)
         self._ok(self._L.otprg_shard_finish(self._ctx, C.byref(r)))
         return Solver._pack(r, bufs)
+
+    def ipc_export(self, n_groups: int, my_group: int) -> bytes:
+        from . import _native as N
+        h = (C.c_char * N.IPC_HANDLE_BYTES)()
+        self._ok(self._L.otprg_shard_ipc_export(self._ctx, n_groups, my_group, h))
+        return bytes(h)
+
+    def ipc_attach(self, handles: list, group_shard_lo: list):
+        blob = b"".join(handles)
+        lo = np.asarray(group_shard_lo, np.int32)
+        self._ok(self._L.otprg_shard_ipc_attach(self._ctx, blob, len(handles), lo.ctypes.data))
 
     def set_stream(self, stream_handle: int):
         self._ok(self._L.otprg_set_stream(self._ctx, stream_handle))
@@ -166,19 +184,35 @@ def run_phases(ranks, exchange, cand_ptr, meta_ptr, cap: int, gather_args=()):
     return rounds
 
 
+def solve_resident(ranks):
+    """otprg_shard_solve_resident over this process's ranks: (Matching, SolveStats)."""
+    L = ranks[0]._L
+    n_a, n_b, eps = ranks[0].shape
+    r, bufs = ranks[0].solver._result(n_a, n_b, eps)
+    arr = (C.c_void_p * len(ranks))(*[x._ctx for x in ranks])
+    st = L.otprg_shard_solve_resident(arr, len(ranks), C.byref(r))
+    if st:
+        ranks[0].solver._raise(st)
+    return Solver._pack(r, bufs)
+
+
 class ShardedSolver:
     """Prepared sharded solve, reusable across solves of the same instance.
 
     ``distributed=False``: all ``n_shards`` shards live in this process on
-    ``opt.device`` (LocalExchange).  ``distributed=True``: this process is
-    rank ``dist.get_rank()`` of ``dist.get_world_size()`` shards on GPU
-    LOCAL_RANK (TorchDistExchange over NCCL)."""
+    ``opt.device`` (logical shards; ``devices``: one device per shard).
+    ``distributed=True``: this process is rank ``dist.get_rank()`` of
+    ``dist.get_world_size()`` shards on GPU LOCAL_RANK (or OTPRG_DEVICE).
+    ``resident``: device-resident loop (default; across processes it needs
+    distinct GPUs per rank), else the host-driven protocol."""
 
     def __init__(self, inst: AssignmentInstance, opt: AssignmentOptions, n_shards: int = 1,
-                 K: int = K_DEFAULT, distributed: bool = False, on_the_fly: bool = False):
+                 K: int = K_DEFAULT, distributed: bool = False, on_the_fly: bool = False,
+                 resident: bool | None = None, devices: list | None = None):
         _check_options(inst, opt)
         if inst.pts_a is None or inst.pts_b is None:
             raise ParameterError("the sharded path builds slabs from 2-D point sets")
+        self.distributed = distributed
         if distributed:
             import torch.distributed as dist
             rank, world = dist.get_rank(), dist.get_world_size()
@@ -188,28 +222,55 @@ class ShardedSolver:
             self.ranks[0].prepare(inst, opt.eps, world, rank, K, opt.storage, on_the_fly)
             self.n_shards = world
             self.exchange = TorchDistExchange(rank, world)
+            if resident is None:  # the flag waits need one GPU per rank
+                import torch
+                devs = [None] * world
+                dist.all_gather_object(devs, (socket_host(), device))
+                resident = len(set(devs)) == world
+            if resident:
+                h = self.ranks[0].ipc_export(world, rank)
+                handles = [None] * world
+                dist.all_gather_object(handles, h)
+                self.ranks[0].ipc_attach(handles, list(range(world)))
         else:
-            device = opt.device
-            self.ranks = [DeviceRank(device) for _ in range(n_shards)]
+            devs = list(devices) if devices is not None else [opt.device] * n_shards
+            if len(devs) != n_shards:
+                raise ParameterError("one device per shard")
+            device = devs[0]
+            self.ranks = [DeviceRank(d) for d in devs]
             for g, r in enumerate(self.ranks):
                 r.prepare(inst, opt.eps, n_shards, g, K, opt.storage, on_the_fly)
             self.n_shards = n_shards
             self.exchange = LocalExchange()
+            if resident is None:
+                resident = True
+            if not resident and len(set(devs)) > 1:
+                raise ParameterError("the host-driven protocol keeps in-process shards on one device")
+        self.resident = bool(resident)
         self.cap = self.ranks[0].cap
-        self.cand, self.meta = _buffers(self.n_shards, self.cap, K, device)
-        self.gather_args = (self.cand, self.meta, K) if distributed else ()
-        # one stream for every context of this process and the exchange:
-        # scan -> all-gather -> DA are ordered on it without host syncs
-        import torch
-        self.stream = torch.cuda.Stream(device=device)
-        for r in self.ranks:
-            r.set_stream(self.stream.cuda_stream)
+        if not self.resident:
+            self.cand, self.meta = _buffers(self.n_shards, self.cap, K, device)
+            self.gather_args = (self.cand, self.meta, K) if distributed else ()
+            # one stream for every context of this process and the exchange:
+            # scan -> all-gather -> DA are ordered on it without host syncs
+            import torch
+            self.stream = torch.cuda.Stream(device=device)
+            for r in self.ranks:
+                r.set_stream(self.stream.cuda_stream)
 
     def solve(self, keep_state: bool = False):
         """One full solve (state re-initialised).  Returns (Matching,
         SolveStats) of the first local rank after checking local ranks agree.
-        ``keep_state``: also return the state before completion (rank 0's
-        snapshot) as a third element, for verify_feasibility."""
+        ``keep_state`` (host-driven mode): also return the state before
+        completion (rank 0's snapshot) as a third element, for
+        verify_feasibility."""
+        if self.resident:
+            if keep_state:
+                raise ParameterError("keep_state needs the host-driven protocol (resident=False)")
+            if self.distributed:
+                import torch.distributed as dist
+                dist.barrier()  # every rank's graph launches after every rank attached
+            return solve_resident(self.ranks)
         import torch
         with torch.cuda.stream(self.stream):
             rounds = run_phases(self.ranks, self.exchange, self.cand.data_ptr(),
@@ -238,12 +299,18 @@ class ShardedSolver:
             r.close()
 
 
+def socket_host() -> str:
+    import socket
+    return socket.gethostname()
+
+
 def solve_assignment_sharded(inst: AssignmentInstance, opt: AssignmentOptions, n_shards: int,
-                             K: int = K_DEFAULT, on_the_fly: bool = False):
-    """All shards in this process on opt.device (LocalExchange): G logical
-    shards on one GPU.  ``on_the_fly``: no kT slabs, costs from the points in
-    the scans (OTPRG_FLAG_ON_THE_FLY).  Returns (Matching, SolveStats)."""
-    sv = ShardedSolver(inst, opt, n_shards, K, on_the_fly=on_the_fly)
+                             K: int = K_DEFAULT, on_the_fly: bool = False, resident: bool = True,
+                             devices: list | None = None):
+    """All shards in this process (on opt.device, or one per entry of
+    ``devices``).  ``on_the_fly``: no kT slabs, costs from the points in the
+    scans (OTPRG_FLAG_ON_THE_FLY).  Returns (Matching, SolveStats)."""
+    sv = ShardedSolver(inst, opt, n_shards, K, on_the_fly=on_the_fly, resident=resident, devices=devices)
     try:
         return sv.solve()
     finally:
@@ -251,11 +318,74 @@ def solve_assignment_sharded(inst: AssignmentInstance, opt: AssignmentOptions, n
 
 
 def solve_assignment_distributed(inst: AssignmentInstance, opt: AssignmentOptions,
-                                 K: int = K_DEFAULT, on_the_fly: bool = False):
-    """One rank per process/GPU under torch.distributed (NCCL): each process
-    calls this with the same instance; every rank returns the same result."""
-    sv = ShardedSolver(inst, opt, K=K, distributed=True, on_the_fly=on_the_fly)
+                                 K: int = K_DEFAULT, on_the_fly: bool = False,
+                                 resident: bool | None = None):
+    """One rank per process/GPU under torch.distributed: each process calls
+    this with the same instance; every rank returns the same result."""
+    sv = ShardedSolver(inst, opt, K=K, distributed=True, on_the_fly=on_the_fly, resident=resident)
     try:
         return sv.solve()
     finally:
         sv.close()
+
+
+class MultiSolver:
+    """A multi-device context (otprg_create_multi): point instances are
+    A-row-sharded over ``devices`` (one shard per entry; a device listed
+    several times holds several logical shards) and solved by the resident
+    loop; other instances run on the first device.  The C++ drop-in's
+    otprg::AssignmentOptions::devices takes the same path."""
+
+    def __init__(self, devices: list, K: int = K_DEFAULT):
+        from . import _native as N
+        self._L = N.lib()
+        self._ctx = C.c_void_p()
+        arr = (C.c_int32 * len(devices))(*devices)
+        st = self._L.otprg_create_multi(arr, len(devices), C.byref(self._ctx))
+        if st:
+            from .api import DeviceError
+            raise DeviceError(f"otprg_create_multi({devices}) failed with status {st}")
+        self.devices = list(devices)
+        self._keep = ()
+        st = self._L.otprg_set_shard_k(self._ctx, K)
+        if st:
+            self._raise(st)
+
+    # the Solver helpers work on any object with _L / _ctx / _keep
+    _raise = Solver._raise
+    _problem = Solver._problem
+    _result = Solver._result
+
+    def prepare(self, inst: AssignmentInstance, eps: float, storage: str = "auto", on_the_fly: bool = False):
+        from . import _native as N
+        p = self._problem(inst, eps, storage)
+        if on_the_fly:
+            p.flags |= N.FLAG_ON_THE_FLY
+        r = N.Result()
+        st = self._L.otprg_prepare(self._ctx, C.byref(p), C.byref(r))
+        if st:
+            self._raise(st)
+        self._shape = (inst.n_a, inst.n_b, eps)
+
+    def solve_prepared(self):
+        n_a, n_b, eps = self._shape
+        r, bufs = self._result(n_a, n_b, eps)
+        st = self._L.otprg_solve_prepared(self._ctx, C.byref(r))
+        if st:
+            self._raise(st)
+        return Solver._pack(r, bufs)
+
+    def solve(self, inst: AssignmentInstance, opt: AssignmentOptions, on_the_fly: bool = False):
+        self.prepare(inst, opt.eps, opt.storage, on_the_fly)
+        return self.solve_prepared()
+
+    def close(self):
+        if self._ctx:
+            self._L.otprg_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

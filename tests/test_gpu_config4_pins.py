@@ -54,10 +54,11 @@ def test_fused_20k(pins20k, key, storage):
 
 @pytest.mark.parametrize("key", KEYS)
 @pytest.mark.parametrize("G,K", [(1, 16), (2, 16), (4, 1), (8, 16), (8, 1), (3, 4)])
-def test_sharded_20k(pins20k, key, G, K):
+@pytest.mark.parametrize("resident", [True, False])
+def test_sharded_20k(pins20k, key, G, K, resident):
     v = pins20k[key]
     m, s = sharded.solve_assignment_sharded(otprg.gen_uniform_square(v["n_a"], v["seed"]),
-                                            otprg.AssignmentOptions(eps=v["eps"]), G, K=K)
+                                            otprg.AssignmentOptions(eps=v["eps"]), G, K=K, resident=resident)
     _check(pins20k, key, m, s)
 
 
@@ -112,7 +113,7 @@ def test_100k_feasibility_and_bounds():
     assert m.size() == n and s.phases > 0
     # the sharded and on-the-fly results, checked against the fused context's kT
     for G, otf in ((8, False), (1, True)):
-        sv2 = sharded.ShardedSolver(inst, opt, G, K=16, on_the_fly=otf)
+        sv2 = sharded.ShardedSolver(inst, opt, G, K=16, on_the_fly=otf, resident=False)
         try:
             m2, s2, pre = sv2.solve(keep_state=True)
         finally:
