@@ -104,15 +104,21 @@ __global__ void round_points_div_kernel(const double2* __restrict__ pa,
 
 // K2 on the exact threshold table (otprg_points_threshold_table):
 // k(a,b) = max{j : thr[j] <= d2} with d2 = dx*dx + dy*dy in IEEE RN (the
-// reference's bits up to the sqrt), so no FP64 sqrt or division.  The float
-// estimate e = floor(sqrt(d2 / 2) / eps) (approximate sqrt, relative error
-// ~2^-21, so |e - x| < 0.004 for the real x = sqrt(d2/2)/eps <= 8190) and the
-// exact k = scaled_floor(c, eps) both lie in {floor(x) - 1, floor(x),
-// floor(x) + 1} and cannot sit on opposite ends of it, so |e - k| <= 1: one
-// upward and one downward exact comparison against the table (shared
-// memory) settle k.  Every thread owns 16 B of a kT row (kV consecutive demand
-// points, held in registers) and walks a strided set of supply rows, storing
-// one 16-byte vector per row: the build is bound by its HBM writes.
+// reference's bits up to the sqrt), so no FP64 sqrt or division.
+//
+// The float estimate x_f = sqrt(d2) / (sqrt(2) eps) (approximate sqrt) is
+// within B = x_max * 2^-21 of the real x = c / eps (x <= x_max = 1/eps + 1).
+// When x_f is at least `margin` (= 4 B) away from every integer, x is too,
+// and then scaled_floor(c, eps) = floor(x) exactly (its division and repair
+// steps move k only when x lies within a few ulps of an integer) — no table
+// access at all.  Only the lanes near a level boundary (a fraction ~2 margin of
+// the elements: < 0.1 % at eps = 0.01) settle k exactly against the table in
+// shared memory: with e = floor(x_f), |e - k| <= 1, so one upward and one
+// downward comparison suffice.  (A table lookup for every element made the
+// kernel shared-memory bound: 5 wavefronts per random 8-byte lookup.)
+// Every thread owns 16 B of a kT row (kV consecutive demand points, held in
+// registers) and walks a strided set of supply rows, storing one 16-byte
+// vector per row: the build is bound by its FP64 work and its HBM writes.
 constexpr int kThrSmemMax = 8192;
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
@@ -123,8 +129,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __restrict__ pa,
                                                                const double2* __restrict__ pb,
                                                                int n_ai, int n_bi, const double* __restrict__ thr,
-                                                               int thr_n, float inv_step, T* __restrict__ kT,
-                                                               int lda) {
+                                                               int thr_n, float inv_step, float margin,
+                                                               T* __restrict__ kT, int lda) {
   constexpr int kV = 16 / sizeof(T), kPer = 4 / sizeof(T);  // entries per 16 B / per 32-bit word
   extern __shared__ double s_thr[];
   for (int j = threadIdx.x; j < thr_n; j += blockDim.x) s_thr[j] = thr[j];
@@ -142,9 +148,13 @@ __global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __
     for (int j = 0; j < kV; ++j) {
       const double dx = __dsub_rn(p[j].x, q.x), dy = __dsub_rn(p[j].y, q.y);
       const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-      int k = min(uf, (int)(sqrt_approx(__double2float_rn(d2)) * inv_step));
-      k += s_thr[k + 1] <= d2;
-      k -= s_thr[k] > d2;
+      const float xf = sqrt_approx(__double2float_rn(d2)) * inv_step;
+      int k = min(uf, (int)xf);
+      const float fr = xf - (float)k;
+      if (!(fr >= margin && fr <= 1.0f - margin) || k == uf) {  // near a level boundary: exact
+        k += s_thr[k + 1] <= d2;
+        k -= s_thr[k] > d2;
+      }
       const uint32_t v = a0 + j < n_ai ? (uint32_t)k : type_max<T>();
       w[j / kPer] |= v << (8 * sizeof(T) * (j % kPer));
     }
@@ -328,12 +338,14 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
     const int bx = (threads_x + 255) / 256;
     const int by = std::max(1, std::min(n_bi, (148 * 8 + bx - 1) / bx * 4));
     const float inv_step = (float)(1.0 / (std::sqrt(2.0) * eps));
+    // 4 x the float estimate's error bound (x <= 1/eps + 1, relative 2^-21)
+    const float margin = (float)((1.0 / eps + 1.0) * std::ldexp(1.0, -19) + 1e-6);
     const size_t smem = (size_t)thr_n * sizeof(double);
     with_width(width, [&](auto tag) {
       using T = decltype(tag);
       auto fn = round_points_thr_kernel<T>;
       if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fn<<<dim3(bx, std::min(by, 65535)), 256, smem, s>>>(a2, b2, n_ai, n_bi, thr, thr_n, inv_step,
+      fn<<<dim3(bx, std::min(by, 65535)), 256, smem, s>>>(a2, b2, n_ai, n_bi, thr, thr_n, inv_step, margin,
                                                            static_cast<T*>(kT), lda);
       return 0;
     });

@@ -404,7 +404,7 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
   const int ia = ctx->ia, ib = ctx->ib;
   cudaStream_t s = ctx->stream;
   // One batch of async copies into pinned staging, one sync.
-  const size_t o_ma = 256, o_mb = o_ma + ia * 4ull, o_yb = o_mb + ib * 4ull,
+  const size_t o_ma = (sizeof(Ctl) + 255) / 256 * 256, o_mb = o_ma + ia * 4ull, o_yb = o_mb + ib * 4ull,
                o_t = o_yb + ib * 4ull, o_fc = (o_t + static_cast<size_t>(ia) * ctx->width + 7) & ~7ull;
   const int64_t fc_first = std::min<int64_t>(
       std::min<int64_t>(ctx->fc_cap, r->free_counts ? r->free_cap : 0), 65536);

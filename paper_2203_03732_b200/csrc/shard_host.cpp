@@ -382,7 +382,17 @@ int run_plan(otprg_ctx* ctx, ResPlan& P, otprg_result* res) {
       CK(cudaMemcpy(&h, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost), "D2H ctl");
       if ((st = check_status(c, h, true))) return fail(ctx, st, "shard " + std::to_string(c->sh_shard) + ": " + c->err);
       if (h.phase != h0.phase || h.sum_ni != h0.sum_ni || h.sh_rounds != h0.sh_rounds || h.done != h0.done)
-        return fail(ctx, OTPRG_INVARIANT, "shards ended in different states");
+        return fail(ctx, OTPRG_INVARIANT,
+                    "shards ended in different states: shard " + std::to_string(c->sh_shard) + " [phase,sum_ni,rounds,done]=" +
+                        std::to_string(h.phase) + "," + std::to_string(h.sum_ni) + "," + std::to_string(h.sh_rounds) + "," +
+                        std::to_string(h.done) + " vs " + std::to_string(h0.phase) + "," + std::to_string(h0.sum_ni) + "," +
+                        std::to_string(h0.sh_rounds) + "," + std::to_string(h0.done) + " [mode,nreq,epoch,live,park,w1,st]=" +
+                        std::to_string(h.sh_mode) + "," + std::to_string(h.sh_nreq) + "," + std::to_string(h.sh_epoch) + "," +
+                        std::to_string(h.sh_live) + "," + std::to_string(h.sh_park_cur) + "," + std::to_string(h.work[1]) + "," +
+                        std::to_string(h.status) + " vs " +
+                        std::to_string(h0.sh_mode) + "," + std::to_string(h0.sh_nreq) + "," + std::to_string(h0.sh_epoch) + "," +
+                        std::to_string(h0.sh_live) + "," + std::to_string(h0.sh_park_cur) + "," + std::to_string(h0.work[1]) + "," +
+                        std::to_string(h0.status) + " sizeof(Ctl)=" + std::to_string(sizeof(Ctl)));
       c->sh_epoch = h.sh_epoch;
     }
   }
@@ -750,6 +760,7 @@ int otprg_selftest_exchange(int32_t device, int32_t n_groups, int32_t shards_per
                  cudaMemcpyHostToDevice);
       Ctl h{};
       h.sh_nreq = nreq;
+      h.sh_live = 1;
       h.sh_epoch = static_cast<uint32_t>(r);
       cudaMemcpy(ctls[q].p, &h, sizeof(h), cudaMemcpyHostToDevice);
       S[q].ctl = ctls[q].as<Ctl>();

@@ -134,6 +134,41 @@ def test_rounding_dense_and_points_match_oracle(oracle, eps):
     np.testing.assert_array_equal(otprg.scale_round_costs(inst_p, eps).k, want)
 
 
+@pytest.mark.parametrize("eps", [0.01, 0.1, 1.0 / 300.0, 0.125, 0.003, 1.0 / 8000.0, 0.07])
+def test_points_rounding_at_level_boundaries(oracle, eps):
+    """K2 decides most entries from a float estimate and consults the exact
+    threshold table only near a level boundary: points placed a few ulps on
+    either side of every level's threshold distance (and random ones) must
+    round exactly like the reference's scale_round_costs of the dense cost."""
+    from paper_2203_03732_b200 import _native as N
+    import ctypes as C
+    n = N.lib().otprg_points_threshold_table(eps, None, 0)
+    thr = np.zeros(n)
+    N.lib().otprg_points_threshold_table(eps, thr.ctypes.data, n)
+    rng = np.random.default_rng(int(1 / eps))
+    levels = np.arange(1, n - 1)
+    if len(levels) > 600:
+        levels = np.sort(rng.choice(levels, 600, replace=False))
+    pts = []
+    for j in levels:
+        r0 = np.sqrt(thr[j])
+        for d in range(-3, 4):
+            r = r0
+            for _ in range(abs(d)):
+                r = np.nextafter(r, np.inf if d > 0 else -np.inf)
+            th = rng.random() * np.pi / 2
+            pts.append((r, 0.0))
+            pts.append((r * np.cos(th), r * np.sin(th)))
+    pts = np.clip(np.array(pts), 0.0, 1.0)
+    pb = np.concatenate([pts, rng.random((500, 2))])
+    pa = np.array([[0.0, 0.0], [1.0, 1.0], [0.25, 0.75]])
+    for A, B in ((pa, pb), (pb, pa)):
+        inst = otprg.AssignmentInstance(len(A), len(B), pts_a=A, pts_b=B)
+        got = otprg.scale_round_costs(inst, eps).k
+        want = oracle.scale_round_costs(otprg.points_cost(A, B), eps)[0]
+        assert np.array_equal(got, want), int((got != want).sum())
+
+
 def test_rounding_unbalanced_both_orientations(oracle):
     for n_a, n_b in ((37, 301), (301, 37)):
         cost = random_instance(n_a, n_b, 99)
