@@ -402,17 +402,21 @@ def e2e_points(otprg, local, args) -> dict:
 def run_sharded(args, world, rank, local, steps: int, warmup: int, on_the_fly: bool = False) -> dict:
     """Config 4: n=100k points, eps=0.01, A rows sharded across the ranks
     (SURVEY §8(e)); one step = one full sharded solve with every rank's slab
-    resident (20 GB / N of uint16 kT: far larger than L2), or with
+    resident (100k x 100k / N of kT, far larger than L2), or with
     ``on_the_fly`` no slab at all (the scans round the point costs through the
-    exact threshold table).  Timed with CUDA events on each rank's
-    solver stream, max over ranks."""
+    exact threshold table).  The solve is the device-resident loop
+    (one CUDA graph per GPU, candidate slots pushed over NVLink peer memory
+    through CUDA IPC mappings; one host sync per solve); with
+    OTPRG_BENCH_SHARE_GPU the host-driven protocol (gloo).  Timed with CUDA
+    events on each rank's solver stream, max over ranks."""
     import paper_2203_03732_b200 as otprg
     from paper_2203_03732_b200.sharded import ShardedSolver
 
     inst = otprg.gen_uniform_square(N4, 1)
-    opt = otprg.AssignmentOptions(eps=EPS, storage=args.storage, device=local)
+    opt = otprg.AssignmentOptions(eps=EPS, storage=args.storage4, device=local)
     t0 = time.perf_counter()
-    sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1, on_the_fly=on_the_fly)
+    sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1, on_the_fly=on_the_fly,
+                       resident=False if share_gpu() and world > 1 else None)
     barrier(world)
     prep_s = allreduce_max(time.perf_counter() - t0, world)
     m, s = sv.solve()
@@ -428,30 +432,53 @@ def run_sharded(args, world, rank, local, steps: int, warmup: int, on_the_fly: b
     barrier(world)
     ms = allreduce_max(float(np.mean(times)), world)
     P, R = int(s.phases), int(s.device["refill_rounds"])
+    width = {"u8": 1, "u16": 2, "u32": 4}.get(args.storage4, 2)
+    lo, hi = int(sv.ranks[0].bounds[rank]), int(sv.ranks[0].bounds[rank + 1])
+    launches = int(s.device.get("gpu_launches") or 0) or (6 + 6 * (P + R))
     out = {
         "value": round(ms, 3), "unit": "ms", "n_gpus": world, "steps": steps, "warmup": warmup,
         "phases": P, "sum_ni": int(s.sum_ni), "refill_rounds": R, "K": args.K,
+        "driver": "resident CUDA-graph loop (WHILE node), 1 host sync per solve" if sv.resident
+                  else "host-driven rounds (1 host sync per round)",
         "costs": "on the fly from the points (threshold table, no kT slab)" if on_the_fly
-                 else "precomputed uint16 kT slab",
+                 else f"precomputed {ctype(width)} kT slab",
         "slab_build_ms": round(float(s.device["build_ms"]), 3),
         "prepare_wall_s": round(prep_s, 3),
-        # init + first top (top, 2 compaction passes) + per DA round (scan, DA, top,
-        # 2 compaction passes) + completion
-        "gpu_launches_per_step": 5 + 5 * (P + R),
+        "gpu_launches_per_step": launches,
         "clocks": clk.summary(),
     }
+    if not on_the_fly:
+        # B_alg = sum_i n_i * n_a * w over all ranks; this rank's share
+        # is sum_i n_i * (its slab width) * w.  Scans stop at the K-th candidate, so
+        # the bytes actually read are fewer (latency-bound rounds).
+        b_all = int(s.sum_ni) * N4 * width
+        peak, peak_kind = peaks()
+        ach = b_all / (ms * 1e-3) / 1e9
+        out["roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "peak_kind": peak_kind,
+                           "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                           "algorithmic_bytes_total": b_all,
+                           "algorithmic_bytes_per_rank": int(s.sum_ni) * (hi - lo) * width,
+                           "note": "whole solve (all rounds) on the max-over-ranks device time"}
     sv.close()
     if rank == 0 and not args.no_parity:
         # bit-identity against the single-GPU fused solver (no CPU oracle
         # finishes n=100k in bench time); outside the timed region
-        ref_m, ref_s = otprg.Solver(local).solve(inst, opt)
+        fsv = otprg.Solver(local)
+        fsv.prepare(inst, EPS, args.storage4)
+        ref_m, ref_s = fsv.solve_prepared()
+        ft = []
+        for _ in range(3):
+            fsv.timer_start()
+            fsv.solve_prepared()
+            ft.append(fsv.timer_stop())
+        fsv.close()
         out["bit_identical_to_single_gpu_solver"] = bool(
             np.array_equal(ref_m.match_of_a, m.match_of_a)
             and np.array_equal(ref_s.duals_final.y_a, s.duals_final.y_a)
             and np.array_equal(ref_s.duals_final.y_b, s.duals_final.y_b)
             and np.array_equal(ref_s.free_counts, s.free_counts)
             and ref_s.device["cost"] == s.device["cost"])
-        out["single_gpu_fused_solver_ms"] = round(float(ref_s.device["solve_ms"]), 3)
+        out["single_gpu_fused_solver_ms"] = round(float(np.median(ft)), 3)
     return out
 
 
@@ -461,44 +488,53 @@ def run_config4(args, world, rank, local) -> None:
         r_otf = run_sharded(args, world, rank, local, min(args.steps, 3), min(args.warmup, 3), on_the_fly=True)
     except Exception as e:  # noqa: BLE001
         r_otf = {"error": f"{type(e).__name__}: {e}"[:300]}
-    # e2e: host point sets in, slab build + solve + results out, every step
+    # e2e: host point sets in; H2D, slab build, resident-loop setup, solve and
+    # the results back in the host, every step (wall clock between barriers,
+    # max over ranks)
     import paper_2203_03732_b200 as otprg
     from paper_2203_03732_b200.sharded import ShardedSolver
+    import torch
     inst = otprg.gen_uniform_square(N4, 1)
-    opt = otprg.AssignmentOptions(eps=EPS, storage=args.storage, device=local)
+    opt = otprg.AssignmentOptions(eps=EPS, storage=args.storage4, device=local)
     e2e = []
     for _ in range(max(1, min(args.steps, 3))):
         barrier(world)
-        import torch
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1)
+        sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1,
+                           resident=False if share_gpu() and world > 1 else None)
         sv.solve()
         torch.cuda.synchronize()
         e2e.append(allreduce_max(time.perf_counter() - t0, world) * 1e3)
         sv.close()
+    width = {"u8": 1, "u16": 2, "u32": 4}.get(args.storage4, 2)
     line = {
         "metric": METRIC, "value": r["value"], "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["value"],
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u16" if args.storage != "u8" else "u8", "data": "synthetic",
+        "dtype": dtype_of(width), "data": "synthetic",
         "config": {"workload": f"config 4: gen_uniform_square(n={N4}, seed 1) points, eps={EPS}, "
-                               f"A rows sharded across {world} GPU(s), per-rank uint16 kT slab "
+                               f"A rows sharded across {world} GPU(s), per-rank {ctype(width)} kT slab "
                                "built on the device from the points and resident",
-                   "l2": f"inputs larger than L2 ({N4 * N4 * 2 // world // 10**9} GB of kT per rank)",
-                   "parallelism": f"A-row shards x{world}, candidate all-gather per phase (NCCL)",
+                   "l2": f"inputs larger than L2 ({N4 * N4 * width // world // 10**9} GB of kT per rank)",
+                   "parallelism": f"A-row shards x{world}, " + (
+                       "candidate slots pushed over NVLink peer memory (CUDA IPC) inside the resident loop"
+                       if not share_gpu() else "host-driven gloo all-gather (all ranks share one GPU: "
+                                               "functional check, not a scaling point)"),
                    "K": args.K},
         "sharded": r,
         "on_the_fly": r_otf,
+        "roofline": r.get("roofline"),
         "scaling_series": "config 4 (n=100k, eps=0.01) strong scaling: this line is its N-GPU point; the "
                           "N=1 point is the N=1 line's config4_1gpu (that line's headline value is "
                           "config 2, the metric's n=10k workload)",
         "gpu_launches": r["gpu_launches_per_step"] * args.steps,
         "clocks": r["clocks"],
+        "bit_identical": r.get("bit_identical_to_single_gpu_solver"),
         "e2e": {"value": round(float(np.mean(e2e)), 3), "unit": "ms",
                 "h2d_bytes_per_step": N4 * 2 * 16,
                 "d2h_bytes_per_step": N4 * (4 + 4 + 8 + 8) + 8 * r["phases"],
-                "input": "2-D point sets in host memory; slab build, solve, D2H of matching/duals",
+                "input": "2-D point sets in host memory; slab build, loop setup, solve, D2H of matching/duals",
                 "timer": "wall clock between synchronised barriers, max over ranks"},
     }
     if rank == 0:
@@ -506,6 +542,11 @@ def run_config4(args, world, rank, local) -> None:
 
 
 def run_reference(args, world, rank) -> None:
+    """The reference's own CPU solver (oracle/_ref, threads = all host cores:
+    its parallel mode) on this arm's workload.  N = 1: config 2.  N > 1 (our
+    line is config 4, n = 100k, which the reference cannot hold: ~120 GB of
+    dense f64 + int32 matrices): the bounded sample is the same generator and
+    eps at n = 20,000, the largest size it runs here (~4.8 GB)."""
     if rank != 0:
         return
     from oracle.pyoracle import Reference
@@ -514,29 +555,32 @@ def run_reference(args, world, rank) -> None:
         return
     ref = Reference.get()
     threads = os.cpu_count() or 1
+    n = N if world == 1 else 20_000
     budget_s, t_start = 240.0, time.time()
     for w in range(args.warmup):
-        if time.time() - t_start > budget_s / 4:
+        if time.time() - t_start > budget_s / 4 or world > 1:
             break
-        ref.solve_uniform_square(N, SEEDS[w % 3], EPS, threads=threads)
+        ref.solve_uniform_square(n, SEEDS[w % 3], EPS, threads=threads)
     times, phases = [], []
     for k in range(args.steps):
-        r = ref.solve_uniform_square(N, SEEDS[k % 3], EPS, threads=threads)
+        r = ref.solve_uniform_square(n, SEEDS[k % 3] if world == 1 else 1, EPS, threads=threads)
         times.append(r.solve_ms)
         phases.append(r.phases)
         if time.time() - t_start > budget_s:
             break
     ms = float(np.mean(times))
-    sample = (f"full solves of gen_uniform_square({N}, seeds 1/2/3 rotating), eps={EPS}, "
-              f"threads={threads} (reference parallel mode, non-deterministic), steady_clock "
+    sample = (f"full solves of gen_uniform_square({n}, " + ("seeds 1/2/3 rotating" if world == 1 else "seed 1")
+              + f"), eps={EPS}, threads={threads} (reference parallel mode, non-deterministic), steady_clock "
               "around otpr::solve_assignment incl. its rounding")
+    workload = (f"config 2: gen_uniform_square(n={N}), eps={EPS}" if world == 1 else
+                f"config 4 sample: gen_uniform_square(n=20000), eps={EPS} (n=100k does not fit the "
+                "reference's dense host matrices)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms",
         "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic",
-        "config": {"workload": f"config 2: gen_uniform_square(n={N}), eps={EPS}",
-                   "parallelism": f"CPU threads={threads}"},
+        "higher_is_better": False, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic",
+        "config": {"workload": workload, "parallelism": f"CPU threads={threads}"},
         "phases": phases,
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": threads,
                          "kind": "reference", "sample": sample},
@@ -558,6 +602,8 @@ def main() -> None:
     ap.add_argument("--workload", default="auto", choices=["auto", "config2", "config4"],
                     help="auto: config 2 on one GPU, config 4 (sharded n=100k) on N>1")
     ap.add_argument("--K", type=int, default=16, help="candidates per shard per scan (config 4)")
+    ap.add_argument("--storage4", default="u8", choices=["u8", "u16"],
+                    help="kT storage of the config-4 slabs (eps = 0.01 fits uint8)")
     ap.add_argument("--no-config4", action="store_true",
                     help="skip the 1-GPU config-4 point in the config-2 line")
     args = ap.parse_args()
