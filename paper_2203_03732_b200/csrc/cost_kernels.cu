@@ -103,22 +103,23 @@ __global__ void round_points_div_kernel(const double2* __restrict__ pa,
 }
 
 // K2 on the exact threshold table (otprg_points_threshold_table):
-// k(a,b) = max{j : thr[j] <= d2} with d2 = dx*dx + dy*dy in IEEE RN (the
-// reference's bits up to the sqrt), so no FP64 sqrt or division.
+// k(a,b) = scaled_floor(sqrt(d2) / sqrt(2), eps) = max{j : thr[j] <= d2} with
+// d2 = dx*dx + dy*dy in IEEE RN (the reference's bits up to the sqrt).
 //
-// The float estimate x_f = sqrt(d2) / (sqrt(2) eps) (approximate sqrt) is
-// within B = x_max * 2^-21 of the real x = c / eps (x <= x_max = 1/eps + 1).
-// When x_f is at least `margin` (= 4 B) away from every integer, x is too,
-// and then scaled_floor(c, eps) = floor(x) exactly (its division and repair
-// steps move k only when x lies within a few ulps of an integer) — no table
-// access at all.  Only the lanes near a level boundary (a fraction ~2 margin of
-// the elements: < 0.1 % at eps = 0.01) settle k exactly against the table in
-// shared memory: with e = floor(x_f), |e - k| <= 1, so one upward and one
-// downward comparison suffice.  (A table lookup for every element made the
-// kernel shared-memory bound: 5 wavefronts per random 8-byte lookup.)
-// Every thread owns 16 B of a kT row (kV consecutive demand points, held in
-// registers) and walks a strided set of supply rows, storing one 16-byte
-// vector per row: the build is bound by its FP64 work and its HBM writes.
+// Fast path, FP32 only: x_f = sqrt(dx_f^2 + dy_f^2) / (sqrt(2) eps) from
+// float copies of the coordinates is within B of the real x = c / eps, B
+// bounded on the host from the coordinates' magnitude and eps (`margin`).
+// When floor(x_f - margin) == floor(x_f + margin), x is at least margin -
+// B > 0 away from every integer, and then scaled_floor(c, eps) = floor(x)
+// exactly (its division and repair steps move k only when x lies within a
+// few ulps of an integer).  Lanes near a level boundary (a fraction ~2 margin
+// of the elements: ~0.05 % at eps = 0.01 on the unit square) compute the
+// exact FP64 d2 and walk the table in shared memory from floor(x_f - margin)
+// - 1 <= k upwards.  No FP64 sqrt or division anywhere, FP64 work only on
+// the rare slow lanes; the fast path is ~12 FP32/INT/MUFU instructions per
+// entry.  Every thread owns 16 B of a kT row (kV consecutive demand points,
+// float copies in registers) and walks a strided set of supply rows, storing
+// one 16-byte vector per row: the build is bound by issue and HBM writes.
 constexpr int kThrSmemMax = 8192;
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
@@ -138,27 +139,37 @@ __global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __
   const int uf = thr_n - 2;  // unit_floor: thr[uf + 1] = +inf
   const int a0 = (blockIdx.x * blockDim.x + threadIdx.x) * kV;
   if (a0 >= lda) return;
-  double2 p[kV];
+  float2 pf[kV];
 #pragma unroll
-  for (int j = 0; j < kV; ++j) p[j] = a0 + j < n_ai ? pa[a0 + j] : make_double2(0.0, 0.0);
+  for (int j = 0; j < kV; ++j) {
+    const double2 p = a0 + j < n_ai ? pa[a0 + j] : make_double2(0.0, 0.0);
+    pf[j] = make_float2(__double2float_rn(p.x), __double2float_rn(p.y));
+  }
+  // pad entries (a >= n_ai) hold the type maximum
+  uint32_t padw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < kV; ++j)
+    if (a0 + j >= n_ai) padw[j / kPer] |= type_max<T>() << (8 * sizeof(T) * (j % kPer));
   for (int b = blockIdx.y; b < n_bi; b += gridDim.y) {
     const double2 q = pb[b];
+    const float qx = __double2float_rn(q.x), qy = __double2float_rn(q.y);
     uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
-      const double dx = __dsub_rn(p[j].x, q.x), dy = __dsub_rn(p[j].y, q.y);
-      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-      const float xf = sqrt_approx(__double2float_rn(d2)) * inv_step;
-      int k = min(uf, (int)xf);
-      const float fr = xf - (float)k;
-      if (!(fr >= margin && fr <= 1.0f - margin) || k == uf) {  // near a level boundary: exact
-        k += s_thr[k + 1] <= d2;
-        k -= s_thr[k] > d2;
+      const float dx = pf[j].x - qx, dy = pf[j].y - qy;
+      const float xf = sqrt_approx(fmaf(dy, dy, dx * dx)) * inv_step;
+      int k = (int)(xf - margin);
+      if (k != (int)(xf + margin)) {  // near a level boundary: the exact FP64 d2 and the table
+        const double2 p = pa[min(a0 + j, n_ai - 1)];
+        const double ex = __dsub_rn(p.x, q.x), ey = __dsub_rn(p.y, q.y);
+        const double d2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+        k = max(0, min(k - 1, uf));
+        while (k < uf && s_thr[k + 1] <= d2) ++k;
       }
-      const uint32_t v = a0 + j < n_ai ? (uint32_t)k : type_max<T>();
-      w[j / kPer] |= v << (8 * sizeof(T) * (j % kPer));
+      w[j / kPer] |= (uint32_t)k << (8 * sizeof(T) * (j % kPer));
     }
-    *reinterpret_cast<uint4*>(kT + (size_t)b * lda + a0) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(kT + (size_t)b * lda + a0) =
+        make_uint4(w[0] | padw[0], w[1] | padw[1], w[2] | padw[2], w[3] | padw[3]);
   }
 }
 
@@ -327,8 +338,8 @@ cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swappe
 }
 
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
-                                  double eps, double sqrt2, const double* thr, int thr_n, void* kT,
-                                  int lda, int width, cudaStream_t s) {
+                                  double eps, double sqrt2, const double* thr, int thr_n, double absmax,
+                                  void* kT, int lda, int width, cudaStream_t s) {
   const double2* a2 = reinterpret_cast<const double2*>(pa);
   const double2* b2 = reinterpret_cast<const double2*>(pb);
   if (thr && thr_n >= 2 && thr_n <= kThrSmemMax) {
@@ -338,8 +349,14 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
     const int bx = (threads_x + 255) / 256;
     const int by = std::max(1, std::min(n_bi, (148 * 8 + bx - 1) / bx * 4));
     const float inv_step = (float)(1.0 / (std::sqrt(2.0) * eps));
-    // 4 x the float estimate's error bound (x <= 1/eps + 1, relative 2^-21)
-    const float margin = (float)((1.0 / eps + 1.0) * std::ldexp(1.0, -19) + 1e-6);
+    // Bound on |x_f - x| (x = c / eps <= 1/eps + 1): float coordinates are off
+    // by <= C 2^-24 each (C = max |coordinate|), so dx_f, dy_f by <= 3 C 2^-24
+    // and d_f by <= 4.3 C 2^-24 + |d| 2^-22; x_f adds ~3 roundings (2^-22
+    // relative, the approximate sqrt included).  margin = 4 x that bound.
+    const double xmax = 1.0 / eps + 1.0;
+    const double bound = (4.3 * absmax * std::ldexp(1.0, -24) + std::sqrt(2.0) * std::ldexp(1.0, -22)) /
+                             (std::sqrt(2.0) * eps) + xmax * std::ldexp(1.0, -21);
+    const float margin = (float)std::min(0.5, 4.0 * bound + 1e-7);
     const size_t smem = (size_t)thr_n * sizeof(double);
     with_width(width, [&](auto tag) {
       using T = decltype(tag);

@@ -90,6 +90,7 @@ struct otprg_ctx {
   std::vector<double> thr_host;
   double thr_eps = -1.0;
   int thr_n = 0;
+  double pts_absmax = 1.0;  // largest |coordinate| of the prepared point sets (K2's error bound)
   void* hpin = nullptr;  // pinned D2H staging
   size_t hpin_n = 0;
   cudaEvent_t timer[2] = {};

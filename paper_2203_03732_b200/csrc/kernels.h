@@ -53,9 +53,11 @@ struct SolveArgs {
 // width = sizeof(T) of kT (1 or 2).
 cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swapped, double eps,
                                void* kT, int lda, int width, int* status, cudaStream_t s);
+// thr: exact threshold table (thr_n entries, <= 8192) or nullptr (exact
+// division form); absmax: the largest |coordinate| of either point set.
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
-                                  double eps, double sqrt2, const double* thr, int thr_n, void* kT,
-                                  int lda, int width, cudaStream_t s);
+                                  double eps, double sqrt2, const double* thr, int thr_n, double absmax,
+                                  void* kT, int lda, int width, cudaStream_t s);
 // First (a, b) (row-major, original orientation) whose point cost is outside
 // [0, 1]: atomicMin into *first (initialise to ~0).
 cudaError_t launch_points_range(const double* pa, const double* pb, int n_a, int n_b, double d2_max,

@@ -108,6 +108,7 @@ int check_points_range(otprg_ctx* ctx, const otprg_problem* p, const double* dpa
       hi[i & 1] = std::max(hi[i & 1], x);
     }
   }
+  ctx->pts_absmax = std::max(std::max(std::fabs(lo[0]), std::fabs(hi[0])), std::max(std::fabs(lo[1]), std::fabs(hi[1])));
   if (!nan) {
     const double dx = hi[0] - lo[0], dy = hi[1] - lo[1];
     if (dx * dx + dy * dy <= points_d2_max()) return OTPRG_OK;
@@ -251,7 +252,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
     int thr_n = 0;
     if ((st = points_table(ctx, p->eps, &thr_n))) return st;
     CK(otprg::launch_round_points2d(dpa, dpb, ctx->ia, ctx->ib, p->eps, std::sqrt(2.0),
-                                    thr_n ? ctx->thr_dev.as<double>() : nullptr, thr_n, ctx->kT.p,
+                                    thr_n ? ctx->thr_dev.as<double>() : nullptr, thr_n, ctx->pts_absmax, ctx->kT.p,
                                     ctx->lda, width, ctx->stream),
        "round_points launch");
     ctx->build_launches = 1;

@@ -516,7 +516,7 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   } else if (ctx->sh_hi > ctx->sh_lo) {
     CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb, ctx->sh_hi - ctx->sh_lo,
                                     ctx->ib, p->eps, std::sqrt(2.0), thr_n ? ctx->thr_dev.as<double>() : nullptr,
-                                    thr_n, ctx->kT.p, ctx->lda, width, ctx->stream),
+                                    thr_n, ctx->pts_absmax, ctx->kT.p, ctx->lda, width, ctx->stream),
        "round_points launch");
   }
   CK(cudaEventRecord(ctx->ev[5], ctx->stream), "event");

@@ -162,7 +162,9 @@ def test_points_rounding_at_level_boundaries(oracle, eps):
     pts = np.clip(np.array(pts), 0.0, 1.0)
     pb = np.concatenate([pts, rng.random((500, 2))])
     pa = np.array([[0.0, 0.0], [1.0, 1.0], [0.25, 0.75]])
-    for A, B in ((pa, pb), (pb, pa)):
+    # shifted copies: float coordinates lose precision far from the origin (wider margin)
+    shift = 777.0
+    for A, B in ((pa, pb), (pb, pa), (pa + shift, pb + shift)):
         inst = otprg.AssignmentInstance(len(A), len(B), pts_a=A, pts_b=B)
         got = otprg.scale_round_costs(inst, eps).k
         want = oracle.scale_round_costs(otprg.points_cost(A, B), eps)[0]
