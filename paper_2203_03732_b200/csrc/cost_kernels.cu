@@ -109,13 +109,13 @@ __global__ void round_points_div_kernel(const double2* __restrict__ pa,
 // Fast path, FP32 only: x_f = sqrt(dx_f^2 + dy_f^2) / (sqrt(2) eps) from
 // float copies of the coordinates is within B of the real x = c / eps, B
 // bounded on the host from the coordinates' magnitude and eps (`margin`).
-// When floor(x_f - margin) == floor(x_f + margin), x is at least margin -
-// B > 0 away from every integer, and then scaled_floor(c, eps) = floor(x)
-// exactly (its division and repair steps move k only when x lies within a
-// few ulps of an integer).  Lanes near a level boundary (a fraction ~2 margin
-// of the elements: ~0.05 % at eps = 0.01 on the unit square) compute the
-// exact FP64 d2 and walk the table in shared memory from floor(x_f - margin)
-// - 1 <= k upwards.  No FP64 sqrt or division anywhere, FP64 work only on
+// When x_f is more than margin (= 4 B) from its nearest integer, x is more
+// than 3 B away from every integer, and then scaled_floor(c, eps) = floor(x)
+// = floor(x_f) exactly (its division and repair steps move k only when x
+// lies within a few ulps of an integer).  Lanes near a level boundary (a
+// fraction ~2 margin of the elements: ~0.05 % at eps = 0.01 on the unit
+// square) compute the exact FP64 d2 and walk the table in shared memory from
+// floor(x_f) - 2 (<= k) upwards.  No FP64 sqrt or division anywhere, FP64 work only on
 // the rare slow lanes; the fast path is ~12 FP32/INT/MUFU instructions per
 // entry.  Every thread owns 16 B of a kT row (kV consecutive demand points,
 // float copies in registers) and walks a strided set of supply rows, storing
@@ -132,44 +132,89 @@ __global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __
                                                                int n_ai, int n_bi, const double* __restrict__ thr,
                                                                int thr_n, float inv_step, float margin,
                                                                T* __restrict__ kT, int lda) {
-  constexpr int kV = 16 / sizeof(T), kPer = 4 / sizeof(T);  // entries per 16 B / per 32-bit word
-  extern __shared__ double s_thr[];
+  // entries per thread (one 8-byte store for u8, 16-byte for u16 / u32), per 32-bit word
+  constexpr int kV = sizeof(T) == 1 ? 8 : 16 / sizeof(T), kPer = 4 / sizeof(T), kW = kV / kPer;
+  // shared: this block's demand points in double (the slow path's exact d2
+  // reads them here instead of from L2), then the threshold table
+  extern __shared__ __align__(16) double s_dyn_k2[];
+  double2* s_pts = reinterpret_cast<double2*>(s_dyn_k2);
+  double* s_thr = s_dyn_k2 + 2 * kV * blockDim.x;
   for (int j = threadIdx.x; j < thr_n; j += blockDim.x) s_thr[j] = thr[j];
-  __syncthreads();
   const int uf = thr_n - 2;  // unit_floor: thr[uf + 1] = +inf
+  const float lim = 0.5f - margin;  // |z - rint(z)| >= lim: within margin of a level boundary
   const int a0 = (blockIdx.x * blockDim.x + threadIdx.x) * kV;
-  if (a0 >= lda) return;
   float2 pf[kV];
+  double2* my = s_pts + threadIdx.x * kV;
 #pragma unroll
   for (int j = 0; j < kV; ++j) {
     const double2 p = a0 + j < n_ai ? pa[a0 + j] : make_double2(0.0, 0.0);
+    my[j] = p;
     pf[j] = make_float2(__double2float_rn(p.x), __double2float_rn(p.y));
   }
+  __syncthreads();
+  if (a0 >= lda) return;
   // pad entries (a >= n_ai) hold the type maximum
   uint32_t padw[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int j = 0; j < kV; ++j)
     if (a0 + j >= n_ai) padw[j / kPer] |= type_max<T>() << (8 * sizeof(T) * (j % kPer));
+  double2 q_next = blockIdx.y < (unsigned)n_bi ? pb[blockIdx.y] : make_double2(0.0, 0.0);
   for (int b = blockIdx.y; b < n_bi; b += gridDim.y) {
-    const double2 q = pb[b];
+    const double2 q = q_next;  // the next row's point is in flight during this row
+    if (b + (int)gridDim.y < n_bi) q_next = pb[b + gridDim.y];
     const float qx = __double2float_rn(q.x), qy = __double2float_rn(q.y);
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    // all kV estimates first (branch-free, independent: ILP across entries).
+    // z = x_f - 1/2 and y = z + 1.5 * 2^23 (FP32): y's low bits are then
+    // rint(z) = floor(x_f), and |z - rint(z)| = 1/2 - (distance of x_f to the
+    // nearest integer) — so one max over the kV entries tells whether any of
+    // them lies within margin of a level boundary (FP32/INT only; the
+    // float->int conversion pipe is quarter rate and was the limit).
+    uint32_t yv[kV];
+    float dmax = 0.0f;
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
       const float dx = pf[j].x - qx, dy = pf[j].y - qy;
-      const float xf = sqrt_approx(fmaf(dy, dy, dx * dx)) * inv_step;
-      int k = (int)(xf - margin);
-      if (k != (int)(xf + margin)) {  // near a level boundary: the exact FP64 d2 and the table
-        const double2 p = pa[min(a0 + j, n_ai - 1)];
-        const double ex = __dsub_rn(p.x, q.x), ey = __dsub_rn(p.y, q.y);
-        const double d2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
-        k = max(0, min(k - 1, uf));
-        while (k < uf && s_thr[k + 1] <= d2) ++k;
-      }
-      w[j / kPer] |= (uint32_t)k << (8 * sizeof(T) * (j % kPer));
+      const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
+      const float y = __fadd_rn(z, 12582912.0f);
+      yv[j] = __float_as_uint(y);
+      dmax = fmaxf(dmax, fabsf(__fsub_rn(z, __fsub_rn(y, 12582912.0f))));
     }
-    *reinterpret_cast<uint4*>(kT + (size_t)b * lda + a0) =
-        make_uint4(w[0] | padw[0], w[1] | padw[1], w[2] | padw[2], w[3] | padw[3]);
+    if (dmax >= lim) {  // some entry near a level boundary: the exact FP64 d2 and the table
+#pragma unroll
+      for (int j = 0; j < kV; ++j) {
+        const float dx = pf[j].x - qx, dy = pf[j].y - qy;
+        const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
+        const float y = __fadd_rn(z, 12582912.0f);
+        if (fabsf(__fsub_rn(z, __fsub_rn(y, 12582912.0f))) >= lim) {
+          const double2 p = my[j];
+          const double ex = __dsub_rn(p.x, q.x), ey = __dsub_rn(p.y, q.y);
+          const double d2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+          // floor(x_f) = yv - 0x4B400000 and |x_f - x| < margin < 1, so the exact
+          // level (>= floor(x) - 1 >= floor(x_f) - 2) is reached walking up from there
+          int k = max(0, min((int)(yv[j] - 0x4B400000u) - 2, uf));
+          while (k < uf && s_thr[k + 1] <= d2) ++k;
+          yv[j] = 0x4B400000u + (uint32_t)k;
+        }
+      }
+    }
+    uint32_t w[4];
+    if constexpr (sizeof(T) == 1) {
+#pragma unroll
+      for (int q4 = 0; q4 < kW; ++q4)
+        w[q4] = __byte_perm(__byte_perm(yv[4 * q4], yv[4 * q4 + 1], 0x0040), __byte_perm(yv[4 * q4 + 2], yv[4 * q4 + 3], 0x0040),
+                            0x5410);
+    } else if constexpr (sizeof(T) == 2) {
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) w[q4] = __byte_perm(yv[2 * q4], yv[2 * q4 + 1], 0x5410);
+    } else {
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) w[q4] = yv[q4] - 0x4B400000u;
+    }
+    if constexpr (kW == 2)
+      *reinterpret_cast<uint2*>(kT + (size_t)b * lda + a0) = make_uint2(w[0] | padw[0], w[1] | padw[1]);
+    else
+      *reinterpret_cast<uint4*>(kT + (size_t)b * lda + a0) =
+          make_uint4(w[0] | padw[0], w[1] | padw[1], w[2] | padw[2], w[3] | padw[3]);
   }
 }
 
@@ -343,11 +388,11 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
   const double2* a2 = reinterpret_cast<const double2*>(pa);
   const double2* b2 = reinterpret_cast<const double2*>(pb);
   if (thr && thr_n >= 2 && thr_n <= kThrSmemMax) {
-    // threads own 16 B of a row (lda is a multiple of 512 B / width); ~8 resident
-    // blocks per SM over the columns, the supply rows strided over grid.y
-    const int threads_x = lda * width / 16;
+    // threads own kV entries of a row (8 B for u8, 16 B otherwise); the grid is
+    // one resident wave (occupancy-sized), the supply rows strided over grid.y
+    const int kv = width == 1 ? 8 : 16 / width;
+    const int threads_x = (lda + kv - 1) / kv;
     const int bx = (threads_x + 255) / 256;
-    const int by = std::max(1, std::min(n_bi, (148 * 8 + bx - 1) / bx * 4));
     const float inv_step = (float)(1.0 / (std::sqrt(2.0) * eps));
     // Bound on |x_f - x| (x = c / eps <= 1/eps + 1): float coordinates are off
     // by <= C 2^-24 each (C = max |coordinate|), so dx_f, dy_f by <= 3 C 2^-24
@@ -357,11 +402,16 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
     const double bound = (4.3 * absmax * std::ldexp(1.0, -24) + std::sqrt(2.0) * std::ldexp(1.0, -22)) /
                              (std::sqrt(2.0) * eps) + xmax * std::ldexp(1.0, -21);
     const float margin = (float)std::min(0.5, 4.0 * bound + 1e-7);
-    const size_t smem = (size_t)thr_n * sizeof(double);
+    const size_t smem = (size_t)thr_n * sizeof(double) + 256 * (size_t)kv * sizeof(double2);
     with_width(width, [&](auto tag) {
       using T = decltype(tag);
       auto fn = round_points_thr_kernel<T>;
       if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0, dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
+      const int by = std::max(1, std::min(n_bi, sms * per_sm / bx));
       fn<<<dim3(bx, std::min(by, 65535)), 256, smem, s>>>(a2, b2, n_ai, n_bi, thr, thr_n, inv_step, margin,
                                                            static_cast<T*>(kT), lda);
       return 0;
