@@ -173,6 +173,13 @@ struct AssignmentOptions {
   // matrix would not fit in free device memory), 1 matrix, 2 on the fly (the
   // scans round the point costs through the exact threshold table; no kT).
   int costs = 0;
+  // Multi-GPU: non-empty = the rows of A are sharded over these
+  // CUDA devices (one shard per entry; a device listed several times holds
+  // several logical shards) and solved by the device-resident loop
+  // (otprg_create_multi / otprg_shard_solve_resident).  Point instances only;
+  // results are bit-identical to the single-GPU solve.
+  std::vector<int> devices;
+  int shard_k = 16;  // candidates per shard and proposer per exchange round
 };
 
 struct FeasibilityReport {

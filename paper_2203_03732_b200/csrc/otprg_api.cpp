@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <map>
+#include <memory>
 #include <set>
 #include <string>
 #include <tuple>
@@ -370,6 +371,21 @@ bool on_the_fly(const AssignmentInstance& inst, const AssignmentOptions& opt) {
   return static_cast<double>(need) > 0.9 * static_cast<double>(free_b);
 }
 
+// Multi-device contexts, one per device list (and thread), kept for reuse.
+otprg_ctx* multi_context(const std::vector<int>& devices, int K) {
+  static thread_local std::map<std::vector<int>, std::unique_ptr<otprg_ctx, void (*)(otprg_ctx*)>> cache;
+  auto it = cache.find(devices);
+  if (it == cache.end()) {
+    otprg_ctx* c = nullptr;
+    std::vector<int32_t> d(devices.begin(), devices.end());
+    if (otprg_create_multi(d.data(), static_cast<int32_t>(d.size()), &c) != OTPRG_OK)
+      throw DeviceError("otprg: cannot create a multi-device context");
+    it = cache.emplace(devices, std::unique_ptr<otprg_ctx, void (*)(otprg_ctx*)>(c, otprg_destroy)).first;
+  }
+  check(otprg_set_shard_k(it->second.get(), K), it->second.get());
+  return it->second.get();
+}
+
 // One shard, no kT (OTPRG_FLAG_ON_THE_FLY): the per-phase protocol of
 // paper_2203_03732_b200/sharded.py run_phases with a local "exchange".
 void solve_on_the_fly(otprg_ctx* ctx, otprg_problem p, otprg_result* r, int device) {
@@ -424,6 +440,12 @@ std::pair<Matching, SolveStats> solve_assignment(const AssignmentInstance& inst,
   if (opt.observer || opt.check_invariants || opt.demand_groups) return solve_debug(ctx, inst, opt);
   otprg_problem p = problem_of(inst, opt.eps, opt.storage);
   ResultBufs rb(inst.n_a, inst.n_b, opt.eps);
+  if (!opt.devices.empty() && p.cost_kind == OTPRG_COST_POINTS2D) {  // A rows sharded over the devices
+    otprg_ctx* mc = multi_context(opt.devices, opt.shard_k);
+    if (opt.costs == 2 || (opt.costs == 0 && on_the_fly(inst, opt))) p.flags |= OTPRG_FLAG_ON_THE_FLY;
+    check(otprg_solve_assignment(mc, &p, &rb.r), mc);
+    return rb.take();
+  }
   if (p.cost_kind == OTPRG_COST_POINTS2D && on_the_fly(inst, opt)) {
     solve_on_the_fly(ctx, p, &rb.r, opt.device);
     return rb.take();

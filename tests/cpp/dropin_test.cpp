@@ -86,6 +86,16 @@ static void assignment_cases() {
     gf.costs = 2;
     auto [mf, sf] = otprg::solve_assignment(gp, gf);
     same_result(mr, sr, mf, sf, "square points, costs on the fly");
+    // A rows sharded over several (logical) devices: the resident multi-GPU loop
+    for (int G : {1, 3}) {
+      otprg::AssignmentOptions gm = go;
+      gm.devices.assign(G, 0);
+      auto [mm, sm] = otprg::solve_assignment(gp, gm);
+      same_result(mr, sr, mm, sm, G == 1 ? "sharded, 1 device" : "sharded, 3 logical devices");
+      gm.costs = 2;
+      auto [mo, so] = otprg::solve_assignment(gp, gm);
+      same_result(mr, sr, mo, so, "sharded on the fly");
+    }
   }
   for (auto [na, nb] : {std::pair{300, 170}, std::pair{170, 300}}) {
     const otpr::AssignmentInstance r = random_instance(na, nb, 40 + na);
