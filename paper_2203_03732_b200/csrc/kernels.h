@@ -160,6 +160,68 @@ cudaError_t launch_ot_scan(const void* kT, int lda, int width, const void* t0, c
                            const int4* req, int nreq, int K, int32_t* out, int2* meta,
                            cudaStream_t s);
 
+// ---- OT copy/cluster phase on the device (ot_device.cu) ---------------------
+constexpr int32_t kFreeB = 0x7fffffff;  // flow-entry "b" of a demand cluster's free copies
+enum OtCtr { kCtrNi = 0, kCtrFree = 1, kCtrNew = 2, kCtrE = 3, kCtrRec = 4, kCtrCount = 8 };
+struct OtDev {
+  int n_a, n_b, lda, width;
+  const void* kT;      // [n_b][lda] rounded costs at eps/3
+  void* t;             // [2][lda] width-typed: t_ci(a) = -y(a, ci), type max if absent
+  // demand clusters: code 2a + slot (slot 0 the higher dual), count 0 = absent
+  int32_t* dy;
+  int64_t* dfree;
+  int64_t* dmatched;
+  int64_t* consumed;   // copies given this phase
+  // flows: CSR by code, entries ascending b then the free-copy sentinel (b = kFreeB)
+  int64_t* fl_off;     // [2 n_a + 1]
+  int32_t* fl_code;
+  int32_t* fl_b;
+  int64_t* fl_cnt;
+  int64_t* fl_pre;     // matched copies of the cluster before this entry
+  // supply clusters: 2b + slot (slot 0 the higher dual)
+  int32_t* sy;
+  int64_t* sfree;
+  int64_t* smatched;
+  int64_t* sfreed;     // displaced copies returning free this phase
+  // the phase's free supply vertices (list index i, ascending b)
+  int32_t* fb;
+  int32_t* fy;
+  int32_t* fpos;       // frontier index in the admissible list
+  int32_t* fidx;       // [n_b] list index or -1
+  int64_t* fu0;        // free copies at phase start
+  int64_t* fu;         // copies not (yet) placed
+  int64_t* adm_len;
+  int64_t* adm_off;
+  int32_t* adm;        // admissible cluster codes, ascending a
+  // DA entries (key = code << 32 | i) and next-state records
+  unsigned long long* e_key;
+  int64_t* e_val;
+  unsigned long long* r_key;
+  int64_t* r_val;
+  int64_t* ctr;        // [kCtrCount]
+  int* status;
+  int32_t* err;        // [3]
+};
+cudaError_t ot_dev_free_list(OtDev& D, int* scratch, cudaStream_t s);
+cudaError_t ot_dev_t(OtDev& D, cudaStream_t s);
+cudaError_t ot_dev_adm(OtDev& D, int pass, cudaStream_t s);
+cudaError_t ot_dev_propose(OtDev& D, cudaStream_t s);
+cudaError_t ot_dev_resolve(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                           unsigned long long* out_key, int64_t* out_val, cudaStream_t s);
+cudaError_t ot_dev_consumed(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                            cudaStream_t s);
+cudaError_t ot_dev_records(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                           cudaStream_t s);
+cudaError_t ot_dev_rebuild(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                           cudaStream_t s);
+cudaError_t ot_sort_pairs(void* temp, size_t& temp_bytes, const unsigned long long* kin, unsigned long long* kout,
+                          const int64_t* vin, int64_t* vout, long long n, int end_bit, cudaStream_t s);
+cudaError_t ot_reduce_by_key(void* temp, size_t& temp_bytes, const unsigned long long* kin,
+                             unsigned long long* kout, const int64_t* vin, int64_t* vout, long long* nout,
+                             long long n, cudaStream_t s);
+cudaError_t ot_exclusive_sum(void* temp, size_t& temp_bytes, const int64_t* in, int64_t* out, int n,
+                             cudaStream_t s);
+
 // Phase loop.
 cudaError_t launch_init_state(const SolveArgs& a, int n_a, int n_b, int lda, int width,
                               cudaStream_t s);

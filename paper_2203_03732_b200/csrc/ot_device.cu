@@ -1,0 +1,555 @@
+// ot_device.cu — the OT copy/cluster phase on the device (SURVEY §8(a) O2/O3,
+// kernels K10/K11; reference semantics: solve_copy_matching, src/ot.cpp:418-637).
+//
+// State (every vertex carries at most two dual clusters, ot.hpp:65-96):
+//   demand cluster code = 2a + slot (slot 0 the higher dual; count 0 = absent):
+//     dy, dfree, dmatched; its flow (b, copies) ascending b in CSR by code,
+//     followed by one sentinel entry b = kFreeB holding the free copies;
+//   supply cluster 2b + slot (slot 0 the higher dual): sy, sfree, smatched.
+//
+// One phase:
+//   free list    supply vertices with free copies, ascending b, their dual y_b
+//                and copy count; n_i for the termination test;
+//   admissible   every free b's admissible clusters, y(a,ci) = k(a,b)+1-y_b,
+//                ascending a (CSR; count pass + fill pass over kT rows);
+//   claim (K10)  capacitated deferred acceptance: each b proposes its
+//                unplaced copies to its frontier cluster; a cluster keeps the
+//                lowest b's up to its capacity (free + matched copies at phase
+//                start) and returns the rest; a b rejected at its frontier
+//                moves on, copies returned from an earlier cluster go to the
+//                frontier again.  With one priority order (b ascending) over
+//                every cluster this reaches exactly the reference's greedy
+//                claims (b ascending, each taking min(remaining, available)
+//                from its admissible clusters in ascending a; checked against
+//                a serial restatement on random instances and by the goldens);
+//   update (K11) a cluster that gave c copies lost min(c, free) free copies
+//                and its first c - min(c, free) matched copies in ascending
+//                partner order (ot.cpp:504-514); the displaced partners' copies
+//                return free at their old dual k(a,b_old) - y; the claiming
+//                b's copies join the cluster one dual below; supply copies
+//                left free go up a unit; then both sides are normalised
+//                (free supply copies lifted to the vertex maximum, equal duals
+//                merged, empty clusters dropped, at most two per vertex,
+//                ot.cpp:362-414) — by one sort of all flow records keyed
+//                (a, descending y, b) and per-vertex passes.
+// Errors (the reference's InvariantViolation messages) are reported as status
+// 5 with a code in err[0]: 1 third demand dual, 2 third supply dual, 3
+// displaced copy without a supply cluster, 4 storage bound exceeded.
+#include <climits>
+#include <cub/cub.cuh>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace otprg {
+
+namespace {
+
+__device__ __forceinline__ void ot_fail(OtDev& D, int code, int x = 0, int y = 0) {
+  if (atomicCAS(D.status, 0, 5) == 0) {
+    D.err[0] = code;
+    D.err[1] = x;
+    D.err[2] = y;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t k_at(const OtDev& D, int a, int b) {
+  return static_cast<const T*>(D.kT)[(size_t)b * D.lda + a];
+}
+
+// ---- free list ---------------------------------------------------------------
+// Per supply vertex: total free copies (after normalisation at most one slot
+// holds free copies: the vertex maximum).
+__device__ __forceinline__ int64_t sfree_total(const OtDev& D, int b) {
+  return D.sfree[2 * b] + D.sfree[2 * b + 1];
+}
+
+constexpr int kListBlocks = 148;
+
+__global__ void __launch_bounds__(1024) ot_free_count_kernel(OtDev D, int* counts) {
+  const int n = D.n_b, chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int lo = min(n, (int)blockIdx.x * chunk), hi = min(n, lo + chunk);
+  int c = 0;
+  long long tot = 0;
+  for (int b = lo + threadIdx.x; b < hi; b += blockDim.x) {
+    const int64_t f = sfree_total(D, b);
+    c += f > 0;
+    tot += f;
+  }
+  __shared__ int s_c;
+  __shared__ unsigned long long s_t;
+  if (threadIdx.x == 0) s_c = 0, s_t = 0;
+  __syncthreads();
+  c = __reduce_add_sync(kFull, c);
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+  if ((threadIdx.x & 31) == 0) {
+    if (c) atomicAdd(&s_c, c);
+    if (tot) atomicAdd(&s_t, (unsigned long long)tot);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    counts[blockIdx.x] = s_c;
+    if (s_t) atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrNi]), s_t);
+  }
+}
+
+__global__ void __launch_bounds__(1024) ot_free_write_kernel(OtDev D, const int* counts) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int n = D.n_b, chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int lo = min(n, (int)blockIdx.x * chunk), hi = min(n, lo + chunk);
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int g = 0; g < (int)blockIdx.x; ++g) off += counts[g];
+    s_base = off;
+    if (blockIdx.x == gridDim.x - 1) D.ctr[kCtrFree] = off + counts[blockIdx.x];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int t0 = lo; t0 < hi; t0 += blockDim.x) {
+    const int b = t0 + threadIdx.x;
+    int64_t f = 0;
+    if (b < hi) f = sfree_total(D, b);
+    const bool on = f > 0;
+    const unsigned bal = __ballot_sync(kFull, on);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      if (w < warp) before += s_warp[w];
+      total += s_warp[w];
+    }
+    if (b < hi) D.fidx[b] = -1;
+    if (on) {
+      const int pos = s_base + before + __popc(bal & ((1u << lane) - 1u));
+      D.fb[pos] = b;
+      D.fu0[pos] = f;
+      D.fu[pos] = f;
+      D.fpos[pos] = 0;
+      D.fy[pos] = D.sfree[2 * b] > 0 ? D.sy[2 * b] : D.sy[2 * b + 1];
+      D.fidx[b] = pos;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
+}
+
+// t_ci(a) = -y of cluster (a, ci), type max when absent (never admissible).
+template <typename T>
+__global__ void ot_t_kernel(OtDev D) {
+  T* t = static_cast<T*>(D.t);
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < D.lda; a += gridDim.x * blockDim.x)
+    for (int s = 0; s < 2; ++s) {
+      uint32_t v = type_max<T>();
+      if (a < D.n_a && D.dfree[2 * a + s] + D.dmatched[2 * a + s] > 0) {
+        const int64_t ty = -(int64_t)D.dy[2 * a + s];
+        if (ty < 0 || ty > (int64_t)type_max<T>() - 2) ot_fail(D, 4, a, (int)ty);
+        else v = (uint32_t)ty;
+      }
+      t[(size_t)s * D.lda + a] = (T)v;
+    }
+}
+
+// ---- admissible clusters (warp per free b, full row) ---------------------------
+// pass 0: count; pass 1: write codes 2a + ci ascending a at adm_off[i].
+template <typename T, int kPass>
+__global__ void __launch_bounds__(256) ot_adm_kernel(OtDev D) {
+  using S = Simd<T>;
+  constexpr int kEpv = 16 / sizeof(T);
+  const int lane = threadIdx.x & 31;
+  const int nf = D.ctr[kCtrFree];
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint4* v0 = static_cast<const uint4*>(D.t);
+  const uint4* v1 = reinterpret_cast<const uint4*>(static_cast<const T*>(D.t) + D.lda);
+  const int nv = D.lda / kEpv;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nf; i += nwarps) {
+    const int b = D.fb[i];
+    const uint32_t tg = S::rep((uint32_t)(D.fy[i] - 1));
+    const uint4* rv = reinterpret_cast<const uint4*>(static_cast<const T*>(D.kT) + (size_t)b * D.lda);
+    int64_t pos = kPass ? D.adm_off[i] : 0;
+    int cnt = 0;
+    for (int v0i = 0; v0i < nv; v0i += 32) {
+      const int vi = v0i + lane;
+      uint32_t m0 = 0, m1 = 0;
+      if (vi < nv) {
+        const uint4 k = __ldg(rv + vi), x0 = __ldg(v0 + vi), x1 = __ldg(v1 + vi);
+        const uint32_t kw[4] = {k.x, k.y, k.z, k.w}, w0[4] = {x0.x, x0.y, x0.z, x0.w},
+                       w1[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          m0 |= S::bits(S::eq(S::add(kw[q], w0[q]), tg)) << (q * S::kEpw);
+          m1 |= S::bits(S::eq(S::add(kw[q], w1[q]), tg)) << (q * S::kEpw);
+        }
+      }
+      const uint32_t m = m0 | m1;  // (the two clusters of a have distinct duals: one bit per a at most)
+      const int c = __popc(m);
+      if (!__ballot_sync(kFull, c != 0)) continue;
+      int inc = c;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const int y = __shfl_up_sync(kFull, inc, s);
+        if (lane >= s) inc += y;
+      }
+      if (kPass) {
+        int64_t o = pos + inc - c;
+        uint32_t bm = m;
+        while (bm) {
+          const int e = __ffs(bm) - 1;
+          bm &= bm - 1;
+          const int a = vi * kEpv + e;
+          D.adm[o++] = 2 * a + ((m1 >> e) & 1);
+        }
+      }
+      const int tot = __shfl_sync(kFull, inc, 31);
+      cnt += tot;
+      pos += tot;
+    }
+    if (!kPass && lane == 0) D.adm_len[i] = cnt;
+  }
+}
+
+// ---- deferred acceptance -------------------------------------------------------
+// Entries: key = (code << 32) | list index, value = copies.
+__global__ void ot_da_propose_kernel(OtDev D) {
+  const int nf = D.ctr[kCtrFree];
+  const long long base = D.ctr[kCtrE];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    const int64_t u = D.fu[i];
+    if (u <= 0) continue;
+    const int p = D.fpos[i];
+    if (p >= D.adm_len[i]) continue;  // admissible set exhausted: these copies stay free
+    const int code = D.adm[D.adm_off[i] + p];
+    const long long slot = base + atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrNew]), 1ull);
+    D.e_key[slot] = ((unsigned long long)(uint32_t)code << 32) | (uint32_t)i;
+    D.e_val[slot] = u;
+    D.fu[i] = 0;
+  }
+}
+
+// After the sort: every run of equal keys (a b that re-proposed to a cluster it
+// holds) is summed into its last entry; within a cluster's segment the copies
+// of lower b's come first.  The entry keeps min(amount, capacity left); the
+// rest returns to its b, which leaves a frontier cluster that rejected it.
+__global__ void ot_da_resolve_kernel(OtDev D, const unsigned long long* __restrict__ key,
+                                     const int64_t* __restrict__ val, long long n,
+                                     unsigned long long* __restrict__ out_key, int64_t* __restrict__ out_val) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long kj = key[j];
+    if (j + 1 < n && key[j + 1] == kj) continue;  // the run's last entry carries it
+    const uint32_t code = (uint32_t)(kj >> 32);
+    const int i = (int)(uint32_t)kj;
+    int64_t amt = val[j], pre = 0;
+    long long q = j - 1;
+    for (; q >= 0 && key[q] == kj; --q) amt += val[q];
+    for (; q >= 0 && (uint32_t)(key[q] >> 32) == code; --q) pre += val[q];
+    const int64_t cap = D.dfree[code] + D.dmatched[code];
+    const int64_t acc = max((int64_t)0, min(amt, cap - pre));
+    const int64_t rej = amt - acc;
+    if (rej > 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&D.fu[i]), (unsigned long long)rej);
+      const int p = D.fpos[i];
+      if (p < D.adm_len[i] && D.adm[D.adm_off[i] + p] == (int)code) D.fpos[i] = p + 1;
+    }
+    if (acc > 0) {
+      const long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrE]), 1ull);
+      out_key[slot] = kj;
+      out_val[slot] = acc;
+    }
+  }
+}
+
+// ---- updates -------------------------------------------------------------------
+// Copies each demand cluster gave this phase (final claims sorted by code).
+__global__ void ot_consumed_kernel(OtDev D, const unsigned long long* __restrict__ key,
+                                   const int64_t* __restrict__ val, long long n) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&D.consumed[key[j] >> 32]), (unsigned long long)val[j]);
+}
+
+// Records of the next state, key (a, descending y, b), b = kFreeB for free
+// demand copies: surviving flow entries (the displaced prefix removed, its
+// supply copies freed at their old dual), the free copies left, the claims
+// one dual below.
+constexpr uint32_t kYBias = 1u << 20;
+__device__ __forceinline__ unsigned long long rec_key(int a, int y, int b) {
+  const unsigned long long bk = b == kFreeB ? (1ull << 21) - 1 : (unsigned long long)b;
+  return ((unsigned long long)a << 42) | ((unsigned long long)(kYBias - y) << 21) | bk;
+}
+
+__device__ __forceinline__ void put_rec(OtDev& D, int a, int y, int b, int64_t cnt) {
+  const long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrRec]), 1ull);
+  D.r_key[slot] = rec_key(a, y, b);
+  D.r_val[slot] = cnt;
+}
+
+template <typename T>
+__global__ void ot_flow_records_kernel(OtDev D) {
+  const long long nfl = D.fl_off[2 * D.n_a];
+  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < nfl; f += (long long)gridDim.x * blockDim.x) {
+    const int code = D.fl_code[f];
+    const int a = code >> 1, y = D.dy[code], b = D.fl_b[f];
+    const int64_t cnt = D.fl_cnt[f];
+    const int64_t cons = D.consumed[code];
+    if (b == kFreeB) {  // free copies go first
+      const int64_t left = cnt - min(cons, cnt);
+      if (left > 0) put_rec(D, a, y, kFreeB, left);
+      continue;
+    }
+    // matched copies, ascending partner: displaced are the first cons - free of them
+    const int64_t free_c = D.dfree[code];
+    const int64_t disp_total = max((int64_t)0, cons - free_c);
+    const int64_t before = D.fl_pre[f];
+    const int64_t disp = max((int64_t)0, min(cnt, disp_total - before));
+    if (cnt - disp > 0) put_rec(D, a, y, b, cnt - disp);
+    if (disp > 0) {  // the partner's copies return free at their old dual k(a,b) - y (ot.cpp:560-575)
+      const int y_old = (int)k_at<T>(D, a, b) - y;
+      int s = -1;
+      for (int q = 0; q < 2; ++q)
+        if (D.sfree[2 * b + q] + D.smatched[2 * b + q] > 0 && D.sy[2 * b + q] == y_old) s = q;
+      if (s < 0) {
+        ot_fail(D, 3, a, b);
+        continue;
+      }
+      atomicAdd(reinterpret_cast<unsigned long long*>(&D.sfreed[2 * b + s]), (unsigned long long)disp);
+    }
+  }
+}
+
+__global__ void ot_claim_records_kernel(OtDev D, const unsigned long long* __restrict__ key,
+                                        const int64_t* __restrict__ val, long long n) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const int code = (int)(key[j] >> 32), i = (int)(uint32_t)key[j];
+    put_rec(D, code >> 1, D.dy[code] - 1, D.fb[i], val[j]);
+  }
+}
+
+// Supply side (ot.cpp:540-553, 580-588): a free b's copies placed this phase
+// join its free cluster's matched copies, the rest go up a unit; displaced
+// copies come back free at their cluster; then normalize_supply: every free
+// copy lifted to the vertex maximum dual, equal duals merged, empty dropped,
+// at most two clusters (slot 0 the higher dual).
+__global__ void ot_supply_kernel(OtDev D) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < D.n_b; b += gridDim.x * blockDim.x) {
+    int y[3];
+    int64_t fr[3], mt[3];
+    int n = 0;
+    const int i = D.fidx[b];
+    for (int s = 0; s < 2; ++s) {
+      int64_t f = D.sfree[2 * b + s], m = D.smatched[2 * b + s];
+      const int64_t back = D.sfreed[2 * b + s];
+      D.sfreed[2 * b + s] = 0;
+      if (f + m == 0) continue;
+      if (i >= 0 && f > 0) {  // this phase's free cluster
+        m += D.fu0[i] - D.fu[i];
+        f = 0;
+      }
+      m -= back;  // displaced copies leave the matched count ...
+      f += back;  // ... and come back free at this dual
+      if (m < 0) ot_fail(D, 3, -1, b);
+      y[n] = D.sy[2 * b + s];
+      fr[n] = f;
+      mt[n] = m;
+      ++n;
+    }
+    if (i >= 0 && D.fu[i] > 0) {  // copies left free: one dual up
+      y[n] = D.fy[i] + 1;
+      fr[n] = D.fu[i];
+      mt[n] = 0;
+      ++n;
+    }
+    // normalize_supply
+    int64_t free_tot = 0;
+    int ymax = INT_MIN;
+    for (int q = 0; q < n; ++q)
+      if (fr[q] + mt[q] > 0) {
+        free_tot += fr[q];
+        ymax = max(ymax, y[q]);
+      }
+    int oy[2] = {0, 0};
+    int64_t ofr[2] = {0, 0}, omt[2] = {0, 0};
+    int m = 0;
+    auto add = [&](int yy, int64_t f, int64_t mm) {
+      for (int q = 0; q < m; ++q)
+        if (oy[q] == yy) {
+          ofr[q] += f;
+          omt[q] += mm;
+          return;
+        }
+      if (m == 2) {
+        ot_fail(D, 2, b);
+        return;
+      }
+      oy[m] = yy;
+      ofr[m] = f;
+      omt[m] = mm;
+      ++m;
+    };
+    for (int q = 0; q < n; ++q)
+      if (mt[q] > 0) add(y[q], 0, mt[q]);
+    if (free_tot > 0) add(ymax, free_tot, 0);
+    if (m == 2 && oy[1] > oy[0]) {
+      const int ty = oy[0];
+      oy[0] = oy[1];
+      oy[1] = ty;
+      const int64_t tf = ofr[0], tm = omt[0];
+      ofr[0] = ofr[1];
+      omt[0] = omt[1];
+      ofr[1] = tf;
+      omt[1] = tm;
+    }
+    for (int q = 0; q < 2; ++q) {
+      D.sy[2 * b + q] = q < m ? oy[q] : INT_MIN;
+      D.sfree[2 * b + q] = q < m ? ofr[q] : 0;
+      D.smatched[2 * b + q] = q < m ? omt[q] : 0;
+    }
+  }
+}
+
+// After the records are sorted and merged (unique keys, summed counts): the
+// record's demand slot (0 for the vertex's first dual, 1 for the second; a
+// third is the reference's "third dual value" violation) and its code.
+__global__ void ot_slot_kernel(OtDev D, const unsigned long long* __restrict__ key, long long n) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long kj = key[j];
+    const unsigned long long a = kj >> 42, yk = (kj >> 21) & ((1ull << 21) - 1);
+    // first record of a: lower_bound of (a, 0, 0)
+    long long lo = 0, hi = j;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if ((key[mid] >> 42) < a) lo = mid + 1;
+      else hi = mid;
+    }
+    const unsigned long long yk0 = (key[lo] >> 21) & ((1ull << 21) - 1);
+    int slot = 0;
+    if (yk != yk0) {
+      // first record of a with a different dual
+      long long l2 = lo, h2 = j;
+      while (l2 < h2) {
+        const long long mid = (l2 + h2) >> 1;
+        if (((key[mid] >> 21) & ((1ull << 21) - 1)) == yk0) l2 = mid + 1;
+        else h2 = mid;
+      }
+      slot = (((key[l2] >> 21) & ((1ull << 21) - 1)) == yk) ? 1 : 2;
+      if (slot == 2) ot_fail(D, 1, (int)a);
+    }
+    D.fl_code[j] = (int)(2 * a) + min(slot, 1);
+  }
+}
+
+// New CSR: fl_off[c] = first record of code c (lower bound), cluster fields
+// from the code's segment, the flow prefix sums for the next displacement.
+__global__ void ot_rebuild_kernel(OtDev D, const unsigned long long* __restrict__ key,
+                                  const int64_t* __restrict__ val, long long n) {
+  const int nc = 2 * D.n_a;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= nc; c += gridDim.x * blockDim.x) {
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (D.fl_code[mid] < c) lo = mid + 1;
+      else hi = mid;
+    }
+    D.fl_off[c] = lo;
+    if (c == nc) continue;
+    int64_t fr = 0, mt = 0;
+    int y = INT_MIN;
+    for (long long f = lo; f < n && D.fl_code[f] == c; ++f) {
+      const unsigned long long kf = key[f];
+      y = (int)((long long)kYBias - (long long)((kf >> 21) & ((1ull << 21) - 1)));
+      const unsigned long long bk = kf & ((1ull << 21) - 1);
+      D.fl_b[f] = bk == (1ull << 21) - 1 ? kFreeB : (int)bk;
+      D.fl_cnt[f] = val[f];
+      D.fl_pre[f] = mt;
+      if (bk == (1ull << 21) - 1) fr += val[f];
+      else mt += val[f];
+    }
+    D.dy[c] = y;
+    D.dfree[c] = fr;
+    D.dmatched[c] = mt;
+    D.consumed[c] = 0;
+  }
+}
+
+}  // namespace
+
+cudaError_t ot_dev_free_list(OtDev& D, int* scratch, cudaStream_t s) {
+  ot_free_count_kernel<<<kListBlocks, 1024, 0, s>>>(D, scratch);
+  ot_free_write_kernel<<<kListBlocks, 1024, 0, s>>>(D, scratch);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_t(OtDev& D, cudaStream_t s) {
+  with_width(D.width, [&](auto tag) {
+    ot_t_kernel<decltype(tag)><<<148, 256, 0, s>>>(D);
+    return 0;
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_adm(OtDev& D, int pass, cudaStream_t s) {
+  with_width(D.width, [&](auto tag) {
+    if (pass == 0) ot_adm_kernel<decltype(tag), 0><<<148 * 8, 256, 0, s>>>(D);
+    else ot_adm_kernel<decltype(tag), 1><<<148 * 8, 256, 0, s>>>(D);
+    return 0;
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_propose(OtDev& D, cudaStream_t s) {
+  ot_da_propose_kernel<<<148 * 4, 256, 0, s>>>(D);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_resolve(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                           unsigned long long* out_key, int64_t* out_val, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  ot_da_resolve_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, val, n, out_key,
+                                                                                          out_val);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_consumed(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                            cudaStream_t s) {
+  if (n > 0)
+    ot_consumed_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, val, n);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_records(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                           cudaStream_t s) {
+  with_width(D.width, [&](auto tag) {
+    ot_flow_records_kernel<decltype(tag)><<<148 * 8, 256, 0, s>>>(D);
+    return 0;
+  });
+  if (n > 0)
+    ot_claim_records_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, val, n);
+  ot_supply_kernel<<<(D.n_b + 255) / 256, 256, 0, s>>>(D);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_rebuild(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
+                           cudaStream_t s) {
+  if (n > 0) ot_slot_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, n);
+  ot_rebuild_kernel<<<(2 * D.n_a + 1 + 255) / 256, 256, 0, s>>>(D, key, val, n);
+  return cudaGetLastError();
+}
+
+// CUB helpers (temp storage grown on demand by the caller).
+cudaError_t ot_sort_pairs(void* temp, size_t& temp_bytes, const unsigned long long* kin, unsigned long long* kout,
+                          const int64_t* vin, int64_t* vout, long long n, int end_bit, cudaStream_t s) {
+  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, n, 0, end_bit, s);
+}
+
+cudaError_t ot_reduce_by_key(void* temp, size_t& temp_bytes, const unsigned long long* kin,
+                             unsigned long long* kout, const int64_t* vin, int64_t* vout, long long* nout,
+                             long long n, cudaStream_t s) {
+  return cub::DeviceReduce::ReduceByKey(temp, temp_bytes, kin, kout, vin, vout, nout, cub::Sum(), n, s);
+}
+
+cudaError_t ot_exclusive_sum(void* temp, size_t& temp_bytes, const int64_t* in, int64_t* out, int n,
+                             cudaStream_t s) {
+  return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, n, s);
+}
+
+}  // namespace otprg

@@ -4,16 +4,17 @@
 //
 // Division of labour:
 //   device  rounding of the dense cost at eps/3 into kT (K1, cost_kernels.cu)
-//           and, every phase, the admissible-cluster scan of every free
-//           supply vertex's row (ot_kernels.cu) — the O(n^2) work;
-//   host    the per-phase claim step over the scanned candidate lists and
-//           the per-vertex cluster bookkeeping (O(n + claims) per phase),
-//           completion and plan_from_flow on the sparse flow.
-// The claim order is the reference's: supply vertices ascending, each
-// consuming admissible demand clusters ascending by a; within a cluster, free
-// copies first, then matched copies ascending by current partner.  All
-// floating-point operations of plan_from_flow run in the reference's order
-// on the nonzero entries only, so the plan's masses and cost are bit-equal.
+//           and the whole phase (ot_device.cu): free list, admissible
+//           clusters of every free supply vertex, the claim step as a
+//           capacitated deferred acceptance (K10), the cluster updates and
+//           normalisation (K11) — the cluster state never leaves the device;
+//   host    the phase loop's control (a few synchronisations per phase: the
+//           termination test, buffer sizes, the DA rounds), the completion
+//           and plan_from_flow on the final sparse flow, and the debug hooks
+//           (check_invariants / observer) on an exported copy of the state.
+// All floating-point operations of plan_from_flow run in the reference's
+// order on the nonzero entries only, so the plan's masses and cost are
+// bit-equal.
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -36,11 +37,6 @@ using otprg::DevBuf;
 using otprg::host_scaled_floor;
 
 constexpr double kMassTolerance = 1e-9;  // ot.cpp:15
-// Admissible clusters returned per scan request.  A free supply vertex walks
-// past clusters already used up by lower b's, so the list must usually cover
-// its whole admissible set (~n / (3/eps) entries for uniform costs); a list
-// that runs out while the row has more is extended by a rescan.
-constexpr int kCand = 256;
 
 struct OtError {
   int code;
@@ -60,137 +56,6 @@ int64_t exact_ceil(double x) {  // ot.cpp:24-29
   while (static_cast<double>(c) < x) ++c;
   return c;
 }
-
-using Flow = std::vector<std::pair<int32_t, int64_t>>;  // (b, copies), ascending b
-
-struct DemandC {
-  int64_t y = 0, free = 0;
-  Flow flow;
-  int64_t mt = 0;  // sum of the flow counts, kept in step by dflow_add / dflow_sub
-  int64_t matched() const { return mt; }
-  int64_t count() const { return free + mt; }
-};
-
-struct SupplyC {
-  int64_t y = 0, free = 0, matched = 0;
-  int64_t count() const { return free + matched; }
-};
-
-void flow_add(Flow& f, int32_t b, int64_t cnt) {
-  if (cnt == 0) return;
-  auto it = std::lower_bound(f.begin(), f.end(), b,
-                             [](const std::pair<int32_t, int64_t>& e, int32_t k) { return e.first < k; });
-  if (it != f.end() && it->first == b)
-    it->second += cnt;
-  else
-    f.insert(it, {b, cnt});
-}
-
-void flow_sub(Flow& f, int32_t b, int64_t cnt) {
-  auto it = std::lower_bound(f.begin(), f.end(), b,
-                             [](const std::pair<int32_t, int64_t>& e, int32_t k) { return e.first < k; });
-  if (it == f.end() || it->first != b || it->second < cnt)
-    throw OtError{OTPRG_INVARIANT, "cluster flow underflow while rematching"};
-  it->second -= cnt;
-  if (it->second == 0) f.erase(it);
-}
-
-void dflow_add(DemandC& c, int32_t b, int64_t cnt) {
-  flow_add(c.flow, b, cnt);
-  c.mt += cnt;
-}
-
-void dflow_sub(DemandC& c, int32_t b, int64_t cnt) {
-  flow_sub(c.flow, b, cnt);
-  c.mt -= cnt;
-}
-
-DemandC& demand_at(std::vector<DemandC>& cs, int64_t y) {
-  for (DemandC& c : cs)
-    if (c.y == y) return c;
-  cs.push_back(DemandC{y, 0, {}});
-  return cs.back();
-}
-
-SupplyC& supply_at(std::vector<SupplyC>& cs, int64_t y) {
-  for (SupplyC& c : cs)
-    if (c.y == y) return c;
-  cs.push_back(SupplyC{y, 0, 0});
-  return cs.back();
-}
-
-// Merge equal duals, drop empty clusters, descending dual order (ot.cpp:362-383).
-void normalize_demand(std::vector<DemandC>& cs, int32_t a) {
-  // fast paths (most vertices, every phase): nothing to merge
-  if (cs.size() == 1) {
-    if (cs[0].count() == 0) cs.clear();
-    return;
-  }
-  if (cs.size() == 2 && cs[0].y != cs[1].y && cs[0].count() > 0 && cs[1].count() > 0) {
-    if (cs[0].y < cs[1].y) std::swap(cs[0], cs[1]);
-    return;
-  }
-  std::sort(cs.begin(), cs.end(), [](const DemandC& x, const DemandC& y) { return x.y > y.y; });
-  std::vector<DemandC> out;
-  for (DemandC& c : cs) {
-    if (c.count() == 0) continue;
-    if (!out.empty() && out.back().y == c.y) {
-      out.back().free += c.free;
-      for (const auto& e : c.flow) dflow_add(out.back(), e.first, e.second);
-    } else {
-      out.push_back(std::move(c));
-    }
-  }
-  cs = std::move(out);
-  if (cs.size() > 2)
-    throw OtError{OTPRG_INVARIANT, "third dual value among copies of demand vertex " + std::to_string(a)};
-}
-
-// Lift free copies to the vertex maximum, merge, drop empty (ot.cpp:385-414).
-void normalize_supply(std::vector<SupplyC>& cs, int32_t b) {
-  if (cs.size() == 1) {  // fast path: free copies already sit at the only dual
-    if (cs[0].count() == 0) cs.clear();
-    return;
-  }
-  int64_t max_y = std::numeric_limits<int64_t>::min(), total_free = 0;
-  for (const SupplyC& c : cs) {
-    if (c.count() == 0) continue;
-    max_y = std::max(max_y, c.y);
-    total_free += c.free;
-  }
-  for (SupplyC& c : cs) c.free = 0;
-  if (total_free > 0) supply_at(cs, max_y).free = total_free;
-  std::sort(cs.begin(), cs.end(), [](const SupplyC& x, const SupplyC& y) { return x.y > y.y; });
-  std::vector<SupplyC> out;
-  for (const SupplyC& c : cs) {
-    if (c.count() == 0) continue;
-    if (!out.empty() && out.back().y == c.y) {
-      out.back().free += c.free;
-      out.back().matched += c.matched;
-    } else {
-      out.push_back(c);
-    }
-  }
-  cs = std::move(out);
-  if (cs.size() > 2)
-    throw OtError{OTPRG_INVARIANT, "third dual value among copies of supply vertex " + std::to_string(b)};
-}
-
-struct Claim {
-  int32_t a, ci, b;
-  int64_t take_free;
-  int64_t total;
-  size_t disp_begin, disp_end;  // range in the displaced array
-};
-
-// Per-phase consumption cursor of one demand cluster (the reference's
-// "avail" snapshot, ot.cpp:459-469, kept as an offset into free + flow).
-struct Cursor {
-  int32_t stamp = -1;
-  int64_t used = 0;   // copies already claimed this phase
-  size_t fidx = 0;    // first flow entry not fully consumed
-  int64_t foff = 0;   // copies consumed from flow[fidx]
-};
 
 struct Timer {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
@@ -253,44 +118,23 @@ struct FlatState {
   std::vector<int32_t> dem_off, flow_b, sup_off;
   std::vector<int64_t> dem_y, dem_free, flow_off, flow_cnt, sup_y, sup_free, sup_matched;
 
-  void build(const std::vector<std::vector<DemandC>>& dem, const std::vector<std::vector<SupplyC>>& sup) {
-    n_a = static_cast<int32_t>(dem.size());
-    n_b = static_cast<int32_t>(sup.size());
-    dem_off.assign(1, 0);
-    sup_off.assign(1, 0);
-    flow_off.assign(1, 0);
-    dem_y.clear(), dem_free.clear(), flow_b.clear(), flow_cnt.clear();
-    sup_y.clear(), sup_free.clear(), sup_matched.clear();
-    for (const auto& cs : dem) {
-      for (const DemandC& c : cs) {
-        dem_y.push_back(c.y);
-        dem_free.push_back(c.free);
-        for (const auto& e : c.flow) flow_b.push_back(e.first), flow_cnt.push_back(e.second);
-        flow_off.push_back(static_cast<int64_t>(flow_b.size()));
-      }
-      dem_off.push_back(static_cast<int32_t>(dem_y.size()));
-    }
-    for (const auto& cs : sup) {
-      for (const SupplyC& c : cs) sup_y.push_back(c.y), sup_free.push_back(c.free), sup_matched.push_back(c.matched);
-      sup_off.push_back(static_cast<int32_t>(sup_y.size()));
-    }
-  }
   otprg_cluster_state view() const {
     return otprg_cluster_state{n_a,          n_b,          dem_off.data(), dem_y.data(),  dem_free.data(),
                                flow_off.data(), flow_b.data(), flow_cnt.data(), sup_off.data(), sup_y.data(),
                                sup_free.data(), sup_matched.data()};
   }
+  // ClusterState::sum_abs_duals (ot.cpp:181-188)
+  int64_t sum_abs_duals() const {
+    int64_t t = 0;
+    for (size_t c = 0; c < dem_y.size(); ++c) {
+      int64_t cnt = dem_free[c];
+      for (int64_t f = flow_off[c]; f < flow_off[c + 1]; ++f) cnt += flow_cnt[f];
+      t += std::llabs(dem_y[c]) * cnt;
+    }
+    for (size_t c = 0; c < sup_y.size(); ++c) t += std::llabs(sup_y[c]) * (sup_free[c] + sup_matched[c]);
+    return t;
+  }
 };
-
-int64_t sum_abs_duals(const std::vector<std::vector<DemandC>>& dem,
-                      const std::vector<std::vector<SupplyC>>& sup) {  // ot.cpp:181-188
-  int64_t t = 0;
-  for (const auto& cs : dem)
-    for (const DemandC& c : cs) t += std::llabs(c.y) * c.count();
-  for (const auto& cs : sup)
-    for (const SupplyC& c : cs) t += std::llabs(c.y) * c.count();
-  return t;
-}
 
 // check_cluster_invariant (ot.cpp:190-265) on the flat form.
 std::vector<std::string> check_invariant(const otprg_cluster_state& st, const otprg_copy_instance& in) {
@@ -475,8 +319,7 @@ class OtSolver {
       build_costs_from_k();
       solve_copy_matching();
     } else {  // nothing to match: the loop ends at once (n_i = 0)
-      dem_.assign(n_a_, {});
-      sup_.assign(n_b_, {});
+      st_ = initial_state();
       flow_.assign(n_a_, {});
       tmp.full_match_termination = 1;
     }
@@ -521,26 +364,45 @@ class OtSolver {
   int64_t unit_ceil_ = 0;                // dual bound - 2 of the hooks' CopyInstance
   const int32_t* hk_ = nullptr;          // host k (copy instance / debug mode), row-major
   std::vector<int32_t> hk_store_;
-  std::vector<std::vector<DemandC>> dem_;
-  std::vector<std::vector<SupplyC>> sup_;
+  FlatState st_;                         // ClusterState exported from the device (hooks, final)
   std::vector<std::vector<std::pair<int32_t, int64_t>>> flow_;  // final sparse flow per a
 
   bool debug() const { return opt_ && (opt_->check_invariants || opt_->observer); }
 
-  int64_t k_of(int32_t a, int32_t b) const {
-    if (hk_) return hk_[static_cast<size_t>(a) * n_b_ + b];
-    return host_scaled_floor(p_->cost[static_cast<size_t>(a) * n_b_ + b], eps_in_);
-  }
 
   otprg_copy_instance copy_instance() const {
     return otprg_copy_instance{n_a_, n_b_, hk_, unit_ceil_, sm_.d.data(), sm_.s.data()};
   }
 
   // ClusterSolveResult::state (before completion) kept on the context.
-  void save_state() {
-    auto fs = std::make_shared<FlatState>();
-    fs->build(dem_, sup_);
-    ctx_->ot_state = fs;
+  void save_state() { ctx_->ot_state = std::make_shared<FlatState>(st_); }
+
+  // The state solve_copy_matching starts from (ot.cpp:430-437): one demand
+  // cluster at dual 0 with every copy free, one supply cluster at dual 1.
+  FlatState initial_state() const {
+    FlatState f;
+    f.n_a = n_a_;
+    f.n_b = n_b_;
+    f.dem_off.assign(1, 0);
+    f.flow_off.assign(1, 0);
+    f.sup_off.assign(1, 0);
+    for (int32_t a = 0; a < n_a_; ++a) {
+      if (sm_.d[a] > 0) {
+        f.dem_y.push_back(0);
+        f.dem_free.push_back(sm_.d[a]);
+        f.flow_off.push_back(0);
+      }
+      f.dem_off.push_back(static_cast<int32_t>(f.dem_y.size()));
+    }
+    for (int32_t b = 0; b < n_b_; ++b) {
+      if (sm_.s[b] > 0) {
+        f.sup_y.push_back(1);
+        f.sup_free.push_back(sm_.s[b]);
+        f.sup_matched.push_back(0);
+      }
+      f.sup_off.push_back(static_cast<int32_t>(f.sup_y.size()));
+    }
+    return f;
   }
 
   // scale_round_costs(costs, eps/3) on the device (core.cpp:34-53), kT[b][a].
@@ -574,7 +436,7 @@ class OtSolver {
     if (dstatus) throw OtError{OTPRG_PARAMETER, "OT cost entry outside [0,1]"};
     launches_ += 1;
     r_->build_ms = t.ms();
-    alloc_scan_buffers();
+    alloc_device();
   }
 
   // The copy instance's k (host int32, row-major) -> kT on the device.
@@ -600,270 +462,383 @@ class OtSolver {
     OT_CK(cudaStreamSynchronize(ctx_->stream), "k upload");
     launches_ += 1;
     r_->build_ms = t.ms();
-    alloc_scan_buffers();
+    alloc_device();
   }
 
-  void alloc_scan_buffers() {
-    // per-phase scan buffers: t0/t1 (2 x lda) + requests + candidates
-    OT_CK(ctx_->ot_t.ensure(2 * static_cast<size_t>(lda_) * width_), "alloc t");
-    OT_CK(ctx_->ot_req.ensure(static_cast<size_t>(n_b_) * sizeof(int4)), "alloc req");
-    OT_CK(ctx_->ot_out.ensure(static_cast<size_t>(n_b_) * (kCand * 4 + sizeof(int2))), "alloc out");
-    const size_t hp = static_cast<size_t>(lda_) * 2 * width_ + static_cast<size_t>(n_b_) * sizeof(int4) +
-                      static_cast<size_t>(n_b_) * (kCand * 4 + sizeof(int2)) + 64;
-    if (ctx_->ot_hpin_n < hp) {
+  // ---- device state (ot_device.cu) --------------------------------------------
+  // ctx->ot_dev[] slots
+  enum Buf {
+    bT, bDy, bDfree, bDmatched, bConsumed, bFlOff, bFlCode, bFlB, bFlCnt, bFlPre, bSy, bSfree, bSmatched,
+    bSfreed, bFb, bFy, bFpos, bFidx, bFu0, bFu, bAdmLen, bAdmOff, bAdm, bEk0, bEv0, bEk1, bEv1, bRk0, bRv0,
+    bRk1, bRv1, bCtr, bTemp, bScratch, bNum
+  };
+  otprg::OtDev D_{};
+  int64_t fl_cap_ = 0, adm_cap_ = 0, e_cap_ = 0, r_cap_ = 0;
+  size_t temp_cap_ = 0;
+  int launches_ = 0;
+  int64_t scan_bytes_ = 0;
+  int64_t* hctr_ = nullptr;  // pinned: counters + status
+
+  DevBuf& buf(Buf b) { return ctx_->ot_dev[b]; }
+  template <typename T>
+  T* ensure(Buf b, size_t n) {
+    OT_CK(buf(b).ensure(std::max<size_t>(n, 1) * sizeof(T)), "alloc OT device state");
+    return buf(b).as<T>();
+  }
+
+  void alloc_device() {
+    static_assert(bNum <= 40, "ot_dev slots");
+    if (n_b_ >= (1 << 21) - 1 || n_a_ >= (1 << 21) || unit_ceil_ + 4 >= (1 << 19))
+      throw OtError{OTPRG_PARAMETER, "OT instance beyond the device state's index range (n < 2^21, 1/eps < 2^19)"};
+    const size_t na2 = 2 * static_cast<size_t>(n_a_), nb = n_b_, nb2 = 2 * nb;
+    D_.n_a = n_a_;
+    D_.n_b = n_b_;
+    D_.lda = lda_;
+    D_.width = width_;
+    D_.kT = ctx_->kT.p;
+    D_.t = ensure<char>(bT, 2 * static_cast<size_t>(lda_) * width_);
+    D_.dy = ensure<int32_t>(bDy, na2);
+    D_.dfree = ensure<int64_t>(bDfree, na2);
+    D_.dmatched = ensure<int64_t>(bDmatched, na2);
+    D_.consumed = ensure<int64_t>(bConsumed, na2);
+    D_.fl_off = ensure<int64_t>(bFlOff, na2 + 1);
+    D_.sy = ensure<int32_t>(bSy, nb2);
+    D_.sfree = ensure<int64_t>(bSfree, nb2);
+    D_.smatched = ensure<int64_t>(bSmatched, nb2);
+    D_.sfreed = ensure<int64_t>(bSfreed, nb2);
+    D_.fb = ensure<int32_t>(bFb, nb);
+    D_.fy = ensure<int32_t>(bFy, nb);
+    D_.fpos = ensure<int32_t>(bFpos, nb);
+    D_.fidx = ensure<int32_t>(bFidx, nb);
+    D_.fu0 = ensure<int64_t>(bFu0, nb);
+    D_.fu = ensure<int64_t>(bFu, nb);
+    D_.adm_len = ensure<int64_t>(bAdmLen, nb + 1);
+    D_.adm_off = ensure<int64_t>(bAdmOff, nb + 1);
+    D_.ctr = ensure<int64_t>(bCtr, otprg::kCtrCount + 8);
+    D_.status = reinterpret_cast<int*>(D_.ctr + otprg::kCtrCount);
+    D_.err = reinterpret_cast<int32_t*>(D_.ctr + otprg::kCtrCount + 1);
+    fl_cap_ = adm_cap_ = e_cap_ = r_cap_ = 0;
+    grow_flows(na2);
+    if (ctx_->ot_hpin_n < 256) {
       if (ctx_->ot_hpin) cudaFreeHost(ctx_->ot_hpin);
       ctx_->ot_hpin = nullptr;
       ctx_->ot_hpin_n = 0;
-      OT_CK(cudaMallocHost(&ctx_->ot_hpin, hp), "pinned staging");
-      ctx_->ot_hpin_n = hp;
+      OT_CK(cudaMallocHost(&ctx_->ot_hpin, 256), "pinned staging");
+      ctx_->ot_hpin_n = 256;
+    }
+    hctr_ = static_cast<int64_t*>(ctx_->ot_hpin);
+  }
+
+  void grow_flows(int64_t n) {
+    if (n <= fl_cap_) return;
+    const int64_t c = std::max<int64_t>(n, fl_cap_ * 3 / 2);
+    // (a growth keeps nothing: called before the rebuild writes the new flows)
+    D_.fl_code = ensure<int32_t>(bFlCode, c);
+    D_.fl_b = ensure<int32_t>(bFlB, c);
+    D_.fl_cnt = ensure<int64_t>(bFlCnt, c);
+    D_.fl_pre = ensure<int64_t>(bFlPre, c);
+    fl_cap_ = c;
+  }
+
+  void grow(int64_t& cap, int64_t n, Buf k0, Buf v0, Buf k1, Buf v1, bool keep0) {
+    if (n <= cap) return;
+    const int64_t c = std::max<int64_t>(n, cap * 3 / 2);
+    if (keep0 && cap > 0) {  // the live prefix of buffer 0 moves along
+      DevBuf tk, tv;
+      OT_CK(tk.ensure(cap * 8), "alloc");
+      OT_CK(tv.ensure(cap * 8), "alloc");
+      OT_CK(cudaMemcpyAsync(tk.p, buf(k0).p, cap * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(tv.p, buf(v0).p, cap * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      ensure<unsigned long long>(k0, c);
+      ensure<int64_t>(v0, c);
+      OT_CK(cudaMemcpyAsync(buf(k0).p, tk.p, cap * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(buf(v0).p, tv.p, cap * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaStreamSynchronize(ctx_->stream), "grow");
+    } else {
+      ensure<unsigned long long>(k0, c);
+      ensure<int64_t>(v0, c);
+    }
+    ensure<unsigned long long>(k1, c);
+    ensure<int64_t>(v1, c);
+    cap = c;
+  }
+
+  void temp_need(size_t bytes) {
+    if (bytes > temp_cap_) {
+      ensure<char>(bTemp, bytes);
+      temp_cap_ = bytes;
+    }
+  }
+  void sort(const unsigned long long* kin, unsigned long long* kout, const int64_t* vin, int64_t* vout, int64_t n,
+            int end_bit) {
+    size_t tb = 0;
+    OT_CK(otprg::ot_sort_pairs(nullptr, tb, kin, kout, vin, vout, n, end_bit, ctx_->stream), "sort size");
+    temp_need(tb);
+    tb = temp_cap_;
+    OT_CK(otprg::ot_sort_pairs(buf(bTemp).p, tb, kin, kout, vin, vout, n, end_bit, ctx_->stream), "sort");
+    launches_ += 4;
+  }
+
+  // Counters / status to the host (one sync).
+  void read_ctr() {
+    OT_CK(cudaMemcpyAsync(hctr_, D_.ctr, (otprg::kCtrCount + 5) * 8, cudaMemcpyDeviceToHost, ctx_->stream), "D2H");
+    OT_CK(cudaStreamSynchronize(ctx_->stream), "OT phase");
+    check_status();
+  }
+  void check_status() {
+    const int* st = reinterpret_cast<const int*>(hctr_ + otprg::kCtrCount);
+    const int32_t* err = reinterpret_cast<const int32_t*>(hctr_ + otprg::kCtrCount + 1);
+    if (st[0] == 0) return;
+    switch (err[0]) {
+      case 1: throw OtError{OTPRG_INVARIANT, "third dual value among copies of demand vertex " + std::to_string(err[1])};
+      case 2: throw OtError{OTPRG_INVARIANT, "third dual value among copies of supply vertex " + std::to_string(err[1])};
+      case 3: throw OtError{OTPRG_INVARIANT, "displaced supply copy has no cluster"};
+      case 4: throw OtError{OTPRG_INVARIANT, "demand dual beyond the device storage at a=" + std::to_string(err[1])};
+      default: throw OtError{OTPRG_INVARIANT, "OT device state corrupt"};
     }
   }
 
-  int launches_ = 0;
-  int64_t scan_bytes_ = 0;
-  double prof_[4] = {0, 0, 0, 0};  // host ms: claim walk, state updates (OTPRG_OT_PROFILE)
-
-  // Scan requests on the device; results land in cand / meta (host views).
-  void scan(const std::vector<int4>& reqs, std::vector<int32_t>& cand, std::vector<int2>& meta) {
-    const int nreq = static_cast<int>(reqs.size());
-    cand.resize(static_cast<size_t>(nreq) * kCand);
-    meta.resize(nreq);
-    if (nreq == 0) return;
-    char* hp = static_cast<char*>(ctx_->ot_hpin);
-    const size_t tbytes = static_cast<size_t>(lda_) * 2 * width_;
-    int4* hreq = reinterpret_cast<int4*>(hp + ((tbytes + 15) & ~15ull));
-    int32_t* hcand = reinterpret_cast<int32_t*>(hreq + n_b_);
-    int2* hmeta = reinterpret_cast<int2*>(hcand + static_cast<size_t>(n_b_) * kCand);
-    std::memcpy(hreq, reqs.data(), nreq * sizeof(int4));
-    OT_CK(cudaMemcpyAsync(ctx_->ot_req.p, hreq, nreq * sizeof(int4), cudaMemcpyHostToDevice,
-                          ctx_->stream), "H2D requests");
-    int32_t* dcand = ctx_->ot_out.as<int32_t>();
-    int2* dmeta = reinterpret_cast<int2*>(dcand + static_cast<size_t>(n_b_) * kCand);
-    const void* t0 = ctx_->ot_t.p;
-    const void* t1 = static_cast<const char*>(ctx_->ot_t.p) + static_cast<size_t>(lda_) * width_;
-    OT_CK(otprg::launch_ot_scan(ctx_->kT.p, lda_, width_, t0, t1, ctx_->ot_req.as<int4>(), nreq, kCand,
-                                dcand, dmeta, ctx_->stream), "ot_scan launch");
-    launches_ += 1;
-    OT_CK(cudaMemcpyAsync(hcand, dcand, static_cast<size_t>(nreq) * kCand * 4, cudaMemcpyDeviceToHost,
-                          ctx_->stream), "D2H candidates");
-    OT_CK(cudaMemcpyAsync(hmeta, dmeta, nreq * sizeof(int2), cudaMemcpyDeviceToHost, ctx_->stream),
-          "D2H meta");
-    OT_CK(cudaStreamSynchronize(ctx_->stream), "ot scan");
-    std::memcpy(cand.data(), hcand, static_cast<size_t>(nreq) * kCand * 4);
-    std::memcpy(meta.data(), hmeta, nreq * sizeof(int2));
-    scan_bytes_ += static_cast<int64_t>(nreq) * lda_ * width_;
-  }
-
-  // Cluster duals of every demand vertex to the device: t_ci = -y (type max if absent).
-  void upload_cluster_duals() {
-    char* hp = static_cast<char*>(ctx_->ot_hpin);
-    const uint32_t none = width_ == 1 ? 0xffu : width_ == 2 ? 0xffffu : 0xffffffffu;
-    const int64_t tmax = otprg::storage_tmax(width_);
-    auto put = [&](size_t i, uint32_t v) {
-      if (width_ == 1) reinterpret_cast<uint8_t*>(hp)[i] = static_cast<uint8_t>(v);
-      else if (width_ == 2) reinterpret_cast<uint16_t*>(hp)[i] = static_cast<uint16_t>(v);
-      else reinterpret_cast<uint32_t*>(hp)[i] = v;
-    };
-    for (int32_t a = 0; a < lda_; ++a) {
-      uint32_t v0 = none, v1 = none;
-      if (a < n_a_) {
-        const auto& cs = dem_[a];
-        if (cs.size() >= 1) v0 = static_cast<uint32_t>(-cs[0].y);
-        if (cs.size() >= 2) v1 = static_cast<uint32_t>(-cs[1].y);
-        if ((cs.size() >= 1 && -cs[0].y > tmax) || (cs.size() >= 2 && -cs[1].y > tmax))
-          throw OtError{OTPRG_INVARIANT, "demand dual beyond the device storage at a=" + std::to_string(a)};
+  // Initial state (ot.cpp:430-437) to the device.
+  void upload_initial() {
+    const size_t na2 = 2 * static_cast<size_t>(n_a_), nb2 = 2 * static_cast<size_t>(n_b_);
+    std::vector<int32_t> dy(na2, INT32_MIN), sy(nb2, INT32_MIN), code, fb;
+    std::vector<int64_t> dfree(na2, 0), dz(na2, 0), sfree(nb2, 0), sz(nb2, 0), off(na2 + 1, 0), cnt, pre;
+    for (int32_t a = 0; a < n_a_; ++a) {
+      off[2 * a] = static_cast<int64_t>(code.size());
+      if (sm_.d[a] > 0) {
+        dy[2 * a] = 0;
+        dfree[2 * a] = sm_.d[a];
+        code.push_back(2 * a);
+        fb.push_back(otprg::kFreeB);
+        cnt.push_back(sm_.d[a]);
+        pre.push_back(0);
       }
-      put(a, v0);
-      put(static_cast<size_t>(lda_) + a, v1);
+      off[2 * a + 1] = static_cast<int64_t>(code.size());
     }
-    OT_CK(cudaMemcpyAsync(ctx_->ot_t.p, hp, static_cast<size_t>(lda_) * 2 * width_,
-                          cudaMemcpyHostToDevice, ctx_->stream), "H2D cluster duals");
+    off[na2] = static_cast<int64_t>(code.size());
+    for (int32_t b = 0; b < n_b_; ++b)
+      if (sm_.s[b] > 0) {
+        sy[2 * b] = 1;
+        sfree[2 * b] = sm_.s[b];
+      }
+    grow_flows(static_cast<int64_t>(code.size()));
+    cudaStream_t s = ctx_->stream;
+    auto up = [&](void* d, const void* h, size_t bytes) {
+      if (bytes) OT_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "H2D OT state");
+    };
+    up(D_.dy, dy.data(), na2 * 4);
+    up(D_.dfree, dfree.data(), na2 * 8);
+    up(D_.dmatched, dz.data(), na2 * 8);
+    up(D_.consumed, dz.data(), na2 * 8);
+    up(D_.fl_off, off.data(), (na2 + 1) * 8);
+    up(D_.fl_code, code.data(), code.size() * 4);
+    up(D_.fl_b, fb.data(), fb.size() * 4);
+    up(D_.fl_cnt, cnt.data(), cnt.size() * 8);
+    up(D_.fl_pre, pre.data(), pre.size() * 8);
+    up(D_.sy, sy.data(), nb2 * 4);
+    up(D_.sfree, sfree.data(), nb2 * 8);
+    up(D_.smatched, sz.data(), nb2 * 8);
+    up(D_.sfreed, sz.data(), nb2 * 8);
+    OT_CK(cudaMemsetAsync(D_.ctr, 0, (otprg::kCtrCount + 5) * 8, s), "memset");
+    n_flows_ = static_cast<int64_t>(code.size());
+  }
+  int64_t n_flows_ = 0;
+
+  // The device ClusterState as a flat host state (dem clusters in slot order).
+  FlatState export_state() {
+    const size_t na2 = 2 * static_cast<size_t>(n_a_), nb2 = 2 * static_cast<size_t>(n_b_);
+    std::vector<int32_t> dy(na2), sy(nb2), fb(n_flows_);
+    std::vector<int64_t> dfree(na2), dmatched(na2), off(na2 + 1), cnt(n_flows_), sfree(nb2), smatched(nb2);
+    cudaStream_t s = ctx_->stream;
+    auto down = [&](void* h, const void* d, size_t bytes) {
+      if (bytes) OT_CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "D2H OT state");
+    };
+    down(dy.data(), D_.dy, na2 * 4);
+    down(dfree.data(), D_.dfree, na2 * 8);
+    down(dmatched.data(), D_.dmatched, na2 * 8);
+    down(off.data(), D_.fl_off, (na2 + 1) * 8);
+    down(fb.data(), D_.fl_b, n_flows_ * 4);
+    down(cnt.data(), D_.fl_cnt, n_flows_ * 8);
+    down(sy.data(), D_.sy, nb2 * 4);
+    down(sfree.data(), D_.sfree, nb2 * 8);
+    down(smatched.data(), D_.smatched, nb2 * 8);
+    OT_CK(cudaStreamSynchronize(s), "OT state export");
+    FlatState f;
+    f.n_a = n_a_;
+    f.n_b = n_b_;
+    f.dem_off.assign(1, 0);
+    f.flow_off.assign(1, 0);
+    f.sup_off.assign(1, 0);
+    for (int32_t a = 0; a < n_a_; ++a) {
+      for (int sl = 0; sl < 2; ++sl) {
+        const size_t c = 2 * static_cast<size_t>(a) + sl;
+        if (dfree[c] + dmatched[c] == 0) continue;
+        f.dem_y.push_back(dy[c]);
+        f.dem_free.push_back(dfree[c]);
+        for (int64_t e = off[c]; e < off[c + 1]; ++e)
+          if (fb[e] != otprg::kFreeB) {
+            f.flow_b.push_back(fb[e]);
+            f.flow_cnt.push_back(cnt[e]);
+          }
+        f.flow_off.push_back(static_cast<int64_t>(f.flow_b.size()));
+      }
+      f.dem_off.push_back(static_cast<int32_t>(f.dem_y.size()));
+    }
+    for (int32_t b = 0; b < n_b_; ++b) {
+      for (int sl = 0; sl < 2; ++sl) {
+        const size_t c = 2 * static_cast<size_t>(b) + sl;
+        if (sfree[c] + smatched[c] == 0) continue;
+        f.sup_y.push_back(sy[c]);
+        f.sup_free.push_back(sfree[c]);
+        f.sup_matched.push_back(smatched[c]);
+      }
+      f.sup_off.push_back(static_cast<int32_t>(f.sup_y.size()));
+    }
+    return f;
   }
 
-  // solve_copy_matching (ot.cpp:418-637).
+  // Greedy maximality (ot.cpp:524-533, check_invariants only): a supply vertex
+  // left with free copies must have found every admissible cluster used up.
+  void check_maximality(int32_t n_free) {
+    std::vector<int64_t> len(n_free), off(n_free), fu(n_free), cons(2 * static_cast<size_t>(n_a_)),
+        dfree(cons.size()), dmatched(cons.size());
+    cudaStream_t s = ctx_->stream;
+    OT_CK(cudaMemcpyAsync(len.data(), D_.adm_len, n_free * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(off.data(), D_.adm_off, n_free * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(fu.data(), D_.fu, n_free * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(cons.data(), D_.consumed, cons.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(dfree.data(), D_.dfree, cons.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaMemcpyAsync(dmatched.data(), D_.dmatched, cons.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    const int64_t total = n_free ? off[n_free - 1] + len[n_free - 1] : 0;
+    std::vector<int32_t> adm(total);
+    if (total) OT_CK(cudaMemcpyAsync(adm.data(), D_.adm, total * 4, cudaMemcpyDeviceToHost, s), "D2H");
+    OT_CK(cudaStreamSynchronize(s), "maximality check");
+    for (int32_t i = 0; i < n_free; ++i) {
+      if (fu[i] == 0) continue;
+      for (int64_t e = off[i]; e < off[i] + len[i]; ++e)
+        if (dfree[adm[e]] + dmatched[adm[e]] - cons[adm[e]] > 0)
+          throw OtError{OTPRG_INVARIANT, "greedy step left an admissible pair unmatched"};
+    }
+  }
+
+  // solve_copy_matching (ot.cpp:418-637): the phases on the device.
   void solve_copy_matching() {
-    dem_.assign(n_a_, {});
-    sup_.assign(n_b_, {});
-    for (int32_t a = 0; a < n_a_; ++a)
-      if (sm_.d[a] > 0) dem_[a].push_back(DemandC{0, sm_.d[a], {}});
-    for (int32_t b = 0; b < n_b_; ++b)
-      if (sm_.s[b] > 0) sup_[b].push_back(SupplyC{1, sm_.s[b], 0});
+    upload_initial();
     const double threshold = eps_in_ * static_cast<double>(sm_.total_s);
     const int64_t phase_cap =
         static_cast<int64_t>(std::ceil((1.0 + 2.0 * eps_in_) / (eps_in_ * eps_in_))) + 8;
-
-    std::vector<std::array<Cursor, 2>> cur(n_a_);
-    std::vector<int64_t> avail(2 * static_cast<size_t>(n_a_));
-    std::vector<int64_t> matched_from_b(n_b_), remaining_free(n_b_), free_dual(n_b_);
-    std::vector<std::vector<std::pair<int64_t, int64_t>>> freed_at(n_b_);
-    std::vector<int32_t> free_bs;
-    std::vector<int4> reqs;
-    std::vector<int32_t> cand;
-    std::vector<int2> meta;
-    std::vector<Claim> claims;
-    std::vector<std::pair<int32_t, int64_t>> displaced;
-    int64_t phases = 0, sum_ni = 0;
+    cudaStream_t s = ctx_->stream;
+    int64_t phases = 0, sum_ni = 0, rounds_total = 0;
     std::vector<int64_t> free_counts;
     Timer loop_t;
-    double scan_ms = 0.0;
-
+    int* scratch = ensure<int>(bScratch, 256);
+    if (debug()) st_ = export_state();
     while (true) {
-      int64_t n_i = 0;
-      for (const auto& cs : sup_)
-        for (const SupplyC& c : cs) n_i += c.free;
+      // free list + n_i (one sync: the termination test, ot.cpp:442-446)
+      OT_CK(cudaMemsetAsync(D_.ctr, 0, otprg::kCtrCount * 8, s), "memset");
+      OT_CK(otprg::ot_dev_free_list(D_, scratch, s), "free list");
+      launches_ += 2;
+      read_ctr();
+      const int64_t n_i = hctr_[otprg::kCtrNi];
+      const int32_t n_free = static_cast<int32_t>(hctr_[otprg::kCtrFree]);
       if (static_cast<double>(n_i) <= threshold) {
         r_->full_match_termination = (n_i == 0);
         break;
       }
-      const int32_t stamp = static_cast<int32_t>(phases);
-      const int64_t sum_before = opt_ && opt_->observer ? sum_abs_duals(dem_, sup_) : 0;
-
-      // free supply vertices (ascending) and their free-copy duals
-      free_bs.clear();
-      reqs.clear();
-      for (int32_t b = 0; b < n_b_; ++b) {
-        int64_t free_b = 0, y_b = 0;
-        for (const SupplyC& c : sup_[b])
-          if (c.free > 0) {
-            free_b += c.free;
-            y_b = c.y;
-          }
-        remaining_free[b] = free_b;
-        free_dual[b] = y_b;
-        matched_from_b[b] = 0;
-        freed_at[b].clear();
-        if (free_b == 0) continue;
-        free_bs.push_back(b);
-        reqs.push_back(make_int4(b, static_cast<int>(y_b - 1), 0, 0));
+      const int64_t sum_before = opt_ && opt_->observer ? st_.sum_abs_duals() : 0;
+      // admissible clusters of every free b: count, offsets, fill
+      OT_CK(otprg::ot_dev_t(D_, s), "cluster duals");
+      OT_CK(otprg::ot_dev_adm(D_, 0, s), "admissible count");
+      OT_CK(cudaMemsetAsync(D_.adm_len + n_free, 0, 8, s), "memset");
+      {
+        size_t tb = 0;
+        OT_CK(otprg::ot_exclusive_sum(nullptr, tb, D_.adm_len, D_.adm_off, n_free + 1, s), "scan size");
+        temp_need(tb);
+        tb = temp_cap_;
+        OT_CK(otprg::ot_exclusive_sum(buf(bTemp).p, tb, D_.adm_len, D_.adm_off, n_free + 1, s), "scan");
       }
-      Timer st;
-      upload_cluster_duals();
-      scan(reqs, cand, meta);
-      scan_ms += st.ms();
-
-      Timer tc;
-      // copies of every demand cluster still claimable this phase, by scan code 2a + ci
-      for (int32_t a = 0; a < n_a_; ++a) {
-        const auto& cs = dem_[a];
-        avail[2 * a] = cs.size() >= 1 ? cs[0].count() : 0;
-        avail[2 * a + 1] = cs.size() >= 2 ? cs[1].count() : 0;
+      int64_t adm_total = 0;
+      OT_CK(cudaMemcpyAsync(&hctr_[otprg::kCtrCount + 4], D_.adm_off + n_free, 8, cudaMemcpyDeviceToHost, s), "D2H");
+      OT_CK(cudaStreamSynchronize(s), "admissible count");
+      adm_total = hctr_[otprg::kCtrCount + 4];
+      if (adm_total > adm_cap_) {
+        adm_cap_ = std::max<int64_t>(adm_total, adm_cap_ * 3 / 2);
+        D_.adm = ensure<int32_t>(bAdm, adm_cap_);
       }
-      // claim step (ot.cpp:471-522): b ascending, admissible clusters ascending a
-      claims.clear();
-      displaced.clear();
-      std::vector<int32_t> more;
-      std::vector<int2> more_meta;
-      for (size_t q = 0; q < free_bs.size(); ++q) {
-        const int32_t b = free_bs[q];
-        int64_t remaining = remaining_free[b];
-        const int32_t* list = cand.data() + q * kCand;
-        int cnt = meta[q].x, resume = meta[q].y;
-        int idx = 0;
-        while (remaining > 0) {
-          if (idx == cnt) {
-            if (resume < 0) break;  // row exhausted
-            std::vector<int4> one{make_int4(b, static_cast<int>(free_dual[b] - 1), resume, 0)};
-            scan(one, more, more_meta);
-            list = more.data();
-            cnt = more_meta[0].x;
-            resume = more_meta[0].y;
-            idx = 0;
-            continue;
-          }
-          const int32_t code = list[idx++];
-          if (avail[code] == 0) continue;  // used up this phase (flat filter: no cluster access)
-          const int32_t a = code >> 1, ci = code & 1;
-          DemandC& c = dem_[a][ci];
-          Cursor& cu = cur[a][ci];
-          if (cu.stamp != stamp) cu = Cursor{stamp, 0, 0, 0};
-          const int64_t total = c.free + c.matched() - cu.used;
-          if (total == 0) continue;
-          const int64_t take = std::min(remaining, total);
-          Claim cl{a, ci, b, 0, take, displaced.size(), 0};
-          const int64_t free_left = std::max<int64_t>(0, c.free - cu.used);
-          cl.take_free = std::min(take, free_left);
-          int64_t rest = take - cl.take_free;
-          while (rest > 0) {  // matched copies ascending by partner
-            const auto& e = c.flow[cu.fidx];
-            const int64_t use = std::min(e.second - cu.foff, rest);
-            if (use > 0) displaced.emplace_back(e.first, use);
-            cu.foff += use;
-            rest -= use;
-            if (cu.foff == e.second) {
-              ++cu.fidx;
-              cu.foff = 0;
-            }
-          }
-          cu.used += take;
-          avail[code] -= take;
-          cl.disp_end = displaced.size();
-          claims.push_back(cl);
-          remaining -= take;
-        }
-        matched_from_b[b] = remaining_free[b] - remaining;
-        remaining_free[b] = remaining;
+      OT_CK(otprg::ot_dev_adm(D_, 1, s), "admissible fill");
+      launches_ += 5;
+      scan_bytes_ += 2 * static_cast<int64_t>(n_free) * lda_ * width_;
+      // claims (K10): deferred-acceptance rounds; entries live in buffers 0
+      grow(e_cap_, std::max<int64_t>(adm_total + n_free, 1), bEk0, bEv0, bEk1, bEv1, false);
+      D_.e_key = buf(bEk0).as<unsigned long long>();
+      D_.e_val = buf(bEv0).as<int64_t>();
+      int64_t n_e = 0;
+      const int end_bit = 32 + 1 + static_cast<int>(std::ceil(std::log2(2.0 * n_a_ + 1.0)));
+      while (true) {
+        OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrNew], 0, 8, s), "memset");
+        OT_CK(otprg::ot_dev_propose(D_, s), "propose");
+        read_ctr();
+        const int64_t n_new = hctr_[otprg::kCtrNew];
+        n_e = hctr_[otprg::kCtrE];
+        if (n_new == 0) break;
+        const int64_t n = n_e + n_new;
+        sort(buf(bEk0).as<unsigned long long>(), buf(bEk1).as<unsigned long long>(), buf(bEv0).as<int64_t>(),
+             buf(bEv1).as<int64_t>(), n, std::min(64, end_bit));
+        OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrE], 0, 8, s), "memset");
+        OT_CK(otprg::ot_dev_resolve(D_, buf(bEk1).as<unsigned long long>(), buf(bEv1).as<int64_t>(), n,
+                                    buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), s),
+              "resolve");
+        launches_ += 2;
+        ++rounds_total;
       }
+      // updates (K11): consumed copies, displaced partners, records of the next state
+      const int64_t rec_need = n_flows_ + n_e + 2 * static_cast<int64_t>(n_a_) + 16;
+      grow(r_cap_, rec_need, bRk0, bRv0, bRk1, bRv1, false);
+      D_.r_key = buf(bRk0).as<unsigned long long>();
+      D_.r_val = buf(bRv0).as<int64_t>();
       if (opt_ && opt_->check_invariants) {
-        // greedy maximality (ot.cpp:524-533): a supply vertex keeps free
-        // copies only when every admissible demand cluster was used up
-        for (int32_t b : free_bs) {
-          if (remaining_free[b] == 0) continue;
-          for (int32_t a = 0; a < n_a_; ++a)
-            for (size_t ci = 0; ci < dem_[a].size() && ci < 2; ++ci) {
-              const DemandC& c = dem_[a][ci];
-              const Cursor& cu = cur[a][ci];
-              const int64_t avail = c.free + c.matched() - (cu.stamp == stamp ? cu.used : 0);
-              if (c.y == k_of(a, b) + 1 - free_dual[b] && avail > 0)
-                throw OtError{OTPRG_INVARIANT, "greedy step left an admissible pair unmatched"};
-            }
-        }
+        OT_CK(otprg::ot_dev_consumed(D_, buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), n_e, s),
+              "consumed");
+        check_maximality(n_free);
+      } else {
+        OT_CK(otprg::ot_dev_consumed(D_, buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), n_e, s),
+              "consumed");
       }
-
-      prof_[0] += tc.ms();
-      Timer tu;
-      // supply side: claimed copies become matched at their dual, the
-      // phase's leftover free copies go up a unit (ot.cpp:540-553)
-      for (int32_t b : free_bs) {
-        for (SupplyC& c : sup_[b]) {
-          if (c.free == 0) continue;
-          c.free = 0;
-          c.matched += matched_from_b[b];
-        }
-        if (remaining_free[b] > 0) supply_at(sup_[b], free_dual[b] + 1).free += remaining_free[b];
+      OT_CK(otprg::ot_dev_records(D_, buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), n_e, s),
+            "records");
+      launches_ += 4;
+      read_ctr();
+      const int64_t n_rec = hctr_[otprg::kCtrRec];
+      sort(buf(bRk0).as<unsigned long long>(), buf(bRk1).as<unsigned long long>(), buf(bRv0).as<int64_t>(),
+           buf(bRv1).as<int64_t>(), n_rec, 63);
+      {
+        long long* d_nu = reinterpret_cast<long long*>(&D_.ctr[otprg::kCtrCount + 4]);
+        size_t tb = 0;
+        OT_CK(otprg::ot_reduce_by_key(nullptr, tb, buf(bRk1).as<unsigned long long>(),
+                                      buf(bRk0).as<unsigned long long>(), buf(bRv1).as<int64_t>(),
+                                      buf(bRv0).as<int64_t>(), d_nu, n_rec, s),
+              "reduce size");
+        temp_need(tb);
+        tb = temp_cap_;
+        OT_CK(otprg::ot_reduce_by_key(buf(bTemp).p, tb, buf(bRk1).as<unsigned long long>(),
+                                      buf(bRk0).as<unsigned long long>(), buf(bRv1).as<int64_t>(),
+                                      buf(bRv0).as<int64_t>(), d_nu, n_rec, s),
+              "reduce");
       }
-      // demand side + displaced supply copies (ot.cpp:556-578)
-      for (const Claim& cl : claims) {
-        DemandC& src = dem_[cl.a][cl.ci];
-        src.free -= cl.take_free;
-        for (size_t i = cl.disp_begin; i < cl.disp_end; ++i) {
-          const int32_t b_old = displaced[i].first;
-          const int64_t cnt = displaced[i].second;
-          dflow_sub(src, b_old, cnt);
-          const int64_t y_old = k_of(cl.a, b_old) - src.y;
-          bool found = false;
-          for (SupplyC& c : sup_[b_old])
-            if (c.y == y_old && c.matched >= cnt) {
-              c.matched -= cnt;
-              found = true;
-              break;
-            }
-          if (!found) throw OtError{OTPRG_INVARIANT, "displaced supply copy has no cluster"};
-          freed_at[b_old].emplace_back(y_old, cnt);
-        }
-        const int64_t dst_y = src.y - 1;
-        dflow_add(demand_at(dem_[cl.a], dst_y), cl.b, cl.total);
-      }
-      for (int32_t b = 0; b < n_b_; ++b) {
-        for (const auto& [y_old, cnt] : freed_at[b]) supply_at(sup_[b], y_old).free += cnt;
-        normalize_supply(sup_[b], b);
-      }
-      for (int32_t a = 0; a < n_a_; ++a) normalize_demand(dem_[a], a);
-      prof_[1] += tu.ms();
-
+      read_ctr();
+      n_flows_ = hctr_[otprg::kCtrCount + 4];
+      grow_flows(n_flows_);
+      OT_CK(otprg::ot_dev_rebuild(D_, buf(bRk0).as<unsigned long long>(), buf(bRv0).as<int64_t>(), n_flows_, s),
+            "rebuild");
+      launches_ += 4;
       phases += 1;
       free_counts.push_back(n_i);
       sum_ni += n_i;
-      if (debug()) phase_hooks(phases, n_i, sum_before);
+      if (debug()) {
+        read_ctr();  // the rebuild's normalisation checks
+        st_ = export_state();
+        phase_hooks(phases, n_i, sum_before);
+      }
       if (phases > phase_cap)
         throw OtError{OTPRG_INVARIANT, "phase count exceeded the proven bound; solver state is corrupt"};
     }
@@ -872,37 +847,54 @@ class OtSolver {
     if (r_->free_counts && r_->free_cap > 0)
       std::memcpy(r_->free_counts, free_counts.data(),
                   static_cast<size_t>(std::min<int64_t>(phases, r_->free_cap)) * 8);
+    st_ = export_state();
     r_->loop_ms = loop_t.ms();
     if (std::getenv("OTPRG_OT_PROFILE"))
-      std::fprintf(stderr, "ot loop %.2f ms: scan %.2f claim %.2f update %.2f\n", r_->loop_ms, scan_ms, prof_[0],
-                   prof_[1]);
-    r_->scan_ms = scan_ms;
+      std::fprintf(stderr, "ot loop %.2f ms: %lld phases, %lld DA rounds\n", r_->loop_ms, (long long)phases,
+                   (long long)rounds_total);
+    r_->scan_ms = 0.0;
     r_->bytes_touched = scan_bytes_;
     r_->gpu_launches = launches_;
+    complete();
+  }
 
-    // flow matrix (sparse, per a ascending b) + completion (ot.cpp:615-635)
+  // Flow matrix (sparse, per a ascending b) + completion (ot.cpp:615-635): the
+  // leftover free supply copies go to spare demand copies, both ascending.
+  void complete() {
+    const FlatState& f = st_;
     flow_.assign(n_a_, {});
-    for (int32_t a = 0; a < n_a_; ++a)
-      for (const DemandC& c : dem_[a])
-        for (const auto& e : c.flow) flow_add(flow_[a], e.first, e.second);
+    std::vector<int64_t> spare(n_a_, 0);
+    for (int32_t a = 0; a < n_a_; ++a) {
+      auto& row = flow_[a];
+      for (int32_t c = f.dem_off[a]; c < f.dem_off[a + 1]; ++c) {
+        spare[a] += f.dem_free[c];
+        for (int64_t e = f.flow_off[c]; e < f.flow_off[c + 1]; ++e) row.emplace_back(f.flow_b[e], f.flow_cnt[e]);
+      }
+      // (two clusters: merge their b-ascending lists)
+      std::sort(row.begin(), row.end());
+      size_t w = 0;
+      for (size_t r = 0; r < row.size(); ++r) {
+        if (w > 0 && row[w - 1].first == row[r].first) row[w - 1].second += row[r].second;
+        else row[w++] = row[r];
+      }
+      row.resize(w);
+    }
     int32_t a_cursor = 0;
-    auto free_demand_of = [&](int32_t a) {
-      int64_t t = 0;
-      for (const DemandC& c : dem_[a]) t += c.free;
-      return t;
-    };
-    int64_t a_spare = n_a_ > 0 ? free_demand_of(0) : 0;
+    int64_t a_spare = n_a_ > 0 ? spare[0] : 0;
     for (int32_t b = 0; b < n_b_; ++b) {
       int64_t need = 0;
-      for (const SupplyC& c : sup_[b]) need += c.free;
+      for (int32_t c = f.sup_off[b]; c < f.sup_off[b + 1]; ++c) need += f.sup_free[c];
       while (need > 0) {
         while (a_spare == 0) {
           ++a_cursor;
           if (a_cursor >= n_a_) throw OtError{OTPRG_INVARIANT, "completion ran out of demand copies"};
-          a_spare = free_demand_of(a_cursor);
+          a_spare = spare[a_cursor];
         }
         const int64_t take = std::min(need, a_spare);
-        flow_add(flow_[a_cursor], b, take);
+        auto& row = flow_[a_cursor];
+        auto it = std::lower_bound(row.begin(), row.end(), std::make_pair(b, int64_t{0}));
+        if (it != row.end() && it->first == b) it->second += take;
+        else row.insert(it, {b, take});
         need -= take;
         a_spare -= take;
       }
@@ -911,9 +903,7 @@ class OtSolver {
 
   // check_invariants / observer after a phase (ot.cpp:594-608).
   void phase_hooks(int64_t phase, int64_t n_i, int64_t sum_before) {
-    FlatState fs;
-    fs.build(dem_, sup_);
-    const otprg_cluster_state st = fs.view();
+    const otprg_cluster_state st = st_.view();
     const otprg_copy_instance in = copy_instance();
     if (opt_->check_invariants) {
       for (int which = 0; which < 2; ++which) {
@@ -922,7 +912,7 @@ class OtSolver {
       }
     }
     if (opt_->observer) {
-      const otprg_cluster_snapshot snap{phase, n_i, sum_before, sum_abs_duals(dem_, sup_), in, st};
+      const otprg_cluster_snapshot snap{phase, n_i, sum_before, st_.sum_abs_duals(), in, st};
       if (opt_->observer(&snap, opt_->user) != 0)
         throw OtError{OTPRG_ABORTED, "observer stopped the solve at phase " + std::to_string(phase)};
     }
