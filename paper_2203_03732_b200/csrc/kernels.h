@@ -172,6 +172,7 @@ struct OtDev {
   int64_t* dfree;
   int64_t* dmatched;
   int64_t* consumed;   // copies given this phase
+  int32_t* cl_cut;     // DA: highest holder list index of a full cluster (INT_MAX: room)
   // flows: CSR by code, entries ascending b then the free-copy sentinel (b = kFreeB)
   int64_t* fl_off;     // [2 n_a + 1]
   int32_t* fl_code;
@@ -205,6 +206,7 @@ struct OtDev {
 cudaError_t ot_dev_free_list(OtDev& D, int* scratch, cudaStream_t s);
 cudaError_t ot_dev_t(OtDev& D, cudaStream_t s);
 cudaError_t ot_dev_adm(OtDev& D, int pass, cudaStream_t s);
+cudaError_t ot_dev_cut_init(OtDev& D, cudaStream_t s);
 cudaError_t ot_dev_propose(OtDev& D, cudaStream_t s);
 cudaError_t ot_dev_resolve(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
                            unsigned long long* out_key, int64_t* out_val, cudaStream_t s);

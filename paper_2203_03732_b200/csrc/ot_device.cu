@@ -211,18 +211,31 @@ __global__ void __launch_bounds__(256) ot_adm_kernel(OtDev D) {
 }
 
 // ---- deferred acceptance -------------------------------------------------------
-// Entries: key = (code << 32) | list index, value = copies.
+// Entries: key = (code << 21) | list index, value = copies.
+// cl_cut[c]: when cluster c is full, the highest list index among its holders
+// (-1: capacity 0); INT_MAX while it has room.  A b above the cut would be
+// rejected there, so it skips the cluster without a round (the cut only falls
+// once set, so a stale value only skips less).
+__global__ void ot_cut_init_kernel(OtDev D) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 2 * D.n_a; c += gridDim.x * blockDim.x)
+    D.cl_cut[c] = D.dfree[c] + D.dmatched[c] > 0 ? INT_MAX : -1;
+}
+
 __global__ void ot_da_propose_kernel(OtDev D) {
   const int nf = D.ctr[kCtrFree];
   const long long base = D.ctr[kCtrE];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
     const int64_t u = D.fu[i];
     if (u <= 0) continue;
-    const int p = D.fpos[i];
-    if (p >= D.adm_len[i]) continue;  // admissible set exhausted: these copies stay free
-    const int code = D.adm[D.adm_off[i] + p];
+    int p = D.fpos[i];
+    const int len = (int)D.adm_len[i];
+    const int32_t* list = D.adm + D.adm_off[i];
+    while (p < len && __ldcg(&D.cl_cut[list[p]]) < i) ++p;  // full of lower b's: rejected anyway
+    D.fpos[i] = p;
+    if (p >= len) continue;  // admissible set exhausted: these copies stay free
+    const int code = list[p];
     const long long slot = base + atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrNew]), 1ull);
-    D.e_key[slot] = ((unsigned long long)(uint32_t)code << 32) | (uint32_t)i;
+    D.e_key[slot] = ((unsigned long long)(uint32_t)code << 21) | (uint32_t)i;
     D.e_val[slot] = u;
     D.fu[i] = 0;
   }
@@ -238,15 +251,16 @@ __global__ void ot_da_resolve_kernel(OtDev D, const unsigned long long* __restri
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
     const unsigned long long kj = key[j];
     if (j + 1 < n && key[j + 1] == kj) continue;  // the run's last entry carries it
-    const uint32_t code = (uint32_t)(kj >> 32);
-    const int i = (int)(uint32_t)kj;
+    const uint32_t code = (uint32_t)(kj >> 21);
+    const int i = (int)(kj & ((1u << 21) - 1));
     int64_t amt = val[j], pre = 0;
     long long q = j - 1;
     for (; q >= 0 && key[q] == kj; --q) amt += val[q];
-    for (; q >= 0 && (uint32_t)(key[q] >> 32) == code; --q) pre += val[q];
+    for (; q >= 0 && (uint32_t)(key[q] >> 21) == code; --q) pre += val[q];
     const int64_t cap = D.dfree[code] + D.dmatched[code];
     const int64_t acc = max((int64_t)0, min(amt, cap - pre));
     const int64_t rej = amt - acc;
+    if (acc > 0 && pre + acc == cap) D.cl_cut[code] = i;  // full: holders up to list index i
     if (rej > 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(&D.fu[i]), (unsigned long long)rej);
       const int p = D.fpos[i];
@@ -265,7 +279,7 @@ __global__ void ot_da_resolve_kernel(OtDev D, const unsigned long long* __restri
 __global__ void ot_consumed_kernel(OtDev D, const unsigned long long* __restrict__ key,
                                    const int64_t* __restrict__ val, long long n) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&D.consumed[key[j] >> 32]), (unsigned long long)val[j]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&D.consumed[key[j] >> 21]), (unsigned long long)val[j]);
 }
 
 // Records of the next state, key (a, descending y, b), b = kFreeB for free
@@ -320,7 +334,7 @@ __global__ void ot_flow_records_kernel(OtDev D) {
 __global__ void ot_claim_records_kernel(OtDev D, const unsigned long long* __restrict__ key,
                                         const int64_t* __restrict__ val, long long n) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
-    const int code = (int)(key[j] >> 32), i = (int)(uint32_t)key[j];
+    const int code = (int)(key[j] >> 21), i = (int)(key[j] & ((1u << 21) - 1));
     put_rec(D, code >> 1, D.dy[code] - 1, D.fb[i], val[j]);
   }
 }
@@ -493,6 +507,11 @@ cudaError_t ot_dev_adm(OtDev& D, int pass, cudaStream_t s) {
     else ot_adm_kernel<decltype(tag), 1><<<148 * 8, 256, 0, s>>>(D);
     return 0;
   });
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_cut_init(OtDev& D, cudaStream_t s) {
+  ot_cut_init_kernel<<<(2 * D.n_a + 255) / 256, 256, 0, s>>>(D);
   return cudaGetLastError();
 }
 

@@ -470,7 +470,7 @@ class OtSolver {
   enum Buf {
     bT, bDy, bDfree, bDmatched, bConsumed, bFlOff, bFlCode, bFlB, bFlCnt, bFlPre, bSy, bSfree, bSmatched,
     bSfreed, bFb, bFy, bFpos, bFidx, bFu0, bFu, bAdmLen, bAdmOff, bAdm, bEk0, bEv0, bEk1, bEv1, bRk0, bRv0,
-    bRk1, bRv1, bCtr, bTemp, bScratch, bNum
+    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bNum
   };
   otprg::OtDev D_{};
   int64_t fl_cap_ = 0, adm_cap_ = 0, e_cap_ = 0, r_cap_ = 0;
@@ -501,6 +501,7 @@ class OtSolver {
     D_.dfree = ensure<int64_t>(bDfree, na2);
     D_.dmatched = ensure<int64_t>(bDmatched, na2);
     D_.consumed = ensure<int64_t>(bConsumed, na2);
+    D_.cl_cut = ensure<int32_t>(bCut, na2);
     D_.fl_off = ensure<int64_t>(bFlOff, na2 + 1);
     D_.sy = ensure<int32_t>(bSy, nb2);
     D_.sfree = ensure<int64_t>(bSfree, nb2);
@@ -773,7 +774,9 @@ class OtSolver {
       D_.e_key = buf(bEk0).as<unsigned long long>();
       D_.e_val = buf(bEv0).as<int64_t>();
       int64_t n_e = 0;
-      const int end_bit = 32 + 1 + static_cast<int>(std::ceil(std::log2(2.0 * n_a_ + 1.0)));
+      const int end_bit = 21 + 1 + static_cast<int>(std::ceil(std::log2(2.0 * n_a_ + 1.0)));
+      OT_CK(otprg::ot_dev_cut_init(D_, s), "cut init");
+      launches_ += 1;
       while (true) {
         OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrNew], 0, 8, s), "memset");
         OT_CK(otprg::ot_dev_propose(D_, s), "propose");
