@@ -564,7 +564,7 @@ def solve_assignment(inst: AssignmentInstance, opt: AssignmentOptions):
         raise ParameterError(f"unknown costs mode {opt.costs!r}")
     if opt.observer is not None or opt.check_invariants or opt.demand_groups is not None:
         return _solve_debug(get_solver(opt.device), inst, opt)
-    if inst.pts_a is not None and inst.cost is None and (
+    if inst.cost is None and (inst.pts_a is not None or inst.img_a is not None) and (
             opt.costs == "on_the_fly" or (opt.costs == "auto" and not _matrix_fits(inst, opt))):
         from .sharded import solve_assignment_sharded  # one shard, no kT anywhere
         return solve_assignment_sharded(inst, opt, 1, on_the_fly=True)

@@ -17,15 +17,6 @@ namespace otprg {
 
 namespace {
 
-// scaled_floor (core.cpp:26-32): floor(c/eps), repaired so that
-// RN(k*eps) <= c < RN((k+1)*eps).
-__device__ __forceinline__ long long scaled_floor_dev(double c, double eps) {
-  long long k = (long long)floor(__ddiv_rn(c, eps));
-  while (__dmul_rn((double)(k + 1), eps) <= c) ++k;
-  while (k > 0 && __dmul_rn((double)k, eps) > c) --k;
-  return k;
-}
-
 template <typename T>
 __device__ __forceinline__ T clamp_store(long long k) {
   // k <= unit_floor < type max by construction of the storage choice.
@@ -269,7 +260,7 @@ __global__ void l1_normalize_kernel(const uint8_t* __restrict__ img, int count, 
 // bits match.  Block tile 64 a x 64 b, thread tile 4 x 4, pixels staged in
 // shared memory in chunks of kP, p-major.
 constexpr int kL1Tile = 64, kL1P = 16, kL1T = 4;
-template <typename T>
+template <typename T, bool kStore = true>
 __global__ void __launch_bounds__(256) l1_round_kernel(const double* __restrict__ xa,
                                                        const double* __restrict__ yb, int n_ai,
                                                        int n_bi, int dim, double eps,
@@ -316,14 +307,35 @@ __global__ void __launch_bounds__(256) l1_round_kernel(const double* __restrict_
         const double c = __ddiv_rn(acc[i][j], 2.0);
         if (!(c >= 0.0 && c <= 1.0)) {
           atomicCAS(status, 0, 2);  // core.cpp:18-21 rejects it (ParameterError)
-          kT[(size_t)b * lda + a] = (T)type_max<T>();
-        } else {
+          if (kStore) kT[(size_t)b * lda + a] = (T)type_max<T>();
+        } else if (kStore) {
           kT[(size_t)b * lda + a] = clamp_store<T>(scaled_floor_dev(c, eps));
         }
-      } else if (a < lda) {
+      } else if (kStore && a < lda) {
         kT[(size_t)b * lda + a] = (T)type_max<T>();
       }
     }
+  }
+}
+
+// Matched-pair L1/2 costs (load_mnist_pair's cost, instances.cpp:134-141, for
+// matching_cost core.cpp:95-102): thread per original a, its partner's row,
+// the pixel differences summed in ascending p (no FMA) exactly as K3.  self
+// rows are xa (self_is_a) or yb; partners index the other side.
+__global__ void l1_matched_cost_kernel(const double* __restrict__ xa, const double* __restrict__ yb, int dim,
+                                       const int32_t* __restrict__ match, int n, int self_is_a,
+                                       double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int j = match[i];
+    if (j < 0) {
+      out[i] = 0.0;
+      continue;
+    }
+    const double* x = self_is_a ? xa + (size_t)i * dim : yb + (size_t)i * dim;
+    const double* y = self_is_a ? yb + (size_t)j * dim : xa + (size_t)j * dim;
+    double acc = 0.0;
+    for (int p = 0; p < dim; ++p) acc = __dadd_rn(acc, fabs(__dsub_rn(x[p], y[p])));
+    out[i] = __ddiv_rn(acc, 2.0);
   }
 }
 
@@ -451,6 +463,39 @@ cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_
     l1_round_kernel<T><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps, static_cast<T*>(kT), lda, status);
     return 0;
   });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l1_check(const double* xa, const double* yb, int n_ai, int n_bi, int dim, int* status,
+                            cudaStream_t s) {
+  dim3 grid((n_ai + kL1Tile - 1) / kL1Tile, (n_bi + kL1Tile - 1) / kL1Tile);
+  l1_round_kernel<uint8_t, false><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, 0.5, nullptr, 0, status);
+  return cudaGetLastError();
+}
+
+__global__ void transpose_f64_kernel(const double* __restrict__ in, int n, int dim, double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const int i0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r, p = p0 + threadIdx.x;
+    if (i < n && p < dim) tile[r][threadIdx.x] = in[(size_t)i * dim + p];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int p = p0 + r, i = i0 + threadIdx.x;
+    if (i < n && p < dim) out[(size_t)p * n + i] = tile[threadIdx.x][r];
+  }
+}
+
+cudaError_t launch_transpose_f64(const double* in, int n, int dim, double* out, cudaStream_t s) {
+  transpose_f64_kernel<<<dim3((n + 31) / 32, (dim + 31) / 32), dim3(32, 8), 0, s>>>(in, n, dim, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l1_matched_cost(const double* xa, const double* yb, int dim, const int32_t* match, int n,
+                                   bool self_is_a, double* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  l1_matched_cost_kernel<<<(n + 127) / 128, 128, 0, s>>>(xa, yb, dim, match, n, self_is_a ? 1 : 0, out);
   return cudaGetLastError();
 }
 

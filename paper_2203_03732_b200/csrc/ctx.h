@@ -114,6 +114,7 @@ struct otprg_ctx {
   bool sh_otf = false;  // OTPRG_FLAG_ON_THE_FLY: no kT slab, threshold-table scans
   bool sh_otf_tiled = true;
   int sh_thr_n = 0;
+  size_t sh_l1_xt = 0;  // on-the-fly L1: byte offset of the transposed demand pixels in pts
   std::shared_ptr<void> sh_plan;    // resident loop (graphs, exchange blocks, peers): shard_host.cpp
   // multi-device context (otprg_create_multi): one shard context per device
   std::vector<otprg_ctx*> multi;

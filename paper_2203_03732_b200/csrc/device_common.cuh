@@ -75,6 +75,15 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// scaled_floor (core.cpp:26-32): floor(c/eps), repaired so that
+// RN(k*eps) <= c < RN((k+1)*eps).
+__device__ __forceinline__ long long scaled_floor_dev(double c, double eps) {
+  long long k = (long long)floor(__ddiv_rn(c, eps));
+  while (__dmul_rn((double)(k + 1), eps) <= c) ++k;
+  while (k > 0 && __dmul_rn((double)k, eps) > c) --k;
+  return k;
+}
+
 // Records the first failure: only the thread that moves status from 0 writes
 // the details, so they are never mixed between reporters.
 __device__ __forceinline__ void report(Ctl* ctl, int code, int e0, int e1 = 0, int e2 = 0,

@@ -70,6 +70,14 @@ cudaError_t launch_l1_normalize(const uint8_t* img, int count, int dim, double* 
                                 cudaStream_t s);
 cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_bi, int dim,
                             double eps, void* kT, int lda, int width, int* status, cudaStream_t s);
+// The range check of K3 alone (status 2 when a cost leaves [0,1]), no kT.
+cudaError_t launch_l1_check(const double* xa, const double* yb, int n_ai, int n_bi, int dim, int* status,
+                            cudaStream_t s);
+// out[p * n + i] = in[i * dim + p] (pixels of the on-the-fly L1 scans).
+cudaError_t launch_transpose_f64(const double* in, int n, int dim, double* out, cudaStream_t s);
+// Costs of the matched pairs of an L1 image instance (thread per original a).
+cudaError_t launch_l1_matched_cost(const double* xa, const double* yb, int dim, const int32_t* match, int n,
+                                   bool self_is_a, double* out, cudaStream_t s);
 // Rounded matrix back to int32 row-major in the ORIGINAL orientation (for
 // otprg_scale_round_costs).
 cudaError_t launch_k_to_kT(const int32_t* k, int n_a, int n_b, void* kT, int lda, int width,
@@ -111,6 +119,12 @@ struct ShardArgs {
   const double* thr;
   int thr_n;
   int otf_tiled;           // the tiled on-the-fly kernel fits shared memory (else the per-row kernel)
+  // On-the-fly L1 image costs (l1x != nullptr): normalised demand pixels
+  // transposed [dim][n_a] (global a), supply pixels row-major [n_b][dim], eps.
+  const double* l1x;
+  const double* l1y;
+  int dim, na_full;
+  double eps;
 };
 constexpr int kSegWarps = 32768;
 constexpr int kMaxSegs = 32;

@@ -446,7 +446,7 @@ std::pair<Matching, SolveStats> solve_assignment(const AssignmentInstance& inst,
     check(otprg_solve_assignment(mc, &p, &rb.r), mc);
     return rb.take();
   }
-  if (p.cost_kind == OTPRG_COST_POINTS2D && on_the_fly(inst, opt)) {
+  if ((p.cost_kind == OTPRG_COST_POINTS2D || p.cost_kind == OTPRG_COST_L1_U8) && on_the_fly(inst, opt)) {
     solve_on_the_fly(ctx, p, &rb.r, opt.device);
     return rb.take();
   }

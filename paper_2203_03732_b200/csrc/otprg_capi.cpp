@@ -409,7 +409,11 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
                o_t = o_yb + ib * 4ull, o_fc = (o_t + static_cast<size_t>(ia) * ctx->width + 7) & ~7ull;
   const int64_t fc_first = std::min<int64_t>(
       std::min<int64_t>(ctx->fc_cap, r->free_counts ? r->free_cap : 0), 65536);
-  const size_t need = o_fc + static_cast<size_t>(fc_first) * 8;
+  // L1 image costs of the matched pairs are evaluated on the device (the
+  // reference's arithmetic, K3's normalised pixels), one per original a
+  const bool l1 = ctx->cost_kind == OTPRG_COST_L1_U8;
+  const size_t o_pc = o_fc + static_cast<size_t>(fc_first) * 8;
+  const size_t need = o_pc + (l1 ? static_cast<size_t>(ctx->n_a) * 8 : 0);
   if (ctx->hpin_n < need) {
     if (ctx->hpin) cudaFreeHost(ctx->hpin);
     ctx->hpin = nullptr;
@@ -426,6 +430,17 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
                      cudaMemcpyDeviceToHost, s), "D2H");
   if (fc_first > 0)
     CK(cudaMemcpyAsync(hp + o_fc, ctx->fc.p, fc_first * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  if (l1) {
+    const size_t dim = ctx->img_dim;
+    const double* xa = ctx->pts.as<double>();
+    const double* yb = xa + static_cast<size_t>(ctx->ia) * dim;
+    CK(ctx->v_ya.ensure(static_cast<size_t>(ctx->n_a) * 8), "alloc pair costs");
+    // original a = internal a (unswapped, partner match_a) or internal b (swapped, partner match_b)
+    CK(otprg::launch_l1_matched_cost(xa, yb, ctx->img_dim, ctx->swapped ? ctx->mb.as<int32_t>() : ctx->ma.as<int32_t>(),
+                                     ctx->n_a, !ctx->swapped, ctx->v_ya.as<double>(), s),
+       "pair cost launch");
+    CK(cudaMemcpyAsync(hp + o_pc, ctx->v_ya.p, static_cast<size_t>(ctx->n_a) * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  }
   CK(cudaEventRecord(ctx->ev[3], s), "event");
   CK(cudaStreamSynchronize(s), "solve");
   Ctl h;
@@ -468,10 +483,11 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
   r->sum_ni = h.sum_ni;
   r->swapped = ctx->swapped;
   r->full_match_termination = h.full_match;
-  double total = 0.0;  // matching_cost, core.cpp:95-102
+  double total = 0.0;  // matching_cost, core.cpp:95-102 (sequential over a: the reference's bits)
+  const double* pc = reinterpret_cast<const double*>(hp + o_pc);
   for (int32_t a = 0; a < ctx->n_a; ++a) {
     const int32_t b = r->match_of_a[a];
-    if (b != -1) total += pair_cost(ctx, a, b);
+    if (b != -1) total += l1 ? pc[a] : pair_cost(ctx, a, b);
   }
   r->cost = total;
   r->build_ms = ctx->build_ms;

@@ -69,7 +69,14 @@ otprg::ShardArgs shard_args(otprg_ctx* ctx) {
   S.seg_hits = ctx->sh_seg.as<int32_t>();
   S.seg_cnt = S.seg_hits + static_cast<size_t>(otprg::kSegWarps) * ctx->sh_K;
   S.row_cnt = S.seg_cnt + otprg::kSegWarps;
-  if (ctx->sh_otf) {
+  if (ctx->sh_otf && ctx->cost_kind == OTPRG_COST_L1_U8) {
+    const size_t dim = ctx->img_dim;
+    S.l1x = reinterpret_cast<const double*>(static_cast<const char*>(ctx->pts.p) + ctx->sh_l1_xt);
+    S.l1y = ctx->pts.as<double>() + static_cast<size_t>(ctx->ia) * dim;
+    S.dim = ctx->img_dim;
+    S.na_full = ctx->ia;
+    S.eps = ctx->eps;
+  } else if (ctx->sh_otf) {
     S.pa = ctx->pts.as<double2>();
     S.pb = S.pa + ctx->ia;
     S.thr = ctx->thr_dev.as<double>();
@@ -425,8 +432,8 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   if (!ctx) return OTPRG_PARAMETER;
   int st = validate_problem(ctx, p);
   if (st) return st;
-  if (p->cost_kind != OTPRG_COST_POINTS2D)
-    return fail(ctx, OTPRG_PARAMETER, "sharded mode builds its slab from 2-D point sets");
+  if (p->cost_kind != OTPRG_COST_POINTS2D && p->cost_kind != OTPRG_COST_L1_U8)
+    return fail(ctx, OTPRG_PARAMETER, "sharded mode builds its slab from 2-D point sets or L1 images");
   if (n_shards < 1 || shard < 0 || shard >= n_shards)
     return fail(ctx, OTPRG_PARAMETER, "bad shard index");
   if (K < 1 || K > 32) return fail(ctx, OTPRG_PARAMETER, "K must lie in [1, 32]");
@@ -496,36 +503,78 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
   CK(ctx->fc.ensure(ctx->fc_cap * 8), "alloc free_counts");
   CK(cudaMemcpyAsync(ctx->sh_bounds.p, bounds.data(), (n_shards + 1) * sizeof(int),
                      cudaMemcpyHostToDevice, ctx->stream), "H2D bounds");
-  // this shard's slab of kT from the points (K2 on the demand range)
-  const double* pa = ctx->swapped ? p->pts_b : p->pts_a;
-  const double* pb = ctx->swapped ? p->pts_a : p->pts_b;
-  CK(ctx->pts.ensure((ia + ib) * 2 * sizeof(double)), "alloc points");
-  double* dpa = ctx->pts.as<double>();
-  double* dpb = dpa + ia * 2;
-  CK(cudaMemcpyAsync(dpa, pa, ia * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-  CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-  CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
-  if ((st = check_points_range(ctx, p, ctx->swapped ? dpb : dpa, ctx->swapped ? dpa : dpb))) return st;
-  int thr_n = 0;
-  if ((st = points_table(ctx, p->eps, &thr_n))) return st;
-  if (ctx->sh_otf) {  // the exact threshold table replaces the slab
-    if (thr_n == 0)
-      return fail(ctx, OTPRG_PARAMETER, "on-the-fly costs need 1/eps <= 8190 (threshold table in shared memory)");
-    ctx->sh_thr_n = thr_n;
-    ctx->sh_otf_tiled = otprg::shard_otf_tiled_fits(width, thr_n, ctx->device);
-  } else if (ctx->sh_hi > ctx->sh_lo) {
-    CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb, ctx->sh_hi - ctx->sh_lo,
-                                    ctx->ib, p->eps, std::sqrt(2.0), thr_n ? ctx->thr_dev.as<double>() : nullptr,
-                                    thr_n, ctx->pts_absmax, ctx->kT.p, ctx->lda, width, ctx->stream),
-       "round_points launch");
+  if (p->cost_kind == OTPRG_COST_L1_U8) {
+    // load_mnist_pair's cost (instances.cpp:114-142): normalised pixels (K3a) of
+    // both sides; the slab by K3b, or on the fly (the scans sum the pixel
+    // differences themselves) after a device pass of the reference's range check
+    const size_t dim = static_cast<size_t>(p->dim);
+    const uint8_t* ia_img = ctx->swapped ? p->img_b : p->img_a;
+    const uint8_t* ib_img = ctx->swapped ? p->img_a : p->img_b;
+    const size_t raw_off = (ia + ib) * dim * sizeof(double);
+    const size_t xt_off = (raw_off + (ia + ib) * dim + 255) / 256 * 256;
+    CK(ctx->pts.ensure(xt_off + (ctx->sh_otf ? ia * dim * sizeof(double) : 0)), "alloc images");
+    double* xa = ctx->pts.as<double>();
+    double* yb = xa + ia * dim;
+    uint8_t* raw = static_cast<uint8_t*>(ctx->pts.p) + raw_off;
+    CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
+    CK(cudaMemcpyAsync(raw, ia_img, ia * dim, cudaMemcpyHostToDevice, ctx->stream), "H2D images");
+    CK(cudaMemcpyAsync(raw + ia * dim, ib_img, ib * dim, cudaMemcpyHostToDevice, ctx->stream), "H2D images");
+    CK(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(Ctl), ctx->stream), "memset");
+    int* status = &ctx->ctl.as<Ctl>()->status;
+    CK(otprg::launch_l1_normalize(raw, static_cast<int>(ia + ib), p->dim, xa, status, ctx->stream), "l1 normalize");
+    if (ctx->sh_otf) {
+      CK(otprg::launch_l1_check(xa, yb, ctx->ia, ctx->ib, p->dim, status, ctx->stream), "l1 check");
+      CK(otprg::launch_transpose_f64(xa, ctx->ia, p->dim,
+                                     reinterpret_cast<double*>(static_cast<char*>(ctx->pts.p) + xt_off), ctx->stream),
+         "transpose");
+    } else if (ctx->sh_hi > ctx->sh_lo) {
+      CK(otprg::launch_l1_round(xa + static_cast<size_t>(ctx->sh_lo) * dim, yb, ctx->sh_hi - ctx->sh_lo, ctx->ib,
+                                p->dim, p->eps, ctx->kT.p, ctx->lda, width, status, ctx->stream),
+         "l1 round");
+    }
+    int dstatus = 0;
+    CK(cudaMemcpyAsync(&dstatus, status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
+    CK(cudaStreamSynchronize(ctx->stream), "image slab build");
+    if (dstatus == OTPRG_PARAMETER) return fail(ctx, OTPRG_PARAMETER, "cost entry outside [0,1]");
+    if (dstatus == OTPRG_INPUT) return fail(ctx, OTPRG_INPUT, "image has zero total intensity");
+    if (dstatus) return fail(ctx, dstatus, "cost build failed");
+    ctx->img_dim = p->dim;
+    ctx->sh_l1_xt = xt_off;
+    ctx->sh_thr_n = 0;
+  } else {
+    // this shard's slab of kT from the points (K2 on the demand range)
+    const double* pa = ctx->swapped ? p->pts_b : p->pts_a;
+    const double* pb = ctx->swapped ? p->pts_a : p->pts_b;
+    CK(ctx->pts.ensure((ia + ib) * 2 * sizeof(double)), "alloc points");
+    double* dpa = ctx->pts.as<double>();
+    double* dpb = dpa + ia * 2;
+    CK(cudaMemcpyAsync(dpa, pa, ia * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    CK(cudaMemcpyAsync(dpb, pb, ib * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    CK(cudaEventRecord(ctx->ev[4], ctx->stream), "event");
+    if ((st = check_points_range(ctx, p, ctx->swapped ? dpb : dpa, ctx->swapped ? dpa : dpb))) return st;
+    int thr_n = 0;
+    if ((st = points_table(ctx, p->eps, &thr_n))) return st;
+    if (ctx->sh_otf) {  // the exact threshold table replaces the slab
+      if (thr_n == 0)
+        return fail(ctx, OTPRG_PARAMETER, "on-the-fly costs need 1/eps <= 8190 (threshold table in shared memory)");
+      ctx->sh_thr_n = thr_n;
+      ctx->sh_otf_tiled = otprg::shard_otf_tiled_fits(width, thr_n, ctx->device);
+    } else if (ctx->sh_hi > ctx->sh_lo) {
+      CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb, ctx->sh_hi - ctx->sh_lo,
+                                      ctx->ib, p->eps, std::sqrt(2.0), thr_n ? ctx->thr_dev.as<double>() : nullptr,
+                                      thr_n, ctx->pts_absmax, ctx->kT.p, ctx->lda, width, ctx->stream),
+         "round_points launch");
+    }
   }
   CK(cudaEventRecord(ctx->ev[5], ctx->stream), "event");
   CK(cudaStreamSynchronize(ctx->stream), "slab build");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]);
   ctx->build_ms = ms;
-  ctx->pts_a.assign(p->pts_a, p->pts_a + 2 * static_cast<size_t>(p->n_a));
-  ctx->pts_b.assign(p->pts_b, p->pts_b + 2 * static_cast<size_t>(p->n_b));
+  if (p->cost_kind == OTPRG_COST_POINTS2D) {
+    ctx->pts_a.assign(p->pts_a, p->pts_a + 2 * static_cast<size_t>(p->n_a));
+    ctx->pts_b.assign(p->pts_b, p->pts_b + 2 * static_cast<size_t>(p->n_b));
+  }
   {
     const otprg::ShardArgs S = shard_args(ctx);
     ctx->sh_grid = otprg::shard_scan_grid(S, ctx->num_sms);

@@ -79,7 +79,7 @@ __device__ __forceinline__ Round round_of(const ShardArgs& S) {
 // cover the GPU (~16 resident per SM) when requests are few, each piece >=
 // one 4 KB warp step, at most kMaxSegs, within the merge buffers.
 __device__ __forceinline__ int scan_segs(const ShardArgs& S, int nreq) {
-  const int units = S.thr ? ((S.hi - S.lo) + 31) / 32                 // 32-element groups (on the fly)
+  const int units = (S.thr || S.l1x) ? ((S.hi - S.lo) + 31) / 32      // 32-element groups (on the fly)
                           : ((S.hi - S.lo) * S.width + 511) / 512;    // 32-vector units of a slab row
   const int target = 148 * 16;
   int segs = 1;
@@ -649,6 +649,113 @@ __device__ __forceinline__ void scan_otf_item(const ShardArgs& S, const double* 
 }
 
 
+// On-the-fly L1 image costs (load_mnist_pair's cost, instances.cpp:134-141;
+// north star (1): costs from d-dim vectors when the matrix does not fit).
+// A warp per (request, piece): the supply image's normalised pixels sit in
+// the warp's shared-memory slice, each lane sums |x_a[p] - y_b[p]| over
+// ascending p for its demand vertex (pixels transposed [p][a]: a warp reads 32
+// consecutive a per p), halves it and rounds it exactly (scaled_floor), the
+// reference's bits; admissible iff k + t(a) == Y(b) - 1.  FP64-bound (2 dim
+// operations per entry), which is why the materialised matrix is preferred
+// whenever it fits.  Outputs, pieces and the merge as the other scans.
+template <typename T>
+__device__ __forceinline__ void scan_l1_item(const ShardArgs& S, double* __restrict__ s_y, const int4* __restrict__ req,
+                                             int segs, int w, int32_t* __restrict__ cand, int2* __restrict__ meta) {
+  const int lane = threadIdx.x & 31;
+  const int r = w / segs, sg = w - r * segs;
+  int i, b, start;
+  if (req) {
+    const int4 q = req[r];
+    i = q.x;
+    b = q.y;
+    start = q.z;
+  } else {
+    i = r;
+    b = __ldcg(S.list_in + r);
+    start = 0;
+  }
+  const int64_t target = (int64_t)(uint32_t)__ldcg(S.yb + b) - 1;
+  const int lo = S.lo, hi = S.hi, K = S.K, width_local = hi - lo, dim = S.dim;
+  const size_t na_full = (size_t)S.na_full;
+  int32_t* o = segs == 1 ? cand + ((size_t)S.shard * S.cap + i) * K : S.seg_hits + (size_t)w * K;
+  int cnt = 0, cov = hi;
+  const int lstart = max(start, lo) - lo;
+  __syncwarp();
+  for (int p = lane; p < dim; p += 32) s_y[p] = S.l1y[(size_t)b * dim + p];
+  __syncwarp();
+  if (start < hi) {
+    const T* tl = static_cast<const T*>(S.t) + lo;
+    const int groups = (width_local + 31) >> 5, g0 = lstart >> 5;
+    const int per = (groups - g0 + segs - 1) / segs;
+    const int gb = g0 + sg * per, ge = min(groups, g0 + (sg + 1) * per);
+    for (int g = gb; g < ge; ++g) {
+      const int e = g * 32 + lane;
+      bool hit = false;
+      if (e < width_local && e >= lstart) {
+        const double* x = S.l1x + lo + e;
+        double acc = 0.0;
+        for (int p = 0; p < dim; ++p) acc = __dadd_rn(acc, fabs(__dsub_rn(__ldg(x + (size_t)p * na_full), s_y[p])));
+        const long long k = scaled_floor_dev(__ddiv_rn(acc, 2.0), S.eps);
+        hit = k + (long long)__ldcg(tl + e) == target;
+      }
+      const unsigned bal = __ballot_sync(kFull, hit);
+      if (!bal) continue;
+      const int idx = cnt + __popc(bal & ((1u << lane) - 1u));
+      if (hit && idx < K) o[idx] = lo + e;
+      const int c = __popc(bal);
+      if (cnt + c >= K) {
+        unsigned bm = bal;
+        for (int t2 = 1; t2 < K - cnt; ++t2) bm &= bm - 1;
+        cov = lo + g * 32 + __ffs(bm);
+        cnt = K;
+        break;
+      }
+      cnt += c;
+    }
+  }
+  if (segs == 1) {
+    if (lane == 0) meta[(size_t)S.shard * S.cap + i] = make_int2(cnt, cov);
+    return;
+  }
+  int prev = 0;
+  if (lane == 0) {
+    S.seg_cnt[w] = cnt;
+    __threadfence();
+    prev = atomicAdd(S.row_cnt + r, 1);
+  }
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != segs - 1) return;
+  __threadfence();
+  int32_t* out = cand + ((size_t)S.shard * S.cap + i) * K;
+  const int wb = r * segs;
+  int tot = 0, rcov = hi;
+  for (int pc = 0; pc < segs && tot < K; ++pc) {
+    const int c = __ldcg(S.seg_cnt + wb + pc);
+    const int32_t* src = S.seg_hits + (size_t)(wb + pc) * K;
+    if (lane < c && tot + lane < K) out[tot + lane] = __ldcg(src + lane);
+    if (tot + c >= K) rcov = __ldcg(src + (K - 1 - tot)) + 1;
+    tot = min(K, tot + c);
+  }
+  if (lane == 0) {
+    meta[(size_t)S.shard * S.cap + i] = make_int2(tot, rcov);
+    S.row_cnt[r] = 0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) shard_scan_l1_kernel(ShardArgs S, int32_t* __restrict__ cand,
+                                                            int2* __restrict__ meta) {
+  const Round rd = round_of(S);
+  if (rd.stop) return;
+  extern __shared__ double s_l1y[];  // [warps per block][dim]
+  double* s_y = s_l1y + (size_t)(threadIdx.x >> 5) * S.dim;
+  const int segs = scan_segs(S, rd.nreq);
+  const int work = rd.nreq * segs;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < work; w += nwarps)
+    scan_l1_item<T>(S, s_y, rd.req, segs, w, cand, meta);
+}
+
 // Few requests (or no room for the tiled kernel): a warp per (request, piece).
 template <typename T>
 __global__ void __launch_bounds__(256) shard_scan_otf_kernel(ShardArgs S, int32_t* __restrict__ cand,
@@ -931,7 +1038,11 @@ int shard_scan_grid(const ShardArgs& a, int num_sms) {
   int g = 0;
   with_width(a.width, [&](auto tag) {
     using T = decltype(tag);
-    if (a.thr) {
+    if (a.l1x) {
+      const size_t smem = (size_t)8 * a.dim * sizeof(double);
+      cudaFuncSetAttribute(shard_scan_l1_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      g = num_sms * blocks_per_sm(shard_scan_l1_kernel<T>, 256, smem);
+    } else if (a.thr) {
       const int simple = blocks_per_sm(shard_scan_otf_kernel<T>, 256, (size_t)a.thr_n * sizeof(double));
       g = num_sms * simple;
       if (a.otf_tiled) {
@@ -958,7 +1069,12 @@ bool shard_otf_tiled_fits(int width, int thr_n, int device) {
 cudaError_t launch_shard_scan(const ShardArgs& a, int32_t* cand, int2* meta, int grid, cudaStream_t s) {
   with_width(a.width, [&](auto tag) {
     using T = decltype(tag);
-    if (a.thr) {
+    if (a.l1x) {
+      const size_t smem = (size_t)8 * a.dim * sizeof(double);
+      auto fn = shard_scan_l1_kernel<T>;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      fn<<<grid, 256, smem, s>>>(a, cand, meta);
+    } else if (a.thr) {
       const size_t smem1 = (size_t)a.thr_n * sizeof(double);
       auto fn1 = shard_scan_otf_kernel<T>;
       if (smem1 > 48 * 1024) cudaFuncSetAttribute(fn1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);

@@ -210,8 +210,8 @@ class ShardedSolver:
                  K: int = K_DEFAULT, distributed: bool = False, on_the_fly: bool = False,
                  resident: bool | None = None, devices: list | None = None):
         _check_options(inst, opt)
-        if inst.pts_a is None or inst.pts_b is None:
-            raise ParameterError("the sharded path builds slabs from 2-D point sets")
+        if (inst.pts_a is None or inst.pts_b is None) and (inst.img_a is None or inst.img_b is None):
+            raise ParameterError("the sharded path builds slabs from 2-D point sets or L1 images")
         self.distributed = distributed
         if distributed:
             import torch.distributed as dist
