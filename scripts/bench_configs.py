@@ -1,7 +1,7 @@
 """Timings of BASELINE.json configs 1, 3, 4, 5 on one B200 (config 2 is bench.py),
 each with its parity check, next to the reference CPU solver.
 
-    python scripts/bench_configs.py > profiles/r01_configs.json
+    python scripts/bench_configs.py > profiles/r02_configs.json
 
 Reference CPU times: config 1 is measured live here (oracle/_ref, 1 thread);
 configs 3 and 5 are the reference timings recorded when the golden fixtures
@@ -90,9 +90,18 @@ def config3():
                      "bit_exact": None if w is None else all(pins(m, s)[k] == w[k] for k in PIN_KEYS),
                      "reference_cpu_ms": None if w is None else
                      round(w["ref_load_s"] * 1e3 + w["ref_solve_ms"], 1)})
+    otf = []
+    for eps in (0.1, 0.01):
+        ms, (m, s) = wall(lambda: otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=eps, costs="on_the_fly")), 2)
+        w = g.get(f"mnist_n10000_eps{eps!r}_s1")
+        otf.append({"eps": eps, "gpu_e2e_ms": round(ms, 3), "phases": s.phases,
+                    "bit_exact": None if w is None else all(pins(m, s)[k] == w[k] for k in PIN_KEYS)})
     return {"workload": "config 3: synthetic MNIST-shaped IDX3 (20000 images, seed 0), "
                         "load_mnist_pair(n=10000, seed=1), L1/2 cost built on the device",
             "runs": rows,
+            "on_the_fly_runs": otf,
+            "on_the_fly_note": "no rounded matrix: the scans sum the 784 pixel differences per entry "
+                               "(FP64, reference order); includes the up-front range check pass",
             "reference_note": "reference = load_mnist_pair cost build + solve_assignment, recorded "
                               "at golden generation (build container, 1 thread)"}
 
@@ -100,20 +109,33 @@ def config3():
 def config4():
     from paper_2203_03732_b200.sharded import ShardedSolver
     inst = otprg.gen_uniform_square(100_000, 1)
-    sv = otprg.Solver(0)
-    ms, (m1, s1) = wall(lambda: sv.solve(inst, otprg.AssignmentOptions(eps=0.01)), 2)
-    sh = ShardedSolver(inst, otprg.AssignmentOptions(eps=0.01), 1)
-    sms, (m2, s2) = wall(sh.solve, 2)
-    same = bool(np.array_equal(m1.match_of_a, m2.match_of_a)
-                and np.array_equal(s1.duals_final.y_a, s2.duals_final.y_a))
-    sh.close()
-    sv.close()
-    return {"workload": "config 4: gen_uniform_square(100000, 1) points, eps=0.01 (uint16 kT 20 GB)",
-            "single_gpu_fused": {"e2e_ms": round(ms, 2), "build_ms": round(s1.device["build_ms"], 2),
-                                 "solve_ms": round(s1.device["solve_ms"], 3), "phases": s1.phases},
-            "sharded_g1_wall_ms": round(sms, 2), "sharded_bit_identical": same,
-            "note": "no CPU reference at this size (the reference needs hours); parity through the "
-                    "sharded/fused bit-identity and the sharded golden tests"}
+    out = {"workload": "config 4: gen_uniform_square(100000, 1) points, eps=0.01"}
+    ref = None
+    for storage in ("u8", "u16"):
+        sv = otprg.Solver(0)
+        ms, (m1, s1) = wall(lambda: sv.solve(inst, otprg.AssignmentOptions(eps=0.01, storage=storage)), 2)
+        if ref is None:
+            ref = (m1, s1)
+        out[f"single_gpu_fused_{storage}"] = {"e2e_ms": round(ms, 2), "build_ms": round(s1.device["build_ms"], 2),
+                                              "solve_ms": round(s1.device["solve_ms"], 3), "phases": s1.phases}
+        sv.close()
+    for storage, otf in (("u8", False), ("u16", False), ("u8", True)):
+        sh = ShardedSolver(inst, otprg.AssignmentOptions(eps=0.01, storage=storage), 1, on_the_fly=otf)
+        times = []
+        for _ in range(3):
+            sh.timer_start()
+            m2, s2 = sh.solve()
+            times.append(sh.timer_stop())
+        same = bool(np.array_equal(ref[0].match_of_a, m2.match_of_a)
+                    and np.array_equal(ref[1].duals_final.y_a, s2.duals_final.y_a))
+        sh.close()
+        out[f"sharded_g1_{storage}{'_on_the_fly' if otf else ''}"] = {
+            "device_ms_median": round(statistics.median(times), 3), "bit_identical": same,
+            "refill_rounds": s2.device["refill_rounds"], "gpu_launches": s2.device["gpu_launches"],
+            "driver": "resident CUDA-graph loop"}
+    out["note"] = ("no CPU reference at this size (the reference needs ~120 GB); parity through the "
+                   "n=20k reference pins of the same code paths and bit-identity with the fused solver")
+    return out
 
 
 def config5():
