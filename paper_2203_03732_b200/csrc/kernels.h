@@ -165,6 +165,9 @@ cudaError_t launch_shard_da(const ShardArgs& a, const int32_t* cand, const int2*
 cudaError_t launch_shard_after_da(const ShardArgs& a, cudaStream_t s);
 cudaError_t launch_shard_ctl(const ShardArgs& a, cudaGraphConditionalHandle cond, bool use_cond,
                              cudaStream_t s);
+// top + compaction + bookkeeping as one cooperative launch (148 blocks, grid barriers)
+cudaError_t launch_shard_round_end(const ShardArgs& a, cudaGraphConditionalHandle cond, bool use_cond,
+                                   cudaStream_t s);
 // Before the first round: phase 0 top (termination test, first free list) and ctl.
 cudaError_t launch_shard_first_top(const ShardArgs& a, cudaStream_t s);
 

@@ -286,8 +286,7 @@ int build_graph(otprg_ctx* ctx, ResPlan& P, ResGroup& g, int gi) {
     otprg_ctx* c = g.shards[i];
     const otprg::ShardArgs S = args(c);
     if (otprg::launch_shard_da(S, xcand, xmeta, c->sh_da_grid, g.cap_stream) != cudaSuccess ||
-        otprg::launch_shard_after_da(S, g.cap_stream) != cudaSuccess ||
-        otprg::launch_shard_ctl(S, cond, i + 1 == g.shards.size(), g.cap_stream) != cudaSuccess)
+        otprg::launch_shard_round_end(S, cond, i + 1 == g.shards.size(), g.cap_stream) != cudaSuccess)
       st = OTPRG_DEVICE;
   }
   cudaGraph_t captured = nullptr;
@@ -411,12 +410,12 @@ int run_plan(otprg_ctx* ctx, ResPlan& P, otprg_result* res) {
   res->refill_rounds = h0.sh_rounds;
   res->n_shards = P.n_shards;
   // launches per local shard: init + phase-0 top (top, 2 compaction, ctl) +
-  // complete, and per round: scan (1 slab / 2 on the fly) + DA + top + 2
-  // compaction + ctl; + one push per group and round when there are peers
+  // complete, and per round: scan (1 slab / 2 on the fly) + DA + the
+  // cooperative round end; + one push per group and round when there are peers
   int launches = 0;
   const int rounds = static_cast<int>(h0.phase) + h0.sh_rounds;
   for (ResGroup* g : local) {
-    for (otprg_ctx* c : g->shards) launches += 6 + rounds * ((c->sh_otf ? 2 : 1) + 5);
+    for (otprg_ctx* c : g->shards) launches += 6 + rounds * ((c->sh_otf ? 2 : 1) + 2);
     if (P.groups.size() > 1) launches += rounds;
   }
   res->gpu_launches = launches;
@@ -633,8 +632,7 @@ int otprg_shard_da(otprg_ctx* ctx, const int32_t* cand, const int32_t* meta_word
   CK(otprg::launch_shard_da(S, cand, meta, ctx->sh_da_grid, ctx->stream), "shard_da launch");
   // complete phase -> its top (apply M', termination, next free list); then
   // the round bookkeeping — all decided on the device
-  CK(otprg::launch_shard_after_da(S, ctx->stream), "shard top launch");
-  CK(otprg::launch_shard_ctl(S, cudaGraphConditionalHandle{}, false, ctx->stream), "shard ctl launch");
+  CK(otprg::launch_shard_round_end(S, cudaGraphConditionalHandle{}, false, ctx->stream), "shard round-end launch");
   Ctl h{};
   const int st = read_ctl(ctx, &h);
   if (st) return st;

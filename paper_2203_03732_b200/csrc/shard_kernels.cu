@@ -248,11 +248,14 @@ __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, int32_t* _
 // (nothing to apply).  Skipped while chains are parked (the phase goes on).
 // Reads only what earlier kernels wrote (ctl->phase is advanced by the ctl
 // kernel), so its blocks never race with its own thread 0.
-__global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, int first) {
+__device__ __forceinline__ bool top_runs(const Ctl* ctl, int first) {
+  if (__ldcg(&ctl->status)) return false;
+  return first || (__ldcg(&ctl->work[1]) == 0 && __ldcg(&ctl->sh_live) != 0);
+}
+
+__device__ __forceinline__ void top_body(const ShardArgs& S, int first, uint32_t phase_now) {
   Ctl* ctl = S.ctl;
-  if (__ldcg(&ctl->status)) return;
-  if (!first && (__ldcg(&ctl->work[1]) != 0 || __ldcg(&ctl->sh_live) == 0)) return;
-  const uint32_t phase_done = first ? 0u : __ldcg(&ctl->phase) + 1u;
+  const uint32_t phase_done = first ? 0u : phase_now + 1u;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
   const int par = phase_done & 1;
   if (!first) {
@@ -288,6 +291,11 @@ __global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, int first)
   }
 }
 
+__global__ void __launch_bounds__(1024) shard_top_kernel(ShardArgs S, int first) {
+  if (!top_runs(S.ctl, first)) return;
+  top_body(S, first, __ldcg(&S.ctl->phase));
+}
+
 // The free list of the coming phase, ascending b (identical on every rank,
 // so list indices name the same b everywhere), and its inverse.  Two passes
 // over kCompactBlocks contiguous ranges: per-range counts, then ordered writes
@@ -298,8 +306,7 @@ __device__ __forceinline__ bool compact_skip(const Ctl* c) {
   return __ldcg(&c->done) || __ldcg(&c->status) || __ldcg(&c->work[1]) != 0;
 }
 
-__global__ void __launch_bounds__(1024) shard_compact_count_kernel(ShardArgs S, int* counts) {
-  if (compact_skip(S.ctl)) return;
+__device__ __forceinline__ void compact_count_body(const ShardArgs& S, int* counts) {
   const int n_b = S.ctl->n_b;
   const int chunk = (n_b + gridDim.x - 1) / gridDim.x;
   const int lo = min(n_b, (int)blockIdx.x * chunk), hi = min(n_b, lo + chunk);
@@ -314,8 +321,12 @@ __global__ void __launch_bounds__(1024) shard_compact_count_kernel(ShardArgs S, 
   if (threadIdx.x == 0) counts[blockIdx.x] = s_sum;
 }
 
-__global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, const int* counts) {
+__global__ void __launch_bounds__(1024) shard_compact_count_kernel(ShardArgs S, int* counts) {
   if (compact_skip(S.ctl)) return;
+  compact_count_body(S, counts);
+}
+
+__device__ __forceinline__ void compact_write_body(const ShardArgs& S, const int* counts) {
   __shared__ int s_warp[32];
   __shared__ int s_base;
   const int n_b = S.ctl->n_b;
@@ -351,17 +362,23 @@ __global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, 
   }
 }
 
+__global__ void __launch_bounds__(1024) shard_compact_write_kernel(ShardArgs S, const int* counts) {
+  if (compact_skip(S.ctl)) return;
+  compact_write_body(S, counts);
+}
+
 // Round bookkeeping (one thread), after the DA (and the top when the phase
 // completed): parked chains -> a refill round over them; else the phase is
 // complete -> the next phase's first round over its free list.  Sets the
 // resident loop's WHILE condition (continue while not finished and no error).
-__global__ void shard_ctl_kernel(ShardArgs S, int first, cudaGraphConditionalHandle cond, int use_cond) {
+// parked: the DA's parked-chain count (read by the caller before any reset).
+__device__ __forceinline__ void ctl_body(const ShardArgs& S, int first, int parked, cudaGraphConditionalHandle cond,
+                                        int use_cond) {
   Ctl* c = S.ctl;
   if (!first && !c->sh_live) {  // a loop entered after the solve had finished: nothing ran
     if (use_cond) cudaGraphSetConditional(cond, 0u);
     return;
   }
-  const int parked = first ? 0 : c->work[1];
   if (parked > 0) {
     c->sh_mode = 1;
     c->sh_nreq = parked;
@@ -380,6 +397,38 @@ __global__ void shard_ctl_kernel(ShardArgs S, int first, cudaGraphConditionalHan
   const int go = !c->done && !c->status;
   c->sh_live = go;
   if (use_cond) cudaGraphSetConditional(cond, go ? 1u : 0u);
+}
+
+__global__ void shard_ctl_kernel(ShardArgs S, int first, cudaGraphConditionalHandle cond, int use_cond) {
+  ctl_body(S, first, first ? 0 : S.ctl->work[1], cond, use_cond);
+}
+
+// Everything after a round's DA in ONE cooperative launch (one block per SM,
+// co-resident): the top when the phase is complete, the compaction's count
+// and write passes, and the round bookkeeping, separated by two grid
+// barriers (the monotone arrival counter of device_common.cuh; its base is
+// carried across launches in ctl->bar_base).  Every value a later part of
+// the kernel changes (work[1], sh_live, phase) is read before the first
+// barrier.
+__global__ void __launch_bounds__(1024) shard_round_end_kernel(ShardArgs S, int first,
+                                                               cudaGraphConditionalHandle cond, int use_cond) {
+  Ctl* c = S.ctl;
+  unsigned target = ld_cg(reinterpret_cast<const unsigned*>(&c->bar_base));
+  const bool runs = top_runs(c, first);
+  const int parked = first ? 0 : __ldcg(&c->work[1]);
+  const uint32_t phase_now = __ldcg(&c->phase);
+  if (runs) top_body(S, first, phase_now);
+  target += gridDim.x;
+  grid_barrier(c, target);
+  const bool compact = runs && !__ldcg(&c->done) && !__ldcg(&c->status);
+  if (compact) compact_count_body(S, S.scratch);
+  target += gridDim.x;
+  grid_barrier(c, target);
+  if (compact) compact_write_body(S, S.scratch);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl_body(S, first, parked, cond, use_cond);
+    c->bar_base = target;  // every block has passed both barriers
+  }
 }
 
 // Deferred acceptance over merged candidate lists, one warp per chain
@@ -1124,6 +1173,20 @@ cudaError_t launch_shard_ctl(const ShardArgs& a, cudaGraphConditionalHandle cond
                              cudaStream_t s) {
   shard_ctl_kernel<<<1, 1, 0, s>>>(a, 0, cond, use_cond ? 1 : 0);
   return cudaGetLastError();
+}
+
+cudaError_t launch_shard_round_end(const ShardArgs& a, cudaGraphConditionalHandle cond, bool use_cond,
+                                   cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kCompactBlocks);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, shard_round_end_kernel, a, 0, cond, use_cond ? 1 : 0);
 }
 
 cudaError_t launch_shard_first_top(const ShardArgs& a, cudaStream_t s) {
