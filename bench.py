@@ -419,7 +419,22 @@ def run_sharded(args, world, rank, local, steps: int, warmup: int, on_the_fly: b
                        resident=False if share_gpu() and world > 1 else None)
     barrier(world)
     prep_s = allreduce_max(time.perf_counter() - t0, world)
-    m, s = sv.solve()
+    fallback = getattr(sv, "resident_error", None)
+    try:
+        m, s = sv.solve()
+        ok = 1
+    except Exception as e:  # noqa: BLE001  (a failed resident exchange: rerun host-driven, say so)
+        fallback, ok = f"{type(e).__name__}: {e}"[:200], 0
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t_ok = torch.tensor([ok], dtype=torch.int32, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+        ok = int(t_ok.item())
+    if not ok:
+        sv.close()
+        sv = ShardedSolver(inst, opt, 1, K=args.K, distributed=world > 1, on_the_fly=on_the_fly, resident=False)
+        m, s = sv.solve()
     for _ in range(warmup):
         sv.solve()
     times = []
@@ -447,6 +462,8 @@ def run_sharded(args, world, rank, local, steps: int, warmup: int, on_the_fly: b
         "gpu_launches_per_step": launches,
         "clocks": clk.summary(),
     }
+    if fallback:
+        out["resident_fallback"] = fallback
     if not on_the_fly:
         # B_alg = sum_i n_i * n_a * w over all ranks; this rank's share
         # is sum_i n_i * (its slab width) * w.  Scans stop at the K-th candidate, so

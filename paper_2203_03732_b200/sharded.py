@@ -228,10 +228,26 @@ class ShardedSolver:
                 dist.all_gather_object(devs, (socket_host(), device))
                 resident = len(set(devs)) == world
             if resident:
-                h = self.ranks[0].ipc_export(world, rank)
+                ok = 1
+                try:
+                    h = self.ranks[0].ipc_export(world, rank)
+                except Exception:  # noqa: BLE001
+                    h, ok = b"", 0
                 handles = [None] * world
                 dist.all_gather_object(handles, h)
-                self.ranks[0].ipc_attach(handles, list(range(world)))
+                try:
+                    if ok and all(handles):
+                        self.ranks[0].ipc_attach(handles, list(range(world)))
+                    else:
+                        ok = 0
+                except Exception:  # noqa: BLE001
+                    ok = 0
+                oks = [None] * world
+                dist.all_gather_object(oks, ok)
+                if not all(oks):  # no peer mapping on some rank: the host-driven protocol everywhere
+                    resident = False
+                    self.resident_error = "CUDA IPC attach failed on some rank"
+                    self.ranks[0].prepare(inst, opt.eps, world, rank, K, opt.storage, on_the_fly)
         else:
             devs = list(devices) if devices is not None else [opt.device] * n_shards
             if len(devs) != n_shards:
