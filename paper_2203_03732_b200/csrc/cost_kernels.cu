@@ -418,7 +418,7 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
     with_width(width, [&](auto tag) {
       using T = decltype(tag);
       auto fn = round_points_thr_kernel<T>;
-      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_attr_raise(fn, smem);
       int per_sm = 0, dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -8,6 +8,15 @@
 
 namespace otprg {
 
+// Raises (never lowers) a kernel's opt-in dynamic shared-memory limit on the
+// current device: the attribute is per function, so contexts prepared with
+// different sizes must not shrink it under each other (kernel_attrs.cpp).
+cudaError_t smem_attr_raise(const void* fn, size_t bytes);
+template <typename F>
+inline cudaError_t smem_attr_raise(F* fn, size_t bytes) {
+  return smem_attr_raise(reinterpret_cast<const void*>(fn), bytes);
+}
+
 // Low-set cache per supply vertex b (see solve_kernels.cu): the ascending
 // positions a < cov with k(a,b) + t(a) <= upto at the time of the scan that
 // built it, up to kLowCap entries, each packed as (k << 32) | a.

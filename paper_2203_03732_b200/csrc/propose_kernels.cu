@@ -193,16 +193,10 @@ cudaError_t launch_propose_stream(const void* kT, int lda, int n_b, int width, i
   const int rpw = (n_b + max_warps - 1) / max_warps;
   const int warps = (n_b + rpw - 1) / rpw;
   const int grid = std::min(num_sms, warps);
-  // raise the opt-in shared-memory limit once per device and width
-  static size_t smem_set[64][3] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  size_t* smem_set_dev = smem_set[dev & 63];
   with_width(width, [&](auto tag) {
     using T = decltype(tag);
     auto fn = propose_stream_kernel<T>;
-    size_t& set = smem_set_dev[sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : 2];
-    if (set < smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(set = smem));
+    smem_attr_raise(fn, smem);  // (only ever raised: per function and device)
     fn<<<grid, kStreamThreads, smem, s>>>(static_cast<const T*>(kT), lda, n_b, chunk, cpr, rpw, lmeta,
                                           lent, static_cast<T*>(rowmin), ctl);
     return 0;

@@ -27,6 +27,7 @@
 //               whatever the shard count.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -101,9 +102,10 @@ __device__ __forceinline__ int scan_segs(const ShardArgs& S, int nreq) {
 // piece in S.seg_hits, and the last warp of the request to finish merges the
 // pieces in order (the first K hits overall; resume after the K-th), so a
 // 200 KB row costs a few dependent steps instead of ~50.
-template <typename T, bool kP1>
+template <typename T, bool kP1, bool kSmemT>
 __device__ __forceinline__ void scan_slab_item(const ShardArgs& S, const int4* __restrict__ req, int segs,
-                                               int w, int32_t* __restrict__ cand, int2* __restrict__ meta) {
+                                               int w, int32_t* __restrict__ cand, int2* __restrict__ meta,
+                                               const uint4* __restrict__ s_t) {
   using SD = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
   constexpr int kU = OTPRG_SHARD_UNROLL;  // 16-byte loads in flight per lane (12: 6 KB per warp step)
@@ -127,7 +129,7 @@ __device__ __forceinline__ void scan_slab_item(const ShardArgs& S, const int4* _
   const int lstart = max(start, lo) - lo;
   if (start < hi) {
     const uint4* rv = reinterpret_cast<const uint4*>(static_cast<const T*>(S.kT) + (size_t)b * S.lda);
-    const uint4* tv = reinterpret_cast<const uint4*>(static_cast<const T*>(S.t) + lo);
+    const uint4* tv = kSmemT ? s_t : reinterpret_cast<const uint4*>(static_cast<const T*>(S.t) + lo);
     const int nv = (width_local + kEpv - 1) / kEpv;
     // this warp's piece, in 32-vector units
     const int u0 = (lstart / kEpv) >> 5, units = (nv + 31) >> 5;
@@ -135,25 +137,31 @@ __device__ __forceinline__ void scan_slab_item(const ShardArgs& S, const int4* _
     const int vb = (u0 + sg * per) * 32, ve = min(nv, (u0 + (sg + 1) * per) * 32);
     bool full = false;
     for (int v = vb; v < ve && !full; v += 32 * kU) {
-      uint4 kr[kU], tr[kU];
+      // t from shared memory (kSmemT: read at use) or preloaded with the kT loads
+      uint4 kr[kU], tr[(kP1 || kSmemT) ? 1 : kU];
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
         const int vi = v + j * 32 + lane;
         if (vi < ve) {
           kr[j] = __ldg(rv + vi);
-          // phase 1: t == 0 everywhere (init_state), no t traffic
-          tr[j] = kP1 ? make_uint4(0u, 0u, 0u, 0u) : __ldcg(tv + vi);
+          if constexpr (!kP1 && !kSmemT) tr[j] = __ldcg(tv + vi);
         } else {
           kr[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
-          tr[j] = make_uint4(0u, 0u, 0u, 0u);
+          if constexpr (!kP1 && !kSmemT) tr[j] = make_uint4(0u, 0u, 0u, 0u);
         }
       }
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
         if (full) break;
-        const int e0 = (v + j * 32 + lane) * kEpv;  // local element index
+        const int vi = v + j * 32 + lane;
+        const int e0 = vi * kEpv;  // local element index
+        uint4 tj = make_uint4(0u, 0u, 0u, 0u);  // phase 1: t == 0 everywhere (init_state), no t traffic
+        if constexpr (!kP1) {
+          if constexpr (kSmemT) tj = vi < ve ? tv[vi] : make_uint4(0u, 0u, 0u, 0u);
+          else tj = tr[j];
+        }
         const uint32_t kw[4] = {kr[j].x, kr[j].y, kr[j].z, kr[j].w};
-        const uint32_t tw[4] = {tr[j].x, tr[j].y, tr[j].z, tr[j].w};
+        const uint32_t tw[4] = {tj.x, tj.y, tj.z, tj.w};
         uint32_t m = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) m |= SD::bits(SD::eq(SD::add(kw[q], tw[q]), tg)) << (q * SD::kEpw);
@@ -226,19 +234,29 @@ __device__ __forceinline__ void scan_slab_item(const ShardArgs& S, const int4* _
   }
 }
 
-template <typename T>
+// kSmemT: the slab's t staged in shared memory once per launch (the kernel is
+// grid-stride: a block serves many rows), so every in-flight load slot of a
+// lane carries kT bytes (round 2: the global-t form spent half of them on t).
+template <typename T, bool kSmemT>
 __global__ void __launch_bounds__(256) shard_scan_kernel(ShardArgs S, int32_t* __restrict__ cand,
                                                          int2* __restrict__ meta) {
+  extern __shared__ __align__(16) uint4 s_tslab[];
   const Round rd = round_of(S);
   if (rd.stop) return;
+  if (kSmemT && rd.phase != 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(S.t) + S.lo);
+    const int nv = ((S.hi - S.lo) * (int)sizeof(T) + 15) / 16;
+    for (int q = threadIdx.x; q < nv; q += blockDim.x) s_tslab[q] = __ldcg(src + q);
+    __syncthreads();
+  }
   const int segs = scan_segs(S, rd.nreq);
   const int work = rd.nreq * segs;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < work; w += nwarps) {
     if (rd.phase == 0)  // phase 1: t == 0 everywhere (init_state), no t traffic
-      scan_slab_item<T, true>(S, rd.req, segs, w, cand, meta);
+      scan_slab_item<T, true, kSmemT>(S, rd.req, segs, w, cand, meta, s_tslab);
     else
-      scan_slab_item<T, false>(S, rd.req, segs, w, cand, meta);
+      scan_slab_item<T, false, kSmemT>(S, rd.req, segs, w, cand, meta, s_tslab);
   }
 }
 
@@ -1078,6 +1096,20 @@ int blocks_per_sm(K fn, int threads, size_t smem) {
 }
 }  // namespace
 
+// Shared memory for the slab's t in the slab scan (0: too large, t from L2).
+// Off by default: A/B on config 4 (G = 1, u8, resident; scripts/probe_k.py):
+// 9.2-9.6 ms with t from L2, 9.6-10.3 ms staged — every launch restages the
+// slab's t per block (296 blocks x 100 KB from L2 per round) and occupancy
+// does not rise (2 blocks per SM either way).  OTPRG_SLAB_TSMEM=1 turns it on.
+size_t slab_t_smem(const ShardArgs& a) {
+  static const bool on = [] {
+    const char* e = std::getenv("OTPRG_SLAB_TSMEM");
+    return e && e[0] == '1';
+  }();
+  const size_t bytes = ((size_t)(a.hi - a.lo) * a.width + 15) / 16 * 16;
+  return on && bytes <= 96 * 1024 ? std::max<size_t>(bytes, 16) : 0;
+}
+
 static_assert(kOtfChunk % (32 * OTPRG_OTF_GU) == 0, "OTPRG_OTF_CHUNK must be a multiple of 32 * OTPRG_OTF_GU");
 static_assert((kOtfChunk * 16) % 16 == 0 && kOtfChunk % 16 == 0, "OTPRG_OTF_CHUNK must keep 16-byte stages");
 
@@ -1089,18 +1121,24 @@ int shard_scan_grid(const ShardArgs& a, int num_sms) {
     using T = decltype(tag);
     if (a.l1x) {
       const size_t smem = (size_t)8 * a.dim * sizeof(double);
-      cudaFuncSetAttribute(shard_scan_l1_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_attr_raise(shard_scan_l1_kernel<T>, smem);
       g = num_sms * blocks_per_sm(shard_scan_l1_kernel<T>, 256, smem);
     } else if (a.thr) {
       const int simple = blocks_per_sm(shard_scan_otf_kernel<T>, 256, (size_t)a.thr_n * sizeof(double));
       g = num_sms * simple;
       if (a.otf_tiled) {
         const size_t smem = otf_tiled_smem(a.width, a.thr_n);
-        cudaFuncSetAttribute(shard_scan_otf_tiled_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_attr_raise(shard_scan_otf_tiled_kernel<T>, smem);
         g = std::max(g, num_sms * blocks_per_sm(shard_scan_otf_tiled_kernel<T>, kOtfRows * 32, smem));
       }
     } else {
-      g = num_sms * blocks_per_sm(shard_scan_kernel<T>, 256, 0);
+      const size_t st = slab_t_smem(a);
+      if (st) {
+        smem_attr_raise(shard_scan_kernel<T, true>, st);
+        g = num_sms * blocks_per_sm(shard_scan_kernel<T, true>, 256, st);
+      } else {
+        g = num_sms * blocks_per_sm(shard_scan_kernel<T, false>, 256, 0);
+      }
     }
     return 0;
   });
@@ -1121,22 +1159,24 @@ cudaError_t launch_shard_scan(const ShardArgs& a, int32_t* cand, int2* meta, int
     if (a.l1x) {
       const size_t smem = (size_t)8 * a.dim * sizeof(double);
       auto fn = shard_scan_l1_kernel<T>;
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_attr_raise(fn, smem);
       fn<<<grid, 256, smem, s>>>(a, cand, meta);
     } else if (a.thr) {
       const size_t smem1 = (size_t)a.thr_n * sizeof(double);
       auto fn1 = shard_scan_otf_kernel<T>;
-      if (smem1 > 48 * 1024) cudaFuncSetAttribute(fn1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+      smem_attr_raise(fn1, smem1);
       // each of the two exits at once unless the round's request count is its regime
       fn1<<<grid, 256, smem1, s>>>(a, cand, meta);
       if (a.otf_tiled) {
         const size_t smem = otf_tiled_smem(a.width, a.thr_n);
         auto fn = shard_scan_otf_tiled_kernel<T>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_attr_raise(fn, smem);
         fn<<<grid, kOtfRows * 32, smem, s>>>(a, cand, meta);
       }
     } else {
-      shard_scan_kernel<T><<<grid, 256, 0, s>>>(a, cand, meta);
+      const size_t st = slab_t_smem(a);
+      if (st) shard_scan_kernel<T, true><<<grid, 256, st, s>>>(a, cand, meta);
+      else shard_scan_kernel<T, false><<<grid, 256, 0, s>>>(a, cand, meta);
     }
     return 0;
   });

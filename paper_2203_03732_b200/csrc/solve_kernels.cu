@@ -849,7 +849,7 @@ int phase_loop_grid(int width, bool smem_t, int lda, int num_sms) {
   void* fn = pick_loop(width, smem_t);
   const size_t smem = phase_loop_smem(width, smem_t, lda);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_attr_raise(fn, smem);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem) != cudaSuccess)
     return 0;
