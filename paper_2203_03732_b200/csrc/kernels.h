@@ -188,7 +188,13 @@ cudaError_t launch_ot_scan(const void* kT, int lda, int width, const void* t0, c
 
 // ---- OT copy/cluster phase on the device (ot_device.cu) ---------------------
 constexpr int32_t kFreeB = 0x7fffffff;  // flow-entry "b" of a demand cluster's free copies
-enum OtCtr { kCtrNi = 0, kCtrFree = 1, kCtrNew = 2, kCtrE = 3, kCtrRec = 4, kCtrCount = 8 };
+// kCtrTouch..kCtrBig: the device-sized DA rounds (ot_dev_da_rounds): clusters
+// proposed to this round, segment space handed out, rounds over (1) or a
+// segment too large for the warp resolve (2), entries this round.
+enum OtCtr {
+  kCtrNi = 0, kCtrFree = 1, kCtrNew = 2, kCtrE = 3, kCtrRec = 4,
+  kCtrTouch = 5, kCtrAlloc = 6, kCtrDone = 7, kCtrN = 8, kCtrBig = 9, kCtrRounds = 10, kCtrCount = 12
+};
 struct OtDev {
   int n_a, n_b, lda, width;
   const void* kT;      // [n_b][lda] rounded costs at eps/3
@@ -223,6 +229,12 @@ struct OtDev {
   // DA entries (key = code << 32 | i) and next-state records
   unsigned long long* e_key;
   int64_t* e_val;
+  unsigned long long* s_key;  // the round's entries grouped by cluster (segment per code)
+  int64_t* s_val;
+  int32_t* da_cnt;     // [2 n_a] entries per cluster this round (0 between rounds)
+  int32_t* da_fill;    // [2 n_a] scatter cursor (0 between rounds)
+  int64_t* da_off;     // [2 n_a] segment start
+  int32_t* da_touch;   // [2 n_a] clusters proposed to this round
   unsigned long long* r_key;
   int64_t* r_val;
   int64_t* ctr;        // [kCtrCount]
@@ -234,6 +246,14 @@ cudaError_t ot_dev_t(OtDev& D, cudaStream_t s);
 cudaError_t ot_dev_adm(OtDev& D, int pass, cudaStream_t s);
 cudaError_t ot_dev_cut_init(OtDev& D, cudaStream_t s);
 cudaError_t ot_dev_propose(OtDev& D, cudaStream_t s);
+// R device-sized DA rounds (no host sizes): propose, count per cluster,
+// segment allocation, scatter, warp-per-cluster resolve.  ctr[kCtrDone] = 1
+// once a round finds no proposal; 2 when a cluster got more than
+// kDaWarpMax entries (that round's entries stay in e_key[0, ctr[kCtrN]) for
+// the sorted path, ot_dev_da_clear resets the per-cluster counts).
+constexpr int kDaWarpMax = 256;
+cudaError_t ot_dev_da_rounds(OtDev& D, int rounds, cudaStream_t s);
+cudaError_t ot_dev_da_clear(OtDev& D, cudaStream_t s);
 cudaError_t ot_dev_resolve(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
                            unsigned long long* out_key, int64_t* out_val, cudaStream_t s);
 cudaError_t ot_dev_consumed(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,

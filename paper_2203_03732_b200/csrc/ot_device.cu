@@ -274,6 +274,155 @@ __global__ void ot_da_resolve_kernel(OtDev D, const unsigned long long* __restri
   }
 }
 
+// ---- device-sized rounds ---------------------------------------------------------
+// The same round without a sort or a host size: the entries (survivors in
+// e_key[0, E), this round's proposals after them) are grouped by cluster into
+// per-cluster segments of s_key (count, allocate, scatter), then one warp per
+// cluster proposed to ranks its entries by list index and resolves them
+// exactly as ot_da_resolve_kernel does on the sorted run.  Every kernel
+// returns at once when the rounds are over (ctr[kCtrDone]), so a batch of
+// rounds is launched without looking at the counters.
+__device__ __forceinline__ bool da_over(const OtDev& D) { return *(volatile int64_t*)&D.ctr[kCtrDone] != 0; }
+
+__global__ void ot_da_propose_batched_kernel(OtDev D) {
+  if (da_over(D)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // (unused by propose; reset for this round's count / alloc)
+    D.ctr[kCtrTouch] = 0;
+    D.ctr[kCtrAlloc] = 0;
+  }
+  const int nf = D.ctr[kCtrFree];
+  const long long base = D.ctr[kCtrE];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    const int64_t u = D.fu[i];
+    if (u <= 0) continue;
+    int p = D.fpos[i];
+    const int len = (int)D.adm_len[i];
+    const int32_t* list = D.adm + D.adm_off[i];
+    while (p < len && __ldcg(&D.cl_cut[list[p]]) < i) ++p;
+    D.fpos[i] = p;
+    if (p >= len) continue;
+    const int code = list[p];
+    const long long slot = base + atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrNew]), 1ull);
+    D.e_key[slot] = ((unsigned long long)(uint32_t)code << 21) | (uint32_t)i;
+    D.e_val[slot] = u;
+    D.fu[i] = 0;
+  }
+}
+
+__global__ void ot_da_count_kernel(OtDev D) {
+  if (da_over(D)) return;
+  const long long nn = D.ctr[kCtrNew];
+  if (nn == 0) {  // no b has copies to place and a cluster to try: the claims are final
+    if (blockIdx.x == 0 && threadIdx.x == 0) D.ctr[kCtrDone] = 1;
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ++D.ctr[kCtrRounds];
+  const long long n = D.ctr[kCtrE] + nn;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const int code = (int)(D.e_key[j] >> 21);
+    if (atomicAdd(&D.da_cnt[code], 1) == 0)
+      D.da_touch[atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrTouch]), 1ull)] = code;
+  }
+}
+
+__global__ void ot_da_alloc_kernel(OtDev D) {
+  if (da_over(D)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // (nobody below reads E / New)
+    D.ctr[kCtrN] = D.ctr[kCtrE] + D.ctr[kCtrNew];
+    D.ctr[kCtrE] = 0;
+  }
+  const int nt = (int)D.ctr[kCtrTouch];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    const int code = D.da_touch[t];
+    const int c = D.da_cnt[code];
+    if (c > kDaWarpMax) D.ctr[kCtrBig] = 1;  // this round goes the sorted way
+    D.da_off[code] = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrAlloc]), (unsigned long long)c);
+  }
+}
+
+__global__ void ot_da_scatter_kernel(OtDev D) {
+  if (da_over(D)) return;
+  if (D.ctr[kCtrBig]) {  // (set by the allocation: every block sees it)
+    if (blockIdx.x == 0 && threadIdx.x == 0) D.ctr[kCtrDone] = 2;
+    return;
+  }
+  const long long n = D.ctr[kCtrN];
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = D.e_key[j];
+    const int code = (int)(k >> 21);
+    const long long pos = D.da_off[code] + atomicAdd(&D.da_fill[code], 1);
+    D.s_key[pos] = k;
+    D.s_val[pos] = D.e_val[j];
+  }
+}
+
+__global__ void ot_da_resolve_warp_kernel(OtDev D) {
+  if (da_over(D)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) D.ctr[kCtrNew] = 0;  // (count has read it) next round's proposals
+  const int lane = threadIdx.x & 31;
+  const int nt = (int)D.ctr[kCtrTouch];
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nt; t += warps) {
+    const int code = D.da_touch[t];
+    const int c = D.da_cnt[code];
+    const long long o = D.da_off[code];
+    const int64_t cap = D.dfree[code] + D.dmatched[code];
+    for (int b0 = 0; b0 < c; b0 += 32) {
+      const int e = b0 + lane;
+      const bool valid = e < c;
+      const unsigned long long ke = valid ? D.s_key[o + e] : 0ull;
+      const int ie = valid ? (int)(ke & ((1u << 21) - 1)) : INT_MAX;
+      int64_t amt = 0, pre = 0;
+      bool last = true;
+      for (int b1 = 0; b1 < c; b1 += 32) {
+        const int e2 = b1 + lane;
+        const int i2 = e2 < c ? (int)(D.s_key[o + e2] & ((1u << 21) - 1)) : INT_MAX;
+        const int64_t v2 = e2 < c ? D.s_val[o + e2] : 0;
+        const int m = min(32, c - b1);
+        for (int q = 0; q < m; ++q) {
+          const int iq = __shfl_sync(0xffffffffu, i2, q);
+          const int64_t vq = __shfl_sync(0xffffffffu, v2, q);
+          if (iq < ie) pre += vq;
+          else if (iq == ie) {
+            amt += vq;
+            if (b1 + q > e) last = false;  // a later duplicate carries the run
+          }
+        }
+      }
+      if (!valid || !last) continue;
+      const int i = ie;
+      const int64_t acc = max((int64_t)0, min(amt, cap - pre));
+      const int64_t rej = amt - acc;
+      if (acc > 0 && pre + acc == cap) D.cl_cut[code] = i;
+      if (rej > 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&D.fu[i]), (unsigned long long)rej);
+        const int p = D.fpos[i];
+        if (p < D.adm_len[i] && D.adm[D.adm_off[i] + p] == code) D.fpos[i] = p + 1;
+      }
+      if (acc > 0) {
+        const long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrE]), 1ull);
+        D.e_key[slot] = ke;
+        D.e_val[slot] = acc;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      D.da_cnt[code] = 0;
+      D.da_fill[code] = 0;
+    }
+  }
+}
+
+// After a round that went the sorted way: the per-cluster counts back to 0.
+__global__ void ot_da_clear_kernel(OtDev D) {
+  const int nt = (int)D.ctr[kCtrTouch];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    const int code = D.da_touch[t];
+    D.da_cnt[code] = 0;
+    D.da_fill[code] = 0;
+  }
+}
+
 // ---- updates -------------------------------------------------------------------
 // Copies each demand cluster gave this phase (final claims sorted by code).
 __global__ void ot_consumed_kernel(OtDev D, const unsigned long long* __restrict__ key,
@@ -517,6 +666,22 @@ cudaError_t ot_dev_cut_init(OtDev& D, cudaStream_t s) {
 
 cudaError_t ot_dev_propose(OtDev& D, cudaStream_t s) {
   ot_da_propose_kernel<<<148 * 4, 256, 0, s>>>(D);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_da_rounds(OtDev& D, int rounds, cudaStream_t s) {
+  for (int r = 0; r < rounds; ++r) {
+    ot_da_propose_batched_kernel<<<148 * 2, 256, 0, s>>>(D);
+    ot_da_count_kernel<<<148 * 2, 256, 0, s>>>(D);
+    ot_da_alloc_kernel<<<148, 256, 0, s>>>(D);
+    ot_da_scatter_kernel<<<148 * 2, 256, 0, s>>>(D);
+    ot_da_resolve_warp_kernel<<<148 * 2, 256, 0, s>>>(D);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_da_clear(OtDev& D, cudaStream_t s) {
+  ot_da_clear_kernel<<<148, 256, 0, s>>>(D);
   return cudaGetLastError();
 }
 

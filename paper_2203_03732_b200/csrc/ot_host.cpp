@@ -470,7 +470,7 @@ class OtSolver {
   enum Buf {
     bT, bDy, bDfree, bDmatched, bConsumed, bFlOff, bFlCode, bFlB, bFlCnt, bFlPre, bSy, bSfree, bSmatched,
     bSfreed, bFb, bFy, bFpos, bFidx, bFu0, bFu, bAdmLen, bAdmOff, bAdm, bEk0, bEv0, bEk1, bEv1, bRk0, bRv0,
-    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bNum
+    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bDaCnt, bDaFill, bDaOff, bDaTouch, bNum
   };
   otprg::OtDev D_{};
   int64_t fl_cap_ = 0, adm_cap_ = 0, e_cap_ = 0, r_cap_ = 0;
@@ -478,6 +478,13 @@ class OtSolver {
   int launches_ = 0;
   int64_t scan_bytes_ = 0;
   int64_t* hctr_ = nullptr;  // pinned: counters + status
+  // DA rounds launched per host look (0: the sorted, one-sync-per-round path;
+  // OTPRG_OT_DA_BATCH), rounds that fell back to the sort
+  int da_batch_ = [] {
+    const char* e = std::getenv("OTPRG_OT_DA_BATCH");
+    return e ? std::max(0, std::atoi(e)) : 4;
+  }();
+  int64_t sorted_rounds_ = 0;
 
   DevBuf& buf(Buf b) { return ctx_->ot_dev[b]; }
   template <typename T>
@@ -515,6 +522,12 @@ class OtSolver {
     D_.fu = ensure<int64_t>(bFu, nb);
     D_.adm_len = ensure<int64_t>(bAdmLen, nb + 1);
     D_.adm_off = ensure<int64_t>(bAdmOff, nb + 1);
+    D_.da_cnt = ensure<int32_t>(bDaCnt, na2);
+    D_.da_fill = ensure<int32_t>(bDaFill, na2);
+    D_.da_off = ensure<int64_t>(bDaOff, na2);
+    D_.da_touch = ensure<int32_t>(bDaTouch, na2);
+    OT_CK(cudaMemsetAsync(D_.da_cnt, 0, na2 * 4, ctx_->stream), "memset");
+    OT_CK(cudaMemsetAsync(D_.da_fill, 0, na2 * 4, ctx_->stream), "memset");
     D_.ctr = ensure<int64_t>(bCtr, otprg::kCtrCount + 8);
     D_.status = reinterpret_cast<int*>(D_.ctr + otprg::kCtrCount);
     D_.err = reinterpret_cast<int32_t*>(D_.ctr + otprg::kCtrCount + 1);
@@ -777,22 +790,51 @@ class OtSolver {
       const int end_bit = 21 + 1 + static_cast<int>(std::ceil(std::log2(2.0 * n_a_ + 1.0)));
       OT_CK(otprg::ot_dev_cut_init(D_, s), "cut init");
       launches_ += 1;
-      while (true) {
-        OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrNew], 0, 8, s), "memset");
-        OT_CK(otprg::ot_dev_propose(D_, s), "propose");
-        read_ctr();
-        const int64_t n_new = hctr_[otprg::kCtrNew];
+      D_.s_key = buf(bEk1).as<unsigned long long>();
+      D_.s_val = buf(bEv1).as<int64_t>();
+      if (da_batch_ > 0) {
+        // device-sized rounds, da_batch_ per host look (ot_dev_da_rounds)
+        while (true) {
+          OT_CK(otprg::ot_dev_da_rounds(D_, da_batch_, s), "DA rounds");
+          launches_ += 5 * da_batch_;
+          read_ctr();
+          const int64_t done = hctr_[otprg::kCtrDone];
+          if (done == 1) break;
+          if (done == 2) {  // a cluster with more entries than a warp resolves: this round sorted
+            const int64_t n = hctr_[otprg::kCtrN];
+            sort(buf(bEk0).as<unsigned long long>(), buf(bEk1).as<unsigned long long>(), buf(bEv0).as<int64_t>(),
+                 buf(bEv1).as<int64_t>(), n, std::min(64, end_bit));
+            OT_CK(otprg::ot_dev_resolve(D_, buf(bEk1).as<unsigned long long>(), buf(bEv1).as<int64_t>(), n,
+                                        buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), s),
+                  "resolve");
+            OT_CK(otprg::ot_dev_da_clear(D_, s), "DA clear");
+            OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrNew], 0, 8, s), "memset");
+            OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrDone], 0, 8, s), "memset");
+            OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrBig], 0, 8, s), "memset");
+            launches_ += 2;
+            ++sorted_rounds_;
+          }
+        }
         n_e = hctr_[otprg::kCtrE];
-        if (n_new == 0) break;
-        const int64_t n = n_e + n_new;
-        sort(buf(bEk0).as<unsigned long long>(), buf(bEk1).as<unsigned long long>(), buf(bEv0).as<int64_t>(),
-             buf(bEv1).as<int64_t>(), n, std::min(64, end_bit));
-        OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrE], 0, 8, s), "memset");
-        OT_CK(otprg::ot_dev_resolve(D_, buf(bEk1).as<unsigned long long>(), buf(bEv1).as<int64_t>(), n,
-                                    buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), s),
-              "resolve");
-        launches_ += 2;
-        ++rounds_total;
+        rounds_total += hctr_[otprg::kCtrRounds];
+      } else {
+        while (true) {
+          OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrNew], 0, 8, s), "memset");
+          OT_CK(otprg::ot_dev_propose(D_, s), "propose");
+          read_ctr();
+          const int64_t n_new = hctr_[otprg::kCtrNew];
+          n_e = hctr_[otprg::kCtrE];
+          if (n_new == 0) break;
+          const int64_t n = n_e + n_new;
+          sort(buf(bEk0).as<unsigned long long>(), buf(bEk1).as<unsigned long long>(), buf(bEv0).as<int64_t>(),
+               buf(bEv1).as<int64_t>(), n, std::min(64, end_bit));
+          OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrE], 0, 8, s), "memset");
+          OT_CK(otprg::ot_dev_resolve(D_, buf(bEk1).as<unsigned long long>(), buf(bEv1).as<int64_t>(), n,
+                                      buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), s),
+                "resolve");
+          launches_ += 2;
+          ++rounds_total;
+        }
       }
       // updates (K11): consumed copies, displaced partners, records of the next state
       const int64_t rec_need = n_flows_ + n_e + 2 * static_cast<int64_t>(n_a_) + 16;
@@ -853,8 +895,8 @@ class OtSolver {
     st_ = export_state();
     r_->loop_ms = loop_t.ms();
     if (std::getenv("OTPRG_OT_PROFILE"))
-      std::fprintf(stderr, "ot loop %.2f ms: %lld phases, %lld DA rounds\n", r_->loop_ms, (long long)phases,
-                   (long long)rounds_total);
+      std::fprintf(stderr, "ot loop %.2f ms: %lld phases, %lld DA rounds (%lld sorted)\n", r_->loop_ms,
+                   (long long)phases, (long long)rounds_total, (long long)sorted_rounds_);
     r_->scan_ms = 0.0;
     r_->bytes_touched = scan_bytes_;
     r_->gpu_launches = launches_;
