@@ -259,49 +259,116 @@ __global__ void l1_normalize_kernel(const uint8_t* __restrict__ img, int count, 
 // ascending p exactly like the reference (no reassociation, no FMA), so the
 // bits match.  Block tile 64 a x 64 b, thread tile 4 x 4, pixels staged in
 // shared memory in chunks of kP, p-major.
-constexpr int kL1Tile = 64, kL1P = 16, kL1T = 4;
+#ifndef OTPRG_L1_TA
+#define OTPRG_L1_TA 4
+#endif
+#ifndef OTPRG_L1_TB
+#define OTPRG_L1_TB 4
+#endif
+#ifndef OTPRG_L1_MINB
+#define OTPRG_L1_MINB 1
+#endif
+constexpr int kL1TA = OTPRG_L1_TA, kL1TB = OTPRG_L1_TB;  // a / b entries per thread
+constexpr int kL1TileA = 16 * kL1TA, kL1TileB = 16 * kL1TB, kL1P = 16, kL1MaxList = 2048;
+
+// Pixel-support masks: bit p of tile g's words is set when any image of the
+// image tile g has pixel p != 0.  A pixel that is zero in every image of
+// both tiles adds |0 - 0| = +0 to every sum of the block, which leaves the
+// sum's bits unchanged (acc >= +0), so l1_round_kernel walks only the union
+// of the two tiles' supports (config 3: about half the frame is empty).
+__global__ void l1_tile_mask_kernel(const double* __restrict__ x, int n, int dim, int tiles, int rows,
+                                    uint32_t* __restrict__ mask) {
+  const int nw = (dim + 31) / 32;
+  for (int g = blockIdx.x; g < tiles; g += gridDim.x) {
+    const int r0 = g * rows, r1 = min(n, r0 + rows);
+    for (int p0 = 0; p0 < nw * 32; p0 += blockDim.x) {
+      const int p = p0 + threadIdx.x;
+      bool any = false;
+      if (p < dim)
+        for (int r = r0; r < r1 && !any; ++r) any = x[(size_t)r * dim + p] != 0.0;
+      const unsigned bal = __ballot_sync(kFull, any);
+      if ((threadIdx.x & 31) == 0 && p < nw * 32) mask[(size_t)g * nw + (p >> 5)] = bal;
+    }
+  }
+}
+
 template <typename T, bool kStore = true>
-__global__ void __launch_bounds__(256) l1_round_kernel(const double* __restrict__ xa,
+__global__ void __launch_bounds__(256, OTPRG_L1_MINB) l1_round_kernel(const double* __restrict__ xa,
                                                        const double* __restrict__ yb, int n_ai,
                                                        int n_bi, int dim, double eps,
-                                                       T* __restrict__ kT, int lda, int* status) {
-  __shared__ __align__(16) double As[kL1P][kL1Tile];
-  __shared__ __align__(16) double Bs[kL1P][kL1Tile];
+                                                       T* __restrict__ kT, int lda, int* status,
+                                                       const uint32_t* __restrict__ mask_a,
+                                                       const uint32_t* __restrict__ mask_b) {
+  __shared__ __align__(16) double As[kL1P][kL1TileA];
+  __shared__ __align__(16) double Bs[kL1P][kL1TileB];
+  __shared__ short s_pl[kL1MaxList];  // ascending pixels in either tile's support
+  __shared__ int s_np;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int a0 = blockIdx.x * kL1Tile, b0 = blockIdx.y * kL1Tile;
-  double acc[kL1T][kL1T];
+  const int a0 = blockIdx.x * kL1TileA, b0 = blockIdx.y * kL1TileB;
+  const bool listed = mask_a != nullptr;  // (dim <= kL1MaxList)
+  int np = dim;
+  if (listed) {
+    if (threadIdx.x < 32) {
+      const int nw = (dim + 31) / 32;
+      const uint32_t* ma = mask_a + (size_t)blockIdx.x * nw;
+      const uint32_t* mb = mask_b + (size_t)blockIdx.y * nw;
+      int base = 0;
+      for (int w0 = 0; w0 < nw; w0 += 32) {
+        const int w = w0 + (int)threadIdx.x;
+        uint32_t m = w < nw ? (ma[w] | mb[w]) : 0u;
+        const int c = __popc(m);
+        int inc = c;
 #pragma unroll
-  for (int i = 0; i < kL1T; ++i)
-#pragma unroll
-    for (int j = 0; j < kL1T; ++j) acc[i][j] = 0.0;
-  for (int p0 = 0; p0 < dim; p0 += kL1P) {
-    for (int e = threadIdx.x; e < kL1Tile * kL1P; e += blockDim.x) {
-      const int r = e / kL1P, pp = e % kL1P, p = p0 + pp;
-      const int a = a0 + r, b = b0 + r;
-      As[pp][r] = (a < n_ai && p < dim) ? xa[(size_t)a * dim + p] : 0.0;
-      Bs[pp][r] = (b < n_bi && p < dim) ? yb[(size_t)b * dim + p] : 0.0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, inc, o);
+          if ((int)threadIdx.x >= o) inc += y;
+        }
+        int pos = base + inc - c;
+        while (m) {
+          s_pl[pos++] = (short)(w * 32 + __ffs(m) - 1);
+          m &= m - 1;
+        }
+        base += __shfl_sync(kFull, inc, 31);
+      }
+      if (threadIdx.x == 0) s_np = base;
     }
     __syncthreads();
-    const int pend = min(kL1P, dim - p0);
+    np = s_np;
+  }
+  double acc[kL1TA][kL1TB];
+#pragma unroll
+  for (int i = 0; i < kL1TA; ++i)
+#pragma unroll
+    for (int j = 0; j < kL1TB; ++j) acc[i][j] = 0.0;
+  for (int p0 = 0; p0 < np; p0 += kL1P) {
+    for (int e = threadIdx.x; e < max(kL1TileA, kL1TileB) * kL1P; e += blockDim.x) {
+      const int r = e / kL1P, pp = e % kL1P, q = p0 + pp;
+      const int p = q < np ? (listed ? (int)s_pl[q] : q) : -1;
+      const int a = a0 + r, b = b0 + r;
+      if (r < kL1TileA) As[pp][r] = (a < n_ai && p >= 0) ? xa[(size_t)a * dim + p] : 0.0;
+      if (r < kL1TileB) Bs[pp][r] = (b < n_bi && p >= 0) ? yb[(size_t)b * dim + p] : 0.0;
+    }
+    __syncthreads();
+    const int pend = min(kL1P, np - p0);
     for (int pp = 0; pp < pend; ++pp) {
-      double av[kL1T], bv[kL1T];
+      double av[kL1TA], bv[kL1TB];
 #pragma unroll
-      for (int i = 0; i < kL1T; ++i) av[i] = As[pp][ty * kL1T + i];
+      for (int i = 0; i < kL1TA; ++i) av[i] = As[pp][ty * kL1TA + i];
 #pragma unroll
-      for (int j = 0; j < kL1T; ++j) bv[j] = Bs[pp][tx * kL1T + j];
+      for (int j = 0; j < kL1TB; ++j) bv[j] = Bs[pp][tx * kL1TB + j];
 #pragma unroll
-      for (int i = 0; i < kL1T; ++i)
+      for (int i = 0; i < kL1TA; ++i)
 #pragma unroll
-        for (int j = 0; j < kL1T; ++j) acc[i][j] = __dadd_rn(acc[i][j], fabs(__dsub_rn(av[i], bv[j])));
+        for (int j = 0; j < kL1TB; ++j) acc[i][j] = __dadd_rn(acc[i][j], fabs(__dsub_rn(av[i], bv[j])));
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < kL1T; ++i) {
-    const int a = a0 + ty * kL1T + i;
+  for (int i = 0; i < kL1TA; ++i) {
+    const int a = a0 + ty * kL1TA + i;
 #pragma unroll
-    for (int j = 0; j < kL1T; ++j) {
-      const int b = b0 + tx * kL1T + j;
+    for (int j = 0; j < kL1TB; ++j) {
+      const int b = b0 + tx * kL1TB + j;
       if (b >= n_bi) continue;
       if (a < n_ai) {
         const double c = __ddiv_rn(acc[i][j], 2.0);
@@ -454,22 +521,50 @@ cudaError_t launch_l1_normalize(const uint8_t* img, int count, int dim, double* 
   return cudaGetLastError();
 }
 
+size_t l1_mask_bytes(int n_ai, int n_bi, int lda, int dim) {
+  const int tiles = std::max(lda, n_ai) / kL1TileA + 1 + (n_bi + kL1TileB - 1) / kL1TileB;
+  return (size_t)tiles * ((dim + 31) / 32) * sizeof(uint32_t);
+}
+
+namespace {
+// masks of the A tiles (grid.x of them) and B tiles (grid.y); false when the
+// walk goes over every pixel (dim beyond the list, or no mask buffer)
+bool l1_masks(const double* xa, const double* yb, int n_ai, int n_bi, int dim, dim3 grid, uint32_t* masks,
+              const uint32_t** ma, const uint32_t** mb, cudaStream_t s) {
+  *ma = *mb = nullptr;
+  if (!masks || dim > kL1MaxList) return false;
+  const int nw = (dim + 31) / 32;
+  uint32_t* b_masks = masks + (size_t)grid.x * nw;
+  const int thr = std::min(1024, nw * 32);
+  l1_tile_mask_kernel<<<std::min<int>(grid.x, 4096), thr, 0, s>>>(xa, n_ai, dim, grid.x, kL1TileA, masks);
+  l1_tile_mask_kernel<<<std::min<int>(grid.y, 4096), thr, 0, s>>>(yb, n_bi, dim, grid.y, kL1TileB, b_masks);
+  *ma = masks;
+  *mb = b_masks;
+  return true;
+}
+}  // namespace
+
 cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_bi, int dim,
                             double eps, void* kT, int lda, int width, int* status,
-                            cudaStream_t s) {
-  dim3 grid(lda / kL1Tile, (n_bi + kL1Tile - 1) / kL1Tile);
+                            cudaStream_t s, uint32_t* masks) {
+  dim3 grid((lda + kL1TileA - 1) / kL1TileA, (n_bi + kL1TileB - 1) / kL1TileB);
+  const uint32_t *ma, *mb;
+  l1_masks(xa, yb, n_ai, n_bi, dim, grid, masks, &ma, &mb, s);
   with_width(width, [&](auto tag) {
     using T = decltype(tag);
-    l1_round_kernel<T><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps, static_cast<T*>(kT), lda, status);
+    l1_round_kernel<T><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, eps, static_cast<T*>(kT), lda, status, ma,
+                                            mb);
     return 0;
   });
   return cudaGetLastError();
 }
 
 cudaError_t launch_l1_check(const double* xa, const double* yb, int n_ai, int n_bi, int dim, int* status,
-                            cudaStream_t s) {
-  dim3 grid((n_ai + kL1Tile - 1) / kL1Tile, (n_bi + kL1Tile - 1) / kL1Tile);
-  l1_round_kernel<uint8_t, false><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, 0.5, nullptr, 0, status);
+                            cudaStream_t s, uint32_t* masks) {
+  dim3 grid((n_ai + kL1TileA - 1) / kL1TileA, (n_bi + kL1TileB - 1) / kL1TileB);
+  const uint32_t *ma, *mb;
+  l1_masks(xa, yb, n_ai, n_bi, dim, grid, masks, &ma, &mb, s);
+  l1_round_kernel<uint8_t, false><<<grid, 256, 0, s>>>(xa, yb, n_ai, n_bi, dim, 0.5, nullptr, 0, status, ma, mb);
   return cudaGetLastError();
 }
 

@@ -77,11 +77,16 @@ cudaError_t launch_points_range(const double* pa, const double* pb, int n_a, int
 // when a cost leaves [0,1]).  lda must be a multiple of 64.
 cudaError_t launch_l1_normalize(const uint8_t* img, int count, int dim, double* out, int* status,
                                 cudaStream_t s);
+// masks: scratch of l1_mask_bytes() for the tiles' pixel-support masks (the
+// sums skip pixels that are zero in every image of both tiles; nullptr: every
+// pixel is summed).
+size_t l1_mask_bytes(int n_ai, int n_bi, int lda, int dim);
 cudaError_t launch_l1_round(const double* xa, const double* yb, int n_ai, int n_bi, int dim,
-                            double eps, void* kT, int lda, int width, int* status, cudaStream_t s);
+                            double eps, void* kT, int lda, int width, int* status, cudaStream_t s,
+                            uint32_t* masks);
 // The range check of K3 alone (status 2 when a cost leaves [0,1]), no kT.
 cudaError_t launch_l1_check(const double* xa, const double* yb, int n_ai, int n_bi, int dim, int* status,
-                            cudaStream_t s);
+                            cudaStream_t s, uint32_t* masks);
 // out[p * n + i] = in[i * dim + p] (pixels of the on-the-fly L1 scans).
 cudaError_t launch_transpose_f64(const double* in, int n, int dim, double* out, cudaStream_t s);
 // Costs of the matched pairs of an L1 image instance (thread per original a).

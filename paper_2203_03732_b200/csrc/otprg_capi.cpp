@@ -229,10 +229,11 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
     int* status = &ctx->ctl.as<Ctl>()->status;
     CK(otprg::launch_l1_normalize(raw, static_cast<int>(ia + ib), p->dim, xa, status, ctx->stream),
        "l1 normalize launch");
+    CK(ctx->l1_mask.ensure(otprg::l1_mask_bytes(ctx->ia, ctx->ib, ctx->lda, p->dim)), "alloc masks");
     CK(otprg::launch_l1_round(xa, yb, ctx->ia, ctx->ib, p->dim, p->eps, ctx->kT.p, ctx->lda, width,
-                              status, ctx->stream),
+                              status, ctx->stream, ctx->l1_mask.as<uint32_t>()),
        "l1 round launch");
-    ctx->build_launches = 2;
+    ctx->build_launches = 4;
     ctx->img_dim = p->dim;
     ctx->img_a.assign(p->img_a, p->img_a + dim * p->n_a);
     ctx->img_b.assign(p->img_b, p->img_b + dim * p->n_b);

@@ -522,13 +522,17 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
     int* status = &ctx->ctl.as<Ctl>()->status;
     CK(otprg::launch_l1_normalize(raw, static_cast<int>(ia + ib), p->dim, xa, status, ctx->stream), "l1 normalize");
     if (ctx->sh_otf) {
-      CK(otprg::launch_l1_check(xa, yb, ctx->ia, ctx->ib, p->dim, status, ctx->stream), "l1 check");
+      CK(ctx->l1_mask.ensure(otprg::l1_mask_bytes(ctx->ia, ctx->ib, ctx->ia, p->dim)), "alloc masks");
+      CK(otprg::launch_l1_check(xa, yb, ctx->ia, ctx->ib, p->dim, status, ctx->stream, ctx->l1_mask.as<uint32_t>()),
+         "l1 check");
       CK(otprg::launch_transpose_f64(xa, ctx->ia, p->dim,
                                      reinterpret_cast<double*>(static_cast<char*>(ctx->pts.p) + xt_off), ctx->stream),
          "transpose");
     } else if (ctx->sh_hi > ctx->sh_lo) {
+      CK(ctx->l1_mask.ensure(otprg::l1_mask_bytes(ctx->sh_hi - ctx->sh_lo, ctx->ib, ctx->lda, p->dim)), "alloc masks");
       CK(otprg::launch_l1_round(xa + static_cast<size_t>(ctx->sh_lo) * dim, yb, ctx->sh_hi - ctx->sh_lo, ctx->ib,
-                                p->dim, p->eps, ctx->kT.p, ctx->lda, width, status, ctx->stream),
+                                p->dim, p->eps, ctx->kT.p, ctx->lda, width, status, ctx->stream,
+                                ctx->l1_mask.as<uint32_t>()),
          "l1 round");
     }
     int dstatus = 0;

@@ -91,3 +91,29 @@ def test_validation_errors():  # test_ot.cpp:127-135
         otprg.solve_ot(bad, 0.1)
     with pytest.raises(otprg.ParameterError):
         otprg.solve_ot(otprg.OTInstance(np.array([1.0]), np.array([1.0]), np.array([[1.5]])), 0.1)
+
+
+def _same_as_reference(reference, mu, nu, cost, eps):
+    inst = otprg.OTInstance(mu, nu, cost)
+    plan, stats = otprg.solve_ot(inst, eps)
+    r = reference.solve_ot(mu, nu, cost, eps)
+    assert stats.phases == r["phases"] and stats.sum_ni == r["sum_ni"]
+    assert np.array_equal(plan.a, r["a"]) and np.array_equal(plan.b, r["b"])
+    assert np.array_equal(plan.mass, r["mass"]) and float(plan.cost).hex() == float(r["cost"]).hex()
+
+
+@pytest.mark.parametrize("batch", ["0", "1", "4"])
+def test_da_round_paths_on_degenerate_costs(reference, monkeypatch, batch):
+    """The claim rounds with host-sized sorts (batch 0) and device-sized
+    segments (ot_dev_da_rounds): constant and two-level costs send every free
+    b to the same cluster (segments past kDaWarpMax take the sorted round),
+    few-level costs give runs of re-proposals; plans equal the reference's."""
+    monkeypatch.setenv("OTPRG_OT_DA_BATCH", batch)
+    rng = np.random.default_rng(7)
+    for n_a, n_b, levels in ((40, 900, 1), (600, 600, 2), (300, 700, 5), (257, 1000, 3)):
+        mu = rng.integers(1, 50, n_a).astype(np.float64)
+        nu = rng.integers(1, 50, n_b).astype(np.float64)
+        mu /= mu.sum()
+        nu /= nu.sum()
+        cost = rng.integers(0, levels, (n_a, n_b)) / max(1, levels - 1) if levels > 1 else np.full((n_a, n_b), 0.5)
+        _same_as_reference(reference, mu, nu, cost, 0.05)
