@@ -117,95 +117,201 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+#ifndef OTPRG_K2_ROWS
+#define OTPRG_K2_ROWS 2
+#endif
+constexpr int kK2Rows = OTPRG_K2_ROWS;  // supply rows per loop iteration (amortises the row overhead)
+
+template <typename T>
+struct K2Shape {
+  // entries per thread (one 8-byte store for u8, 16-byte for u16 / u32), per 32-bit word
+  static constexpr int kV = sizeof(T) == 1 ? 8 : 16 / sizeof(T), kPer = 4 / sizeof(T), kW = kV / kPer;
+};
+
+// The exact level of entries (b, a0 .. a0 + kV) from FP64 d2 and the table,
+// walking up from floor(x_f) - 2 (<= the level: |x_f - x| < margin < 1);
+// pads (a >= n_ai) get the type maximum.  The rare lanes near a level
+// boundary, inline or deferred to round_points_fix_kernel.
+template <typename T>
+__device__ __forceinline__ void k2_exact_row(const double2* __restrict__ pa, double2 q, int n_ai, int a0,
+                                             const double* thr, int uf, float inv_step, T* __restrict__ out) {
+  constexpr int kV = K2Shape<T>::kV, kPer = K2Shape<T>::kPer, kW = K2Shape<T>::kW;
+  const float qx = __double2float_rn(q.x), qy = __double2float_rn(q.y);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < kV; ++j) {
+    uint32_t v = type_max<T>();
+    if (a0 + j < n_ai) {
+      const double2 p = pa[a0 + j];
+      const float dx = __double2float_rn(p.x) - qx, dy = __double2float_rn(p.y) - qy;
+      const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
+      const float y = __fadd_rn(z, 12582912.0f);
+      const double ex = __dsub_rn(p.x, q.x), ey = __dsub_rn(p.y, q.y);
+      const double d2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+      int k = max(0, min((int)(__float_as_uint(y) - 0x4B400000u) - 2, uf));
+      while (k < uf && thr[k + 1] <= d2) ++k;
+      v = (uint32_t)k;
+    }
+    w[j / kPer] |= v << (8 * sizeof(T) * (j % kPer));
+  }
+  if constexpr (kW == 2)
+    *reinterpret_cast<uint2*>(out) = make_uint2(w[0], w[1]);
+  else
+    *reinterpret_cast<uint4*>(out) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// The rows of one thread: kR supply rows per iteration, all kR * kV estimates
+// first (branch-free, independent: ILP across entries), one store per row.
+// A row with an entry within margin of a level boundary is queued as (b, a0)
+// in this block's fix-up list (fixed by round_points_fix_kernel after the
+// build; inline when the list is full), so the fast loop never recomputes.
+// kPad: this thread's 16 bytes include pad columns (a >= n_ai), which hold
+// the type maximum.
+template <typename T, bool kPad, int kR>
+__device__ __forceinline__ void k2_rows(const float2 (&pf)[K2Shape<T>::kV], const double2* __restrict__ pa,
+                                        const double2* __restrict__ pb, int n_ai, int n_bi, const double* s_thr,
+                                        int uf, float inv_step, float lim, const uint32_t (&padw)[4],
+                                        T* __restrict__ kT, int lda, int a0, uint2* fix, int fix_cap,
+                                        int* s_fix) {
+  constexpr int kV = K2Shape<T>::kV, kW = K2Shape<T>::kW;
+  const int step = gridDim.y;
+  double2 qn[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int b = blockIdx.y + r * step;
+    qn[r] = b < n_bi ? pb[b] : make_double2(0.0, 0.0);
+  }
+  for (int b = blockIdx.y; b < n_bi; b += kR * step) {
+    double2 q[kR];
+    float qx[kR], qy[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      q[r] = qn[r];  // the next rows' points are in flight during these rows
+      const int nb = b + (kR + r) * step;
+      if (nb < n_bi) qn[r] = pb[nb];
+      qx[r] = __double2float_rn(q[r].x);
+      qy[r] = __double2float_rn(q[r].y);
+    }
+    // z = x_f - 1/2 and y = z + 1.5 * 2^23 (FP32): y's low bits are then
+    // rint(z) = floor(x_f), and |z - rint(z)| = 1/2 - (distance of x_f to the
+    // nearest integer) — so one max per row tells whether any entry lies
+    // within margin of a level boundary (FP32/INT only; the float->int
+    // conversion pipe is quarter rate and was the limit).
+    uint32_t yv[kR][kV];
+    float dm[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      dm[r] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kV; ++j) {
+        const float dx = pf[j].x - qx[r], dy = pf[j].y - qy[r];
+        const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
+        const float y = __fadd_rn(z, 12582912.0f);
+        yv[r][j] = __float_as_uint(y);
+        dm[r] = fmaxf(dm[r], fabsf(__fsub_rn(z, __fsub_rn(y, 12582912.0f))));
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int br = b + r * step;
+      if (br >= n_bi) break;
+      uint32_t w[4];
+      if constexpr (sizeof(T) == 1) {
+#pragma unroll
+        for (int q4 = 0; q4 < kW; ++q4)
+          w[q4] = __byte_perm(__byte_perm(yv[r][4 * q4], yv[r][4 * q4 + 1], 0x0040),
+                              __byte_perm(yv[r][4 * q4 + 2], yv[r][4 * q4 + 3], 0x0040), 0x5410);
+      } else if constexpr (sizeof(T) == 2) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) w[q4] = __byte_perm(yv[r][2 * q4], yv[r][2 * q4 + 1], 0x5410);
+      } else {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) w[q4] = yv[r][q4] - 0x4B400000u;
+      }
+      if constexpr (kPad) {
+#pragma unroll
+        for (int q4 = 0; q4 < kW; ++q4) w[q4] |= padw[q4];
+      }
+      T* out = kT + (size_t)br * lda + a0;
+      if (dm[r] >= lim) {  // near a level boundary: exact, now or after the build
+        const int slot = atomicAdd(s_fix, 1);
+        if (slot < fix_cap) {
+          fix[slot] = make_uint2((uint32_t)br, (uint32_t)a0);
+        } else {
+          k2_exact_row<T>(pa, q[r], n_ai, a0, s_thr, uf, inv_step, out);
+          continue;
+        }
+      }
+      if constexpr (kW == 2)
+        *reinterpret_cast<uint2*>(out) = make_uint2(w[0], w[1]);
+      else
+        *reinterpret_cast<uint4*>(out) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+// fix: per block (linear index) a count word in fix_cnt and fix_cap entries.
 template <typename T>
 __global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __restrict__ pa,
                                                                const double2* __restrict__ pb,
                                                                int n_ai, int n_bi, const double* __restrict__ thr,
                                                                int thr_n, float inv_step, float margin,
-                                                               T* __restrict__ kT, int lda) {
-  // entries per thread (one 8-byte store for u8, 16-byte for u16 / u32), per 32-bit word
-  constexpr int kV = sizeof(T) == 1 ? 8 : 16 / sizeof(T), kPer = 4 / sizeof(T), kW = kV / kPer;
-  // shared: this block's demand points in double (the slow path's exact d2
-  // reads them here instead of from L2), then the threshold table
-  extern __shared__ __align__(16) double s_dyn_k2[];
-  double2* s_pts = reinterpret_cast<double2*>(s_dyn_k2);
-  double* s_thr = s_dyn_k2 + 2 * kV * blockDim.x;
+                                                               T* __restrict__ kT, int lda, uint2* __restrict__ fix,
+                                                               int* __restrict__ fix_cnt, int fix_cap) {
+  constexpr int kV = K2Shape<T>::kV, kPer = K2Shape<T>::kPer;
+  extern __shared__ __align__(16) double s_thr[];  // the threshold table (the inline exact rows)
+  __shared__ int s_fix;
   for (int j = threadIdx.x; j < thr_n; j += blockDim.x) s_thr[j] = thr[j];
+  if (threadIdx.x == 0) s_fix = 0;
   const int uf = thr_n - 2;  // unit_floor: thr[uf + 1] = +inf
   const float lim = 0.5f - margin;  // |z - rint(z)| >= lim: within margin of a level boundary
   const int a0 = (blockIdx.x * blockDim.x + threadIdx.x) * kV;
+  const int blk = blockIdx.y * gridDim.x + blockIdx.x;
   float2 pf[kV];
-  double2* my = s_pts + threadIdx.x * kV;
 #pragma unroll
   for (int j = 0; j < kV; ++j) {
     const double2 p = a0 + j < n_ai ? pa[a0 + j] : make_double2(0.0, 0.0);
-    my[j] = p;
     pf[j] = make_float2(__double2float_rn(p.x), __double2float_rn(p.y));
   }
   __syncthreads();
-  if (a0 >= lda) return;
-  // pad entries (a >= n_ai) hold the type maximum
-  uint32_t padw[4] = {0u, 0u, 0u, 0u};
+  if (a0 < lda) {
+    // pad entries (a >= n_ai) hold the type maximum
+    uint32_t padw[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-  for (int j = 0; j < kV; ++j)
-    if (a0 + j >= n_ai) padw[j / kPer] |= type_max<T>() << (8 * sizeof(T) * (j % kPer));
-  double2 q_next = blockIdx.y < (unsigned)n_bi ? pb[blockIdx.y] : make_double2(0.0, 0.0);
-  for (int b = blockIdx.y; b < n_bi; b += gridDim.y) {
-    const double2 q = q_next;  // the next row's point is in flight during this row
-    if (b + (int)gridDim.y < n_bi) q_next = pb[b + gridDim.y];
-    const float qx = __double2float_rn(q.x), qy = __double2float_rn(q.y);
-    // all kV estimates first (branch-free, independent: ILP across entries).
-    // z = x_f - 1/2 and y = z + 1.5 * 2^23 (FP32): y's low bits are then
-    // rint(z) = floor(x_f), and |z - rint(z)| = 1/2 - (distance of x_f to the
-    // nearest integer) — so one max over the kV entries tells whether any of
-    // them lies within margin of a level boundary (FP32/INT only; the
-    // float->int conversion pipe is quarter rate and was the limit).
-    uint32_t yv[kV];
-    float dmax = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kV; ++j) {
-      const float dx = pf[j].x - qx, dy = pf[j].y - qy;
-      const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
-      const float y = __fadd_rn(z, 12582912.0f);
-      yv[j] = __float_as_uint(y);
-      dmax = fmaxf(dmax, fabsf(__fsub_rn(z, __fsub_rn(y, 12582912.0f))));
-    }
-    if (dmax >= lim) {  // some entry near a level boundary: the exact FP64 d2 and the table
-#pragma unroll
-      for (int j = 0; j < kV; ++j) {
-        const float dx = pf[j].x - qx, dy = pf[j].y - qy;
-        const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
-        const float y = __fadd_rn(z, 12582912.0f);
-        if (fabsf(__fsub_rn(z, __fsub_rn(y, 12582912.0f))) >= lim) {
-          const double2 p = my[j];
-          const double ex = __dsub_rn(p.x, q.x), ey = __dsub_rn(p.y, q.y);
-          const double d2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
-          // floor(x_f) = yv - 0x4B400000 and |x_f - x| < margin < 1, so the exact
-          // level (>= floor(x) - 1 >= floor(x_f) - 2) is reached walking up from there
-          int k = max(0, min((int)(yv[j] - 0x4B400000u) - 2, uf));
-          while (k < uf && s_thr[k + 1] <= d2) ++k;
-          yv[j] = 0x4B400000u + (uint32_t)k;
-        }
-      }
-    }
-    uint32_t w[4];
-    if constexpr (sizeof(T) == 1) {
-#pragma unroll
-      for (int q4 = 0; q4 < kW; ++q4)
-        w[q4] = __byte_perm(__byte_perm(yv[4 * q4], yv[4 * q4 + 1], 0x0040), __byte_perm(yv[4 * q4 + 2], yv[4 * q4 + 3], 0x0040),
-                            0x5410);
-    } else if constexpr (sizeof(T) == 2) {
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) w[q4] = __byte_perm(yv[2 * q4], yv[2 * q4 + 1], 0x5410);
-    } else {
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) w[q4] = yv[q4] - 0x4B400000u;
-    }
-    if constexpr (kW == 2)
-      *reinterpret_cast<uint2*>(kT + (size_t)b * lda + a0) = make_uint2(w[0] | padw[0], w[1] | padw[1]);
+    for (int j = 0; j < kV; ++j)
+      if (a0 + j >= n_ai) padw[j / kPer] |= type_max<T>() << (8 * sizeof(T) * (j % kPer));
+    uint2* my_fix = fix + (size_t)blk * fix_cap;
+    if (a0 + kV <= n_ai)
+      k2_rows<T, false, kK2Rows>(pf, pa, pb, n_ai, n_bi, s_thr, uf, inv_step, lim, padw, kT, lda, a0, my_fix,
+                                 fix_cap, &s_fix);
     else
-      *reinterpret_cast<uint4*>(kT + (size_t)b * lda + a0) =
-          make_uint4(w[0] | padw[0], w[1] | padw[1], w[2] | padw[2], w[3] | padw[3]);
+      k2_rows<T, true, kK2Rows>(pf, pa, pb, n_ai, n_bi, s_thr, uf, inv_step, lim, padw, kT, lda, a0, my_fix,
+                                fix_cap, &s_fix);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) fix_cnt[blk] = min(s_fix, fix_cap);
+}
+
+// The queued rows: the exact levels, over the fast pass's stores.
+template <typename T>
+__global__ void __launch_bounds__(256) round_points_fix_kernel(const double2* __restrict__ pa,
+                                                               const double2* __restrict__ pb, int n_ai,
+                                                               const double* __restrict__ thr, int thr_n,
+                                                               float inv_step, T* __restrict__ kT, int lda,
+                                                               const uint2* __restrict__ fix,
+                                                               const int* __restrict__ fix_cnt, int fix_cap,
+                                                               int blocks) {
+  extern __shared__ __align__(16) double s_thr[];
+  for (int j = threadIdx.x; j < thr_n; j += blockDim.x) s_thr[j] = thr[j];
+  __syncthreads();
+  for (int blk = blockIdx.x; blk < blocks; blk += gridDim.x) {
+    const int n = fix_cnt[blk];
+    const uint2* f = fix + (size_t)blk * fix_cap;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const uint2 ba = f[e];
+      k2_exact_row<T>(pa, pb[ba.x], n_ai, (int)ba.y, s_thr, thr_n - 2, inv_step,
+                      kT + (size_t)ba.x * lda + ba.y);
+    }
   }
 }
 
@@ -461,38 +567,67 @@ cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swappe
   return cudaGetLastError();
 }
 
+namespace {
+// Bound on |x_f - x| (x = c / eps <= 1/eps + 1): float coordinates are off
+// by <= C 2^-24 each (C = max |coordinate|), so dx_f, dy_f by <= 3 C 2^-24
+// and d_f by <= 4.3 C 2^-24 + |d| 2^-22; x_f adds ~3 roundings (2^-22
+// relative, the approximate sqrt included).  margin = 4 x that bound.
+float k2_margin(double eps, double absmax) {
+  const double xmax = 1.0 / eps + 1.0;
+  const double bound = (4.3 * absmax * std::ldexp(1.0, -24) + std::sqrt(2.0) * std::ldexp(1.0, -22)) /
+                           (std::sqrt(2.0) * eps) + xmax * std::ldexp(1.0, -21);
+  return (float)std::min(0.5, 4.0 * bound + 1e-7);
+}
+constexpr int kK2MaxBlocks = 4096;
+}  // namespace
+
+size_t round_points_fix_bytes(int n_ai, int n_bi, int lda, int width, double eps, double absmax) {
+  // twice the expected rows with an entry within margin of a boundary (a
+  // full list only sends rows to the inline path), >= 1 M entries, <= 512 MB
+  const int kv = width == 1 ? 8 : 16 / width;
+  const double m = k2_margin(eps, absmax);
+  const double p_row = 1.0 - std::pow(std::max(0.0, 1.0 - 2.0 * m), kv);
+  const double rows = (double)n_bi * ((lda + kv - 1) / kv);
+  const double want = std::min(64.0 * 1024 * 1024, std::max(1024.0 * 1024, 2.0 * rows * p_row + 65536.0));
+  (void)n_ai;
+  return 256 + (size_t)want * sizeof(uint2) + kK2MaxBlocks * sizeof(int);
+}
+
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
                                   double eps, double sqrt2, const double* thr, int thr_n, double absmax,
-                                  void* kT, int lda, int width, cudaStream_t s) {
+                                  void* kT, int lda, int width, void* fix_buf, size_t fix_bytes, cudaStream_t s) {
   const double2* a2 = reinterpret_cast<const double2*>(pa);
   const double2* b2 = reinterpret_cast<const double2*>(pb);
-  if (thr && thr_n >= 2 && thr_n <= kThrSmemMax) {
+  if (thr && thr_n >= 2 && thr_n <= kThrSmemMax && fix_buf && fix_bytes > 256 + kK2MaxBlocks * sizeof(int)) {
     // threads own kV entries of a row (8 B for u8, 16 B otherwise); the grid is
     // one resident wave (occupancy-sized), the supply rows strided over grid.y
     const int kv = width == 1 ? 8 : 16 / width;
     const int threads_x = (lda + kv - 1) / kv;
     const int bx = (threads_x + 255) / 256;
     const float inv_step = (float)(1.0 / (std::sqrt(2.0) * eps));
-    // Bound on |x_f - x| (x = c / eps <= 1/eps + 1): float coordinates are off
-    // by <= C 2^-24 each (C = max |coordinate|), so dx_f, dy_f by <= 3 C 2^-24
-    // and d_f by <= 4.3 C 2^-24 + |d| 2^-22; x_f adds ~3 roundings (2^-22
-    // relative, the approximate sqrt included).  margin = 4 x that bound.
-    const double xmax = 1.0 / eps + 1.0;
-    const double bound = (4.3 * absmax * std::ldexp(1.0, -24) + std::sqrt(2.0) * std::ldexp(1.0, -22)) /
-                             (std::sqrt(2.0) * eps) + xmax * std::ldexp(1.0, -21);
-    const float margin = (float)std::min(0.5, 4.0 * bound + 1e-7);
-    const size_t smem = (size_t)thr_n * sizeof(double) + 256 * (size_t)kv * sizeof(double2);
+    const float margin = k2_margin(eps, absmax);
+    const size_t smem = (size_t)thr_n * sizeof(double);
+    int* fix_cnt = static_cast<int*>(fix_buf);
+    uint2* fix = reinterpret_cast<uint2*>(static_cast<char*>(fix_buf) + 256 + kK2MaxBlocks * sizeof(int));
+    const size_t fix_total = (fix_bytes - 256 - kK2MaxBlocks * sizeof(int)) / sizeof(uint2);
     with_width(width, [&](auto tag) {
       using T = decltype(tag);
       auto fn = round_points_thr_kernel<T>;
+      auto fx = round_points_fix_kernel<T>;
       smem_attr_raise(fn, smem);
+      smem_attr_raise(fx, smem);
       int per_sm = 0, dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
-      const int by = std::max(1, std::min(n_bi, sms * per_sm / bx));
-      fn<<<dim3(bx, std::min(by, 65535)), 256, smem, s>>>(a2, b2, n_ai, n_bi, thr, thr_n, inv_step, margin,
-                                                           static_cast<T*>(kT), lda);
+      int by = std::max(1, std::min(n_bi, sms * per_sm / bx));
+      by = std::min(by, std::max(1, kK2MaxBlocks / bx));
+      const int blocks = bx * by;
+      const int cap = (int)std::min<size_t>(fix_total / blocks, (size_t)1 << 30);
+      fn<<<dim3(bx, by), 256, smem, s>>>(a2, b2, n_ai, n_bi, thr, thr_n, inv_step, margin, static_cast<T*>(kT),
+                                         lda, fix, fix_cnt, cap);
+      fx<<<std::min(blocks, sms * 4), 256, smem, s>>>(a2, b2, n_ai, thr, thr_n, inv_step, static_cast<T*>(kT), lda,
+                                                      fix, fix_cnt, cap, blocks);
       return 0;
     });
     return cudaGetLastError();

@@ -10,7 +10,9 @@
 namespace otprg {
 
 cudaError_t smem_attr_raise(const void* fn, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;  // within the default limit
+  // (also below 48 KB: the default limit covers static + dynamic shared memory,
+  // so a kernel with static shared memory needs the opt-in earlier)
+  if (bytes == 0) return cudaSuccess;
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, size_t> set;
   int dev = 0;

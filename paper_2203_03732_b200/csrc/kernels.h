@@ -63,10 +63,13 @@ struct SolveArgs {
 cudaError_t launch_round_dense(const double* cost, int n_a, int n_b, bool swapped, double eps,
                                void* kT, int lda, int width, int* status, cudaStream_t s);
 // thr: exact threshold table (thr_n entries, <= 8192) or nullptr (exact
-// division form); absmax: the largest |coordinate| of either point set.
+// division form); absmax: the largest |coordinate| of either point set;
+// fix_buf: scratch of round_points_fix_bytes() for the rows deferred to the
+// exact fix-up pass (nullptr: the exact division form).
+size_t round_points_fix_bytes(int n_ai, int n_bi, int lda, int width, double eps, double absmax);
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
                                   double eps, double sqrt2, const double* thr, int thr_n, double absmax,
-                                  void* kT, int lda, int width, cudaStream_t s);
+                                  void* kT, int lda, int width, void* fix_buf, size_t fix_bytes, cudaStream_t s);
 // First (a, b) (row-major, original orientation) whose point cost is outside
 // [0, 1]: atomicMin into *first (initialise to ~0).
 cudaError_t launch_points_range(const double* pa, const double* pb, int n_a, int n_b, double d2_max,

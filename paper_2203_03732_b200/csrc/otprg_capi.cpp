@@ -252,11 +252,14 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
     if (st) return st;
     int thr_n = 0;
     if ((st = points_table(ctx, p->eps, &thr_n))) return st;
+    const size_t fix_bytes =
+        otprg::round_points_fix_bytes(ctx->ia, ctx->ib, ctx->lda, width, p->eps, ctx->pts_absmax);
+    CK(ctx->k2_fix.ensure(fix_bytes), "alloc K2 fix-up list");
     CK(otprg::launch_round_points2d(dpa, dpb, ctx->ia, ctx->ib, p->eps, std::sqrt(2.0),
                                     thr_n ? ctx->thr_dev.as<double>() : nullptr, thr_n, ctx->pts_absmax, ctx->kT.p,
-                                    ctx->lda, width, ctx->stream),
+                                    ctx->lda, width, ctx->k2_fix.p, fix_bytes, ctx->stream),
        "round_points launch");
-    ctx->build_launches = 1;
+    ctx->build_launches = thr_n ? 2 : 1;
     ctx->pts_a.assign(p->pts_a, p->pts_a + 2 * static_cast<size_t>(p->n_a));
     ctx->pts_b.assign(p->pts_b, p->pts_b + 2 * static_cast<size_t>(p->n_b));
   }

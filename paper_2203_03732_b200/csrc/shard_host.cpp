@@ -563,9 +563,13 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
       ctx->sh_thr_n = thr_n;
       ctx->sh_otf_tiled = otprg::shard_otf_tiled_fits(width, thr_n, ctx->device);
     } else if (ctx->sh_hi > ctx->sh_lo) {
+      const size_t fix_bytes = otprg::round_points_fix_bytes(ctx->sh_hi - ctx->sh_lo, ctx->ib, ctx->lda, width,
+                                                             p->eps, ctx->pts_absmax);
+      CK(ctx->k2_fix.ensure(fix_bytes), "alloc K2 fix-up list");
       CK(otprg::launch_round_points2d(dpa + static_cast<size_t>(ctx->sh_lo) * 2, dpb, ctx->sh_hi - ctx->sh_lo,
                                       ctx->ib, p->eps, std::sqrt(2.0), thr_n ? ctx->thr_dev.as<double>() : nullptr,
-                                      thr_n, ctx->pts_absmax, ctx->kT.p, ctx->lda, width, ctx->stream),
+                                      thr_n, ctx->pts_absmax, ctx->kT.p, ctx->lda, width, ctx->k2_fix.p, fix_bytes,
+                                      ctx->stream),
          "round_points launch");
     }
   }
