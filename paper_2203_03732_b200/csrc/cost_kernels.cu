@@ -117,135 +117,113 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-#ifndef OTPRG_K2_ROWS
-#define OTPRG_K2_ROWS 2
-#endif
-constexpr int kK2Rows = OTPRG_K2_ROWS;  // supply rows per loop iteration (amortises the row overhead)
-
 template <typename T>
 struct K2Shape {
-  // entries per thread (one 8-byte store for u8, 16-byte for u16 / u32), per 32-bit word
-  static constexpr int kV = sizeof(T) == 1 ? 8 : 16 / sizeof(T), kPer = 4 / sizeof(T), kW = kV / kPer;
+  // entries per thread (16 for u8 / u16, 8 for u32: one or two 16-byte
+  // stores per row), entries per 32-bit word, words
+  static constexpr int kV = sizeof(T) == 4 ? 8 : 16, kPer = 4 / sizeof(T), kW = kV / kPer;
 };
 
-// The exact level of entries (b, a0 .. a0 + kV) from FP64 d2 and the table,
-// walking up from floor(x_f) - 2 (<= the level: |x_f - x| < margin < 1);
-// pads (a >= n_ai) get the type maximum.  The rare lanes near a level
-// boundary, inline or deferred to round_points_fix_kernel.
-template <typename T>
-__device__ __forceinline__ void k2_exact_row(const double2* __restrict__ pa, double2 q, int n_ai, int a0,
-                                             const double* thr, int uf, float inv_step, T* __restrict__ out) {
-  constexpr int kV = K2Shape<T>::kV, kPer = K2Shape<T>::kPer, kW = K2Shape<T>::kW;
-  const float qx = __double2float_rn(q.x), qy = __double2float_rn(q.y);
-  uint32_t w[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-  for (int j = 0; j < kV; ++j) {
-    uint32_t v = type_max<T>();
-    if (a0 + j < n_ai) {
-      const double2 p = pa[a0 + j];
-      const float dx = __double2float_rn(p.x) - qx, dy = __double2float_rn(p.y) - qy;
-      const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
-      const float y = __fadd_rn(z, 12582912.0f);
-      const double ex = __dsub_rn(p.x, q.x), ey = __dsub_rn(p.y, q.y);
-      const double d2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
-      int k = max(0, min((int)(__float_as_uint(y) - 0x4B400000u) - 2, uf));
-      while (k < uf && thr[k + 1] <= d2) ++k;
-      v = (uint32_t)k;
-    }
-    w[j / kPer] |= v << (8 * sizeof(T) * (j % kPer));
-  }
-  if constexpr (kW == 2)
-    *reinterpret_cast<uint2*>(out) = make_uint2(w[0], w[1]);
-  else
-    *reinterpret_cast<uint4*>(out) = make_uint4(w[0], w[1], w[2], w[3]);
+// FP32 estimate of entry (a, b): z = x_f - 1/2, y = z + 1.5 * 2^23 (FP32):
+// y's low bits are then rint(z) = floor(x_f), and |z - rint(z)| = 1/2 -
+// (distance of x_f to the nearest integer), returned as the nearness.
+__device__ __forceinline__ uint32_t k2_estimate(float px, float py, float qx, float qy, float inv_step,
+                                                float& near) {
+  const float dx = px - qx, dy = py - qy;
+  const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
+  const float y = __fadd_rn(z, 12582912.0f);
+  near = fabsf(__fsub_rn(z, __fsub_rn(y, 12582912.0f)));
+  return __float_as_uint(y);
 }
 
-// The rows of one thread: kR supply rows per iteration, all kR * kV estimates
-// first (branch-free, independent: ILP across entries), one store per row.
-// A row with an entry within margin of a level boundary is queued as (b, a0)
-// in this block's fix-up list (fixed by round_points_fix_kernel after the
-// build; inline when the list is full), so the fast loop never recomputes.
-// kPad: this thread's 16 bytes include pad columns (a >= n_ai), which hold
-// the type maximum.
-template <typename T, bool kPad, int kR>
-__device__ __forceinline__ void k2_rows(const float2 (&pf)[K2Shape<T>::kV], const double2* __restrict__ pa,
-                                        const double2* __restrict__ pb, int n_ai, int n_bi, const double* s_thr,
-                                        int uf, float inv_step, float lim, const uint32_t (&padw)[4],
-                                        T* __restrict__ kT, int lda, int a0, uint2* fix, int fix_cap,
-                                        int* s_fix) {
-  constexpr int kV = K2Shape<T>::kV, kW = K2Shape<T>::kW;
-  const int step = gridDim.y;
-  double2 qn[kR];
-#pragma unroll
-  for (int r = 0; r < kR; ++r) {
-    const int b = blockIdx.y + r * step;
-    qn[r] = b < n_bi ? pb[b] : make_double2(0.0, 0.0);
+// The exact level from FP64 d2 and the table, walking up from floor(x_f) - 2
+// (<= the level: |x_f - x| < margin < 1).
+__device__ __forceinline__ int k2_exact_level(double2 p, double2 q, uint32_t y, const double* thr, int uf) {
+  const double ex = __dsub_rn(p.x, q.x), ey = __dsub_rn(p.y, q.y);
+  const double d2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+  int k = max(0, min((int)(y - 0x4B400000u) - 2, uf));
+  while (k < uf && thr[k + 1] <= d2) ++k;
+  return k;
+}
+
+// The entries (b, a0 .. a0 + kV/2) that lie near a level boundary (nearness
+// >= lim, a superset of the fast pass's test) get their exact level from
+// FP64 d2 and the table, walking up from floor(x_f) - 2 (<= the level:
+// |x_f - x| < margin < 1); single-element stores over the fast pass's row.
+template <typename T>
+__device__ __forceinline__ void k2_patch_half(const double2* __restrict__ pa, double2 q, int n_ai, int a0,
+                                              const double* thr, int uf, float inv_step, float lim,
+                                              T* __restrict__ out) {
+  constexpr int kV = K2Shape<T>::kV;
+  const float qx = __double2float_rn(q.x), qy = __double2float_rn(q.y);
+  for (int j = 0; j < kV / 2 && a0 + j < n_ai; ++j) {
+    const double2 p = pa[a0 + j];
+    float near;
+    const uint32_t y = k2_estimate(__double2float_rn(p.x), __double2float_rn(p.y), qx, qy, inv_step, near);
+    if (near < lim) continue;
+    out[j] = (T)k2_exact_level(p, q, y, thr, uf);
   }
-  for (int b = blockIdx.y; b < n_bi; b += kR * step) {
-    double2 q[kR];
-    float qx[kR], qy[kR];
+}
+
+// One chunk of rows of one thread: its block owns the contiguous supply rows
+// [b_lo, b_hi), staged kK2Chunk at a time in shared memory as float points
+// (one broadcast load per row).  Per row: the kV estimates (branch-free,
+// independent: ILP across entries), one max of their nearness, the packed
+// store.  A row with an entry within margin of a level boundary is queued as
+// (b, a0) in this block's fix-up list and patched by round_points_fix_kernel
+// after the build (inline when the list is full), so the fast loop never
+// recomputes.  kPad: this thread's entries include pad columns (a >= n_ai),
+// which hold the type maximum.
+constexpr int kK2Chunk = 256;
+template <typename T, bool kPad>
+__device__ __forceinline__ void k2_chunk(const float2 (&pf)[K2Shape<T>::kV], const double2* __restrict__ pa,
+                                         const double2* __restrict__ pb, int n_ai, int c0, int nr,
+                                         const double* s_thr, const float2* s_q, int uf, float inv_step, float lim,
+                                         float lim_patch, const uint32_t (&padw)[K2Shape<T>::kW],
+                                         T* __restrict__ kT, int lda, int a0, uint2* fix, int fix_cap, int* s_fix) {
+  constexpr int kV = K2Shape<T>::kV, kW = K2Shape<T>::kW;
+  T* out = kT + (size_t)c0 * lda + a0;
+  const float2* qp = s_q;
+  for (int r = 0; r < nr; ++r, out += lda, ++qp) {
+    const float2 q = *qp;
+    uint32_t yv[kV];
+    float dm[2] = {0.0f, 0.0f};  // nearness of each half of the entries
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      q[r] = qn[r];  // the next rows' points are in flight during these rows
-      const int nb = b + (kR + r) * step;
-      if (nb < n_bi) qn[r] = pb[nb];
-      qx[r] = __double2float_rn(q[r].x);
-      qy[r] = __double2float_rn(q[r].y);
+    for (int j = 0; j < kV; ++j) {
+      float nr_j;
+      yv[j] = k2_estimate(pf[j].x, pf[j].y, q.x, q.y, inv_step, nr_j);
+      dm[j / (kV / 2)] = fmaxf(dm[j / (kV / 2)], nr_j);
     }
-    // z = x_f - 1/2 and y = z + 1.5 * 2^23 (FP32): y's low bits are then
-    // rint(z) = floor(x_f), and |z - rint(z)| = 1/2 - (distance of x_f to the
-    // nearest integer) — so one max per row tells whether any entry lies
-    // within margin of a level boundary (FP32/INT only; the float->int
-    // conversion pipe is quarter rate and was the limit).
-    uint32_t yv[kR][kV];
-    float dm[kR];
+    uint32_t w[kW];
+    if constexpr (sizeof(T) == 1) {
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      dm[r] = 0.0f;
+      for (int q4 = 0; q4 < kW; ++q4)
+        w[q4] = __byte_perm(__byte_perm(yv[4 * q4], yv[4 * q4 + 1], 0x0040),
+                            __byte_perm(yv[4 * q4 + 2], yv[4 * q4 + 3], 0x0040), 0x5410);
+    } else if constexpr (sizeof(T) == 2) {
 #pragma unroll
-      for (int j = 0; j < kV; ++j) {
-        const float dx = pf[j].x - qx[r], dy = pf[j].y - qy[r];
-        const float z = fmaf(sqrt_approx(fmaf(dy, dy, dx * dx)), inv_step, -0.5f);
-        const float y = __fadd_rn(z, 12582912.0f);
-        yv[r][j] = __float_as_uint(y);
-        dm[r] = fmaxf(dm[r], fabsf(__fsub_rn(z, __fsub_rn(y, 12582912.0f))));
-      }
+      for (int q4 = 0; q4 < kW; ++q4) w[q4] = __byte_perm(yv[2 * q4], yv[2 * q4 + 1], 0x5410);
+    } else {
+#pragma unroll
+      for (int q4 = 0; q4 < kW; ++q4) w[q4] = yv[q4] - 0x4B400000u;
+    }
+    if constexpr (kPad) {
+#pragma unroll
+      for (int q4 = 0; q4 < kW; ++q4) w[q4] |= padw[q4];
     }
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      const int br = b + r * step;
-      if (br >= n_bi) break;
-      uint32_t w[4];
-      if constexpr (sizeof(T) == 1) {
+    for (int v = 0; v < kW / 4; ++v)
+      reinterpret_cast<uint4*>(out)[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+    if (fmaxf(dm[0], dm[1]) >= lim) {  // near a level boundary: patched after the build, or now
+      const int br = c0 + r;
 #pragma unroll
-        for (int q4 = 0; q4 < kW; ++q4)
-          w[q4] = __byte_perm(__byte_perm(yv[r][4 * q4], yv[r][4 * q4 + 1], 0x0040),
-                              __byte_perm(yv[r][4 * q4 + 2], yv[r][4 * q4 + 3], 0x0040), 0x5410);
-      } else if constexpr (sizeof(T) == 2) {
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) w[q4] = __byte_perm(yv[r][2 * q4], yv[r][2 * q4 + 1], 0x5410);
-      } else {
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) w[q4] = yv[r][q4] - 0x4B400000u;
-      }
-      if constexpr (kPad) {
-#pragma unroll
-        for (int q4 = 0; q4 < kW; ++q4) w[q4] |= padw[q4];
-      }
-      T* out = kT + (size_t)br * lda + a0;
-      if (dm[r] >= lim) {  // near a level boundary: exact, now or after the build
+      for (int h = 0; h < 2; ++h) {
+        if (dm[h] < lim) continue;
+        const int ah = a0 + h * (kV / 2);
         const int slot = atomicAdd(s_fix, 1);
-        if (slot < fix_cap) {
-          fix[slot] = make_uint2((uint32_t)br, (uint32_t)a0);
-        } else {
-          k2_exact_row<T>(pa, q[r], n_ai, a0, s_thr, uf, inv_step, out);
-          continue;
-        }
+        if (slot < fix_cap) fix[slot] = make_uint2((uint32_t)br, (uint32_t)ah);
+        else k2_patch_half<T>(pa, pb[br], n_ai, ah, s_thr, uf, inv_step, lim_patch, out + h * (kV / 2));
       }
-      if constexpr (kW == 2)
-        *reinterpret_cast<uint2*>(out) = make_uint2(w[0], w[1]);
-      else
-        *reinterpret_cast<uint4*>(out) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
 }
@@ -257,60 +235,93 @@ __global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __
                                                                int n_ai, int n_bi, const double* __restrict__ thr,
                                                                int thr_n, float inv_step, float margin,
                                                                T* __restrict__ kT, int lda, uint2* __restrict__ fix,
-                                                               int* __restrict__ fix_cnt, int fix_cap) {
-  constexpr int kV = K2Shape<T>::kV, kPer = K2Shape<T>::kPer;
-  extern __shared__ __align__(16) double s_thr[];  // the threshold table (the inline exact rows)
+                                                               int* __restrict__ fix_cnt, int fix_cap,
+                                                               float2* __restrict__ pa_f, float2* __restrict__ pb_f) {
+  constexpr int kV = K2Shape<T>::kV, kPer = K2Shape<T>::kPer, kW = K2Shape<T>::kW;
+  extern __shared__ __align__(16) double s_thr[];  // the threshold table (the inline patches)
+  __shared__ float2 s_q[kK2Chunk];
   __shared__ int s_fix;
   for (int j = threadIdx.x; j < thr_n; j += blockDim.x) s_thr[j] = thr[j];
   if (threadIdx.x == 0) s_fix = 0;
   const int uf = thr_n - 2;  // unit_floor: thr[uf + 1] = +inf
-  const float lim = 0.5f - margin;  // |z - rint(z)| >= lim: within margin of a level boundary
+  const float lim = 0.5f - margin;  // nearness >= lim: within margin of a level boundary
+  const float lim_patch = lim - 1e-5f;  // the patch's test: a superset
   const int a0 = (blockIdx.x * blockDim.x + threadIdx.x) * kV;
   const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+  // this block's supply rows: a contiguous range
+  const int per = (n_bi + gridDim.y - 1) / gridDim.y;
+  const int b_lo = min(n_bi, (int)blockIdx.y * per), b_hi = min(n_bi, b_lo + per);
   float2 pf[kV];
 #pragma unroll
   for (int j = 0; j < kV; ++j) {
     const double2 p = a0 + j < n_ai ? pa[a0 + j] : make_double2(0.0, 0.0);
     pf[j] = make_float2(__double2float_rn(p.x), __double2float_rn(p.y));
+    if (blockIdx.y == 0 && a0 + j < n_ai) pa_f[a0 + j] = pf[j];  // (for the fix-up pass)
   }
-  __syncthreads();
-  if (a0 < lda) {
-    // pad entries (a >= n_ai) hold the type maximum
-    uint32_t padw[4] = {0u, 0u, 0u, 0u};
+  // pad entries (a >= n_ai) hold the type maximum
+  uint32_t padw[kW];
 #pragma unroll
-    for (int j = 0; j < kV; ++j)
-      if (a0 + j >= n_ai) padw[j / kPer] |= type_max<T>() << (8 * sizeof(T) * (j % kPer));
-    uint2* my_fix = fix + (size_t)blk * fix_cap;
-    if (a0 + kV <= n_ai)
-      k2_rows<T, false, kK2Rows>(pf, pa, pb, n_ai, n_bi, s_thr, uf, inv_step, lim, padw, kT, lda, a0, my_fix,
-                                 fix_cap, &s_fix);
+  for (int q4 = 0; q4 < kW; ++q4) padw[q4] = 0u;
+#pragma unroll
+  for (int j = 0; j < kV; ++j)
+    if (a0 + j >= n_ai) padw[j / kPer] |= type_max<T>() << (8 * sizeof(T) * (j % kPer));
+  const bool active = a0 < lda, full = a0 + kV <= n_ai;
+  uint2* my_fix = fix + (size_t)blk * fix_cap;
+  for (int c0 = b_lo; c0 < b_hi; c0 += kK2Chunk) {
+    const int nr = min(kK2Chunk, b_hi - c0);
+    __syncthreads();  // (the previous chunk's points are consumed)
+    for (int j = threadIdx.x; j < nr; j += blockDim.x) {
+      const double2 q = pb[c0 + j];
+      s_q[j] = make_float2(__double2float_rn(q.x), __double2float_rn(q.y));
+      if (blockIdx.x == 0) pb_f[c0 + j] = s_q[j];
+    }
+    __syncthreads();
+    if (!active) continue;
+    if (full)
+      k2_chunk<T, false>(pf, pa, pb, n_ai, c0, nr, s_thr, s_q, uf, inv_step, lim, lim_patch, padw, kT, lda, a0,
+                         my_fix, fix_cap, &s_fix);
     else
-      k2_rows<T, true, kK2Rows>(pf, pa, pb, n_ai, n_bi, s_thr, uf, inv_step, lim, padw, kT, lda, a0, my_fix,
-                                fix_cap, &s_fix);
+      k2_chunk<T, true>(pf, pa, pb, n_ai, c0, nr, s_thr, s_q, uf, inv_step, lim, lim_patch, padw, kT, lda, a0,
+                        my_fix, fix_cap, &s_fix);
   }
   __syncthreads();
   if (threadIdx.x == 0) fix_cnt[blk] = min(s_fix, fix_cap);
 }
 
-// The queued rows: the exact levels, over the fast pass's stores.
+constexpr int kFixSlices = 8;
+// The queued half rows: a thread per entry (half row, j) recomputes the
+// estimate from the float copies and takes the exact level (FP64 d2 and the
+// table) of the near ones, over the fast pass's store.
 template <typename T>
 __global__ void __launch_bounds__(256) round_points_fix_kernel(const double2* __restrict__ pa,
                                                                const double2* __restrict__ pb, int n_ai,
                                                                const double* __restrict__ thr, int thr_n,
-                                                               float inv_step, T* __restrict__ kT, int lda,
-                                                               const uint2* __restrict__ fix,
+                                                               float inv_step, float margin, T* __restrict__ kT,
+                                                               int lda, const uint2* __restrict__ fix,
                                                                const int* __restrict__ fix_cnt, int fix_cap,
-                                                               int blocks) {
+                                                               int blocks, const float2* __restrict__ pa_f,
+                                                               const float2* __restrict__ pb_f) {
+  constexpr int kH = K2Shape<T>::kV / 2;
   extern __shared__ __align__(16) double s_thr[];
   for (int j = threadIdx.x; j < thr_n; j += blockDim.x) s_thr[j] = thr[j];
   __syncthreads();
-  for (int blk = blockIdx.x; blk < blocks; blk += gridDim.x) {
-    const int n = fix_cnt[blk];
+  const float lim_patch = 0.5f - margin - 1e-5f;
+  const int uf = thr_n - 2;
+  // kFixSlices blocks per main-kernel block (its list): latency-bound
+  // dependent loads, so many threads in flight
+  for (int w = blockIdx.x; w < blocks * kFixSlices; w += gridDim.x) {
+    const int blk = w / kFixSlices, sl = w % kFixSlices;
+    const int n = fix_cnt[blk] * kH;
     const uint2* f = fix + (size_t)blk * fix_cap;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-      const uint2 ba = f[e];
-      k2_exact_row<T>(pa, pb[ba.x], n_ai, (int)ba.y, s_thr, thr_n - 2, inv_step,
-                      kT + (size_t)ba.x * lda + ba.y);
+    for (int e = sl * blockDim.x + threadIdx.x; e < n; e += kFixSlices * blockDim.x) {
+      const uint2 ba = f[e / kH];
+      const int a = (int)ba.y + e % kH;
+      if (a >= n_ai) continue;
+      const float2 pf = pa_f[a], qf = pb_f[ba.x];
+      float nr;
+      const uint32_t y = k2_estimate(pf.x, pf.y, qf.x, qf.y, inv_step, nr);
+      if (nr < lim_patch) continue;
+      kT[(size_t)ba.x * lda + a] = (T)k2_exact_level(pa[a], pb[ba.x], y, s_thr, uf);
     }
   }
 }
@@ -584,13 +595,13 @@ constexpr int kK2MaxBlocks = 4096;
 size_t round_points_fix_bytes(int n_ai, int n_bi, int lda, int width, double eps, double absmax) {
   // twice the expected rows with an entry within margin of a boundary (a
   // full list only sends rows to the inline path), >= 1 M entries, <= 512 MB
-  const int kv = width == 1 ? 8 : 16 / width;
+  const int kv = width == 4 ? 8 : 16;
   const double m = k2_margin(eps, absmax);
-  const double p_row = 1.0 - std::pow(std::max(0.0, 1.0 - 2.0 * m), kv);
-  const double rows = (double)n_bi * ((lda + kv - 1) / kv);
+  const double p_row = 1.0 - std::pow(std::max(0.0, 1.0 - 2.0 * m), kv / 2);  // (half rows)
+  const double rows = 2.0 * n_bi * ((lda + kv - 1) / kv);
   const double want = std::min(64.0 * 1024 * 1024, std::max(1024.0 * 1024, 2.0 * rows * p_row + 65536.0));
-  (void)n_ai;
-  return 256 + (size_t)want * sizeof(uint2) + kK2MaxBlocks * sizeof(int);
+  return 512 + (size_t)want * sizeof(uint2) + kK2MaxBlocks * sizeof(int) + ((size_t)n_ai + n_bi) * sizeof(float2) +
+         64 * 1024;
 }
 
 cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, int n_bi,
@@ -598,18 +609,24 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
                                   void* kT, int lda, int width, void* fix_buf, size_t fix_bytes, cudaStream_t s) {
   const double2* a2 = reinterpret_cast<const double2*>(pa);
   const double2* b2 = reinterpret_cast<const double2*>(pb);
-  if (thr && thr_n >= 2 && thr_n <= kThrSmemMax && fix_buf && fix_bytes > 256 + kK2MaxBlocks * sizeof(int)) {
-    // threads own kV entries of a row (8 B for u8, 16 B otherwise); the grid is
-    // one resident wave (occupancy-sized), the supply rows strided over grid.y
-    const int kv = width == 1 ? 8 : 16 / width;
+  const size_t head = kK2MaxBlocks * sizeof(int) + ((size_t)n_ai + n_bi) * sizeof(float2);
+  const size_t head_al = (head + 255) / 256 * 256;
+  if (thr && thr_n >= 2 && thr_n <= kThrSmemMax && fix_buf && fix_bytes >= head_al + 64 * 1024) {
+    // threads own kV entries of a row (16 for u8 / u16, 8 for u32); the grid
+    // is one resident wave (occupancy-sized), contiguous supply row ranges
+    // over grid.y
+    const int kv = width == 4 ? 8 : 16;
     const int threads_x = (lda + kv - 1) / kv;
     const int bx = (threads_x + 255) / 256;
     const float inv_step = (float)(1.0 / (std::sqrt(2.0) * eps));
     const float margin = k2_margin(eps, absmax);
     const size_t smem = (size_t)thr_n * sizeof(double);
+    // [per-block counts | float copies of the points | queued half rows]
     int* fix_cnt = static_cast<int*>(fix_buf);
-    uint2* fix = reinterpret_cast<uint2*>(static_cast<char*>(fix_buf) + 256 + kK2MaxBlocks * sizeof(int));
-    const size_t fix_total = (fix_bytes - 256 - kK2MaxBlocks * sizeof(int)) / sizeof(uint2);
+    float2* pa_f = reinterpret_cast<float2*>(static_cast<char*>(fix_buf) + kK2MaxBlocks * sizeof(int));
+    float2* pb_f = pa_f + n_ai;
+    uint2* fix = reinterpret_cast<uint2*>(static_cast<char*>(fix_buf) + head_al);
+    const size_t fix_total = (fix_bytes - head_al) / sizeof(uint2);
     with_width(width, [&](auto tag) {
       using T = decltype(tag);
       auto fn = round_points_thr_kernel<T>;
@@ -625,9 +642,9 @@ cudaError_t launch_round_points2d(const double* pa, const double* pb, int n_ai, 
       const int blocks = bx * by;
       const int cap = (int)std::min<size_t>(fix_total / blocks, (size_t)1 << 30);
       fn<<<dim3(bx, by), 256, smem, s>>>(a2, b2, n_ai, n_bi, thr, thr_n, inv_step, margin, static_cast<T*>(kT),
-                                         lda, fix, fix_cnt, cap);
-      fx<<<std::min(blocks, sms * 4), 256, smem, s>>>(a2, b2, n_ai, thr, thr_n, inv_step, static_cast<T*>(kT), lda,
-                                                      fix, fix_cnt, cap, blocks);
+                                         lda, fix, fix_cnt, cap, pa_f, pb_f);
+      fx<<<std::min(blocks * kFixSlices, 65535), 256, smem, s>>>(a2, b2, n_ai, thr, thr_n, inv_step, margin,
+                                                      static_cast<T*>(kT), lda, fix, fix_cnt, cap, blocks, pa_f, pb_f);
       return 0;
     });
     return cudaGetLastError();
