@@ -673,6 +673,13 @@ cudaError_t launch_l1_normalize(const uint8_t* img, int count, int dim, double* 
   return cudaGetLastError();
 }
 
+cudaError_t launch_l1_group_masks(const double* x, int n, int dim, int rows, uint32_t* mask, cudaStream_t s) {
+  const int tiles = (n + rows - 1) / rows, nw = (dim + 31) / 32;
+  if (tiles > 0)
+    l1_tile_mask_kernel<<<std::min(tiles, 8192), std::min(1024, nw * 32), 0, s>>>(x, n, dim, tiles, rows, mask);
+  return cudaGetLastError();
+}
+
 size_t l1_mask_bytes(int n_ai, int n_bi, int lda, int dim) {
   const int tiles = std::max(lda, n_ai) / kL1TileA + 1 + (n_bi + kL1TileB - 1) / kL1TileB;
   return (size_t)tiles * ((dim + 31) / 32) * sizeof(uint32_t);

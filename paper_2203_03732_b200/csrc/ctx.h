@@ -86,6 +86,7 @@ struct otprg_ctx {
   DevBuf stage, pts, flush;
   DevBuf l1_mask;  // K3 tile pixel-support masks
   DevBuf k2_fix;   // K2 rows deferred to the exact fix-up pass
+  DevBuf l1_otf_mask;  // on-the-fly L1: demand group / supply image pixel-support masks
   // exact threshold table of the 2-D point cost for eps = thr_eps (K2 and the
   // on-the-fly scans; otprg_points_threshold_table), cached across prepares
   DevBuf thr_dev, range_first;

@@ -142,7 +142,16 @@ struct ShardArgs {
   const double* l1y;
   int dim, na_full;
   double eps;
+  // pixel-support masks ((dim + 31) / 32 words each): of the slab's 32-image
+  // demand groups (group g = images lo + 32 g ..) and of every supply image;
+  // the sums walk the union only (a pixel zero on both sides adds +0)
+  const uint32_t* l1_gmask;
+  const uint32_t* l1_bmask;
 };
+// Pixel-support masks of groups of `rows` consecutive images of x (n images
+// of dim pixels): bit p of group g when any image of the group has pixel p
+// != 0; (dim + 31) / 32 words per group.
+cudaError_t launch_l1_group_masks(const double* x, int n, int dim, int rows, uint32_t* mask, cudaStream_t s);
 constexpr int kSegWarps = 32768;
 constexpr int kMaxSegs = 32;
 constexpr int kMaxShardPeers = 8;  // device groups one group pushes to (<= 8 GPUs per node + slack)

@@ -76,6 +76,8 @@ otprg::ShardArgs shard_args(otprg_ctx* ctx) {
     S.dim = ctx->img_dim;
     S.na_full = ctx->ia;
     S.eps = ctx->eps;
+    S.l1_gmask = ctx->l1_otf_mask.as<uint32_t>();
+    S.l1_bmask = S.l1_gmask + static_cast<size_t>((ctx->sh_hi - ctx->sh_lo + 31) / 32) * ((dim + 31) / 32);
   } else if (ctx->sh_otf) {
     S.pa = ctx->pts.as<double2>();
     S.pb = S.pa + ctx->ia;
@@ -528,6 +530,14 @@ int otprg_shard_prepare(otprg_ctx* ctx, const otprg_problem* p, int32_t n_shards
       CK(otprg::launch_transpose_f64(xa, ctx->ia, p->dim,
                                      reinterpret_cast<double*>(static_cast<char*>(ctx->pts.p) + xt_off), ctx->stream),
          "transpose");
+      const size_t nw = (dim + 31) / 32, groups = (ctx->sh_hi - ctx->sh_lo + 31) / 32;
+      CK(ctx->l1_otf_mask.ensure((groups + ib) * nw * 4 + 4), "alloc masks");
+      uint32_t* gm = ctx->l1_otf_mask.as<uint32_t>();
+      CK(otprg::launch_l1_group_masks(xa + static_cast<size_t>(ctx->sh_lo) * dim, ctx->sh_hi - ctx->sh_lo, p->dim, 32,
+                                      gm, ctx->stream),
+         "group masks");
+      CK(otprg::launch_l1_group_masks(yb, static_cast<int>(ib), p->dim, 1, gm + groups * nw, ctx->stream),
+         "image masks");
     } else if (ctx->sh_hi > ctx->sh_lo) {
       CK(ctx->l1_mask.ensure(otprg::l1_mask_bytes(ctx->sh_hi - ctx->sh_lo, ctx->ib, ctx->lda, p->dim)), "alloc masks");
       CK(otprg::launch_l1_round(xa + static_cast<size_t>(ctx->sh_lo) * dim, yb, ctx->sh_hi - ctx->sh_lo, ctx->ib,

@@ -761,7 +761,19 @@ __device__ __forceinline__ void scan_l1_item(const ShardArgs& S, double* __restr
       if (e < width_local && e >= lstart) {
         const double* x = S.l1x + lo + e;
         double acc = 0.0;
-        for (int p = 0; p < dim; ++p) acc = __dadd_rn(acc, fabs(__dsub_rn(__ldg(x + (size_t)p * na_full), s_y[p])));
+        // ascending p over the union of the group's and b's pixel supports
+        // (a pixel zero in both adds +0: the sum's bits are unchanged)
+        const int nw = (dim + 31) >> 5;
+        const uint32_t* gm = S.l1_gmask + (size_t)g * nw;
+        const uint32_t* bm = S.l1_bmask + (size_t)b * nw;
+        for (int wd = 0; wd < nw; ++wd) {
+          uint32_t m = __ldg(gm + wd) | __ldg(bm + wd);
+          while (m) {
+            const int p = (wd << 5) + __ffs(m) - 1;
+            m &= m - 1;
+            acc = __dadd_rn(acc, fabs(__dsub_rn(__ldg(x + (size_t)p * na_full), s_y[p])));
+          }
+        }
         const long long k = scaled_floor_dev(__ddiv_rn(acc, 2.0), S.eps);
         hit = k + (long long)__ldcg(tl + e) == target;
       }
