@@ -175,6 +175,13 @@ __device__ __forceinline__ void k2_patch_half(const double2* __restrict__ pa, do
 // recomputes.  kPad: this thread's entries include pad columns (a >= n_ai),
 // which hold the type maximum.
 constexpr int kK2Chunk = 256;
+#ifndef OTPRG_K2_PREFETCH
+#define OTPRG_K2_PREFETCH 0
+#endif
+#ifndef OTPRG_K2_UNROLL
+#define OTPRG_K2_UNROLL 1
+#endif
+constexpr int kK2Unroll = OTPRG_K2_UNROLL;
 template <typename T, bool kPad>
 __device__ __forceinline__ void k2_chunk(const float2 (&pf)[K2Shape<T>::kV], const double2* __restrict__ pa,
                                          const double2* __restrict__ pb, int n_ai, int c0, int nr,
@@ -184,8 +191,17 @@ __device__ __forceinline__ void k2_chunk(const float2 (&pf)[K2Shape<T>::kV], con
   constexpr int kV = K2Shape<T>::kV, kW = K2Shape<T>::kW;
   T* out = kT + (size_t)c0 * lda + a0;
   const float2* qp = s_q;
+#if OTPRG_K2_PREFETCH
+  float2 qn = qp[0];
+#endif
+#pragma unroll kK2Unroll
   for (int r = 0; r < nr; ++r, out += lda, ++qp) {
+#if OTPRG_K2_PREFETCH
+    const float2 q = qn;
+    qn = qp[r + 1 < nr ? 1 : 0];  // the next row's point in flight during this row
+#else
     const float2 q = *qp;
+#endif
     uint32_t yv[kV];
     float dm[2] = {0.0f, 0.0f};  // nearness of each half of the entries
 #pragma unroll

@@ -332,11 +332,26 @@ __global__ void ot_da_alloc_kernel(OtDev D) {
     D.ctr[kCtrE] = 0;
   }
   const int nt = (int)D.ctr[kCtrTouch];
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
-    const int code = D.da_touch[t];
-    const int c = D.da_cnt[code];
-    if (c > kDaWarpMax) D.ctr[kCtrBig] = 1;  // this round goes the sorted way
-    D.da_off[code] = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrAlloc]), (unsigned long long)c);
+  const int lane = threadIdx.x & 31;
+  // whole warps iterate (one aggregated atomic per warp)
+  for (int t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; t0 < nt; t0 += gridDim.x * blockDim.x) {
+    const int t = t0 + lane;
+    int code = -1, c = 0;
+    if (t < nt) {
+      code = D.da_touch[t];
+      c = D.da_cnt[code];
+      if (c > kDaWarpMax) D.ctr[kCtrBig] = 1;  // this round goes the sorted way
+    }
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrAlloc]), (unsigned long long)inc);
+    base = __shfl_sync(kFull, base, 31);
+    if (code >= 0) D.da_off[code] = (int64_t)(base + inc - c);
   }
 }
 
@@ -675,7 +690,7 @@ cudaError_t ot_dev_da_rounds(OtDev& D, int rounds, cudaStream_t s) {
     ot_da_count_kernel<<<148 * 2, 256, 0, s>>>(D);
     ot_da_alloc_kernel<<<148, 256, 0, s>>>(D);
     ot_da_scatter_kernel<<<148 * 2, 256, 0, s>>>(D);
-    ot_da_resolve_warp_kernel<<<148 * 2, 256, 0, s>>>(D);
+    ot_da_resolve_warp_kernel<<<148 * 8, 256, 0, s>>>(D);
   }
   return cudaGetLastError();
 }
