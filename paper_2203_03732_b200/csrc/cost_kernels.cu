@@ -176,12 +176,15 @@ __device__ __forceinline__ void k2_patch_half(const double2* __restrict__ pa, do
 // which hold the type maximum.
 constexpr int kK2Chunk = 256;
 #ifndef OTPRG_K2_PREFETCH
-#define OTPRG_K2_PREFETCH 0
+#define OTPRG_K2_PREFETCH 1
 #endif
 #ifndef OTPRG_K2_UNROLL
 #define OTPRG_K2_UNROLL 1
 #endif
 constexpr int kK2Unroll = OTPRG_K2_UNROLL;
+#ifndef OTPRG_K2_MINB
+#define OTPRG_K2_MINB 1
+#endif
 template <typename T, bool kPad>
 __device__ __forceinline__ void k2_chunk(const float2 (&pf)[K2Shape<T>::kV], const double2* __restrict__ pa,
                                          const double2* __restrict__ pb, int n_ai, int c0, int nr,
@@ -246,7 +249,7 @@ __device__ __forceinline__ void k2_chunk(const float2 (&pf)[K2Shape<T>::kV], con
 
 // fix: per block (linear index) a count word in fix_cnt and fix_cap entries.
 template <typename T>
-__global__ void __launch_bounds__(256) round_points_thr_kernel(const double2* __restrict__ pa,
+__global__ void __launch_bounds__(256, OTPRG_K2_MINB) round_points_thr_kernel(const double2* __restrict__ pa,
                                                                const double2* __restrict__ pb,
                                                                int n_ai, int n_bi, const double* __restrict__ thr,
                                                                int thr_n, float inv_step, float margin,
