@@ -396,16 +396,19 @@ __global__ void l1_normalize_kernel(const uint8_t* __restrict__ img, int count, 
 // bits match.  Block tile 64 a x 64 b, thread tile 4 x 4, pixels staged in
 // shared memory in chunks of kP, p-major.
 #ifndef OTPRG_L1_TA
-#define OTPRG_L1_TA 4
+#define OTPRG_L1_TA 8
 #endif
 #ifndef OTPRG_L1_TB
 #define OTPRG_L1_TB 4
 #endif
 #ifndef OTPRG_L1_MINB
-#define OTPRG_L1_MINB 1
+#define OTPRG_L1_MINB 2
 #endif
 constexpr int kL1TA = OTPRG_L1_TA, kL1TB = OTPRG_L1_TB;  // a / b entries per thread
-constexpr int kL1TileA = 16 * kL1TA, kL1TileB = 16 * kL1TB, kL1P = 16, kL1MaxList = 2048;
+#ifndef OTPRG_L1_P
+#define OTPRG_L1_P 4
+#endif
+constexpr int kL1TileA = 16 * kL1TA, kL1TileB = 16 * kL1TB, kL1P = OTPRG_L1_P, kL1MaxList = 2048;
 
 // Pixel-support masks: bit p of tile g's words is set when any image of the
 // image tile g has pixel p != 0.  A pixel that is zero in every image of
