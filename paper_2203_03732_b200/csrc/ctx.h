@@ -144,7 +144,7 @@ struct otprg_ctx {
 
   // optimal transport (ot_host.cpp): per-phase scan inputs / outputs
   DevBuf ot_t, ot_req, ot_out;
-  DevBuf ot_dev[40];  // the OT cluster state and phase buffers on the device (ot_host.cpp)
+  DevBuf ot_dev[48];  // the OT cluster state and phase buffers on the device (ot_host.cpp)
   void* ot_hpin = nullptr;
   std::shared_ptr<void> ot_state;  // flat ClusterState of the last copy/cluster solve (ot_host.cpp)
   size_t ot_hpin_n = 0;

@@ -207,10 +207,15 @@ cudaError_t launch_ot_scan(const void* kT, int lda, int width, const void* t0, c
 constexpr int32_t kFreeB = 0x7fffffff;  // flow-entry "b" of a demand cluster's free copies
 // kCtrTouch..kCtrBig: the device-sized DA rounds (ot_dev_da_rounds): clusters
 // proposed to this round, segment space handed out, rounds over (1) or a
-// segment too large for the warp resolve (2), entries this round.
+// segment too large for the warp resolve (2), entries this round.  kCtrHold:
+// the device-sized phase (ot_host.cpp) stopped at a step the host must
+// finish (1 admissible lists beyond adm_cap, 2 claim rounds not over, 3 more
+// records than one block sorts); every later kernel of the phase returns at
+// once while it is set.  kCtrNFlows: records after the merge.
 enum OtCtr {
   kCtrNi = 0, kCtrFree = 1, kCtrNew = 2, kCtrE = 3, kCtrRec = 4,
-  kCtrTouch = 5, kCtrAlloc = 6, kCtrDone = 7, kCtrN = 8, kCtrBig = 9, kCtrRounds = 10, kCtrCount = 12
+  kCtrTouch = 5, kCtrAlloc = 6, kCtrDone = 7, kCtrN = 8, kCtrBig = 9, kCtrRounds = 10,
+  kCtrHold = 11, kCtrNFlows = 12, kCtrCount = 14
 };
 struct OtDev {
   int n_a, n_b, lda, width;
@@ -243,6 +248,12 @@ struct OtDev {
   int64_t* adm_len;
   int64_t* adm_off;
   int32_t* adm;        // admissible cluster codes, ascending a
+  int64_t adm_cap;     // entries adm holds (the device-sized phase checks it)
+  int64_t e_cap, r_cap;  // DA entries / records the buffers hold (the persistent loop checks them)
+  unsigned* bar;       // [2] persistent loop: grid barrier count, count at the last exit
+  int64_t* loop;       // [4] persistent loop: phases this launch, claim rounds
+  int64_t* fcounts;    // [fc_cap] persistent loop: n_i of the phases of this launch
+  int64_t fc_cap;
   // DA entries (key = code << 32 | i) and next-state records
   unsigned long long* e_key;
   int64_t* e_val;
@@ -271,6 +282,22 @@ cudaError_t ot_dev_propose(OtDev& D, cudaStream_t s);
 constexpr int kDaWarpMax = 256;
 cudaError_t ot_dev_da_rounds(OtDev& D, int rounds, cudaStream_t s);
 cudaError_t ot_dev_da_clear(OtDev& D, cudaStream_t s);
+// The device-sized phase (no host sizes; see kCtrHold): counters of the
+// phase to zero (all but n_i / n_free), the admissible offsets by one
+// block, the claim-rounds gate, the updates, the record merge in one block
+// (<= kOtSmallRec records), the CSR rebuild; n < 0 in ot_dev_consumed /
+// ot_dev_records / ot_dev_rebuild reads the size from the counters.
+constexpr int kOtSmallRec = 8192;
+cudaError_t ot_dev_phase_begin(OtDev& D, cudaStream_t s);
+cudaError_t ot_dev_adm_scan(OtDev& D, cudaStream_t s);
+cudaError_t ot_dev_da_gate(OtDev& D, cudaStream_t s);
+cudaError_t ot_dev_small_merge(OtDev& D, unsigned long long* key, int64_t* val, cudaStream_t s);
+// The whole phase loop as one cooperative launch (a grid barrier between the
+// steps above): from `stage` (0 phase start, 1 admissible fill, 2 claim
+// rounds, 3 updates, 4 CSR rebuild) through every phase until it stops with
+// ctr[kCtrHold] = 9 (n_i <= threshold), 10 (fcounts full), 1-4 (as above; 4:
+// records beyond r_cap) or 11 (status set).  Records go to r_key / r_val.
+cudaError_t ot_dev_phase_loop(OtDev& D, int stage, double threshold, int* scratch, cudaStream_t s);
 cudaError_t ot_dev_resolve(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
                            unsigned long long* out_key, int64_t* out_val, cudaStream_t s);
 cudaError_t ot_dev_consumed(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,

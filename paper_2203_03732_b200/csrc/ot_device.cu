@@ -53,6 +53,9 @@ __device__ __forceinline__ void ot_fail(OtDev& D, int code, int x = 0, int y = 0
   }
 }
 
+// The device-sized phase stopped for the host (kCtrHold): later steps return.
+__device__ __forceinline__ bool ot_hold(const OtDev& D) { return *(volatile int64_t*)&D.ctr[kCtrHold] != 0; }
+
 template <typename T>
 __device__ __forceinline__ uint32_t k_at(const OtDev& D, int a, int b) {
   return static_cast<const T*>(D.kT)[(size_t)b * D.lda + a];
@@ -67,9 +70,10 @@ __device__ __forceinline__ int64_t sfree_total(const OtDev& D, int b) {
 
 constexpr int kListBlocks = 148;
 
-__global__ void __launch_bounds__(1024) ot_free_count_kernel(OtDev D, int* counts) {
-  const int n = D.n_b, chunk = (n + gridDim.x - 1) / gridDim.x;
-  const int lo = min(n, (int)blockIdx.x * chunk), hi = min(n, lo + chunk);
+__device__ __forceinline__ void ot_free_count_body(OtDev& D, int* counts, int bid, int nb) {
+  if (ot_hold(D)) return;
+  const int n = D.n_b, chunk = (n + nb - 1) / nb;
+  const int lo = min(n, bid * chunk), hi = min(n, lo + chunk);
   int c = 0;
   long long tot = 0;
   for (int b = lo + threadIdx.x; b < hi; b += blockDim.x) {
@@ -89,21 +93,23 @@ __global__ void __launch_bounds__(1024) ot_free_count_kernel(OtDev D, int* count
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    counts[blockIdx.x] = s_c;
+    counts[bid] = s_c;
     if (s_t) atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrNi]), s_t);
   }
 }
+__global__ void __launch_bounds__(1024) ot_free_count_kernel(OtDev D, int* counts) { ot_free_count_body(D, counts, blockIdx.x, gridDim.x); }
 
-__global__ void __launch_bounds__(1024) ot_free_write_kernel(OtDev D, const int* counts) {
+__device__ __forceinline__ void ot_free_write_body(OtDev& D, const int* counts, int bid, int nb) {
+  if (ot_hold(D)) return;
   __shared__ int s_warp[32];
   __shared__ int s_base;
-  const int n = D.n_b, chunk = (n + gridDim.x - 1) / gridDim.x;
-  const int lo = min(n, (int)blockIdx.x * chunk), hi = min(n, lo + chunk);
+  const int n = D.n_b, chunk = (n + nb - 1) / nb;
+  const int lo = min(n, bid * chunk), hi = min(n, lo + chunk);
   if (threadIdx.x == 0) {
     int off = 0;
-    for (int g = 0; g < (int)blockIdx.x; ++g) off += counts[g];
+    for (int g = 0; g < bid; ++g) off += counts[g];
     s_base = off;
-    if (blockIdx.x == gridDim.x - 1) D.ctr[kCtrFree] = off + counts[blockIdx.x];
+    if (bid == nb - 1) D.ctr[kCtrFree] = off + counts[bid];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -135,12 +141,13 @@ __global__ void __launch_bounds__(1024) ot_free_write_kernel(OtDev D, const int*
     __syncthreads();
   }
 }
+__global__ void __launch_bounds__(1024) ot_free_write_kernel(OtDev D, const int* counts) { ot_free_write_body(D, counts, blockIdx.x, gridDim.x); }
 
 // t_ci(a) = -y of cluster (a, ci), type max when absent (never admissible).
 template <typename T>
-__global__ void ot_t_kernel(OtDev D) {
+__device__ __forceinline__ void ot_t_body(OtDev& D, int bid, int nb) {
   T* t = static_cast<T*>(D.t);
-  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < D.lda; a += gridDim.x * blockDim.x)
+  for (int a = bid * blockDim.x + threadIdx.x; a < D.lda; a += nb * blockDim.x)
     for (int s = 0; s < 2; ++s) {
       uint32_t v = type_max<T>();
       if (a < D.n_a && D.dfree[2 * a + s] + D.dmatched[2 * a + s] > 0) {
@@ -151,20 +158,27 @@ __global__ void ot_t_kernel(OtDev D) {
       t[(size_t)s * D.lda + a] = (T)v;
     }
 }
+template <typename T>
+__global__ void ot_t_kernel(OtDev D) { ot_t_body<T>(D, blockIdx.x, gridDim.x); }
 
 // ---- admissible clusters (warp per free b, full row) ---------------------------
 // pass 0: count; pass 1: write codes 2a + ci ascending a at adm_off[i].
 template <typename T, int kPass>
-__global__ void __launch_bounds__(256) ot_adm_kernel(OtDev D) {
+__device__ __forceinline__ void ot_adm_body(OtDev& D, int bid, int nb) {
   using S = Simd<T>;
   constexpr int kEpv = 16 / sizeof(T);
   const int lane = threadIdx.x & 31;
+  if (ot_hold(D)) return;
   const int nf = D.ctr[kCtrFree];
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  if (kPass && D.adm_cap > 0 && D.adm_off[nf] > D.adm_cap) {  // (device-sized phase) the host grows adm
+    if (bid == 0 && threadIdx.x == 0) D.ctr[kCtrHold] = 1;
+    return;
+  }
+  const int nwarps = (nb * blockDim.x) >> 5;
   const uint4* v0 = static_cast<const uint4*>(D.t);
   const uint4* v1 = reinterpret_cast<const uint4*>(static_cast<const T*>(D.t) + D.lda);
   const int nv = D.lda / kEpv;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nf; i += nwarps) {
+  for (int i = (bid * blockDim.x + threadIdx.x) >> 5; i < nf; i += nwarps) {
     const int b = D.fb[i];
     const uint32_t tg = S::rep((uint32_t)(D.fy[i] - 1));
     const uint4* rv = reinterpret_cast<const uint4*>(static_cast<const T*>(D.kT) + (size_t)b * D.lda);
@@ -209,6 +223,8 @@ __global__ void __launch_bounds__(256) ot_adm_kernel(OtDev D) {
     if (!kPass && lane == 0) D.adm_len[i] = cnt;
   }
 }
+template <typename T, int kPass>
+__global__ void __launch_bounds__(256) ot_adm_kernel(OtDev D) { ot_adm_body<T, kPass>(D, blockIdx.x, gridDim.x); }
 
 // ---- deferred acceptance -------------------------------------------------------
 // Entries: key = (code << 21) | list index, value = copies.
@@ -216,10 +232,12 @@ __global__ void __launch_bounds__(256) ot_adm_kernel(OtDev D) {
 // (-1: capacity 0); INT_MAX while it has room.  A b above the cut would be
 // rejected there, so it skips the cluster without a round (the cut only falls
 // once set, so a stale value only skips less).
-__global__ void ot_cut_init_kernel(OtDev D) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 2 * D.n_a; c += gridDim.x * blockDim.x)
+__device__ __forceinline__ void ot_cut_init_body(OtDev& D, int bid, int nb) {
+  if (ot_hold(D)) return;
+  for (int c = bid * blockDim.x + threadIdx.x; c < 2 * D.n_a; c += nb * blockDim.x)
     D.cl_cut[c] = D.dfree[c] + D.dmatched[c] > 0 ? INT_MAX : -1;
 }
+__global__ void ot_cut_init_kernel(OtDev D) { ot_cut_init_body(D, blockIdx.x, gridDim.x); }
 
 __global__ void ot_da_propose_kernel(OtDev D) {
   const int nf = D.ctr[kCtrFree];
@@ -282,17 +300,19 @@ __global__ void ot_da_resolve_kernel(OtDev D, const unsigned long long* __restri
 // exactly as ot_da_resolve_kernel does on the sorted run.  Every kernel
 // returns at once when the rounds are over (ctr[kCtrDone]), so a batch of
 // rounds is launched without looking at the counters.
-__device__ __forceinline__ bool da_over(const OtDev& D) { return *(volatile int64_t*)&D.ctr[kCtrDone] != 0; }
+__device__ __forceinline__ bool da_over(const OtDev& D) {
+  return *(volatile int64_t*)&D.ctr[kCtrDone] != 0 || ot_hold(D);
+}
 
-__global__ void ot_da_propose_batched_kernel(OtDev D) {
+__device__ __forceinline__ void ot_da_propose_batched_body(OtDev& D, int bid, int nb) {
   if (da_over(D)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // (unused by propose; reset for this round's count / alloc)
+  if (bid == 0 && threadIdx.x == 0) {  // (unused by propose; reset for this round's count / alloc)
     D.ctr[kCtrTouch] = 0;
     D.ctr[kCtrAlloc] = 0;
   }
   const int nf = D.ctr[kCtrFree];
   const long long base = D.ctr[kCtrE];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+  for (int i = bid * blockDim.x + threadIdx.x; i < nf; i += nb * blockDim.x) {
     const int64_t u = D.fu[i];
     if (u <= 0) continue;
     int p = D.fpos[i];
@@ -308,33 +328,35 @@ __global__ void ot_da_propose_batched_kernel(OtDev D) {
     D.fu[i] = 0;
   }
 }
+__global__ void ot_da_propose_batched_kernel(OtDev D) { ot_da_propose_batched_body(D, blockIdx.x, gridDim.x); }
 
-__global__ void ot_da_count_kernel(OtDev D) {
+__device__ __forceinline__ void ot_da_count_body(OtDev& D, int bid, int nb) {
   if (da_over(D)) return;
   const long long nn = D.ctr[kCtrNew];
   if (nn == 0) {  // no b has copies to place and a cluster to try: the claims are final
-    if (blockIdx.x == 0 && threadIdx.x == 0) D.ctr[kCtrDone] = 1;
+    if (bid == 0 && threadIdx.x == 0) D.ctr[kCtrDone] = 1;
     return;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ++D.ctr[kCtrRounds];
+  if (bid == 0 && threadIdx.x == 0) ++D.ctr[kCtrRounds];
   const long long n = D.ctr[kCtrE] + nn;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+  for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x) {
     const int code = (int)(D.e_key[j] >> 21);
     if (atomicAdd(&D.da_cnt[code], 1) == 0)
       D.da_touch[atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrTouch]), 1ull)] = code;
   }
 }
+__global__ void ot_da_count_kernel(OtDev D) { ot_da_count_body(D, blockIdx.x, gridDim.x); }
 
-__global__ void ot_da_alloc_kernel(OtDev D) {
+__device__ __forceinline__ void ot_da_alloc_body(OtDev& D, int bid, int nb) {
   if (da_over(D)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // (nobody below reads E / New)
+  if (bid == 0 && threadIdx.x == 0) {  // (nobody below reads E / New)
     D.ctr[kCtrN] = D.ctr[kCtrE] + D.ctr[kCtrNew];
     D.ctr[kCtrE] = 0;
   }
   const int nt = (int)D.ctr[kCtrTouch];
   const int lane = threadIdx.x & 31;
   // whole warps iterate (one aggregated atomic per warp)
-  for (int t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; t0 < nt; t0 += gridDim.x * blockDim.x) {
+  for (int t0 = (bid * blockDim.x + threadIdx.x) & ~31; t0 < nt; t0 += nb * blockDim.x) {
     const int t = t0 + lane;
     int code = -1, c = 0;
     if (t < nt) {
@@ -354,15 +376,16 @@ __global__ void ot_da_alloc_kernel(OtDev D) {
     if (code >= 0) D.da_off[code] = (int64_t)(base + inc - c);
   }
 }
+__global__ void ot_da_alloc_kernel(OtDev D) { ot_da_alloc_body(D, blockIdx.x, gridDim.x); }
 
-__global__ void ot_da_scatter_kernel(OtDev D) {
+__device__ __forceinline__ void ot_da_scatter_body(OtDev& D, int bid, int nb) {
   if (da_over(D)) return;
   if (D.ctr[kCtrBig]) {  // (set by the allocation: every block sees it)
-    if (blockIdx.x == 0 && threadIdx.x == 0) D.ctr[kCtrDone] = 2;
+    if (bid == 0 && threadIdx.x == 0) D.ctr[kCtrDone] = 2;
     return;
   }
   const long long n = D.ctr[kCtrN];
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+  for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x) {
     const unsigned long long k = D.e_key[j];
     const int code = (int)(k >> 21);
     const long long pos = D.da_off[code] + atomicAdd(&D.da_fill[code], 1);
@@ -370,14 +393,15 @@ __global__ void ot_da_scatter_kernel(OtDev D) {
     D.s_val[pos] = D.e_val[j];
   }
 }
+__global__ void ot_da_scatter_kernel(OtDev D) { ot_da_scatter_body(D, blockIdx.x, gridDim.x); }
 
-__global__ void ot_da_resolve_warp_kernel(OtDev D) {
+__device__ __forceinline__ void ot_da_resolve_warp_body(OtDev& D, int bid, int nb) {
   if (da_over(D)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) D.ctr[kCtrNew] = 0;  // (count has read it) next round's proposals
+  if (bid == 0 && threadIdx.x == 0) D.ctr[kCtrNew] = 0;  // (count has read it) next round's proposals
   const int lane = threadIdx.x & 31;
   const int nt = (int)D.ctr[kCtrTouch];
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nt; t += warps) {
+  const int warps = nb * (blockDim.x >> 5);
+  for (int t = bid * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nt; t += warps) {
     const int code = D.da_touch[t];
     const int c = D.da_cnt[code];
     const long long o = D.da_off[code];
@@ -427,6 +451,7 @@ __global__ void ot_da_resolve_warp_kernel(OtDev D) {
     }
   }
 }
+__global__ void ot_da_resolve_warp_kernel(OtDev D) { ot_da_resolve_warp_body(D, blockIdx.x, gridDim.x); }
 
 // After a round that went the sorted way: the per-cluster counts back to 0.
 __global__ void ot_da_clear_kernel(OtDev D) {
@@ -440,11 +465,15 @@ __global__ void ot_da_clear_kernel(OtDev D) {
 
 // ---- updates -------------------------------------------------------------------
 // Copies each demand cluster gave this phase (final claims sorted by code).
-__global__ void ot_consumed_kernel(OtDev D, const unsigned long long* __restrict__ key,
-                                   const int64_t* __restrict__ val, long long n) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+__device__ __forceinline__ void ot_consumed_body(OtDev& D, const unsigned long long* __restrict__ key,
+                                   const int64_t* __restrict__ val, long long n, int bid, int nb) {
+  if (ot_hold(D)) return;
+  if (n < 0) n = D.ctr[kCtrE];
+  for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x)
     atomicAdd(reinterpret_cast<unsigned long long*>(&D.consumed[key[j] >> 21]), (unsigned long long)val[j]);
 }
+__global__ void ot_consumed_kernel(OtDev D, const unsigned long long* __restrict__ key,
+                                   const int64_t* __restrict__ val, long long n) { ot_consumed_body(D, key, val, n, blockIdx.x, gridDim.x); }
 
 // Records of the next state, key (a, descending y, b), b = kFreeB for free
 // demand copies: surviving flow entries (the displaced prefix removed, its
@@ -463,9 +492,10 @@ __device__ __forceinline__ void put_rec(OtDev& D, int a, int y, int b, int64_t c
 }
 
 template <typename T>
-__global__ void ot_flow_records_kernel(OtDev D) {
+__device__ __forceinline__ void ot_flow_records_body(OtDev& D, int bid, int nb) {
+  if (ot_hold(D)) return;
   const long long nfl = D.fl_off[2 * D.n_a];
-  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < nfl; f += (long long)gridDim.x * blockDim.x) {
+  for (long long f = bid * (long long)blockDim.x + threadIdx.x; f < nfl; f += (long long)nb * blockDim.x) {
     const int code = D.fl_code[f];
     const int a = code >> 1, y = D.dy[code], b = D.fl_b[f];
     const int64_t cnt = D.fl_cnt[f];
@@ -494,22 +524,29 @@ __global__ void ot_flow_records_kernel(OtDev D) {
     }
   }
 }
+template <typename T>
+__global__ void ot_flow_records_kernel(OtDev D) { ot_flow_records_body<T>(D, blockIdx.x, gridDim.x); }
 
-__global__ void ot_claim_records_kernel(OtDev D, const unsigned long long* __restrict__ key,
-                                        const int64_t* __restrict__ val, long long n) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void ot_claim_records_body(OtDev& D, const unsigned long long* __restrict__ key,
+                                        const int64_t* __restrict__ val, long long n, int bid, int nb) {
+  if (ot_hold(D)) return;
+  if (n < 0) n = D.ctr[kCtrE];
+  for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x) {
     const int code = (int)(key[j] >> 21), i = (int)(key[j] & ((1u << 21) - 1));
     put_rec(D, code >> 1, D.dy[code] - 1, D.fb[i], val[j]);
   }
 }
+__global__ void ot_claim_records_kernel(OtDev D, const unsigned long long* __restrict__ key,
+                                        const int64_t* __restrict__ val, long long n) { ot_claim_records_body(D, key, val, n, blockIdx.x, gridDim.x); }
 
 // Supply side (ot.cpp:540-553, 580-588): a free b's copies placed this phase
 // join its free cluster's matched copies, the rest go up a unit; displaced
 // copies come back free at their cluster; then normalize_supply: every free
 // copy lifted to the vertex maximum dual, equal duals merged, empty dropped,
 // at most two clusters (slot 0 the higher dual).
-__global__ void ot_supply_kernel(OtDev D) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < D.n_b; b += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void ot_supply_body(OtDev& D, int bid, int nb) {
+  if (ot_hold(D)) return;
+  for (int b = bid * blockDim.x + threadIdx.x; b < D.n_b; b += nb * blockDim.x) {
     int y[3];
     int64_t fr[3], mt[3];
     int n = 0;
@@ -584,12 +621,15 @@ __global__ void ot_supply_kernel(OtDev D) {
     }
   }
 }
+__global__ void ot_supply_kernel(OtDev D) { ot_supply_body(D, blockIdx.x, gridDim.x); }
 
 // After the records are sorted and merged (unique keys, summed counts): the
 // record's demand slot (0 for the vertex's first dual, 1 for the second; a
 // third is the reference's "third dual value" violation) and its code.
-__global__ void ot_slot_kernel(OtDev D, const unsigned long long* __restrict__ key, long long n) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void ot_slot_body(OtDev& D, const unsigned long long* __restrict__ key, long long n, int bid, int nb) {
+  if (ot_hold(D)) return;
+  if (n < 0) n = D.ctr[kCtrNFlows];
+  for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x) {
     const unsigned long long kj = key[j];
     const unsigned long long a = kj >> 42, yk = (kj >> 21) & ((1ull << 21) - 1);
     // first record of a: lower_bound of (a, 0, 0)
@@ -615,13 +655,16 @@ __global__ void ot_slot_kernel(OtDev D, const unsigned long long* __restrict__ k
     D.fl_code[j] = (int)(2 * a) + min(slot, 1);
   }
 }
+__global__ void ot_slot_kernel(OtDev D, const unsigned long long* __restrict__ key, long long n) { ot_slot_body(D, key, n, blockIdx.x, gridDim.x); }
 
 // New CSR: fl_off[c] = first record of code c (lower bound), cluster fields
 // from the code's segment, the flow prefix sums for the next displacement.
-__global__ void ot_rebuild_kernel(OtDev D, const unsigned long long* __restrict__ key,
-                                  const int64_t* __restrict__ val, long long n) {
+__device__ __forceinline__ void ot_rebuild_body(OtDev& D, const unsigned long long* __restrict__ key,
+                                  const int64_t* __restrict__ val, long long n, int bid, int nb) {
+  if (ot_hold(D)) return;
+  if (n < 0) n = D.ctr[kCtrNFlows];
   const int nc = 2 * D.n_a;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= nc; c += gridDim.x * blockDim.x) {
+  for (int c = bid * blockDim.x + threadIdx.x; c <= nc; c += nb * blockDim.x) {
     long long lo = 0, hi = n;
     while (lo < hi) {
       const long long mid = (lo + hi) >> 1;
@@ -647,6 +690,231 @@ __global__ void ot_rebuild_kernel(OtDev D, const unsigned long long* __restrict_
     D.dmatched[c] = mt;
     D.consumed[c] = 0;
   }
+}
+__global__ void ot_rebuild_kernel(OtDev D, const unsigned long long* __restrict__ key,
+                                  const int64_t* __restrict__ val, long long n) { ot_rebuild_body(D, key, val, n, blockIdx.x, gridDim.x); }
+
+// ---- device-sized phase helpers ----------------------------------------------
+// adm_off = exclusive prefix of adm_len[0, nf), adm_off[nf] = total: one
+// block (n_free <= n_b), each thread a contiguous chunk.
+__device__ __forceinline__ void ot_adm_scan_body(OtDev& D, int bid, int nb) {
+  if (ot_hold(D)) return;
+  const int nf = (int)D.ctr[kCtrFree];
+  const int per = (nf + blockDim.x - 1) / blockDim.x;
+  const int lo = min(nf, (int)threadIdx.x * per), hi = min(nf, lo + per);
+  int64_t sum = 0;
+  for (int i = lo; i < hi; ++i) sum += D.adm_len[i];
+  __shared__ int64_t s_part[1024];
+  s_part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // inclusive (Hillis-Steele)
+    const int64_t y = (int)threadIdx.x >= o ? s_part[threadIdx.x - o] : 0;
+    __syncthreads();
+    s_part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  int64_t run = s_part[threadIdx.x] - sum;
+  for (int i = lo; i < hi; ++i) {
+    D.adm_off[i] = run;
+    run += D.adm_len[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) D.adm_off[nf] = s_part[threadIdx.x];
+}
+__global__ void __launch_bounds__(1024) ot_adm_scan_kernel(OtDev D) { ot_adm_scan_body(D, blockIdx.x, gridDim.x); }
+
+// After the batch of claim rounds: not over (or a round that needs the sort)
+// -> the host continues them.
+__device__ __forceinline__ void ot_da_gate_body(OtDev& D, int bid, int nb) {
+  if (!ot_hold(D) && D.ctr[kCtrDone] != 1) D.ctr[kCtrHold] = 2;
+}
+__global__ void ot_da_gate_kernel(OtDev D) { ot_da_gate_body(D, blockIdx.x, gridDim.x); }
+
+// The records (keys, counts) of the next state sorted and merged in one block
+// (bitonic sort of the next power of two in shared memory, then one thread
+// per run of equal keys), written back over the input; ctr[kCtrNFlows] =
+// runs.  More than kOtSmallRec records: kCtrHold = 3 (the host sorts).
+__device__ __forceinline__ void ot_small_merge_body(OtDev& D, unsigned long long* __restrict__ key,
+                                                             int64_t* __restrict__ val, int bid, int nb) {
+  if (ot_hold(D)) return;
+  const int n = (int)D.ctr[kCtrRec];
+  if (n > kOtSmallRec) {
+    if (threadIdx.x == 0) D.ctr[kCtrHold] = 3;
+    return;
+  }
+  extern __shared__ __align__(16) unsigned long long s_key[];
+  int P = 2;
+  while (P < n) P <<= 1;
+  int64_t* s_val = reinterpret_cast<int64_t*>(s_key + P);
+  __shared__ int s_heads[1024];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    s_key[i] = i < n ? key[i] : ~0ull;
+    s_val[i] = i < n ? val[i] : 0;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long ki = s_key[i], kl = s_key[l];
+          if (((i & k) == 0) == (ki > kl)) {
+            s_key[i] = kl;
+            s_key[l] = ki;
+            const int64_t t = s_val[i];
+            s_val[i] = s_val[l];
+            s_val[l] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // runs: thread chunks of the sorted keys, heads counted per chunk, scanned
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  int h = 0;
+  for (int i = lo; i < hi; ++i) h += (i == 0 || s_key[i] != s_key[i - 1]);
+  s_heads[threadIdx.x] = h;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int y = (int)threadIdx.x >= o ? s_heads[threadIdx.x - o] : 0;
+    __syncthreads();
+    s_heads[threadIdx.x] += y;
+    __syncthreads();
+  }
+  int out = s_heads[threadIdx.x] - h;
+  for (int i = lo; i < hi; ++i) {
+    if (i != 0 && s_key[i] == s_key[i - 1]) continue;
+    int64_t sum = 0;
+    for (int q = i; q < n && s_key[q] == s_key[i]; ++q) sum += s_val[q];
+    key[out] = s_key[i];
+    val[out] = sum;
+    ++out;
+  }
+  if (threadIdx.x == blockDim.x - 1) D.ctr[kCtrNFlows] = s_heads[threadIdx.x];
+}
+__global__ void __launch_bounds__(1024) ot_small_merge_kernel(OtDev D, unsigned long long* __restrict__ key,
+                                                             int64_t* __restrict__ val) { ot_small_merge_body(D, key, val, blockIdx.x, gridDim.x); }
+
+
+// ---- the persistent phase loop (one cooperative launch) --------------------------
+__device__ __forceinline__ void ot_grid_bar(OtDev& D, unsigned& target, int nb) {
+  if (nb == 1) {  // one block: the block barrier is the grid barrier
+    __syncthreads();
+    return;
+  }
+  target += (unsigned)nb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(D.bar) : "memory");
+    if ((int)(ld_acquire(D.bar) - target) < 0) {
+      const unsigned long long t0 = globaltimer();
+      while ((int)(ld_acquire(D.bar) - target) < 0) {
+        if (globaltimer() - t0 > 4000000000ull) {
+          ot_fail(D, 6, (int)blockIdx.x);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int64_t ot_vol(const int64_t* p) { return *(volatile const int64_t*)p; }
+
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) ot_phase_loop_kernel(OtDev D, int stage, double threshold, int* counts) {
+  const int bid = blockIdx.x, nb = gridDim.x;
+  const bool lead = bid == 0 && threadIdx.x == 0;
+  unsigned target = *(volatile unsigned*)(D.bar + 1);
+  int64_t* ctr = D.ctr;
+  while (true) {
+    if (stage <= 0) {
+      const int64_t n_i = ot_vol(ctr + kCtrNi);
+      if ((double)n_i <= threshold || ot_vol(D.loop) >= D.fc_cap || *(volatile int*)D.status != 0) {
+        if (lead) ctr[kCtrHold] = *(volatile int*)D.status != 0 ? 11 : ((double)n_i <= threshold ? 9 : 10);
+        break;
+      }
+      if (lead) {
+        for (int k = 2; k < kCtrCount; ++k) ctr[k] = 0;
+        D.fcounts[D.loop[0]] = n_i;
+      }
+      ot_grid_bar(D, target, nb);
+      ot_t_body<T>(D, bid, nb);
+      ot_grid_bar(D, target, nb);
+      ot_adm_body<T, 0>(D, bid, nb);
+      ot_grid_bar(D, target, nb);
+      if (bid == 0) ot_adm_scan_body(D, bid, 1);
+      ot_grid_bar(D, target, nb);
+    }
+    if (stage <= 1) {
+      const int nf = (int)ot_vol(ctr + kCtrFree);
+      const int64_t total = ot_vol(D.adm_off + nf);
+      if (total > D.adm_cap || total + nf + 1 > D.e_cap) {  // (uniform: every block reads the same)
+        if (lead) ctr[kCtrHold] = 1;
+        break;
+      }
+      ot_adm_body<T, 1>(D, bid, nb);
+      ot_cut_init_body(D, bid, nb);
+      ot_grid_bar(D, target, nb);
+    }
+    if (stage <= 2) {
+      bool big = false;
+      while (true) {
+        ot_da_propose_batched_body(D, bid, nb);
+        ot_grid_bar(D, target, nb);
+        ot_da_count_body(D, bid, nb);
+        ot_grid_bar(D, target, nb);
+        if (ot_vol(ctr + kCtrDone) != 0) break;
+        ot_da_alloc_body(D, bid, nb);
+        ot_grid_bar(D, target, nb);
+        ot_da_scatter_body(D, bid, nb);
+        ot_grid_bar(D, target, nb);
+        if (ot_vol(ctr + kCtrDone) == 2) {
+          big = true;
+          break;
+        }
+        ot_da_resolve_warp_body(D, bid, nb);
+        ot_grid_bar(D, target, nb);
+      }
+      if (big) {  // a cluster past the warp resolve: that round sorted on the host
+        if (lead) ctr[kCtrHold] = 2;
+        break;
+      }
+    }
+    if (stage <= 3) {
+      if (ot_vol(D.fl_off + 2 * D.n_a) + ot_vol(ctr + kCtrE) + 2 * (int64_t)D.n_a + 16 > D.r_cap) {
+        if (lead) ctr[kCtrHold] = 4;
+        break;
+      }
+      ot_consumed_body(D, D.e_key, D.e_val, -1, bid, nb);
+      ot_claim_records_body(D, D.e_key, D.e_val, -1, bid, nb);
+      ot_grid_bar(D, target, nb);
+      ot_flow_records_body<T>(D, bid, nb);
+      ot_grid_bar(D, target, nb);
+      ot_supply_body(D, bid, nb);
+      if (bid == 0) {
+        __syncthreads();  // (block 0's supply threads done; the merge needs the whole block)
+        ot_small_merge_body(D, D.r_key, D.r_val, bid, 1);
+      }
+      ot_grid_bar(D, target, nb);
+      if (ot_vol(ctr + kCtrHold) != 0) break;  // 3: more records than one block merges
+    }
+    ot_slot_body(D, D.r_key, -1, bid, nb);
+    ot_grid_bar(D, target, nb);
+    ot_rebuild_body(D, D.r_key, D.r_val, -1, bid, nb);
+    if (lead) {
+      ctr[kCtrNi] = 0;
+      D.loop[0] += 1;
+      D.loop[1] += ctr[kCtrRounds];
+    }
+    ot_grid_bar(D, target, nb);
+    ot_free_count_body(D, counts, bid, nb);
+    ot_grid_bar(D, target, nb);
+    ot_free_write_body(D, counts, bid, nb);
+    ot_grid_bar(D, target, nb);
+    stage = 0;
+  }
+  if (lead) D.bar[1] = target;
 }
 
 }  // namespace
@@ -695,6 +963,52 @@ cudaError_t ot_dev_da_rounds(OtDev& D, int rounds, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t ot_dev_phase_begin(OtDev& D, cudaStream_t s) {
+  return cudaMemsetAsync(D.ctr + 2, 0, (kCtrCount - 2) * sizeof(int64_t), s);
+}
+
+cudaError_t ot_dev_adm_scan(OtDev& D, cudaStream_t s) {
+  ot_adm_scan_kernel<<<1, 1024, 0, s>>>(D);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_da_gate(OtDev& D, cudaStream_t s) {
+  ot_da_gate_kernel<<<1, 1, 0, s>>>(D);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_small_merge(OtDev& D, unsigned long long* key, int64_t* val, cudaStream_t s) {
+  const size_t smem = (size_t)kOtSmallRec * 16;
+  smem_attr_raise(reinterpret_cast<const void*>(ot_small_merge_kernel), smem);
+  ot_small_merge_kernel<<<1, 1024, smem, s>>>(D, key, val);
+  return cudaGetLastError();
+}
+
+cudaError_t ot_dev_phase_loop(OtDev& D, int stage, double threshold, int* scratch, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  with_width(D.width, [&](auto tag) {
+    using T = decltype(tag);
+    auto fn = ot_phase_loop_kernel<T>;
+    const size_t smem = (size_t)kOtSmallRec * 16;
+    smem_attr_raise(reinterpret_cast<const void*>(fn), smem);
+    int dev = 0, sms = 148, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 1024, smem) != cudaSuccess || per < 1) {
+      e = cudaErrorLaunchOutOfResources;
+      return 0;
+    }
+    // blocks: one per 64 supply vertices up to one per SM (small instances
+    // are barrier-bound: fewer blocks, cheaper barriers; one block needs none)
+    const int grid = std::max(1, std::min(std::min(sms, kListBlocks), D.n_b / 64));
+    void* args[] = {&D, &stage, &threshold, &scratch};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(1024), args, smem, s);
+    return 0;
+  });
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t ot_dev_da_clear(OtDev& D, cudaStream_t s) {
   ot_da_clear_kernel<<<148, 256, 0, s>>>(D);
   return cudaGetLastError();
@@ -710,8 +1024,9 @@ cudaError_t ot_dev_resolve(OtDev& D, const unsigned long long* key, const int64_
 
 cudaError_t ot_dev_consumed(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
                             cudaStream_t s) {
-  if (n > 0)
-    ot_consumed_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, val, n);
+  if (n != 0)
+    ot_consumed_kernel<<<n < 0 ? 148 * 4 : (int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key,
+                                                                                                       val, n);
   return cudaGetLastError();
 }
 
@@ -721,15 +1036,17 @@ cudaError_t ot_dev_records(OtDev& D, const unsigned long long* key, const int64_
     ot_flow_records_kernel<decltype(tag)><<<148 * 8, 256, 0, s>>>(D);
     return 0;
   });
-  if (n > 0)
-    ot_claim_records_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, val, n);
+  if (n != 0)
+    ot_claim_records_kernel<<<n < 0 ? 148 * 4 : (int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(
+        D, key, val, n);
   ot_supply_kernel<<<(D.n_b + 255) / 256, 256, 0, s>>>(D);
   return cudaGetLastError();
 }
 
 cudaError_t ot_dev_rebuild(OtDev& D, const unsigned long long* key, const int64_t* val, long long n,
                            cudaStream_t s) {
-  if (n > 0) ot_slot_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, n);
+  if (n != 0)
+    ot_slot_kernel<<<n < 0 ? 148 * 4 : (int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(D, key, n);
   ot_rebuild_kernel<<<(2 * D.n_a + 1 + 255) / 256, 256, 0, s>>>(D, key, val, n);
   return cudaGetLastError();
 }

@@ -470,7 +470,7 @@ class OtSolver {
   enum Buf {
     bT, bDy, bDfree, bDmatched, bConsumed, bFlOff, bFlCode, bFlB, bFlCnt, bFlPre, bSy, bSfree, bSmatched,
     bSfreed, bFb, bFy, bFpos, bFidx, bFu0, bFu, bAdmLen, bAdmOff, bAdm, bEk0, bEv0, bEk1, bEv1, bRk0, bRv0,
-    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bDaCnt, bDaFill, bDaOff, bDaTouch, bNum
+    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bDaCnt, bDaFill, bDaOff, bDaTouch, bBar, bLoop, bFcounts, bNum
   };
   otprg::OtDev D_{};
   int64_t fl_cap_ = 0, adm_cap_ = 0, e_cap_ = 0, r_cap_ = 0;
@@ -494,7 +494,7 @@ class OtSolver {
   }
 
   void alloc_device() {
-    static_assert(bNum <= 40, "ot_dev slots");
+    static_assert(bNum <= 48, "ot_dev slots");
     if (n_b_ >= (1 << 21) - 1 || n_a_ >= (1 << 21) || unit_ceil_ + 4 >= (1 << 19))
       throw OtError{OTPRG_PARAMETER, "OT instance beyond the device state's index range (n < 2^21, 1/eps < 2^19)"};
     const size_t na2 = 2 * static_cast<size_t>(n_a_), nb = n_b_, nb2 = 2 * nb;
@@ -735,8 +735,388 @@ class OtSolver {
     }
   }
 
+
+  // The flow arrays grown with their live entries (n_flows_) kept.
+  void grow_flows_keep(int64_t n) {
+    if (n <= fl_cap_) return;
+    const int64_t c = std::max<int64_t>(n, fl_cap_ * 3 / 2);
+    const size_t live = static_cast<size_t>(n_flows_);
+    DevBuf tmp;
+    if (live) {
+      OT_CK(tmp.ensure(live * 24), "alloc");
+      char* t = static_cast<char*>(tmp.p);
+      OT_CK(cudaMemcpyAsync(t, D_.fl_code, live * 4, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(t + live * 4, D_.fl_b, live * 4, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(t + live * 8, D_.fl_cnt, live * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(t + live * 16, D_.fl_pre, live * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaStreamSynchronize(ctx_->stream), "grow");
+    }
+    D_.fl_code = ensure<int32_t>(bFlCode, c);
+    D_.fl_b = ensure<int32_t>(bFlB, c);
+    D_.fl_cnt = ensure<int64_t>(bFlCnt, c);
+    D_.fl_pre = ensure<int64_t>(bFlPre, c);
+    fl_cap_ = c;
+    if (live) {
+      const char* t = static_cast<const char*>(tmp.p);
+      OT_CK(cudaMemcpyAsync(D_.fl_code, t, live * 4, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(D_.fl_b, t + live * 4, live * 4, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(D_.fl_cnt, t + live * 8, live * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaMemcpyAsync(D_.fl_pre, t + live * 16, live * 8, cudaMemcpyDeviceToDevice, ctx_->stream), "copy");
+      OT_CK(cudaStreamSynchronize(ctx_->stream), "grow");
+    }
+  }
+
+
+  // solve_copy_matching as one cooperative launch for the whole phase loop
+  // (ot_dev_phase_loop: the steps of the device-sized phase separated by grid
+  // barriers, the claim rounds looped on the device); the host relaunches
+  // only when the loop holds (capacity, a round for the sort, records beyond
+  // one block's merge) after finishing that step, as in the launch-sequence
+  // form below.
+  void solve_copy_matching_persistent() {
+    upload_initial();
+    const double threshold = eps_in_ * static_cast<double>(sm_.total_s);
+    const int64_t phase_cap =
+        static_cast<int64_t>(std::ceil((1.0 + 2.0 * eps_in_) / (eps_in_ * eps_in_))) + 8;
+    cudaStream_t s = ctx_->stream;
+    int64_t holds = 0, relaunches = 0;
+    std::vector<int64_t> free_counts;
+    Timer loop_t;
+    int* scratch = ensure<int>(bScratch, 256);
+    const int end_bit = 21 + 1 + static_cast<int>(std::ceil(std::log2(2.0 * n_a_ + 1.0)));
+    // (test knob: tiny buffers, so every hold of the loop is taken)
+    const bool small_caps = std::getenv("OTPRG_OT_SMALL_CAPS") != nullptr;
+    D_.bar = ensure<unsigned>(bBar, 2);
+    D_.loop = ensure<int64_t>(bLoop, 4);
+    D_.fc_cap = small_caps ? 3 : std::min<int64_t>(phase_cap + 2, int64_t(1) << 20);
+    D_.fcounts = ensure<int64_t>(bFcounts, D_.fc_cap);
+    OT_CK(cudaMemsetAsync(D_.bar, 0, 2 * sizeof(unsigned), s), "memset");
+    OT_CK(cudaMemsetAsync(D_.loop, 0, 4 * sizeof(int64_t), s), "memset");
+    if (adm_cap_ < 1 || small_caps) {
+      adm_cap_ = small_caps ? 8 : std::max<int64_t>(int64_t(1) << 20, 8 * static_cast<int64_t>(n_b_));
+      D_.adm = ensure<int32_t>(bAdm, adm_cap_);
+    }
+    D_.adm_cap = adm_cap_;
+    auto set_caps = [&](int64_t n_flows) {
+      if (small_caps) {  // (capacities exactly as needed now: the device checks hold the rest)
+        e_cap_ = std::max<int64_t>(e_cap_, adm_cap_ + n_b_ + 1);
+        ensure<unsigned long long>(bEk0, e_cap_);
+        ensure<int64_t>(bEv0, e_cap_);
+        ensure<unsigned long long>(bEk1, e_cap_);
+        ensure<int64_t>(bEv1, e_cap_);
+        D_.e_key = buf(bEk0).as<unsigned long long>();
+        D_.e_val = buf(bEv0).as<int64_t>();
+        D_.s_key = buf(bEk1).as<unsigned long long>();
+        D_.s_val = buf(bEv1).as<int64_t>();
+        D_.e_cap = e_cap_;
+        const int64_t r = n_flows + 2 * static_cast<int64_t>(n_a_) + 17;
+        grow(r_cap_, r, bRk0, bRv0, bRk1, bRv1, false);
+        D_.r_key = buf(bRk0).as<unsigned long long>();
+        D_.r_val = buf(bRv0).as<int64_t>();
+        D_.r_cap = std::max<int64_t>(r, std::min<int64_t>(r_cap_, r));
+        grow_flows_keep(r_cap_);
+        return;
+      }
+      grow(e_cap_, adm_cap_ + n_b_ + 1, bEk0, bEv0, bEk1, bEv1, false);
+      D_.e_key = buf(bEk0).as<unsigned long long>();
+      D_.e_val = buf(bEv0).as<int64_t>();
+      D_.s_key = buf(bEk1).as<unsigned long long>();
+      D_.s_val = buf(bEv1).as<int64_t>();
+      D_.e_cap = e_cap_;
+      grow(r_cap_, 2 * n_flows + e_cap_ + 2 * static_cast<int64_t>(n_a_) + 16, bRk0, bRv0, bRk1, bRv1, false);
+      D_.r_key = buf(bRk0).as<unsigned long long>();
+      D_.r_val = buf(bRv0).as<int64_t>();
+      D_.r_cap = r_cap_;
+      grow_flows_keep(r_cap_);
+    };
+    auto read_loop = [&](int64_t* out, int n) {
+      OT_CK(cudaMemcpyAsync(out, D_.loop, n * 8, cudaMemcpyDeviceToHost, s), "D2H");
+      OT_CK(cudaStreamSynchronize(s), "OT loop counters");
+    };
+    auto drain = [&] {  // n_i of the phases of the launches so far
+      int64_t lp[4];
+      read_loop(lp, 4);
+      if (lp[0] > 0) {
+        const size_t k = free_counts.size();
+        free_counts.resize(k + lp[0]);
+        OT_CK(cudaMemcpyAsync(free_counts.data() + k, D_.fcounts, lp[0] * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        OT_CK(cudaStreamSynchronize(s), "free counts");
+      }
+      return lp[1];
+    };
+    // the live flow count of the device state (phases advance on the device):
+    // the buffers' growth keeps that many entries
+    auto device_flows = [&] {
+      int64_t nfl = 0;
+      OT_CK(cudaMemcpy(&nfl, D_.fl_off + 2 * static_cast<size_t>(n_a_), 8, cudaMemcpyDeviceToHost), "D2H");
+      n_flows_ = nfl;
+      return nfl;
+    };
+    set_caps(n_flows_);
+    // the first phase's free list
+    OT_CK(cudaMemsetAsync(D_.ctr, 0, otprg::kCtrCount * 8, s), "memset");
+    OT_CK(otprg::ot_dev_free_list(D_, scratch, s), "free list");
+    launches_ += 2;
+    int stage = 0;
+    int64_t rounds_total = 0;
+    while (true) {
+      OT_CK(otprg::ot_dev_phase_loop(D_, stage, threshold, scratch, s), "OT phase loop launch");
+      ++relaunches;
+      launches_ += 1;
+      read_ctr();
+      const int64_t hold = hctr_[otprg::kCtrHold];
+      if (hold == 9) break;
+      ++holds;
+      if (hold == 10) {  // the free-count buffer is full: drain it
+        rounds_total += drain();
+        OT_CK(cudaMemsetAsync(D_.loop, 0, 4 * sizeof(int64_t), s), "memset");
+        if (static_cast<int64_t>(free_counts.size()) > phase_cap)
+          throw OtError{OTPRG_INVARIANT, "phase count exceeded the proven bound; solver state is corrupt"};
+        stage = 0;
+      } else if (hold == 1) {  // admissible lists / entries beyond their buffers
+        const int64_t n_free = hctr_[otprg::kCtrFree];
+        OT_CK(cudaMemcpyAsync(&hctr_[otprg::kCtrCount + 4], D_.adm_off + n_free, 8, cudaMemcpyDeviceToHost, s),
+              "D2H");
+        OT_CK(cudaStreamSynchronize(s), "admissible count");
+        const int64_t total = hctr_[otprg::kCtrCount + 4];
+        if (total > adm_cap_) {
+          adm_cap_ = std::max<int64_t>(total + total / 4, adm_cap_ * 3 / 2);
+          D_.adm = ensure<int32_t>(bAdm, adm_cap_);
+          D_.adm_cap = adm_cap_;
+        }
+        set_caps(device_flows());
+        stage = 1;
+      } else if (hold == 2) {  // a claim round for the sort
+        const int64_t n = hctr_[otprg::kCtrN];
+        sort(buf(bEk0).as<unsigned long long>(), buf(bEk1).as<unsigned long long>(), buf(bEv0).as<int64_t>(),
+             buf(bEv1).as<int64_t>(), n, std::min(64, end_bit));
+        OT_CK(otprg::ot_dev_resolve(D_, buf(bEk1).as<unsigned long long>(), buf(bEv1).as<int64_t>(), n,
+                                    buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), s),
+              "resolve");
+        OT_CK(otprg::ot_dev_da_clear(D_, s), "DA clear");
+        OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrNew], 0, 8, s), "memset");
+        OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrDone], 0, 8, s), "memset");
+        OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrBig], 0, 8, s), "memset");
+        launches_ += 2;
+        ++sorted_rounds_;
+        stage = 2;
+      } else if (hold == 3) {  // records beyond one block: CUB sort + merge
+        const int64_t n_rec = hctr_[otprg::kCtrRec];
+        auto rk0 = buf(bRk0).as<unsigned long long>();
+        auto rv0 = buf(bRv0).as<int64_t>();
+        sort(rk0, buf(bRk1).as<unsigned long long>(), rv0, buf(bRv1).as<int64_t>(), n_rec, 63);
+        long long* d_nu = reinterpret_cast<long long*>(&D_.ctr[otprg::kCtrNFlows]);
+        size_t tb = 0;
+        OT_CK(otprg::ot_reduce_by_key(nullptr, tb, buf(bRk1).as<unsigned long long>(), rk0, buf(bRv1).as<int64_t>(),
+                                      rv0, d_nu, n_rec, s),
+              "reduce size");
+        temp_need(tb);
+        tb = temp_cap_;
+        OT_CK(otprg::ot_reduce_by_key(buf(bTemp).p, tb, buf(bRk1).as<unsigned long long>(), rk0,
+                                      buf(bRv1).as<int64_t>(), rv0, d_nu, n_rec, s),
+              "reduce");
+        launches_ += 2;
+        stage = 4;
+      } else if (hold == 4) {  // records beyond r_cap: the flows of this phase decide
+        const int64_t nfl = device_flows();
+        set_caps(nfl + hctr_[otprg::kCtrE]);
+        stage = 3;
+      } else {
+        throw OtError{OTPRG_INVARIANT, "OT device phase loop stopped in an unknown state"};
+      }
+      OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrHold], 0, 8, s), "memset");
+    }
+    rounds_total += drain();
+    const int64_t phases = static_cast<int64_t>(free_counts.size());
+    if (phases > phase_cap)
+      throw OtError{OTPRG_INVARIANT, "phase count exceeded the proven bound; solver state is corrupt"};
+    int64_t sum_ni = 0;
+    for (int64_t v : free_counts) sum_ni += v;
+    r_->full_match_termination = (hctr_[otprg::kCtrNi] == 0);
+    if (phases > 0) n_flows_ = hctr_[otprg::kCtrNFlows];
+    r_->phases = phases;
+    r_->sum_ni = sum_ni;
+    if (r_->free_counts && r_->free_cap > 0)
+      std::memcpy(r_->free_counts, free_counts.data(),
+                  static_cast<size_t>(std::min<int64_t>(phases, r_->free_cap)) * 8);
+    st_ = export_state();
+    r_->loop_ms = loop_t.ms();
+    if (std::getenv("OTPRG_OT_PROFILE"))
+      std::fprintf(stderr, "ot loop %.2f ms: %lld phases, %lld DA rounds (%lld sorted), %lld holds (persistent, %lld launches)\n",
+                   r_->loop_ms, (long long)phases, (long long)rounds_total, (long long)sorted_rounds_,
+                   (long long)holds, (long long)relaunches);
+    r_->scan_ms = 0.0;
+    r_->bytes_touched = 0;
+    r_->gpu_launches = launches_;
+    complete();
+  }
+
+  // solve_copy_matching with device-sized phases: one phase is one launch
+  // sequence (admissible lists, claim rounds, updates, record merge, CSR
+  // rebuild, the next phase's free list) and one look at the counters; the
+  // host steps in only when the phase holds (kCtrHold: admissible lists past
+  // their capacity, claim rounds not over after the batch, more records than
+  // one block merges), finishes that step and resumes the sequence there.
+  // Capacities are grown before the phase from host-known bounds (entries <=
+  // admissible + free, records <= flows + entries + 2 n_a).
+  void solve_copy_matching_dev() {
+    upload_initial();
+    const double threshold = eps_in_ * static_cast<double>(sm_.total_s);
+    const int64_t phase_cap =
+        static_cast<int64_t>(std::ceil((1.0 + 2.0 * eps_in_) / (eps_in_ * eps_in_))) + 8;
+    cudaStream_t s = ctx_->stream;
+    int64_t phases = 0, sum_ni = 0, rounds_total = 0, holds = 0;
+    std::vector<int64_t> free_counts;
+    Timer loop_t;
+    int* scratch = ensure<int>(bScratch, 256);
+    const int end_bit = 21 + 1 + static_cast<int>(std::ceil(std::log2(2.0 * n_a_ + 1.0)));
+    if (adm_cap_ < 1) {
+      adm_cap_ = std::max<int64_t>(int64_t(1) << 20, 8 * static_cast<int64_t>(n_b_));
+      D_.adm = ensure<int32_t>(bAdm, adm_cap_);
+    }
+    D_.adm_cap = adm_cap_;
+    auto set_caps = [&](int64_t n_free) {
+      grow(e_cap_, adm_cap_ + n_free + 1, bEk0, bEv0, bEk1, bEv1, false);
+      D_.e_key = buf(bEk0).as<unsigned long long>();
+      D_.e_val = buf(bEv0).as<int64_t>();
+      D_.s_key = buf(bEk1).as<unsigned long long>();
+      D_.s_val = buf(bEv1).as<int64_t>();
+      grow(r_cap_, n_flows_ + e_cap_ + 2 * static_cast<int64_t>(n_a_) + 16, bRk0, bRv0, bRk1, bRv1, false);
+      D_.r_key = buf(bRk0).as<unsigned long long>();
+      D_.r_val = buf(bRv0).as<int64_t>();
+      grow_flows_keep(r_cap_);
+    };
+    auto rk0 = [&] { return buf(bRk0).as<unsigned long long>(); };
+    auto rv0 = [&] { return buf(bRv0).as<int64_t>(); };
+    // stage 0: the phase from its start; 1 from the admissible fill; 2 from
+    // the claim rounds; 3 from the CSR rebuild
+    auto launch_from = [&](int stage) {
+      if (stage <= 0) {
+        OT_CK(otprg::ot_dev_phase_begin(D_, s), "memset");
+        OT_CK(otprg::ot_dev_t(D_, s), "cluster duals");
+        OT_CK(otprg::ot_dev_adm(D_, 0, s), "admissible count");
+        OT_CK(otprg::ot_dev_adm_scan(D_, s), "admissible offsets");
+        launches_ += 3;
+      }
+      if (stage <= 1) {
+        OT_CK(otprg::ot_dev_adm(D_, 1, s), "admissible fill");
+        OT_CK(otprg::ot_dev_cut_init(D_, s), "cut init");
+        launches_ += 2;
+      }
+      if (stage <= 2) {
+        OT_CK(otprg::ot_dev_da_rounds(D_, da_batch_, s), "DA rounds");
+        OT_CK(otprg::ot_dev_da_gate(D_, s), "DA gate");
+        OT_CK(otprg::ot_dev_consumed(D_, D_.e_key, D_.e_val, -1, s), "consumed");
+        OT_CK(otprg::ot_dev_records(D_, D_.e_key, D_.e_val, -1, s), "records");
+        OT_CK(otprg::ot_dev_small_merge(D_, rk0(), rv0(), s), "record merge");
+        launches_ += 5 * da_batch_ + 6;
+      }
+      OT_CK(otprg::ot_dev_rebuild(D_, rk0(), rv0(), -1, s), "rebuild");
+      OT_CK(cudaMemsetAsync(D_.ctr, 0, 8, s), "memset");  // n_i of the next phase
+      OT_CK(otprg::ot_dev_free_list(D_, scratch, s), "free list");
+      launches_ += 4;
+    };
+    auto clear_hold = [&] { OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrHold], 0, 8, s), "memset"); };
+    // the first phase's free list
+    OT_CK(cudaMemsetAsync(D_.ctr, 0, otprg::kCtrCount * 8, s), "memset");
+    OT_CK(otprg::ot_dev_free_list(D_, scratch, s), "free list");
+    launches_ += 2;
+    read_ctr();
+    while (true) {
+      const int64_t n_i = hctr_[otprg::kCtrNi];
+      const int32_t n_free = static_cast<int32_t>(hctr_[otprg::kCtrFree]);
+      if (static_cast<double>(n_i) <= threshold) {
+        r_->full_match_termination = (n_i == 0);
+        break;
+      }
+      set_caps(n_free);
+      scan_bytes_ += 2 * static_cast<int64_t>(n_free) * lda_ * width_;
+      int stage = 0;
+      while (true) {
+        launch_from(stage);
+        read_ctr();
+        const int64_t hold = hctr_[otprg::kCtrHold];
+        if (hold == 0) break;
+        ++holds;
+        if (hold == 1) {  // admissible lists beyond adm_cap: grow, refill
+          int64_t total = 0;
+          OT_CK(cudaMemcpyAsync(&hctr_[otprg::kCtrCount + 4], D_.adm_off + n_free, 8, cudaMemcpyDeviceToHost, s),
+                "D2H");
+          OT_CK(cudaStreamSynchronize(s), "admissible count");
+          total = hctr_[otprg::kCtrCount + 4];
+          adm_cap_ = std::max<int64_t>(total + total / 4, adm_cap_ * 3 / 2);
+          D_.adm = ensure<int32_t>(bAdm, adm_cap_);
+          D_.adm_cap = adm_cap_;
+          set_caps(n_free);
+          stage = 1;
+        } else if (hold == 2) {  // claim rounds not over (or a round for the sort)
+          if (hctr_[otprg::kCtrDone] == 2) {
+            const int64_t n = hctr_[otprg::kCtrN];
+            sort(buf(bEk0).as<unsigned long long>(), buf(bEk1).as<unsigned long long>(), buf(bEv0).as<int64_t>(),
+                 buf(bEv1).as<int64_t>(), n, std::min(64, end_bit));
+            OT_CK(otprg::ot_dev_resolve(D_, buf(bEk1).as<unsigned long long>(), buf(bEv1).as<int64_t>(), n,
+                                        buf(bEk0).as<unsigned long long>(), buf(bEv0).as<int64_t>(), s),
+                  "resolve");
+            OT_CK(otprg::ot_dev_da_clear(D_, s), "DA clear");
+            OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrNew], 0, 8, s), "memset");
+            OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrDone], 0, 8, s), "memset");
+            OT_CK(cudaMemsetAsync(&D_.ctr[otprg::kCtrBig], 0, 8, s), "memset");
+            launches_ += 2;
+            ++sorted_rounds_;
+          }
+          stage = 2;
+        } else if (hold == 3) {  // records beyond one block: CUB sort + merge
+          const int64_t n_rec = hctr_[otprg::kCtrRec];
+          sort(rk0(), buf(bRk1).as<unsigned long long>(), rv0(), buf(bRv1).as<int64_t>(), n_rec, 63);
+          long long* d_nu = reinterpret_cast<long long*>(&D_.ctr[otprg::kCtrNFlows]);
+          size_t tb = 0;
+          OT_CK(otprg::ot_reduce_by_key(nullptr, tb, buf(bRk1).as<unsigned long long>(), rk0(),
+                                        buf(bRv1).as<int64_t>(), rv0(), d_nu, n_rec, s),
+                "reduce size");
+          temp_need(tb);
+          tb = temp_cap_;
+          OT_CK(otprg::ot_reduce_by_key(buf(bTemp).p, tb, buf(bRk1).as<unsigned long long>(), rk0(),
+                                        buf(bRv1).as<int64_t>(), rv0(), d_nu, n_rec, s),
+                "reduce");
+          launches_ += 2;
+          stage = 3;
+        } else {
+          throw OtError{OTPRG_INVARIANT, "OT device phase stopped in an unknown state"};
+        }
+        clear_hold();
+      }
+      n_flows_ = hctr_[otprg::kCtrNFlows];
+      rounds_total += hctr_[otprg::kCtrRounds];
+      phases += 1;
+      free_counts.push_back(n_i);
+      sum_ni += n_i;
+      if (phases > phase_cap)
+        throw OtError{OTPRG_INVARIANT, "phase count exceeded the proven bound; solver state is corrupt"};
+    }
+    r_->phases = phases;
+    r_->sum_ni = sum_ni;
+    if (r_->free_counts && r_->free_cap > 0)
+      std::memcpy(r_->free_counts, free_counts.data(),
+                  static_cast<size_t>(std::min<int64_t>(phases, r_->free_cap)) * 8);
+    st_ = export_state();
+    r_->loop_ms = loop_t.ms();
+    if (std::getenv("OTPRG_OT_PROFILE"))
+      std::fprintf(stderr, "ot loop %.2f ms: %lld phases, %lld DA rounds (%lld sorted), %lld holds (device-sized)\n",
+                   r_->loop_ms, (long long)phases, (long long)rounds_total, (long long)sorted_rounds_,
+                   (long long)holds);
+    r_->scan_ms = 0.0;
+    r_->bytes_touched = scan_bytes_;
+    r_->gpu_launches = launches_;
+    complete();
+  }
+
   // solve_copy_matching (ot.cpp:418-637): the phases on the device.
   void solve_copy_matching() {
+    if (!debug() && da_batch_ > 0 && !std::getenv("OTPRG_OT_HOST_SIZED")) {
+      if (std::getenv("OTPRG_OT_SEQ")) solve_copy_matching_dev();
+      else solve_copy_matching_persistent();
+      return;
+    }
     upload_initial();
     const double threshold = eps_in_ * static_cast<double>(sm_.total_s);
     const int64_t phase_cap =

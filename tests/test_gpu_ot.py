@@ -102,13 +102,21 @@ def _same_as_reference(reference, mu, nu, cost, eps):
     assert np.array_equal(plan.mass, r["mass"]) and float(plan.cost).hex() == float(r["cost"]).hex()
 
 
-@pytest.mark.parametrize("batch", ["0", "1", "4"])
+@pytest.mark.parametrize("batch", ["0", "1", "4", "seq", "host"])
 def test_da_round_paths_on_degenerate_costs(reference, monkeypatch, batch):
-    """The claim rounds with host-sized sorts (batch 0) and device-sized
-    segments (ot_dev_da_rounds): constant and two-level costs send every free
-    b to the same cluster (segments past kDaWarpMax take the sorted round),
-    few-level costs give runs of re-proposals; plans equal the reference's."""
-    monkeypatch.setenv("OTPRG_OT_DA_BATCH", batch)
+    """The phase loop forms: host-sized phases with sorted claim rounds (batch
+    0), host-sized phases with device-sized rounds ("host"), the device-sized
+    phase as a launch sequence ("seq", 4 rounds per look) and the persistent
+    phase loop (the default; batch 1 / 4).  Constant and two-level costs send
+    every free b to the same cluster (segments past kDaWarpMax take the
+    sorted round), few-level costs give runs of re-proposals; plans equal the
+    reference's."""
+    if batch == "seq":
+        monkeypatch.setenv("OTPRG_OT_SEQ", "1")
+    elif batch == "host":
+        monkeypatch.setenv("OTPRG_OT_HOST_SIZED", "1")
+    else:
+        monkeypatch.setenv("OTPRG_OT_DA_BATCH", batch)
     rng = np.random.default_rng(7)
     for n_a, n_b, levels in ((40, 900, 1), (600, 600, 2), (300, 700, 5), (257, 1000, 3)):
         mu = rng.integers(1, 50, n_a).astype(np.float64)
@@ -117,3 +125,31 @@ def test_da_round_paths_on_degenerate_costs(reference, monkeypatch, batch):
         nu /= nu.sum()
         cost = rng.integers(0, levels, (n_a, n_b)) / max(1, levels - 1) if levels > 1 else np.full((n_a, n_b), 0.5)
         _same_as_reference(reference, mu, nu, cost, 0.05)
+
+
+def test_persistent_loop_holds(pins):
+    """The persistent phase loop with tiny buffers (OTPRG_OT_SMALL_CAPS, in a
+    fresh process so every buffer starts small): every phase stops for the
+    host at least once (admissible lists past adm_cap, records past r_cap,
+    the free-count buffer full every 3 phases) and resumes at the held step,
+    growing the buffers with the live device state; plans equal the
+    reference's."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, json; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "import paper_2203_03732_b200 as otprg\n"
+        "from test_gpu_ot import _pins\n"
+        "out = {}\n"
+        "for n in (1000, 5000):\n"
+        "    plan, st = otprg.solve_ot(otprg.gen_random_ot_rational(n, n, 1), 0.01)\n"
+        "    out[n] = _pins(plan, st)\n"
+        "print(json.dumps(out))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OTPRG_OT_SMALL_CAPS="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    for n, key in (("1000", "ot_rational_1000x1000_s1_eps0.01"), ("5000", "ot_rational_5000x5000_s1_eps0.01")):
+        bad = {k: (got[n][k], pins[key][k]) for k in KEYS if got[n][k] != pins[key][k]}
+        assert not bad, f"{key}: {bad}"
