@@ -113,7 +113,7 @@ def config4():
     ref = None
     for storage in ("u8", "u16"):
         sv = otprg.Solver(0)
-        ms, (m1, s1) = wall(lambda: sv.solve(inst, otprg.AssignmentOptions(eps=0.01, storage=storage)), 2)
+        ms, (m1, s1) = wall(lambda: sv.solve(inst, otprg.AssignmentOptions(eps=0.01, storage=storage)), 3)
         if ref is None:
             ref = (m1, s1)
         out[f"single_gpu_fused_{storage}"] = {"e2e_ms": round(ms, 2), "build_ms": round(s1.device["build_ms"], 2),
