@@ -253,6 +253,10 @@ struct OtDev {
   unsigned* bar;       // [2] persistent loop: grid barrier count, count at the last exit
   int64_t* loop;       // [4] persistent loop: phases this launch, claim rounds
   int64_t* fcounts;    // [fc_cap] persistent loop: n_i of the phases of this launch
+  int64_t* rec_off;    // [n_a + 1] persistent loop: merged records per demand vertex, scanned
+  int small_rec;       // persistent loop: records merged by one block up to this many (else buckets)
+  unsigned long long* r_key2;  // [r_cap] records scratch (the bucket merge; the host sort's output)
+  int64_t* r_val2;
   int64_t fc_cap;
   // DA entries (key = code << 32 | i) and next-state records
   unsigned long long* e_key;

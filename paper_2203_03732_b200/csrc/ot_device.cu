@@ -796,6 +796,159 @@ __global__ void __launch_bounds__(1024) ot_small_merge_kernel(OtDev D, unsigned 
                                                              int64_t* __restrict__ val) { ot_small_merge_body(D, key, val, blockIdx.x, gridDim.x); }
 
 
+
+// ---- record merge beyond one block: buckets per demand vertex ------------------
+// (persistent loop, n_rec > kOtSmallRec) records counted per vertex a (da_cnt,
+// zero outside the claim rounds), bucket offsets by one block (da_off), the
+// records scattered into their buckets (r_key2 / r_val2, da_fill), then a warp
+// per vertex ranks its bucket (keys within one a differ in (y, b)), merges
+// equal keys into the first of them and writes the unique records sorted at
+// the bucket start, the unique counts scanned again, and the buckets copied
+// compactly to key / val: the CUB sort + reduce-by-key result.  A bucket of
+// more than kOtBucketMax records holds (3) for the host sort.
+constexpr int kOtBucketMax = 1024;
+
+__device__ __forceinline__ int ot_rec_a(unsigned long long k) { return (int)(k >> 42); }
+
+__device__ __forceinline__ void ot_bucket_count_body(OtDev& D, const unsigned long long* key, int bid, int nb) {
+  const long long n = D.ctr[kCtrRec];
+  for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x)
+    atomicAdd(&D.da_cnt[ot_rec_a(key[j])], 1);
+}
+
+// one block: da_off[a] = exclusive prefix of cnt[0, n_a); a bucket past the
+// cap sets the hold
+__device__ __forceinline__ void ot_bucket_scan_body(OtDev& D, const int32_t* cnt, int64_t* off, int64_t* total) {
+  const int n = D.n_a;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  int64_t sum = 0;
+  bool big = false;
+  for (int i = lo; i < hi; ++i) {
+    sum += cnt[i];
+    big |= cnt[i] > kOtBucketMax;
+  }
+  __shared__ int64_t s_p[1024];
+  s_p[threadIdx.x] = sum;
+  if (big) D.ctr[kCtrHold] = 3;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int64_t y = (int)threadIdx.x >= o ? s_p[threadIdx.x - o] : 0;
+    __syncthreads();
+    s_p[threadIdx.x] += y;
+    __syncthreads();
+  }
+  int64_t run = s_p[threadIdx.x] - sum;
+  for (int i = lo; i < hi; ++i) {
+    off[i] = run;
+    run += cnt[i];
+  }
+  if (threadIdx.x == blockDim.x - 1 && total) *total = s_p[threadIdx.x];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void ot_bucket_scatter_body(OtDev& D, const unsigned long long* key, const int64_t* val,
+                                                       int bid, int nb) {
+  const long long n = D.ctr[kCtrRec];
+  for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x) {
+    const unsigned long long k = key[j];
+    const int a = ot_rec_a(k);
+    const long long pos = D.da_off[a] + atomicAdd(&D.da_fill[a], 1);
+    D.r_key2[pos] = k;
+    D.r_val2[pos] = val[j];
+  }
+}
+
+// warp per vertex: unique keys sorted at the bucket start, da_cnt[a] = their
+// count.  Lane-held chunks of the bucket: pass 1 gives every entry its run's
+// sum and whether it is the first of its run; pass 2 counts the first entries
+// with smaller keys (the entry's slot among the unique keys); the first
+// entries then write their run in place (every read is done by then).
+__device__ __forceinline__ void ot_bucket_merge_body(OtDev& D, int bid, int nb) {
+  constexpr int kCh = kOtBucketMax / 32;
+  const int lane = threadIdx.x & 31;
+  const int warps = nb * (blockDim.x >> 5);
+  for (int a = bid * (blockDim.x >> 5) + (threadIdx.x >> 5); a < D.n_a; a += warps) {
+    const int c = D.da_cnt[a];
+    if (c == 0) continue;
+    const long long o = D.da_off[a];
+    unsigned long long* k = D.r_key2 + o;
+    int64_t* v = D.r_val2 + o;
+    const int chunks = (c + 31) >> 5;
+    unsigned long long hk[kCh];
+    int64_t hs[kCh];
+    bool first[kCh];
+    int rank[kCh];
+#pragma unroll 1
+    for (int q = 0; q < chunks; ++q) {
+      const int e = q * 32 + lane;
+      const unsigned long long ke = e < c ? k[e] : ~0ull;
+      int64_t sum = 0;
+      bool f = e < c;
+#pragma unroll 1
+      for (int b1 = 0; b1 < c; b1 += 32) {
+        const int e2 = b1 + lane;
+        const unsigned long long k2 = e2 < c ? k[e2] : ~0ull;
+        const int64_t v2 = e2 < c ? v[e2] : 0;
+        const int m = min(32, c - b1);
+        for (int t = 0; t < m; ++t) {
+          const unsigned long long kt = __shfl_sync(kFull, k2, t);
+          const int64_t vt = __shfl_sync(kFull, v2, t);
+          if (kt == ke) {
+            sum += vt;
+            if (b1 + t < e) f = false;
+          }
+        }
+      }
+      hk[q] = ke;
+      hs[q] = sum;
+      first[q] = f;
+      rank[q] = 0;
+    }
+#pragma unroll 1
+    for (int q2 = 0; q2 < chunks; ++q2) {
+      const unsigned long long kq = hk[q2];
+      const int fq = first[q2] ? 1 : 0;
+      const int m = min(32, c - q2 * 32);
+      for (int t = 0; t < m; ++t) {
+        const unsigned long long kt = __shfl_sync(kFull, kq, t);
+        if (__shfl_sync(kFull, fq, t))
+          for (int q = 0; q < chunks; ++q) rank[q] += kt < hk[q];
+      }
+    }
+    int uniq = 0;
+    for (int q = 0; q < chunks; ++q) uniq += __popc(__ballot_sync(kFull, first[q]));
+    __syncwarp();
+    for (int q = 0; q < chunks; ++q)
+      if (first[q]) {
+        k[rank[q]] = hk[q];
+        v[rank[q]] = hs[q];
+      }
+    if (lane == 0) D.da_cnt[a] = uniq;
+  }
+}
+
+// the unique runs of every bucket to key / val, compact and in vertex order
+// (rec_off: the scan of the unique counts); the bucket counters back to zero
+__device__ __forceinline__ void ot_bucket_copy_body(OtDev& D, unsigned long long* key, int64_t* val, int bid,
+                                                    int nb) {
+  const int lane = threadIdx.x & 31;
+  const int warps = nb * (blockDim.x >> 5);
+  for (int a = bid * (blockDim.x >> 5) + (threadIdx.x >> 5); a < D.n_a; a += warps) {
+    const int u = D.da_cnt[a];
+    const long long src = D.da_off[a], dst = D.rec_off[a];
+    for (int j = lane; j < u; j += 32) {
+      key[dst + j] = D.r_key2[src + j];
+      val[dst + j] = D.r_val2[src + j];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      D.da_cnt[a] = 0;
+      D.da_fill[a] = 0;
+    }
+  }
+}
+
 // ---- the persistent phase loop (one cooperative launch) --------------------------
 __device__ __forceinline__ void ot_grid_bar(OtDev& D, unsigned& target, int nb) {
   if (nb == 1) {  // one block: the block barrier is the grid barrier
@@ -892,11 +1045,31 @@ __global__ void __launch_bounds__(1024, 1) ot_phase_loop_kernel(OtDev D, int sta
       ot_flow_records_body<T>(D, bid, nb);
       ot_grid_bar(D, target, nb);
       ot_supply_body(D, bid, nb);
-      if (bid == 0) {
-        __syncthreads();  // (block 0's supply threads done; the merge needs the whole block)
-        ot_small_merge_body(D, D.r_key, D.r_val, bid, 1);
+      if (ot_vol(ctr + kCtrRec) <= min(D.small_rec, kOtSmallRec)) {  // one block: bitonic sort + merge
+        if (bid == 0) {
+          __syncthreads();  // (block 0's supply threads done; the merge needs the whole block)
+          ot_small_merge_body(D, D.r_key, D.r_val, bid, 1);
+        }
+        ot_grid_bar(D, target, nb);
+      } else {  // buckets per demand vertex (the r_key2 / r_val2 scratch, da_cnt / da_fill / da_off)
+        ot_bucket_count_body(D, D.r_key, bid, nb);
+        ot_grid_bar(D, target, nb);
+        if (bid == 0) ot_bucket_scan_body(D, D.da_cnt, D.da_off, nullptr);
+        ot_grid_bar(D, target, nb);
+        if (ot_vol(ctr + kCtrHold) != 0) {  // a bucket past the cap: counters back to zero, host sort
+          for (int a = bid * blockDim.x + threadIdx.x; a < D.n_a; a += nb * blockDim.x) D.da_cnt[a] = 0;
+          ot_grid_bar(D, target, nb);
+          break;
+        }
+        ot_bucket_scatter_body(D, D.r_key, D.r_val, bid, nb);
+        ot_grid_bar(D, target, nb);
+        ot_bucket_merge_body(D, bid, nb);
+        ot_grid_bar(D, target, nb);
+        if (bid == 0) ot_bucket_scan_body(D, D.da_cnt, D.rec_off, ctr + kCtrNFlows);
+        ot_grid_bar(D, target, nb);
+        ot_bucket_copy_body(D, D.r_key, D.r_val, bid, nb);
+        ot_grid_bar(D, target, nb);
       }
-      ot_grid_bar(D, target, nb);
       if (ot_vol(ctr + kCtrHold) != 0) break;  // 3: more records than one block merges
     }
     ot_slot_body(D, D.r_key, -1, bid, nb);

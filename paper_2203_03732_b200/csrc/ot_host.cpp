@@ -470,7 +470,7 @@ class OtSolver {
   enum Buf {
     bT, bDy, bDfree, bDmatched, bConsumed, bFlOff, bFlCode, bFlB, bFlCnt, bFlPre, bSy, bSfree, bSmatched,
     bSfreed, bFb, bFy, bFpos, bFidx, bFu0, bFu, bAdmLen, bAdmOff, bAdm, bEk0, bEv0, bEk1, bEv1, bRk0, bRv0,
-    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bDaCnt, bDaFill, bDaOff, bDaTouch, bBar, bLoop, bFcounts, bNum
+    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bDaCnt, bDaFill, bDaOff, bDaTouch, bBar, bLoop, bFcounts, bRecOff, bNum
   };
   otprg::OtDev D_{};
   int64_t fl_cap_ = 0, adm_cap_ = 0, e_cap_ = 0, r_cap_ = 0;
@@ -790,6 +790,9 @@ class OtSolver {
     D_.loop = ensure<int64_t>(bLoop, 4);
     D_.fc_cap = small_caps ? 3 : std::min<int64_t>(phase_cap + 2, int64_t(1) << 20);
     D_.fcounts = ensure<int64_t>(bFcounts, D_.fc_cap);
+    D_.rec_off = ensure<int64_t>(bRecOff, static_cast<size_t>(n_a_) + 1);
+    // (test knob: every record merge through the per-vertex buckets)
+    D_.small_rec = std::getenv("OTPRG_OT_BUCKETS") ? 0 : otprg::kOtSmallRec;
     OT_CK(cudaMemsetAsync(D_.bar, 0, 2 * sizeof(unsigned), s), "memset");
     OT_CK(cudaMemsetAsync(D_.loop, 0, 4 * sizeof(int64_t), s), "memset");
     if (adm_cap_ < 1 || small_caps) {
@@ -813,6 +816,8 @@ class OtSolver {
         grow(r_cap_, r, bRk0, bRv0, bRk1, bRv1, false);
         D_.r_key = buf(bRk0).as<unsigned long long>();
         D_.r_val = buf(bRv0).as<int64_t>();
+        D_.r_key2 = buf(bRk1).as<unsigned long long>();
+        D_.r_val2 = buf(bRv1).as<int64_t>();
         D_.r_cap = std::max<int64_t>(r, std::min<int64_t>(r_cap_, r));
         grow_flows_keep(r_cap_);
         return;
@@ -826,6 +831,8 @@ class OtSolver {
       grow(r_cap_, 2 * n_flows + e_cap_ + 2 * static_cast<int64_t>(n_a_) + 16, bRk0, bRv0, bRk1, bRv1, false);
       D_.r_key = buf(bRk0).as<unsigned long long>();
       D_.r_val = buf(bRv0).as<int64_t>();
+      D_.r_key2 = buf(bRk1).as<unsigned long long>();
+      D_.r_val2 = buf(bRv1).as<int64_t>();
       D_.r_cap = r_cap_;
       grow_flows_keep(r_cap_);
     };

@@ -132,7 +132,8 @@ def test_persistent_loop_holds(pins):
     fresh process so every buffer starts small): every phase stops for the
     host at least once (admissible lists past adm_cap, records past r_cap,
     the free-count buffer full every 3 phases) and resumes at the held step,
-    growing the buffers with the live device state; plans equal the
+    growing the buffers with the live device state; every record merge goes
+    through the per-vertex buckets (OTPRG_OT_BUCKETS); plans equal the
     reference's."""
     import subprocess
     import sys
@@ -146,7 +147,7 @@ def test_persistent_loop_holds(pins):
         "    out[n] = _pins(plan, st)\n"
         "print(json.dumps(out))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, OTPRG_OT_SMALL_CAPS="1")
+    env = dict(os.environ, OTPRG_OT_SMALL_CAPS="1", OTPRG_OT_BUCKETS="1")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     got = json.loads(r.stdout.strip().splitlines()[-1])
