@@ -867,7 +867,16 @@ class OtSolver {
     int stage = 0;
     int64_t rounds_total = 0;
     while (true) {
-      OT_CK(otprg::ot_dev_phase_loop(D_, stage, threshold, scratch, s), "OT phase loop launch");
+      const cudaError_t le = otprg::ot_dev_phase_loop(D_, stage, threshold, scratch, s);
+      if (le != cudaSuccess && relaunches == 0 &&
+          (le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorLaunchOutOfResources)) {
+        // the loop's blocks are not co-resident here (e.g. other work holds the
+        // SMs): nothing has changed yet, run the launch-sequence form instead
+        cudaGetLastError();
+        solve_copy_matching_dev();
+        return;
+      }
+      OT_CK(le, "OT phase loop launch");
       ++relaunches;
       launches_ += 1;
       read_ctr();
