@@ -112,11 +112,6 @@ __global__ void round_points_div_kernel(const double2* __restrict__ pa,
 // float copies in registers) and walks a strided set of supply rows, storing
 // one 16-byte vector per row: the build is bound by issue and HBM writes.
 constexpr int kThrSmemMax = 8192;
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float r;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
 template <typename T>
 struct K2Shape {
   // entries per thread (16 for u8 / u16, 8 for u32: one or two 16-byte

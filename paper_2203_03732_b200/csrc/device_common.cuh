@@ -126,6 +126,12 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned target,
   __syncthreads();
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // ---- mbarrier + 1-D TMA bulk copies (cp.async.bulk) -----------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
