@@ -23,9 +23,18 @@ while time.time() < t_end:
     seed = seed0 * 1_000_003 + case
     rng = np.random.default_rng(seed)
     kind = "ot" if rng.random() < 0.6 else "copy"
-    n_a, n_b = int(rng.integers(1, 120)), int(rng.integers(1, 120))
-    eps = float(np.exp(rng.uniform(np.log(0.02), np.log(0.6))))
-    cost = rng.random((n_a, n_b))
+    big = rng.random() < 0.25  # (multi-block persistent loop, bucket merges)
+    n_a, n_b = (int(rng.integers(100, 1500)), int(rng.integers(100, 1500))) if big else \
+        (int(rng.integers(1, 120)), int(rng.integers(1, 120)))
+    eps = float(np.exp(rng.uniform(np.log(0.02 if not big else 0.05), np.log(0.6))))
+    fam = rng.random()
+    if fam < 0.7:
+        cost = rng.random((n_a, n_b))
+    elif fam < 0.9:  # few levels: ties and runs of re-proposals in the claim rounds
+        lv = int(rng.integers(2, 6))
+        cost = rng.integers(0, lv, (n_a, n_b)) / (lv - 1)
+    else:  # constant: every free b at the same cluster
+        cost = np.full((n_a, n_b), float(rng.random()))
     if kind == "ot":
         w_a = rng.integers(0, 50, n_a).astype(np.float64)
         w_b = rng.integers(0, 50, n_b).astype(np.float64)
@@ -53,8 +62,9 @@ while time.time() < t_end:
             tot += c
         s = np.array(s, np.int64)
         want = ref.solve_copy_matching(k, eps, uf, uc, d, s, eps, check=True, phase_cap=1)
+        chk = bool(rng.random() < 0.5)  # (without the checks: the persistent phase loop)
         res = otprg.solve_copy_matching(otprg.CopyInstance(otprg.ScaledCosts(eps, k, uf, uc), d, s), eps,
-                                        otprg.ClusterOptions(check_invariants=True))
+                                        otprg.ClusterOptions(check_invariants=chk))
         ok = (np.array_equal(res.flow, want["flow"]) and res.stats.phases == want["phases"]
               and np.array_equal(res.stats.free_counts, want["free_counts"]))
         tag = f"copy {n_a}x{n_b} eps={eps:.3g} copies {int(d.sum())}/{int(s.sum())}"
