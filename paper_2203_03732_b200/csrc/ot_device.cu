@@ -36,6 +36,7 @@
 // 5 with a code in err[0]: 1 third demand dual, 2 third supply dual, 3
 // displaced copy without a supply cluster, 4 storage bound exceeded.
 #include <climits>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "device_common.cuh"
@@ -1175,7 +1176,16 @@ cudaError_t ot_dev_phase_loop(OtDev& D, int stage, double threshold, int* scratc
     // are barrier-bound: fewer blocks, cheaper barriers; one block needs none)
     const int grid = std::max(1, std::min(std::min(sms, kListBlocks), D.n_b / 64));
     void* args[] = {&D, &stage, &threshold, &scratch};
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(1024), args, smem, s);
+    // threads per block: 1024 for few blocks (the one-block merges dominate),
+    // 512 from 32 blocks on (scripts/ab_ot_threads.sh: n = 5k / 20k -15 / -7 %,
+    // n = 1k +4 %); OTPRG_OT_THREADS overrides (A/B)
+    static const int forced = [] {
+      const char* v = std::getenv("OTPRG_OT_THREADS");
+      const int t = v ? std::atoi(v) : 0;
+      return t >= 128 && t <= 1024 && t % 32 == 0 ? t : 0;
+    }();
+    const int threads = forced ? forced : (grid >= 32 ? 512 : 1024);
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(threads), args, smem, s);
     return 0;
   });
   if (e != cudaSuccess) return e;
