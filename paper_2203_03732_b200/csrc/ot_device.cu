@@ -98,7 +98,9 @@ __device__ __forceinline__ void ot_free_count_body(OtDev& D, int* counts, int bi
     if (s_t) atomicAdd(reinterpret_cast<unsigned long long*>(&D.ctr[kCtrNi]), s_t);
   }
 }
-__global__ void __launch_bounds__(1024) ot_free_count_kernel(OtDev D, int* counts) { ot_free_count_body(D, counts, blockIdx.x, gridDim.x); }
+__global__ void __launch_bounds__(1024) ot_free_count_kernel(OtDev D, int* counts) {
+  ot_free_count_body(D, counts, blockIdx.x, gridDim.x);
+}
 
 __device__ __forceinline__ void ot_free_write_body(OtDev& D, const int* counts, int bid, int nb) {
   if (ot_hold(D)) return;
@@ -142,7 +144,9 @@ __device__ __forceinline__ void ot_free_write_body(OtDev& D, const int* counts, 
     __syncthreads();
   }
 }
-__global__ void __launch_bounds__(1024) ot_free_write_kernel(OtDev D, const int* counts) { ot_free_write_body(D, counts, blockIdx.x, gridDim.x); }
+__global__ void __launch_bounds__(1024) ot_free_write_kernel(OtDev D, const int* counts) {
+  ot_free_write_body(D, counts, blockIdx.x, gridDim.x);
+}
 
 // t_ci(a) = -y of cluster (a, ci), type max when absent (never admissible).
 template <typename T>
@@ -474,7 +478,9 @@ __device__ __forceinline__ void ot_consumed_body(OtDev& D, const unsigned long l
     atomicAdd(reinterpret_cast<unsigned long long*>(&D.consumed[key[j] >> 21]), (unsigned long long)val[j]);
 }
 __global__ void ot_consumed_kernel(OtDev D, const unsigned long long* __restrict__ key,
-                                   const int64_t* __restrict__ val, long long n) { ot_consumed_body(D, key, val, n, blockIdx.x, gridDim.x); }
+                                   const int64_t* __restrict__ val, long long n) {
+  ot_consumed_body(D, key, val, n, blockIdx.x, gridDim.x);
+}
 
 // Records of the next state, key (a, descending y, b), b = kFreeB for free
 // demand copies: surviving flow entries (the displaced prefix removed, its
@@ -538,7 +544,9 @@ __device__ __forceinline__ void ot_claim_records_body(OtDev& D, const unsigned l
   }
 }
 __global__ void ot_claim_records_kernel(OtDev D, const unsigned long long* __restrict__ key,
-                                        const int64_t* __restrict__ val, long long n) { ot_claim_records_body(D, key, val, n, blockIdx.x, gridDim.x); }
+                                        const int64_t* __restrict__ val, long long n) {
+  ot_claim_records_body(D, key, val, n, blockIdx.x, gridDim.x);
+}
 
 // Supply side (ot.cpp:540-553, 580-588): a free b's copies placed this phase
 // join its free cluster's matched copies, the rest go up a unit; displaced
@@ -627,7 +635,8 @@ __global__ void ot_supply_kernel(OtDev D) { ot_supply_body(D, blockIdx.x, gridDi
 // After the records are sorted and merged (unique keys, summed counts): the
 // record's demand slot (0 for the vertex's first dual, 1 for the second; a
 // third is the reference's "third dual value" violation) and its code.
-__device__ __forceinline__ void ot_slot_body(OtDev& D, const unsigned long long* __restrict__ key, long long n, int bid, int nb) {
+__device__ __forceinline__ void ot_slot_body(OtDev& D, const unsigned long long* __restrict__ key, long long n,
+                                             int bid, int nb) {
   if (ot_hold(D)) return;
   if (n < 0) n = D.ctr[kCtrNFlows];
   for (long long j = bid * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)nb * blockDim.x) {
@@ -656,7 +665,9 @@ __device__ __forceinline__ void ot_slot_body(OtDev& D, const unsigned long long*
     D.fl_code[j] = (int)(2 * a) + min(slot, 1);
   }
 }
-__global__ void ot_slot_kernel(OtDev D, const unsigned long long* __restrict__ key, long long n) { ot_slot_body(D, key, n, blockIdx.x, gridDim.x); }
+__global__ void ot_slot_kernel(OtDev D, const unsigned long long* __restrict__ key, long long n) {
+  ot_slot_body(D, key, n, blockIdx.x, gridDim.x);
+}
 
 // New CSR: fl_off[c] = first record of code c (lower bound), cluster fields
 // from the code's segment, the flow prefix sums for the next displacement.
@@ -693,7 +704,9 @@ __device__ __forceinline__ void ot_rebuild_body(OtDev& D, const unsigned long lo
   }
 }
 __global__ void ot_rebuild_kernel(OtDev D, const unsigned long long* __restrict__ key,
-                                  const int64_t* __restrict__ val, long long n) { ot_rebuild_body(D, key, val, n, blockIdx.x, gridDim.x); }
+                                  const int64_t* __restrict__ val, long long n) {
+  ot_rebuild_body(D, key, val, n, blockIdx.x, gridDim.x);
+}
 
 // ---- device-sized phase helpers ----------------------------------------------
 // adm_off = exclusive prefix of adm_len[0, nf), adm_off[nf] = total: one
@@ -794,7 +807,9 @@ __device__ __forceinline__ void ot_small_merge_body(OtDev& D, unsigned long long
   if (threadIdx.x == blockDim.x - 1) D.ctr[kCtrNFlows] = s_heads[threadIdx.x];
 }
 __global__ void __launch_bounds__(1024) ot_small_merge_kernel(OtDev D, unsigned long long* __restrict__ key,
-                                                             int64_t* __restrict__ val) { ot_small_merge_body(D, key, val, blockIdx.x, gridDim.x); }
+                                                             int64_t* __restrict__ val) {
+  ot_small_merge_body(D, key, val, blockIdx.x, gridDim.x);
+}
 
 
 

@@ -958,7 +958,8 @@ class OtSolver {
     st_ = export_state();
     r_->loop_ms = loop_t.ms();
     if (std::getenv("OTPRG_OT_PROFILE"))
-      std::fprintf(stderr, "ot loop %.2f ms: %lld phases, %lld DA rounds (%lld sorted), %lld holds (persistent, %lld launches)\n",
+      std::fprintf(stderr,
+                   "ot loop %.2f ms: %lld phases, %lld DA rounds (%lld sorted), %lld holds (persistent, %lld launches)\n",
                    r_->loop_ms, (long long)phases, (long long)rounds_total, (long long)sorted_rounds_,
                    (long long)holds, (long long)relaunches);
     r_->scan_ms = 0.0;
