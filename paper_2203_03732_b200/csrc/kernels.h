@@ -252,6 +252,7 @@ struct OtDev {
   int64_t e_cap, r_cap;  // DA entries / records the buffers hold (the persistent loop checks them)
   unsigned* bar;       // [2] persistent loop: grid barrier count, count at the last exit
   int64_t* loop;       // [4] persistent loop: phases this launch, claim rounds
+  unsigned long long* steptime;  // [32] persistent loop timeline (OTPRG_OT_STEPTIME) or nullptr
   int64_t* fcounts;    // [fc_cap] persistent loop: n_i of the phases of this launch
   int64_t* rec_off;    // [n_a + 1] persistent loop: merged records per demand vertex, scanned
   int small_rec;       // persistent loop: records merged by one block up to this many (else buckets)

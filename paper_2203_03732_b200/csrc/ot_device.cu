@@ -996,6 +996,18 @@ __global__ void __launch_bounds__(1024, 1) ot_phase_loop_kernel(OtDev D, int sta
   const bool lead = bid == 0 && threadIdx.x == 0;
   unsigned target = *(volatile unsigned*)(D.bar + 1);
   int64_t* ctr = D.ctr;
+  // (optional per-step timeline: block 0's time from the previous barrier to
+  // the end of barrier k, summed over the launch into D.steptime[k])
+  unsigned long long t_prev = (D.steptime && lead) ? globaltimer() : 0ull;
+#define OT_BAR(k)                                                   \
+  do {                                                              \
+    ot_grid_bar(D, target, nb);                                     \
+    if (D.steptime && lead) {                                       \
+      const unsigned long long now_ = globaltimer();                \
+      D.steptime[k] += now_ - t_prev;                               \
+      t_prev = now_;                                                \
+    }                                                               \
+  } while (0)
   while (true) {
     if (stage <= 0) {
       const int64_t n_i = ot_vol(ctr + kCtrNi);
@@ -1007,13 +1019,13 @@ __global__ void __launch_bounds__(1024, 1) ot_phase_loop_kernel(OtDev D, int sta
         for (int k = 2; k < kCtrCount; ++k) ctr[k] = 0;
         D.fcounts[D.loop[0]] = n_i;
       }
-      ot_grid_bar(D, target, nb);
+      OT_BAR(1);
       ot_t_body<T>(D, bid, nb);
-      ot_grid_bar(D, target, nb);
+      OT_BAR(2);
       ot_adm_body<T, 0>(D, bid, nb);
-      ot_grid_bar(D, target, nb);
+      OT_BAR(3);
       if (bid == 0) ot_adm_scan_body(D, bid, 1);
-      ot_grid_bar(D, target, nb);
+      OT_BAR(4);
     }
     if (stage <= 1) {
       const int nf = (int)ot_vol(ctr + kCtrFree);
@@ -1024,26 +1036,26 @@ __global__ void __launch_bounds__(1024, 1) ot_phase_loop_kernel(OtDev D, int sta
       }
       ot_adm_body<T, 1>(D, bid, nb);
       ot_cut_init_body(D, bid, nb);
-      ot_grid_bar(D, target, nb);
+      OT_BAR(5);
     }
     if (stage <= 2) {
       bool big = false;
       while (true) {
         ot_da_propose_batched_body(D, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(6);
         ot_da_count_body(D, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(7);
         if (ot_vol(ctr + kCtrDone) != 0) break;
         ot_da_alloc_body(D, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(8);
         ot_da_scatter_body(D, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(9);
         if (ot_vol(ctr + kCtrDone) == 2) {
           big = true;
           break;
         }
         ot_da_resolve_warp_body(D, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(10);
       }
       if (big) {  // a cluster past the warp resolve: that round sorted on the host
         if (lead) ctr[kCtrHold] = 2;
@@ -1057,52 +1069,53 @@ __global__ void __launch_bounds__(1024, 1) ot_phase_loop_kernel(OtDev D, int sta
       }
       ot_consumed_body(D, D.e_key, D.e_val, -1, bid, nb);
       ot_claim_records_body(D, D.e_key, D.e_val, -1, bid, nb);
-      ot_grid_bar(D, target, nb);
+      OT_BAR(11);
       ot_flow_records_body<T>(D, bid, nb);
-      ot_grid_bar(D, target, nb);
+      OT_BAR(12);
       ot_supply_body(D, bid, nb);
       if (ot_vol(ctr + kCtrRec) <= min(D.small_rec, kOtSmallRec)) {  // one block: bitonic sort + merge
         if (bid == 0) {
           __syncthreads();  // (block 0's supply threads done; the merge needs the whole block)
           ot_small_merge_body(D, D.r_key, D.r_val, bid, 1);
         }
-        ot_grid_bar(D, target, nb);
+        OT_BAR(13);
       } else {  // buckets per demand vertex (the r_key2 / r_val2 scratch, da_cnt / da_fill / da_off)
         ot_bucket_count_body(D, D.r_key, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(14);
         if (bid == 0) ot_bucket_scan_body(D, D.da_cnt, D.da_off, nullptr);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(15);
         if (ot_vol(ctr + kCtrHold) != 0) {  // a bucket past the cap: counters back to zero, host sort
           for (int a = bid * blockDim.x + threadIdx.x; a < D.n_a; a += nb * blockDim.x) D.da_cnt[a] = 0;
-          ot_grid_bar(D, target, nb);
+          OT_BAR(16);
           break;
         }
         ot_bucket_scatter_body(D, D.r_key, D.r_val, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(17);
         ot_bucket_merge_body(D, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(18);
         if (bid == 0) ot_bucket_scan_body(D, D.da_cnt, D.rec_off, ctr + kCtrNFlows);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(19);
         ot_bucket_copy_body(D, D.r_key, D.r_val, bid, nb);
-        ot_grid_bar(D, target, nb);
+        OT_BAR(20);
       }
       if (ot_vol(ctr + kCtrHold) != 0) break;  // 3: more records than one block merges
     }
     ot_slot_body(D, D.r_key, -1, bid, nb);
-    ot_grid_bar(D, target, nb);
+    OT_BAR(21);
     ot_rebuild_body(D, D.r_key, D.r_val, -1, bid, nb);
     if (lead) {
       ctr[kCtrNi] = 0;
       D.loop[0] += 1;
       D.loop[1] += ctr[kCtrRounds];
     }
-    ot_grid_bar(D, target, nb);
+    OT_BAR(22);
     ot_free_count_body(D, counts, bid, nb);
-    ot_grid_bar(D, target, nb);
+    OT_BAR(23);
     ot_free_write_body(D, counts, bid, nb);
-    ot_grid_bar(D, target, nb);
+    OT_BAR(24);
     stage = 0;
   }
+#undef OT_BAR
   if (lead) D.bar[1] = target;
 }
 

@@ -470,7 +470,7 @@ class OtSolver {
   enum Buf {
     bT, bDy, bDfree, bDmatched, bConsumed, bFlOff, bFlCode, bFlB, bFlCnt, bFlPre, bSy, bSfree, bSmatched,
     bSfreed, bFb, bFy, bFpos, bFidx, bFu0, bFu, bAdmLen, bAdmOff, bAdm, bEk0, bEv0, bEk1, bEv1, bRk0, bRv0,
-    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bDaCnt, bDaFill, bDaOff, bDaTouch, bBar, bLoop, bFcounts, bRecOff, bNum
+    bRk1, bRv1, bCtr, bTemp, bScratch, bCut, bDaCnt, bDaFill, bDaOff, bDaTouch, bBar, bLoop, bFcounts, bRecOff, bStep, bNum
   };
   otprg::OtDev D_{};
   int64_t fl_cap_ = 0, adm_cap_ = 0, e_cap_ = 0, r_cap_ = 0;
@@ -791,8 +791,14 @@ class OtSolver {
     D_.fc_cap = small_caps ? 3 : std::min<int64_t>(phase_cap + 2, int64_t(1) << 20);
     D_.fcounts = ensure<int64_t>(bFcounts, D_.fc_cap);
     D_.rec_off = ensure<int64_t>(bRecOff, static_cast<size_t>(n_a_) + 1);
+    const bool steptime = std::getenv("OTPRG_OT_STEPTIME") != nullptr;
+    D_.steptime = steptime ? ensure<unsigned long long>(bStep, 32) : nullptr;
+    if (steptime) OT_CK(cudaMemsetAsync(D_.steptime, 0, 32 * 8, s), "memset");
     // (test knob: every record merge through the per-vertex buckets)
-    D_.small_rec = std::getenv("OTPRG_OT_BUCKETS") ? 0 : otprg::kOtSmallRec;
+    // one-block bitonic merge up to 1,024 records, buckets beyond (scripts/ot_steptime.py:
+    // n = 100 phases merge ~500 records, bitonic 12 us vs buckets 17 us per phase;
+    // n = 1,000 ~4,000 records, bitonic 78 us vs buckets 27 us)
+    D_.small_rec = std::getenv("OTPRG_OT_BUCKETS") ? 0 : 1024;
     OT_CK(cudaMemsetAsync(D_.bar, 0, 2 * sizeof(unsigned), s), "memset");
     OT_CK(cudaMemsetAsync(D_.loop, 0, 4 * sizeof(int64_t), s), "memset");
     if (adm_cap_ < 1 || small_caps) {
@@ -957,6 +963,14 @@ class OtSolver {
                   static_cast<size_t>(std::min<int64_t>(phases, r_->free_cap)) * 8);
     st_ = export_state();
     r_->loop_ms = loop_t.ms();
+    if (D_.steptime) {
+      unsigned long long st[32];
+      OT_CK(cudaMemcpy(st, D_.steptime, sizeof(st), cudaMemcpyDeviceToHost), "D2H");
+      std::fprintf(stderr, "ot step times (us, summed):");
+      for (int k = 1; k < 32; ++k)
+        if (st[k]) std::fprintf(stderr, " %d:%.0f", k, st[k] * 1e-3);
+      std::fprintf(stderr, "\n");
+    }
     if (std::getenv("OTPRG_OT_PROFILE"))
       std::fprintf(stderr,
                    "ot loop %.2f ms: %lld phases, %lld DA rounds (%lld sorted), %lld holds (persistent, %lld launches)\n",
