@@ -256,6 +256,7 @@ struct OtDev {
   int64_t* fcounts;    // [fc_cap] persistent loop: n_i of the phases of this launch
   int64_t* rec_off;    // [n_a + 1] persistent loop: merged records per demand vertex, scanned
   int small_rec;       // persistent loop: records merged by one block up to this many (else buckets)
+  int in_loop;         // set inside the persistent loop: the steps skip their own hold / done checks
   unsigned long long* r_key2;  // [r_cap] records scratch (the bucket merge; the host sort's output)
   int64_t* r_val2;
   int64_t fc_cap;

@@ -55,7 +55,11 @@ __device__ __forceinline__ void ot_fail(OtDev& D, int code, int x = 0, int y = 0
 }
 
 // The device-sized phase stopped for the host (kCtrHold): later steps return.
-__device__ __forceinline__ bool ot_hold(const OtDev& D) { return *(volatile int64_t*)&D.ctr[kCtrHold] != 0; }
+// (inside the persistent loop the loop itself tests the hold between steps,
+// so the steps skip this round trip)
+__device__ __forceinline__ bool ot_hold(const OtDev& D) {
+  return !D.in_loop && *(volatile int64_t*)&D.ctr[kCtrHold] != 0;
+}
 
 template <typename T>
 __device__ __forceinline__ uint32_t k_at(const OtDev& D, int a, int b) {
@@ -306,7 +310,7 @@ __global__ void ot_da_resolve_kernel(OtDev D, const unsigned long long* __restri
 // returns at once when the rounds are over (ctr[kCtrDone]), so a batch of
 // rounds is launched without looking at the counters.
 __device__ __forceinline__ bool da_over(const OtDev& D) {
-  return *(volatile int64_t*)&D.ctr[kCtrDone] != 0 || ot_hold(D);
+  return !D.in_loop && (*(volatile int64_t*)&D.ctr[kCtrDone] != 0 || ot_hold(D));
 }
 
 __device__ __forceinline__ void ot_da_propose_batched_body(OtDev& D, int bid, int nb) {
@@ -996,6 +1000,7 @@ __global__ void __launch_bounds__(1024, 1) ot_phase_loop_kernel(OtDev D, int sta
   const bool lead = bid == 0 && threadIdx.x == 0;
   unsigned target = *(volatile unsigned*)(D.bar + 1);
   int64_t* ctr = D.ctr;
+  D.in_loop = 1;
   // (optional per-step timeline: block 0's time from the previous barrier to
   // the end of barrier k, summed over the launch into D.steptime[k])
   unsigned long long t_prev = (D.steptime && lead) ? globaltimer() : 0ull;
