@@ -764,6 +764,71 @@ __device__ __forceinline__ void ot_small_merge_body(OtDev& D, unsigned long long
   while (P < n) P <<= 1;
   int64_t* s_val = reinterpret_cast<int64_t*>(s_key + P);
   __shared__ int s_heads[1024];
+  if (max(P, 32) <= (int)blockDim.x) {
+    // One element per thread: the bitonic network in registers, strides
+    // below 32 by warp shuffles (no block barrier), larger ones through
+    // shared memory; then the runs by a warp-shuffle block scan.
+    const int P32 = max(P, 32), t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    s_val = reinterpret_cast<int64_t*>(s_key + P32);
+    unsigned long long kk = t < n ? key[t] : ~0ull;
+    int64_t vv = t < n ? val[t] : 0;
+    for (int k = 2; k <= P32; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        unsigned long long kp = 0ull;
+        int64_t vp = 0;
+        if (j >= 32) {
+          __syncthreads();
+          if (t < P32) {
+            s_key[t] = kk;
+            s_val[t] = vv;
+          }
+          __syncthreads();
+          if (t < P32) {
+            kp = s_key[t ^ j];
+            vp = s_val[t ^ j];
+          }
+        } else if (t < P32) {  // (whole warps: P32 is a multiple of 32)
+          kp = __shfl_xor_sync(kFull, kk, j);
+          vp = __shfl_xor_sync(kFull, vv, j);
+        }
+        if (t < P32) {
+          const bool up = (t & k) == 0, lower = (t & j) == 0;
+          if (lower == up ? (kp < kk) : (kp > kk)) {  // the lower index keeps the min when ascending
+            kk = kp;
+            vv = vp;
+          }
+        }
+      }
+    __syncthreads();
+    if (t < P32) {
+      s_key[t] = kk;
+      s_val[t] = vv;
+    }
+    __syncthreads();
+    const int hd = (t < n && (t == 0 || s_key[t] != s_key[t - 1])) ? 1 : 0;
+    int inc = hd;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_heads[wid] = inc;
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < wid) before += s_heads[w];
+      total += s_heads[w];
+    }
+    if (hd) {
+      int64_t sum = 0;
+      for (int q = t; q < n && s_key[q] == kk; ++q) sum += s_val[q];
+      const int out = before + inc - 1;
+      key[out] = kk;
+      val[out] = sum;
+    }
+    if (t == 0) D.ctr[kCtrNFlows] = total;
+    __syncthreads();
+    return;
+  }
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
     s_key[i] = i < n ? key[i] : ~0ull;
     s_val[i] = i < n ? val[i] : 0;
