@@ -476,9 +476,11 @@ __device__ __forceinline__ void da_chain(const ShardArgs& S, const Round& rd, in
     for (int g = 0; g < G; ++g) {  // next candidate >= start, shard-ascending
       const int ghi = S.bounds[g + 1];
       if (start >= ghi) continue;
+      // the slot's candidates are loaded with its meta (one round trip), then
+      // cut to the meta's count
+      const int cc = lane < K ? __ldcg(cand + ((size_t)g * S.cap + i) * K + lane) : -1;
       const int2 mt = __ldcg(meta + (size_t)g * S.cap + i);
-      int c = -1;
-      if (lane < mt.x && lane < K) c = __ldcg(cand + ((size_t)g * S.cap + i) * K + lane);
+      const int c = lane < mt.x ? cc : -1;
       const unsigned bal = __ballot_sync(kFull, c >= start);
       if (bal) {
         a = __shfl_sync(kFull, c, __ffs(bal) - 1);
