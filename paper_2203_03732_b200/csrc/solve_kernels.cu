@@ -62,6 +62,16 @@ constexpr bool kTeams = OTPRG_TEAMS != 0;  // multi-warp rows in small phases
 #ifndef OTPRG_TEAM_DEN
 #define OTPRG_TEAM_DEN 1
 #endif
+#ifndef OTPRG_STATIC
+#define OTPRG_STATIC 1
+#endif
+// Static slots (small phases): the chain of input slot i writes output slot i
+// and its team keeps the next proposer's prologue in registers (no list read
+// at the next top).
+constexpr bool kStatic = OTPRG_STATIC != 0;
+#ifndef OTPRG_STATIC_HOLES
+#define OTPRG_STATIC_HOLES 16  // static slots while holes <= 1/this of the slots (A/B: 2 / 4 / 8 / 16)
+#endif
 #ifndef OTPRG_BULK
 #define OTPRG_BULK 1
 #endif
@@ -264,7 +274,8 @@ struct PhasePtrs {
 
 // A proposer's chain prologue (Y(b), low-set meta/entries, row min), loaded
 // at the top of the phase together with the phase counters so the first
-// chain of every warp starts without further dependent loads.
+// chain of every warp starts without further dependent loads -- or, after a
+// static-slot phase, carried in registers from the chain that produced it.
 struct Prefetch {
   bool ok;
   int i, b;
@@ -279,7 +290,8 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
                                           int lane, unsigned long long& bytes,
                                           unsigned long long& steps, unsigned long long& walks,
                                           unsigned* s_stat, unsigned long long* acc,
-                                          const Team& tm, const Prefetch& pf, bool use_pf) {
+                                          const Team& tm, const Prefetch& pf, bool use_pf,
+                                          int in_slot, Prefetch& nx) {
   const bool lead = lane == 0 && tm.rank == 0;  // performs the chain's global side effects
 #define OTPRG_STAT(k) \
   if (lead) atomicAdd(&s_stat[k], 1u)
@@ -287,8 +299,10 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
   // Every chain ends in exactly one event (b exhausted, or a first take of
   // some a), written to its own output slot: the slot is reserved now, so
   // the reservation's round trip overlaps the chain instead of ending it.
-  int slot = 0;
-  if (lead) slot = atomicAdd(P.slot_out, 1);
+  // Static slots: output slot = input slot (in_slot >= 0), the next
+  // proposer's prologue goes to nx (nx.ok = false: reload it at the top).
+  int slot = in_slot;
+  if (lead && in_slot < 0) slot = atomicAdd(P.slot_out, 1);
   using S = Simd<T>;
   Ctl* ctl = A.ctl;
   const T* kT = static_cast<const T*>(A.kT);
@@ -408,6 +422,20 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
         atomicAdd(P.cnt_out, 1);  // results unused: compiled to fire-and-forget reductions
         atomicAdd(P.exh_out, 1);
       }
+      if (in_slot >= 0) {  // b proposes again next phase from the same slot
+        // (a displaced b continuing here: its cache may be written this
+        // phase by its own chain, not in this warp's registers -> reload)
+        nx.ok = fresh;
+        nx.b = b;
+        nx.yb = yb + 1;
+        nx.rowmin = track_min ? (uint32_t)(T)m : rmin;
+        nx.meta = meta;
+        nx.ent = ent;
+        if (fresh && dirty) {  // entries rewritten by this warp's lanes
+          __syncwarp();
+          nx.ent = lane < kLowCap ? __ldcg(A.lent + (size_t)b * kLowCap + lane) : 0ull;
+        }
+      }
       return;
     }
     const unsigned long long key = ((unsigned long long)cur_tag << 32) | (uint32_t)b;
@@ -449,20 +477,32 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
       lb.on = false;
       continue;
     }
+    int partner = -1;
     if (lead) {
       // a is taken for the first time this phase: its partner before this
       // phase is displaced (it is freed by apply_phase).  If a was matched in
       // the previous phase, that partner is the previous phase's winner (the
-      // global matching is being updated concurrently at this phase's top);
+      // global matching is being updated concurrently in this phase);
       // otherwise match_a, which is complete for all earlier phases (the
       // apply of M'_{phase-1} only writes match_a of a in M'_{phase-1}).
-      const int partner = (uint32_t)(hp >> 32) == prev_tag ? (int)(uint32_t)hp : ma;
+      partner = (uint32_t)(hp >> 32) == prev_tag ? (int)(uint32_t)hp : ma;
       if (partner >= 0) {
         atomicAdd(P.cnt_out, 1);
       }
       P.list_out[slot] = partner;  // -1: a hole in the next list
       P.mp_out[slot] = make_int2(a, partner);
       atomicAdd(P.mp_cnt_out, 1);
+    }
+    if (in_slot >= 0) {  // the displaced partner proposes next phase from this slot
+      partner = (int)team_bcast(tm, (unsigned long long)(unsigned)partner, lane);
+      nx.ok = true;
+      nx.b = partner;
+      if (partner >= 0) {  // matched since an earlier phase: its state is stable
+        nx.yb = (uint32_t)__ldcg(A.yb + partner);
+        nx.meta = __ldcg(A.lmeta + partner);
+        nx.ent = lane < kLowCap ? __ldcg(A.lent + (size_t)partner * kLowCap + lane) : 0ull;
+        nx.rowmin = (uint32_t)__ldcg(rowmin + partner);
+      }
     }
     return;
   }
@@ -539,6 +579,12 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     }
   };
   const int q0 = (int)threadIdx.x * (int)gridDim.x + (int)blockIdx.x;
+  // This warp's first proposer of the coming phase: prefetched at the top,
+  // or (after a static-slot phase) carried over from the chain that produced it.
+  Prefetch pf;
+  pf.ok = false;
+  pf.i = -1;
+  bool prev_static = false;  // the previous phase wrote its outputs to static slots
   while (true) {
     const int r_prev = phase % 3, r_cur = (phase + 1) % 3, r_nxt = (phase + 2) % 3;
     // apply M'_{phase} unless the previous launch already did
@@ -559,10 +605,11 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     // first proposer of the coming phase (static index under the previous
     // team size; b is clamped, used only if the index is < n) and its chain
     // prologue, and this thread's M' entry.
-    Prefetch pf;
-    pf.i = (wib / tsize_prev) * (int)gridDim.x + (int)blockIdx.x;
-    pf.ok = pf.i < n_b;
-    if (pf.ok) {
+    if (!prev_static) {  // (else pf holds the carry: same team size and slot)
+      pf.i = (wib / tsize_prev) * (int)gridDim.x + (int)blockIdx.x;
+      pf.ok = pf.i < n_b;
+    }
+    if (!prev_static && pf.ok) {
       pf.b = __ldcg(list_in + pf.i);  // may be a hole (-1)
       const int bb = min(max(pf.b, 0), n_b - 1);
       pf.yb = (uint32_t)__ldcg(A.yb + bb);
@@ -724,12 +771,27 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     // reads them), hence the same-team-size condition.
     bool use_pf = pf.ok && !bulk && i == pf.i && tsize == tsize_prev;
     const bool single = n_slots <= total_teams;  // every team has at most its static slot
+    // Static slots for the outputs of this phase: every team has at most its
+    // slot, few holes (the slot range is not compacted), same team size next
+    // phase (it depends on the slot count only).
+    const bool static_out = kStatic && kSmem && single && !bulk && (n_slots - n) * OTPRG_STATIC_HOLES <= n_slots;
+    if (static_out && leader) ctl->slots[r_cur] = n_slots;
     tsize_prev = tsize;
+    pf.ok = false;  // (from here on: the carry for the next phase)
+    pf.i = i;
     while (i < n_slots) {
       const int b = use_pf ? pf.b : __ldcg(list_in + i);
-      if (b >= 0)
+      if (b >= 0) {
         run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
-                            tr ? acc : nullptr, tm, pf, use_pf);
+                            tr ? acc : nullptr, tm, pf, use_pf, static_out ? i : -1, pf);
+      } else if (static_out) {  // a hole stays a hole
+        if (lane == 0 && tm.rank == 0) {
+          P.list_out[i] = -1;
+          P.mp_out[i] = make_int2(-1, -1);
+        }
+        pf.ok = true;
+        pf.b = -1;
+      }
       use_pf = false;
       if (single) break;
       unsigned long long nx = 0;
@@ -745,6 +807,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       atomicMax(tr + 11, walks - walks0);
       atomicMax(tr + 12, acc[2]);
     }
+    prev_static = static_out;
     bar_target += gridDim.x;
     grid_barrier(ctl, bar_target, tr ? tr + 2 : nullptr, tr ? tr + 3 : nullptr);
     if (tr && leader) tr[4] = globaltimer();
