@@ -72,6 +72,20 @@ __global__ void __launch_bounds__(512, 1) bar_kernel(unsigned* count, unsigned* 
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
       }
     }
+    if constexpr (MODE == 10 || MODE == 11 || MODE == 12) {  // two-level: groups of GS blocks
+      constexpr int GS = MODE == 10 ? 8 : (MODE == 11 ? 16 : 12);
+      const int ng = (gridDim.x + GS - 1) / GS;
+      const int g = blockIdx.x / GS;
+      const int gsize = min(GS, (int)gridDim.x - g * GS);
+      if (threadIdx.x == 0) {
+        unsigned* grp = flags + 32 * (g + 1);  // one 128-byte line per group
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(grp) : "memory");
+        if (old + 1 == (unsigned)(it * gsize))  // last of its group
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+        while ((int)(ld_acq(count) - (unsigned)(it * ng)) < 0) {}
+      }
+    }
     if constexpr (MODE == 5 || MODE == 6) {  // counter barrier, then every block reads all P slots
       target += gridDim.x;
       if (threadIdx.x < P) junk[(1u << 22) - 4096 + threadIdx.x * 2] = it;  // (slot stores, tags)
@@ -112,7 +126,7 @@ template <int MODE>
 float run(int grid, int iters, int S, unsigned* count, unsigned* flags, unsigned* junk,
           unsigned long long* out) {
   cudaMemset(count, 0, 4);
-  cudaMemset(flags, 0, 4096);
+  cudaMemset(flags, 0, 65536);
   void* args[] = {&count, &flags, &iters, &S, &junk, &out};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -133,7 +147,7 @@ int main() {
   unsigned *count, *flags, *junk;
   unsigned long long* out;
   cudaMalloc(&count, 4);
-  cudaMalloc(&flags, 4096);
+  cudaMalloc(&flags, 65536);
   cudaMalloc(&junk, 4u << 22);
   cudaMalloc(&out, 16);
   const int iters = 20000;
@@ -145,6 +159,14 @@ int main() {
   const char* names[] = {"counter red.release + ld.acquire polls", "counter red.release + relaxed polls + fence",
                          "per-block flags st.release + relaxed polls + fence", "per-block flags + acquire polls",
                          "counter atom.release (last skips poll) + relaxed polls"};
+  for (int rep = 0; rep < 2; ++rep) {
+    printf("two-level, groups of 8 : %.3f us\n", run<10>(sms, iters, 0, count, flags, junk, out));
+    printf("two-level, groups of 16: %.3f us\n", run<11>(sms, iters, 0, count, flags, junk, out));
+    printf("two-level, groups of 12: %.3f us\n", run<12>(sms, iters, 0, count, flags, junk, out));
+    printf("flat counter           : %.3f us\n", run<0>(sms, iters, 0, count, flags, junk, out));
+    printf("two-level 8, S=4       : %.3f us\n", run<10>(sms, iters, 4, count, flags, junk, out));
+    printf("flat counter, S=4      : %.3f us\n", run<0>(sms, iters, 4, count, flags, junk, out));
+  }
   for (int S : {0, 4, 16}) {
     for (int rep = 0; rep < 2; ++rep) {
       float us[5] = {run<0>(sms, iters, S, count, flags, junk, out), run<1>(sms, iters, S, count, flags, junk, out),
