@@ -330,7 +330,8 @@ def run_ours(args, world, rank, local) -> None:
                                                        if d["seed"] == sd])), 4)
                         for sd in SEEDS if any(d["seed"] == sd for d in dev)},
         "roofline": roofline,
-        "gpu_launches": 4 * args.steps,  # init, propose scan, phase loop, completion
+        # init, propose scan, phase loop, completion, matched-pair costs (per step, as reported)
+        "gpu_launches": int(sum(d["gpu_launches"] for d in dev)),
         "clocks": clk.summary(),
     }
 

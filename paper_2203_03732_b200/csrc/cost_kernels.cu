@@ -540,6 +540,32 @@ __global__ void l1_matched_cost_kernel(const double* __restrict__ xa, const doub
   }
 }
 
+// Matched-pair point costs: x = this side's points, y = the other side's
+// (the squared difference is symmetric, so either orientation gives the
+// reference's bits for c(a, b)).
+__global__ void points_matched_cost_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                           const int32_t* __restrict__ match, int n, double* __restrict__ out) {
+  const double sqrt2 = __dsqrt_rn(2.0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int j = match[i];
+    if (j < 0) {
+      out[i] = 0.0;
+      continue;
+    }
+    const double dx = __dsub_rn(x[2 * (size_t)i], y[2 * (size_t)j]);
+    const double dy = __dsub_rn(x[2 * (size_t)i + 1], y[2 * (size_t)j + 1]);
+    out[i] = __ddiv_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))), sqrt2);
+  }
+}
+
+__global__ void dense_matched_cost_kernel(const double* __restrict__ cost, int n_b,
+                                          const int32_t* __restrict__ match, int n, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int j = match[i];
+    out[i] = j < 0 ? 0.0 : cost[(size_t)i * n_b + j];
+  }
+}
+
 // A given rounded-cost matrix (copy instances, ot.hpp:52-63): k[a][b]
 // row-major int32 -> kT[b][a] (32x32 shared-memory transpose), pads = type max.
 template <typename T>
@@ -767,6 +793,20 @@ cudaError_t launch_l1_matched_cost(const double* xa, const double* yb, int dim, 
                                    bool self_is_a, double* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   l1_matched_cost_kernel<<<(n + 127) / 128, 128, 0, s>>>(xa, yb, dim, match, n, self_is_a ? 1 : 0, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_points_matched_cost(const double* xa, const double* yb, const int32_t* match, int n,
+                                       double* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  points_matched_cost_kernel<<<(n + 255) / 256, 256, 0, s>>>(xa, yb, match, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_matched_cost(const double* cost, int n_b, const int32_t* match, int n, double* out,
+                                      cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  dense_matched_cost_kernel<<<(n + 255) / 256, 256, 0, s>>>(cost, n_b, match, n, out);
   return cudaGetLastError();
 }
 

@@ -76,6 +76,7 @@ struct otprg_ctx {
   int32_t unit_floor = 0, unit_ceil = 0;
   int cost_kind = 0;
   const double* host_cost = nullptr;  // caller buffer (DENSE); valid until next prepare
+  bool stage_holds_cost = false;      // stage = the prepared dense f64 matrix (caller orientation)
   std::vector<double> pts_a, pts_b;   // original orientation (POINTS2D)
   std::vector<uint8_t> img_a, img_b;  // original orientation (L1_U8)
   int img_dim = 0;

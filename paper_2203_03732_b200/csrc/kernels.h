@@ -95,6 +95,13 @@ cudaError_t launch_transpose_f64(const double* in, int n, int dim, double* out, 
 // Costs of the matched pairs of an L1 image instance (thread per original a).
 cudaError_t launch_l1_matched_cost(const double* xa, const double* yb, int dim, const int32_t* match, int n,
                                    bool self_is_a, double* out, cudaStream_t s);
+// Matched-pair costs for matching_cost (core.cpp:95-102), one per caller a
+// (0 where unmatched): 2-D points (instances.cpp:70-75, sqrt(dx*dx+dy*dy)/sqrt(2)
+// in IEEE round-to-nearest, no FMA) or a gather from the dense f64 matrix on the device.
+cudaError_t launch_points_matched_cost(const double* xa, const double* yb, const int32_t* match, int n,
+                                       double* out, cudaStream_t s);
+cudaError_t launch_dense_matched_cost(const double* cost, int n_b, const int32_t* match, int n, double* out,
+                                      cudaStream_t s);
 // Rounded matrix back to int32 row-major in the ORIGINAL orientation (for
 // otprg_scale_round_costs).
 cudaError_t launch_k_to_kT(const int32_t* k, int n_a, int n_b, void* kT, int lda, int width,

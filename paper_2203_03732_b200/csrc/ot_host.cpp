@@ -420,6 +420,7 @@ class OtSolver {
     lda_ = (n_a_ + align - 1) / align * align;
     OT_CK(cudaSetDevice(ctx_->device), "cudaSetDevice");
     const size_t bytes = static_cast<size_t>(n_a_) * n_b_ * sizeof(double);
+    ctx_->stage_holds_cost = false;
     OT_CK(ctx_->stage.ensure(bytes), "alloc cost staging");
     OT_CK(ctx_->kT.ensure(static_cast<size_t>(n_b_) * lda_ * width_), "alloc kT");
     OT_CK(ctx_->ctl.ensure(sizeof(otprg::Ctl)), "alloc ctl");
@@ -453,6 +454,7 @@ class OtSolver {
     const int align = 512 / width_;
     lda_ = (n_a_ + align - 1) / align * align;
     OT_CK(cudaSetDevice(ctx_->device), "cudaSetDevice");
+    ctx_->stage_holds_cost = false;
     OT_CK(ctx_->stage.ensure(nn * 4), "alloc k staging");
     OT_CK(ctx_->kT.ensure(static_cast<size_t>(n_b_) * lda_ * width_), "alloc kT");
     OT_CK(ctx_->ctl.ensure(sizeof(otprg::Ctl)), "alloc ctl");

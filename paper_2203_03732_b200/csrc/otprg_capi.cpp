@@ -204,8 +204,10 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
   ctx->build_launches = 0;
   if (p->cost_kind == OTPRG_COST_DENSE_F64) {
     const size_t bytes = static_cast<size_t>(p->n_a) * p->n_b * sizeof(double);
+    ctx->stage_holds_cost = false;
     CK(ctx->stage.ensure(bytes), "alloc cost staging");
     CK(otprg::h2d_large(ctx, ctx->stage.p, p->cost, bytes), "H2D cost");
+    ctx->stage_holds_cost = true;
     CK(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(Ctl), ctx->stream), "memset");
     int* status = &ctx->ctl.as<Ctl>()->status;
     CK(otprg::launch_round_dense(ctx->stage.as<double>(), p->n_a, p->n_b, ctx->swapped, p->eps,
@@ -214,6 +216,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
     ctx->build_launches = 1;
     ctx->host_cost = p->cost;
   } else if (p->cost_kind == OTPRG_COST_L1_U8) {
+    ctx->stage_holds_cost = false;
     // load_mnist_pair's cost (instances.cpp:114-142) from raw pixels
     const size_t dim = static_cast<size_t>(p->dim);
     const uint8_t* ia_img = ctx->swapped ? p->img_b : p->img_a;  // internal demand side
@@ -238,6 +241,7 @@ int do_prepare(otprg_ctx* ctx, const otprg_problem* p) {
     ctx->img_a.assign(p->img_a, p->img_a + dim * p->n_a);
     ctx->img_b.assign(p->img_b, p->img_b + dim * p->n_b);
   } else {
+    ctx->stage_holds_cost = false;
     const double* pa = ctx->swapped ? p->pts_b : p->pts_a;  // internal demand points
     const double* pb = ctx->swapped ? p->pts_a : p->pts_b;
     CK(ctx->pts.ensure((ia + ib) * 2 * sizeof(double)), "alloc points");
@@ -403,6 +407,12 @@ int check_status(otprg_ctx* ctx, const Ctl& h, bool need_done) {
   }
 }
 
+// Whether export_state evaluates the matched-pair costs on the device.
+bool dev_pair_costs(const otprg_ctx* ctx) {
+  return ctx->cost_kind == OTPRG_COST_L1_U8 || ctx->cost_kind == OTPRG_COST_POINTS2D ||
+         (ctx->cost_kind == OTPRG_COST_DENSE_F64 && ctx->stage_holds_cost);
+}
+
 // Copies the current device state into the caller's result (caller
 // orientation for the matching; internal orientation for the duals).
 int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
@@ -413,11 +423,13 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
                o_t = o_yb + ib * 4ull, o_fc = (o_t + static_cast<size_t>(ia) * ctx->width + 7) & ~7ull;
   const int64_t fc_first = std::min<int64_t>(
       std::min<int64_t>(ctx->fc_cap, r->free_counts ? r->free_cap : 0), 65536);
-  // L1 image costs of the matched pairs are evaluated on the device (the
-  // reference's arithmetic, K3's normalised pixels), one per original a
+  // Costs of the matched pairs are evaluated on the device (the reference's
+  // arithmetic: L1 over K3's normalised pixels, the point formula, or a
+  // gather from the dense matrix), one per original a; the host only sums.
   const bool l1 = ctx->cost_kind == OTPRG_COST_L1_U8;
+  const bool dev_pc = dev_pair_costs(ctx);
   const size_t o_pc = o_fc + static_cast<size_t>(fc_first) * 8;
-  const size_t need = o_pc + (l1 ? static_cast<size_t>(ctx->n_a) * 8 : 0);
+  const size_t need = o_pc + (dev_pc ? static_cast<size_t>(ctx->n_a) * 8 : 0);
   if (ctx->hpin_n < need) {
     if (ctx->hpin) cudaFreeHost(ctx->hpin);
     ctx->hpin = nullptr;
@@ -434,15 +446,28 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
                      cudaMemcpyDeviceToHost, s), "D2H");
   if (fc_first > 0)
     CK(cudaMemcpyAsync(hp + o_fc, ctx->fc.p, fc_first * 8, cudaMemcpyDeviceToHost, s), "D2H");
-  if (l1) {
-    const size_t dim = ctx->img_dim;
-    const double* xa = ctx->pts.as<double>();
-    const double* yb = xa + static_cast<size_t>(ctx->ia) * dim;
+  if (dev_pc) {
     CK(ctx->v_ya.ensure(static_cast<size_t>(ctx->n_a) * 8), "alloc pair costs");
     // original a = internal a (unswapped, partner match_a) or internal b (swapped, partner match_b)
-    CK(otprg::launch_l1_matched_cost(xa, yb, ctx->img_dim, ctx->swapped ? ctx->mb.as<int32_t>() : ctx->ma.as<int32_t>(),
-                                     ctx->n_a, !ctx->swapped, ctx->v_ya.as<double>(), s),
-       "pair cost launch");
+    const int32_t* m_orig = ctx->swapped ? ctx->mb.as<int32_t>() : ctx->ma.as<int32_t>();
+    if (l1) {
+      const size_t dim = ctx->img_dim;
+      const double* xa = ctx->pts.as<double>();
+      const double* yb = xa + static_cast<size_t>(ctx->ia) * dim;
+      CK(otprg::launch_l1_matched_cost(xa, yb, ctx->img_dim, m_orig, ctx->n_a, !ctx->swapped,
+                                       ctx->v_ya.as<double>(), s),
+         "pair cost launch");
+    } else if (ctx->cost_kind == OTPRG_COST_POINTS2D) {
+      const double* dpa = ctx->pts.as<double>();  // internal demand points, then supply points
+      const double* dpb = dpa + static_cast<size_t>(ia) * 2;
+      CK(otprg::launch_points_matched_cost(ctx->swapped ? dpb : dpa, ctx->swapped ? dpa : dpb, m_orig, ctx->n_a,
+                                           ctx->v_ya.as<double>(), s),
+         "pair cost launch");
+    } else {
+      CK(otprg::launch_dense_matched_cost(ctx->stage.as<double>(), ctx->n_b, m_orig, ctx->n_a,
+                                          ctx->v_ya.as<double>(), s),
+         "pair cost launch");
+    }
     CK(cudaMemcpyAsync(hp + o_pc, ctx->v_ya.p, static_cast<size_t>(ctx->n_a) * 8, cudaMemcpyDeviceToHost, s), "D2H");
   }
   CK(cudaEventRecord(ctx->ev[3], s), "event");
@@ -491,7 +516,7 @@ int export_state(otprg_ctx* ctx, otprg_result* r, Ctl* hout) {
   const double* pc = reinterpret_cast<const double*>(hp + o_pc);
   for (int32_t a = 0; a < ctx->n_a; ++a) {
     const int32_t b = r->match_of_a[a];
-    if (b != -1) total += l1 ? pc[a] : pair_cost(ctx, a, b);
+    if (b != -1) total += dev_pc ? pc[a] : pair_cost(ctx, a, b);
   }
   r->cost = total;
   r->build_ms = ctx->build_ms;
@@ -529,7 +554,7 @@ int do_solve(otprg_ctx* ctx, otprg_result* r) {
   r->solve_ms = ms_all;
   r->phase1_ms = ms_p1;
   r->solve_d2h_ms = ms_d2h;
-  r->gpu_launches = 4;  // init, phase-1 propose scan, phase loop, complete
+  r->gpu_launches = 4 + (dev_pair_costs(ctx) ? 1 : 0);  // init, phase-1 scan, loop, complete[, pair costs]
   return OTPRG_OK;
 }
 }  // namespace otprg_capi
@@ -685,6 +710,7 @@ int otprg_scale_round_costs(otprg_ctx* ctx, const otprg_problem* prob, int32_t* 
   int st = do_prepare(ctx, prob);
   if (st) return st;
   const size_t total = static_cast<size_t>(ctx->n_a) * ctx->n_b;
+  ctx->stage_holds_cost = false;
   CK(ctx->stage.ensure(std::max(ctx->stage.n, total * 4)), "alloc export");
   // the staging buffer may hold the dense input; it is no longer needed
   CK(otprg::launch_export_k(ctx->kT.p, ctx->ia, ctx->ib, ctx->lda, ctx->width, ctx->swapped,
