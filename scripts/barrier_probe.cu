@@ -159,6 +159,9 @@ int main() {
   const char* names[] = {"counter red.release + ld.acquire polls", "counter red.release + relaxed polls + fence",
                          "per-block flags st.release + relaxed polls + fence", "per-block flags + acquire polls",
                          "counter atom.release (last skips poll) + relaxed polls"};
+  for (int g : {148, 128, 96, 74, 48, 37, 16})
+    printf("flat counter, grid %3d: %.3f us (S=4: %.3f us)\n", g, run<0>(g, iters, 0, count, flags, junk, out),
+           run<0>(g, iters, 4, count, flags, junk, out));
   for (int rep = 0; rep < 2; ++rep) {
     printf("two-level, groups of 8 : %.3f us\n", run<10>(sms, iters, 0, count, flags, junk, out));
     printf("two-level, groups of 16: %.3f us\n", run<11>(sms, iters, 0, count, flags, junk, out));
