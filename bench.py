@@ -212,6 +212,9 @@ def check_pins(m, s, seed: int) -> bool:
     return all(got[k] == want[k] for k in got)
 
 
+LAT_FLOOR_US = round(1.25 + 460 / 1965.0 + 712 / 1965.0, 3)  # see "latency_floor" in the line
+
+
 def ncu_traffic() -> dict | None:
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
@@ -225,7 +228,7 @@ def cpu_baseline_ref(gpu_result) -> dict:
     """The unmodified reference, 1 thread, one full solve of seed 1 (~10-30 s)."""
     from oracle.pyoracle import Oracle, Reference
     if Reference.available():
-        r = Reference.get().solve_uniform_square(N, 1, EPS, threads=1)
+        r = Reference.get().solve_uniform_square(N, 1, EPS, threads=1, time_rounding=True)
         kind, ms = "reference", r.solve_ms
     else:  # the C restatement (port), timed around its solve
         o = Oracle.get()
@@ -243,7 +246,11 @@ def cpu_baseline_ref(gpu_result) -> dict:
             "sample": f"one full solve of gen_uniform_square({N}, seed=1), eps={EPS}, "
                       "threads=1 (deterministic mode), steady_clock around solve_assignment "
                       "(includes its cost rounding, bench.cpp:62-64)",
-            "phases": int(r.phases), "gpu_bit_exact_vs_this_run": bool(same)}
+            "phases": int(r.phases), "gpu_bit_exact_vs_this_run": bool(same),
+            # the reference timer includes its rounding, so also
+            # report it without (scale_round_costs timed separately, same run)
+            "rounding_ms": round(float(getattr(r, "round_ms", 0.0) or 0.0), 3),
+            "value_minus_rounding": round(ms - float(getattr(r, "round_ms", 0.0) or 0.0), 3)}
 
 
 def run_ours(args, world, rank, local) -> None:
@@ -307,6 +314,17 @@ def run_ours(args, world, rank, local) -> None:
             "traffic": (traffic or {}).get("propose_dram_bytes_per_launch"),
             "launch_ms": round(float(np.mean([d["phase1_ms"] for d in dev])), 4),
             "timer": "device %globaltimer span of the launch (first block start to last warp end)"},
+        # The loop is latency-bound: per phase it needs at least one
+        # grid barrier, one dependent L2 read at the top and one proposal atomic.
+        # Those latencies are measured on this pool (profiles/r02c_barrier_probe.txt:
+        # 1.25 us barrier at 148 blocks, 460-cycle L2 hit, 712-cycle 64-bit atomicMin
+        # at 1965 MHz); frac = that floor / the measured time per phase.
+        "latency_floor": {
+            "per_phase_us": LAT_FLOOR_US,
+            "measured_per_phase_us": round(float(np.mean([d["loop_ms"] * 1e3 / d["phases"] for d in dev])), 3),
+            "frac": round(LAT_FLOOR_US / float(np.mean([d["loop_ms"] * 1e3 / d["phases"] for d in dev])), 4),
+            "source": "grid barrier 1.25 us + L2 hit 0.234 us + atomicMin64 0.362 us "
+                      "(scripts/barrier_probe.cu, scripts/latency_probe.cu)"},
         "bytes_touched_per_step": int(np.mean([d["bytes_touched"] for d in dev])),
         "bytes_alg_per_step": int(np.mean([d["bytes_alg"] for d in dev])),
     }
