@@ -7,9 +7,14 @@ exact_ot via oracle/_ref) as the optimum:
   3  transport cost <= optimal + eps, complete plans (:252-291)
   4  per-phase invariant suite over 1-3              (device verify + observer)
   5  phase and free-count bounds                     (:213-224)
+  6  at most two dual clusters per vertex            (:252-291, the cluster checks after every phase)
+  9  baseline comparison at high accuracy            (:390-449, device form: the GPU Sinkhorn
+     baseline blows a 10x budget or underflows; its time-ratio window is a statement about the
+     reference's CPU scaling, here only "no worse than quadratic" is asserted)
  10  sequential runs bit-for-bit deterministic       (:451-479)
-(Criterion 9 is a CPU-scaling statement about the reference itself.)  Seed
-ranges are thinned from 30 to keep the GPU suite short."""
+(Criteria 7-8 compare the reference's own oracles and flow forms; the OT per-phase flows
+are pinned in test_gpu_ot_clusters.py.)  Seed ranges are thinned from 30 to keep the GPU
+suite short."""
 import ctypes as C
 
 import numpy as np
@@ -105,9 +110,42 @@ def test_criterion_3_transport(oracles):
             inst = otprg.gen_random_ot_rational(n, n, seed * 1009 + n)
             opt_cost = exact_ot(inst.mu, inst.nu, inst.cost)
             for eps in (0.25, 0.1):
-                plan, s = otprg.solve_ot(inst, eps)
+                # criterion 6: the cluster invariant (<= 2 dual clusters per vertex,
+                # ot.cpp:190-250) is checked after every phase; a violation raises
+                plan, s = otprg.solve_ot(inst, eps, otprg.OTOptions(check_invariants=True))
                 assert plan.cost <= opt_cost + eps
                 assert np.abs(plan.col_sums(n) - inst.nu).max() <= 1e-12   # complete plans
+
+
+def test_criterion_9_baseline_and_scaling():
+    import time
+    times = {}
+    for n in (1000, 2000, 4000):
+        inst = otprg.gen_uniform_square(n, 4242)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=0.1))
+            ts.append(time.perf_counter() - t0)
+        times[n] = sorted(ts)[1]
+    assert times[2000] / times[1000] <= 6.0 and times[4000] / times[2000] <= 6.0
+    # acceptance.cpp:418-446: at eps = 0.01 the entropic baseline must blow a 10x
+    # budget or raise the documented underflow error
+    n, hard_eps = 2000, 0.01
+    inst = otprg.gen_uniform_square(n, 777, dense=True)
+    otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=hard_eps))  # (warm)
+    t0 = time.perf_counter()
+    otprg.solve_assignment(inst, otprg.AssignmentOptions(eps=hard_eps))
+    pr_ms = (time.perf_counter() - t0) * 1e3
+    cfg = otprg.SinkhornConfig(reg=otprg.reg_for_eps(hard_eps, n), tol=1e-6, max_iters=1000000,
+                               time_budget_ms=10.0 * pr_ms)
+    try:
+        ot = otprg.OTInstance(np.full(n, 1.0 / n), np.full(n, 1.0 / n),
+                              np.ascontiguousarray(inst.dense_cost(), np.float64))  # assignment_to_ot
+        res = otprg.sinkhorn(ot, cfg, entries=False)
+        assert not res.converged
+    except otprg.NumericalError:
+        pass
 
 
 def test_criterion_10_determinism():
