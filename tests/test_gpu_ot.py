@@ -55,6 +55,21 @@ def test_one_by_one_ships_everything():  # test_ot.cpp:90-97
     assert abs(plan.total_mass() - 1.0) <= 1e-12 and abs(plan.cost - 0.2) <= 1e-12
 
 
+def test_zero_mass_points(reference):  # test_ot.cpp:348-368
+    mu, nu = np.array([0.0, 0.6, 0.4]), np.array([0.5, 0.0, 0.5])
+    cost = np.full((3, 3), 0.4)
+    cost[1, 0], cost[2, 2] = 0.1, 0.2
+    plan, stats = otprg.solve_ot(otprg.OTInstance(mu, nu, cost), 0.2)
+    cols, rows = plan.col_sums(3), plan.row_sums(3)
+    assert abs(cols[0] - 0.5) <= 1e-12 and cols[1] == 0.0 and abs(cols[2] - 0.5) <= 1e-12
+    assert rows[0] == 0.0 and rows[1] <= 0.6 + 1e-12 and rows[2] <= 0.4 + 1e-12
+    # and bit for bit what the unmodified reference ships
+    r = reference.solve_ot(mu, nu, cost, 0.2)
+    assert stats.phases == r["phases"] and float(plan.cost).hex() == float(r["cost"]).hex()
+    assert np.array_equal(plan.a, r["a"]) and np.array_equal(plan.b, r["b"])
+    assert np.array_equal(plan.mass, r["mass"])
+
+
 def test_rational_instances_match_reference(pins):
     keys = sorted(k for k, w in pins.items() if w["kind"] == "rational" and w["n_a"] * w["n_b"] <= 2_000_000)
     assert keys
