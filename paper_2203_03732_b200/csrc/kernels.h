@@ -52,6 +52,7 @@ struct SolveArgs {
   Ctl* ctl;
   uint32_t max_phase;           // run phases up to and including this one
   int32_t pre_scanned;          // phase-1 lists/rowmin built by launch_propose_stream
+  int32_t tail_switch;          // (full loop) stop where the tail-specialised loop takes over
   // Optional device timeline (%globaltimer ns), kTraceSlots u64 per phase, indexed by
   // phase - 1; nullptr disables tracing.
   unsigned long long* trace;
@@ -332,6 +333,8 @@ cudaError_t launch_init_state(const SolveArgs& a, int n_a, int n_b, int lda, int
                               cudaStream_t s);
 cudaError_t launch_phase_loop(const SolveArgs& a, int width, bool smem_t, int lda, int grid,
                               cudaStream_t s);
+// Launches launch_phase_loop issues (2 when the tail-specialised loop follows).
+int phase_loop_launches(int width, bool smem_t, int lda, int grid);
 int phase_loop_grid(int width, bool smem_t, int lda, int num_sms);
 size_t phase_loop_smem(int width, bool smem_t, int lda);
 // Phase-1 propose scan (propose_kernels.cu): every row's k == 0 positions

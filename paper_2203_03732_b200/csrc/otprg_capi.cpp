@@ -403,6 +403,7 @@ int check_status(otprg_ctx* ctx, const Ctl& h, bool need_done) {
     case 11: return fail(ctx, OTPRG_INVARIANT, "supply dual exceeded the device storage bound [phase,b,y]=" + d);
     case 12: return fail(ctx, OTPRG_INVARIANT, "demand dual exceeded the device storage bound [phase,a,t]=" + d);
     case 13: return fail(ctx, OTPRG_INVARIANT, "holder key from a later phase [phase,b,a,key_phase,key_b]=" + d);
+    case 14: return fail(ctx, OTPRG_DEVICE, "tail loop entered above its team-size regime [phase,slots]=" + d);
     default: return fail(ctx, h.status, "device solve failed [" + d + "]");
   }
 }
@@ -554,7 +555,9 @@ int do_solve(otprg_ctx* ctx, otprg_result* r) {
   r->solve_ms = ms_all;
   r->phase1_ms = ms_p1;
   r->solve_d2h_ms = ms_d2h;
-  r->gpu_launches = 4 + (dev_pair_costs(ctx) ? 1 : 0);  // init, phase-1 scan, loop, complete[, pair costs]
+  // init, phase-1 scan, loop (+ its tail launch), complete[, pair costs]
+  r->gpu_launches = 3 + otprg::phase_loop_launches(ctx->width, ctx->smem_t, ctx->lda, ctx->loop_grid) +
+                    (dev_pair_costs(ctx) ? 1 : 0);
   return OTPRG_OK;
 }
 }  // namespace otprg_capi

@@ -75,6 +75,12 @@ constexpr bool kStatic = OTPRG_STATIC != 0;
 #ifndef OTPRG_BULK
 #define OTPRG_BULK 1
 #endif
+#ifndef OTPRG_TAIL
+#define OTPRG_TAIL 1  // small phases (teams of 8 warps) run in a second, specialised launch
+#endif
+#ifndef OTPRG_TAIL_CONST
+#define OTPRG_TAIL_CONST 1  // the tail launch with a compile-time team size
+#endif
 constexpr bool kBulk = OTPRG_BULK != 0;  // streaming list build in large phases
 constexpr int kUnroll = 4;       // 128-bit loads in flight per lane (global t)
 #ifndef OTPRG_UNROLL_SMEM
@@ -284,7 +290,7 @@ struct Prefetch {
   unsigned long long ent;
 };
 
-template <typename T, bool kSmem>
+template <typename T, bool kSmem, bool kTail>
 __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const PhasePtrs& P,
                                           const T* tp, int lda, uint32_t phase, uint32_t tmax,
                                           int lane, unsigned long long& bytes,
@@ -344,7 +350,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     } else {  // full scan from position 0 (rebuilding the low set in warp mode)
       OTPRG_STAT(5);
       track_min = true;
-      if (tm.size == 1) {
+      if (!kTail && tm.size == 1) {
         meta = make_int4((int)(target + kLowLevels), 0, 0, 0);
         lb.on = true;
         lb.cnt = 0;
@@ -374,7 +380,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
         walk = false;
         scanning = true;
         start = max(start, meta.y);
-        if (tm.size == 1 && meta.z < kLowCap && start == meta.y) {  // extend the cache
+        if (!kTail && tm.size == 1 && meta.z < kLowCap && start == meta.y) {  // extend the cache
           lb.on = true;
           lb.cnt = meta.z;
           lb.up_rep = S::rep((uint32_t)meta.x);
@@ -508,7 +514,13 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
   }
 }
 
-template <typename T, bool kSmem>
+// kTail: the same loop specialised for small phases (every chain run by a
+// team): no streaming list build, no low-set construction in the scans (only
+// warp-mode chains build caches), so less live state and code.  The full
+// loop stops at the first phase small enough for teams of 8 when A.tail_switch
+// is set, and the tail launch continues from there (multi-launch state as
+// for the stepping API: bar_base, applied).
+template <typename T, bool kSmem, bool kTail>
 __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* s_t = reinterpret_cast<T*>(smem_raw);
@@ -664,6 +676,8 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       if (leader) report(ctl, 5, (int)phase);
       break;
     }
+    if (!kTail && A.tail_switch && n_slots * 8 <= total_warps * OTPRG_TEAM_OVERSUB / OTPRG_TEAM_DEN)
+      break;  // the tail launch takes over from this phase
     phase += 1;
     n_prev = n;
     // Barriers only in iterations that run a phase, so every executed phase
@@ -725,8 +739,17 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       else if (n_slots * 4 <= tw) tsize = 4;
       else if (n_slots * 2 <= tw) tsize = 2;
     }
+    if constexpr (kTail && OTPRG_TAIL_CONST) {
+      // the tail starts at a phase with teams of 8 and the slot count never
+      // grows: a compile-time team size (and one slot per team)
+      if (tsize != 8) {
+        if (leader) report(ctl, 14, (int)phase, n_slots);
+        break;
+      }
+      tsize = 8;
+    }
     // (phase 1's lists come from the streaming propose kernel when it ran)
-    const bool bulk = kBulk && n >= total_warps && !(phase == 1 && A.pre_scanned);
+    const bool bulk = !kTail && kBulk && n >= total_warps && !(phase == 1 && A.pre_scanned);
     if (bulk) {
       // Large phase: first stream every proposer's row once at full HBM
       // bandwidth (warps in flight, no dependent atomics), recording its
@@ -782,7 +805,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     while (i < n_slots) {
       const int b = use_pf ? pf.b : __ldcg(list_in + i);
       if (b >= 0) {
-        run_chain<T, kSmem>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
+        run_chain<T, kSmem, kTail>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
                             tr ? acc : nullptr, tm, pf, use_pf, static_out ? i : -1, pf);
       } else if (static_out) {  // a hole stays a hole
         if (lane == 0 && tm.rank == 0) {
@@ -793,7 +816,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
         pf.b = -1;
       }
       use_pf = false;
-      if (single) break;
+      if (single || (kTail && OTPRG_TAIL_CONST)) break;
       unsigned long long nx = 0;
       if (lane == 0 && tm.rank == 0) nx = (unsigned long long)(total_teams + atomicAdd(&ctl->work[r_cur], 1));
       i = (int)team_bcast(tm, nx, lane);
@@ -888,15 +911,16 @@ __global__ void flush_kernel(uint4* buf, size_t n) {
     buf[i] = make_uint4((unsigned)i, 0u, 0u, 0u);
 }
 
-template <typename T, bool kSmem>
+template <typename T, bool kSmem, bool kTail>
 void* loop_fn() {
-  return reinterpret_cast<void*>(&phase_loop_kernel<T, kSmem>);
+  return reinterpret_cast<void*>(&phase_loop_kernel<T, kSmem, kTail>);
 }
 
-void* pick_loop(int width, bool smem_t) {
+void* pick_loop(int width, bool smem_t, bool tail = false) {
   return with_width(width, [&](auto tag) {
     using T = decltype(tag);
-    return smem_t ? loop_fn<T, true>() : loop_fn<T, false>();
+    if (tail) return loop_fn<T, true, true>();
+    return smem_t ? loop_fn<T, true, false>() : loop_fn<T, false, false>();
   });
 }
 
@@ -919,13 +943,34 @@ int phase_loop_grid(int width, bool smem_t, int lda, int num_sms) {
   return per_sm * num_sms;
 }
 
+// Whether the tail-specialised loop can follow the full one on `grid` blocks.
+static bool tail_usable(int width, bool smem_t, int lda, int grid) {
+  if (!OTPRG_TAIL || !smem_t) return false;
+  void* fn = pick_loop(width, true, true);
+  const size_t smem = phase_loop_smem(width, true, lda);
+  if (smem > 48 * 1024) smem_attr_raise(fn, smem);
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem) != cudaSuccess) return false;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms >= grid;
+}
+
+int phase_loop_launches(int width, bool smem_t, int lda, int grid) {
+  return tail_usable(width, smem_t, lda, grid) ? 2 : 1;
+}
+
 cudaError_t launch_phase_loop(const SolveArgs& a, int width, bool smem_t, int lda, int grid,
                               cudaStream_t s) {
-  void* fn = pick_loop(width, smem_t);
+  const bool tail = tail_usable(width, smem_t, lda, grid);
   SolveArgs args = a;
+  args.tail_switch = tail ? 1 : 0;
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), params,
-                                     phase_loop_smem(width, smem_t, lda), s);
+  const size_t smem = phase_loop_smem(width, smem_t, lda);
+  cudaError_t e = cudaLaunchCooperativeKernel(pick_loop(width, smem_t), dim3(grid), dim3(kBlock), params, smem, s);
+  if (e != cudaSuccess || !tail) return e;
+  // (a solve that already ended returns at the tail's first top)
+  return cudaLaunchCooperativeKernel(pick_loop(width, true, true), dim3(grid), dim3(kBlock), params, smem, s);
 }
 
 cudaError_t launch_init_state(const SolveArgs& a, int n_a, int n_b, int lda, int width,
