@@ -78,6 +78,9 @@ constexpr bool kStatic = OTPRG_STATIC != 0;
 #ifndef OTPRG_TAIL
 #define OTPRG_TAIL 1  // small phases (teams of 8 warps) run in a second, specialised launch
 #endif
+#ifndef OTPRG_TAIL_UNROLL
+#define OTPRG_TAIL_UNROLL 5  // 128-bit loads in flight per lane in the tail's row scans (A/B 4/5/6/8: a team step of 8 warps then covers 20 KB, one n = 10k uint16 row)
+#endif
 #ifndef OTPRG_TAIL_CONST
 #define OTPRG_TAIL_CONST 1  // the tail launch with a compile-time team size
 #endif
@@ -153,7 +156,7 @@ __device__ __forceinline__ int team_min(const Team& tm, int v, int lane) {
 // kU in flight per lane); a team of warps covers consecutive chunks and
 // agrees on the first hit per step.  track_min folds min_a (k + t) into mnw;
 // lb (warp mode only) appends the low-set entries at positions <= the hit.
-template <typename T, bool kSmem>
+template <typename T, bool kSmem, int kUS = kUnrollSmem>
 __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tvec, int lda,
                                          int start, uint32_t target, bool track_min,
                                          uint32_t& mnw, LowBuild& lb, int lane, const Team& tm,
@@ -164,7 +167,7 @@ __device__ __forceinline__ int warp_scan(const T* __restrict__ row, const T* tve
   const uint4* rv = reinterpret_cast<const uint4*>(row);
   const uint4* tv = reinterpret_cast<const uint4*>(tvec);
   const int nv = lda / kEpv;  // multiple of 32
-  constexpr int kU = kSmem ? kUnrollSmem : kUnroll;
+  constexpr int kU = kSmem ? kUS : kUnroll;
   const int tstride = tm.size * 32 * kU;
   for (int vt = (start / kEpv) & ~31; vt < nv; vt += tstride) {
     const int v = vt + tm.rank * 32 * kU;  // this warp's chunk of the team step
@@ -391,7 +394,8 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     }
     if (scanning) {
       const unsigned long long ts0 = acc ? globaltimer() : 0;
-      a = warp_scan<T, kSmem>(kT + (size_t)b * lda, tp, lda, start, target, track_min, mnw, lb,
+      a = warp_scan<T, kSmem, kTail ? OTPRG_TAIL_UNROLL : kUnrollSmem>(kT + (size_t)b * lda, tp, lda, start,
+                                                                       target, track_min, mnw, lb,
                               lane, tm, bytes);
       if (acc) acc[0] += globaltimer() - ts0;
       if (lead) ++steps;
