@@ -13,7 +13,7 @@ if [ "$1" == "ncu" ]; then
   python scripts/profile_solve.py > gpurun_out/plain.log 2>&1 &&
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_solve.csv \
       python scripts/profile_solve.py > gpurun_out/ncu_launch.log 2>&1 &&
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:phase_loop -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:phase_loop -s 2 -c 2 \
       -o gpurun_out/prof_loop python scripts/profile_solve.py > gpurun_out/ncu_loop.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_loop.log
 fi
