@@ -81,6 +81,12 @@ constexpr bool kStatic = OTPRG_STATIC != 0;
 #ifndef OTPRG_TAIL_UNROLL
 #define OTPRG_TAIL_UNROLL 5  // 128-bit loads in flight per lane in the tail's row scans (A/B 4/5/6/8: a team step of 8 warps then covers 20 KB, one n = 10k uint16 row)
 #endif
+#ifndef OTPRG_MID
+#define OTPRG_MID 1  // the phases with teams of 4 in their own specialised launch too
+#endif
+#ifndef OTPRG_MID_UNROLL
+#define OTPRG_MID_UNROLL 5
+#endif
 #ifndef OTPRG_TAIL_CONST
 #define OTPRG_TAIL_CONST 1  // the tail launch with a compile-time team size
 #endif
@@ -293,7 +299,7 @@ struct Prefetch {
   unsigned long long ent;
 };
 
-template <typename T, bool kSmem, bool kTail>
+template <typename T, bool kSmem, bool kTail, int kMid = 0>
 __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const PhasePtrs& P,
                                           const T* tp, int lda, uint32_t phase, uint32_t tmax,
                                           int lane, unsigned long long& bytes,
@@ -394,7 +400,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
     }
     if (scanning) {
       const unsigned long long ts0 = acc ? globaltimer() : 0;
-      a = warp_scan<T, kSmem, kTail ? OTPRG_TAIL_UNROLL : kUnrollSmem>(kT + (size_t)b * lda, tp, lda, start,
+      a = warp_scan<T, kSmem, kMid ? OTPRG_MID_UNROLL : (kTail ? OTPRG_TAIL_UNROLL : kUnrollSmem)>(kT + (size_t)b * lda, tp, lda, start,
                                                                        target, track_min, mnw, lb,
                               lane, tm, bytes);
       if (acc) acc[0] += globaltimer() - ts0;
@@ -524,7 +530,7 @@ __device__ __forceinline__ void run_chain(int b, const SolveArgs& A, const Phase
 // loop stops at the first phase small enough for teams of 8 when A.tail_switch
 // is set, and the tail launch continues from there (multi-launch state as
 // for the stepping API: bar_base, applied).
-template <typename T, bool kSmem, bool kTail>
+template <typename T, bool kSmem, bool kTail, int kMid = 0>
 __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* s_t = reinterpret_cast<T*>(smem_raw);
@@ -680,8 +686,11 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
       if (leader) report(ctl, 5, (int)phase);
       break;
     }
-    if (!kTail && A.tail_switch && n_slots * 8 <= total_warps * OTPRG_TEAM_OVERSUB / OTPRG_TEAM_DEN)
-      break;  // the tail launch takes over from this phase
+    if (!kTail && A.tail_switch && n_slots * (OTPRG_MID ? 4 : 8) <= total_warps * OTPRG_TEAM_OVERSUB / OTPRG_TEAM_DEN)
+      break;  // the tail launch(es) take over from this phase
+    if constexpr (kMid != 0) {
+      if (n_slots * 8 <= total_warps * OTPRG_TEAM_OVERSUB / OTPRG_TEAM_DEN) break;  // teams of 8 from here
+    }
     phase += 1;
     n_prev = n;
     // Barriers only in iterations that run a phase, so every executed phase
@@ -746,11 +755,11 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     if constexpr (kTail && OTPRG_TAIL_CONST) {
       // the tail starts at a phase with teams of 8 and the slot count never
       // grows: a compile-time team size (and one slot per team)
-      if (tsize != 8) {
+      if (tsize != (kMid ? kMid : 8)) {
         if (leader) report(ctl, 14, (int)phase, n_slots);
         break;
       }
-      tsize = 8;
+      tsize = kMid ? kMid : 8;
     }
     // (phase 1's lists come from the streaming propose kernel when it ran)
     const bool bulk = !kTail && kBulk && n >= total_warps && !(phase == 1 && A.pre_scanned);
@@ -809,7 +818,7 @@ __global__ void __launch_bounds__(kBlock, 1) phase_loop_kernel(SolveArgs A) {
     while (i < n_slots) {
       const int b = use_pf ? pf.b : __ldcg(list_in + i);
       if (b >= 0) {
-        run_chain<T, kSmem, kTail>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
+        run_chain<T, kSmem, kTail, kMid>(b, A, P, tp, lda, phase, tmax, lane, bytes, steps, walks, s_stat,
                             tr ? acc : nullptr, tm, pf, use_pf, static_out ? i : -1, pf);
       } else if (static_out) {  // a hole stays a hole
         if (lane == 0 && tm.rank == 0) {
@@ -915,14 +924,16 @@ __global__ void flush_kernel(uint4* buf, size_t n) {
     buf[i] = make_uint4((unsigned)i, 0u, 0u, 0u);
 }
 
-template <typename T, bool kSmem, bool kTail>
+template <typename T, bool kSmem, bool kTail, int kMid = 0>
 void* loop_fn() {
-  return reinterpret_cast<void*>(&phase_loop_kernel<T, kSmem, kTail>);
+  return reinterpret_cast<void*>(&phase_loop_kernel<T, kSmem, kTail, kMid>);
 }
 
-void* pick_loop(int width, bool smem_t, bool tail = false) {
+// tail: 0 the full loop, 4 the mid loop (teams of 4), 8 the tail loop (teams of 8)
+void* pick_loop(int width, bool smem_t, int tail = 0) {
   return with_width(width, [&](auto tag) {
     using T = decltype(tag);
+    if (tail == 4) return loop_fn<T, true, true, 4>();
     if (tail) return loop_fn<T, true, true>();
     return smem_t ? loop_fn<T, true, false>() : loop_fn<T, false, false>();
   });
@@ -948,9 +959,10 @@ int phase_loop_grid(int width, bool smem_t, int lda, int num_sms) {
 }
 
 // Whether the tail-specialised loop can follow the full one on `grid` blocks.
-static bool tail_usable(int width, bool smem_t, int lda, int grid) {
+static bool tail_usable(int width, bool smem_t, int lda, int grid, int ts = 8) {
   if (!OTPRG_TAIL || !smem_t) return false;
-  void* fn = pick_loop(width, true, true);
+  if (OTPRG_MID && ts == 8 && !tail_usable(width, smem_t, lda, grid, 4)) return false;  // (both or neither)
+  void* fn = pick_loop(width, true, ts);
   const size_t smem = phase_loop_smem(width, true, lda);
   if (smem > 48 * 1024) smem_attr_raise(fn, smem);
   int per_sm = 0, dev = 0, sms = 0;
@@ -961,7 +973,7 @@ static bool tail_usable(int width, bool smem_t, int lda, int grid) {
 }
 
 int phase_loop_launches(int width, bool smem_t, int lda, int grid) {
-  return tail_usable(width, smem_t, lda, grid) ? 2 : 1;
+  return tail_usable(width, smem_t, lda, grid) ? (OTPRG_MID ? 3 : 2) : 1;
 }
 
 cudaError_t launch_phase_loop(const SolveArgs& a, int width, bool smem_t, int lda, int grid,
@@ -974,7 +986,11 @@ cudaError_t launch_phase_loop(const SolveArgs& a, int width, bool smem_t, int ld
   cudaError_t e = cudaLaunchCooperativeKernel(pick_loop(width, smem_t), dim3(grid), dim3(kBlock), params, smem, s);
   if (e != cudaSuccess || !tail) return e;
   // (a solve that already ended returns at the tail's first top)
-  return cudaLaunchCooperativeKernel(pick_loop(width, true, true), dim3(grid), dim3(kBlock), params, smem, s);
+  if (OTPRG_MID) {
+    e = cudaLaunchCooperativeKernel(pick_loop(width, true, 4), dim3(grid), dim3(kBlock), params, smem, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaLaunchCooperativeKernel(pick_loop(width, true, 8), dim3(grid), dim3(kBlock), params, smem, s);
 }
 
 cudaError_t launch_init_state(const SolveArgs& a, int n_a, int n_b, int lda, int width,
