@@ -297,9 +297,9 @@ def run_ours(args, world, rank, local) -> None:
     a_loop = float(np.mean(loop_ach))
     roofline = {
         "bound": "hbm",
-        "kernel": f"phase_loop_kernel<{ctype(width)},true,false> + <...,true,true> "
-                  "(the full and tail-specialised launches of the phase loop: all phases' proposal "
-                  "chains + phases >= 2 scans; traffic = both launches' DRAM bytes)",
+        "kernel": f"phase_loop_kernel<{ctype(width)},true,...> (the full, mid (teams of 4) and tail "
+                  "(teams of 8) launches of the phase loop: all phases' proposal chains + phases >= 2 "
+                  "scans; traffic = the launches' DRAM bytes, profiles/ncu_summary.json)",
         "achieved": round(a_loop, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
         "frac": round(a_loop / peak, 4),
         "traffic": (traffic or {}).get("loop_dram_bytes_per_launch"),
