@@ -85,7 +85,7 @@ constexpr bool kStatic = OTPRG_STATIC != 0;
 #define OTPRG_MID 1  // the phases with teams of 4 in their own specialised launch too
 #endif
 #ifndef OTPRG_MID_UNROLL
-#define OTPRG_MID_UNROLL 5
+#define OTPRG_MID_UNROLL 4  // (A/B 4 / 5 / 6 / 8: 2.953 / 2.958 / 2.967 / 2.970 ms)
 #endif
 #ifndef OTPRG_TAIL_CONST
 #define OTPRG_TAIL_CONST 1  // the tail launch with a compile-time team size
